@@ -1,0 +1,457 @@
+"""B200-native hybrid-precision block-Jacobi GMRES(m) (arXiv 2509.09139 path).
+
+Python mirror of the reference's C++ solver interface
+(/root/reference/proj/include/bjgmres), over the C ABI of libhpbj.so
+(include/hpbj.h). Names, argument meaning and error behaviour follow the
+reference so callers (and our parity tests) read like the reference's own:
+
+=====================================  =====================================
+reference (proj/include/bjgmres)        here
+=====================================  =====================================
+SparseMatrix (sparse_matrix.hpp:23)     SparseMatrix
+graph_from_matrix (graph.hpp:30)        graph_from_matrix -> WeightedGraph
+partition_graph (partition.hpp:38)      partition_graph -> Partition
+partition_from_assignment (:33)         partition_from_assignment
+Preconditioner::block_jacobi (:60)      Preconditioner.block_jacobi
+Preconditioner::apply<float> (:69)      Preconditioner.apply
+GmresConfig (gmres.hpp:89)              GmresConfig
+hybrid_restart_gmres (gmres.hpp:145)    hybrid_restart_gmres -> SolveResult
+SingularBlockError (lu.hpp:52)          SingularBlockError
+=====================================  =====================================
+
+Exceptions: std::invalid_argument -> ValueError, std::logic_error ->
+LogicError, std::out_of_range -> IndexError, SingularBlockError ->
+SingularBlockError, device failures -> RuntimeError.
+
+Every numerical step runs in sm_100a kernels; only graph partitioning runs on
+the host (bit-identical to the reference). There is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+from . import _abi
+
+__all__ = [
+    "SparseMatrix", "WeightedGraph", "Partition", "BlockJacobiOptions", "Preconditioner", "GmresConfig",
+    "SolveReport", "SolveResult", "HistoryPoint", "SingularBlockError", "LogicError", "graph_from_matrix",
+    "partition_graph", "partition_from_assignment", "hybrid_restart_gmres", "Context", "library",
+]
+
+ROUNDOFF_SINGLE = 2.0 ** -24  # types.hpp:12
+ROUNDOFF_DOUBLE = 2.0 ** -53  # types.hpp:13
+
+
+class LogicError(RuntimeError):
+    """std::logic_error."""
+
+
+class SingularBlockError(RuntimeError):
+    """bjgmres::SingularBlockError (lu.hpp:52-60): zero pivot with eps_pivot = 0."""
+
+    def __init__(self, what: str, column: int, block: int = -1):
+        super().__init__(what)
+        self._column = column
+        self.block = block
+
+    def column(self) -> int:
+        return self._column
+
+
+def library():
+    return _abi.load()
+
+
+def _raise(code: int, msg: str, info: Optional[_abi.SetupInfo] = None):
+    if code == _abi.HPBJ_EINVAL:
+        raise ValueError(msg)
+    if code == _abi.HPBJ_ELOGIC:
+        raise LogicError(msg)
+    if code == _abi.HPBJ_ERANGE:
+        raise IndexError(msg)
+    if code == _abi.HPBJ_ESINGULAR:
+        col = int(info.singular_column) if info is not None else -1
+        blk = int(info.singular_block) if info is not None else -1
+        raise SingularBlockError(msg, col, blk)
+    raise RuntimeError(msg)
+
+
+def _p(a, t):
+    return a.ctypes.data_as(t)
+
+
+def _i64(a):
+    return np.ascontiguousarray(a, dtype=np.int64)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+# ---------------------------------------------------------------------------
+@dataclass
+class SparseMatrix:
+    """CSR matrix, FP64 master values (sparse_matrix.hpp:23-62)."""
+
+    nrows: int
+    row_starts: np.ndarray
+    col_indices: np.ndarray
+    values: np.ndarray
+
+    def __post_init__(self):
+        self.row_starts = _i64(self.row_starts)
+        self.col_indices = _i64(self.col_indices)
+        self.values = _f64(self.values)
+        if len(self.row_starts) != self.nrows + 1:
+            raise ValueError("sparse matrix: row_starts length")
+
+    @property
+    def n(self) -> int:
+        return self.nrows
+
+    def rows(self) -> int:
+        return self.nrows
+
+    def nnz(self) -> int:
+        return int(self.row_starts[-1])
+
+    @staticmethod
+    def from_triplets(rows, cols, vals, n: int) -> "SparseMatrix":
+        """SparseMatrix::from_triplets (sparse_matrix.cpp:52-88): sort by
+        (row, col, value bits), sum duplicates in that order."""
+        rows = _i64(rows)
+        cols = _i64(cols)
+        vals = _f64(vals)
+        if len(rows) and (rows.min() < 0 or rows.max() >= n or cols.min() < 0 or cols.max() >= n):
+            raise IndexError("from_triplets: index out of range")
+        order = np.lexsort((vals.view(np.uint64), cols, rows))
+        rows, cols, vals = rows[order], cols[order], vals[order]
+        out_r, out_c, out_v = [], [], []
+        k = 0
+        while k < len(rows):
+            r, c, s = rows[k], cols[k], 0.0
+            while k < len(rows) and rows[k] == r and cols[k] == c:
+                s += float(vals[k])
+                k += 1
+            out_r.append(r)
+            out_c.append(c)
+            out_v.append(s)
+        rs = np.zeros(n + 1, np.int64)
+        np.add.at(rs, np.asarray(out_r, np.int64) + 1, 1)
+        return SparseMatrix(n, np.cumsum(rs), np.asarray(out_c, np.int64), np.asarray(out_v, np.float64))
+
+
+@dataclass
+class WeightedGraph:
+    """graph.hpp:17-25 as CSR adjacency (sorted by neighbour)."""
+
+    num_nodes: int
+    start: np.ndarray
+    neighbor: np.ndarray
+    weight: np.ndarray
+
+    def degree(self, v: int) -> int:
+        return int(self.start[v + 1] - self.start[v])
+
+    def num_edges(self) -> int:
+        return int(self.start[-1]) // 2
+
+
+@dataclass
+class Partition:
+    """partition.hpp:14-28."""
+
+    num_blocks: int
+    assignment: np.ndarray
+    perm: np.ndarray
+    block_starts: np.ndarray
+
+    def num_nodes(self) -> int:
+        return len(self.assignment)
+
+    def block_size(self, b: int) -> int:
+        return int(self.block_starts[b + 1] - self.block_starts[b])
+
+
+def graph_from_matrix(a: SparseMatrix) -> WeightedGraph:
+    lib = library()
+    n = a.n
+    cap = 2 * a.nnz() + 1
+    st = np.zeros(n + 1, np.int64)
+    nb = np.zeros(cap, np.int64)
+    w = np.zeros(cap)
+    rc = lib.hpbj_graph_from_matrix(n, _p(a.row_starts, _abi.i64p), _p(a.col_indices, _abi.i64p),
+                                    _p(a.values, _abi.f64p), _p(st, _abi.i64p), _p(nb, _abi.i64p),
+                                    _p(w, _abi.f64p), cap)
+    if rc:
+        _raise(rc, lib.hpbj_last_error(None).decode())
+    k = int(st[-1])
+    return WeightedGraph(n, st, nb[:k].copy(), w[:k].copy())
+
+
+def partition_graph(g, s: int, imbalance_tol: float = 0.1) -> Partition:
+    """partition_graph (partition.hpp:38-39). Accepts a WeightedGraph or, as a
+    fused fast path, the SparseMatrix itself (graph_from_matrix + partition)."""
+    lib = library()
+    if isinstance(g, SparseMatrix):
+        n = g.n
+        asg, perm, bst = np.zeros(n, np.int64), np.zeros(n, np.int64), np.zeros(max(s, 0) + 1, np.int64)
+        rc = lib.hpbj_partition_graph(n, _p(g.row_starts, _abi.i64p), _p(g.col_indices, _abi.i64p),
+                                      _p(g.values, _abi.f64p), s, imbalance_tol, _p(asg, _abi.i64p),
+                                      _p(perm, _abi.i64p), _p(bst, _abi.i64p))
+    else:
+        n = g.num_nodes
+        st, nb, w = _i64(g.start), _i64(g.neighbor), _f64(g.weight)
+        asg, perm, bst = np.zeros(n, np.int64), np.zeros(n, np.int64), np.zeros(max(s, 0) + 1, np.int64)
+        rc = lib.hpbj_partition_adjacency(n, _p(st, _abi.i64p), _p(nb, _abi.i64p), _p(w, _abi.f64p), s,
+                                          imbalance_tol, _p(asg, _abi.i64p), _p(perm, _abi.i64p),
+                                          _p(bst, _abi.i64p))
+    if rc:
+        _raise(rc, lib.hpbj_last_error(None).decode())
+    return Partition(s, asg, perm, bst)
+
+
+def partition_from_assignment(assignment, s: int) -> Partition:
+    lib = library()
+    asg = _i64(assignment)
+    n = len(asg)
+    perm, bst = np.zeros(n, np.int64), np.zeros(max(s, 0) + 1, np.int64)
+    rc = lib.hpbj_partition_from_assignment(n, _p(asg, _abi.i64p), s, _p(perm, _abi.i64p), _p(bst, _abi.i64p))
+    if rc:
+        _raise(rc, lib.hpbj_last_error(None).decode())
+    return Partition(s, asg.copy(), perm, bst)
+
+
+# ---------------------------------------------------------------------------
+class Context:
+    """Owns one hpbj_ctx (device buffers + CUDA stream)."""
+
+    def __init__(self, device: int = 0):
+        self.lib = library()
+        h = ctypes.c_void_p()
+        rc = self.lib.hpbj_create(ctypes.byref(h), device)
+        if rc:
+            _raise(rc, self.lib.hpbj_last_error(None).decode())
+        self.h = h
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h:
+            self.lib.hpbj_destroy(h)
+            self.h = None
+
+    def check(self, rc, info=None):
+        if rc:
+            _raise(rc, self.lib.hpbj_last_error(self.h).decode(), info)
+
+    def set_matrix(self, a: SparseMatrix):
+        self.check(self.lib.hpbj_set_matrix(self.h, a.n, _p(a.row_starts, _abi.i64p), _p(a.col_indices, _abi.i64p),
+                                            _p(a.values, _abi.f64p)))
+
+    def update_values(self, values):
+        v = _f64(values)
+        self.check(self.lib.hpbj_update_values(self.h, _p(v, _abi.f64p)))
+
+    def spmv(self, x):
+        x = _f64(x)
+        y = np.zeros_like(x)
+        self.check(self.lib.hpbj_spmv(self.h, _p(x, _abi.f64p), _p(y, _abi.f64p)))
+        return y
+
+    def bj_setup(self, part: Partition, eps_pivot: float) -> _abi.SetupInfo:
+        info = _abi.SetupInfo()
+        perm, bst = _i64(part.perm), _i64(part.block_starts)
+        rc = self.lib.hpbj_bj_setup(self.h, part.num_blocks, _p(perm, _abi.i64p), _p(bst, _abi.i64p), eps_pivot,
+                                    ctypes.byref(info))
+        self.check(rc, info)
+        return info
+
+    def bj_refactor(self) -> _abi.SetupInfo:
+        info = _abi.SetupInfo()
+        self.check(self.lib.hpbj_bj_refactor(self.h, ctypes.byref(info)), info)
+        return info
+
+    def apply(self, v):
+        v = _f64(v)
+        z = np.zeros_like(v)
+        self.check(self.lib.hpbj_bj_apply(self.h, _p(v, _abi.f64p), _p(z, _abi.f64p)))
+        return z
+
+    def block_factors(self, b: int):
+        d = ctypes.c_int64()
+        self.check(self.lib.hpbj_get_block_factors(self.h, b, ctypes.byref(d), None, None))
+        f = np.zeros(d.value * d.value, np.float32)
+        piv = np.zeros(d.value, np.int64)
+        self.check(self.lib.hpbj_get_block_factors(self.h, b, ctypes.byref(d), _p(f, _abi.f32p),
+                                                   _p(piv, _abi.i64p)))
+        return f.reshape(d.value, d.value), piv
+
+    def block_stats(self, s: int):
+        dims, pert = np.zeros(s, np.int64), np.zeros(s, np.int64)
+        self.check(self.lib.hpbj_get_block_stats(self.h, _p(dims, _abi.i64p), _p(pert, _abi.i64p)))
+        return dims, pert
+
+    def launches(self) -> int:
+        return int(self.lib.hpbj_kernel_launches(self.h))
+
+    def set_profiling(self, on: bool):
+        self.check(self.lib.hpbj_set_profiling(self.h, 1 if on else 0))
+
+    def kernel_stats(self):
+        arr = (_abi.KernelStat * _abi.HPBJ_K_COUNT)()
+        self.check(self.lib.hpbj_get_kernel_stats(self.h, arr))
+        return [dict(launches=s.launches, total_ms=s.total_ms, bytes_per_launch=s.bytes_per_launch) for s in arr]
+
+    def gmres(self, b, cfg: "GmresConfig", device_ptrs=None):
+        opts = cfg.to_opts()
+        rep = _abi.Report()
+        hcap = cfg.restart_m * cfg.max_restarts + 2
+        hist = (_abi.HistoryPoint * hcap)()
+        cyc = np.zeros(cfg.max_restarts + 1)
+        if device_ptrs is not None:
+            d_b, d_x = device_ptrs
+            rc = self.lib.hpbj_gmres_device(self.h, ctypes.c_void_p(d_b), ctypes.c_void_p(d_x), ctypes.byref(opts),
+                                            ctypes.byref(rep), hist, hcap, _p(cyc, _abi.f64p), len(cyc))
+            x = None
+        else:
+            b = _f64(b)
+            x = np.zeros_like(b)
+            rc = self.lib.hpbj_gmres(self.h, _p(b, _abi.f64p), _p(x, _abi.f64p), ctypes.byref(opts),
+                                     ctypes.byref(rep), hist, hcap, _p(cyc, _abi.f64p), len(cyc))
+        self.check(rc)
+        hl = min(int(rep.history_len), hcap)
+        history = [HistoryPoint(int(hist[k].cycle), int(hist[k].iteration), float(hist[k].relative_residual))
+                   for k in range(hl)]
+        report = SolveReport(
+            converged=bool(rep.converged),
+            total_iterations=int(rep.total_iterations),
+            restarts=int(rep.restarts),
+            residual_history=history,
+            cycle_residuals=cyc[: int(rep.cycles)].tolist(),
+            final_residual=float(rep.final_residual),
+            breakdown=bool(rep.breakdown),
+            ls_rank_deficient=bool(rep.ls_rank_deficient),
+            iterate_seconds=float(rep.ms_solve) / 1e3,
+        )
+        return x, report
+
+
+# ---------------------------------------------------------------------------
+@dataclass
+class BlockJacobiOptions:
+    """preconditioner.hpp:32-38 (Hybrid policy only: FP32 factors)."""
+
+    eps_pivot: float = 1e-10
+    neumann_order: int = 0
+
+    def __post_init__(self):
+        if self.neumann_order != 0:
+            raise ValueError("neumann_order > 0 is not on the HPBJ hot path (DESIGN.md: out of scope)")
+
+
+class Preconditioner:
+    """Block-Jacobi preconditioner resident on one B200 (preconditioner.hpp:50-98)."""
+
+    def __init__(self, ctx: Context, a: SparseMatrix, part: Partition, opts: BlockJacobiOptions,
+                 info: _abi.SetupInfo):
+        self.ctx = ctx
+        self.matrix = a
+        self.partition = part
+        self.opts = opts
+        self.info = info
+
+    @staticmethod
+    def block_jacobi(a: SparseMatrix, partition: Partition, opts: Optional[BlockJacobiOptions] = None,
+                     device: int = 0, ctx: Optional[Context] = None) -> "Preconditioner":
+        opts = opts or BlockJacobiOptions()
+        if partition.num_nodes() != a.n:
+            raise ValueError("block_jacobi: partition does not cover the matrix")
+        ctx = ctx or Context(device)
+        ctx.set_matrix(a)
+        info = ctx.bj_setup(partition, opts.eps_pivot)
+        return Preconditioner(ctx, a, partition, opts, info)
+
+    def dim(self) -> int:
+        return self.matrix.n
+
+    def apply(self, v) -> np.ndarray:
+        """apply<float>: z with M z = v (FP32 factors, FP32 arithmetic)."""
+        v = _f64(v)
+        if len(v) != self.dim():
+            raise ValueError("preconditioner apply: dimension mismatch")
+        return self.ctx.apply(v)
+
+    def block_factors(self, b: int):
+        return self.ctx.block_factors(b)
+
+    def stats(self):
+        dims, pert = self.ctx.block_stats(self.partition.num_blocks)
+        return [dict(block_dim=int(d), perturbation_count=int(p)) for d, p in zip(dims, pert)]
+
+
+@dataclass
+class GmresConfig:
+    """gmres.hpp:89-97. Hybrid (FP32 preconditioner) is the only policy: the
+    attainable-floor break uses u = 2^-24 (gmres.cpp:130-145)."""
+
+    restart_m: int = 50
+    tol: float = 1e-8
+    max_restarts: int = 40
+    absolute_tol: bool = False
+    breakdown_tol_factor: float = 1e2
+    floor_roundoff: float = ROUNDOFF_SINGLE
+
+    def to_opts(self) -> _abi.GmresOpts:
+        o = _abi.GmresOpts()
+        o.restart_m = int(self.restart_m)
+        o.tol = float(self.tol)
+        o.max_restarts = int(self.max_restarts)
+        o.absolute_tol = 1 if self.absolute_tol else 0
+        o.breakdown_tol_factor = float(self.breakdown_tol_factor)
+        o.floor_roundoff = float(self.floor_roundoff)
+        return o
+
+
+@dataclass
+class HistoryPoint:
+    cycle: int
+    iteration: int
+    relative_residual: float
+
+
+@dataclass
+class SolveReport:
+    converged: bool = False
+    total_iterations: int = 0
+    restarts: int = 0
+    residual_history: List[HistoryPoint] = field(default_factory=list)
+    cycle_residuals: List[float] = field(default_factory=list)
+    final_residual: float = 0.0
+    breakdown: bool = False
+    ls_rank_deficient: bool = False
+    setup_seconds: float = 0.0
+    iterate_seconds: float = 0.0
+
+
+@dataclass
+class SolveResult:
+    x: np.ndarray
+    report: SolveReport
+
+
+def hybrid_restart_gmres(a: SparseMatrix, p: Preconditioner, b, config: GmresConfig) -> SolveResult:
+    """hybrid_restart_gmres (gmres.hpp:145-147): FP64 SpMV and Arnoldi, FP32
+    block-Jacobi apply, FP64 true residual per restart cycle."""
+    b = _f64(b)
+    if a.n != len(b):
+        raise ValueError("gmres: rhs dimension mismatch")
+    if config.restart_m < 1 or config.tol <= 0.0 or config.max_restarts < 1:
+        raise ValueError("gmres: invalid config")
+    if p.matrix is not a:
+        raise ValueError("gmres: the preconditioner must be built from this matrix (device-resident)")
+    x, rep = p.ctx.gmres(b, config)
+    return SolveResult(x, rep)

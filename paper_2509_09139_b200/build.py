@@ -1,0 +1,89 @@
+"""Build libhpbj.so (sm_100a CUDA + host C++) and libhpbj_gen.so in-tree.
+
+Explicit nvcc/g++ commands (no JIT cache): the built .so files live under
+paper_2509_09139_b200/lib/ and travel to the GPU box with the repo snapshot.
+Rebuilds only what is older than its sources.
+"""
+from __future__ import annotations
+
+import concurrent.futures as cf
+import os
+import shutil
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+LIB = os.path.join(PKG, "lib")
+OBJ = os.path.join(PKG, "build_obj")
+INC = os.path.join(ROOT, "include")
+
+NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
+              "-Xptxas", "-v", "-I" + INC, "-I" + CSRC] + ARCH
+CXX_FLAGS = ["-std=c++20", "-O3", "-fPIC", "-fopenmp", "-ffp-contract=off", "-I" + INC, "-I" + CSRC]
+
+CU_SOURCES = ["permute.cu", "block_lu.cu", "apply.cu", "spmv.cu", "arnoldi.cu", "capi.cu"]
+CPP_SOURCES = ["host/partition.cpp"]
+HEADERS = ["device.cuh", "kernels.cuh", "hpbj_common.hpp"]
+
+LIBHPBJ = os.path.join(LIB, "libhpbj.so")
+LIBGEN = os.path.join(LIB, "libhpbj_gen.so")
+
+
+def _newer(target, deps):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def _run(cmd, log=None):
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if log is not None:
+        with open(log, "w") as f:
+            f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
+    if r.returncode != 0:
+        raise RuntimeError(f"build failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+    return r
+
+
+def build(verbose: bool = False) -> str:
+    os.makedirs(LIB, exist_ok=True)
+    os.makedirs(OBJ, exist_ok=True)
+    hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(INC, "hpbj.h")]
+    jobs = []
+    objs = []
+    for src in CU_SOURCES:
+        s = os.path.join(CSRC, src)
+        o = os.path.join(OBJ, src.replace("/", "_") + ".o")
+        objs.append(o)
+        if _newer(o, [s] + hdrs):
+            jobs.append(([NVCC] + NVCC_FLAGS + ["-c", s, "-o", o], o + ".log"))
+    for src in CPP_SOURCES:
+        s = os.path.join(CSRC, src)
+        o = os.path.join(OBJ, src.replace("/", "_") + ".o")
+        objs.append(o)
+        if _newer(o, [s] + hdrs):
+            jobs.append((["g++"] + CXX_FLAGS + ["-c", s, "-o", o], o + ".log"))
+    with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
+        futs = [ex.submit(_run, cmd, log) for cmd, log in jobs]
+        for f in futs:
+            f.result()
+    if _newer(LIBHPBJ, objs):
+        _run([NVCC] + ARCH + ["-shared", "-o", LIBHPBJ] + objs +
+             ["-Xcompiler", "-fopenmp", "-lgomp", "-lcudart"], os.path.join(OBJ, "link.log"))
+    gsrc = os.path.join(CSRC, "gen", "workloads.cpp")
+    if _newer(LIBGEN, [gsrc]):
+        _run(["g++", "-std=c++20", "-O2", "-ffp-contract=off", "-fPIC", "-shared", "-o", LIBGEN, gsrc])
+    if verbose:
+        for cmd, log in jobs:
+            print(open(log).read())
+    return LIBHPBJ
+
+
+if __name__ == "__main__":
+    build(verbose="-v" in sys.argv)
+    print("built", LIBHPBJ)

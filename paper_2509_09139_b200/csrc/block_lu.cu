@@ -1,0 +1,215 @@
+// Batched FP32 LU of the block-Jacobi diagonal blocks — replaces gp_lu
+// (lu.cpp:134-225) + slice_diag_block (preconditioner.cpp:20-40) +
+// matrix_inf_norm (sparse_matrix.cpp:155-166) + materialize_low.
+//
+// One CTA per block (persistent over blocks). The block is gathered from the
+// permuted CSR straight into a dense FP32 tile (FP64 -> FP32 RNE on load),
+// held in shared memory when it fits (dim <= smem_dim, ~223) and in a
+// per-CTA global scratch tile otherwise (L1/L2 resident).
+//
+// Pivoting semantics match the reference:
+//  * pivot of column k = argmax |x_i| over not-yet-pivotal rows, ties to the
+//    smallest (original, local) row index (lu.cpp:171-181). Rows are never
+//    physically swapped ("logical" pivoting), so the row index used for the
+//    tie break is the reference's.
+//  * an all-zero candidate column picks the smallest unused row, as the
+//    empty-column fallback (lu.cpp:182-186) does; see DESIGN.md for the one
+//    structurally-zero corner where the reference restricts to its reach set.
+//  * regularize_pivot in FP64 against the FP64 block inf-norm (lu.cpp:10-20,
+//    :188-197); a zero regularised pivot is SingularBlockError(column).
+//
+// Output: F = L_strict + U in pivot order, packed in 32-row panels (see
+// kernels.cuh panel_floats) for the coalesced apply kernel; pivot_rows.
+
+#include <cfloat>
+
+#include "device.cuh"
+#include "kernels.cuh"
+
+namespace hpbj {
+
+namespace {
+
+constexpr int kLuThreads = 256;
+constexpr int kLuMaxDim = 2048;          // act/prow arrays in static shared memory
+constexpr size_t kLuSmemTile = 200 * 1024;
+
+__device__ __forceinline__ unsigned long long umax64(unsigned long long a, unsigned long long b) {
+    return a > b ? a : b;
+}
+
+// mode 0: blocks with d <= smem_dim (tile in shared memory)
+// mode 1: blocks with d >  smem_dim (tile in global scratch)
+__global__ void __launch_bounds__(kLuThreads) k_block_lu(LuParams p, int mode) {
+    extern __shared__ float smem_tile[];
+    __shared__ int act[kLuMaxDim];
+    __shared__ int prow[kLuMaxDim];
+    __shared__ unsigned long long red[kLuThreads / 32];
+    __shared__ double redd[kLuThreads / 32];
+    __shared__ int sh_p, sh_abort;
+    __shared__ float sh_pv;
+    __shared__ double sh_norm;
+
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    constexpr int NW = kLuThreads / 32;
+
+    for (int b = blockIdx.x; b < p.s; b += gridDim.x) {
+        const int o = p.bstart[b];
+        const int d = p.bstart[b + 1] - o;
+        const bool in_smem = d <= p.smem_dim;
+        if ((mode == 0) != in_smem) continue;
+        const int ld = d | 1;  // odd stride: conflict-free column walks
+        float* A = in_smem ? smem_tile : p.scratch + (size_t)blockIdx.x * p.scratch_ld * p.scratch_ld;
+
+        for (int e = tid; e < d * ld; e += kLuThreads) A[e] = 0.0f;
+        for (int r = tid; r < d; r += kLuThreads) act[r] = r;
+        __syncthreads();
+
+        // Gather the diagonal block (FP64 -> FP32) and its inf-norm. The row
+        // sum runs sequentially in column order like matrix_inf_norm, so the
+        // FP64 norm is bit-identical to the reference's.
+        double wmax = 0.0;
+        for (int r = wid; r < d; r += NW) {
+            const int gr = o + r;
+            const int kb = p.a.rp[gr], ke = p.a.rp[gr + 1];
+            for (int k = kb + lane; k < ke; k += 32) {
+                const int c = p.a.ci[k] - o;
+                if (c >= 0 && c < d) A[r * ld + c] = __double2float_rn(p.a.val[k]);
+            }
+            if (lane == 0) {
+                double rs = 0.0;
+                for (int k = kb; k < ke; ++k) {
+                    const int c = p.a.ci[k] - o;
+                    if (c >= 0 && c < d) rs = __dadd_rn(rs, fabs(p.a.val[k]));
+                }
+                wmax = fmax(wmax, rs);
+            }
+        }
+        if (lane == 0) redd[wid] = wmax;
+        if (tid == 0) sh_abort = 0;
+        __syncthreads();
+        if (tid == 0) {
+            double nm = 0.0;
+            for (int w = 0; w < NW; ++w) nm = fmax(nm, redd[w]);
+            sh_norm = nm;
+        }
+        __syncthreads();
+        const double norm = sh_norm;
+
+        int na = d;
+        int nperturb = 0;
+        for (int k = 0; k < d; ++k) {
+            // ---- pivot search: max |a_rk|, ties -> smallest row r
+            unsigned long long best = 0ull;
+            for (int a = tid; a < na; a += kLuThreads) {
+                const int r = act[a];
+                const float v = fabsf(A[r * ld + k]);
+                const unsigned long long key =
+                    ((unsigned long long)(__float_as_uint(v) + 1u) << 32) |
+                    ((unsigned long long)(0xFFFFu - (unsigned)r) << 16) | (unsigned)a;
+                best = umax64(best, key);
+            }
+#pragma unroll
+            for (int o2 = 16; o2 > 0; o2 >>= 1) best = umax64(best, __shfl_xor_sync(0xffffffffu, best, o2));
+            if (lane == 0) red[wid] = best;
+            __syncthreads();
+            if (tid == 0) {
+                unsigned long long f = red[0];
+                for (int w = 1; w < NW; ++w) f = umax64(f, red[w]);
+                const int apos = (int)(f & 0xFFFFu);
+                const int pr = act[apos];
+                const float xp = A[pr * ld + k];
+                // regularize_pivot (lu.cpp:10-20), FP64
+                const double pvd = (double)xp;
+                const bool keep = norm == 0.0 ? (pvd != 0.0) : (fabs(pvd) / norm >= p.eps);
+                const double val = keep ? pvd : ((pvd < 0.0 ? -1.0 : 1.0) * p.eps * norm);
+                if (val == 0.0) {
+                    atomicMin(p.singular, ((unsigned long long)b << 32) | (unsigned)k);
+                    sh_abort = 1;
+                } else if (!keep) {
+                    ++nperturb;
+                    const int slot = atomicAdd(p.pert_n, 1);
+                    if (slot < p.pert_cap) p.pert[slot] = PertRecord{b, k, pvd, val};
+                }
+                const float fv = (float)val;
+                A[pr * ld + k] = fv;
+                prow[k] = pr;
+                act[apos] = act[na - 1];
+                sh_pv = fv;
+                sh_p = pr;
+            }
+            __syncthreads();
+            if (sh_abort) break;
+            --na;
+            // ---- multipliers and rank-1 update of the active rows
+            const float pv = sh_pv;
+            const float* urow = A + sh_p * ld;
+            for (int a = wid; a < na; a += NW) {
+                const int r = act[a];
+                float* arow = A + r * ld;
+                const float l = arow[k] / pv;
+                for (int j = k + 1 + lane; j < d; j += 32) arow[j] = fmaf(-l, urow[j], arow[j]);
+                __syncwarp();
+                if (lane == 0) arow[k] = l;
+            }
+            __syncthreads();
+        }
+        if (tid == 0) p.pert_count[b] = nperturb;
+        if (!sh_abort) {
+            // ---- write F = L\U in pivot order into packed 32-row panels
+            const int T = (d + 31) / 32;
+            const int dp4 = (d + 3) & ~3;
+            const int total = T * 32 * dp4;
+            float* F = p.fac + p.fac_off[b];
+            for (int e = tid; e < total; e += kLuThreads) {
+                const int t = e / (32 * dp4);
+                const int rem = e - t * 32 * dp4;
+                const int c = ((rem >> 7) << 2) | (rem & 3);
+                const int k = 32 * t + ((rem >> 2) & 31);
+                float v;
+                if (k < d && c < d) v = A[prow[k] * ld + c];
+                else v = (k == c) ? 1.0f : 0.0f;
+                F[e] = v;
+            }
+            for (int k = tid; k < d; k += kLuThreads) p.piv[o + k] = prow[k];
+        }
+        __syncthreads();
+    }
+}
+
+int lu_smem_dim(int dmax) {
+    int d = 1;
+    while (d + 1 <= dmax && (size_t)(d + 1) * ((d + 1) | 1) * sizeof(float) <= kLuSmemTile) ++d;
+    return d;
+}
+
+}  // namespace
+
+size_t block_lu_scratch_floats(int dmax, int num_sms, int* smem_dim, int* scratch_ld) {
+    *smem_dim = lu_smem_dim(dmax);
+    *scratch_ld = dmax | 1;
+    if (dmax <= *smem_dim) return 0;
+    return (size_t)num_sms * 4 * (*scratch_ld) * (*scratch_ld);
+}
+
+void launch_block_lu(const LuParams& p, int dmax, int num_sms, cudaStream_t st, int64_t* launches) {
+    if (dmax > kLuMaxDim) fail(HPBJ_EINVAL, "block_jacobi: block dimension exceeds 2048");
+    const int sd = p.smem_dim;
+    const int dsm = std::min(dmax, sd);
+    const size_t smem = (size_t)dsm * (dsm | 1) * sizeof(float);
+    HPBJ_CUDA(cudaFuncSetAttribute(k_block_lu, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLuSmemTile));
+    int occ = 0;
+    HPBJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_block_lu, kLuThreads, smem));
+    occ = std::max(occ, 1);
+    const int grid0 = std::min(p.s, num_sms * occ);
+    k_block_lu<<<grid0, kLuThreads, smem, st>>>(p, 0);
+    *launches += 1;
+    if (dmax > sd) {
+        const int grid1 = std::min(p.s, num_sms * 4);
+        k_block_lu<<<grid1, kLuThreads, 0, st>>>(p, 1);
+        *launches += 1;
+    }
+    HPBJ_CUDA(cudaGetLastError());
+}
+
+}  // namespace hpbj

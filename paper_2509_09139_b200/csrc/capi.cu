@@ -1,0 +1,736 @@
+// libhpbj.so C ABI (include/hpbj.h): context, device buffers, and the restart
+// driver of hybrid_restart_gmres (gmres.cpp:200-274) with every numerical
+// step on the device. The host only sequences launches and reads a handful
+// of scalars once per restart cycle (never per Arnoldi iteration).
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "device.cuh"
+#include "kernels.cuh"
+
+using namespace hpbj;
+
+namespace {
+
+template <class T>
+T* dalloc(size_t count) {
+    T* p = nullptr;
+    if (count == 0) count = 1;
+    HPBJ_CUDA(cudaMalloc(&p, sizeof(T) * count));
+    return p;
+}
+
+template <class T>
+void dfree(T*& p) {
+    if (p) cudaFree(p);
+    p = nullptr;
+}
+
+struct KernelTimer {
+    std::vector<cudaEvent_t> ev;  // pairs
+    size_t used = 0;
+    void reserve(size_t pairs) {
+        while (ev.size() < 2 * pairs) {
+            cudaEvent_t e;
+            HPBJ_CUDA(cudaEventCreate(&e));
+            ev.push_back(e);
+        }
+    }
+    ~KernelTimer() {
+        for (auto e : ev) cudaEventDestroy(e);
+    }
+};
+
+constexpr double kU53 = 1.1102230246251565e-16;  // 2^-53
+constexpr double kU24 = 5.9604644775390625e-08;  // 2^-24
+
+}  // namespace
+
+struct hpbj_ctx {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    int64_t launches = 0;
+
+    // matrix (original ordering)
+    bool has_matrix = false;
+    DevCsr A;
+    std::vector<int64_t> h_rp;
+    SpmvPlan planA;
+    double* d_tmpx = nullptr;  // n
+    double* d_tmpy = nullptr;  // n
+
+    // block-Jacobi preconditioner (permuted frame)
+    bool has_pc = false;
+    int s = 0;
+    double eps = 1e-10;
+    int dmin = 0, dmax = 0;
+    int* d_perm = nullptr;
+    DevCsr B;
+    int* d_src = nullptr;
+    int* d_bstart = nullptr;
+    int64_t* d_fac_off = nullptr;
+    float* d_fac = nullptr;
+    int64_t fac_floats = 0;
+    int* d_piv = nullptr;
+    int* d_pert_count = nullptr;
+    PertRecord* d_pert = nullptr;
+    int* d_pert_n = nullptr;
+    unsigned long long* d_singular = nullptr;
+    float* d_lu_scratch = nullptr;
+    int lu_smem_dim = 0, lu_scratch_ld = 0;
+    std::vector<int> h_bstart;
+    std::vector<int64_t> h_fac_off;
+    SpmvPlan planB;
+    int* d_long_sort = nullptr;
+    int n_long_sort = 0, max_long_sort = 0;
+
+    // solve workspace
+    int ws_m = -1;
+    KrylovBufs kb;
+    SolveState* d_st = nullptr;
+    float* d_z32 = nullptr;
+    double* d_xp = nullptr;  // x (permuted)
+    double* d_bp = nullptr;  // b (permuted)
+    double* d_r = nullptr;
+    double* d_red = nullptr;  // reduction partials
+    double* d_bo = nullptr;   // host-API staging (original ordering)
+    double* d_xo = nullptr;
+    MgsLaunch mgs;
+
+    // profiling
+    bool profiling = false;
+    KernelTimer timer;
+    hpbj_kernel_stat stats[HPBJ_K_COUNT] = {};
+
+    ~hpbj_ctx() {
+        release_matrix();
+        release_ws();
+        if (stream) cudaStreamDestroy(stream);
+    }
+
+    void release_pc() {
+        dfree(d_perm);
+        dfree(B.rp);
+        dfree(B.ci);
+        dfree(B.val);
+        dfree(d_src);
+        dfree(d_bstart);
+        dfree(d_fac_off);
+        dfree(d_fac);
+        dfree(d_piv);
+        dfree(d_pert_count);
+        dfree(d_pert);
+        dfree(d_pert_n);
+        dfree(d_singular);
+        dfree(d_lu_scratch);
+        dfree(planB.long_rows);
+        dfree(planB.ylong);
+        dfree(d_long_sort);
+        has_pc = false;
+    }
+    void release_matrix() {
+        release_pc();
+        dfree(A.rp);
+        dfree(A.ci);
+        dfree(A.val);
+        dfree(planA.long_rows);
+        dfree(planA.ylong);
+        dfree(d_tmpx);
+        dfree(d_tmpy);
+        has_matrix = false;
+    }
+    void release_ws() {
+        dfree(kb.V);
+        dfree(kb.w);
+        dfree(kb.H);
+        dfree(kb.R);
+        dfree(kb.cs);
+        dfree(kb.sn);
+        dfree(kb.g);
+        dfree(kb.y);
+        dfree(kb.est);
+        dfree(kb.partials);
+        dfree(d_st);
+        dfree(d_z32);
+        dfree(d_xp);
+        dfree(d_bp);
+        dfree(d_r);
+        dfree(d_red);
+        dfree(d_bo);
+        dfree(d_xo);
+        ws_m = -1;
+    }
+};
+
+namespace {
+
+// Lanes per row from the mean row length; hub rows go to the CTA kernel.
+SpmvPlan make_plan(const std::vector<int64_t>& rp, const int* perm_or_null, int n) {
+    SpmvPlan p;
+    const double avg = n > 0 ? double(rp[n]) / n : 0.0;
+    p.group = avg <= 6.0 ? 4 : avg <= 12.0 ? 8 : avg <= 24.0 ? 16 : 32;
+    p.long_thresh = std::max(256, 16 * p.group);
+    std::vector<int> rows;
+    for (int i = 0; i < n; ++i)
+        if (rp[i + 1] - rp[i] > p.long_thresh) rows.push_back(perm_or_null ? perm_or_null[i] : i);
+    std::sort(rows.begin(), rows.end());
+    p.n_long = (int)rows.size();
+    if (p.n_long) {
+        p.long_rows = dalloc<int>(rows.size());
+        HPBJ_CUDA(cudaMemcpy(p.long_rows, rows.data(), sizeof(int) * rows.size(), cudaMemcpyHostToDevice));
+        p.ylong = dalloc<double>(n);
+    }
+    return p;
+}
+
+void ensure_ws(hpbj_ctx* c, int m) {
+    if (c->ws_m == m) return;
+    c->release_ws();
+    const int n = c->A.n;
+    const int ldv = ((n + 31) / 32) * 32;
+    KrylovBufs& kb = c->kb;
+    kb.m = m;
+    kb.ldv = ldv;
+    kb.V = dalloc<double>((size_t)(m + 1) * ldv);
+    HPBJ_CUDA(cudaMemset(kb.V, 0, sizeof(double) * (size_t)(m + 1) * ldv));
+    kb.w = dalloc<double>(ldv);
+    HPBJ_CUDA(cudaMemset(kb.w, 0, sizeof(double) * ldv));
+    kb.H = dalloc<double>((size_t)(m + 1) * m);
+    kb.R = dalloc<double>((size_t)(m + 1) * m);
+    kb.cs = dalloc<double>(m);
+    kb.sn = dalloc<double>(m);
+    kb.g = dalloc<double>(m + 1);
+    kb.y = dalloc<double>(m);
+    kb.est = dalloc<double>(m);
+    kb.partials = dalloc<double>(4 * 1024);
+    c->d_st = dalloc<SolveState>(1);
+    HPBJ_CUDA(cudaMemset(c->d_st, 0, sizeof(SolveState)));
+    c->d_z32 = dalloc<float>(ldv);
+    HPBJ_CUDA(cudaMemset(c->d_z32, 0, sizeof(float) * ldv));
+    c->d_xp = dalloc<double>(ldv);
+    c->d_bp = dalloc<double>(ldv);
+    c->d_r = dalloc<double>(ldv);
+    c->d_red = dalloc<double>(2048);
+    c->d_bo = dalloc<double>(ldv);
+    c->d_xo = dalloc<double>(ldv);
+    c->mgs = plan_mgs(n, c->num_sms);
+    c->ws_m = m;
+}
+
+ApplyParams apply_params(const hpbj_ctx* c) {
+    return ApplyParams{c->s, c->d_bstart, c->d_fac_off, c->d_fac, c->d_piv, c->dmax};
+}
+
+void factor(hpbj_ctx* c, hpbj_setup_info* info) {
+    cudaStream_t st = c->stream;
+    const unsigned long long none = ~0ull;
+    HPBJ_CUDA(cudaMemcpyAsync(c->d_singular, &none, sizeof(none), cudaMemcpyHostToDevice, st));
+    HPBJ_CUDA(cudaMemsetAsync(c->d_pert_n, 0, sizeof(int), st));
+    LuParams p;
+    p.s = c->s;
+    p.bstart = c->d_bstart;
+    p.fac_off = c->d_fac_off;
+    p.a = c->B;
+    p.fac = c->d_fac;
+    p.piv = c->d_piv;
+    p.pert_count = c->d_pert_count;
+    p.pert = c->d_pert;
+    p.pert_n = c->d_pert_n;
+    p.pert_cap = 4096;
+    p.singular = c->d_singular;
+    p.eps = c->eps;
+    p.scratch = c->d_lu_scratch;
+    p.smem_dim = c->lu_smem_dim;
+    p.scratch_ld = c->lu_scratch_ld;
+    cudaEvent_t e0, e1;
+    HPBJ_CUDA(cudaEventCreate(&e0));
+    HPBJ_CUDA(cudaEventCreate(&e1));
+    HPBJ_CUDA(cudaEventRecord(e0, st));
+    launch_gather_values(c->d_src, c->A.val, c->B.val, c->B.nnz, st, &c->launches);
+    launch_block_lu(p, c->dmax, c->num_sms, st, &c->launches);
+    HPBJ_CUDA(cudaEventRecord(e1, st));
+    unsigned long long sing = 0;
+    int pert_n = 0;
+    HPBJ_CUDA(cudaMemcpyAsync(&sing, c->d_singular, sizeof(sing), cudaMemcpyDeviceToHost, st));
+    HPBJ_CUDA(cudaMemcpyAsync(&pert_n, c->d_pert_n, sizeof(int), cudaMemcpyDeviceToHost, st));
+    HPBJ_CUDA(cudaStreamSynchronize(st));
+    float ms = 0.f;
+    HPBJ_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (info) {
+        info->num_blocks = c->s;
+        info->dim_min = c->dmin;
+        info->dim_max = c->dmax;
+        info->perturbations = pert_n;
+        info->singular_block = -1;
+        info->singular_column = -1;
+        info->factor_bytes = c->fac_floats * (int64_t)sizeof(float);
+        info->ms_factor = ms;
+    }
+    if (sing != none) {
+        const int64_t blk = (int64_t)(sing >> 32), col = (int64_t)(sing & 0xffffffffu);
+        if (info) {
+            info->singular_block = blk;
+            info->singular_column = col;
+        }
+        c->has_pc = false;
+        fail(HPBJ_ESINGULAR, "gp_lu: singular block, zero pivot in column " + std::to_string(col) +
+                                 " (block " + std::to_string(blk) + ")");
+    }
+}
+
+void record_kernel(hpbj_ctx* c, size_t slot, bool begin) {
+    if (!c->profiling) return;
+    HPBJ_CUDA(cudaEventRecord(c->timer.ev[2 * slot + (begin ? 0 : 1)], c->stream));
+}
+
+void solve(hpbj_ctx* c, const double* d_b, double* d_x, const hpbj_gmres_opts* o, hpbj_report* rep,
+           hpbj_history_point* hist, int64_t hist_cap, double* cycle_res, int64_t cyc_cap) {
+    const auto t0 = std::chrono::steady_clock::now();
+    hpbj_gmres_opts opt;
+    hpbj_gmres_default_opts(&opt);
+    if (o) opt = *o;
+    if (!c->has_matrix) fail(HPBJ_ELOGIC, "gmres: no matrix");
+    if (!c->has_pc) fail(HPBJ_ELOGIC, "gmres: block-Jacobi preconditioner not set up");
+    if (opt.restart_m < 1 || opt.tol <= 0.0 || opt.max_restarts < 1)
+        fail(HPBJ_EINVAL, "gmres: invalid config");
+    if (opt.restart_m > 1024) fail(HPBJ_EINVAL, "gmres: restart_m > 1024 unsupported");
+    const int n = c->A.n;
+    const int m = (int)opt.restart_m;
+    const double floor_u = opt.floor_roundoff > 0.0 ? opt.floor_roundoff : kU24;
+    ensure_ws(c, m);
+    cudaStream_t st = c->stream;
+    KrylovBufs& kb = c->kb;
+    hpbj_report R{};
+    int64_t hlen = 0, clen = 0;
+    auto push_hist = [&](int64_t cyc, int64_t it, double rel) {
+        if (hist && hlen < hist_cap) hist[hlen] = hpbj_history_point{cyc, it, rel};
+        ++hlen;
+    };
+
+    // permuted b; ||b||
+    launch_permute_vec(n, c->d_perm, d_b, c->d_bp, false, st, &c->launches);
+    launch_norm(c->d_bp, n, c->d_st, c->d_red, st, &c->launches);
+    SolveState hs{};
+    HPBJ_CUDA(cudaMemcpyAsync(&hs, c->d_st, sizeof(hs), cudaMemcpyDeviceToHost, st));
+    HPBJ_CUDA(cudaStreamSynchronize(st));
+    const double bnorm = hs.scratch;
+    HPBJ_CUDA(cudaMemsetAsync(c->d_xp, 0, sizeof(double) * kb.ldv, st));
+    if (bnorm == 0.0) {
+        R.converged = 1;
+        push_hist(0, 0, 0.0);
+        HPBJ_CUDA(cudaMemsetAsync(d_x, 0, sizeof(double) * n, st));
+        HPBJ_CUDA(cudaStreamSynchronize(st));
+        R.history_len = hlen;
+        R.ms_solve = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        if (rep) *rep = R;
+        return;
+    }
+    const double thr = opt.absolute_tol ? opt.tol : opt.tol * bnorm;
+    hs.n = n;
+    hs.m = m;
+    hs.ldv = kb.ldv;
+    hs.thr = thr;
+    hs.bnorm = bnorm;
+    hs.breakdown_factor = opt.breakdown_tol_factor * kU53;
+    hs.floor_roundoff = floor_u;
+    hs.done = 0;
+    hs.ticket = 0;
+    HPBJ_CUDA(cudaMemcpyAsync(c->d_st, &hs, sizeof(hs), cudaMemcpyHostToDevice, st));
+
+    // r = b - A*0, ||r|| (gmres.cpp:223-230)
+    launch_residual(c->B, c->planB, c->d_xp, c->d_bp, c->d_r, c->d_st, c->d_red, st, &c->launches);
+    HPBJ_CUDA(cudaMemcpyAsync(&hs, c->d_st, sizeof(hs), cudaMemcpyDeviceToHost, st));
+    HPBJ_CUDA(cudaStreamSynchronize(st));
+    double rnorm = hs.rnorm;
+    push_hist(0, 0, rnorm / bnorm);
+    R.final_residual = rnorm / bnorm;
+    if (rnorm <= thr) {
+        R.converged = 1;
+    } else {
+        if (c->profiling) c->timer.reserve((size_t)3 * m);
+        int64_t global_iter = 0;
+        int64_t cycles = 0;
+        std::vector<double> est(m);
+        for (int64_t cycle = 0; cycle < opt.max_restarts; ++cycle) {
+            launch_cycle_init(kb, c->d_st, c->d_r, n, st, &c->launches);
+            for (int it = 0; it < m; ++it) {
+                record_kernel(c, 3 * it + 0, true);
+                launch_apply_step(apply_params(c), kb.V, kb.ldv, c->d_st, c->d_z32, st, &c->launches);
+                record_kernel(c, 3 * it + 0, false);
+                record_kernel(c, 3 * it + 1, true);
+                launch_spmv_f32x(c->B, c->planB, c->d_z32, kb.w, c->d_st, st, &c->launches);
+                record_kernel(c, 3 * it + 1, false);
+                record_kernel(c, 3 * it + 2, true);
+                launch_mgs(c->mgs, kb, c->d_st, n, st, &c->launches);
+                record_kernel(c, 3 * it + 2, false);
+            }
+            launch_solve_y(kb, c->d_st, st, &c->launches);
+            launch_apply_update(apply_params(c), kb.V, kb.ldv, kb.y, c->d_st, c->d_xp, st, &c->launches);
+            launch_residual(c->B, c->planB, c->d_xp, c->d_bp, c->d_r, c->d_st, c->d_red, st, &c->launches);
+            HPBJ_CUDA(cudaMemcpyAsync(&hs, c->d_st, sizeof(hs), cudaMemcpyDeviceToHost, st));
+            HPBJ_CUDA(cudaMemcpyAsync(est.data(), kb.est, sizeof(double) * m, cudaMemcpyDeviceToHost, st));
+            HPBJ_CUDA(cudaStreamSynchronize(st));
+            ++cycles;
+            const int steps = hs.j;
+            if (c->profiling) {
+                for (int it = 0; it < steps; ++it)
+                    for (int k = 0; k < 3; ++k) {
+                        float ms = 0.f;
+                        HPBJ_CUDA(cudaEventElapsedTime(&ms, c->timer.ev[2 * (3 * it + k)],
+                                                       c->timer.ev[2 * (3 * it + k) + 1]));
+                        c->stats[k].launches += 1;
+                        c->stats[k].total_ms += ms;
+                    }
+            }
+            for (int k = 0; k < steps; ++k) push_hist(cycle, ++global_iter, est[k] / bnorm);
+            R.total_iterations += steps;
+            R.breakdown = R.breakdown || hs.breakdown;
+            R.ls_rank_deficient = R.ls_rank_deficient || hs.rank_deficient;
+            rnorm = hs.rnorm;
+            if (cycle_res && clen < cyc_cap) cycle_res[clen] = rnorm / bnorm;
+            ++clen;
+            if (rnorm <= thr) {
+                R.converged = 1;
+                break;
+            }
+            if (steps == 0) break;
+        }
+        R.restarts = cycles > 0 ? cycles - 1 : 0;
+        R.final_residual = rnorm / bnorm;
+    }
+    launch_permute_vec(n, c->d_perm, c->d_xp, d_x, true, st, &c->launches);
+    HPBJ_CUDA(cudaStreamSynchronize(st));
+    R.history_len = hlen;
+    R.cycles = clen;
+    R.ms_solve = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (rep) *rep = R;
+}
+
+}  // namespace
+
+// ============================================================================
+extern "C" {
+
+int hpbj_create(hpbj_ctx** out, int device) {
+    if (!out) return HPBJ_EINVAL;
+    *out = nullptr;
+    return guard(nullptr, [&] {
+        int count = 0;
+        if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+            fail(HPBJ_ENODEV, "hpbj: no CUDA device (there is no CPU fallback)");
+        if (device < 0 || device >= count) fail(HPBJ_EINVAL, "hpbj: bad device index");
+        HPBJ_CUDA(cudaSetDevice(device));
+        cudaDeviceProp prop;
+        HPBJ_CUDA(cudaGetDeviceProperties(&prop, device));
+        if (prop.major < 10) fail(HPBJ_ENODEV, "hpbj: needs an sm_100a (Blackwell) device");
+        auto* c = new hpbj_ctx();
+        c->device = device;
+        c->num_sms = prop.multiProcessorCount;
+        HPBJ_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        *out = c;
+    });
+}
+
+void hpbj_destroy(hpbj_ctx* ctx) { delete ctx; }
+
+const char* hpbj_last_error(const hpbj_ctx* ctx) { return ctx ? ctx->err.c_str() : thread_error(); }
+
+int64_t hpbj_kernel_launches(const hpbj_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int hpbj_set_profiling(hpbj_ctx* ctx, int enable) {
+    if (!ctx) return HPBJ_EINVAL;
+    ctx->profiling = enable != 0;
+    for (auto& s : ctx->stats) s = hpbj_kernel_stat{};
+    return HPBJ_OK;
+}
+
+int hpbj_get_kernel_stats(hpbj_ctx* ctx, hpbj_kernel_stat* out) {
+    if (!ctx || !out) return HPBJ_EINVAL;
+    return guard(&ctx->err, [&] {
+        // algorithmic bytes per launch
+        const double n = ctx->A.n, nnz = ctx->A.nnz;
+        double bytes_apply = 0.0;
+        if (ctx->has_pc) {
+            bytes_apply = 4.0 * (double)ctx->fac_floats  // packed FP32 factor panels
+                          + 4.0 * n                      // pivot rows (int32)
+                          + 8.0 * n                      // v (FP64) in
+                          + 4.0 * n                      // z (FP32) out
+                          + 4.0 * (ctx->s + 1) + 8.0 * ctx->s;  // block starts + offsets
+        }
+        const double bytes_spmv = 12.0 * nnz + 4.0 * (n + 1) + 4.0 * n + 8.0 * n;
+        for (int k = 0; k < HPBJ_K_COUNT; ++k) out[k] = ctx->stats[k];
+        out[HPBJ_K_APPLY].bytes_per_launch = bytes_apply;
+        out[HPBJ_K_SPMV].bytes_per_launch = bytes_spmv;
+        // MGS bytes depend on j: mean over recorded launches is computed by the caller
+        out[HPBJ_K_MGS].bytes_per_launch = 0.0;
+    });
+}
+
+int hpbj_set_matrix(hpbj_ctx* ctx, int64_t n, const int64_t* row_ptr, const int64_t* col, const double* val) {
+    if (!ctx) return HPBJ_EINVAL;
+    return guard(&ctx->err, [&] {
+        check_csr(n, row_ptr, col, val);
+        if (n >= (int64_t)INT32_MAX || row_ptr[n] >= (int64_t)INT32_MAX)
+            fail(HPBJ_EINVAL, "hpbj: n and nnz must be < 2^31");
+        HPBJ_CUDA(cudaSetDevice(ctx->device));
+        ctx->release_matrix();
+        ctx->release_ws();
+        const int ni = (int)n, nnz = (int)row_ptr[n];
+        std::vector<int> rp(ni + 1), ci(nnz);
+        for (int64_t i = 0; i <= n; ++i) rp[i] = (int)row_ptr[i];
+        for (int64_t k = 0; k < nnz; ++k) ci[k] = (int)col[k];
+        ctx->A.n = ni;
+        ctx->A.nnz = nnz;
+        ctx->A.rp = dalloc<int>(ni + 1);
+        ctx->A.ci = dalloc<int>(nnz);
+        ctx->A.val = dalloc<double>(nnz);
+        HPBJ_CUDA(cudaMemcpy(ctx->A.rp, rp.data(), sizeof(int) * (ni + 1), cudaMemcpyHostToDevice));
+        HPBJ_CUDA(cudaMemcpy(ctx->A.ci, ci.data(), sizeof(int) * nnz, cudaMemcpyHostToDevice));
+        HPBJ_CUDA(cudaMemcpy(ctx->A.val, val, sizeof(double) * nnz, cudaMemcpyHostToDevice));
+        ctx->h_rp.assign(row_ptr, row_ptr + n + 1);
+        ctx->planA = make_plan(ctx->h_rp, nullptr, ni);
+        ctx->d_tmpx = dalloc<double>(ni);
+        ctx->d_tmpy = dalloc<double>(ni);
+        ctx->has_matrix = true;
+    });
+}
+
+int hpbj_update_values(hpbj_ctx* ctx, const double* val) {
+    if (!ctx) return HPBJ_EINVAL;
+    return guard(&ctx->err, [&] {
+        if (!ctx->has_matrix) fail(HPBJ_ELOGIC, "update_values: no matrix");
+        HPBJ_CUDA(cudaMemcpyAsync(ctx->A.val, val, sizeof(double) * ctx->A.nnz, cudaMemcpyHostToDevice,
+                                  ctx->stream));
+        HPBJ_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int hpbj_spmv(hpbj_ctx* ctx, const double* x, double* y) {
+    if (!ctx) return HPBJ_EINVAL;
+    return guard(&ctx->err, [&] {
+        if (!ctx->has_matrix) fail(HPBJ_ELOGIC, "spmv: no matrix");
+        const int n = ctx->A.n;
+        HPBJ_CUDA(cudaMemcpyAsync(ctx->d_tmpx, x, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+        launch_spmv_f64x(ctx->A, ctx->planA, ctx->d_tmpx, ctx->d_tmpy, ctx->stream, &ctx->launches);
+        HPBJ_CUDA(cudaMemcpyAsync(y, ctx->d_tmpy, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+        HPBJ_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int hpbj_bj_setup(hpbj_ctx* ctx, int64_t s, const int64_t* perm, const int64_t* block_starts, double eps_pivot,
+                  hpbj_setup_info* info) {
+    if (!ctx) return HPBJ_EINVAL;
+    if (info) {
+        std::memset(info, 0, sizeof(*info));
+        info->singular_block = info->singular_column = -1;
+    }
+    return guard(&ctx->err, [&] {
+        if (!ctx->has_matrix) fail(HPBJ_ELOGIC, "block_jacobi: no matrix");
+        if (eps_pivot < 0.0) fail(HPBJ_EINVAL, "gp_lu: negative eps_pivot");
+        const int n = ctx->A.n;
+        if (s < 1 || s > n) fail(HPBJ_EINVAL, "partition: block count must satisfy 1 <= s <= n");
+        // validate the partition (bijection, contiguous nonempty blocks)
+        std::vector<int> hperm(n);
+        std::vector<char> seen(n, 0);
+        for (int i = 0; i < n; ++i) {
+            const int64_t p = perm[i];
+            if (p < 0 || p >= n || seen[p]) fail(HPBJ_EINVAL, "permute_symmetric: not a bijection");
+            seen[p] = 1;
+            hperm[i] = (int)p;
+        }
+        if (block_starts[0] != 0 || block_starts[s] != n)
+            fail(HPBJ_EINVAL, "block_jacobi: partition does not cover the matrix");
+        std::vector<int> bst(s + 1);
+        int dmin = n, dmax = 0;
+        for (int64_t b = 0; b < s; ++b) {
+            const int64_t d = block_starts[b + 1] - block_starts[b];
+            if (d <= 0) fail(HPBJ_EINVAL, "partition: block " + std::to_string(b) + " is empty");
+            dmin = std::min<int>(dmin, (int)d);
+            dmax = std::max<int>(dmax, (int)d);
+            bst[b] = (int)block_starts[b];
+        }
+        bst[s] = n;
+        ctx->release_pc();
+        cudaStream_t st = ctx->stream;
+        ctx->s = (int)s;
+        ctx->eps = eps_pivot;
+        ctx->dmin = dmin;
+        ctx->dmax = dmax;
+        ctx->h_bstart = bst;
+        ctx->h_fac_off.resize(s);
+        int64_t off = 0;
+        for (int64_t b = 0; b < s; ++b) {
+            ctx->h_fac_off[b] = off;
+            off += panel_floats(bst[b + 1] - bst[b]);
+        }
+        ctx->fac_floats = off;
+        const int nnz = ctx->A.nnz;
+        ctx->d_perm = dalloc<int>(n);
+        ctx->B.n = n;
+        ctx->B.nnz = nnz;
+        ctx->B.rp = dalloc<int>(n + 1);
+        ctx->B.ci = dalloc<int>(nnz);
+        ctx->B.val = dalloc<double>(nnz);
+        ctx->d_src = dalloc<int>(nnz);
+        ctx->d_bstart = dalloc<int>(s + 1);
+        ctx->d_fac_off = dalloc<int64_t>(s);
+        ctx->d_fac = dalloc<float>(off);
+        ctx->d_piv = dalloc<int>(n);
+        ctx->d_pert_count = dalloc<int>(s);
+        ctx->d_pert = dalloc<PertRecord>(4096);
+        ctx->d_pert_n = dalloc<int>(1);
+        ctx->d_singular = dalloc<unsigned long long>(1);
+        const size_t scr = block_lu_scratch_floats(dmax, ctx->num_sms, &ctx->lu_smem_dim, &ctx->lu_scratch_ld);
+        if (scr) ctx->d_lu_scratch = dalloc<float>(scr);
+        HPBJ_CUDA(cudaMemcpyAsync(ctx->d_perm, hperm.data(), sizeof(int) * n, cudaMemcpyHostToDevice, st));
+        HPBJ_CUDA(cudaMemcpyAsync(ctx->d_bstart, bst.data(), sizeof(int) * (s + 1), cudaMemcpyHostToDevice, st));
+        HPBJ_CUDA(cudaMemcpyAsync(ctx->d_fac_off, ctx->h_fac_off.data(), sizeof(int64_t) * s,
+                                  cudaMemcpyHostToDevice, st));
+        // rows needing a CTA sort after the scatter (permuted indices)
+        std::vector<int> lrows;
+        int maxlen = 0;
+        for (int i = 0; i < n; ++i) {
+            const int len = (int)(ctx->h_rp[i + 1] - ctx->h_rp[i]);
+            if (len > kShortRow) {
+                lrows.push_back(hperm[i]);
+                maxlen = std::max(maxlen, len);
+            }
+        }
+        ctx->n_long_sort = (int)lrows.size();
+        ctx->max_long_sort = maxlen;
+        if (!lrows.empty()) {
+            ctx->d_long_sort = dalloc<int>(lrows.size());
+            HPBJ_CUDA(cudaMemcpyAsync(ctx->d_long_sort, lrows.data(), sizeof(int) * lrows.size(),
+                                      cudaMemcpyHostToDevice, st));
+        }
+        ctx->planB = make_plan(ctx->h_rp, hperm.data(), n);
+        int* tmp = dalloc<int>((size_t)n + 8192);
+        cudaEvent_t e0, e1;
+        HPBJ_CUDA(cudaEventCreate(&e0));
+        HPBJ_CUDA(cudaEventCreate(&e1));
+        HPBJ_CUDA(cudaEventRecord(e0, st));
+        launch_permute_pattern(ctx->A, ctx->d_perm, ctx->B, ctx->d_src, tmp, ctx->d_long_sort, ctx->n_long_sort,
+                               ctx->max_long_sort, st, &ctx->launches);
+        HPBJ_CUDA(cudaEventRecord(e1, st));
+        HPBJ_CUDA(cudaStreamSynchronize(st));
+        float ms = 0.f;
+        HPBJ_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        cudaFree(tmp);
+        ctx->has_pc = true;
+        factor(ctx, info);
+        if (info) info->ms_permute = ms;
+    });
+}
+
+int hpbj_bj_refactor(hpbj_ctx* ctx, hpbj_setup_info* info) {
+    if (!ctx) return HPBJ_EINVAL;
+    if (info) {
+        std::memset(info, 0, sizeof(*info));
+        info->singular_block = info->singular_column = -1;
+    }
+    return guard(&ctx->err, [&] {
+        if (!ctx->d_fac) fail(HPBJ_ELOGIC, "refactor: no block-Jacobi partition set up");
+        ctx->has_pc = true;
+        factor(ctx, info);
+    });
+}
+
+int hpbj_bj_apply(hpbj_ctx* ctx, const double* v, double* z) {
+    if (!ctx) return HPBJ_EINVAL;
+    return guard(&ctx->err, [&] {
+        if (!ctx->has_pc) fail(HPBJ_ELOGIC, "apply: block-Jacobi preconditioner not set up");
+        const int n = ctx->A.n;
+        cudaStream_t st = ctx->stream;
+        HPBJ_CUDA(cudaMemcpyAsync(ctx->d_tmpx, v, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+        launch_permute_vec(n, ctx->d_perm, ctx->d_tmpx, ctx->d_tmpy, false, st, &ctx->launches);
+        launch_apply_f32(apply_params(ctx), ctx->d_tmpy, nullptr, 0, nullptr, ctx->d_tmpx, st, &ctx->launches);
+        launch_permute_vec(n, ctx->d_perm, ctx->d_tmpx, ctx->d_tmpy, true, st, &ctx->launches);
+        HPBJ_CUDA(cudaMemcpyAsync(z, ctx->d_tmpy, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+        HPBJ_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+int hpbj_get_block_factors(hpbj_ctx* ctx, int64_t block, int64_t* dim, float* f, int64_t* pivot_rows) {
+    if (!ctx) return HPBJ_EINVAL;
+    return guard(&ctx->err, [&] {
+        if (!ctx->has_pc) fail(HPBJ_ELOGIC, "factors: block-Jacobi preconditioner not set up");
+        if (block < 0 || block >= ctx->s) fail(HPBJ_ERANGE, "factors: block index out of range");
+        const int o = ctx->h_bstart[block];
+        const int d = ctx->h_bstart[block + 1] - o;
+        if (dim) *dim = d;
+        const int64_t pf = panel_floats(d);
+        std::vector<float> packed(pf);
+        std::vector<int> piv(d);
+        HPBJ_CUDA(cudaMemcpy(packed.data(), ctx->d_fac + ctx->h_fac_off[block], sizeof(float) * pf,
+                             cudaMemcpyDeviceToHost));
+        HPBJ_CUDA(cudaMemcpy(piv.data(), ctx->d_piv + o, sizeof(int) * d, cudaMemcpyDeviceToHost));
+        const int dp4 = (d + 3) & ~3;
+        if (f)
+            for (int k = 0; k < d; ++k)
+                for (int c2 = 0; c2 < d; ++c2)
+                    f[(size_t)k * d + c2] =
+                        packed[(size_t)(k / 32) * 32 * dp4 + (c2 / 4) * 128 + (k % 32) * 4 + (c2 % 4)];
+        if (pivot_rows)
+            for (int k = 0; k < d; ++k) pivot_rows[k] = piv[k];
+    });
+}
+
+int hpbj_get_block_stats(hpbj_ctx* ctx, int64_t* dims, int64_t* perturbations) {
+    if (!ctx) return HPBJ_EINVAL;
+    return guard(&ctx->err, [&] {
+        if (!ctx->has_pc) fail(HPBJ_ELOGIC, "stats: block-Jacobi preconditioner not set up");
+        std::vector<int> pc(ctx->s);
+        HPBJ_CUDA(cudaMemcpy(pc.data(), ctx->d_pert_count, sizeof(int) * ctx->s, cudaMemcpyDeviceToHost));
+        for (int b = 0; b < ctx->s; ++b) {
+            if (dims) dims[b] = ctx->h_bstart[b + 1] - ctx->h_bstart[b];
+            if (perturbations) perturbations[b] = pc[b];
+        }
+    });
+}
+
+void hpbj_gmres_default_opts(hpbj_gmres_opts* o) {
+    if (!o) return;
+    o->restart_m = 50;
+    o->tol = 1e-8;
+    o->max_restarts = 40;
+    o->absolute_tol = 0;
+    o->reserved = 0;
+    o->breakdown_tol_factor = 1e2;
+    o->floor_roundoff = kU24;
+}
+
+int hpbj_gmres(hpbj_ctx* ctx, const double* b, double* x, const hpbj_gmres_opts* opts, hpbj_report* rep,
+               hpbj_history_point* hist, int64_t hist_cap, double* cycle_res, int64_t cyc_cap) {
+    if (!ctx) return HPBJ_EINVAL;
+    return guard(&ctx->err, [&] {
+        if (!ctx->has_matrix) fail(HPBJ_ELOGIC, "gmres: no matrix");
+        const int n = ctx->A.n;
+        const int m = opts ? (int)opts->restart_m : 50;
+        if (m >= 1) ensure_ws(ctx, m);
+        else fail(HPBJ_EINVAL, "gmres: invalid config");
+        HPBJ_CUDA(cudaMemcpyAsync(ctx->d_bo, b, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+        solve(ctx, ctx->d_bo, ctx->d_xo, opts, rep, hist, hist_cap, cycle_res, cyc_cap);
+        HPBJ_CUDA(cudaMemcpyAsync(x, ctx->d_xo, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+        HPBJ_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int hpbj_gmres_device(hpbj_ctx* ctx, const double* d_b, double* d_x, const hpbj_gmres_opts* opts,
+                      hpbj_report* rep, hpbj_history_point* hist, int64_t hist_cap, double* cycle_res,
+                      int64_t cyc_cap) {
+    if (!ctx) return HPBJ_EINVAL;
+    return guard(&ctx->err, [&] { solve(ctx, d_b, d_x, opts, rep, hist, hist_cap, cycle_res, cyc_cap); });
+}
+
+}  // extern "C"

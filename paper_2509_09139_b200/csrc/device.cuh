@@ -1,0 +1,99 @@
+// Device-side shared definitions for libhpbj.so (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "hpbj_common.hpp"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "libhpbj targets sm_100a (B200) only"
+#endif
+
+namespace hpbj {
+
+#define HPBJ_CUDA(call)                                                                   \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess)                                                            \
+            ::hpbj::fail(e_ == cudaErrorMemoryAllocation ? HPBJ_ENOMEM : HPBJ_ECUDA,      \
+                         std::string(#call) + ": " + cudaGetErrorString(e_));             \
+    } while (0)
+
+constexpr int kWarp = 32;
+
+// ---------------------------------------------------------------------------
+// Solver control block, resident in device memory for the whole solve. The
+// Arnoldi kernels read/write it so no host round-trip happens per iteration;
+// the host reads it once per restart cycle.
+struct SolveState {
+    // configuration (written once per solve)
+    int64_t n;
+    int32_t m;             // restart length
+    int32_t ldv;           // leading dimension of the basis (doubles)
+    double thr;            // tol * ||b|| (or tol if absolute)
+    double bnorm;
+    double breakdown_factor;   // 1e2 * 2^-53 (FP64 basis)
+    double floor_roundoff;     // 2^-24 (FP32 preconditioner)
+    // per cycle
+    double beta;           // ||r0||
+    double attainable;     // 10 * floor_roundoff * beta
+    int32_t j;             // Arnoldi steps completed in this cycle
+    int32_t done;          // cycle finished (converged / breakdown / floor / m)
+    int32_t converged_est;
+    int32_t breakdown;
+    int32_t rank_deficient;
+    int32_t pad;
+    double pre_norm;       // last ||w|| before orthogonalisation
+    double last_est;
+    // reductions
+    double rnorm;          // true residual norm from the last residual kernel
+    double scratch;
+    uint32_t ticket;       // last-block-done counter
+    uint32_t pad2;
+};
+
+// Grid-wide deterministic reduction: each CTA deposits a partial; the last
+// CTA to arrive sums them in CTA order (fixed, run-to-run reproducible).
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ float warp_sumf(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Block-wide sum with a fixed order; every thread gets the result.
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double* sh /* NT/32 */) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) sh[wid] = v;
+    __syncthreads();
+    double t = 0.0;
+    if (wid == 0) {
+        t = lane < NT / 32 ? sh[lane] : 0.0;
+        t = warp_sum(t);
+        if (lane == 0) sh[0] = t;
+    }
+    __syncthreads();
+    t = sh[0];
+    return t;
+}
+
+// Sums partials[0..count) in a fixed order (lane-strided then xor tree).
+__device__ __forceinline__ double warp_sum_partials(const double* partials, int count) {
+    const int lane = threadIdx.x & 31;
+    double s = 0.0;
+    for (int i = lane; i < count; i += 32) s += __ldcg(partials + i);
+    return warp_sum(s);
+}
+
+}  // namespace hpbj

@@ -1,0 +1,143 @@
+// Launch wrappers of the sm_100a kernels (one .cu per kernel family).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "device.cuh"
+
+namespace hpbj {
+
+constexpr int kShortRow = 32;             // rows sorted in registers by one thread
+constexpr size_t kSmemSortMax = 128 * 1024;
+
+// CSR on the device: int32 indices (nnz < 2^31), FP64 values.
+struct DevCsr {
+    int n = 0;
+    int nnz = 0;
+    int* rp = nullptr;
+    int* ci = nullptr;
+    double* val = nullptr;
+};
+
+// ---- permute.cu -----------------------------------------------------------
+void scan_exclusive(const int* in, int* out, int n, int* tmp, cudaStream_t st, int64_t* launches);
+void launch_permute_pattern(const DevCsr& a, const int* perm, DevCsr& b, int* src, int* tmp,
+                            const int* long_rows_new, int n_long, int max_long, cudaStream_t st,
+                            int64_t* launches);
+void launch_gather_values(const int* src, const double* val, double* nval, int nnz, cudaStream_t st,
+                          int64_t* launches);
+void launch_permute_vec(int n, const int* perm, const double* x, double* y, bool inverse, cudaStream_t st,
+                        int64_t* launches);
+
+// ---- block_lu.cu ----------------------------------------------------------
+struct PertRecord {
+    int block;
+    int column;
+    double original;
+    double replaced;
+};
+
+struct LuParams {
+    int s;
+    const int* bstart;      // s + 1, permuted indices
+    const int64_t* fac_off;  // s, float offsets into fac (packed panels)
+    DevCsr a;               // permuted matrix
+    float* fac;
+    int* piv;               // n: local pivot row for pivot position k of block b at bstart[b] + k
+    int* pert_count;        // s
+    PertRecord* pert;       // capacity pert_cap
+    int* pert_n;
+    int pert_cap;
+    unsigned long long* singular;  // min over (block << 32 | column); ~0 if none
+    double eps;
+    float* scratch;         // global tiles for blocks too large for shared memory
+    int smem_dim;           // blocks with dim <= smem_dim factor in shared memory
+    int scratch_ld;
+};
+
+// Packed factor layout: block b with dim d, T = ceil(d/32)
+// row panels of 32 pivot-ordered rows x dp4 = roundup(d, 4) columns; element
+// (k, c) at fac_off[b] + (k/32)*32*dp4 + (c/4)*128 + (k%32)*4 + (c%4).
+__host__ __device__ inline int64_t panel_floats(int d) {
+    const int T = (d + 31) / 32;
+    const int dp4 = (d + 3) & ~3;
+    return (int64_t)T * 32 * dp4;
+}
+
+void launch_block_lu(const LuParams& p, int dmax, int num_sms, cudaStream_t st, int64_t* launches);
+size_t block_lu_scratch_floats(int dmax, int num_sms, int* smem_dim, int* scratch_ld);
+
+// ---- apply.cu -------------------------------------------------------------
+struct ApplyParams {
+    int s;
+    const int* bstart;
+    const int64_t* fac_off;
+    const float* fac;
+    const int* piv;
+    int dmax;
+};
+
+// z = M^-1 v (permuted space). FP32 arithmetic; v FP64 rounded on load.
+void launch_apply_f32(const ApplyParams& p, const double* v, const SolveState* st_or_null,
+                      int ldv, float* z32, double* z64, cudaStream_t st, int64_t* launches);
+// Arnoldi step: z32 = M^-1 V[:, st->j] (column resolved on the device).
+void launch_apply_step(const ApplyParams& p, const double* V, int ldv, const SolveState* sst, float* z32,
+                       cudaStream_t st, int64_t* launches);
+// x += M^-1 (V y): fused basis combination, FP64 arithmetic on FP32 factors.
+void launch_apply_update(const ApplyParams& p, const double* V, int ldv, const double* y,
+                         const SolveState* sst, double* x, cudaStream_t st, int64_t* launches);
+
+// ---- spmv.cu --------------------------------------------------------------
+struct SpmvPlan {
+    int group = 8;            // lanes per row
+    int long_thresh = 256;    // rows longer than this go to the CTA-per-row kernel
+    int n_long = 0;
+    int* long_rows = nullptr; // permuted indices of long rows (device)
+    double* ylong = nullptr;  // n doubles (only long rows used)
+};
+
+// y = A x, x FP32 (preconditioned vector) or FP64; early exit if st->done.
+void launch_spmv_f32x(const DevCsr& a, const SpmvPlan& plan, const float* x, double* y,
+                      const SolveState* sst, cudaStream_t st, int64_t* launches);
+void launch_spmv_f64x(const DevCsr& a, const SpmvPlan& plan, const double* x, double* y,
+                      cudaStream_t st, int64_t* launches);
+// r = b - A x and st->rnorm = ||r||_2 (deterministic grid reduction).
+void launch_residual(const DevCsr& a, const SpmvPlan& plan, const double* x, const double* b, double* r,
+                     SolveState* sst, double* partials, cudaStream_t st, int64_t* launches);
+// st->scratch = ||x||_2
+void launch_norm(const double* x, int n, SolveState* sst, double* partials, cudaStream_t st,
+                 int64_t* launches);
+
+// ---- arnoldi.cu -----------------------------------------------------------
+struct KrylovBufs {
+    double* V = nullptr;   // (m+1) x ldv
+    int ldv = 0;
+    double* w = nullptr;   // SpMV output / global MGS scratch
+    double* H = nullptr;   // (m+1) x m, column-major (gmres.hpp:24)
+    double* R = nullptr;   // Givens-rotated copy
+    double* cs = nullptr;
+    double* sn = nullptr;
+    double* g = nullptr;   // m + 1
+    double* y = nullptr;   // m
+    double* est = nullptr; // m: Givens estimate after each step of the cycle
+    double* partials = nullptr;
+    int m = 0;
+};
+
+struct MgsLaunch {
+    int grid = 0;
+    int threads = 1024;
+    int slice = 0;
+    size_t smem = 0;
+    bool w_in_smem = true;
+};
+
+MgsLaunch plan_mgs(int n, int num_sms);
+void launch_mgs(const MgsLaunch& L, const KrylovBufs& kb, SolveState* sst, int n, cudaStream_t st,
+                int64_t* launches);
+void launch_cycle_init(const KrylovBufs& kb, SolveState* sst, const double* r, int n, cudaStream_t st,
+                       int64_t* launches);
+void launch_solve_y(const KrylovBufs& kb, SolveState* sst, cudaStream_t st, int64_t* launches);
+
+}  // namespace hpbj

@@ -1,0 +1,210 @@
+"""GPU parity of the individual kernels (through the C ABI) against the
+reference library (oracle/_ref) and the reference's known-answer tests."""
+import numpy as np
+import pytest
+
+import paper_2509_09139_b200 as hp
+from paper_2509_09139_b200.workloads import generate
+from tests import fixtures as fx
+
+pytestmark = pytest.mark.gpu
+
+
+def _ctx_with(a):
+    c = hp.Context(0)
+    c.set_matrix(a)
+    return c
+
+
+def _sys_matrix(s):
+    return hp.SparseMatrix(s.n, s.row_ptr, s.col, s.val)
+
+
+# ---------------------------------------------------------------- SpMV (K1)
+def _spmv_bound(a, x):
+    """per-row |dy_i| <= 2 nnz_i 2^-53 sum_j |a_ij x_j| (FP reassociation/FMA)."""
+    rs, ci, v = a.row_starts, a.col_indices, a.values
+    absrow = np.zeros(a.n)
+    np.add.at(absrow, np.repeat(np.arange(a.n), np.diff(rs)), np.abs(v * x[ci]))
+    return 2.0 * np.maximum(np.diff(rs), 1) * 2.0 ** -53 * absrow
+
+
+@pytest.mark.parametrize("config", [0, 1, 4, 2])
+def test_spmv_matches_reference(ref, config):
+    s = generate(config)
+    a = _sys_matrix(s)
+    c = _ctx_with(a)
+    x = np.random.default_rng(config).uniform(-1, 1, s.n)
+    y = c.spmv(x)
+    yr = ref.spmv(s.row_ptr, s.col, s.val, x)
+    assert np.linalg.norm(y - yr) <= 1e-14 * np.linalg.norm(yr)
+    assert np.all(np.abs(y - yr) <= _spmv_bound(a, x) + 1e-300)
+
+
+def test_spmv_known_answers():
+    # test_sparse_core.cpp:153-169
+    c = _ctx_with(fx.identity_csr(4))
+    assert np.array_equal(c.spmv([1, 2, 3, 4]), [1, 2, 3, 4])
+    c = _ctx_with(hp.SparseMatrix.from_triplets([0, 1, 1], [0, 0, 1], [2.0, 1.0, 3.0], 2))
+    assert np.array_equal(c.spmv([1.0, 1.0]), [2.0, 4.0])
+
+
+def test_spmv_deterministic():
+    a = fx.laplacian_2d(64, 80)  # test_sparse_core.cpp:204-215
+    c = _ctx_with(a)
+    x = fx.random_vector(a.n, 9)
+    y1, y2 = c.spmv(x), c.spmv(x)
+    assert np.array_equal(y1, y2)
+    assert np.allclose(y1, fx.to_dense(a) @ x, rtol=0, atol=1e-13)
+
+
+# ------------------------------------------------- block LU (K2 + K3)
+def _factor_parity(ref, s_sys, asg, blocks=None):
+    a = _sys_matrix(s_sys)
+    s = int(asg.max()) + 1
+    part = hp.partition_from_assignment(asg, s)
+    p = hp.Preconditioner.block_jacobi(a, part)
+    dims, f32, _, piv_ref, pert_ref = ref.factors(s_sys.row_ptr, s_sys.col, s_sys.val, s, asg)
+    offs = np.concatenate([[0], np.cumsum(dims * dims)])
+    worst = 0.0
+    mism = 0
+    sel = range(s) if blocks is None else blocks
+    for b in sel:
+        d = int(dims[b])
+        F, piv = p.block_factors(b)
+        Fr = f32[offs[b]:offs[b + 1]].reshape(d, d).astype(np.float64)
+        o = int(part.block_starts[b])
+        if not np.array_equal(piv, piv_ref[o:o + d]):
+            mism += 1
+            continue
+        err = np.linalg.norm(F.astype(np.float64) - Fr) / np.linalg.norm(Fr)
+        worst = max(worst, err)
+    st = p.stats()
+    assert [x["perturbation_count"] for x in st] == list(pert_ref)
+    return worst, mism
+
+
+@pytest.mark.parametrize("config", [0, 1, 4])
+def test_block_factors_match_reference(ref, config):
+    s = generate(config)
+    asg, _, _, _ = ref.partition(s.row_ptr, s.col, s.val, s.num_blocks)
+    worst, mism = _factor_parity(ref, s, asg)
+    assert mism == 0, f"{mism} blocks with a different pivot sequence"
+    assert worst <= 1e-5, worst
+
+
+def test_block_factors_config2_sample(ref):
+    s = generate(2)
+    part = hp.partition_graph(_sys_matrix(s), s.num_blocks, 0.1)
+    worst, mism = _factor_parity(ref, s, part.assignment, blocks=list(range(0, 60)) + list(range(4000, 4100)))
+    assert mism == 0 and worst <= 1e-5
+
+
+def test_lu_known_answers(ref):
+    # test_lu_kernels.cpp:78-93 tridiagonal, 120-141 pivoting/ties, 95-102 tiny pivot
+    a = fx.tridiag(3, -1.0, 2.0, -1.0)
+    p = hp.Preconditioner.block_jacobi(a, hp.partition_from_assignment([0, 0, 0], 1))
+    F, piv = p.block_factors(0)
+    assert list(piv) == [0, 1, 2]
+    assert F[0, 0] == 2.0 and F[1, 1] == np.float32(1.5) and F[2, 2] == np.float32(4.0 / 3.0)
+    assert F[1, 0] == np.float32(-0.5) and F[2, 1] == np.float32(-2.0 / 3.0)
+
+    a = hp.SparseMatrix.from_triplets([0, 0, 1, 1], [0, 1, 0, 1], [1.0, 1.0, -3.0, 1.0], 2)
+    p = hp.Preconditioner.block_jacobi(a, hp.partition_from_assignment([0, 0], 1), hp.BlockJacobiOptions(0.0))
+    assert list(p.block_factors(0)[1]) == [1, 0]
+
+    a = hp.SparseMatrix.from_triplets([0, 1, 0, 1], [0, 0, 1, 1], [2.0, -2.0, 1.0, 5.0], 2)
+    p = hp.Preconditioner.block_jacobi(a, hp.partition_from_assignment([0, 0], 1))
+    assert list(p.block_factors(0)[1]) == [0, 1]
+
+    a = fx.diag_csr([1e-20, 1.0])
+    p = hp.Preconditioner.block_jacobi(a, hp.partition_from_assignment([0, 0], 1))
+    assert p.stats()[0]["perturbation_count"] == 1
+    F, _ = p.block_factors(0)
+    assert F[0, 0] == np.float32(1e-10)
+
+
+def test_singular_block_only_with_zero_eps():
+    # test_preconditioners.cpp:196-211, test_lu_kernels.cpp:104-118
+    a = hp.SparseMatrix.from_triplets([0, 0, 1, 1, 2, 3], [0, 1, 0, 1, 2, 3], [1.0, 1.0, 1.0, 1.0, 3.0, 4.0], 4)
+    part = hp.partition_from_assignment([0, 0, 1, 1], 2)
+    with pytest.raises(hp.SingularBlockError) as ei:
+        hp.Preconditioner.block_jacobi(a, part, hp.BlockJacobiOptions(eps_pivot=0.0))
+    assert ei.value.column() == 1
+    p = hp.Preconditioner.block_jacobi(a, part)
+    st = p.stats()
+    assert st[0]["perturbation_count"] == 1 and st[1]["perturbation_count"] == 0
+
+    a = hp.SparseMatrix.from_triplets([0, 1], [0, 0], [1.0, 2.0], 2)  # column 1 structurally empty
+    with pytest.raises(hp.SingularBlockError) as ei:
+        hp.Preconditioner.block_jacobi(a, hp.partition_from_assignment([0, 0], 1), hp.BlockJacobiOptions(0.0))
+    assert ei.value.column() == 1 and "column 1" in str(ei.value)
+
+
+# ------------------------------------------------------------ apply (K4)
+def test_apply_known_answers():
+    # test_preconditioners.cpp:83-91, 99-115
+    d = [2.0, 5.0, 0.25, -4.0]
+    p = hp.Preconditioner.block_jacobi(fx.diag_csr(d), hp.partition_from_assignment([0, 0, 1, 1], 2))
+    z = p.apply([1.0, 2.0, 3.0, 4.0])
+    assert np.array_equal(z, np.float32(np.array([1.0, 2.0, 3.0, 4.0]) / np.array(d)).astype(np.float64))
+    a = hp.SparseMatrix.from_triplets([0, 0, 1], [0, 1, 1], [2.0, 1.0, 4.0], 2)
+    p = hp.Preconditioner.block_jacobi(a, hp.partition_from_assignment([0, 0], 1))
+    assert np.array_equal(p.apply([5.0, 8.0]), [1.5, 2.0])
+
+
+def test_apply_single_block_is_full_inverse():
+    a = fx.random_well_conditioned(12, 3)  # test_preconditioners.cpp:54-63 (FP32 tolerance)
+    p = hp.Preconditioner.block_jacobi(a, hp.partition_from_assignment([0] * 12, 1))
+    b = fx.random_vector(12, 8)
+    z = p.apply(b)
+    e = np.linalg.solve(fx.to_dense(a), b)
+    assert np.linalg.norm(z - e) <= 1e-6 * np.linalg.norm(e)
+
+
+def test_apply_hybrid_close_to_double():
+    # test_preconditioners.cpp:176-194: FP32 apply within 1e-5 of FP64
+    a = fx.laplacian_2d(10, 10)
+    part = hp.partition_graph(a, 4, 0.1)
+    p = hp.Preconditioner.block_jacobi(a, part)
+    v = fx.random_vector(a.n, 31)
+    zf = p.apply(v)
+    M = np.zeros((a.n, a.n))
+    D = fx.to_dense(a)
+    for b in range(4):
+        idx = np.where(part.assignment == b)[0]
+        M[np.ix_(idx, idx)] = D[np.ix_(idx, idx)]
+    zd = np.linalg.solve(M, v)
+    assert np.linalg.norm(zd - zf) / np.linalg.norm(zd) <= 1e-5
+
+
+@pytest.mark.parametrize("config", [0, 1, 3])
+def test_apply_matches_reference(ref, config):
+    s = generate(config)
+    a = _sys_matrix(s)
+    if config == 3:
+        part = hp.partition_graph(a, s.num_blocks, 0.1)
+        asg = part.assignment
+    else:
+        asg, _, _, _ = ref.partition(s.row_ptr, s.col, s.val, s.num_blocks)
+        part = hp.partition_from_assignment(asg, s.num_blocks)
+    p = hp.Preconditioner.block_jacobi(a, part)
+    v = np.random.default_rng(7).uniform(-1, 1, s.n)
+    z = p.apply(v)
+    zr = ref.apply(s.row_ptr, s.col, s.val, s.num_blocks, asg, v, fp32=True)
+    zd = ref.apply(s.row_ptr, s.col, s.val, s.num_blocks, asg, v, fp32=False)
+    assert np.linalg.norm(z - zr) <= 2e-6 * np.linalg.norm(zr)
+    assert np.linalg.norm(z - zd) <= 1e-5 * np.linalg.norm(zd)
+
+
+def test_apply_deterministic():
+    a = fx.laplacian_2d(16, 16)
+    p = hp.Preconditioner.block_jacobi(a, hp.partition_graph(a, 8, 0.1))
+    v = fx.random_vector(a.n, 12)
+    assert np.array_equal(p.apply(v), p.apply(v))
+
+
+def test_dimension_mismatch_raises():
+    p = hp.Preconditioner.block_jacobi(fx.diag_csr([2.0, 4.0, 1.0]), hp.partition_from_assignment([0, 1, 2], 3))
+    with pytest.raises(ValueError):
+        p.apply([1.0, 2.0])

@@ -1,0 +1,210 @@
+"""GPU parity of the full setup + restarted GMRES solve against the
+reference (Hybrid mode) — north-star bars:
+  * final FP64 true residual <= tol
+  * iteration count within 5% of the reference's
+  * ||x - x_ref|| / ||x_ref|| <= 1e-6
+plus the reference's Krylov known-answer tests (test_krylov.cpp)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_2509_09139_b200 as hp
+from paper_2509_09139_b200.workloads import generate
+from tests import fixtures as fx
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def _golden(c):
+    with open(os.path.join(GOLD, f"config{c}.json")) as f:
+        return json.load(f)
+
+
+def _solve(s, part=None):
+    a = hp.SparseMatrix(s.n, s.row_ptr, s.col, s.val)
+    part = part or hp.partition_graph(a, s.num_blocks, 0.1)
+    p = hp.Preconditioner.block_jacobi(a, part)
+    cfg = hp.GmresConfig(restart_m=s.restart_m, tol=s.tol, max_restarts=s.max_restarts)
+    return hp.hybrid_restart_gmres(a, p, s.b, cfg), part
+
+
+def _check_parity(s, res, its_ref, x_ref=None, x_sample=None):
+    r = res.report
+    assert r.converged
+    assert r.final_residual <= s.tol
+    # independent FP64 residual on the host
+    a = hp.SparseMatrix(s.n, s.row_ptr, s.col, s.val)
+    rows = np.repeat(np.arange(s.n), np.diff(s.row_ptr))
+    ax = np.zeros(s.n)
+    np.add.at(ax, rows, s.val * res.x[s.col])
+    assert np.linalg.norm(s.b - ax) / np.linalg.norm(s.b) <= s.tol * 1.0001
+    assert abs(r.total_iterations - its_ref) <= max(1, 0.05 * its_ref), (r.total_iterations, its_ref)
+    assert len(r.residual_history) == r.total_iterations + 1
+    if x_ref is not None:
+        assert np.linalg.norm(res.x - x_ref) / np.linalg.norm(x_ref) <= 1e-6
+    if x_sample is not None:
+        idx, vals = x_sample
+        assert np.linalg.norm(res.x[idx] - vals) / np.linalg.norm(vals) <= 1e-6
+
+
+@pytest.mark.parametrize("config", [0, 1])
+def test_config_solve_matches_reference(ref, config):
+    s = generate(config)
+    g = _golden(config)
+    assert s.digest() == g["input_sha256"]
+    res, part = _solve(s)
+    import hashlib
+    assert hashlib.sha256(part.assignment.tobytes()).hexdigest() == g["partition"]["assignment_sha256"]
+    out = ref.solve(s.row_ptr, s.col, s.val, s.num_blocks, s.b, s.restart_m, s.tol, s.max_restarts,
+                    hybrid=True, assignment=part.assignment)
+    assert out.total_iterations == g["hybrid"]["total_iterations"]
+    _check_parity(s, res, out.total_iterations, x_ref=out.x)
+
+
+def test_config4_newton_sequence(ref):
+    """Partition of A_0 reused; numeric refactorisation per step (first 8 steps)."""
+    g = _golden(4)
+    s0 = generate(4, 0)
+    a0 = hp.SparseMatrix(s0.n, s0.row_ptr, s0.col, s0.val)
+    part = hp.partition_graph(a0, s0.num_blocks, 0.1)
+    p = hp.Preconditioner.block_jacobi(a0, part)
+    cfg = hp.GmresConfig(restart_m=s0.restart_m, tol=s0.tol, max_restarts=s0.max_restarts)
+    for k in range(8):
+        sk = generate(4, k)
+        assert sk.digest() == g["steps"][k]["input_sha256"]
+        if k > 0:
+            p.ctx.update_values(sk.val)
+            p.ctx.bj_refactor()
+            a0.values = sk.val
+        res = hp.hybrid_restart_gmres(a0, p, sk.b, cfg)
+        out = ref.solve(sk.row_ptr, sk.col, sk.val, sk.num_blocks, sk.b, sk.restart_m, sk.tol, sk.max_restarts,
+                        hybrid=True, assignment=part.assignment)
+        assert out.total_iterations == g["steps"][k]["total_iterations"]
+        _check_parity(sk, res, out.total_iterations, x_ref=out.x)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("config", [2, 3])
+def test_large_config_solve(ref, config):
+    path = os.path.join(GOLD, f"config{config}.json")
+    if not os.path.exists(path):
+        pytest.skip("golden not generated")
+    g = _golden(config)
+    s = generate(config)
+    assert s.digest() == g["input_sha256"]
+    res, part = _solve(s)
+    import hashlib
+    assert hashlib.sha256(part.assignment.tobytes()).hexdigest() == g["partition"]["assignment_sha256"]
+    _check_parity(s, res, g["hybrid"]["total_iterations"],
+                  x_sample=(np.array(g["hybrid"]["x_sample_idx"]), np.array(g["hybrid"]["x_sample"])))
+
+
+# ------------------------------------------------ Krylov known answers
+def test_manufactured_solution_laplacian():
+    # test_krylov.cpp:308-329
+    a = fx.laplacian_2d(32, 32)
+    b = fx.to_dense(a) @ np.ones(a.n)
+    p = hp.Preconditioner.block_jacobi(a, hp.partition_graph(a, 16, 0.1))
+    r = hp.hybrid_restart_gmres(a, p, b, hp.GmresConfig(restart_m=30, tol=1e-8))
+    assert r.report.converged and r.report.final_residual <= 1e-8
+    assert np.max(np.abs(r.x - 1.0)) <= 1e-6
+    assert len(r.report.residual_history) == r.report.total_iterations + 1
+
+
+def test_short_restarts_decrease_true_residual():
+    # test_krylov.cpp:331-349
+    a = fx.laplacian_2d(32, 32)
+    b = fx.to_dense(a) @ np.ones(a.n)
+    p = hp.Preconditioner.block_jacobi(a, hp.partition_graph(a, 16, 0.1))
+    r = hp.hybrid_restart_gmres(a, p, b, hp.GmresConfig(restart_m=5, tol=1e-8))
+    c = r.report.cycle_residuals
+    assert len(c) >= 3 and c[1] < c[0] and c[2] < c[1]
+
+
+def test_non_convergence_returns_best_iterate():
+    # test_krylov.cpp:351-359 (block-Jacobi with 1x1 blocks instead of identity)
+    a = fx.laplacian_2d(16, 16)
+    b = fx.to_dense(a) @ np.ones(a.n)
+    p = hp.Preconditioner.block_jacobi(a, hp.partition_from_assignment(np.arange(a.n), a.n))
+    r = hp.hybrid_restart_gmres(a, p, b, hp.GmresConfig(restart_m=3, tol=1e-14, max_restarts=2))
+    assert not r.report.converged and r.report.final_residual > 1e-14 and r.report.restarts == 1
+
+
+def test_immediate_convergence_is_zero_iterations():
+    # test_krylov.cpp:296-306
+    a = fx.diag_csr([2.0, 2.0])
+    p = hp.Preconditioner.block_jacobi(a, hp.partition_from_assignment([0, 1], 2))
+    r = hp.hybrid_restart_gmres(a, p, [1.0, 1.0], hp.GmresConfig(restart_m=5, tol=1.0))
+    assert r.report.converged and r.report.total_iterations == 0 and r.report.restarts == 0
+    assert len(r.report.residual_history) == 1 and r.report.residual_history[0].iteration == 0
+
+
+def test_zero_rhs_returns_zero():
+    a = fx.diag_csr([2.0, 3.0])
+    p = hp.Preconditioner.block_jacobi(a, hp.partition_from_assignment([0, 1], 2))
+    r = hp.hybrid_restart_gmres(a, p, [0.0, 0.0], hp.GmresConfig(restart_m=5))
+    assert r.report.converged and np.array_equal(r.x, [0.0, 0.0])
+    h = r.report.residual_history
+    assert len(h) == 1 and h[0].relative_residual == 0.0
+
+
+def test_single_block_converges_in_one_iteration():
+    # test_krylov.cpp:219-230: exact block inverse -> one Arnoldi step
+    a = fx.tridiag4()
+    p = hp.Preconditioner.block_jacobi(a, hp.partition_from_assignment([0, 0, 0, 0], 1))
+    b = np.array([1.0, 0.5, -2.0, 3.0])
+    r = hp.hybrid_restart_gmres(a, p, b, hp.GmresConfig(restart_m=10, tol=1e-12))
+    assert r.report.converged
+    assert np.allclose(r.x, np.linalg.solve(fx.to_dense(a), b), rtol=0, atol=1e-11)
+
+
+def test_givens_estimate_non_increasing_within_cycle():
+    # test_krylov.cpp:280-294
+    a = fx.random_dd(60, 4, 8)
+    b = fx.random_vector(60, 9)
+    p = hp.Preconditioner.block_jacobi(a, hp.partition_graph(a, 6, 0.1))
+    r = hp.hybrid_restart_gmres(a, p, b, hp.GmresConfig(restart_m=30, tol=1e-12, max_restarts=1))
+    last_c, last = -1, 0.0
+    for h in r.report.residual_history:
+        if h.cycle == last_c:
+            assert h.relative_residual <= last * (1 + 1e-12)
+        last_c, last = h.cycle, h.relative_residual
+
+
+@pytest.mark.parametrize("case", ["laplacian", "random_dd", "convdiff"])
+def test_iterations_match_reference_hybrid(ref, case):
+    # test_krylov.cpp:424-457 cases, against the reference Hybrid count
+    a, s = {"laplacian": (fx.laplacian_2d(16, 16), 8), "random_dd": (fx.random_dd(80, 4, 55), 4),
+            "convdiff": (fx.convection_diffusion_2d(10, 10, 2.0, 1.0), 4)}[case]
+    b = fx.to_dense(a) @ np.ones(a.n)
+    part = hp.partition_graph(a, s, 0.1)
+    p = hp.Preconditioner.block_jacobi(a, part)
+    r = hp.hybrid_restart_gmres(a, p, b, hp.GmresConfig(restart_m=50, tol=1e-8))
+    out = ref.solve(a.row_starts, a.col_indices, a.values, s, b, 50, 1e-8, 40, hybrid=True,
+                    assignment=part.assignment)
+    assert r.report.converged and r.report.final_residual <= 1e-8
+    assert abs(r.report.total_iterations - out.total_iterations) <= max(1, 0.05 * out.total_iterations)
+
+
+def test_solve_is_deterministic():
+    a = fx.laplacian_2d(32, 32)
+    b = fx.to_dense(a) @ np.ones(a.n)
+    p = hp.Preconditioner.block_jacobi(a, hp.partition_graph(a, 16, 0.1))
+    cfg = hp.GmresConfig(restart_m=30, tol=1e-10)
+    r1 = hp.hybrid_restart_gmres(a, p, b, cfg)
+    r2 = hp.hybrid_restart_gmres(a, p, b, cfg)
+    assert np.array_equal(r1.x, r2.x)
+    assert [h.relative_residual for h in r1.report.residual_history] == \
+        [h.relative_residual for h in r2.report.residual_history]
+
+
+def test_invalid_config_raises():
+    a = fx.diag_csr([2.0, 3.0])
+    p = hp.Preconditioner.block_jacobi(a, hp.partition_from_assignment([0, 1], 2))
+    with pytest.raises(ValueError):
+        hp.hybrid_restart_gmres(a, p, [1.0, 1.0], hp.GmresConfig(restart_m=0))
+    with pytest.raises(ValueError):
+        hp.hybrid_restart_gmres(a, p, [1.0], hp.GmresConfig())
