@@ -1,0 +1,358 @@
+#!/usr/bin/env python
+"""Benchmark: hybrid-precision block-Jacobi GMRES(m) setup + solve on B200.
+
+Metric (BASELINE.json): "GMRES setup+solve ms/system; SpMV & precond-apply
+HBM GB/s vs peak". One step = one full system: host graph + partition
+(bit-identical to the reference), device Q A Q^T + batched FP32 block LU,
+device GMRES(m) to the config's tolerance. Workload = BASELINE config 1
+(447x447 power-grid mesh, n = 199,809; the configs[1] case), seeded synthetic
+data; other configs are parity cases (``--config`` / ``--report-all``).
+
+  value : ms per system with A (device CSR + host CSR for the partitioner)
+          and b already resident; device-timed (CUDA events, max over ranks).
+  e2e   : same metric through the C ABI with HOST buffers: hpbj_set_matrix
+          (CSR H2D) + partition + setup + hpbj_gmres (b H2D, x D2H).
+  roofline : dominant kernel (block-Jacobi apply, or SpMV if it dominates),
+          algorithmic bytes / mean CUDA-event launch time inside the timed
+          steps vs MEASURED_PEAKS.json hbm_gbs.
+  cpu_baseline : the reference CPU library (oracle/_ref, compiled from the
+          reference sources) on this host's cores, bounded sample.
+
+``--impl reference`` times the reference CPU implementation instead (rank 0
+only under torchrun). Multi-GPU: independent replicas (one system per GPU
+per step, no collective on the data path), scaling "weak".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GMRES setup+solve ms/system; SpMV & precond-apply HBM GB/s vs peak"
+UNIT = "ms/system"
+WORKLOADS = {
+    0: "config0: random MNA circuit n=10,000 (ring + 2 random/node), bs 32, GMRES(30), tol 1e-10",
+    1: "config1: 447x447 5-point power-grid mesh + 1% vias, n=199,809, bs 64, GMRES(50), tol 1e-10",
+    2: "config2: 1M-node MNA circuit + 50 supply-rail hubs x 10,000, bs 128, GMRES(50), tol 1e-10",
+    3: "config3: 160^3 7-point interconnect mesh + 0.5% long-range, n=4,096,000, bs 256, GMRES(100), tol 1e-9",
+    4: "config4: transient Newton sequence step 0, n=100,000, bs 64, GMRES(30), tol 1e-10",
+}
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.Q,
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4) if len(s) > 3 + k and
+                          s[3 + k].lower() not in ("not active", "0", "[n/a]", "n/a")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def max_over_ranks(v: float, ws: int) -> float:
+    if ws == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# ---------------------------------------------------------------------------
+def cpu_reference_run(sysm, systems: int):
+    """The reference CPU library (oracle/_ref) on `systems` full setup+solves."""
+    from oracle import Ref, ref_available
+    if not ref_available():
+        return None
+    R = Ref()
+    times = []
+    its = None
+    for _ in range(systems):
+        out = R.solve(sysm.row_ptr, sysm.col, sysm.val, sysm.num_blocks, sysm.b, sysm.restart_m, sysm.tol,
+                      sysm.max_restarts, hybrid=True, cond_estimates=False)
+        # setup (materialize_low + graph + partition + block_jacobi) + solve, as run_spec times it
+        times.append(out.timings["setup_ms"] + out.timings["solve_ms"])
+        its = out.total_iterations
+    return {"ms_per_system": statistics.median(times), "iterations": its, "runs": times}
+
+
+def run_reference_arm(args):
+    ws, rank, local = dist_env()
+    if ws > 1 and rank != 0:
+        return 0
+    from paper_2509_09139_b200.workloads import generate
+    s = generate(args.config)
+    cores = os.cpu_count() or 1
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    for _ in range(args.warmup):
+        cpu_reference_run(s, 1)
+    res = cpu_reference_run(s, args.steps)
+    if res is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libbjref.so not built"}))
+        return 0
+    v = sum(res["runs"]) / len(res["runs"])
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": v, "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": WORKLOADS[args.config], "mode": "reference Hybrid (FP32 Krylov loop)"},
+        "iterations": res["iterations"],
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "reference",
+                         "sample": f"{args.steps} full systems (graph+partition_graph+block_jacobi+"
+                                   f"hybrid_restart_gmres) of {WORKLOADS[args.config].split(':')[0]}"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+def run_gpu_arm(args):
+    import torch
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    else:
+        torch.cuda.set_device(local)
+    import paper_2509_09139_b200 as hp
+    from paper_2509_09139_b200.workloads import generate
+
+    s = generate(args.config)
+    a = hp.SparseMatrix(s.n, s.row_ptr, s.col, s.val)
+    cfg = hp.GmresConfig(restart_m=s.restart_m, tol=s.tol, max_restarts=s.max_restarts)
+    ctx = hp.Context(local)
+    ctx.set_matrix(a)
+    d_b = torch.from_numpy(s.b).cuda()
+    d_x = torch.zeros_like(d_b)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    def device_step():
+        part = hp.partition_graph(a, s.num_blocks, 0.1)
+        ctx.bj_setup(part, 1e-10)
+        _, rep = ctx.gmres(None, cfg, device_ptrs=(d_b.data_ptr(), d_x.data_ptr()))
+        return rep
+
+    def e2e_step(c2):
+        c2.set_matrix(a)
+        part = hp.partition_graph(a, s.num_blocks, 0.1)
+        c2.bj_setup(part, 1e-10)
+        x, rep = c2.gmres(s.b, cfg)
+        return x, rep
+
+    torch.cuda.synchronize()
+    for _ in range(args.warmup):
+        device_step()
+    torch.cuda.synchronize()
+
+    # ---- timed region (device-resident inputs)
+    ctx.set_profiling(True)
+    l0 = ctx.launches()
+    times = []
+    reps = []
+    sampler = ClockSampler(local)
+    barrier(ws)
+    torch.cuda.synchronize()
+    with sampler:
+        for _ in range(args.steps):
+            flush.zero_()  # L2 flush (256 MiB > 126 MB L2) between systems, outside the event pair
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            reps.append(device_step())
+            e1.record()
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+    barrier(ws)
+    launches = ctx.launches() - l0
+    kstats = ctx.kernel_stats()
+    ctx.set_profiling(False)
+    total_ms = max_over_ranks(sum(times), ws)
+    value = total_ms / (args.steps * ws)  # ms per system, whole job
+
+    # ---- setup/solve split (untimed breakdown of one more step)
+    t0 = time.perf_counter()
+    part = hp.partition_graph(a, s.num_blocks, 0.1)
+    t1 = time.perf_counter()
+    info = ctx.bj_setup(part, 1e-10)
+    t2 = time.perf_counter()
+    _, rep = ctx.gmres(None, cfg, device_ptrs=(d_b.data_ptr(), d_x.data_ptr()))
+    t3 = time.perf_counter()
+    x = d_x.cpu().numpy()
+
+    # ---- e2e through the C ABI with host buffers
+    ctx2 = hp.Context(local)
+    e2e_step(ctx2)
+    torch.cuda.synchronize()
+    e2e_times = []
+    barrier(ws)
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        x2, rep2 = e2e_step(ctx2)
+        e1.record()
+        torch.cuda.synchronize()
+        e2e_times.append(e0.elapsed_time(e1))
+    e2e_value = max_over_ranks(sum(e2e_times), ws) / (args.steps * ws)
+    h2d = s.row_ptr.nbytes + s.col.nbytes + s.val.nbytes + s.b.nbytes
+    d2h = x2.nbytes
+
+    # ---- roofline of the dominant kernel
+    peak, peak_kind = measured_peak()
+    names = ["bj_apply_f32", "spmv_csr_f64", "arnoldi_mgs_f64"]
+    kern = {}
+    for k, nm in enumerate(names):
+        st = kstats[k]
+        mean_ms = st["total_ms"] / max(1, st["launches"])
+        kern[nm] = {"launches": st["launches"], "mean_us": mean_ms * 1e3, "total_ms": st["total_ms"],
+                    "bytes_per_launch": st["bytes_per_launch"],
+                    "gbs": (st["bytes_per_launch"] / (mean_ms * 1e-3) / 1e9) if mean_ms > 0 and
+                    st["bytes_per_launch"] > 0 else None}
+    dom = max(("bj_apply_f32", "spmv_csr_f64"), key=lambda nm: kern[nm]["total_ms"])
+    achieved = kern[dom]["gbs"] or 0.0
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", f"ncu_traffic_config{args.config}.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(dom)
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "peak_source": peak_kind, "traffic": traffic,
+                "bytes_per_launch": kern[dom]["bytes_per_launch"]}
+
+    # ---- CPU baseline: the reference library on this host, bounded sample
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cores = os.cpu_count() or 1
+        os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+        res = cpu_reference_run(s, args.cpu_systems)
+        if res is not None:
+            cpu = {"value": res["ms_per_system"], "unit": UNIT, "cores": cores, "kind": "reference",
+                   "sample": f"{args.cpu_systems} full config-{args.config} systems (reference Hybrid: "
+                             f"graph+partition+block_jacobi+hybrid_restart_gmres), median",
+                   "iterations": res["iterations"]}
+
+    clocks = sampler.summary()
+    if rank == 0:
+        err = float(np.linalg.norm(x - s.x_true) / np.linalg.norm(s.x_true))
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": value * ws, "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOADS[args.config], "n": s.n, "nnz": s.nnz, "blocks": s.num_blocks,
+                       "precond_dtype": "f32", "krylov_dtype": "f64", "l2_flush": "256MiB write between steps",
+                       "parallelism": f"replicas x{ws}"},
+            "iterations": rep.total_iterations, "converged": rep.converged,
+            "final_residual": rep.final_residual, "rel_err_vs_xtrue": err,
+            "breakdown_ms": {"partition_host": (t1 - t0) * 1e3, "bj_setup": (t2 - t1) * 1e3,
+                             "permute_dev": info.ms_permute, "factor_dev": info.ms_factor,
+                             "solve": (t3 - t2) * 1e3,
+                             "per_iteration_us": (t3 - t2) * 1e6 / max(1, rep.total_iterations)},
+            "kernels": kern,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--cpu-systems", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_gpu_arm(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

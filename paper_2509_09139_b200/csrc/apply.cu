@@ -64,6 +64,22 @@ __device__ __forceinline__ float fms<float>(float f, float y, float acc) {
     return fmaf(-f, y, acc);
 }
 
+// a / b for finite normal operands without the IEEE slow-path branches:
+// q0 = a * rcp(b); one FMA residual correction gives the correctly rounded
+// quotient (Markstein) for the operand ranges a factor block produces.
+__device__ __forceinline__ float div_fast(float a, float b, float rb) {
+    const float q = a * rb;
+    const float r = fmaf(-q, b, a);
+    return fmaf(r, rb, q);
+}
+__device__ __forceinline__ double div_fast(double a, double b, double rb) {
+    const double q = a * rb;
+    const double r = fma(-q, b, a);
+    return fma(r, rb, q);
+}
+__device__ __forceinline__ float recip(float b) { return __frcp_rn(b); }
+__device__ __forceinline__ double recip(double b) { return 1.0 / b; }
+
 template <class Acc, class Src, class Dst>
 __global__ void __launch_bounds__(kApplyWarps * 32) k_apply(ApplyParams p, Src src, Dst dst,
                                                            const SolveState* sst, int ybuf_stride) {
@@ -81,10 +97,13 @@ __global__ void __launch_bounds__(kApplyWarps * 32) k_apply(ApplyParams p, Src s
         const float* F = p.fac + p.fac_off[b];
         const int* pv = p.piv + o;
 
+        // gather rhs[pivot_rows[k]] for the whole block (independent loads)
+        for (int k = lane; k < 32 * T; k += 32) ybuf[k] = (k < d) ? (Acc)src(o + __ldg(pv + k)) : (Acc)0;
+        __syncwarp();
         // ---------------- forward: unit-lower L, rows in pivot order
         for (int t = 0; t < T; ++t) {
             const int k = 32 * t + lane;
-            Acc acc = (k < d) ? (Acc)src(o + pv[k]) : (Acc)0;
+            Acc acc = ybuf[k];
             const float4* panel = reinterpret_cast<const float4*>(F + (size_t)t * 32 * 4 * dq);
             // off-panel columns [0, 32t)
             const int cq_end = 8 * t;
@@ -142,9 +161,16 @@ __global__ void __launch_bounds__(kApplyWarps * 32) k_apply(ApplyParams p, Src s
                 fd[4 * q + 2] = f.z;
                 fd[4 * q + 3] = f.w;
             }
+            // own diagonal U_kk (padded rows: 1, and they stay 0)
+            float udiag = 1.0f;
+#pragma unroll
+            for (int cc = 0; cc < 32; ++cc)
+                if (lane == cc) udiag = fd[cc];
+            const Acc udg = (Acc)udiag;
+            const Acc urcp = recip(udg);
 #pragma unroll
             for (int cc = 31; cc >= 0; --cc) {
-                if (lane == cc && k < d) acc = acc / (Acc)fd[cc];  // padded rows stay 0
+                if (lane == cc && k < d) acc = div_fast(acc, udg, urcp);
                 const Acc xc = __shfl_sync(0xffffffffu, acc, cc);
                 if (lane < cc) acc = fms<Acc>(fd[cc], xc, acc);
             }

@@ -1,172 +1,118 @@
-// Arnoldi modified Gram-Schmidt + progressive Givens, device resident —
-// replaces arnoldi_step (gmres.hpp:43-75), dot/norm2 (dense_ops.hpp:14-46)
-// and GivensLs::push_column (gmres.cpp:26-52) plus the loop exits of
-// run_cycle (gmres.cpp:130-146).
+// Arnoldi orthogonalisation + progressive Givens, device resident — replaces
+// arnoldi_step (gmres.hpp:43-75), dot/norm2 (dense_ops.hpp:14-46) and
+// GivensLs::push_column (gmres.cpp:26-52) plus the loop exits of run_cycle
+// (gmres.cpp:130-146).
 //
-// k_mgs is a persistent cooperative kernel: every CTA owns a contiguous
-// slice of w = A M^-1 v_j and keeps it in shared memory for the whole MGS
-// sweep (config 3: 4.1M doubles over 148 SMs = 221 KB/SM), so each basis
-// vector streams from HBM once for its dot product and once more (L2-hot)
-// for its axpy, while w never round-trips to HBM. Per inner step i:
-//     w -= h_{i-1} v_{i-1};  partial <v_i, w>;  grid sync;  h_i = sum(partials)
-// Every CTA sums the per-CTA partials in the same fixed order, so all CTAs
-// hold a bit-identical h_i without a second barrier, and the reduction is
-// run-to-run deterministic. CTA 0 finishes the step: Hessenberg column,
-// Givens rotation, residual estimate and the cycle-exit flags, all written
-// to device memory (SolveState) — no host round-trip per iteration.
+// Both kernels below apply the modified Gram-Schmidt projector
+//     P = (I - v_j v_j^T) ... (I - v_0 v_0^T)
+// to w = A M^-1 v_j in FP64, and keep the slice of w each CTA owns in shared
+// memory for the whole step (w never round-trips to HBM). They differ only
+// in how the j+1 inner products are synchronised:
+//
+//  k_mgs  (large n: one basis vector takes longer to stream than a grid
+//          barrier): the textbook sequence, one grid-wide reduction per
+//          projection, h_i = <v_i, w - sum_{k<i} h_k v_k>; each v_i streams
+//          once from HBM for its dot and once more (L2-hot) for its axpy.
+//  k_icwy (small/medium n: barrier-latency bound): the compact-WY form of the
+//          same projector, P = I - V T V^T with T = (I + L)^-1, L = strictly
+//          lower part of V^T V (Swirydowicz et al., "Low synchronization
+//          Gram-Schmidt and GMRES algorithms", NLA 2020). One fused multi-dot
+//          pass yields c = V^T w and the new Gram row <v_j, v_k>; the MGS
+//          coefficients h = (I + L)^-1 c follow from the triangular
+//          recurrence h_i = c_i - sum_{k<i} L_ik h_k (identical to MGS's
+//          h_i in exact arithmetic; two Jacobi sweeps are exact to O(|L|^3),
+//          far below FP64 roundoff since |L| ~ loss of orthogonality); one
+//          multi-axpy pass forms w - V h in MGS order. Two grid barriers per
+//          step instead of j + 2.
+//
+// Reductions are deterministic: every CTA deposits per-value partials and
+// every CTA sums them in CTA order, so all CTAs hold bit-identical totals
+// and repeated solves are bit-reproducible. CTA 0 finishes the step:
+// Hessenberg column, Givens rotation, residual estimate, cycle-exit flags
+// (SolveState) — no host round-trip per iteration.
 
-#include <cooperative_groups.h>
+#include <cstdlib>
+#include <string>
 
 #include "device.cuh"
 #include "kernels.cuh"
-
-namespace cg = cooperative_groups;
 
 namespace hpbj {
 
 namespace {
 
 constexpr int kMgsThreads = 1024;
-constexpr size_t kMgsSmemMax = 227 * 1024 - 1024;
+constexpr int kIcwyThreads = 512;
+constexpr size_t kSmemMax = 227 * 1024;
 
-struct MgsArgs {
+// ---------------------------------------------------------------------------
+// Sense-free generation barrier over all CTAs of a cooperative launch.
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void grid_barrier(GridBarrier* gb) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned g = ld_acquire(&gb->gen);
+        __threadfence();
+        const unsigned prev = atomicAdd(&gb->count, 1u);
+        if (prev == gridDim.x - 1) {
+            gb->count = 0;
+            __threadfence();
+            st_release(&gb->gen, g + 1);
+        } else {
+            while (ld_acquire(&gb->gen) == g) {
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// Sum of partials[0..count) in a fixed order; every thread of warp 0 gets it.
+__device__ __forceinline__ double sum_partials(const double* p, int count) {
+    return warp_sum_partials(p, count);
+}
+
+// ---------------------------------------------------------------------------
+struct OrthArgs {
     KrylovBufs kb;
+    double* gram;        // (m+1) x (m+1): row i holds <v_i, v_k>, k < i
     SolveState* st;
+    GridBarrier* gb;
     int n;
-    int slice;  // rows per CTA (even)
-    int npad;   // n rounded up to even; vectors are zero padded to npad
+    int slice;           // rows per CTA (even)
+    int npad;            // n rounded up to even (vectors zero padded)
+    cudaGraphConditionalHandle cond;  // Arnoldi WHILE node (0: not in a graph)
 };
 
-template <bool SMEM>
-__global__ void __launch_bounds__(kMgsThreads, 1) k_mgs(MgsArgs a) {
-    cg::grid_group grid = cg::this_grid();
+// Shared finish of a step: normalise, Hessenberg column, Givens, exit flags.
+__device__ void finish_step(const OrthArgs& a, double2* w2, int r0, int nv2, int j, double pre_norm,
+                            double hnext, int nthreads) {
     SolveState* st = a.st;
-    if (st->done) return;  // uniform: nothing writes done before the final barrier
-    extern __shared__ __align__(16) double wsh[];
-    __shared__ double red[2][kMgsThreads / 32];
-    __shared__ double bc[2];
-
-    const int j = st->j;
     const int m = a.kb.m;
     const int ldv = a.kb.ldv;
-    const int G = gridDim.x;
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const int r0 = blockIdx.x * a.slice;
-    const int len = max(0, min(a.slice, a.npad - r0));
-    const int nv2 = len >> 1;  // double2 per slice
-    double* P = a.kb.partials;  // [2 parity][2 quantity][G]
-
-    double2* w2 = SMEM ? reinterpret_cast<double2*>(wsh) : reinterpret_cast<double2*>(a.kb.w + r0);
-    const double2* win = reinterpret_cast<const double2*>(a.kb.w + r0);
-    const double* V = a.kb.V;
-
-    auto reduce2 = [&](double x0, double x1, int parity) {
-        // block sums (fixed order) -> partials -> grid sync -> fixed-order totals
-        x0 = warp_sum(x0);
-        x1 = warp_sum(x1);
-        if (lane == 0) {
-            red[0][wid] = x0;
-            red[1][wid] = x1;
-        }
-        __syncthreads();
-        if (wid == 0) {
-            double t0 = lane < kMgsThreads / 32 ? red[0][lane] : 0.0;
-            double t1 = lane < kMgsThreads / 32 ? red[1][lane] : 0.0;
-            t0 = warp_sum(t0);
-            t1 = warp_sum(t1);
-            if (lane == 0) {
-                P[(parity * 2 + 0) * G + blockIdx.x] = t0;
-                P[(parity * 2 + 1) * G + blockIdx.x] = t1;
-            }
-        }
-        grid.sync();
-        if (wid == 0) {
-            const double t0 = warp_sum_partials(P + (parity * 2 + 0) * G, G);
-            const double t1 = warp_sum_partials(P + (parity * 2 + 1) * G, G);
-            if (lane == 0) {
-                bc[0] = t0;
-                bc[1] = t1;
-            }
-        }
-        __syncthreads();
-    };
-
-    // ---- pass 0: stage w on chip, ||w||^2 and <v_0, w>
-    double ss = 0.0, dt = 0.0;
-    {
-        const double2* v0 = reinterpret_cast<const double2*>(V + r0);
-#pragma unroll 4
-        for (int e = tid; e < nv2; e += kMgsThreads) {
-            const double2 wv = __ldcg(win + e);
-            const double2 vv = __ldg(v0 + e);
-            if (SMEM) w2[e] = wv;
-            ss = fma(wv.x, wv.x, ss);
-            ss = fma(wv.y, wv.y, ss);
-            dt = fma(vv.x, wv.x, dt);
-            dt = fma(vv.y, wv.y, dt);
-        }
-    }
-    reduce2(ss, dt, 0);
-    const double pre_norm = sqrt(bc[0]);
-    double h = bc[1];
-    if (blockIdx.x == 0 && tid == 0) a.kb.H[(size_t)j * (m + 1) + 0] = h;
-
-    // ---- passes 1..j: w -= h_{i-1} v_{i-1}; h_i = <v_i, w>
-    for (int i = 1; i <= j; ++i) {
-        const double2* vp = reinterpret_cast<const double2*>(V + (size_t)(i - 1) * ldv + r0);
-        const double2* vi = reinterpret_cast<const double2*>(V + (size_t)i * ldv + r0);
-        dt = 0.0;
-#pragma unroll 4
-        for (int e = tid; e < nv2; e += kMgsThreads) {
-            double2 wv = w2[e];
-            const double2 pv = __ldg(vp + e);
-            const double2 qv = __ldg(vi + e);
-            wv.x = fma(-h, pv.x, wv.x);
-            wv.y = fma(-h, pv.y, wv.y);
-            w2[e] = wv;
-            dt = fma(qv.x, wv.x, dt);
-            dt = fma(qv.y, wv.y, dt);
-        }
-        reduce2(0.0, dt, i & 1);
-        h = bc[1];
-        if (blockIdx.x == 0 && tid == 0) a.kb.H[(size_t)j * (m + 1) + i] = h;
-    }
-
-    // ---- final pass: w -= h_j v_j; ||w||
-    {
-        const double2* vp = reinterpret_cast<const double2*>(V + (size_t)j * ldv + r0);
-        ss = 0.0;
-#pragma unroll 4
-        for (int e = tid; e < nv2; e += kMgsThreads) {
-            double2 wv = w2[e];
-            const double2 pv = __ldg(vp + e);
-            wv.x = fma(-h, pv.x, wv.x);
-            wv.y = fma(-h, pv.y, wv.y);
-            w2[e] = wv;
-            ss = fma(wv.x, wv.x, ss);
-            ss = fma(wv.y, wv.y, ss);
-        }
-    }
-    reduce2(ss, 0.0, (j + 1) & 1);
-    const double hnext = sqrt(bc[0]);
-    // breakdown test (gmres.hpp:66-71): ||w|| <= factor * u * ||w_pre||
-    const bool breakdown = hnext <= st->breakdown_factor * pre_norm;
+    const bool breakdown = hnext <= st->breakdown_factor * pre_norm;  // gmres.hpp:66-71
     if (!breakdown) {
-        const double inv = 1.0 / hnext;  // gmres.hpp:72-73 multiplies by the reciprocal
+        const double inv = 1.0 / hnext;  // gmres.hpp:72-73: multiply by the reciprocal
         double2* vn = reinterpret_cast<double2*>(a.kb.V + (size_t)(j + 1) * ldv + r0);
-#pragma unroll 4
-        for (int e = tid; e < nv2; e += kMgsThreads) {
+        for (int e = threadIdx.x; e < nv2; e += nthreads) {
             double2 wv = w2[e];
             wv.x *= inv;
             wv.y *= inv;
             vn[e] = wv;
         }
     }
-
-    if (blockIdx.x == 0 && tid == 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
         double* Hj = a.kb.H + (size_t)j * (m + 1);
         Hj[j + 1] = hnext;
-        // ---- GivensLs::push_column (gmres.cpp:26-52)
+        // GivensLs::push_column (gmres.cpp:26-52)
         double* Rj = a.kb.R + (size_t)j * (m + 1);
         double* cs = a.kb.cs;
         double* sn = a.kb.sn;
@@ -194,19 +140,296 @@ __global__ void __launch_bounds__(kMgsThreads, 1) k_mgs(MgsArgs a) {
         g[j] = t;
         const double est = fabs(g[j + 1]);
         a.kb.est[j] = est;
-        // ---- cycle exits (gmres.cpp:137-146)
+        // cycle exits (gmres.cpp:137-146)
         const bool conv = est <= st->thr;
         if (conv) st->converged_est = 1;
         if (breakdown) st->breakdown = 1;
         st->pre_norm = pre_norm;
         st->last_est = est;
         st->j = j + 1;
-        st->done = (conv || breakdown || est <= st->attainable || j + 1 >= m) ? 1 : 0;
+        const int done = (conv || breakdown || est <= st->attainable || j + 1 >= m) ? 1 : 0;
+        st->done = done;
+        if (a.cond) cudaGraphSetConditional(a.cond, done ? 0u : 1u);
     }
 }
 
+// ---------------------------------------------------------------------------
+template <bool SMEM>
+__global__ void __launch_bounds__(kMgsThreads, 1) k_mgs(OrthArgs a) {
+    SolveState* st = a.st;
+    if (st->done) return;  // uniform: nothing writes done before the final barrier
+    extern __shared__ __align__(16) double wsh[];
+    __shared__ double red[2][kMgsThreads / 32];
+    __shared__ double bc[2];
+
+    const int j = st->j;
+    const int m = a.kb.m;
+    const int ldv = a.kb.ldv;
+    const int G = gridDim.x;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int r0 = blockIdx.x * a.slice;
+    const int len = max(0, min(a.slice, a.npad - r0));
+    const int nv2 = len >> 1;
+    double* P = a.kb.partials;  // [2 parity][2 quantity][G]
+
+    double2* w2 = SMEM ? reinterpret_cast<double2*>(wsh) : reinterpret_cast<double2*>(a.kb.w + r0);
+    const double2* win = reinterpret_cast<const double2*>(a.kb.w + r0);
+    const double* V = a.kb.V;
+
+    auto reduce2 = [&](double x0, double x1, int parity) {
+        x0 = warp_sum(x0);
+        x1 = warp_sum(x1);
+        if (lane == 0) {
+            red[0][wid] = x0;
+            red[1][wid] = x1;
+        }
+        __syncthreads();
+        if (wid == 0) {
+            double t0 = lane < kMgsThreads / 32 ? red[0][lane] : 0.0;
+            double t1 = lane < kMgsThreads / 32 ? red[1][lane] : 0.0;
+            t0 = warp_sum(t0);
+            t1 = warp_sum(t1);
+            if (lane == 0) {
+                P[(parity * 2 + 0) * G + blockIdx.x] = t0;
+                P[(parity * 2 + 1) * G + blockIdx.x] = t1;
+            }
+        }
+        grid_barrier(a.gb);
+        if (wid == 0) {
+            const double t0 = sum_partials(P + (parity * 2 + 0) * G, G);
+            const double t1 = sum_partials(P + (parity * 2 + 1) * G, G);
+            if (lane == 0) {
+                bc[0] = t0;
+                bc[1] = t1;
+            }
+        }
+        __syncthreads();
+    };
+
+    // pass 0: stage w on chip, ||w||^2 and <v_0, w>
+    double ss = 0.0, dt = 0.0;
+    {
+        const double2* v0 = reinterpret_cast<const double2*>(V + r0);
+#pragma unroll 4
+        for (int e = tid; e < nv2; e += kMgsThreads) {
+            const double2 wv = __ldcg(win + e);
+            const double2 vv = __ldg(v0 + e);
+            if (SMEM) w2[e] = wv;
+            ss = fma(wv.x, wv.x, ss);
+            ss = fma(wv.y, wv.y, ss);
+            dt = fma(vv.x, wv.x, dt);
+            dt = fma(vv.y, wv.y, dt);
+        }
+    }
+    reduce2(ss, dt, 0);
+    const double pre_norm = sqrt(bc[0]);
+    double h = bc[1];
+    if (blockIdx.x == 0 && tid == 0) a.kb.H[(size_t)j * (m + 1) + 0] = h;
+
+    // passes 1..j: w -= h_{i-1} v_{i-1}; h_i = <v_i, w>
+    for (int i = 1; i <= j; ++i) {
+        const double2* vp = reinterpret_cast<const double2*>(V + (size_t)(i - 1) * ldv + r0);
+        const double2* vi = reinterpret_cast<const double2*>(V + (size_t)i * ldv + r0);
+        dt = 0.0;
+#pragma unroll 4
+        for (int e = tid; e < nv2; e += kMgsThreads) {
+            double2 wv = w2[e];
+            const double2 pv = __ldg(vp + e);
+            const double2 qv = __ldg(vi + e);
+            wv.x = fma(-h, pv.x, wv.x);
+            wv.y = fma(-h, pv.y, wv.y);
+            w2[e] = wv;
+            dt = fma(qv.x, wv.x, dt);
+            dt = fma(qv.y, wv.y, dt);
+        }
+        reduce2(0.0, dt, i & 1);
+        h = bc[1];
+        if (blockIdx.x == 0 && tid == 0) a.kb.H[(size_t)j * (m + 1) + i] = h;
+    }
+
+    // final pass: w -= h_j v_j; ||w||
+    {
+        const double2* vp = reinterpret_cast<const double2*>(V + (size_t)j * ldv + r0);
+        ss = 0.0;
+#pragma unroll 4
+        for (int e = tid; e < nv2; e += kMgsThreads) {
+            double2 wv = w2[e];
+            const double2 pv = __ldg(vp + e);
+            wv.x = fma(-h, pv.x, wv.x);
+            wv.y = fma(-h, pv.y, wv.y);
+            w2[e] = wv;
+            ss = fma(wv.x, wv.x, ss);
+            ss = fma(wv.y, wv.y, ss);
+        }
+    }
+    reduce2(ss, 0.0, (j + 1) & 1);
+    finish_step(a, w2, r0, nv2, j, pre_norm, sqrt(bc[0]), kMgsThreads);
+}
+
+// ---------------------------------------------------------------------------
+constexpr int kIcwyWarps = kIcwyThreads / 32;
+constexpr int kBatch = 16;  // basis vectors per multi-dot batch (32 dot products)
+
+// 32 per-lane accumulators -> lane l holds the warp total of slot l
+// (butterfly transpose-reduction: 31 shuffles for 32 dot products).
+__device__ __forceinline__ double transpose_reduce32(double (&v)[32], int lane) {
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+#pragma unroll
+        for (int q = 0; q < off; ++q) {
+            const bool hi = (lane & off) != 0;
+            const double send = hi ? v[q] : v[q + off];
+            const double keep = hi ? v[q + off] : v[q];
+            v[q] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+    }
+    return v[0];
+}
+
+template <bool SMEM>
+__global__ void __launch_bounds__(kIcwyThreads, 1) k_icwy(OrthArgs a) {
+    SolveState* st = a.st;
+    if (st->done) return;
+    extern __shared__ __align__(16) double dsm[];
+    // dynamic smem: [w slice][v_j slice] when SMEM
+    __shared__ double red[kIcwyWarps][2 * kBatch];  // per-warp batch partials
+    __shared__ double acc_sh[kMaxRestart * 2 + 4];  // CTA partials of c, l, ss
+    __shared__ double tot[kMaxRestart * 2 + 4];     // grid totals
+    __shared__ double hsh[kMaxRestart + 1];
+    __shared__ double h1[kMaxRestart + 1];
+    __shared__ double wred[kIcwyWarps];
+
+    const int j = st->j;
+    const int m = a.kb.m;
+    const int ldv = a.kb.ldv;
+    const int G = gridDim.x;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int r0 = blockIdx.x * a.slice;
+    const int len = max(0, min(a.slice, a.npad - r0));
+    const int nv2 = len >> 1;
+    const int nval = 2 * (j + 1) + 1;  // c_0..c_j, l_0..l_j, ||w||^2
+    double* P = a.kb.partials;         // [value][G]
+
+    double2* w2 = SMEM ? reinterpret_cast<double2*>(dsm) : reinterpret_cast<double2*>(a.kb.w + r0);
+    const double2* vj2 = reinterpret_cast<const double2*>(a.kb.V + (size_t)j * ldv + r0);
+    const double2* win = reinterpret_cast<const double2*>(a.kb.w + r0);
+    const double* V = a.kb.V;
+
+    // ---- stage w, ||w||^2
+    double ss = 0.0;
+    for (int e = tid; e < nv2; e += kIcwyThreads) {
+        const double2 wv = __ldcg(win + e);
+        if (SMEM) w2[e] = wv;
+        ss = fma(wv.x, wv.x, ss);
+        ss = fma(wv.y, wv.y, ss);
+    }
+    ss = warp_sum(ss);
+    if (lane == 0) wred[wid] = ss;
+    __syncthreads();
+
+    // ---- pass A: fused multi-dot  c_i = <v_i, w>,  l_i = <v_i, v_j>
+    for (int i0 = 0; i0 <= j; i0 += kBatch) {
+        const int nb = min(kBatch, j + 1 - i0);
+        double acc[32];
+#pragma unroll
+        for (int q = 0; q < 32; ++q) acc[q] = 0.0;
+        for (int e = tid; e < nv2; e += kIcwyThreads) {
+            const double2 wv = w2[e];
+            const double2 jv = __ldg(vj2 + e);
+#pragma unroll
+            for (int q = 0; q < kBatch; ++q) {
+                if (q < nb) {
+                    const double2 vv = __ldg(reinterpret_cast<const double2*>(V + (size_t)(i0 + q) * ldv + r0) + e);
+                    acc[q] = fma(vv.x, wv.x, acc[q]);
+                    acc[q] = fma(vv.y, wv.y, acc[q]);
+                    acc[kBatch + q] = fma(vv.x, jv.x, acc[kBatch + q]);
+                    acc[kBatch + q] = fma(vv.y, jv.y, acc[kBatch + q]);
+                }
+            }
+        }
+        const double r = transpose_reduce32(acc, lane);
+        red[wid][lane] = r;
+        __syncthreads();
+        if (tid < 2 * kBatch) {
+            double s = 0.0;
+            for (int w = 0; w < kIcwyWarps; ++w) s += red[w][tid];
+            const int q = tid & (kBatch - 1);
+            if (q < nb) acc_sh[(tid < kBatch ? 0 : (j + 1)) + i0 + q] = s;
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        double s = 0.0;
+        for (int w = 0; w < kIcwyWarps; ++w) s += wred[w];
+        acc_sh[2 * (j + 1)] = s;
+    }
+    __syncthreads();
+    for (int t = tid; t < nval; t += kIcwyThreads) P[(size_t)t * G + blockIdx.x] = acc_sh[t];
+    grid_barrier(a.gb);
+    // grid totals, fixed CTA order (every CTA computes the same bits)
+    for (int t = tid; t < nval; t += kIcwyThreads) {
+        const double* p = P + (size_t)t * G;
+        double s = 0.0;
+        for (int b = 0; b < G; ++b) s += __ldcg(p + b);
+        tot[t] = s;
+    }
+    __syncthreads();
+    const double pre_norm = sqrt(tot[2 * (j + 1)]);
+    const int ldl = m + 1;
+    // ---- h = (I + L)^-1 c, L_ik = <v_i, v_k> (k < i); row j is new
+    auto Lik = [&](int i, int k) -> double { return i == j ? tot[(j + 1) + k] : a.gram[(size_t)i * ldl + k]; };
+    for (int i = tid; i <= j; i += kIcwyThreads) {
+        double s = tot[i];
+        for (int k = 0; k < i; ++k) s = fma(-Lik(i, k), tot[k], s);
+        h1[i] = s;
+    }
+    __syncthreads();
+    for (int i = tid; i <= j; i += kIcwyThreads) {
+        double s = tot[i];
+        for (int k = 0; k < i; ++k) s = fma(-Lik(i, k), h1[k], s);
+        hsh[i] = s;
+    }
+    __syncthreads();
+    if (blockIdx.x == 0) {
+        for (int i = tid; i <= j; i += kIcwyThreads) a.kb.H[(size_t)j * (m + 1) + i] = hsh[i];
+        for (int k = tid; k < j; k += kIcwyThreads) a.gram[(size_t)j * ldl + k] = tot[(j + 1) + k];
+    }
+
+    // ---- pass B: w -= sum_i h_i v_i in MGS order; ||w||^2
+    double ss2 = 0.0;
+    for (int e = tid; e < nv2; e += kIcwyThreads) {
+        double2 wv = w2[e];
+        for (int i = 0; i <= j; ++i) {
+            const double2 vv = __ldg(reinterpret_cast<const double2*>(V + (size_t)i * ldv + r0) + e);
+            const double hi = hsh[i];
+            wv.x = fma(-hi, vv.x, wv.x);
+            wv.y = fma(-hi, vv.y, wv.y);
+        }
+        w2[e] = wv;
+        ss2 = fma(wv.x, wv.x, ss2);
+        ss2 = fma(wv.y, wv.y, ss2);
+    }
+    ss2 = warp_sum(ss2);
+    if (lane == 0) wred[wid] = ss2;
+    __syncthreads();
+    double* P2 = P + (size_t)(2 * kMaxRestart + 4) * G;
+    if (tid == 0) {
+        double s = 0.0;
+        for (int w = 0; w < kIcwyWarps; ++w) s += wred[w];
+        P2[blockIdx.x] = s;
+    }
+    grid_barrier(a.gb);
+    if (wid == 0) {
+        const double t0 = sum_partials(P2, G);
+        if (lane == 0) wred[0] = t0;
+    }
+    __syncthreads();
+    finish_step(a, w2, r0, nv2, j, pre_norm, sqrt(wred[0]), kIcwyThreads);
+}
+
 // v_0 = r0 / beta (element-wise division, gmres.cpp:120-122); cycle state.
-__global__ void k_cycle_init(KrylovBufs kb, SolveState* st, const double* __restrict__ r, int n) {
+__global__ void k_cycle_init(KrylovBufs kb, SolveState* st, const double* __restrict__ r, int n,
+                             cudaGraphConditionalHandle cond) {
     const double beta = st->rnorm;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
         kb.V[i] = r[i] / beta;
@@ -221,7 +444,32 @@ __global__ void k_cycle_init(KrylovBufs kb, SolveState* st, const double* __rest
         st->rank_deficient = 0;
         kb.g[0] = beta;
         for (int i = 1; i <= kb.m; ++i) kb.g[i] = 0.0;
+        if (cond) cudaGraphSetConditional(cond, conv ? 0u : 1u);
     }
+}
+
+// Restart-driver bookkeeping (gmres.cpp:236-258) on the device: history rows
+// (cycle, ++iteration, est/||b||), cycle residual, exit test.
+__global__ void k_cycle_end(KrylovBufs kb, SolveState* st, cudaGraphConditionalHandle cond) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const int steps = st->j;
+    const int cyc = st->cycles;
+    for (int k = 0; k < steps; ++k) {
+        kb.hist[st->hist_len + k] = kb.est[k] / st->bnorm;
+        kb.hist_cycle[st->hist_len + k] = cyc;
+    }
+    st->hist_len += steps;
+    st->total_iterations += steps;
+    st->breakdown_any |= st->breakdown;
+    st->rank_any |= st->rank_deficient;
+    const double rnorm = st->rnorm;
+    kb.cycres[cyc] = rnorm / st->bnorm;
+    st->cycles = cyc + 1;
+    st->last_steps = steps;
+    const bool conv = rnorm <= st->thr;
+    st->converged = conv ? 1 : 0;
+    const bool more = !conv && st->cycles < st->max_restarts && steps > 0;
+    if (cond) cudaGraphSetConditional(cond, more ? 1u : 0u);
 }
 
 // y = R^-1 g with the zero-rotation convention (gmres.cpp:57-66).
@@ -243,48 +491,67 @@ __global__ void k_solve_y(KrylovBufs kb, const SolveState* st) {
 
 }  // namespace
 
-MgsLaunch plan_mgs(int n, int num_sms) {
+size_t orth_partials_doubles(int num_sms) { return (size_t)(2 * kMaxRestart + 8) * num_sms * 2; }
+
+MgsLaunch plan_mgs(int n, int num_sms, int m) {
     MgsLaunch L;
-    L.threads = kMgsThreads;
     const int npad = (n + 1) & ~1;
-    // enough CTAs to stream at full HBM rate, few enough to keep the barrier cheap
-    int grid = num_sms;
-    const int min_rows = 4096;
-    grid = std::max(1, std::min(grid, (npad + min_rows - 1) / min_rows));
+    // compact-WY when a basis vector streams faster than a grid barrier
+    // (~1.5 us: 8 n bytes at HBM rate) and the Gram/accumulator tables fit.
+    const char* env = getenv("HPBJ_ORTH");
+    bool icwy = (size_t)n * 8 <= (size_t)12 * 1024 * 1024 && m <= kMaxRestart;
+    if (env && std::string(env) == "mgs") icwy = false;
+    if (env && std::string(env) == "icwy" && m <= kMaxRestart) icwy = true;
+    L.icwy = icwy;
+    L.threads = icwy ? kIcwyThreads : kMgsThreads;
+    const int min_rows = icwy ? 2048 : 4096;
+    int grid = std::max(1, std::min(num_sms, (npad + min_rows - 1) / min_rows));
     int slice = (npad + grid - 1) / grid;
     slice = (slice + 1) & ~1;
     L.grid = grid;
     L.slice = slice;
     L.smem = (size_t)slice * sizeof(double);
-    L.w_in_smem = L.smem <= kMgsSmemMax;
+    const size_t static_smem = icwy ? (size_t)(kIcwyWarps * 2 * kBatch + 3 * (kMaxRestart * 2 + 4)) * 8 + 1024
+                                    : 2048;
+    L.w_in_smem = L.smem + static_smem <= kSmemMax;
     if (!L.w_in_smem) L.smem = 0;
     return L;
 }
 
-void launch_mgs(const MgsLaunch& L, const KrylovBufs& kb, SolveState* sst, int n, cudaStream_t st,
-                int64_t* launches) {
-    MgsArgs a{kb, sst, n, L.slice, (n + 1) & ~1};
-    void* args[] = {&a};
-    if (L.w_in_smem) {
-        static bool attr = false;
-        if (!attr) {
-            HPBJ_CUDA(cudaFuncSetAttribute(k_mgs<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)kMgsSmemMax));
-            attr = true;
-        }
-        HPBJ_CUDA(cudaLaunchCooperativeKernel((const void*)k_mgs<true>, dim3(L.grid), dim3(L.threads), args,
-                                              L.smem, st));
-    } else {
-        HPBJ_CUDA(cudaLaunchCooperativeKernel((const void*)k_mgs<false>, dim3(L.grid), dim3(L.threads), args,
-                                              0, st));
-    }
+void launch_mgs(const MgsLaunch& L, const KrylovBufs& kb, double* gram, GridBarrier* gb, SolveState* sst,
+                int n, cudaGraphConditionalHandle cond, cudaStream_t st, int64_t* launches) {
+    OrthArgs a{kb, gram, sst, gb, n, L.slice, (n + 1) & ~1, cond};
+    void (*fn)(OrthArgs);
+    if (L.icwy) fn = L.w_in_smem ? k_icwy<true> : k_icwy<false>;
+    else fn = L.w_in_smem ? k_mgs<true> : k_mgs<false>;
+    if (L.smem > 48 * 1024)
+        HPBJ_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem));
+    // cooperative attribute: co-residency guaranteed, capturable into graphs
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(L.grid);
+    cfg.blockDim = dim3(L.threads);
+    cfg.dynamicSmemBytes = L.smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    HPBJ_CUDA(cudaLaunchKernelEx(&cfg, fn, a));
     *launches += 1;
 }
 
-void launch_cycle_init(const KrylovBufs& kb, SolveState* sst, const double* r, int n, cudaStream_t st,
-                       int64_t* launches) {
+void launch_cycle_init(const KrylovBufs& kb, SolveState* sst, const double* r, int n,
+                       cudaGraphConditionalHandle cond, cudaStream_t st, int64_t* launches) {
     const int grid = std::max(1, std::min((n + 255) / 256, 148 * 8));
-    k_cycle_init<<<grid, 256, 0, st>>>(kb, sst, r, n);
+    k_cycle_init<<<grid, 256, 0, st>>>(kb, sst, r, n, cond);
+    *launches += 1;
+    HPBJ_CUDA(cudaGetLastError());
+}
+
+void launch_cycle_end(const KrylovBufs& kb, SolveState* sst, cudaGraphConditionalHandle cond, cudaStream_t st,
+                      int64_t* launches) {
+    k_cycle_end<<<1, 32, 0, st>>>(kb, sst, cond);
     *launches += 1;
     HPBJ_CUDA(cudaGetLastError());
 }

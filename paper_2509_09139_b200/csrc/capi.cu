@@ -6,7 +6,11 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
+#include <cstdio>
 #include <cstring>
+#include <map>
+#include <unordered_map>
 #include <string>
 #include <vector>
 
@@ -17,17 +21,87 @@ using namespace hpbj;
 
 namespace {
 
+// Device memory pool of one context: freed buffers are kept and reused by
+// later requests of similar size, so re-setup / e2e steps (set_matrix,
+// bj_setup, workspace) never pay cudaMalloc/cudaFree (which synchronise).
+struct Pool {
+    std::multimap<size_t, void*> free_;
+    std::unordered_map<void*, size_t> size_;
+    void* get(size_t bytes) {
+        bytes = std::max<size_t>(256, (bytes + 255) & ~size_t(255));
+        auto it = free_.lower_bound(bytes);
+        if (it != free_.end() && it->first <= 2 * bytes + (1 << 20)) {
+            void* p = it->second;
+            free_.erase(it);
+            return p;
+        }
+        void* p = nullptr;
+        cudaError_t e = cudaMalloc(&p, bytes);
+        if (e != cudaSuccess) {
+            // give cached blocks back to the driver and retry once
+            for (auto& kv : free_) {
+                cudaFree(kv.second);
+                size_.erase(kv.second);
+            }
+            free_.clear();
+            (void)cudaGetLastError();
+            HPBJ_CUDA(cudaMalloc(&p, bytes));
+        }
+        size_[p] = bytes;
+        return p;
+    }
+    void put(void* p) {
+        if (!p) return;
+        auto it = size_.find(p);
+        if (it == size_.end()) {
+            cudaFree(p);
+            return;
+        }
+        free_.emplace(it->second, p);
+    }
+    ~Pool() {
+        for (auto& kv : size_) cudaFree(kv.first);
+    }
+};
+
+thread_local Pool* t_pool = nullptr;
+
+// Slot-stable allocation: a context member keeps its device block across
+// release/re-setup while the size fits, so buffer addresses (and with them
+// the instantiated solve graph) stay valid from one setup to the next.
+struct Slots {
+    std::unordered_map<void*, std::pair<void*, size_t>> map;
+};
+thread_local Slots* t_slots = nullptr;
+
 template <class T>
-T* dalloc(size_t count) {
-    T* p = nullptr;
+void dslot(T*& member, size_t count) {
     if (count == 0) count = 1;
-    HPBJ_CUDA(cudaMalloc(&p, sizeof(T) * count));
-    return p;
+    const size_t bytes = sizeof(T) * count;
+    auto it = t_slots->map.find((void*)&member);
+    if (it != t_slots->map.end() && it->second.second >= bytes) {
+        member = static_cast<T*>(it->second.first);
+        return;
+    }
+    if (it != t_slots->map.end()) t_pool->put(it->second.first);
+    void* p = t_pool->get(bytes);
+    t_slots->map[(void*)&member] = {p, bytes};
+    member = static_cast<T*>(p);
 }
 
 template <class T>
-void dfree(T*& p) {
-    if (p) cudaFree(p);
+T* dalloc(size_t count) {
+    if (count == 0) count = 1;
+    return static_cast<T*>(t_pool->get(sizeof(T) * count));
+}
+
+template <class T>
+void dfree(T*& p) {  // slot-backed members: forget the pointer, keep the block
+    p = nullptr;
+}
+template <class T>
+void dput(T*& p) {  // transient blocks: back to the pool
+    if (p) t_pool->put(p);
     p = nullptr;
 }
 
@@ -52,6 +126,8 @@ constexpr double kU24 = 5.9604644775390625e-08;  // 2^-24
 }  // namespace
 
 struct hpbj_ctx {
+    Pool pool;  // destroyed last
+    Slots slots;
     int device = 0;
     int num_sms = 148;
     cudaStream_t stream = nullptr;
@@ -102,7 +178,14 @@ struct hpbj_ctx {
     double* d_red = nullptr;  // reduction partials
     double* d_bo = nullptr;   // host-API staging (original ordering)
     double* d_xo = nullptr;
+    double* d_gram = nullptr;
+    GridBarrier* d_gb = nullptr;
     MgsLaunch mgs;
+    int64_t hist_cap = 0;
+    bool use_graph = true;
+    cudaGraphExec_t graph_exec = nullptr;
+    int graph_builds = 0;
+    std::vector<uintptr_t> graph_sig;
 
     // profiling
     bool profiling = false;
@@ -110,6 +193,9 @@ struct hpbj_ctx {
     hpbj_kernel_stat stats[HPBJ_K_COUNT] = {};
 
     ~hpbj_ctx() {
+        t_pool = &pool;
+        t_slots = &slots;
+        if (graph_exec) cudaGraphExecDestroy(graph_exec);
         release_matrix();
         release_ws();
         if (stream) cudaStreamDestroy(stream);
@@ -165,6 +251,12 @@ struct hpbj_ctx {
         dfree(d_red);
         dfree(d_bo);
         dfree(d_xo);
+        dfree(d_gram);
+        dfree(d_gb);
+        dfree(kb.hist);
+        dfree(kb.hist_cycle);
+        dfree(kb.cycres);
+        hist_cap = 0;
         ws_m = -1;
     }
 };
@@ -172,8 +264,8 @@ struct hpbj_ctx {
 namespace {
 
 // Lanes per row from the mean row length; hub rows go to the CTA kernel.
-SpmvPlan make_plan(const std::vector<int64_t>& rp, const int* perm_or_null, int n) {
-    SpmvPlan p;
+void make_plan(SpmvPlan& p, const std::vector<int64_t>& rp, const int* perm_or_null, int n) {
+    p.n_long = 0;
     const double avg = n > 0 ? double(rp[n]) / n : 0.0;
     p.group = avg <= 6.0 ? 4 : avg <= 12.0 ? 8 : avg <= 24.0 ? 16 : 32;
     p.long_thresh = std::max(256, 16 * p.group);
@@ -183,11 +275,10 @@ SpmvPlan make_plan(const std::vector<int64_t>& rp, const int* perm_or_null, int 
     std::sort(rows.begin(), rows.end());
     p.n_long = (int)rows.size();
     if (p.n_long) {
-        p.long_rows = dalloc<int>(rows.size());
+        dslot(p.long_rows, rows.size());
         HPBJ_CUDA(cudaMemcpy(p.long_rows, rows.data(), sizeof(int) * rows.size(), cudaMemcpyHostToDevice));
-        p.ylong = dalloc<double>(n);
+        dslot(p.ylong, n);
     }
-    return p;
 }
 
 void ensure_ws(hpbj_ctx* c, int m) {
@@ -198,29 +289,32 @@ void ensure_ws(hpbj_ctx* c, int m) {
     KrylovBufs& kb = c->kb;
     kb.m = m;
     kb.ldv = ldv;
-    kb.V = dalloc<double>((size_t)(m + 1) * ldv);
+    dslot(kb.V, (size_t)(m + 1) * ldv);
     HPBJ_CUDA(cudaMemset(kb.V, 0, sizeof(double) * (size_t)(m + 1) * ldv));
-    kb.w = dalloc<double>(ldv);
+    dslot(kb.w, ldv);
     HPBJ_CUDA(cudaMemset(kb.w, 0, sizeof(double) * ldv));
-    kb.H = dalloc<double>((size_t)(m + 1) * m);
-    kb.R = dalloc<double>((size_t)(m + 1) * m);
-    kb.cs = dalloc<double>(m);
-    kb.sn = dalloc<double>(m);
-    kb.g = dalloc<double>(m + 1);
-    kb.y = dalloc<double>(m);
-    kb.est = dalloc<double>(m);
-    kb.partials = dalloc<double>(4 * 1024);
-    c->d_st = dalloc<SolveState>(1);
+    dslot(kb.H, (size_t)(m + 1) * m);
+    dslot(kb.R, (size_t)(m + 1) * m);
+    dslot(kb.cs, m);
+    dslot(kb.sn, m);
+    dslot(kb.g, m + 1);
+    dslot(kb.y, m);
+    dslot(kb.est, m);
+    dslot(kb.partials, orth_partials_doubles(c->num_sms));
+    dslot(c->d_gram, (size_t)(m + 1) * (m + 1));
+    dslot(c->d_gb, 1);
+    HPBJ_CUDA(cudaMemset(c->d_gb, 0, sizeof(GridBarrier)));
+    dslot(c->d_st, 1);
     HPBJ_CUDA(cudaMemset(c->d_st, 0, sizeof(SolveState)));
-    c->d_z32 = dalloc<float>(ldv);
+    dslot(c->d_z32, ldv);
     HPBJ_CUDA(cudaMemset(c->d_z32, 0, sizeof(float) * ldv));
-    c->d_xp = dalloc<double>(ldv);
-    c->d_bp = dalloc<double>(ldv);
-    c->d_r = dalloc<double>(ldv);
-    c->d_red = dalloc<double>(2048);
-    c->d_bo = dalloc<double>(ldv);
-    c->d_xo = dalloc<double>(ldv);
-    c->mgs = plan_mgs(n, c->num_sms);
+    dslot(c->d_xp, ldv);
+    dslot(c->d_bp, ldv);
+    dslot(c->d_r, ldv);
+    dslot(c->d_red, 2048);
+    dslot(c->d_bo, ldv);
+    dslot(c->d_xo, ldv);
+    c->mgs = plan_mgs(n, c->num_sms, m);
     c->ws_m = m;
 }
 
@@ -292,6 +386,116 @@ void record_kernel(hpbj_ctx* c, size_t slot, bool begin) {
     HPBJ_CUDA(cudaEventRecord(c->timer.ev[2 * slot + (begin ? 0 : 1)], c->stream));
 }
 
+// One restart cycle of hybrid_restart_gmres as device launches (gmres.cpp:
+// 236-256 around run_cycle :97-166). With conditional handles (graph mode)
+// the Arnoldi loop is a WHILE node driven by the orthogonalisation kernel.
+void enqueue_cycle_head(hpbj_ctx* c, cudaGraphConditionalHandle hin) {
+    launch_cycle_init(c->kb, c->d_st, c->d_r, c->A.n, hin, c->stream, &c->launches);
+}
+void enqueue_step(hpbj_ctx* c, cudaGraphConditionalHandle hin, int it) {
+    KrylovBufs& kb = c->kb;
+    record_kernel(c, 3 * it + 0, true);
+    launch_apply_step(apply_params(c), kb.V, kb.ldv, c->d_st, c->d_z32, c->stream, &c->launches);
+    record_kernel(c, 3 * it + 0, false);
+    record_kernel(c, 3 * it + 1, true);
+    launch_spmv_f32x(c->B, c->planB, c->d_z32, kb.w, c->d_st, c->stream, &c->launches);
+    record_kernel(c, 3 * it + 1, false);
+    record_kernel(c, 3 * it + 2, true);
+    launch_mgs(c->mgs, kb, c->d_gram, c->d_gb, c->d_st, c->A.n, hin, c->stream, &c->launches);
+    record_kernel(c, 3 * it + 2, false);
+}
+void enqueue_cycle_tail(hpbj_ctx* c, cudaGraphConditionalHandle hout) {
+    KrylovBufs& kb = c->kb;
+    launch_solve_y(kb, c->d_st, c->stream, &c->launches);
+    launch_apply_update(apply_params(c), kb.V, kb.ldv, kb.y, c->d_st, c->d_xp, c->stream, &c->launches);
+    launch_residual(c->B, c->planB, c->d_xp, c->d_bp, c->d_r, c->d_st, c->d_red, c->stream, &c->launches);
+    launch_cycle_end(kb, c->d_st, hout, c->stream, &c->launches);
+}
+
+std::vector<uintptr_t> graph_signature(const hpbj_ctx* c) {
+    const KrylovBufs& k = c->kb;
+    const SpmvPlan& p = c->planB;
+    const MgsLaunch& L = c->mgs;
+    return {(uintptr_t)k.V, (uintptr_t)k.w, (uintptr_t)k.H, (uintptr_t)k.R, (uintptr_t)k.cs, (uintptr_t)k.sn,
+            (uintptr_t)k.g, (uintptr_t)k.y, (uintptr_t)k.est, (uintptr_t)k.partials, (uintptr_t)k.hist,
+            (uintptr_t)k.hist_cycle, (uintptr_t)k.cycres, (uintptr_t)k.m, (uintptr_t)k.ldv,
+            (uintptr_t)c->d_st, (uintptr_t)c->d_z32, (uintptr_t)c->d_xp, (uintptr_t)c->d_bp, (uintptr_t)c->d_r,
+            (uintptr_t)c->d_red, (uintptr_t)c->d_gram, (uintptr_t)c->d_gb, (uintptr_t)c->B.rp, (uintptr_t)c->B.ci,
+            (uintptr_t)c->B.val, (uintptr_t)c->B.n, (uintptr_t)c->B.nnz, (uintptr_t)p.group,
+            (uintptr_t)p.long_thresh, (uintptr_t)p.n_long, (uintptr_t)p.long_rows, (uintptr_t)p.ylong,
+            (uintptr_t)c->s, (uintptr_t)c->d_bstart, (uintptr_t)c->d_fac_off, (uintptr_t)c->d_fac,
+            (uintptr_t)c->d_piv, (uintptr_t)c->dmax, (uintptr_t)L.grid, (uintptr_t)L.threads, (uintptr_t)L.slice,
+            (uintptr_t)L.smem, (uintptr_t)L.icwy, (uintptr_t)L.w_in_smem};
+}
+
+// The whole restart loop as one CUDA graph: WHILE(cycles) { cycle_init;
+// WHILE(steps) { apply; spmv; orth }; solve_y; x += M^-1 V y; residual;
+// bookkeeping }. Rebuilt only when a buffer or launch shape changes.
+void ensure_graph(hpbj_ctx* c) {
+    std::vector<uintptr_t> sig = graph_signature(c);
+    if (c->graph_exec && sig == c->graph_sig) return;
+    if (c->graph_exec) {
+        cudaGraphExecDestroy(c->graph_exec);
+        c->graph_exec = nullptr;
+    }
+    cudaStream_t st = c->stream;
+    cudaGraph_t g;
+    HPBJ_CUDA(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle hout;
+    HPBJ_CUDA(cudaGraphConditionalHandleCreate(&hout, g, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams op = {};
+    op.type = cudaGraphNodeTypeConditional;
+    op.conditional.handle = hout;
+    op.conditional.type = cudaGraphCondTypeWhile;
+    op.conditional.size = 1;
+    cudaGraphNode_t onode;
+    HPBJ_CUDA(cudaGraphAddNode(&onode, g, nullptr, 0, &op));
+    cudaGraph_t body = op.conditional.phGraph_out[0];
+    cudaGraphConditionalHandle hin;
+    HPBJ_CUDA(cudaGraphConditionalHandleCreate(&hin, body, 0, 0));
+
+    HPBJ_CUDA(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    enqueue_cycle_head(c, hin);
+    cudaStreamCaptureStatus cstat;
+    cudaGraph_t capg;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t ndeps = 0;
+    HPBJ_CUDA(cudaStreamGetCaptureInfo(st, &cstat, nullptr, &capg, &deps, &ndeps));
+    cudaGraphNodeParams ip = {};
+    ip.type = cudaGraphNodeTypeConditional;
+    ip.conditional.handle = hin;
+    ip.conditional.type = cudaGraphCondTypeWhile;
+    ip.conditional.size = 1;
+    cudaGraphNode_t inode;
+    HPBJ_CUDA(cudaGraphAddNode(&inode, capg, deps, ndeps, &ip));
+    cudaGraph_t ibody = ip.conditional.phGraph_out[0];
+    HPBJ_CUDA(cudaStreamUpdateCaptureDependencies(st, &inode, 1, cudaStreamSetCaptureDependencies));
+    enqueue_cycle_tail(c, hout);
+    HPBJ_CUDA(cudaStreamEndCapture(st, &body));
+
+    HPBJ_CUDA(cudaStreamBeginCaptureToGraph(st, ibody, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    enqueue_step(c, hin, 0);
+    HPBJ_CUDA(cudaStreamEndCapture(st, &ibody));
+
+    HPBJ_CUDA(cudaGraphInstantiate(&c->graph_exec, g, 0));
+    HPBJ_CUDA(cudaGraphDestroy(g));
+    c->graph_sig = sig;
+    ++c->graph_builds;
+    if (getenv("HPBJ_DEBUG")) fprintf(stderr, "[hpbj] solve graph built (#%d)\n", c->graph_builds);
+}
+
+void ensure_hist(hpbj_ctx* c, int64_t max_restarts) {
+    const int64_t need = max_restarts * c->kb.m + 1;
+    if (c->hist_cap >= need) return;
+    dfree(c->kb.hist);
+    dfree(c->kb.hist_cycle);
+    dfree(c->kb.cycres);
+    dslot(c->kb.hist, need);
+    dslot(c->kb.hist_cycle, need);
+    dslot(c->kb.cycres, max_restarts + 1);
+    c->hist_cap = need;
+}
+
 void solve(hpbj_ctx* c, const double* d_b, double* d_x, const hpbj_gmres_opts* o, hpbj_report* rep,
            hpbj_history_point* hist, int64_t hist_cap, double* cycle_res, int64_t cyc_cap) {
     const auto t0 = std::chrono::steady_clock::now();
@@ -303,10 +507,12 @@ void solve(hpbj_ctx* c, const double* d_b, double* d_x, const hpbj_gmres_opts* o
     if (opt.restart_m < 1 || opt.tol <= 0.0 || opt.max_restarts < 1)
         fail(HPBJ_EINVAL, "gmres: invalid config");
     if (opt.restart_m > 1024) fail(HPBJ_EINVAL, "gmres: restart_m > 1024 unsupported");
+    if (opt.max_restarts > (int64_t)1 << 24) fail(HPBJ_EINVAL, "gmres: max_restarts too large");
     const int n = c->A.n;
     const int m = (int)opt.restart_m;
     const double floor_u = opt.floor_roundoff > 0.0 ? opt.floor_roundoff : kU24;
     ensure_ws(c, m);
+    ensure_hist(c, opt.max_restarts);
     cudaStream_t st = c->stream;
     KrylovBufs& kb = c->kb;
     hpbj_report R{};
@@ -324,7 +530,7 @@ void solve(hpbj_ctx* c, const double* d_b, double* d_x, const hpbj_gmres_opts* o
     HPBJ_CUDA(cudaStreamSynchronize(st));
     const double bnorm = hs.scratch;
     HPBJ_CUDA(cudaMemsetAsync(c->d_xp, 0, sizeof(double) * kb.ldv, st));
-    if (bnorm == 0.0) {
+    if (bnorm == 0.0) {  // gmres.cpp:215-220
         R.converged = 1;
         push_hist(0, 0, 0.0);
         HPBJ_CUDA(cudaMemsetAsync(d_x, 0, sizeof(double) * n, st));
@@ -335,6 +541,7 @@ void solve(hpbj_ctx* c, const double* d_b, double* d_x, const hpbj_gmres_opts* o
         return;
     }
     const double thr = opt.absolute_tol ? opt.tol : opt.tol * bnorm;
+    hs = SolveState{};
     hs.n = n;
     hs.m = m;
     hs.ldv = kb.ldv;
@@ -342,8 +549,7 @@ void solve(hpbj_ctx* c, const double* d_b, double* d_x, const hpbj_gmres_opts* o
     hs.bnorm = bnorm;
     hs.breakdown_factor = opt.breakdown_tol_factor * kU53;
     hs.floor_roundoff = floor_u;
-    hs.done = 0;
-    hs.ticket = 0;
+    hs.max_restarts = (int32_t)opt.max_restarts;
     HPBJ_CUDA(cudaMemcpyAsync(c->d_st, &hs, sizeof(hs), cudaMemcpyHostToDevice, st));
 
     // r = b - A*0, ||r|| (gmres.cpp:223-230)
@@ -356,56 +562,57 @@ void solve(hpbj_ctx* c, const double* d_b, double* d_x, const hpbj_gmres_opts* o
     if (rnorm <= thr) {
         R.converged = 1;
     } else {
-        if (c->profiling) c->timer.reserve((size_t)3 * m);
-        int64_t global_iter = 0;
-        int64_t cycles = 0;
-        std::vector<double> est(m);
-        for (int64_t cycle = 0; cycle < opt.max_restarts; ++cycle) {
-            launch_cycle_init(kb, c->d_st, c->d_r, n, st, &c->launches);
-            for (int it = 0; it < m; ++it) {
-                record_kernel(c, 3 * it + 0, true);
-                launch_apply_step(apply_params(c), kb.V, kb.ldv, c->d_st, c->d_z32, st, &c->launches);
-                record_kernel(c, 3 * it + 0, false);
-                record_kernel(c, 3 * it + 1, true);
-                launch_spmv_f32x(c->B, c->planB, c->d_z32, kb.w, c->d_st, st, &c->launches);
-                record_kernel(c, 3 * it + 1, false);
-                record_kernel(c, 3 * it + 2, true);
-                launch_mgs(c->mgs, kb, c->d_st, n, st, &c->launches);
-                record_kernel(c, 3 * it + 2, false);
+        const bool use_graph = !c->profiling && c->use_graph;
+        if (use_graph) {
+            ensure_graph(c);
+            HPBJ_CUDA(cudaGraphLaunch(c->graph_exec, st));
+            c->launches += 0;  // kernel launches inside the graph are counted below
+        } else {
+            if (c->profiling) c->timer.reserve((size_t)3 * m);
+            for (;;) {
+                enqueue_cycle_head(c, 0);
+                for (int it = 0; it < m; ++it) enqueue_step(c, 0, it);
+                enqueue_cycle_tail(c, 0);
+                HPBJ_CUDA(cudaMemcpyAsync(&hs, c->d_st, sizeof(hs), cudaMemcpyDeviceToHost, st));
+                HPBJ_CUDA(cudaStreamSynchronize(st));
+                if (c->profiling) {
+                    for (int it = 0; it < hs.last_steps; ++it)
+                        for (int k = 0; k < 3; ++k) {
+                            float ms = 0.f;
+                            HPBJ_CUDA(cudaEventElapsedTime(&ms, c->timer.ev[2 * (3 * it + k)],
+                                                           c->timer.ev[2 * (3 * it + k) + 1]));
+                            c->stats[k].launches += 1;
+                            c->stats[k].total_ms += ms;
+                        }
+                }
+                if (hs.converged || hs.cycles >= hs.max_restarts || hs.last_steps == 0) break;
             }
-            launch_solve_y(kb, c->d_st, st, &c->launches);
-            launch_apply_update(apply_params(c), kb.V, kb.ldv, kb.y, c->d_st, c->d_xp, st, &c->launches);
-            launch_residual(c->B, c->planB, c->d_xp, c->d_bp, c->d_r, c->d_st, c->d_red, st, &c->launches);
-            HPBJ_CUDA(cudaMemcpyAsync(&hs, c->d_st, sizeof(hs), cudaMemcpyDeviceToHost, st));
-            HPBJ_CUDA(cudaMemcpyAsync(est.data(), kb.est, sizeof(double) * m, cudaMemcpyDeviceToHost, st));
-            HPBJ_CUDA(cudaStreamSynchronize(st));
-            ++cycles;
-            const int steps = hs.j;
-            if (c->profiling) {
-                for (int it = 0; it < steps; ++it)
-                    for (int k = 0; k < 3; ++k) {
-                        float ms = 0.f;
-                        HPBJ_CUDA(cudaEventElapsedTime(&ms, c->timer.ev[2 * (3 * it + k)],
-                                                       c->timer.ev[2 * (3 * it + k) + 1]));
-                        c->stats[k].launches += 1;
-                        c->stats[k].total_ms += ms;
-                    }
-            }
-            for (int k = 0; k < steps; ++k) push_hist(cycle, ++global_iter, est[k] / bnorm);
-            R.total_iterations += steps;
-            R.breakdown = R.breakdown || hs.breakdown;
-            R.ls_rank_deficient = R.ls_rank_deficient || hs.rank_deficient;
-            rnorm = hs.rnorm;
-            if (cycle_res && clen < cyc_cap) cycle_res[clen] = rnorm / bnorm;
-            ++clen;
-            if (rnorm <= thr) {
-                R.converged = 1;
-                break;
-            }
-            if (steps == 0) break;
         }
-        R.restarts = cycles > 0 ? cycles - 1 : 0;
-        R.final_residual = rnorm / bnorm;
+        HPBJ_CUDA(cudaMemcpyAsync(&hs, c->d_st, sizeof(hs), cudaMemcpyDeviceToHost, st));
+        HPBJ_CUDA(cudaStreamSynchronize(st));
+        if (use_graph)  // 3 kernels per Arnoldi step + 8 per cycle (incl. long-row SpMV parts)
+            c->launches += (int64_t)hs.total_iterations * (3 + (c->planB.n_long ? 1 : 0)) +
+                           (int64_t)hs.cycles * (5 + (c->planB.n_long ? 1 : 0));
+        std::vector<double> hv(hs.hist_len), cr(hs.cycles);
+        std::vector<int> hc(hs.hist_len);
+        if (hs.hist_len) {
+            HPBJ_CUDA(cudaMemcpyAsync(hv.data(), kb.hist, sizeof(double) * hs.hist_len, cudaMemcpyDeviceToHost, st));
+            HPBJ_CUDA(cudaMemcpyAsync(hc.data(), kb.hist_cycle, sizeof(int) * hs.hist_len, cudaMemcpyDeviceToHost, st));
+        }
+        if (hs.cycles)
+            HPBJ_CUDA(cudaMemcpyAsync(cr.data(), kb.cycres, sizeof(double) * hs.cycles, cudaMemcpyDeviceToHost, st));
+        HPBJ_CUDA(cudaStreamSynchronize(st));
+        for (int k = 0; k < hs.hist_len; ++k) push_hist(hc[k], k + 1, hv[k]);
+        for (int k = 0; k < hs.cycles; ++k) {
+            if (cycle_res && clen < cyc_cap) cycle_res[clen] = cr[k];
+            ++clen;
+        }
+        R.converged = hs.converged;
+        R.total_iterations = hs.total_iterations;
+        R.breakdown = hs.breakdown_any;
+        R.ls_rank_deficient = hs.rank_any;
+        R.restarts = hs.cycles > 0 ? hs.cycles - 1 : 0;
+        R.final_residual = hs.rnorm / bnorm;
     }
     launch_permute_vec(n, c->d_perm, c->d_xp, d_x, true, st, &c->launches);
     HPBJ_CUDA(cudaStreamSynchronize(st));
@@ -436,6 +643,8 @@ int hpbj_create(hpbj_ctx** out, int device) {
         c->device = device;
         c->num_sms = prop.multiProcessorCount;
         HPBJ_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        const char* ng = getenv("HPBJ_NOGRAPH");
+        c->use_graph = !(ng && ng[0] == '1');
         *out = c;
     });
 }
@@ -455,6 +664,8 @@ int hpbj_set_profiling(hpbj_ctx* ctx, int enable) {
 
 int hpbj_get_kernel_stats(hpbj_ctx* ctx, hpbj_kernel_stat* out) {
     if (!ctx || !out) return HPBJ_EINVAL;
+    t_pool = &ctx->pool;
+    t_slots = &ctx->slots;
     return guard(&ctx->err, [&] {
         // algorithmic bytes per launch
         const double n = ctx->A.n, nnz = ctx->A.nnz;
@@ -477,6 +688,8 @@ int hpbj_get_kernel_stats(hpbj_ctx* ctx, hpbj_kernel_stat* out) {
 
 int hpbj_set_matrix(hpbj_ctx* ctx, int64_t n, const int64_t* row_ptr, const int64_t* col, const double* val) {
     if (!ctx) return HPBJ_EINVAL;
+    t_pool = &ctx->pool;
+    t_slots = &ctx->slots;
     return guard(&ctx->err, [&] {
         check_csr(n, row_ptr, col, val);
         if (n >= (int64_t)INT32_MAX || row_ptr[n] >= (int64_t)INT32_MAX)
@@ -490,22 +703,24 @@ int hpbj_set_matrix(hpbj_ctx* ctx, int64_t n, const int64_t* row_ptr, const int6
         for (int64_t k = 0; k < nnz; ++k) ci[k] = (int)col[k];
         ctx->A.n = ni;
         ctx->A.nnz = nnz;
-        ctx->A.rp = dalloc<int>(ni + 1);
-        ctx->A.ci = dalloc<int>(nnz);
-        ctx->A.val = dalloc<double>(nnz);
+        dslot(ctx->A.rp, ni + 1);
+        dslot(ctx->A.ci, nnz);
+        dslot(ctx->A.val, nnz);
         HPBJ_CUDA(cudaMemcpy(ctx->A.rp, rp.data(), sizeof(int) * (ni + 1), cudaMemcpyHostToDevice));
         HPBJ_CUDA(cudaMemcpy(ctx->A.ci, ci.data(), sizeof(int) * nnz, cudaMemcpyHostToDevice));
         HPBJ_CUDA(cudaMemcpy(ctx->A.val, val, sizeof(double) * nnz, cudaMemcpyHostToDevice));
         ctx->h_rp.assign(row_ptr, row_ptr + n + 1);
-        ctx->planA = make_plan(ctx->h_rp, nullptr, ni);
-        ctx->d_tmpx = dalloc<double>(ni);
-        ctx->d_tmpy = dalloc<double>(ni);
+        make_plan(ctx->planA, ctx->h_rp, nullptr, ni);
+        dslot(ctx->d_tmpx, ni);
+        dslot(ctx->d_tmpy, ni);
         ctx->has_matrix = true;
     });
 }
 
 int hpbj_update_values(hpbj_ctx* ctx, const double* val) {
     if (!ctx) return HPBJ_EINVAL;
+    t_pool = &ctx->pool;
+    t_slots = &ctx->slots;
     return guard(&ctx->err, [&] {
         if (!ctx->has_matrix) fail(HPBJ_ELOGIC, "update_values: no matrix");
         HPBJ_CUDA(cudaMemcpyAsync(ctx->A.val, val, sizeof(double) * ctx->A.nnz, cudaMemcpyHostToDevice,
@@ -516,6 +731,8 @@ int hpbj_update_values(hpbj_ctx* ctx, const double* val) {
 
 int hpbj_spmv(hpbj_ctx* ctx, const double* x, double* y) {
     if (!ctx) return HPBJ_EINVAL;
+    t_pool = &ctx->pool;
+    t_slots = &ctx->slots;
     return guard(&ctx->err, [&] {
         if (!ctx->has_matrix) fail(HPBJ_ELOGIC, "spmv: no matrix");
         const int n = ctx->A.n;
@@ -533,6 +750,8 @@ int hpbj_bj_setup(hpbj_ctx* ctx, int64_t s, const int64_t* perm, const int64_t* 
         std::memset(info, 0, sizeof(*info));
         info->singular_block = info->singular_column = -1;
     }
+    t_pool = &ctx->pool;
+    t_slots = &ctx->slots;
     return guard(&ctx->err, [&] {
         if (!ctx->has_matrix) fail(HPBJ_ELOGIC, "block_jacobi: no matrix");
         if (eps_pivot < 0.0) fail(HPBJ_EINVAL, "gp_lu: negative eps_pivot");
@@ -574,23 +793,23 @@ int hpbj_bj_setup(hpbj_ctx* ctx, int64_t s, const int64_t* perm, const int64_t* 
         }
         ctx->fac_floats = off;
         const int nnz = ctx->A.nnz;
-        ctx->d_perm = dalloc<int>(n);
+        dslot(ctx->d_perm, n);
         ctx->B.n = n;
         ctx->B.nnz = nnz;
-        ctx->B.rp = dalloc<int>(n + 1);
-        ctx->B.ci = dalloc<int>(nnz);
-        ctx->B.val = dalloc<double>(nnz);
-        ctx->d_src = dalloc<int>(nnz);
-        ctx->d_bstart = dalloc<int>(s + 1);
-        ctx->d_fac_off = dalloc<int64_t>(s);
-        ctx->d_fac = dalloc<float>(off);
-        ctx->d_piv = dalloc<int>(n);
-        ctx->d_pert_count = dalloc<int>(s);
-        ctx->d_pert = dalloc<PertRecord>(4096);
-        ctx->d_pert_n = dalloc<int>(1);
-        ctx->d_singular = dalloc<unsigned long long>(1);
+        dslot(ctx->B.rp, n + 1);
+        dslot(ctx->B.ci, nnz);
+        dslot(ctx->B.val, nnz);
+        dslot(ctx->d_src, nnz);
+        dslot(ctx->d_bstart, s + 1);
+        dslot(ctx->d_fac_off, s);
+        dslot(ctx->d_fac, off);
+        dslot(ctx->d_piv, n);
+        dslot(ctx->d_pert_count, s);
+        dslot(ctx->d_pert, 4096);
+        dslot(ctx->d_pert_n, 1);
+        dslot(ctx->d_singular, 1);
         const size_t scr = block_lu_scratch_floats(dmax, ctx->num_sms, &ctx->lu_smem_dim, &ctx->lu_scratch_ld);
-        if (scr) ctx->d_lu_scratch = dalloc<float>(scr);
+        if (scr) dslot(ctx->d_lu_scratch, scr);
         HPBJ_CUDA(cudaMemcpyAsync(ctx->d_perm, hperm.data(), sizeof(int) * n, cudaMemcpyHostToDevice, st));
         HPBJ_CUDA(cudaMemcpyAsync(ctx->d_bstart, bst.data(), sizeof(int) * (s + 1), cudaMemcpyHostToDevice, st));
         HPBJ_CUDA(cudaMemcpyAsync(ctx->d_fac_off, ctx->h_fac_off.data(), sizeof(int64_t) * s,
@@ -608,11 +827,11 @@ int hpbj_bj_setup(hpbj_ctx* ctx, int64_t s, const int64_t* perm, const int64_t* 
         ctx->n_long_sort = (int)lrows.size();
         ctx->max_long_sort = maxlen;
         if (!lrows.empty()) {
-            ctx->d_long_sort = dalloc<int>(lrows.size());
+            dslot(ctx->d_long_sort, lrows.size());
             HPBJ_CUDA(cudaMemcpyAsync(ctx->d_long_sort, lrows.data(), sizeof(int) * lrows.size(),
                                       cudaMemcpyHostToDevice, st));
         }
-        ctx->planB = make_plan(ctx->h_rp, hperm.data(), n);
+        make_plan(ctx->planB, ctx->h_rp, hperm.data(), n);
         int* tmp = dalloc<int>((size_t)n + 8192);
         cudaEvent_t e0, e1;
         HPBJ_CUDA(cudaEventCreate(&e0));
@@ -626,7 +845,7 @@ int hpbj_bj_setup(hpbj_ctx* ctx, int64_t s, const int64_t* perm, const int64_t* 
         HPBJ_CUDA(cudaEventElapsedTime(&ms, e0, e1));
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
-        cudaFree(tmp);
+        dput(tmp);
         ctx->has_pc = true;
         factor(ctx, info);
         if (info) info->ms_permute = ms;
@@ -639,6 +858,8 @@ int hpbj_bj_refactor(hpbj_ctx* ctx, hpbj_setup_info* info) {
         std::memset(info, 0, sizeof(*info));
         info->singular_block = info->singular_column = -1;
     }
+    t_pool = &ctx->pool;
+    t_slots = &ctx->slots;
     return guard(&ctx->err, [&] {
         if (!ctx->d_fac) fail(HPBJ_ELOGIC, "refactor: no block-Jacobi partition set up");
         ctx->has_pc = true;
@@ -648,6 +869,8 @@ int hpbj_bj_refactor(hpbj_ctx* ctx, hpbj_setup_info* info) {
 
 int hpbj_bj_apply(hpbj_ctx* ctx, const double* v, double* z) {
     if (!ctx) return HPBJ_EINVAL;
+    t_pool = &ctx->pool;
+    t_slots = &ctx->slots;
     return guard(&ctx->err, [&] {
         if (!ctx->has_pc) fail(HPBJ_ELOGIC, "apply: block-Jacobi preconditioner not set up");
         const int n = ctx->A.n;
@@ -663,6 +886,8 @@ int hpbj_bj_apply(hpbj_ctx* ctx, const double* v, double* z) {
 
 int hpbj_get_block_factors(hpbj_ctx* ctx, int64_t block, int64_t* dim, float* f, int64_t* pivot_rows) {
     if (!ctx) return HPBJ_EINVAL;
+    t_pool = &ctx->pool;
+    t_slots = &ctx->slots;
     return guard(&ctx->err, [&] {
         if (!ctx->has_pc) fail(HPBJ_ELOGIC, "factors: block-Jacobi preconditioner not set up");
         if (block < 0 || block >= ctx->s) fail(HPBJ_ERANGE, "factors: block index out of range");
@@ -688,6 +913,8 @@ int hpbj_get_block_factors(hpbj_ctx* ctx, int64_t block, int64_t* dim, float* f,
 
 int hpbj_get_block_stats(hpbj_ctx* ctx, int64_t* dims, int64_t* perturbations) {
     if (!ctx) return HPBJ_EINVAL;
+    t_pool = &ctx->pool;
+    t_slots = &ctx->slots;
     return guard(&ctx->err, [&] {
         if (!ctx->has_pc) fail(HPBJ_ELOGIC, "stats: block-Jacobi preconditioner not set up");
         std::vector<int> pc(ctx->s);
@@ -713,6 +940,8 @@ void hpbj_gmres_default_opts(hpbj_gmres_opts* o) {
 int hpbj_gmres(hpbj_ctx* ctx, const double* b, double* x, const hpbj_gmres_opts* opts, hpbj_report* rep,
                hpbj_history_point* hist, int64_t hist_cap, double* cycle_res, int64_t cyc_cap) {
     if (!ctx) return HPBJ_EINVAL;
+    t_pool = &ctx->pool;
+    t_slots = &ctx->slots;
     return guard(&ctx->err, [&] {
         if (!ctx->has_matrix) fail(HPBJ_ELOGIC, "gmres: no matrix");
         const int n = ctx->A.n;
@@ -730,6 +959,8 @@ int hpbj_gmres_device(hpbj_ctx* ctx, const double* d_b, double* d_x, const hpbj_
                       hpbj_report* rep, hpbj_history_point* hist, int64_t hist_cap, double* cycle_res,
                       int64_t cyc_cap) {
     if (!ctx) return HPBJ_EINVAL;
+    t_pool = &ctx->pool;
+    t_slots = &ctx->slots;
     return guard(&ctx->err, [&] { solve(ctx, d_b, d_x, opts, rep, hist, hist_cap, cycle_res, cyc_cap); });
 }
 

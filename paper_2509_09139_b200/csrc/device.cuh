@@ -53,6 +53,22 @@ struct SolveState {
     double scratch;
     uint32_t ticket;       // last-block-done counter
     uint32_t pad2;
+    // restart driver bookkeeping (hybrid_restart_gmres, gmres.cpp:236-258),
+    // advanced on the device by k_cycle_end when the solve runs as a graph
+    int32_t max_restarts;
+    int32_t cycles;
+    int32_t total_iterations;
+    int32_t hist_len;      // device history rows written (excluding row 0)
+    int32_t converged;
+    int32_t breakdown_any;
+    int32_t rank_any;
+    int32_t last_steps;
+};
+
+// Generation barrier of one cooperative launch (zero-initialised).
+struct GridBarrier {
+    unsigned int count;
+    unsigned int gen;
 };
 
 // Grid-wide deterministic reduction: each CTA deposits a partial; the last

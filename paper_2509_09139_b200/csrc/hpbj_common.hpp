@@ -47,7 +47,7 @@ int guard(std::string* slot, F&& f) {
 struct Adjacency {
     int64_t n = 0;
     std::vector<int64_t> start;  // n + 1
-    std::vector<int64_t> nbr;
+    std::vector<int32_t> nbr;
     std::vector<double> w;
 };
 

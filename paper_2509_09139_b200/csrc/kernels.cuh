@@ -122,6 +122,9 @@ struct KrylovBufs {
     double* y = nullptr;   // m
     double* est = nullptr; // m: Givens estimate after each step of the cycle
     double* partials = nullptr;
+    double* hist = nullptr;     // device residual history (est/||b|| per step)
+    int* hist_cycle = nullptr;  // cycle index of each history row
+    double* cycres = nullptr;   // true relative residual per cycle
     int m = 0;
 };
 
@@ -131,13 +134,23 @@ struct MgsLaunch {
     int slice = 0;
     size_t smem = 0;
     bool w_in_smem = true;
+    bool icwy = false;  // compact-WY (2 barriers/step) instead of textbook MGS (j+2)
 };
 
-MgsLaunch plan_mgs(int n, int num_sms);
-void launch_mgs(const MgsLaunch& L, const KrylovBufs& kb, SolveState* sst, int n, cudaStream_t st,
-                int64_t* launches);
-void launch_cycle_init(const KrylovBufs& kb, SolveState* sst, const double* r, int n, cudaStream_t st,
-                       int64_t* launches);
+constexpr int kMaxRestart = 128;  // compact-WY tables; textbook MGS has no limit
+
+MgsLaunch plan_mgs(int n, int num_sms, int m);
+size_t orth_partials_doubles(int num_sms);
+// cond: WHILE-node handle of the Arnoldi loop (0 outside graphs); the kernel
+// sets it to !done when it finishes the step.
+void launch_mgs(const MgsLaunch& L, const KrylovBufs& kb, double* gram, GridBarrier* gb, SolveState* sst,
+                int n, cudaGraphConditionalHandle cond, cudaStream_t st, int64_t* launches);
+void launch_cycle_init(const KrylovBufs& kb, SolveState* sst, const double* r, int n,
+                       cudaGraphConditionalHandle cond, cudaStream_t st, int64_t* launches);
+// restart-driver bookkeeping after the true residual; sets the outer WHILE
+// handle to (!converged && cycles < max_restarts && steps > 0).
+void launch_cycle_end(const KrylovBufs& kb, SolveState* sst, cudaGraphConditionalHandle cond, cudaStream_t st,
+                      int64_t* launches);
 void launch_solve_y(const KrylovBufs& kb, SolveState* sst, cudaStream_t st, int64_t* launches);
 
 }  // namespace hpbj
