@@ -246,3 +246,115 @@ class Ref:
             },
             perturbations=rep.perturbations,
         )
+
+
+# ---------------------------------------------------------------------------
+class PortReport(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int64) for n in ("converged", "total_iterations", "restarts", "breakdown",
+                                              "rank_deficient", "hist_len", "cyc_len")] + [
+        ("final_residual", ctypes.c_double), ("singular_block", ctypes.c_int64),
+        ("singular_column", ctypes.c_int64)]
+
+
+MODES = {"double": 0, "hybrid": 1, "mix": 2}
+
+
+class Port:
+    """ctypes view of oracle/build/liboracle_port.so (hpbj_oracle.c): our
+    plain-C restatement of the reference algorithm."""
+
+    def __init__(self, path: str = PORT_LIB):
+        if not os.path.exists(path):
+            raise RuntimeError(f"{path} missing: build it with `make -C oracle port`")
+        self.L = ctypes.CDLL(path)
+
+    @staticmethod
+    def _csr(rp, ci, v):
+        return Ref._csr(rp, ci, v)
+
+    def _chk(self, rc, what):
+        if rc != 0:
+            raise OracleError(rc, f"{what}: rc={rc}")
+
+    def spmv(self, rp, ci, v, x, fp32=False):
+        rp, ci, v = self._csr(rp, ci, v)
+        n = len(rp) - 1
+        x = np.ascontiguousarray(x, np.float64)
+        y = np.zeros(n)
+        self._chk(self.L.orc_spmv(ctypes.c_int64(n), _p(rp, _i64p), _p(ci, _i64p), _p(v, _f64p), _p(x, _f64p),
+                                  _p(y, _f64p), ctypes.c_int(int(fp32))), "spmv")
+        return y
+
+    def graph(self, rp, ci, v):
+        rp, ci, v = self._csr(rp, ci, v)
+        n = len(rp) - 1
+        cap = 2 * int(rp[-1]) + 1
+        st, nb, w = np.zeros(n + 1, np.int64), np.zeros(cap, np.int64), np.zeros(cap)
+        self._chk(self.L.orc_graph(ctypes.c_int64(n), _p(rp, _i64p), _p(ci, _i64p), _p(v, _f64p), _p(st, _i64p),
+                                   _p(nb, _i64p), _p(w, _f64p), ctypes.c_int64(cap)), "graph")
+        k = int(st[-1])
+        return st, nb[:k].copy(), w[:k].copy()
+
+    def partition(self, rp, ci, v, s, tol=0.1):
+        rp, ci, v = self._csr(rp, ci, v)
+        n = len(rp) - 1
+        asg = np.zeros(n, np.int64)
+        self._chk(self.L.orc_partition(ctypes.c_int64(n), _p(rp, _i64p), _p(ci, _i64p), _p(v, _f64p),
+                                       ctypes.c_int64(s), ctypes.c_double(tol), _p(asg, _i64p)), "partition")
+        return asg
+
+    def factors(self, rp, ci, v, s, assignment, eps=1e-10):
+        rp, ci, v = self._csr(rp, ci, v)
+        n = len(rp) - 1
+        asg = np.ascontiguousarray(assignment, np.int64)
+        dims = np.bincount(asg, minlength=s).astype(np.int64)
+        f64 = np.zeros(int((dims * dims).sum()))
+        piv = np.zeros(n, np.int64)
+        pert = np.zeros(s, np.int64)
+        sb, sc = ctypes.c_int64(), ctypes.c_int64()
+        rc = self.L.orc_factors(ctypes.c_int64(n), _p(rp, _i64p), _p(ci, _i64p), _p(v, _f64p), ctypes.c_int64(s),
+                                _p(asg, _i64p), ctypes.c_double(eps), _p(f64, _f64p), _p(piv, _i64p),
+                                _p(pert, _i64p), ctypes.byref(sb), ctypes.byref(sc))
+        if rc == 3:
+            raise OracleError(3, f"singular block {sb.value} column {sc.value}")
+        self._chk(rc, "factors")
+        return dims, f64, piv, pert
+
+    def apply(self, rp, ci, v, s, assignment, vin, eps=1e-10, fp32=True):
+        rp, ci, v = self._csr(rp, ci, v)
+        n = len(rp) - 1
+        asg = np.ascontiguousarray(assignment, np.int64)
+        vin = np.ascontiguousarray(vin, np.float64)
+        z = np.zeros(n)
+        self._chk(self.L.orc_apply(ctypes.c_int64(n), _p(rp, _i64p), _p(ci, _i64p), _p(v, _f64p),
+                                   ctypes.c_int64(s), _p(asg, _i64p), ctypes.c_double(eps),
+                                   ctypes.c_int(int(fp32)), _p(vin, _f64p), _p(z, _f64p)), "apply")
+        return z
+
+    def solve_full(self, rp, ci, v, s, assignment, b, m, tol, max_restarts, mode="hybrid", eps=1e-10):
+        rp, ci, v = self._csr(rp, ci, v)
+        n = len(rp) - 1
+        asg = np.ascontiguousarray(assignment, np.int64)
+        b = np.ascontiguousarray(b, np.float64)
+        x = np.zeros(n)
+        rep = PortReport()
+        hcap = m * max_restarts + 2
+        hist = np.zeros(3 * hcap)
+        cyc = np.zeros(max_restarts + 1)
+        self._chk(self.L.orc_solve(ctypes.c_int64(n), _p(rp, _i64p), _p(ci, _i64p), _p(v, _f64p),
+                                   ctypes.c_int64(s), _p(asg, _i64p), _p(b, _f64p), ctypes.c_int64(m),
+                                   ctypes.c_double(tol), ctypes.c_int64(max_restarts), ctypes.c_int(MODES[mode]),
+                                   ctypes.c_double(eps), _p(x, _f64p), ctypes.byref(rep), _p(hist, _f64p),
+                                   ctypes.c_int64(hcap), _p(cyc, _f64p), ctypes.c_int64(max_restarts + 1)),
+                  "solve")
+        hl, cl = rep.hist_len, rep.cyc_len
+        return SolveOut(x=x, converged=bool(rep.converged), total_iterations=rep.total_iterations,
+                        restarts=rep.restarts, final_residual=rep.final_residual, breakdown=bool(rep.breakdown),
+                        ls_rank_deficient=bool(rep.rank_deficient), history=hist[:3 * hl].reshape(hl, 3).copy(),
+                        cycle_residuals=cyc[:cl].copy())
+
+    def solve(self, sysm, assignment, mode="hybrid"):
+        """(iterations, x) of a workloads.System — smoke()'s fallback checker."""
+        out = self.solve_full(sysm.row_ptr, sysm.col, sysm.val, sysm.num_blocks, assignment, sysm.b,
+                              sysm.restart_m, sysm.tol, sysm.max_restarts, mode)
+        return out.total_iterations, out.x

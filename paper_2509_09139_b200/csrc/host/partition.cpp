@@ -197,7 +197,40 @@ void partition_from_assignment(int64_t n, const int64_t* assignment, int64_t s, 
     for (int64_t i = 0; i < n; ++i) perm[i] = next[assignment[i]]++;  // stable gather
 }
 
-void partition_adjacency(const Adjacency& g, int64_t s, double tol, int64_t* assignment) {
+namespace {
+
+// Reusable host workspace (repeated setups — e.g. the transient Newton
+// sequence — never page-fault fresh buffers).
+struct PartWork {
+    std::vector<double> wk;
+    std::vector<int64_t> deg;
+    std::vector<int32_t> state;
+    std::vector<int32_t> queue;
+    std::vector<int32_t> order;
+    std::vector<int64_t> dstart;
+    std::vector<int64_t> sizes;
+    std::vector<double> conn;
+};
+thread_local PartWork t_work;
+
+template <class T>
+void fit(std::vector<T>& v, size_t n) {
+    if (v.size() < n) v.resize(n);
+}
+
+// Graph view: neighbours of u are idx[st[u] .. st[u+1]) whose weight w[k] is
+// kept by the reference rule !(w <= 0) (graph.cpp:41); deg[u] counts them.
+template <class Idx>
+struct GraphView {
+    int64_t n;
+    const int64_t* st;
+    const Idx* idx;
+    const double* w;
+    const int64_t* deg;
+};
+
+template <class Idx>
+void partition_view(const GraphView<Idx>& g, int64_t s, double tol, int64_t* assignment) {
     const int64_t n = g.n;
     if (s < 1) fail(HPBJ_EINVAL, "partition_graph: s must be >= 1");
     if (s > n) fail(HPBJ_EINVAL, "partition_graph: s exceeds node count");
@@ -209,32 +242,43 @@ void partition_adjacency(const Adjacency& g, int64_t s, double tol, int64_t* ass
         static_cast<int64_t>(std::ceil(static_cast<double>(n) / s * (1.0 + tol))),
         (n + s - 1) / s);
 
-    const int64_t* st = g.start.data();
-    const int32_t* nb = g.nbr.data();
-    auto deg = [&](int64_t v) { return st[v + 1] - st[v]; };
+    PartWork& W = t_work;
+    const int64_t* st = g.st;
+    const Idx* nb = g.idx;
+    const double* w = g.w;
+    const int64_t* deg = g.deg;
+    auto kept = [&](int64_t k) { return !(w[k] <= 0.0); };
 
     // per-node state: >= 0 block id, -1 unassigned, -2 unassigned and queued
     constexpr int32_t kFree = -1, kQueued = -2;
-    std::vector<int32_t> state(n, kFree);
-    std::vector<int64_t> sizes(s, 0);
+    fit(W.state, n);
+    int32_t* state = W.state.data();
+    std::fill(state, state + n, kFree);
+    fit(W.sizes, s);
+    int64_t* sizes = W.sizes.data();
+    std::fill(sizes, sizes + s, int64_t(0));
 
     // Seed order: degree desc, index asc (counting sort on degree).
     int64_t maxdeg = 0, connected = 0;
     for (int64_t v = 0; v < n; ++v) {
-        maxdeg = std::max(maxdeg, deg(v));
-        if (deg(v) > 0) ++connected;
+        maxdeg = std::max(maxdeg, deg[v]);
+        if (deg[v] > 0) ++connected;
     }
-    std::vector<int64_t> dstart(maxdeg + 2, 0);
+    fit(W.dstart, maxdeg + 2);
+    int64_t* dstart = W.dstart.data();
+    std::fill(dstart, dstart + maxdeg + 2, int64_t(0));
     for (int64_t v = 0; v < n; ++v)
-        if (deg(v) > 0) ++dstart[maxdeg - deg(v) + 1];
+        if (deg[v] > 0) ++dstart[maxdeg - deg[v] + 1];
     for (int64_t d = 0; d <= maxdeg; ++d) dstart[d + 1] += dstart[d];
-    std::vector<int32_t> order(connected);
+    fit(W.order, connected + 1);
+    int32_t* order = W.order.data();
     for (int64_t v = 0; v < n; ++v)
-        if (deg(v) > 0) order[dstart[maxdeg - deg(v)]++] = (int32_t)v;
+        if (deg[v] > 0) order[dstart[maxdeg - deg[v]]++] = (int32_t)v;
     int64_t cursor = 0;
 
     // Region growing (partition.cpp:74-103).
-    std::vector<int32_t> queue(static_cast<size_t>(n) + 1);
+    fit(W.queue, n + 1);
+    int32_t* queue = W.queue.data();
     int64_t connected_left = connected;
     constexpr int kAhead = 6;
     for (int64_t b = 0; b < s && connected_left > 0; ++b) {
@@ -253,7 +297,7 @@ void partition_adjacency(const Adjacency& g, int64_t s, double tol, int64_t* ass
             }
             if (head + kAhead < tail) {  // prefetch the neighbourhood of a node popped soon
                 const int32_t f = queue[head + kAhead];
-                const int32_t* p = nb + st[f];
+                const Idx* p = nb + st[f];
                 const int64_t dd = st[f + 1] - st[f];
                 for (int64_t q = 0; q < dd && q < 16; ++q) __builtin_prefetch(&state[p[q]], 1, 1);
                 if (head + 2 * kAhead < tail) __builtin_prefetch(nb + st[queue[head + 2 * kAhead]], 0, 1);
@@ -264,10 +308,10 @@ void partition_adjacency(const Adjacency& g, int64_t s, double tol, int64_t* ass
             ++grown;
             --connected_left;
             for (int64_t k = st[u]; k < st[u + 1]; ++k) {
-                const int32_t v = nb[k];
-                if (state[v] == kFree) {
+                const int64_t v = nb[k];
+                if (state[v] == kFree && kept(k)) {
                     state[v] = kQueued;
-                    queue[tail++] = v;
+                    queue[tail++] = (int32_t)v;
                 }
             }
         }
@@ -295,10 +339,11 @@ void partition_adjacency(const Adjacency& g, int64_t s, double tol, int64_t* ass
 
     const auto t_grow = std::chrono::steady_clock::now();
     // One boundary-refinement sweep (partition.cpp:117-141), verbatim order.
-    std::vector<double> conn(s, 0.0);
-    std::vector<int32_t> touched;
-    touched.reserve(64);
-    const double* w = g.w.data();
+    fit(W.conn, s);
+    double* conn = W.conn.data();
+    std::fill(conn, conn + s, 0.0);
+    int32_t touched[4096];
+    std::vector<int32_t> touched_big;
     constexpr int64_t kRefAhead = 8;
     for (int64_t u = 0; u < n; ++u) {
         if (u + kRefAhead < n) {
@@ -307,14 +352,22 @@ void partition_adjacency(const Adjacency& g, int64_t s, double tol, int64_t* ass
         }
         const int32_t bu = state[u];
         if (sizes[bu] <= 1) continue;
-        touched.clear();
+        const int64_t du = st[u + 1] - st[u];
+        int32_t* tch = touched;
+        if (du > 4096) {
+            touched_big.resize(du);
+            tch = touched_big.data();
+        }
+        int nt = 0;
         for (int64_t k = st[u]; k < st[u + 1]; ++k) {
+            if (!kept(k)) continue;
             const int32_t bv = state[nb[k]];
-            if (conn[bv] == 0.0) touched.push_back(bv);
+            if (conn[bv] == 0.0) tch[nt++] = bv;
             conn[bv] += w[k];
         }
         int32_t best = -1;
-        for (int32_t bv : touched) {
+        for (int t = 0; t < nt; ++t) {
+            const int32_t bv = tch[t];
             if (bv == bu || sizes[bv] + 1 > cap) continue;
             if (best < 0 || conn[bv] > conn[best] || (conn[bv] == conn[best] && bv < best)) best = bv;
         }
@@ -323,12 +376,64 @@ void partition_adjacency(const Adjacency& g, int64_t s, double tol, int64_t* ass
             --sizes[bu];
             ++sizes[best];
         }
-        for (int32_t bv : touched) conn[bv] = 0.0;
+        for (int t = 0; t < nt; ++t) conn[tch[t]] = 0.0;
     }
     for (int64_t v = 0; v < n; ++v) assignment[v] = state[v];
     if (getenv("HPBJ_DEBUG"))
         fprintf(stderr, "[hpbj]   refine %.1f ms\n",
                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_grow).count());
+}
+
+}  // namespace
+
+void partition_adjacency(const Adjacency& g, int64_t s, double tol, int64_t* assignment) {
+    std::vector<int64_t> deg(g.n);
+    for (int64_t v = 0; v < g.n; ++v) deg[v] = g.start[v + 1] - g.start[v];
+    GraphView<int32_t> view{g.n, g.start.data(), g.nbr.data(), g.w.data(), deg.data()};
+    partition_view(view, s, tol, assignment);
+}
+
+// graph_from_matrix + partition_graph without materialising the adjacency
+// when the pattern is structurally symmetric: the CSR itself is the graph,
+// with per-entry weights (diagonal / w <= 0 entries masked as -1).
+void partition_csr(int64_t n, const int64_t* rp, const int64_t* ci, const double* val, int64_t s, double tol,
+                   int64_t* assignment) {
+    const int64_t nnz = rp[n];
+    PartWork& W = t_work;
+    fit(W.wk, nnz);
+    fit(W.deg, n);
+    double* wk = W.wk.data();
+    int64_t* deg = W.deg.data();
+    int missing = 0;
+#pragma omp parallel for schedule(dynamic, 2048) reduction(| : missing)
+    for (int64_t u = 0; u < n; ++u) {
+        int64_t d = 0;
+        for (int64_t k = rp[u]; k < rp[u + 1]; ++k) {
+            const int64_t j = ci[k];
+            if (j == u) {
+                wk[k] = -1.0;
+                continue;
+            }
+            const int64_t* b = ci + rp[j];
+            const int64_t* e = ci + rp[j + 1];
+            const int64_t* it = std::lower_bound(b, e, u);
+            if (it == e || *it != u) {
+                missing = 1;
+                break;
+            }
+            const double wt = 0.5 * (std::fabs(val[k]) + std::fabs(val[it - ci]));
+            wk[k] = wt;
+            if (!(wt <= 0.0)) ++d;
+        }
+        deg[u] = d;
+    }
+    if (missing) {
+        const Adjacency g = graph_general(n, rp, ci, val);
+        partition_adjacency(g, s, tol, assignment);
+        return;
+    }
+    GraphView<int64_t> view{n, rp, ci, wk, deg};
+    partition_view(view, s, tol, assignment);
 }
 
 namespace {
@@ -367,9 +472,8 @@ int hpbj_partition_graph(int64_t n, const int64_t* row_ptr, const int64_t* col,
         check_csr(n, row_ptr, col, val);
         if (n >= INT32_MAX) fail(HPBJ_EINVAL, "partition_graph: n must be < 2^31");
         const auto t1 = now();
-        const Adjacency g = graph_from_csr(n, row_ptr, col, val);
         const auto t2 = now();
-        partition_adjacency(g, s, imbalance_tol, assignment);
+        partition_csr(n, row_ptr, col, val, s, imbalance_tol, assignment);
         const auto t3 = now();
         partition_from_assignment(n, assignment, s, perm, block_starts);
         const auto t4 = now();

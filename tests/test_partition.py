@@ -1,0 +1,217 @@
+"""Host partitioner (graph_from_matrix + partition_graph + partition_from_
+assignment, in libhpbj.so) vs the reference library and its known answers
+(test_graph_partition.cpp). CPU only: no kernel is launched."""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_2509_09139_b200 as hp
+from paper_2509_09139_b200.workloads import generate
+from tests import fixtures as fx
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def path_graph(n, w=1.0):
+    st = [0]
+    nb, ws = [], []
+    for i in range(n):
+        for j in (i - 1, i + 1):
+            if 0 <= j < n:
+                nb.append(j)
+                ws.append(w)
+        st.append(len(nb))
+    return hp.WeightedGraph(n, np.array(st, np.int64), np.array(nb, np.int64), np.array(ws))
+
+
+def edge_weight(g, u, v):
+    for k in range(g.start[u], g.start[u + 1]):
+        if g.neighbor[k] == v:
+            return g.weight[k]
+    return 0.0
+
+
+def cut_weight(g, part):
+    c = 0.0
+    for u in range(g.num_nodes):
+        for k in range(g.start[u], g.start[u + 1]):
+            v = g.neighbor[k]
+            if u < v and part.assignment[u] != part.assignment[v]:
+                c += g.weight[k]
+    return c
+
+
+# ---------------------------------------------------------------- graph
+def test_weight_averages_both_directions():
+    a = hp.SparseMatrix.from_triplets([0, 1, 0, 1], [0, 1, 1, 0], [1.0, 1.0, -4.0, 2.0], 2)
+    g = hp.graph_from_matrix(a)  # graph.cpp:17-51; test_graph_partition.cpp:55-60
+    assert edge_weight(g, 0, 1) == 3.0 and edge_weight(g, 1, 0) == 3.0
+
+
+def test_one_sided_entry_makes_an_edge():
+    a = hp.SparseMatrix.from_triplets([0, 1, 0], [0, 1, 1], [1.0, 1.0, 5.0], 2)
+    g = hp.graph_from_matrix(a)  # test_graph_partition.cpp:62-67
+    assert edge_weight(g, 0, 1) == 2.5 and edge_weight(g, 1, 0) == 2.5
+
+
+def test_tridiag_gives_path_graph():
+    g = hp.graph_from_matrix(fx.tridiag4())
+    assert g.num_nodes == 4 and g.num_edges() == 3
+    assert edge_weight(g, 0, 1) == 1.0 and edge_weight(g, 2, 3) == 1.0 and edge_weight(g, 0, 2) == 0.0
+
+
+def test_zero_valued_pairs_are_dropped():
+    a = hp.SparseMatrix.from_triplets([0, 0, 1, 1, 2, 2], [0, 1, 0, 1, 2, 1], [1.0, 0.0, 0.0, 1.0, 1.0, -1.0], 3)
+    g = hp.graph_from_matrix(a)  # graph.cpp:41 (w <= 0 skipped)
+    assert edge_weight(g, 0, 1) == 0.0 and g.degree(0) == 0
+    assert edge_weight(g, 1, 2) == 0.5
+
+
+@pytest.mark.parametrize("seed", [4, 9, 16])
+def test_graph_matches_reference(ref, seed):
+    a = fx.random_dd(30, 4, seed)  # unsymmetric pattern -> general (transpose) path
+    g = hp.graph_from_matrix(a)
+    st, nb, w = ref.graph(a.row_starts, a.col_indices, a.values)
+    assert np.array_equal(g.start, st) and np.array_equal(g.neighbor, nb) and np.array_equal(g.weight, w)
+
+
+@pytest.mark.parametrize("config", [0, 4])
+def test_graph_symmetric_fast_path_matches_reference(ref, config):
+    s = generate(config)
+    a = hp.SparseMatrix(s.n, s.row_ptr, s.col, s.val)
+    g = hp.graph_from_matrix(a)
+    st, nb, w = ref.graph(s.row_ptr, s.col, s.val)
+    assert np.array_equal(g.start, st) and np.array_equal(g.neighbor, nb)
+    assert np.array_equal(g.weight.view(np.uint64), w.view(np.uint64))  # bit-exact
+
+
+def test_graph_rejects_non_square_or_bad_csr():
+    with pytest.raises(ValueError):
+        hp.graph_from_matrix(hp.SparseMatrix(2, np.array([0, 1, 2]), np.array([0, 2]), np.array([1.0, 1.0])))
+    with pytest.raises(ValueError):  # columns not strictly increasing
+        hp.graph_from_matrix(hp.SparseMatrix(2, np.array([0, 2, 2]), np.array([1, 0]), np.array([1.0, 1.0])))
+
+
+# ---------------------------------------------------------------- partition
+def test_single_block_is_degenerate():
+    p = hp.partition_graph(path_graph(5), 1, 0.1)
+    assert list(p.assignment) == [0] * 5 and list(p.perm) == list(range(5))
+
+
+def test_four_node_path_splits_in_the_middle():
+    g = hp.graph_from_matrix(fx.tridiag4())  # test_graph_partition.cpp:116-123
+    p = hp.partition_graph(g, 2, 0.1)
+    a = p.assignment
+    assert a[0] == a[1] and a[2] == a[3] and a[0] != a[2]
+    assert cut_weight(g, p) == 1.0
+
+
+def test_six_node_path_matches_brute_force():
+    g = path_graph(6)
+    p = hp.partition_graph(g, 2, 0.1)
+    a = p.assignment
+    assert list(a) == [a[0]] * 3 + [a[3]] * 3 and a[0] != a[3] and cut_weight(g, p) == 1.0
+
+
+def test_isolated_nodes_go_to_smallest_blocks():
+    p = hp.partition_graph(hp.graph_from_matrix(fx.diag_csr([1, 2, 3, 4, 5, 6])), 3, 0.0)
+    assert [p.block_size(b) for b in range(3)] == [2, 2, 2]
+
+
+def test_s_equals_n_with_zero_tolerance():
+    p = hp.partition_graph(path_graph(5), 5, 0.0)
+    assert [p.block_size(b) for b in range(5)] == [1] * 5
+
+
+def test_rejects_bad_arguments():
+    g = path_graph(4)
+    for s, tol in [(5, 0.1), (0, 0.1), (2, -0.5)]:
+        with pytest.raises(ValueError):
+            hp.partition_graph(g, s, tol)
+
+
+@pytest.mark.parametrize("seed", [3, 7])
+@pytest.mark.parametrize("s", [2, 3, 5, 8])
+def test_partition_matches_reference_random(ref, seed, s):
+    a = fx.random_dd(40, 3, seed)  # test_graph_partition.cpp:137-163 cases
+    p = hp.partition_graph(a, s, 0.1)
+    asg, perm, bst, _ = ref.partition(a.row_starts, a.col_indices, a.values, s)
+    assert np.array_equal(p.assignment, asg) and np.array_equal(p.perm, perm)
+    assert np.array_equal(p.block_starts, bst)
+    q = hp.partition_graph(hp.graph_from_matrix(a), s, 0.1)  # explicit-graph entry point
+    assert np.array_equal(q.assignment, asg)
+
+
+@pytest.mark.parametrize("n,s", [(4, 2), (6, 2), (9, 2), (9, 4), (30, 7)])
+def test_partition_of_explicit_graph_matches_reference(ref, n, s):
+    g = path_graph(n, 0.5)
+    a = hp.partition_graph(g, s, 0.1)
+    r = ref.partition_graph(g.start, g.neighbor, g.weight, s, 0.1)
+    assert np.array_equal(a.assignment, r)
+
+
+def test_laplacian_and_mesh_fixtures_match_reference(ref):
+    for a, s in [(fx.laplacian_2d(32, 32), 16), (fx.laplacian_2d(16, 16), 8), (fx.laplacian_2d(8, 8), 4),
+                 (fx.convection_diffusion_2d(10, 10, 2.0, 1.0), 4), (fx.random_dd(80, 4, 55), 4)]:
+        p = hp.partition_graph(a, s, 0.1)
+        asg, _, _, _ = ref.partition(a.row_starts, a.col_indices, a.values, s)
+        assert np.array_equal(p.assignment, asg)
+
+
+def test_unsymmetric_pattern_with_hub_matches_reference(ref):
+    # one-sided couplings (structurally unsymmetric) + a dense hub row
+    rng = np.random.default_rng(5)
+    n = 300
+    t = [(i, i, 4.0) for i in range(n)]
+    t += [(i, (i + 1) % n, -1.0) for i in range(n)]
+    t += [(0, j, -0.01) for j in rng.choice(np.arange(1, n), 120, replace=False)]
+    t += [(int(i), int(j), float(v)) for i, j, v in zip(rng.integers(0, n, 200), rng.integers(0, n, 200),
+                                                        rng.uniform(-1, 1, 200)) if i != j]
+    r, c, v = zip(*t)
+    a = hp.SparseMatrix.from_triplets(r, c, v, n)
+    for s in (3, 10, 37):
+        p = hp.partition_graph(a, s, 0.1)
+        asg, perm, _, _ = ref.partition(a.row_starts, a.col_indices, a.values, s)
+        assert np.array_equal(p.assignment, asg) and np.array_equal(p.perm, perm)
+
+
+@pytest.mark.parametrize("config", [0, 1, 4, 2, 3])
+def test_config_partition_bit_identical_to_reference(config):
+    """Pinned by tests/golden/config<k>.json (reference partition run once:
+    config 3 took ~1000 s in the reference, O(n*s))."""
+    g = json.load(open(os.path.join(GOLD, f"config{config}.json")))
+    s = generate(config)
+    assert s.digest() == g["input_sha256"]
+    p = hp.partition_graph(hp.SparseMatrix(s.n, s.row_ptr, s.col, s.val), s.num_blocks, 0.1)
+    assert sha(p.assignment) == g["partition"]["assignment_sha256"]
+    assert sha(p.perm) == g["partition"]["perm_sha256"]
+    assert sha(p.block_starts) == g["partition"]["block_starts_sha256"]
+
+
+def test_partition_deterministic():
+    a = fx.random_dd(40, 3, 7)
+    assert np.array_equal(hp.partition_graph(a, 5).assignment, hp.partition_graph(a, 5).assignment)
+
+
+# ------------------------------------------------ partition_from_assignment
+def test_stable_gather():
+    p = hp.partition_from_assignment([1, 0, 1, 0], 2)  # test_graph_partition.cpp:212-216
+    assert list(p.perm) == [2, 0, 3, 1] and list(p.block_starts) == [0, 2, 4]
+    p = hp.partition_from_assignment([0, 0, 1, 1], 2)
+    assert list(p.perm) == [0, 1, 2, 3]
+
+
+def test_assignment_errors():
+    with pytest.raises(IndexError):
+        hp.partition_from_assignment([0, 0, 2, 1], 2)
+    with pytest.raises(ValueError):
+        hp.partition_from_assignment([0, 0, 0, 0], 2)
+    with pytest.raises(ValueError):
+        hp.partition_from_assignment([0, 0], 3)
