@@ -163,6 +163,19 @@ struct hpbj_ctx {
     int lu_smem_dim = 0, lu_scratch_ld = 0;
     std::vector<int> h_bstart;
     std::vector<int64_t> h_fac_off;
+    // sparse-panel (SPK) factors for the apply
+    int num_panels = 0;
+    int64_t spk_entries = 0, spk_diag = 0;
+    int* d_pstart = nullptr;
+    int* d_panel_block = nullptr;
+    int* d_ent_count = nullptr;
+    int* d_ent_off = nullptr;
+    int* d_scan_tmp = nullptr;
+    SpkPanel* d_desc = nullptr;
+    float* d_dtile = nullptr;
+    float* d_eval = nullptr;
+    uint16_t* d_ecol = nullptr;
+    uint8_t* d_erow = nullptr;
     SpmvPlan planB;
     int* d_long_sort = nullptr;
     int n_long_sort = 0, max_long_sort = 0;
@@ -219,6 +232,16 @@ struct hpbj_ctx {
         dfree(planB.long_rows);
         dfree(planB.ylong);
         dfree(d_long_sort);
+        dfree(d_pstart);
+        dfree(d_panel_block);
+        dfree(d_ent_count);
+        dfree(d_ent_off);
+        dfree(d_scan_tmp);
+        dfree(d_desc);
+        dfree(d_dtile);
+        dfree(d_eval);
+        dfree(d_ecol);
+        dfree(d_erow);
         has_pc = false;
     }
     void release_matrix() {
@@ -267,7 +290,10 @@ namespace {
 void make_plan(SpmvPlan& p, const std::vector<int64_t>& rp, const int* perm_or_null, int n) {
     p.n_long = 0;
     const double avg = n > 0 ? double(rp[n]) / n : 0.0;
-    p.group = avg <= 6.0 ? 4 : avg <= 12.0 ? 8 : avg <= 24.0 ? 16 : 32;
+    // measured on B200 (configs 1-3): one thread per row wins up to
+    // ~7.5 nnz/row (FP32 x gathers stay in L1/L2), then 2/4/8 lanes
+    p.group = avg <= 7.5 ? 1 : avg <= 16.0 ? 2 : avg <= 32.0 ? 4 : avg <= 64.0 ? 8 : 32;
+    if (const char* e = getenv("HPBJ_SPMV_G")) p.group = atoi(e);
     p.long_thresh = std::max(256, 16 * p.group);
     std::vector<int> rows;
     for (int i = 0; i < n; ++i)
@@ -318,8 +344,40 @@ void ensure_ws(hpbj_ctx* c, int m) {
     c->ws_m = m;
 }
 
-ApplyParams apply_params(const hpbj_ctx* c) {
-    return ApplyParams{c->s, c->d_bstart, c->d_fac_off, c->d_fac, c->d_piv, c->dmax};
+SpkView spk_view(const hpbj_ctx* c) {
+    return SpkView{c->s,      c->dmax,   c->d_bstart, c->d_pstart, c->d_piv, c->d_desc,
+                   c->d_dtile, c->d_eval, c->d_ecol,  c->d_erow,   c->d_ent_off};
+}
+
+// Repack the dense LU panels into the sparse-panel apply format.
+void build_spk(hpbj_ctx* c) {
+    cudaStream_t st = c->stream;
+    SpkBuild p{};
+    p.s = c->s;
+    p.num_panels = c->num_panels;
+    p.bstart = c->d_bstart;
+    p.pstart = c->d_pstart;
+    p.panel_block = c->d_panel_block;
+    p.fac_off = c->d_fac_off;
+    p.dense = c->d_fac;
+    p.ent_count = c->d_ent_count;
+    p.ent_off = c->d_ent_off;
+    launch_spk_count(p, st, &c->launches);
+    scan_exclusive(c->d_ent_count, c->d_ent_off, c->num_panels, c->d_scan_tmp, st, &c->launches);
+    int tot = 0;
+    HPBJ_CUDA(cudaMemcpyAsync(&tot, c->d_ent_off + c->num_panels, sizeof(int), cudaMemcpyDeviceToHost, st));
+    HPBJ_CUDA(cudaStreamSynchronize(st));
+    if (tot < 0) fail(HPBJ_EINVAL, "block_jacobi: factor nonzeros exceed 2^31");
+    c->spk_entries = tot;
+    dslot(c->d_eval, (size_t)tot + 32);
+    dslot(c->d_ecol, (size_t)tot + 32);
+    dslot(c->d_erow, (size_t)tot + 32);
+    p.desc = c->d_desc;
+    p.dtile = c->d_dtile;
+    p.eval = c->d_eval;
+    p.ecol = c->d_ecol;
+    p.erow = c->d_erow;
+    launch_spk_pack(p, st, &c->launches);
 }
 
 void factor(hpbj_ctx* c, hpbj_setup_info* info) {
@@ -349,6 +407,7 @@ void factor(hpbj_ctx* c, hpbj_setup_info* info) {
     HPBJ_CUDA(cudaEventRecord(e0, st));
     launch_gather_values(c->d_src, c->A.val, c->B.val, c->B.nnz, st, &c->launches);
     launch_block_lu(p, c->dmax, c->num_sms, st, &c->launches);
+    build_spk(c);
     HPBJ_CUDA(cudaEventRecord(e1, st));
     unsigned long long sing = 0;
     int pert_n = 0;
@@ -395,7 +454,7 @@ void enqueue_cycle_head(hpbj_ctx* c, cudaGraphConditionalHandle hin) {
 void enqueue_step(hpbj_ctx* c, cudaGraphConditionalHandle hin, int it) {
     KrylovBufs& kb = c->kb;
     record_kernel(c, 3 * it + 0, true);
-    launch_apply_step(apply_params(c), kb.V, kb.ldv, c->d_st, c->d_z32, c->stream, &c->launches);
+    launch_apply_step(spk_view(c), kb.V, kb.ldv, c->d_st, c->d_z32, c->stream, &c->launches);
     record_kernel(c, 3 * it + 0, false);
     record_kernel(c, 3 * it + 1, true);
     launch_spmv_f32x(c->B, c->planB, c->d_z32, kb.w, c->d_st, c->stream, &c->launches);
@@ -407,7 +466,7 @@ void enqueue_step(hpbj_ctx* c, cudaGraphConditionalHandle hin, int it) {
 void enqueue_cycle_tail(hpbj_ctx* c, cudaGraphConditionalHandle hout) {
     KrylovBufs& kb = c->kb;
     launch_solve_y(kb, c->d_st, c->stream, &c->launches);
-    launch_apply_update(apply_params(c), kb.V, kb.ldv, kb.y, c->d_st, c->d_xp, c->stream, &c->launches);
+    launch_apply_update(spk_view(c), kb.V, kb.ldv, kb.y, c->d_st, c->d_xp, c->stream, &c->launches);
     launch_residual(c->B, c->planB, c->d_xp, c->d_bp, c->d_r, c->d_st, c->d_red, c->stream, &c->launches);
     launch_cycle_end(kb, c->d_st, hout, c->stream, &c->launches);
 }
@@ -424,7 +483,8 @@ std::vector<uintptr_t> graph_signature(const hpbj_ctx* c) {
             (uintptr_t)c->B.val, (uintptr_t)c->B.n, (uintptr_t)c->B.nnz, (uintptr_t)p.group,
             (uintptr_t)p.long_thresh, (uintptr_t)p.n_long, (uintptr_t)p.long_rows, (uintptr_t)p.ylong,
             (uintptr_t)c->s, (uintptr_t)c->d_bstart, (uintptr_t)c->d_fac_off, (uintptr_t)c->d_fac,
-            (uintptr_t)c->d_piv, (uintptr_t)c->dmax, (uintptr_t)L.grid, (uintptr_t)L.threads, (uintptr_t)L.slice,
+            (uintptr_t)c->d_piv, (uintptr_t)c->dmax, (uintptr_t)c->d_pstart, (uintptr_t)c->d_desc,
+            (uintptr_t)c->d_dtile, (uintptr_t)c->d_eval, (uintptr_t)c->d_ecol, (uintptr_t)c->d_erow, (uintptr_t)L.grid, (uintptr_t)L.threads, (uintptr_t)L.slice,
             (uintptr_t)L.smem, (uintptr_t)L.icwy, (uintptr_t)L.w_in_smem};
 }
 
@@ -671,11 +731,12 @@ int hpbj_get_kernel_stats(hpbj_ctx* ctx, hpbj_kernel_stat* out) {
         const double n = ctx->A.n, nnz = ctx->A.nnz;
         double bytes_apply = 0.0;
         if (ctx->has_pc) {
-            bytes_apply = 4.0 * (double)ctx->fac_floats  // packed FP32 factor panels
-                          + 4.0 * n                      // pivot rows (int32)
-                          + 8.0 * n                      // v (FP64) in
-                          + 4.0 * n                      // z (FP32) out
-                          + 4.0 * (ctx->s + 1) + 8.0 * ctx->s;  // block starts + offsets
+            bytes_apply = 7.0 * (double)ctx->spk_entries          // off-panel value + col + row
+                          + (4.0 * 1024 + 16.0) * ctx->num_panels // diagonal tiles + panel descriptors
+                          + 4.0 * n                               // pivot rows (int32)
+                          + 8.0 * n                               // v (FP64) in
+                          + 4.0 * n                               // z (FP32) out
+                          + 8.0 * (ctx->s + 1);                   // block / panel starts
         }
         const double bytes_spmv = 12.0 * nnz + 4.0 * (n + 1) + 4.0 * n + 8.0 * n;
         for (int k = 0; k < HPBJ_K_COUNT; ++k) out[k] = ctx->stats[k];
@@ -792,6 +853,9 @@ int hpbj_bj_setup(hpbj_ctx* ctx, int64_t s, const int64_t* perm, const int64_t* 
             off += panel_floats(bst[b + 1] - bst[b]);
         }
         ctx->fac_floats = off;
+        std::vector<int> hps(s + 1, 0);
+        for (int64_t b = 0; b < s; ++b) hps[b + 1] = hps[b] + (bst[b + 1] - bst[b] + 31) / 32;
+        ctx->num_panels = hps[s];
         const int nnz = ctx->A.nnz;
         dslot(ctx->d_perm, n);
         ctx->B.n = n;
@@ -808,6 +872,15 @@ int hpbj_bj_setup(hpbj_ctx* ctx, int64_t s, const int64_t* perm, const int64_t* 
         dslot(ctx->d_pert, 4096);
         dslot(ctx->d_pert_n, 1);
         dslot(ctx->d_singular, 1);
+        const int np = ctx->num_panels;
+        dslot(ctx->d_pstart, s + 1);
+        dslot(ctx->d_panel_block, np);
+        dslot(ctx->d_ent_count, np);
+        dslot(ctx->d_ent_off, np + 1);
+        dslot(ctx->d_scan_tmp, 16384);
+        dslot(ctx->d_desc, np);
+        dslot(ctx->d_dtile, (size_t)np * 1024);
+        HPBJ_CUDA(cudaMemcpyAsync(ctx->d_pstart, hps.data(), sizeof(int) * (s + 1), cudaMemcpyHostToDevice, st));
         const size_t scr = block_lu_scratch_floats(dmax, ctx->num_sms, &ctx->lu_smem_dim, &ctx->lu_scratch_ld);
         if (scr) dslot(ctx->d_lu_scratch, scr);
         HPBJ_CUDA(cudaMemcpyAsync(ctx->d_perm, hperm.data(), sizeof(int) * n, cudaMemcpyHostToDevice, st));
@@ -877,7 +950,7 @@ int hpbj_bj_apply(hpbj_ctx* ctx, const double* v, double* z) {
         cudaStream_t st = ctx->stream;
         HPBJ_CUDA(cudaMemcpyAsync(ctx->d_tmpx, v, sizeof(double) * n, cudaMemcpyHostToDevice, st));
         launch_permute_vec(n, ctx->d_perm, ctx->d_tmpx, ctx->d_tmpy, false, st, &ctx->launches);
-        launch_apply_f32(apply_params(ctx), ctx->d_tmpy, nullptr, 0, nullptr, ctx->d_tmpx, st, &ctx->launches);
+        launch_apply_vec(spk_view(ctx), ctx->d_tmpy, ctx->d_tmpx, st, &ctx->launches);
         launch_permute_vec(n, ctx->d_perm, ctx->d_tmpx, ctx->d_tmpy, true, st, &ctx->launches);
         HPBJ_CUDA(cudaMemcpyAsync(z, ctx->d_tmpy, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
         HPBJ_CUDA(cudaStreamSynchronize(st));

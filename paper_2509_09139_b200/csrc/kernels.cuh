@@ -68,25 +68,60 @@ __host__ __device__ inline int64_t panel_floats(int d) {
 void launch_block_lu(const LuParams& p, int dmax, int num_sms, cudaStream_t st, int64_t* launches);
 size_t block_lu_scratch_floats(int dmax, int num_sms, int* smem_dim, int* scratch_ld);
 
-// ---- apply.cu -------------------------------------------------------------
-struct ApplyParams {
-    int s;
-    const int* bstart;
-    const int64_t* fac_off;
-    const float* fac;
-    const int* piv;
-    int dmax;
+// ---- spk.cu ---------------------------------------------------------------
+// Sparse-panel factor storage (see spk.cu): per 32-row panel, a row-sorted
+// coordinate list of the off-panel L then U entries and the dense 32x32
+// diagonal tile in a coalesced lane-quad layout.
+struct SpkPanel {
+    int off;   // first entry (L part); U part starts at off + nl
+    int nl;
+    int nu;
+    int doff;  // first compacted diagonal value
 };
 
-// z = M^-1 v (permuted space). FP32 arithmetic; v FP64 rounded on load.
-void launch_apply_f32(const ApplyParams& p, const double* v, const SolveState* st_or_null,
-                      int ldv, float* z32, double* z64, cudaStream_t st, int64_t* launches);
-// Arnoldi step: z32 = M^-1 V[:, st->j] (column resolved on the device).
-void launch_apply_step(const ApplyParams& p, const double* V, int ldv, const SolveState* sst, float* z32,
+struct SpkBuild {
+    int s;
+    int num_panels;
+    const int* bstart;
+    const int* pstart;      // s + 1: first panel of each block
+    int* panel_block;       // num_panels
+    const int64_t* fac_off;
+    const float* dense;     // dense panels from block_lu
+    int* ent_count;         // pass 1 outputs
+    int* diag_count;
+    const int* ent_off;     // exclusive scans of the counts
+    const int* diag_off;
+    SpkPanel* desc;         // pass 2 outputs
+    float* dtile;           // 1024 floats per panel: dense diagonal tile, [q][lane][4]
+    float* eval;
+    uint16_t* ecol;
+    uint8_t* erow;
+};
+
+struct SpkView {
+    int s;
+    int dmax;
+    const int* bstart;
+    const int* pstart;
+    const int* piv;
+    const SpkPanel* desc;
+    const float* dtile;
+    const float* eval;
+    const uint16_t* ecol;
+    const uint8_t* erow;
+    const int* ent_off;   // num_panels + 1 (prefetch ranges)
+};
+
+void launch_spk_count(const SpkBuild& p, cudaStream_t st, int64_t* launches);
+void launch_spk_pack(const SpkBuild& p, cudaStream_t st, int64_t* launches);
+// Arnoldi step: z32 = M^-1 V[:, st->j] (FP32 arithmetic, column resolved on the device).
+void launch_apply_step(const SpkView& v, const double* V, int ldv, const SolveState* sst, float* z32,
                        cudaStream_t st, int64_t* launches);
-// x += M^-1 (V y): fused basis combination, FP64 arithmetic on FP32 factors.
-void launch_apply_update(const ApplyParams& p, const double* V, int ldv, const double* y,
-                         const SolveState* sst, double* x, cudaStream_t st, int64_t* launches);
+// z = M^-1 v (Preconditioner::apply<float>), permuted frame.
+void launch_apply_vec(const SpkView& v, const double* vin, double* z64, cudaStream_t st, int64_t* launches);
+// x += M^-1 (V y): fused basis combination, FP64 arithmetic on the FP32 factors.
+void launch_apply_update(const SpkView& v, const double* V, int ldv, const double* y, const SolveState* sst,
+                         double* x, cudaStream_t st, int64_t* launches);
 
 // ---- spmv.cu --------------------------------------------------------------
 struct SpmvPlan {

@@ -144,6 +144,8 @@ void run(const DevCsr& a, const SpmvPlan& plan, const XT* x, double* y, const do
                                                             sst, partials);                         \
         break;
     switch (G) {
+        HPBJ_SPMV_CASE(1)
+        HPBJ_SPMV_CASE(2)
         HPBJ_SPMV_CASE(4)
         HPBJ_SPMV_CASE(8)
         HPBJ_SPMV_CASE(16)
