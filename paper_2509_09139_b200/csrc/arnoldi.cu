@@ -31,6 +31,7 @@
 // Hessenberg column, Givens rotation, residual estimate, cycle-exit flags
 // (SolveState) — no host round-trip per iteration.
 
+#include <cstdio>
 #include <cstdlib>
 #include <string>
 
@@ -38,6 +39,14 @@
 #include "kernels.cuh"
 
 namespace hpbj {
+
+__device__ unsigned long long g_icwy_t[2][16];
+#define ICWY_MARK(k)                                                                      \
+    if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1)) {           \
+        unsigned long long t_;                                                            \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                            \
+        atomicAdd(&g_icwy_t[blockIdx.x == 0 ? 0 : 1][k], t_);                             \
+    }
 
 namespace {
 
@@ -109,35 +118,57 @@ __device__ void finish_step(const OrthArgs& a, double2* w2, int r0, int nv2, int
             vn[e] = wv;
         }
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        double* Hj = a.kb.H + (size_t)j * (m + 1);
+    if (blockIdx.x != 0) return;
+    // CTA 0: the w slice is spent, reuse it as scratch for the rotation data
+    // (coalesced staging by warp 0, then one thread rotates out of smem).
+    __syncthreads();
+    if (threadIdx.x >= 32) return;
+    const int lane = threadIdx.x;
+    double* Hj = a.kb.H + (size_t)j * (m + 1);
+    double* Rj = a.kb.R + (size_t)j * (m + 1);
+    double* cs = a.kb.cs;
+    double* sn = a.kb.sn;
+    double* g = a.kb.g;
+    double* sR = reinterpret_cast<double*>(w2);  // j + 2
+    double* scs = sR + (j + 2);                  // j
+    double* ssn = scs + j;                       // j
+    for (int i = lane; i <= j; i += 32) sR[i] = __ldcg(Hj + i);
+    for (int i = lane; i < j; i += 32) {
+        scs[i] = __ldcg(cs + i);
+        ssn[i] = __ldcg(sn + i);
+    }
+    __syncwarp();
+    if (lane == 0) {
+        sR[j + 1] = hnext;
         Hj[j + 1] = hnext;
         // GivensLs::push_column (gmres.cpp:26-52)
-        double* Rj = a.kb.R + (size_t)j * (m + 1);
-        double* cs = a.kb.cs;
-        double* sn = a.kb.sn;
-        double* g = a.kb.g;
-        for (int i = 0; i <= j + 1; ++i) Rj[i] = Hj[i];
+        double ri = sR[0];
         for (int i = 0; i < j; ++i) {
-            const double t = cs[i] * Rj[i] + sn[i] * Rj[i + 1];
-            Rj[i + 1] = -sn[i] * Rj[i] + cs[i] * Rj[i + 1];
-            Rj[i] = t;
+            const double rn = sR[i + 1];
+            const double t = scs[i] * ri + ssn[i] * rn;
+            const double r2 = -ssn[i] * ri + scs[i] * rn;
+            sR[i] = t;
+            ri = r2;
         }
-        const double aa = Rj[j], bb = Rj[j + 1];
+        sR[j] = ri;
+        const double aa = sR[j], bb = sR[j + 1];
+        double c, sg;
         if (bb == 0.0) {
-            cs[j] = 1.0;
-            sn[j] = 0.0;
+            c = 1.0;
+            sg = 0.0;
         } else {
             const double hh = hypot(aa, bb);
-            cs[j] = aa / hh;
-            sn[j] = bb / hh;
+            c = aa / hh;
+            sg = bb / hh;
         }
-        Rj[j] = cs[j] * aa + sn[j] * bb;
-        Rj[j + 1] = 0.0;
-        if (Rj[j] == 0.0) st->rank_deficient = 1;
-        const double t = cs[j] * g[j] + sn[j] * g[j + 1];
-        g[j + 1] = -sn[j] * g[j] + cs[j] * g[j + 1];
-        g[j] = t;
+        cs[j] = c;
+        sn[j] = sg;
+        sR[j] = c * aa + sg * bb;
+        sR[j + 1] = 0.0;
+        if (sR[j] == 0.0) st->rank_deficient = 1;
+        const double gj = g[j], gj1 = g[j + 1];
+        g[j + 1] = -sg * gj + c * gj1;
+        g[j] = c * gj + sg * gj1;
         const double est = fabs(g[j + 1]);
         a.kb.est[j] = est;
         // cycle exits (gmres.cpp:137-146)
@@ -151,6 +182,8 @@ __device__ void finish_step(const OrthArgs& a, double2* w2, int r0, int nv2, int
         st->done = done;
         if (a.cond) cudaGraphSetConditional(a.cond, done ? 0u : 1u);
     }
+    __syncwarp();
+    for (int i = lane; i <= j + 1; i += 32) Rj[i] = sR[i];
 }
 
 // ---------------------------------------------------------------------------
@@ -315,6 +348,7 @@ __global__ void __launch_bounds__(kIcwyThreads, 1) k_icwy(OrthArgs a) {
     const double2* win = reinterpret_cast<const double2*>(a.kb.w + r0);
     const double* V = a.kb.V;
 
+    ICWY_MARK(0);
     // ---- stage w, ||w||^2
     double ss = 0.0;
     for (int e = tid; e < nv2; e += kIcwyThreads) {
@@ -327,6 +361,7 @@ __global__ void __launch_bounds__(kIcwyThreads, 1) k_icwy(OrthArgs a) {
     if (lane == 0) wred[wid] = ss;
     __syncthreads();
 
+    ICWY_MARK(1);
     // ---- pass A: fused multi-dot  c_i = <v_i, w>,  l_i = <v_i, v_j>
     for (int i0 = 0; i0 <= j; i0 += kBatch) {
         const int nb = min(kBatch, j + 1 - i0);
@@ -364,38 +399,54 @@ __global__ void __launch_bounds__(kIcwyThreads, 1) k_icwy(OrthArgs a) {
         acc_sh[2 * (j + 1)] = s;
     }
     __syncthreads();
+    ICWY_MARK(2);
     for (int t = tid; t < nval; t += kIcwyThreads) P[(size_t)t * G + blockIdx.x] = acc_sh[t];
     grid_barrier(a.gb);
-    // grid totals, fixed CTA order (every CTA computes the same bits)
-    for (int t = tid; t < nval; t += kIcwyThreads) {
-        const double* p = P + (size_t)t * G;
-        double s = 0.0;
-        for (int b = 0; b < G; ++b) s += __ldcg(p + b);
-        tot[t] = s;
+    ICWY_MARK(3);
+    // grid totals: one warp per value, lane-strided over CTAs then a fixed
+    // xor tree (every CTA computes the same bits)
+    for (int t0 = wid; t0 < nval; t0 += 4 * kIcwyWarps) {
+        double part[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {  // all loads of four values in flight together
+            const int t = t0 + u * kIcwyWarps;
+            if (t < nval)
+                for (int b = lane; b < G; b += 32) part[u] += __ldcg(P + (size_t)t * G + b);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const double tv = warp_sum(part[u]);
+            const int t = t0 + u * kIcwyWarps;
+            if (lane == 0 && t < nval) tot[t] = tv;
+        }
     }
     __syncthreads();
     const double pre_norm = sqrt(tot[2 * (j + 1)]);
     const int ldl = m + 1;
-    // ---- h = (I + L)^-1 c, L_ik = <v_i, v_k> (k < i); row j is new
-    auto Lik = [&](int i, int k) -> double { return i == j ? tot[(j + 1) + k] : a.gram[(size_t)i * ldl + k]; };
-    for (int i = tid; i <= j; i += kIcwyThreads) {
-        double s = tot[i];
-        for (int k = 0; k < i; ++k) s = fma(-Lik(i, k), tot[k], s);
-        h1[i] = s;
-    }
-    __syncthreads();
-    for (int i = tid; i <= j; i += kIcwyThreads) {
-        double s = tot[i];
-        for (int k = 0; k < i; ++k) s = fma(-Lik(i, k), h1[k], s);
-        hsh[i] = s;
-    }
-    __syncthreads();
+    // ---- h = (I + L)^-1 c, L_ik = <v_i, v_k> (k < i); row j is new.
+    // Two Jacobi sweeps h <- c - L h (exact to O(|L|^3)); warp per row,
+    // lanes over k, fixed reduction order.
+    auto sweep = [&](const double* src, double* dst) {
+        for (int i = wid; i <= j; i += kIcwyWarps) {
+            const double* Lrow = (i == j) ? tot + (j + 1) : a.gram + (size_t)i * ldl;
+            double sacc = 0.0;
+            for (int k = lane; k < i; k += 32) sacc = fma(i == j ? Lrow[k] : __ldcg(Lrow + k), src[k], sacc);
+            sacc = warp_sum(sacc);
+            if (lane == 0) dst[i] = tot[i] - sacc;
+        }
+        __syncthreads();
+    };
+    ICWY_MARK(4);
+    sweep(tot, h1);
+    sweep(h1, hsh);
+    ICWY_MARK(5);
     if (blockIdx.x == 0) {
         for (int i = tid; i <= j; i += kIcwyThreads) a.kb.H[(size_t)j * (m + 1) + i] = hsh[i];
         for (int k = tid; k < j; k += kIcwyThreads) a.gram[(size_t)j * ldl + k] = tot[(j + 1) + k];
     }
 
     // ---- pass B: w -= sum_i h_i v_i in MGS order; ||w||^2
+    ICWY_MARK(6);
     double ss2 = 0.0;
     for (int e = tid; e < nv2; e += kIcwyThreads) {
         double2 wv = w2[e];
@@ -418,13 +469,16 @@ __global__ void __launch_bounds__(kIcwyThreads, 1) k_icwy(OrthArgs a) {
         for (int w = 0; w < kIcwyWarps; ++w) s += wred[w];
         P2[blockIdx.x] = s;
     }
+    ICWY_MARK(7);
     grid_barrier(a.gb);
+    ICWY_MARK(8);
     if (wid == 0) {
         const double t0 = sum_partials(P2, G);
         if (lane == 0) wred[0] = t0;
     }
     __syncthreads();
     finish_step(a, w2, r0, nv2, j, pre_norm, sqrt(wred[0]), kIcwyThreads);
+    ICWY_MARK(9);
 }
 
 // v_0 = r0 / beta (element-wise division, gmres.cpp:120-122); cycle state.
@@ -491,6 +545,16 @@ __global__ void k_solve_y(KrylovBufs kb, const SolveState* st) {
 
 }  // namespace
 
+void icwy_dump() {
+    unsigned long long h[2][16];
+    cudaMemcpyFromSymbol(h, g_icwy_t, sizeof(h));
+    for (int c = 0; c < 2; ++c) {
+        fprintf(stderr, "[icwy cta%s] ", c ? "last" : "0");
+        for (int k = 1; k < 10; ++k) fprintf(stderr, "%d:%.1f ", k, (double)(h[c][k] - h[c][k - 1]) / 1e3);
+        fprintf(stderr, " (us summed over launches)\n");
+    }
+}
+
 size_t orth_partials_doubles(int num_sms) { return (size_t)(2 * kMaxRestart + 8) * num_sms * 2; }
 
 MgsLaunch plan_mgs(int n, int num_sms, int m) {
@@ -504,7 +568,7 @@ MgsLaunch plan_mgs(int n, int num_sms, int m) {
     if (env && std::string(env) == "icwy" && m <= kMaxRestart) icwy = true;
     L.icwy = icwy;
     L.threads = icwy ? kIcwyThreads : kMgsThreads;
-    const int min_rows = icwy ? 2048 : 4096;
+    const int min_rows = icwy ? 1024 : 4096;
     int grid = std::max(1, std::min(num_sms, (npad + min_rows - 1) / min_rows));
     int slice = (npad + grid - 1) / grid;
     slice = (slice + 1) & ~1;

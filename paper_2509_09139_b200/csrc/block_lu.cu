@@ -56,6 +56,7 @@ __global__ void __launch_bounds__(kLuThreads) k_block_lu(LuParams p, int mode) {
     for (int b = blockIdx.x; b < p.s; b += gridDim.x) {
         const int o = p.bstart[b];
         const int d = p.bstart[b + 1] - o;
+        if (d <= p.warp_dim) continue;  // warp-per-block kernel
         const bool in_smem = d <= p.smem_dim;
         if ((mode == 0) != in_smem) continue;
         const int ld = d | 1;  // odd stride: conflict-free column walks
@@ -69,22 +70,21 @@ __global__ void __launch_bounds__(kLuThreads) k_block_lu(LuParams p, int mode) {
         // sum runs sequentially in column order like matrix_inf_norm, so the
         // FP64 norm is bit-identical to the reference's.
         double wmax = 0.0;
-        for (int r = wid; r < d; r += NW) {
-            const int gr = o + r;
-            const int kb = p.a.rp[gr], ke = p.a.rp[gr + 1];
-            for (int k = kb + lane; k < ke; k += 32) {
-                const int c = p.a.ci[k] - o;
-                if (c >= 0 && c < d) A[r * ld + c] = __double2float_rn(p.a.val[k]);
-            }
-            if (lane == 0) {
-                double rs = 0.0;
-                for (int k = kb; k < ke; ++k) {
-                    const int c = p.a.ci[k] - o;
-                    if (c >= 0 && c < d) rs = __dadd_rn(rs, fabs(p.a.val[k]));
+        for (int r = tid; r < d; r += kLuThreads) {  // thread per row
+            const int kb = __ldg(p.a.rp + o + r), ke = __ldg(p.a.rp + o + r + 1);
+            double rs = 0.0;
+            for (int k = kb; k < ke; ++k) {
+                const int c = __ldg(p.a.ci + k) - o;
+                if (c >= 0 && c < d) {
+                    const double v = __ldg(p.a.val + k);
+                    A[r * ld + c] = __double2float_rn(v);
+                    rs = __dadd_rn(rs, fabs(v));
                 }
-                wmax = fmax(wmax, rs);
             }
+            wmax = fmax(wmax, rs);
         }
+#pragma unroll
+        for (int o2 = 16; o2 > 0; o2 >>= 1) wmax = fmax(wmax, __shfl_xor_sync(0xffffffffu, wmax, o2));
         if (lane == 0) redd[wid] = wmax;
         if (tid == 0) sh_abort = 0;
         __syncthreads();
@@ -177,6 +177,140 @@ __global__ void __launch_bounds__(kLuThreads) k_block_lu(LuParams p, int mode) {
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Warp-per-block LU for blocks that fit a per-warp shared-memory tile
+// (d <= kWarpLuMax): warp-synchronous right-looking elimination — lane l owns
+// rows l, l+32, ... — so no CTA barrier sits on the per-column critical path.
+// Same pivot rule, regularisation and output as k_block_lu.
+constexpr int kWarpLuMax = 96;  // measured: above this the CTA kernel is faster
+
+template <int kWarpLuRowsPerLane>  // rows per lane = ceil(max block dim / 32)
+__global__ void __launch_bounds__(256) k_block_lu_warp(LuParams p, int dw, int ldw) {
+    extern __shared__ float wsm[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int nwc = blockDim.x >> 5;
+    float* A = wsm + (size_t)wid * (dw * ldw + dw);  // tile + prow
+    int* prow = reinterpret_cast<int*>(A + dw * ldw);
+    const int gw = blockIdx.x * nwc + wid, nw = gridDim.x * nwc;
+    for (int b = gw; b < p.s; b += nw) {
+        const int o = p.bstart[b];
+        const int d = p.bstart[b + 1] - o;
+        if (d > dw) continue;
+        const int ld = d | 1;
+        for (int e = lane; e < d * ld; e += 32) A[e] = 0.0f;
+        __syncwarp();
+        // gather + FP64 inf-norm (row sums sequential in column order, as
+        // matrix_inf_norm sparse_matrix.cpp:155-166)
+        double nrm = 0.0;
+        for (int r = lane; r < d; r += 32) {  // lane per row: all rows' loads in flight
+            const int kb = __ldg(p.a.rp + o + r), ke = __ldg(p.a.rp + o + r + 1);
+            double rs = 0.0;
+            for (int k = kb; k < ke; ++k) {
+                const int c = __ldg(p.a.ci + k) - o;
+                if (c >= 0 && c < d) {
+                    const double v = __ldg(p.a.val + k);
+                    A[r * ld + c] = __double2float_rn(v);
+                    rs = __dadd_rn(rs, fabs(v));
+                }
+            }
+            nrm = fmax(nrm, rs);
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) nrm = fmax(nrm, __shfl_xor_sync(0xffffffffu, nrm, off));
+        __syncwarp();
+        unsigned pivoted = 0u;  // bit q: row lane + 32 q already pivotal
+        int nperturb = 0;
+        bool abort = false;
+        for (int k = 0; k < d; ++k) {
+            // pivot: max |a_rk| over unpivoted rows, ties -> smallest row
+            unsigned long long best = 0ull;
+#pragma unroll
+            for (int q = 0; q < kWarpLuRowsPerLane; ++q) {
+                const int r = lane + 32 * q;
+                if (r < d && !((pivoted >> q) & 1u)) {
+                    const float v = fabsf(A[r * ld + k]);
+                    const unsigned long long key = ((unsigned long long)(__float_as_uint(v) + 1u) << 32) |
+                                                   (unsigned long long)(0xFFFFu - (unsigned)r);
+                    best = umax64(best, key);
+                }
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) best = umax64(best, __shfl_xor_sync(0xffffffffu, best, off));
+            const int pr = (int)(0xFFFFu - (unsigned)(best & 0xFFFFu));
+            const float xp = A[pr * ld + k];
+            // regularize_pivot (lu.cpp:10-20), FP64, identical in every lane
+            const double pvd = (double)xp;
+            const bool keep = nrm == 0.0 ? (pvd != 0.0) : (fabs(pvd) / nrm >= p.eps);
+            const double val = keep ? pvd : ((pvd < 0.0 ? -1.0 : 1.0) * p.eps * nrm);
+            if (val == 0.0) {
+                if (lane == 0) atomicMin(p.singular, ((unsigned long long)b << 32) | (unsigned)k);
+                abort = true;
+                break;
+            }
+            if (!keep) {
+                ++nperturb;
+                if (lane == 0) {
+                    const int slot = atomicAdd(p.pert_n, 1);
+                    if (slot < p.pert_cap) p.pert[slot] = PertRecord{b, k, pvd, val};
+                }
+            }
+            const float pv = (float)val;
+            __syncwarp();
+            if (lane == (pr & 31)) {
+                A[pr * ld + k] = pv;
+                pivoted |= 1u << (pr >> 5);
+                prow[k] = pr;
+            }
+            __syncwarp();
+            const float* urow = A + pr * ld;
+            float lq[kWarpLuRowsPerLane];
+#pragma unroll
+            for (int q = 0; q < kWarpLuRowsPerLane; ++q) {
+                const int r = lane + 32 * q;
+                lq[q] = 0.0f;
+                if (r < d && !((pivoted >> q) & 1u)) {
+                    lq[q] = A[r * ld + k] / pv;  // L(i,k) = x_i / pivot (lu.cpp:207)
+                    A[r * ld + k] = lq[q];
+                }
+            }
+            // rank-1 update, pivot-row value loaded once per column for all
+            // of the lane's rows; rows with l == 0 are left bit-unchanged
+            const int nq = (d - lane + 31) >> 5;  // rows owned by this lane
+#pragma unroll 2
+            for (int j = k + 1; j < d; ++j) {
+                const float u = urow[j];
+#pragma unroll
+                for (int q = 0; q < kWarpLuRowsPerLane; ++q)
+                    if (q < nq && lq[q] != 0.0f) {
+                        float* a = A + (lane + 32 * q) * ld + j;
+                        *a = fmaf(-lq[q], u, *a);
+                    }
+            }
+            __syncwarp();
+        }
+        if (lane == 0) p.pert_count[b] = nperturb;
+        if (!abort) {
+            const int T = (d + 31) / 32;
+            const int dp4 = (d + 3) & ~3;
+            const int total = T * 32 * dp4;
+            float* F = p.fac + p.fac_off[b];
+            for (int e = lane; e < total; e += 32) {
+                const int t = e / (32 * dp4);
+                const int rem = e - t * 32 * dp4;
+                const int c = ((rem >> 7) << 2) | (rem & 3);
+                const int k = 32 * t + ((rem >> 2) & 31);
+                float v;
+                if (k < d && c < d) v = A[prow[k] * ld + c];
+                else v = (k == c) ? 1.0f : 0.0f;
+                F[e] = v;
+            }
+            for (int k = lane; k < d; k += 32) p.piv[o + k] = prow[k];
+        }
+        __syncwarp();
+    }
+}
+
 int lu_smem_dim(int dmax) {
     int d = 1;
     while (d + 1 <= dmax && (size_t)(d + 1) * ((d + 1) | 1) * sizeof(float) <= kLuSmemTile) ++d;
@@ -192,8 +326,37 @@ size_t block_lu_scratch_floats(int dmax, int num_sms, int* smem_dim, int* scratc
     return (size_t)num_sms * 4 * (*scratch_ld) * (*scratch_ld);
 }
 
-void launch_block_lu(const LuParams& p, int dmax, int num_sms, cudaStream_t st, int64_t* launches) {
+void launch_block_lu(const LuParams& p_in, int dmax, int num_sms, cudaStream_t st, int64_t* launches) {
     if (dmax > kLuMaxDim) fail(HPBJ_EINVAL, "block_jacobi: block dimension exceeds 2048");
+    LuParams p = p_in;
+    // blocks up to kWarpLuMax: one warp each, tile in shared memory
+    const int dw = std::min(dmax, kWarpLuMax);
+    p.warp_dim = dw;
+    {
+        const int ldw = dw | 1;
+        const size_t per_warp = ((size_t)dw * ldw + dw) * sizeof(float);
+        // few warps per CTA so several CTAs share an SM's shared memory
+        const int wpc = (int)std::max<size_t>(1, std::min<size_t>(2, (200 * 1024) / per_warp));
+        const size_t smem = per_warp * wpc;
+        void (*fn)(LuParams, int, int) = nullptr;
+        switch ((dw + 31) / 32) {
+            case 1: fn = k_block_lu_warp<1>; break;
+            case 2: fn = k_block_lu_warp<2>; break;
+            case 3: fn = k_block_lu_warp<3>; break;
+            default: fn = k_block_lu_warp<3>; break;
+        }
+        HPBJ_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int occ = 0;
+        HPBJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 32 * wpc, smem));
+        occ = std::max(occ, 1);
+        const int grid = std::max(1, std::min((p.s + wpc - 1) / wpc, num_sms * occ));
+        fn<<<grid, 32 * wpc, smem, st>>>(p, dw, ldw);
+        *launches += 1;
+    }
+    if (dmax <= dw) {
+        HPBJ_CUDA(cudaGetLastError());
+        return;
+    }
     const int sd = p.smem_dim;
     const int dsm = std::min(dmax, sd);
     const size_t smem = (size_t)dsm * (dsm | 1) * sizeof(float);

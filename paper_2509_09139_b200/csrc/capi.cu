@@ -19,6 +19,7 @@
 
 using namespace hpbj;
 
+namespace hpbj { void icwy_dump(); }
 namespace {
 
 // Device memory pool of one context: freed buffers are kept and reused by
@@ -680,6 +681,7 @@ void solve(hpbj_ctx* c, const double* d_b, double* d_x, const hpbj_gmres_opts* o
     R.cycles = clen;
     R.ms_solve = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     if (rep) *rep = R;
+    if (getenv("HPBJ_ICWY_DBG")) icwy_dump();
 }
 
 }  // namespace

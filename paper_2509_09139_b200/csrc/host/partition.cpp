@@ -210,6 +210,9 @@ struct PartWork {
     std::vector<int64_t> dstart;
     std::vector<int64_t> sizes;
     std::vector<double> conn;
+    std::vector<int64_t> adj_start;
+    std::vector<int32_t> adj_nbr;
+    std::vector<double> adj_w;
 };
 thread_local PartWork t_work;
 
@@ -276,6 +279,7 @@ void partition_view(const GraphView<Idx>& g, int64_t s, double tol, int64_t* ass
         if (deg[v] > 0) order[dstart[maxdeg - deg[v]]++] = (int32_t)v;
     int64_t cursor = 0;
 
+    const auto t_seed = std::chrono::steady_clock::now();
     // Region growing (partition.cpp:74-103).
     fit(W.queue, n + 1);
     int32_t* queue = W.queue.data();
@@ -338,6 +342,9 @@ void partition_view(const GraphView<Idx>& g, int64_t s, double tol, int64_t* ass
     }
 
     const auto t_grow = std::chrono::steady_clock::now();
+    if (getenv("HPBJ_DEBUG"))
+        fprintf(stderr, "[hpbj]   bfs+leftovers %.1f ms\n",
+                std::chrono::duration<double, std::milli>(t_grow - t_seed).count());
     // One boundary-refinement sweep (partition.cpp:117-141), verbatim order.
     fit(W.conn, s);
     double* conn = W.conn.data();
@@ -352,6 +359,15 @@ void partition_view(const GraphView<Idx>& g, int64_t s, double tol, int64_t* ass
         }
         const int32_t bu = state[u];
         if (sizes[bu] <= 1) continue;
+        // Interior fast path: with every kept neighbour in bu the reference
+        // touches only bu, which is never a candidate -> no move, no state
+        // change (identical outcome, no floating-point work).
+        {
+            int64_t k = st[u];
+            const int64_t ke = st[u + 1];
+            while (k < ke && (!kept(k) || state[nb[k]] == bu)) ++k;
+            if (k == ke) continue;
+        }
         const int64_t du = st[u + 1] - st[u];
         int32_t* tch = touched;
         if (du > 4096) {
@@ -399,6 +415,7 @@ void partition_adjacency(const Adjacency& g, int64_t s, double tol, int64_t* ass
 void partition_csr(int64_t n, const int64_t* rp, const int64_t* ci, const double* val, int64_t s, double tol,
                    int64_t* assignment) {
     const int64_t nnz = rp[n];
+    const auto t_w0 = std::chrono::steady_clock::now();
     PartWork& W = t_work;
     fit(W.wk, nnz);
     fit(W.deg, n);
@@ -432,7 +449,34 @@ void partition_csr(int64_t n, const int64_t* rp, const int64_t* ci, const double
         partition_adjacency(g, s, tol, assignment);
         return;
     }
-    GraphView<int64_t> view{n, rp, ci, wk, deg};
+    if (getenv("HPBJ_DEBUG"))
+        fprintf(stderr, "[hpbj]   weights %.1f ms\n",
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_w0).count());
+    const auto t_a0 = std::chrono::steady_clock::now();
+    // compact int32 adjacency (kept entries only): 4 B/neighbour for the
+    // sequential BFS instead of 16 B (int64 column + weight) per CSR entry
+    fit(W.adj_start, n + 1);
+    int64_t* ast = W.adj_start.data();
+    ast[0] = 0;
+    for (int64_t u = 0; u < n; ++u) ast[u + 1] = ast[u] + deg[u];
+    fit(W.adj_nbr, ast[n] + 1);
+    fit(W.adj_w, ast[n] + 1);
+    int32_t* anb = W.adj_nbr.data();
+    double* aw = W.adj_w.data();
+#pragma omp parallel for schedule(static, 4096)
+    for (int64_t u = 0; u < n; ++u) {
+        int64_t d = ast[u];
+        for (int64_t k = rp[u]; k < rp[u + 1]; ++k)
+            if (!(wk[k] <= 0.0)) {
+                anb[d] = (int32_t)ci[k];
+                aw[d] = wk[k];
+                ++d;
+            }
+    }
+    if (getenv("HPBJ_DEBUG"))
+        fprintf(stderr, "[hpbj]   adjacency %.1f ms\n",
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_a0).count());
+    GraphView<int32_t> view{n, ast, anb, aw, deg};
     partition_view(view, s, tol, assignment);
 }
 
