@@ -25,9 +25,9 @@ NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xc
               "-Xptxas", "-v", "-I" + INC, "-I" + CSRC] + ARCH
 CXX_FLAGS = ["-std=c++20", "-O3", "-fPIC", "-fopenmp", "-ffp-contract=off", "-I" + INC, "-I" + CSRC]
 
-CU_SOURCES = ["permute.cu", "block_lu.cu", "spk.cu", "spmv.cu", "arnoldi.cu", "capi.cu"]
+CU_SOURCES = ["permute.cu", "block_lu.cu", "spk.cu", "spmv.cu", "arnoldi.cu", "fused.cu", "capi.cu"]
 CPP_SOURCES = ["host/partition.cpp"]
-HEADERS = ["device.cuh", "kernels.cuh", "hpbj_common.hpp"]
+HEADERS = ["device.cuh", "kernels.cuh", "hpbj_common.hpp", "spk_dev.cuh", "sync_dev.cuh"]
 
 LIBHPBJ = os.path.join(LIB, "libhpbj.so")
 LIBGEN = os.path.join(LIB, "libhpbj_gen.so")

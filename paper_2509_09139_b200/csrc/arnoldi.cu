@@ -37,52 +37,18 @@
 
 #include "device.cuh"
 #include "kernels.cuh"
+#include "sync_dev.cuh"
 
 namespace hpbj {
 
-__device__ unsigned long long g_icwy_t[2][16];
-#define ICWY_MARK(k)                                                                      \
-    if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1)) {           \
-        unsigned long long t_;                                                            \
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                            \
-        atomicAdd(&g_icwy_t[blockIdx.x == 0 ? 0 : 1][k], t_);                             \
-    }
-
 namespace {
+
+using sync::grid_barrier;
+using sync::transpose_reduce;
 
 constexpr int kMgsThreads = 1024;
 constexpr int kIcwyThreads = 512;
 constexpr size_t kSmemMax = 227 * 1024;
-
-// ---------------------------------------------------------------------------
-// Sense-free generation barrier over all CTAs of a cooperative launch.
-__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
-    unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-__device__ __forceinline__ void grid_barrier(GridBarrier* gb) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const unsigned g = ld_acquire(&gb->gen);
-        __threadfence();
-        const unsigned prev = atomicAdd(&gb->count, 1u);
-        if (prev == gridDim.x - 1) {
-            gb->count = 0;
-            __threadfence();
-            st_release(&gb->gen, g + 1);
-        } else {
-            while (ld_acquire(&gb->gen) == g) {
-            }
-        }
-        __threadfence();
-    }
-    __syncthreads();
-}
 
 // Sum of partials[0..count) in a fixed order; every thread of warp 0 gets it.
 __device__ __forceinline__ double sum_partials(const double* p, int count) {
@@ -303,22 +269,6 @@ __global__ void __launch_bounds__(kMgsThreads, 1) k_mgs(OrthArgs a) {
 constexpr int kIcwyWarps = kIcwyThreads / 32;
 constexpr int kBatch = 16;  // basis vectors per multi-dot batch (32 dot products)
 
-// 32 per-lane accumulators -> lane l holds the warp total of slot l
-// (butterfly transpose-reduction: 31 shuffles for 32 dot products).
-__device__ __forceinline__ double transpose_reduce32(double (&v)[32], int lane) {
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) {
-#pragma unroll
-        for (int q = 0; q < off; ++q) {
-            const bool hi = (lane & off) != 0;
-            const double send = hi ? v[q] : v[q + off];
-            const double keep = hi ? v[q + off] : v[q];
-            v[q] = keep + __shfl_xor_sync(0xffffffffu, send, off);
-        }
-    }
-    return v[0];
-}
-
 template <bool SMEM>
 __global__ void __launch_bounds__(kIcwyThreads, 1) k_icwy(OrthArgs a) {
     SolveState* st = a.st;
@@ -348,7 +298,6 @@ __global__ void __launch_bounds__(kIcwyThreads, 1) k_icwy(OrthArgs a) {
     const double2* win = reinterpret_cast<const double2*>(a.kb.w + r0);
     const double* V = a.kb.V;
 
-    ICWY_MARK(0);
     // ---- stage w, ||w||^2
     double ss = 0.0;
     for (int e = tid; e < nv2; e += kIcwyThreads) {
@@ -361,7 +310,6 @@ __global__ void __launch_bounds__(kIcwyThreads, 1) k_icwy(OrthArgs a) {
     if (lane == 0) wred[wid] = ss;
     __syncthreads();
 
-    ICWY_MARK(1);
     // ---- pass A: fused multi-dot  c_i = <v_i, w>,  l_i = <v_i, v_j>
     for (int i0 = 0; i0 <= j; i0 += kBatch) {
         const int nb = min(kBatch, j + 1 - i0);
@@ -382,7 +330,7 @@ __global__ void __launch_bounds__(kIcwyThreads, 1) k_icwy(OrthArgs a) {
                 }
             }
         }
-        const double r = transpose_reduce32(acc, lane);
+        const double r = transpose_reduce<32>(acc, lane);
         red[wid][lane] = r;
         __syncthreads();
         if (tid < 2 * kBatch) {
@@ -399,10 +347,8 @@ __global__ void __launch_bounds__(kIcwyThreads, 1) k_icwy(OrthArgs a) {
         acc_sh[2 * (j + 1)] = s;
     }
     __syncthreads();
-    ICWY_MARK(2);
     for (int t = tid; t < nval; t += kIcwyThreads) P[(size_t)t * G + blockIdx.x] = acc_sh[t];
     grid_barrier(a.gb);
-    ICWY_MARK(3);
     // grid totals: one warp per value, lane-strided over CTAs then a fixed
     // xor tree (every CTA computes the same bits)
     for (int t0 = wid; t0 < nval; t0 += 4 * kIcwyWarps) {
@@ -436,17 +382,14 @@ __global__ void __launch_bounds__(kIcwyThreads, 1) k_icwy(OrthArgs a) {
         }
         __syncthreads();
     };
-    ICWY_MARK(4);
     sweep(tot, h1);
     sweep(h1, hsh);
-    ICWY_MARK(5);
     if (blockIdx.x == 0) {
         for (int i = tid; i <= j; i += kIcwyThreads) a.kb.H[(size_t)j * (m + 1) + i] = hsh[i];
         for (int k = tid; k < j; k += kIcwyThreads) a.gram[(size_t)j * ldl + k] = tot[(j + 1) + k];
     }
 
     // ---- pass B: w -= sum_i h_i v_i in MGS order; ||w||^2
-    ICWY_MARK(6);
     double ss2 = 0.0;
     for (int e = tid; e < nv2; e += kIcwyThreads) {
         double2 wv = w2[e];
@@ -469,16 +412,13 @@ __global__ void __launch_bounds__(kIcwyThreads, 1) k_icwy(OrthArgs a) {
         for (int w = 0; w < kIcwyWarps; ++w) s += wred[w];
         P2[blockIdx.x] = s;
     }
-    ICWY_MARK(7);
     grid_barrier(a.gb);
-    ICWY_MARK(8);
     if (wid == 0) {
         const double t0 = sum_partials(P2, G);
         if (lane == 0) wred[0] = t0;
     }
     __syncthreads();
     finish_step(a, w2, r0, nv2, j, pre_norm, sqrt(wred[0]), kIcwyThreads);
-    ICWY_MARK(9);
 }
 
 // v_0 = r0 / beta (element-wise division, gmres.cpp:120-122); cycle state.
@@ -503,21 +443,25 @@ __global__ void k_cycle_init(KrylovBufs kb, SolveState* st, const double* __rest
 }
 
 // Restart-driver bookkeeping (gmres.cpp:236-258) on the device: history rows
-// (cycle, ++iteration, est/||b||), cycle residual, exit test.
+// (cycle, ++iteration, est/||b||), cycle residual, exit test. One warp.
 __global__ void k_cycle_end(KrylovBufs kb, SolveState* st, cudaGraphConditionalHandle cond) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (blockIdx.x != 0) return;
     const int steps = st->j;
     const int cyc = st->cycles;
-    for (int k = 0; k < steps; ++k) {
-        kb.hist[st->hist_len + k] = kb.est[k] / st->bnorm;
-        kb.hist_cycle[st->hist_len + k] = cyc;
+    const int h0 = st->hist_len;
+    const double bnorm = st->bnorm;
+    for (int k = threadIdx.x; k < steps; k += blockDim.x) {
+        kb.hist[h0 + k] = kb.est[k] / bnorm;
+        kb.hist_cycle[h0 + k] = cyc;
     }
-    st->hist_len += steps;
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    st->hist_len = h0 + steps;
     st->total_iterations += steps;
     st->breakdown_any |= st->breakdown;
     st->rank_any |= st->rank_deficient;
     const double rnorm = st->rnorm;
-    kb.cycres[cyc] = rnorm / st->bnorm;
+    kb.cycres[cyc] = rnorm / bnorm;
     st->cycles = cyc + 1;
     st->last_steps = steps;
     const bool conv = rnorm <= st->thr;
@@ -526,34 +470,40 @@ __global__ void k_cycle_end(KrylovBufs kb, SolveState* st, cudaGraphConditionalH
     if (cond) cudaGraphSetConditional(cond, more ? 1u : 0u);
 }
 
-// y = R^-1 g with the zero-rotation convention (gmres.cpp:57-66).
-__global__ void k_solve_y(KrylovBufs kb, const SolveState* st) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+// y = R^-1 g with the zero-rotation convention (gmres.cpp:57-66), same
+// operation order as the reference. The triangle is staged in shared memory
+// by the whole CTA so the single-thread recurrence runs at smem latency.
+constexpr int kSolveYThreads = 256;
+constexpr int kSolveYStagedMax = 160;  // m^2 doubles of shared memory
+template <bool STAGED>
+__global__ void __launch_bounds__(kSolveYThreads) k_solve_y(KrylovBufs kb, const SolveState* st) {
+    extern __shared__ double rs[];  // steps x steps, rs[k * steps + i] = R(i, k)
+    __shared__ double ysh[1024];
     const int steps = st->j;
     const int ld = kb.m + 1;
+    if (STAGED) {
+        for (int t = threadIdx.x; t < steps * steps; t += kSolveYThreads) {
+            const int k = t / steps, i = t - k * steps;
+            rs[t] = kb.R[(size_t)k * ld + i];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x != 0) return;
+    auto R = [&](int i, int k) { return STAGED ? rs[k * steps + i] : kb.R[(size_t)k * ld + i]; };
     for (int i = steps - 1; i >= 0; --i) {
-        const double rii = kb.R[(size_t)i * ld + i];
+        const double rii = R(i, i);
         if (rii == 0.0) {
-            kb.y[i] = 0.0;
+            ysh[i] = 0.0;
             continue;
         }
         double s = kb.g[i];
-        for (int k = i + 1; k < steps; ++k) s -= kb.R[(size_t)k * ld + i] * kb.y[k];
-        kb.y[i] = s / rii;
+        for (int k = i + 1; k < steps; ++k) s -= R(i, k) * ysh[k];
+        ysh[i] = s / rii;
     }
+    for (int i = 0; i < steps; ++i) kb.y[i] = ysh[i];
 }
 
 }  // namespace
-
-void icwy_dump() {
-    unsigned long long h[2][16];
-    cudaMemcpyFromSymbol(h, g_icwy_t, sizeof(h));
-    for (int c = 0; c < 2; ++c) {
-        fprintf(stderr, "[icwy cta%s] ", c ? "last" : "0");
-        for (int k = 1; k < 10; ++k) fprintf(stderr, "%d:%.1f ", k, (double)(h[c][k] - h[c][k - 1]) / 1e3);
-        fprintf(stderr, " (us summed over launches)\n");
-    }
-}
 
 size_t orth_partials_doubles(int num_sms) { return (size_t)(2 * kMaxRestart + 8) * num_sms * 2; }
 
@@ -615,13 +565,20 @@ void launch_cycle_init(const KrylovBufs& kb, SolveState* sst, const double* r, i
 
 void launch_cycle_end(const KrylovBufs& kb, SolveState* sst, cudaGraphConditionalHandle cond, cudaStream_t st,
                       int64_t* launches) {
-    k_cycle_end<<<1, 32, 0, st>>>(kb, sst, cond);
+    k_cycle_end<<<1, 128, 0, st>>>(kb, sst, cond);
     *launches += 1;
     HPBJ_CUDA(cudaGetLastError());
 }
 
 void launch_solve_y(const KrylovBufs& kb, SolveState* sst, cudaStream_t st, int64_t* launches) {
-    k_solve_y<<<1, 32, 0, st>>>(kb, sst);
+    if (kb.m <= kSolveYStagedMax) {
+        const size_t smem = sizeof(double) * (size_t)kb.m * kb.m;
+        if (smem > 48 * 1024)
+            HPBJ_CUDA(cudaFuncSetAttribute(k_solve_y<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_solve_y<true><<<1, kSolveYThreads, smem, st>>>(kb, sst);
+    } else {
+        k_solve_y<false><<<1, kSolveYThreads, 0, st>>>(kb, sst);
+    }
     *launches += 1;
     HPBJ_CUDA(cudaGetLastError());
 }

@@ -19,7 +19,6 @@
 
 using namespace hpbj;
 
-namespace hpbj { void icwy_dump(); }
 namespace {
 
 // Device memory pool of one context: freed buffers are kept and reused by
@@ -175,8 +174,7 @@ struct hpbj_ctx {
     SpkPanel* d_desc = nullptr;
     float* d_dtile = nullptr;
     float* d_eval = nullptr;
-    uint16_t* d_ecol = nullptr;
-    uint8_t* d_erow = nullptr;
+    uint32_t* d_eidx = nullptr;  // packed (col << 5 | row), 16- or 32-bit
     SpmvPlan planB;
     int* d_long_sort = nullptr;
     int n_long_sort = 0, max_long_sort = 0;
@@ -190,6 +188,7 @@ struct hpbj_ctx {
     double* d_bp = nullptr;  // b (permuted)
     double* d_r = nullptr;
     double* d_red = nullptr;  // reduction partials
+    size_t red_cap = 0;
     double* d_bo = nullptr;   // host-API staging (original ordering)
     double* d_xo = nullptr;
     double* d_gram = nullptr;
@@ -197,6 +196,9 @@ struct hpbj_ctx {
     MgsLaunch mgs;
     int64_t hist_cap = 0;
     bool use_graph = true;
+    bool use_fused = true;
+    FusedPlan fused;  // per-solve: whole Arnoldi cycle in one kernel when ok
+    unsigned long long* d_fprof = nullptr;  // HPBJ_FUSED_PROF=1: phase timers of the fused kernel
     cudaGraphExec_t graph_exec = nullptr;
     int graph_builds = 0;
     std::vector<uintptr_t> graph_sig;
@@ -210,6 +212,7 @@ struct hpbj_ctx {
         t_pool = &pool;
         t_slots = &slots;
         if (graph_exec) cudaGraphExecDestroy(graph_exec);
+        if (d_fprof) cudaFree(d_fprof);
         release_matrix();
         release_ws();
         if (stream) cudaStreamDestroy(stream);
@@ -231,7 +234,6 @@ struct hpbj_ctx {
         dfree(d_singular);
         dfree(d_lu_scratch);
         dfree(planB.long_rows);
-        dfree(planB.ylong);
         dfree(d_long_sort);
         dfree(d_pstart);
         dfree(d_panel_block);
@@ -241,8 +243,7 @@ struct hpbj_ctx {
         dfree(d_desc);
         dfree(d_dtile);
         dfree(d_eval);
-        dfree(d_ecol);
-        dfree(d_erow);
+        dfree(d_eidx);
         has_pc = false;
     }
     void release_matrix() {
@@ -251,7 +252,6 @@ struct hpbj_ctx {
         dfree(A.ci);
         dfree(A.val);
         dfree(planA.long_rows);
-        dfree(planA.ylong);
         dfree(d_tmpx);
         dfree(d_tmpy);
         has_matrix = false;
@@ -304,7 +304,6 @@ void make_plan(SpmvPlan& p, const std::vector<int64_t>& rp, const int* perm_or_n
     if (p.n_long) {
         dslot(p.long_rows, rows.size());
         HPBJ_CUDA(cudaMemcpy(p.long_rows, rows.data(), sizeof(int) * rows.size(), cudaMemcpyHostToDevice));
-        dslot(p.ylong, n);
     }
 }
 
@@ -339,6 +338,7 @@ void ensure_ws(hpbj_ctx* c, int m) {
     dslot(c->d_bp, ldv);
     dslot(c->d_r, ldv);
     dslot(c->d_red, 2048);
+    c->red_cap = 2048;
     dslot(c->d_bo, ldv);
     dslot(c->d_xo, ldv);
     c->mgs = plan_mgs(n, c->num_sms, m);
@@ -347,7 +347,7 @@ void ensure_ws(hpbj_ctx* c, int m) {
 
 SpkView spk_view(const hpbj_ctx* c) {
     return SpkView{c->s,      c->dmax,   c->d_bstart, c->d_pstart, c->d_piv, c->d_desc,
-                   c->d_dtile, c->d_eval, c->d_ecol,  c->d_erow,   c->d_ent_off};
+                   c->d_dtile, c->d_eval, c->d_eidx,  c->dmax > kIdx16MaxDim ? 1 : 0, c->d_ent_off};
 }
 
 // Repack the dense LU panels into the sparse-panel apply format.
@@ -370,14 +370,14 @@ void build_spk(hpbj_ctx* c) {
     HPBJ_CUDA(cudaStreamSynchronize(st));
     if (tot < 0) fail(HPBJ_EINVAL, "block_jacobi: factor nonzeros exceed 2^31");
     c->spk_entries = tot;
-    dslot(c->d_eval, (size_t)tot + 32);
-    dslot(c->d_ecol, (size_t)tot + 32);
-    dslot(c->d_erow, (size_t)tot + 32);
+    const bool idx32 = c->dmax > kIdx16MaxDim;
+    dslot(c->d_eval, (size_t)tot + 32);  // parts are 4-entry aligned
+    dslot(c->d_eidx, idx32 ? (size_t)tot + 32 : (size_t)tot / 2 + 16);
     p.desc = c->d_desc;
     p.dtile = c->d_dtile;
     p.eval = c->d_eval;
-    p.ecol = c->d_ecol;
-    p.erow = c->d_erow;
+    p.eidx = c->d_eidx;
+    p.idx32 = idx32 ? 1 : 0;
     launch_spk_pack(p, st, &c->launches);
 }
 
@@ -464,6 +464,11 @@ void enqueue_step(hpbj_ctx* c, cudaGraphConditionalHandle hin, int it) {
     launch_mgs(c->mgs, kb, c->d_gram, c->d_gb, c->d_st, c->A.n, hin, c->stream, &c->launches);
     record_kernel(c, 3 * it + 2, false);
 }
+// The fused path: the whole Arnoldi loop of a cycle is one cooperative kernel.
+void enqueue_cycle_fused(hpbj_ctx* c) {
+    launch_arnoldi_cycle(c->fused, spk_view(c), c->B, c->planB, c->kb, c->d_gram, c->d_st, c->d_gb, c->d_z32,
+                         c->d_fprof, c->stream, &c->launches);
+}
 void enqueue_cycle_tail(hpbj_ctx* c, cudaGraphConditionalHandle hout) {
     KrylovBufs& kb = c->kb;
     launch_solve_y(kb, c->d_st, c->stream, &c->launches);
@@ -482,16 +487,19 @@ std::vector<uintptr_t> graph_signature(const hpbj_ctx* c) {
             (uintptr_t)c->d_st, (uintptr_t)c->d_z32, (uintptr_t)c->d_xp, (uintptr_t)c->d_bp, (uintptr_t)c->d_r,
             (uintptr_t)c->d_red, (uintptr_t)c->d_gram, (uintptr_t)c->d_gb, (uintptr_t)c->B.rp, (uintptr_t)c->B.ci,
             (uintptr_t)c->B.val, (uintptr_t)c->B.n, (uintptr_t)c->B.nnz, (uintptr_t)p.group,
-            (uintptr_t)p.long_thresh, (uintptr_t)p.n_long, (uintptr_t)p.long_rows, (uintptr_t)p.ylong,
+            (uintptr_t)p.long_thresh, (uintptr_t)p.n_long, (uintptr_t)p.long_rows,
             (uintptr_t)c->s, (uintptr_t)c->d_bstart, (uintptr_t)c->d_fac_off, (uintptr_t)c->d_fac,
             (uintptr_t)c->d_piv, (uintptr_t)c->dmax, (uintptr_t)c->d_pstart, (uintptr_t)c->d_desc,
-            (uintptr_t)c->d_dtile, (uintptr_t)c->d_eval, (uintptr_t)c->d_ecol, (uintptr_t)c->d_erow, (uintptr_t)L.grid, (uintptr_t)L.threads, (uintptr_t)L.slice,
-            (uintptr_t)L.smem, (uintptr_t)L.icwy, (uintptr_t)L.w_in_smem};
+            (uintptr_t)c->d_dtile, (uintptr_t)c->d_eval, (uintptr_t)c->d_eidx, (uintptr_t)L.grid, (uintptr_t)L.threads, (uintptr_t)L.slice,
+            (uintptr_t)L.smem, (uintptr_t)L.icwy, (uintptr_t)L.w_in_smem, (uintptr_t)c->fused.ok,
+            (uintptr_t)c->fused.grid, (uintptr_t)c->fused.slice, (uintptr_t)c->fused.ystride,
+            (uintptr_t)c->fused.smem, (uintptr_t)c->d_ent_off};
 }
 
 // The whole restart loop as one CUDA graph: WHILE(cycles) { cycle_init;
 // WHILE(steps) { apply; spmv; orth }; solve_y; x += M^-1 V y; residual;
-// bookkeeping }. Rebuilt only when a buffer or launch shape changes.
+// bookkeeping }, the inner loop being one fused kernel when it fits
+// (fused.cu). Rebuilt only when a buffer or launch shape changes.
 void ensure_graph(hpbj_ctx* c) {
     std::vector<uintptr_t> sig = graph_signature(c);
     if (c->graph_exec && sig == c->graph_sig) return;
@@ -512,32 +520,39 @@ void ensure_graph(hpbj_ctx* c) {
     cudaGraphNode_t onode;
     HPBJ_CUDA(cudaGraphAddNode(&onode, g, nullptr, 0, &op));
     cudaGraph_t body = op.conditional.phGraph_out[0];
-    cudaGraphConditionalHandle hin;
-    HPBJ_CUDA(cudaGraphConditionalHandleCreate(&hin, body, 0, 0));
+    if (c->fused.ok) {
+        // WHILE(cycles) { cycle_init; arnoldi_cycle; solve_y; update; residual; bookkeeping }
+        HPBJ_CUDA(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+        enqueue_cycle_head(c, 0);
+        enqueue_cycle_fused(c);
+        enqueue_cycle_tail(c, hout);
+        HPBJ_CUDA(cudaStreamEndCapture(st, &body));
+    } else {
+        cudaGraphConditionalHandle hin;
+        HPBJ_CUDA(cudaGraphConditionalHandleCreate(&hin, body, 0, 0));
+        HPBJ_CUDA(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+        enqueue_cycle_head(c, hin);
+        cudaStreamCaptureStatus cstat;
+        cudaGraph_t capg;
+        const cudaGraphNode_t* deps = nullptr;
+        size_t ndeps = 0;
+        HPBJ_CUDA(cudaStreamGetCaptureInfo(st, &cstat, nullptr, &capg, &deps, &ndeps));
+        cudaGraphNodeParams ip = {};
+        ip.type = cudaGraphNodeTypeConditional;
+        ip.conditional.handle = hin;
+        ip.conditional.type = cudaGraphCondTypeWhile;
+        ip.conditional.size = 1;
+        cudaGraphNode_t inode;
+        HPBJ_CUDA(cudaGraphAddNode(&inode, capg, deps, ndeps, &ip));
+        cudaGraph_t ibody = ip.conditional.phGraph_out[0];
+        HPBJ_CUDA(cudaStreamUpdateCaptureDependencies(st, &inode, 1, cudaStreamSetCaptureDependencies));
+        enqueue_cycle_tail(c, hout);
+        HPBJ_CUDA(cudaStreamEndCapture(st, &body));
 
-    HPBJ_CUDA(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-    enqueue_cycle_head(c, hin);
-    cudaStreamCaptureStatus cstat;
-    cudaGraph_t capg;
-    const cudaGraphNode_t* deps = nullptr;
-    size_t ndeps = 0;
-    HPBJ_CUDA(cudaStreamGetCaptureInfo(st, &cstat, nullptr, &capg, &deps, &ndeps));
-    cudaGraphNodeParams ip = {};
-    ip.type = cudaGraphNodeTypeConditional;
-    ip.conditional.handle = hin;
-    ip.conditional.type = cudaGraphCondTypeWhile;
-    ip.conditional.size = 1;
-    cudaGraphNode_t inode;
-    HPBJ_CUDA(cudaGraphAddNode(&inode, capg, deps, ndeps, &ip));
-    cudaGraph_t ibody = ip.conditional.phGraph_out[0];
-    HPBJ_CUDA(cudaStreamUpdateCaptureDependencies(st, &inode, 1, cudaStreamSetCaptureDependencies));
-    enqueue_cycle_tail(c, hout);
-    HPBJ_CUDA(cudaStreamEndCapture(st, &body));
-
-    HPBJ_CUDA(cudaStreamBeginCaptureToGraph(st, ibody, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-    enqueue_step(c, hin, 0);
-    HPBJ_CUDA(cudaStreamEndCapture(st, &ibody));
-
+        HPBJ_CUDA(cudaStreamBeginCaptureToGraph(st, ibody, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+        enqueue_step(c, hin, 0);
+        HPBJ_CUDA(cudaStreamEndCapture(st, &ibody));
+    }
     HPBJ_CUDA(cudaGraphInstantiate(&c->graph_exec, g, 0));
     HPBJ_CUDA(cudaGraphDestroy(g));
     c->graph_sig = sig;
@@ -573,6 +588,14 @@ void solve(hpbj_ctx* c, const double* d_b, double* d_x, const hpbj_gmres_opts* o
     const int m = (int)opt.restart_m;
     const double floor_u = opt.floor_roundoff > 0.0 ? opt.floor_roundoff : kU24;
     ensure_ws(c, m);
+    {  // residual partials: one per SpMV CTA incl. one per hub row
+        const size_t need = 1184 + 64 + (size_t)c->planB.n_long;
+        if (need > c->red_cap) {
+            dfree(c->d_red);
+            dslot(c->d_red, need);
+            c->red_cap = need;
+        }
+    }
     ensure_hist(c, opt.max_restarts);
     cudaStream_t st = c->stream;
     KrylovBufs& kb = c->kb;
@@ -624,15 +647,33 @@ void solve(hpbj_ctx* c, const double* d_b, double* d_x, const hpbj_gmres_opts* o
         R.converged = 1;
     } else {
         const bool use_graph = !c->profiling && c->use_graph;
+        // per-kernel events need the unfused kernels
+        c->fused = (c->use_fused && !c->profiling)
+                       ? plan_fused(n, c->s, c->dmax, c->num_sms, m, c->planB.n_long > 0)
+                       : FusedPlan{};
+        if (c->fused.ok && getenv("HPBJ_FUSED_PROF") && !c->d_fprof) {
+            HPBJ_CUDA(cudaMalloc(&c->d_fprof, 8 * sizeof(unsigned long long)));
+            HPBJ_CUDA(cudaMemset(c->d_fprof, 0, 8 * sizeof(unsigned long long)));
+        }
         if (use_graph) {
             ensure_graph(c);
+            const auto tg0 = std::chrono::steady_clock::now();
             HPBJ_CUDA(cudaGraphLaunch(c->graph_exec, st));
+            if (getenv("HPBJ_DEBUG")) {
+                HPBJ_CUDA(cudaStreamSynchronize(st));
+                const auto tg1 = std::chrono::steady_clock::now();
+                fprintf(stderr, "[hpbj] solve: pre-graph %.3f ms, graph %.3f ms\n",
+                        std::chrono::duration<double, std::milli>(tg0 - t0).count(),
+                        std::chrono::duration<double, std::milli>(tg1 - tg0).count());
+            }
             c->launches += 0;  // kernel launches inside the graph are counted below
         } else {
             if (c->profiling) c->timer.reserve((size_t)3 * m);
             for (;;) {
                 enqueue_cycle_head(c, 0);
-                for (int it = 0; it < m; ++it) enqueue_step(c, 0, it);
+                if (c->fused.ok) enqueue_cycle_fused(c);
+                else
+                    for (int it = 0; it < m; ++it) enqueue_step(c, 0, it);
                 enqueue_cycle_tail(c, 0);
                 HPBJ_CUDA(cudaMemcpyAsync(&hs, c->d_st, sizeof(hs), cudaMemcpyDeviceToHost, st));
                 HPBJ_CUDA(cudaStreamSynchronize(st));
@@ -651,9 +692,10 @@ void solve(hpbj_ctx* c, const double* d_b, double* d_x, const hpbj_gmres_opts* o
         }
         HPBJ_CUDA(cudaMemcpyAsync(&hs, c->d_st, sizeof(hs), cudaMemcpyDeviceToHost, st));
         HPBJ_CUDA(cudaStreamSynchronize(st));
-        if (use_graph)  // 3 kernels per Arnoldi step + 8 per cycle (incl. long-row SpMV parts)
-            c->launches += (int64_t)hs.total_iterations * (3 + (c->planB.n_long ? 1 : 0)) +
-                           (int64_t)hs.cycles * (5 + (c->planB.n_long ? 1 : 0));
+        if (use_graph && c->fused.ok)  // per cycle: init, arnoldi_cycle, solve_y, update, residual, end
+            c->launches += (int64_t)hs.cycles * 6;
+        else if (use_graph)  // per step: apply, spmv, orth; per cycle: init, solve_y, update, residual, end
+            c->launches += (int64_t)hs.total_iterations * 3 + (int64_t)hs.cycles * 5;
         std::vector<double> hv(hs.hist_len), cr(hs.cycles);
         std::vector<int> hc(hs.hist_len);
         if (hs.hist_len) {
@@ -668,6 +710,14 @@ void solve(hpbj_ctx* c, const double* d_b, double* d_x, const hpbj_gmres_opts* o
             if (cycle_res && clen < cyc_cap) cycle_res[clen] = cr[k];
             ++clen;
         }
+        if (c->d_fprof && c->fused.ok) {
+            unsigned long long t[4];
+            HPBJ_CUDA(cudaMemcpy(t, c->d_fprof, sizeof(t), cudaMemcpyDeviceToHost));
+            HPBJ_CUDA(cudaMemset(c->d_fprof, 0, sizeof(t)));
+            const double k = 1e-3 / std::max(1, hs.total_iterations);
+            fprintf(stderr, "[hpbj fused] grid %d slice %d: us/step apply+b1 %.2f spmv %.2f passA+b2 %.2f passB+b3 %.2f\n",
+                    c->fused.grid, c->fused.slice, t[0] * k, t[1] * k, t[2] * k, t[3] * k);
+        }
         R.converged = hs.converged;
         R.total_iterations = hs.total_iterations;
         R.breakdown = hs.breakdown_any;
@@ -681,7 +731,6 @@ void solve(hpbj_ctx* c, const double* d_b, double* d_x, const hpbj_gmres_opts* o
     R.cycles = clen;
     R.ms_solve = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     if (rep) *rep = R;
-    if (getenv("HPBJ_ICWY_DBG")) icwy_dump();
 }
 
 }  // namespace
@@ -707,6 +756,8 @@ int hpbj_create(hpbj_ctx** out, int device) {
         HPBJ_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         const char* ng = getenv("HPBJ_NOGRAPH");
         c->use_graph = !(ng && ng[0] == '1');
+        const char* nf = getenv("HPBJ_FUSED");
+        c->use_fused = !(nf && nf[0] == '0');
         *out = c;
     });
 }
@@ -733,8 +784,9 @@ int hpbj_get_kernel_stats(hpbj_ctx* ctx, hpbj_kernel_stat* out) {
         const double n = ctx->A.n, nnz = ctx->A.nnz;
         double bytes_apply = 0.0;
         if (ctx->has_pc) {
-            bytes_apply = 7.0 * (double)ctx->spk_entries          // off-panel value + col + row
-                          + (4.0 * 1024 + 16.0) * ctx->num_panels // diagonal tiles + panel descriptors
+            const double idx_b = ctx->dmax > kIdx16MaxDim ? 4.0 : 2.0;
+            bytes_apply = (4.0 + idx_b) * (double)ctx->spk_entries  // off-panel value + packed index
+                          + (4.0 * 1024 + 16.0) * ctx->num_panels    // tile quads read (8 of 9 per pass) + descriptors
                           + 4.0 * n                               // pivot rows (int32)
                           + 8.0 * n                               // v (FP64) in
                           + 4.0 * n                               // z (FP32) out
@@ -881,7 +933,7 @@ int hpbj_bj_setup(hpbj_ctx* ctx, int64_t s, const int64_t* perm, const int64_t* 
         dslot(ctx->d_ent_off, np + 1);
         dslot(ctx->d_scan_tmp, 16384);
         dslot(ctx->d_desc, np);
-        dslot(ctx->d_dtile, (size_t)np * 1024);
+        dslot(ctx->d_dtile, (size_t)np * kTileFloats);
         HPBJ_CUDA(cudaMemcpyAsync(ctx->d_pstart, hps.data(), sizeof(int) * (s + 1), cudaMemcpyHostToDevice, st));
         const size_t scr = block_lu_scratch_floats(dmax, ctx->num_sms, &ctx->lu_smem_dim, &ctx->lu_scratch_ld);
         if (scr) dslot(ctx->d_lu_scratch, scr);

@@ -70,14 +70,17 @@ void launch_block_lu(const LuParams& p, int dmax, int num_sms, cudaStream_t st, 
 size_t block_lu_scratch_floats(int dmax, int num_sms, int* smem_dim, int* scratch_ld);
 
 // ---- spk.cu ---------------------------------------------------------------
-// Sparse-panel factor storage (see spk.cu): per 32-row panel, a row-sorted
-// coordinate list of the off-panel L then U entries and the dense 32x32
-// diagonal tile in a coalesced lane-quad layout.
+// Sparse-panel factor storage (see spk.cu): per 32-row panel, the off-panel
+// L then U entries row-sorted (FP32 value + packed column << 5 | row), and
+// the inverse of the 32x32 diagonal tile as 9 float4 quads per row.
+constexpr int kTileFloats = 9 * 128;
+constexpr int kIdx16MaxDim = 2047;  // 16-bit packed indices up to this block size
+
 struct SpkPanel {
-    int off;   // first entry (L part); U part starts at off + nl
+    int off;   // first L entry (16-byte aligned)
     int nl;
     int nu;
-    int doff;  // first compacted diagonal value
+    int uoff;  // first U entry (16-byte aligned)
 };
 
 struct SpkBuild {
@@ -88,17 +91,19 @@ struct SpkBuild {
     int* panel_block;       // num_panels
     const int64_t* fac_off;
     const float* dense;     // dense panels from block_lu
-    int* ent_count;         // pass 1 outputs
-    int* diag_count;
-    const int* ent_off;     // exclusive scans of the counts
-    const int* diag_off;
+    int* ent_count;         // pass 1 output (entries, parts padded to 4)
+    const int* ent_off;     // exclusive scan of the counts
     SpkPanel* desc;         // pass 2 outputs
-    float* dtile;           // 1024 floats per panel: dense diagonal tile, [q][lane][4]
+    float* dtile;           // kTileFloats per panel
     float* eval;
-    uint16_t* ecol;
-    uint8_t* erow;
+    void* eidx;             // uint16_t (dmax <= kIdx16MaxDim) or uint32_t
+    int idx32;
 };
 
+// Tile quads of row l (q = 0..7 cover columns 4q..4q+3, qd = l / 4): q < qd
+// strictly-lower Linv, q > qd upper Uinv, q == qd the Linv part of the
+// diagonal quad (zeros from the diagonal on); quad 8 the Uinv part of the
+// diagonal quad. Stored [quad][lane] so a warp's loads are coalesced.
 struct SpkView {
     int s;
     int dmax;
@@ -108,8 +113,8 @@ struct SpkView {
     const SpkPanel* desc;
     const float* dtile;
     const float* eval;
-    const uint16_t* ecol;
-    const uint8_t* erow;
+    const void* eidx;
+    int idx32;
     const int* ent_off;   // num_panels + 1 (prefetch ranges)
 };
 
@@ -127,10 +132,9 @@ void launch_apply_update(const SpkView& v, const double* V, int ldv, const doubl
 // ---- spmv.cu --------------------------------------------------------------
 struct SpmvPlan {
     int group = 8;            // lanes per row
-    int long_thresh = 256;    // rows longer than this go to the CTA-per-row kernel
+    int long_thresh = 256;    // rows longer than this get a CTA of their own
     int n_long = 0;
-    int* long_rows = nullptr; // permuted indices of long rows (device)
-    double* ylong = nullptr;  // n doubles (only long rows used)
+    int* long_rows = nullptr; // indices of long rows (device), one CTA each
 };
 
 // y = A x, x FP32 (preconditioned vector) or FP64; early exit if st->done.
@@ -188,5 +192,21 @@ void launch_cycle_init(const KrylovBufs& kb, SolveState* sst, const double* r, i
 void launch_cycle_end(const KrylovBufs& kb, SolveState* sst, cudaGraphConditionalHandle cond, cudaStream_t st,
                       int64_t* launches);
 void launch_solve_y(const KrylovBufs& kb, SolveState* sst, cudaStream_t st, int64_t* launches);
+
+// ---- fused.cu -------------------------------------------------------------
+// A whole Arnoldi cycle (apply, SpMV, compact-WY MGS, Givens per step) as one
+// persistent cooperative kernel; ok = false when the shared-memory tables do
+// not fit (then the per-kernel path runs).
+struct FusedPlan {
+    bool ok = false;
+    int grid = 0;
+    int slice = 0;
+    int ystride = 0;
+    size_t smem = 0;
+};
+FusedPlan plan_fused(int n, int s, int dmax, int num_sms, int m, bool has_long);
+void launch_arnoldi_cycle(const FusedPlan& F, const SpkView& pc, const DevCsr& a, const SpmvPlan& plan,
+                          const KrylovBufs& kb, double* gram, SolveState* sst, GridBarrier* gb, float* z32,
+                          unsigned long long* prof, cudaStream_t st, int64_t* launches);
 
 }  // namespace hpbj

@@ -1,0 +1,273 @@
+// Device side of the sparse-panel block-Jacobi apply (spk.cu): the per-block
+// substitution as a warp-level device function, shared by the standalone
+// apply kernels (spk.cu) and the fused Arnoldi-cycle kernel (fused.cu).
+#pragma once
+
+#include <cstdint>
+
+#include "device.cuh"
+#include "kernels.cuh"
+
+namespace hpbj {
+namespace spk {
+
+constexpr int kMaxPanels = 9;  // pivots of up to 288 rows gathered with full ILP
+
+// ----------------------------------------------------------------------------
+struct SrcDown {  // (float) V[:, st->j][row]  (Arnoldi step)
+    const double* V;
+    int ldv;
+    const SolveState* sst;
+    __device__ float operator()(int row) const { return __double2float_rn(__ldg(V + (size_t)sst->j * ldv + row)); }
+};
+struct SrcVec {  // (float) v[row]
+    const double* v;
+    __device__ float operator()(int row) const { return __double2float_rn(__ldg(v + row)); }
+};
+struct SrcBasis {  // sum_i y_i V[i][row], i ascending (gmres.cpp:152-157), FP64
+    const double* V;
+    int ldv;
+    const double* y;
+    const SolveState* sst;
+    __device__ double operator()(int row) const {
+        const int steps = sst->j;
+        double u = 0.0;
+        for (int i = 0; i < steps; ++i) u = fma(y[i], __ldg(V + (size_t)i * ldv + row), u);
+        return u;
+    }
+};
+struct DstF32 {
+    float* z;
+    __device__ void operator()(int row, float v) const { z[row] = v; }
+};
+struct DstF64 {
+    double* z;
+    template <class T>
+    __device__ void operator()(int row, T v) const { z[row] = (double)v; }
+};
+struct DstAddX {  // x = x0 + z (gmres.cpp:158-159)
+    double* x;
+    __device__ void operator()(int row, double v) const { x[row] = x[row] + v; }
+};
+
+template <class IdxT>
+struct Idx4;
+template <>
+struct Idx4<uint16_t> {
+    using type = ushort4;
+};
+template <>
+struct Idx4<uint32_t> {
+    using type = uint4;
+};
+
+// acc[row] -= sum val * x[col] over the row-sorted entries [e0, e0 + cnt)
+// (e0 16-byte aligned), branch-free. Each lane takes four consecutive
+// entries (one float4 + one 4-index load) and forms their inclusive
+// segmented sums q_k (runs of equal rows); the run that crosses lane
+// boundaries is completed by a segmented warp scan of the lanes' tail sums,
+// whose carry is added to the lane's head run; the last entry of every row
+// segment flushes into acc. Fixed association: deterministic.
+template <class Acc, class IdxT>
+__device__ __forceinline__ void fold_entries(const float* __restrict__ eval, const IdxT* __restrict__ eidx, int e0,
+                                             int cnt, const Acc* xs, Acc* acc, int lane) {
+    using I4 = typename Idx4<IdxT>::type;
+    const float4* ev = reinterpret_cast<const float4*>(eval + e0);
+    const I4* ei = reinterpret_cast<const I4*>(eidx + e0);
+    for (int base = 0; base < cnt; base += 128) {
+        const int i0 = base + 4 * lane;
+        const int nv = cnt - i0;  // valid entries of this lane (<= 0: none, >= 4: all four)
+        float4 v4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        I4 x4{};
+        if (nv > 0) {  // padding entries inside the last quad are (0, col 0)
+            v4 = __ldg(ev + (i0 >> 2));
+            x4 = __ldg(ei + (i0 >> 2));
+        }
+        const float v[4] = {v4.x, v4.y, v4.z, v4.w};
+        const unsigned xi[4] = {(unsigned)x4.x, (unsigned)x4.y, (unsigned)x4.z, (unsigned)x4.w};
+        int r[4];
+        Acc q[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) r[k] = k < nv ? (int)(xi[k] & 31u) : 32 + 4 * lane + k;  // invalid: unique, never flushed
+        q[0] = (Acc)v[0] * xs[xi[0] >> 5];
+#pragma unroll
+        for (int k = 1; k < 4; ++k) {
+            const Acc xk = xs[xi[k] >> 5];
+            q[k] = (r[k] == r[k - 1]) ? fma((Acc)v[k], xk, q[k - 1]) : (Acc)v[k] * xk;
+        }
+        const int prev_tail = __shfl_up_sync(0xffffffffu, r[3], 1);
+        const int next_head = __shfl_down_sync(0xffffffffu, r[0], 1);
+        const bool cont = lane > 0 && r[0] == prev_tail;  // head run continues the lower lane's tail run
+        const bool start = !(cont && r[3] == r[0]);
+        const unsigned heads = __ballot_sync(0xffffffffu, start);
+        const int dist = lane - (31 - __clz(heads & (0xffffffffu >> (31 - lane))));
+        const int maxd = __reduce_max_sync(0xffffffffu, dist);
+        Acc run = q[3];
+        for (int off = 1; off <= maxd; off <<= 1) {
+            const Acc t = __shfl_up_sync(0xffffffffu, run, off);
+            if (off <= dist) run += t;
+        }
+        const Acc up = __shfl_up_sync(0xffffffffu, run, 1);
+        const Acc carry = cont ? up : (Acc)0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const bool end = (k < 3) ? (r[k] != r[k + 1]) : (lane == 31 || next_head != r[3]);
+            if (end && r[k] < 32) acc[r[k]] -= (r[k] == r[0]) ? q[k] + carry : q[k];
+        }
+        __syncwarp();
+    }
+}
+
+// L2 bulk prefetch of [p, p + bytes) (TMA engine; no registers, no smem).
+__device__ __forceinline__ void prefetch_l2(const void* p, size_t bytes) {
+    const uintptr_t a = (uintptr_t)p & ~(uintptr_t)15;
+    const uintptr_t e = ((uintptr_t)p + bytes + 15) & ~(uintptr_t)15;
+    if (e > a)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((unsigned)(e - a)) : "memory");
+}
+
+// The tile quads a pass reads ([quad][lane] float4, see kernels.cuh): the
+// forward pass quad q for lanes l >= 4q, the backward pass quad q < 8 for
+// lanes l < 4q and all of quad 8. Lanes 8..16 issue one quad each.
+__device__ __forceinline__ void prefetch_tile(const SpkView& p, int P, bool fwd, int lane) {
+    if (lane >= 8 && lane <= 16) {
+        const int q = lane - 8;
+        int l0 = 0, l1 = 32;
+        if (q == 8) l1 = fwd ? 0 : 32;
+        else if (fwd) l0 = 4 * q;
+        else l1 = 4 * q;
+        if (l1 > l0) prefetch_l2(p.dtile + (size_t)P * kTileFloats + q * 128 + l0 * 4, (size_t)16 * (l1 - l0));
+    }
+}
+
+template <class IdxT>
+__device__ __forceinline__ void prefetch_entries(const SpkView& p, int e0, int cnt, int lane, int lv, int li) {
+    if (lane == lv) prefetch_l2(p.eval + e0, sizeof(float) * cnt);
+    else if (lane == li) prefetch_l2(reinterpret_cast<const IdxT*>(p.eidx) + e0, sizeof(IdxT) * cnt);
+}
+
+// Next block's head: descriptors, pivots and its first panel's forward data.
+// Called by the whole warp (one prefetch per lane).
+template <class IdxT>
+__device__ __forceinline__ void prefetch_block_head(const SpkView& p, int b, int lane) {
+    const int P0 = p.pstart[b];
+    if (lane < 4) {
+        const int o = p.bstart[b], d = p.bstart[b + 1] - o;
+        const int e0 = p.ent_off[P0], e1 = p.ent_off[P0 + 1];
+        if (lane == 0) prefetch_l2(p.desc + P0, sizeof(SpkPanel) * (p.pstart[b + 1] - P0));
+        else if (lane == 1) prefetch_l2(p.piv + o, sizeof(int) * d);
+        else prefetch_entries<IdxT>(p, e0, e1 - e0, lane, 2, 3);
+    }
+    prefetch_tile(p, P0, true, lane);
+}
+
+// One block's substitution M_b^-1: gather rhs[piv] from src, forward with
+// the unit-lower factor, backward with the upper one, write through dst.
+// ybuf (Acc[32 T]) and dsh (SpkPanel[T]) are the calling warp's shared
+// memory; next_b (or -1) is the block whose head is prefetched at the end.
+template <class Acc, class IdxT, class Src, class Dst>
+__device__ __forceinline__ void spk_solve_block(const SpkView& p, int b, int next_b, Src src, Dst dst, Acc* ybuf,
+                                                SpkPanel* dsh, int lane) {
+    const IdxT* eidx = reinterpret_cast<const IdxT*>(p.eidx);
+    const int o = p.bstart[b];
+    const int d = p.bstart[b + 1] - o;
+    const int T = (d + 31) >> 5;
+    const int P0 = p.pstart[b];
+    const int qd = lane >> 2;
+    if (lane < T) dsh[lane] = p.desc[P0 + lane];
+    __syncwarp();
+    // rhs[pivot_rows[k]] for the whole block: all pivot loads first, then
+    // all gathers (two latency rounds, not 2T)
+    {
+        int pv[kMaxPanels];
+#pragma unroll
+        for (int t = 0; t < kMaxPanels; ++t) {
+            const int k = 32 * t + lane;
+            pv[t] = (t < T && k < d) ? __ldg(p.piv + o + k) : -1;
+        }
+#pragma unroll
+        for (int t = 0; t < kMaxPanels; ++t)
+            if (t < T) ybuf[32 * t + lane] = pv[t] >= 0 ? (Acc)src(o + pv[t]) : (Acc)0;
+        for (int t = kMaxPanels; t < T; ++t) {
+            const int k = 32 * t + lane;
+            ybuf[k] = (k < d) ? (Acc)src(o + __ldg(p.piv + o + k)) : (Acc)0;
+        }
+    }
+    __syncwarp();
+    // ---- forward: y_k = rhs_k - sum_{c<k} L_kc y_c
+    for (int t = 0; t < T; ++t) {
+        const SpkPanel ds = dsh[t];
+        // next step's data into L2 while this one computes
+        if (t + 1 < T) {
+            prefetch_entries<IdxT>(p, dsh[t + 1].off, dsh[t + 1].nl, lane, 0, 1);
+            prefetch_tile(p, P0 + t + 1, true, lane);
+        } else {
+            prefetch_entries<IdxT>(p, ds.uoff, ds.nu, lane, 0, 1);
+            prefetch_tile(p, P0 + t, false, lane);
+        }
+        fold_entries<Acc, IdxT>(p.eval, eidx, ds.off, ds.nl, ybuf, ybuf + 32 * t, lane);
+        // y_t = Linv_tt r_t: quads 0..qd of row `lane` (zeros from the diagonal on)
+        {
+            const float4* tile = reinterpret_cast<const float4*>(p.dtile + (size_t)(P0 + t) * kTileFloats);
+            float4 f4[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                f4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (q <= qd) f4[q] = __ldg(tile + q * 32 + lane);
+            }
+            const Acc* r = ybuf + 32 * t;
+            Acc a0 = r[lane], a1 = (Acc)0, a2 = (Acc)0, a3 = (Acc)0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                a0 = fma((Acc)f4[q].x, r[4 * q + 0], a0);
+                a1 = fma((Acc)f4[q].y, r[4 * q + 1], a1);
+                a2 = fma((Acc)f4[q].z, r[4 * q + 2], a2);
+                a3 = fma((Acc)f4[q].w, r[4 * q + 3], a3);
+            }
+            const Acc yv = (a0 + a1) + (a2 + a3);
+            __syncwarp();
+            ybuf[32 * t + lane] = yv;
+            __syncwarp();
+        }
+    }
+    // ---- backward: x_k = (y_k - sum_{c>k} U_kc x_c) / U_kk
+    for (int t = T - 1; t >= 0; --t) {
+        const SpkPanel ds = dsh[t];
+        if (t > 0) {
+            prefetch_entries<IdxT>(p, dsh[t - 1].uoff, dsh[t - 1].nu, lane, 0, 1);
+            prefetch_tile(p, P0 + t - 1, false, lane);
+        } else if (next_b >= 0) {
+            prefetch_block_head<IdxT>(p, next_b, lane);
+        }
+        fold_entries<Acc, IdxT>(p.eval, eidx, ds.uoff, ds.nu, ybuf, ybuf + 32 * t, lane);
+        // x_t = Uinv_tt y'_t: quad 8 (the diagonal quad) and quads qd+1..7 of row `lane`
+        const int k = 32 * t + lane;
+        {
+            const float4* tile = reinterpret_cast<const float4*>(p.dtile + (size_t)(P0 + t) * kTileFloats);
+            float4 f4[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                f4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (q >= qd) f4[q] = __ldg(tile + (q == qd ? 8 : q) * 32 + lane);
+            }
+            const Acc* r = ybuf + 32 * t;
+            Acc a0 = (Acc)0, a1 = (Acc)0, a2 = (Acc)0, a3 = (Acc)0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                a0 = fma((Acc)f4[q].x, r[4 * q + 0], a0);
+                a1 = fma((Acc)f4[q].y, r[4 * q + 1], a1);
+                a2 = fma((Acc)f4[q].z, r[4 * q + 2], a2);
+                a3 = fma((Acc)f4[q].w, r[4 * q + 3], a3);
+            }
+            const Acc xv = (a0 + a1) + (a2 + a3);
+            __syncwarp();
+            ybuf[k] = xv;
+            __syncwarp();
+            if (k < d) dst(o + k, xv);
+        }
+    }
+    __syncwarp();
+}
+
+}  // namespace spk
+}  // namespace hpbj

@@ -1,14 +1,13 @@
 // FP64 CSR SpMV — replaces spmv<T> (spmv.hpp:31-47) and residual_vector
 // (gmres.cpp:75-81), on the permuted matrix Q A Q^T.
 //
-// Rows are processed by groups of G lanes (G = 4/8/16/32 by mean row length:
+// Rows are processed by groups of G lanes (G = 1..32 by mean row length:
 // coalesced, vectorised row access); each lane strides the row and the group
 // reduces with G-wide shuffles in a fixed order. Rows longer than
-// plan.long_thresh (supply-rail hubs, ~1e4 nnz in config 2) are split across
-// a whole CTA by a separate kernel that runs first and parks the row sum in
-// ylong[row]; the main kernel then treats the row like any other, so the
-// epilogue (plain store, or r = b - A x with a deterministic grid-wide norm)
-// stays uniform.
+// plan.long_thresh (supply-rail hubs, ~1e4 nnz in config 2) get a whole CTA
+// each, appended to the same grid so they run concurrently with the ordinary
+// rows. The epilogue is a plain store, or r = b - A x with a deterministic
+// grid-wide norm (per-CTA partials summed in CTA order by the last CTA).
 
 #include "device.cuh"
 #include "kernels.cuh"
@@ -18,62 +17,84 @@ namespace hpbj {
 namespace {
 
 constexpr int kSpmvThreads = 256;
-constexpr int kLongThreads = 512;
 
 template <class XT>
 __device__ __forceinline__ double ldx(const XT* x, int c) {
     return (double)__ldg(x + c);
 }
 
-template <class XT>
-__global__ void __launch_bounds__(kLongThreads) k_spmv_long(const int* __restrict__ rows, DevCsr a,
-                                                            const XT* __restrict__ x,
-                                                            double* __restrict__ ylong, const SolveState* sst) {
-    if (sst && sst->done) return;
-    __shared__ double sh[kLongThreads / 32];
-    const int row = rows[blockIdx.x];
-    const int b = a.rp[row], e = a.rp[row + 1];
-    double s = 0.0;
-    for (int k = b + threadIdx.x; k < e; k += kLongThreads) s = fma(a.val[k], ldx(x, a.ci[k]), s);
-    s = block_sum<kLongThreads>(s, sh);
-    if (threadIdx.x == 0) ylong[row] = s;
-}
-
 // MODE 0: y = A x.  MODE 1: y = b - A x, st->rnorm = ||y||_2.
+// CTAs [0, n_long) take one hub row each (dispatched first: they are the
+// longest), CTAs [n_long, n_long + main_grid) sweep the ordinary rows (G lanes
+// per row, hub rows skipped) concurrently.
 template <int G, class XT, int MODE>
 __global__ void __launch_bounds__(kSpmvThreads) k_spmv(DevCsr a, const XT* __restrict__ x,
                                                        double* __restrict__ y, const double* __restrict__ bvec,
-                                                       const double* __restrict__ ylong, int long_thresh,
-                                                       SolveState* sst, double* __restrict__ partials) {
+                                                       const int* __restrict__ long_rows, int long_thresh,
+                                                       int n_long, SolveState* sst, double* __restrict__ partials) {
     if (MODE == 0 && sst && sst->done) return;
-    const int gl = threadIdx.x & (G - 1);
-    const int group = (blockIdx.x * kSpmvThreads + threadIdx.x) / G;
-    const int ngroups = gridDim.x * (kSpmvThreads / G);
-    const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
+    __shared__ double sh[kSpmvThreads / 32];
     double ss = 0.0;
-    for (int row = group; row < a.n; row += ngroups) {
+    if ((int)blockIdx.x < n_long) {
+        const int row = long_rows[blockIdx.x];
         const int b = __ldg(a.rp + row), e = __ldg(a.rp + row + 1);
-        double sum;
-        if (e - b > long_thresh) {
-            sum = ylong[row];
-        } else {
-            sum = 0.0;
-            for (int k = b + gl; k < e; k += G) sum = fma(__ldg(a.val + k), ldx(x, __ldg(a.ci + k)), sum);
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;  // four chains: loads of four strides in flight
+        int k = b + threadIdx.x;
+        for (; k + 3 * kSpmvThreads < e; k += 4 * kSpmvThreads) {
+            s0 = fma(__ldg(a.val + k), ldx(x, __ldg(a.ci + k)), s0);
+            s1 = fma(__ldg(a.val + k + kSpmvThreads), ldx(x, __ldg(a.ci + k + kSpmvThreads)), s1);
+            s2 = fma(__ldg(a.val + k + 2 * kSpmvThreads), ldx(x, __ldg(a.ci + k + 2 * kSpmvThreads)), s2);
+            s3 = fma(__ldg(a.val + k + 3 * kSpmvThreads), ldx(x, __ldg(a.ci + k + 3 * kSpmvThreads)), s3);
+        }
+        for (; k < e; k += kSpmvThreads) s0 = fma(__ldg(a.val + k), ldx(x, __ldg(a.ci + k)), s0);
+        double s = block_sum<kSpmvThreads>((s0 + s1) + (s2 + s3), sh);
+        if (threadIdx.x == 0) {
+            if (MODE == 0) {
+                y[row] = s;
+            } else {
+                const double r = bvec[row] - s;
+                y[row] = r;
+                ss = r * r;
+            }
+        }
+    } else {
+        const int gl = threadIdx.x & (G - 1);
+        const int group = ((blockIdx.x - n_long) * kSpmvThreads + threadIdx.x) / G;
+        const int ngroups = (gridDim.x - n_long) * (kSpmvThreads / G);
+        const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
+        for (int row = group; row < a.n; row += ngroups) {
+            const int b = __ldg(a.rp + row), e = __ldg(a.rp + row + 1);
+            if (e - b > long_thresh) continue;  // uniform within the group
+            double sum = 0.0;
+            // four strides per round: their index/value loads, then their x
+            // gathers, are in flight together (same summation order as a plain loop)
+            for (int k0 = b + gl; k0 < e; k0 += 4 * G) {
+                int c[4];
+                double v[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int k = k0 + u * G;
+                    c[u] = k < e ? __ldg(a.ci + k) : 0;
+                    v[u] = k < e ? __ldg(a.val + k) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (k0 + u * G < e) sum = fma(v[u], ldx(x, c[u]), sum);
+            }
 #pragma unroll
             for (int o = G / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(gmask, sum, o, G);
-        }
-        if (gl == 0) {
-            if (MODE == 0) {
-                y[row] = sum;
-            } else {
-                const double r = bvec[row] - sum;
-                y[row] = r;
-                ss = fma(r, r, ss);
+            if (gl == 0) {
+                if (MODE == 0) {
+                    y[row] = sum;
+                } else {
+                    const double r = bvec[row] - sum;
+                    y[row] = r;
+                    ss = fma(r, r, ss);
+                }
             }
         }
     }
     if (MODE == 1) {
-        __shared__ double sh[kSpmvThreads / 32];
         __shared__ bool last;
         ss = block_sum<kSpmvThreads>(ss, sh);
         if (threadIdx.x == 0) {
@@ -131,17 +152,13 @@ int spmv_grid(int n, int G) {
 template <class XT, int MODE>
 void run(const DevCsr& a, const SpmvPlan& plan, const XT* x, double* y, const double* b, SolveState* sst,
          double* partials, cudaStream_t st, int64_t* launches) {
-    if (plan.n_long > 0) {
-        k_spmv_long<XT><<<plan.n_long, kLongThreads, 0, st>>>(plan.long_rows, a, x, plan.ylong,
-                                                              MODE == 0 ? sst : nullptr);
-        *launches += 1;
-    }
     const int G = plan.group;
-    const int grid = spmv_grid(a.n, G);
-#define HPBJ_SPMV_CASE(GG)                                                                          \
-    case GG:                                                                                        \
-        k_spmv<GG, XT, MODE><<<grid, kSpmvThreads, 0, st>>>(a, x, y, b, plan.ylong, plan.long_thresh, \
-                                                            sst, partials);                         \
+    const int main_grid = spmv_grid(a.n, G);
+    const int grid = main_grid + plan.n_long;
+#define HPBJ_SPMV_CASE(GG)                                                                              \
+    case GG:                                                                                            \
+        k_spmv<GG, XT, MODE><<<grid, kSpmvThreads, 0, st>>>(a, x, y, b, plan.long_rows, plan.long_thresh, \
+                                                            plan.n_long, sst, partials);                \
         break;
     switch (G) {
         HPBJ_SPMV_CASE(1)
