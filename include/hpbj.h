@@ -98,13 +98,16 @@ typedef struct hpbj_history_point {
 typedef struct hpbj_kernel_stat {
     int64_t launches;
     double total_ms;
-    double bytes_per_launch;
+    double bytes_per_launch;  /* total_bytes / launches */
+    int64_t steps;            /* Arnoldi steps covered by these launches */
+    double total_bytes;       /* algorithmic HBM bytes of all launches */
 } hpbj_kernel_stat;
 
-#define HPBJ_K_APPLY 0   /* block forward/back substitution (Arnoldi step) */
-#define HPBJ_K_SPMV 1    /* FP64 CSR SpMV (Arnoldi step)                   */
-#define HPBJ_K_MGS 2     /* fused MGS + norm + Givens (persistent)         */
-#define HPBJ_K_COUNT 3
+#define HPBJ_K_APPLY 0   /* block forward/back substitution (Arnoldi step)       */
+#define HPBJ_K_SPMV 1    /* FP64 CSR SpMV (Arnoldi step)                         */
+#define HPBJ_K_MGS 2     /* compact-WY / textbook MGS + norm + Givens            */
+#define HPBJ_K_CYCLE 3   /* fused Arnoldi cycle (apply+SpMV+MGS+Givens per step) */
+#define HPBJ_K_COUNT 4
 
 /* ---- context ------------------------------------------------------------ */
 int hpbj_create(hpbj_ctx** out, int device);
@@ -115,6 +118,9 @@ const char* hpbj_last_error(const hpbj_ctx* ctx);
 int64_t hpbj_kernel_launches(const hpbj_ctx* ctx);
 int hpbj_set_profiling(hpbj_ctx* ctx, int enable);
 int hpbj_get_kernel_stats(hpbj_ctx* ctx, hpbj_kernel_stat* out /* HPBJ_K_COUNT */);
+/* Whole Arnoldi cycle as one persistent kernel when it fits (default on);
+ * off: one apply, SpMV and orthogonalisation launch per step. */
+int hpbj_set_fused(hpbj_ctx* ctx, int enable);
 
 /* ---- host-side partitioning (bit-identical to the reference) ------------ */
 /* graph_from_matrix (graph.hpp:30, graph.cpp:17-51). Adjacency as CSR:

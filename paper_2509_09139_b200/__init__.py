@@ -304,7 +304,12 @@ class Context:
     def kernel_stats(self):
         arr = (_abi.KernelStat * _abi.HPBJ_K_COUNT)()
         self.check(self.lib.hpbj_get_kernel_stats(self.h, arr))
-        return [dict(launches=s.launches, total_ms=s.total_ms, bytes_per_launch=s.bytes_per_launch) for s in arr]
+        return [dict(launches=s.launches, total_ms=s.total_ms, bytes_per_launch=s.bytes_per_launch, steps=s.steps,
+                     total_bytes=s.total_bytes) for s in arr]
+
+    def set_fused(self, on: bool):
+        """Whole Arnoldi cycle as one persistent kernel when it fits (default)."""
+        self.check(self.lib.hpbj_set_fused(self.h, 1 if on else 0))
 
     def gmres(self, b, cfg: "GmresConfig", device_ptrs=None):
         opts = cfg.to_opts()

@@ -23,7 +23,8 @@ HPBJ_ENODEV = 7
 HPBJ_K_APPLY = 0
 HPBJ_K_SPMV = 1
 HPBJ_K_MGS = 2
-HPBJ_K_COUNT = 3
+HPBJ_K_CYCLE = 3
+HPBJ_K_COUNT = 4
 
 i64 = ctypes.c_int64
 f64 = ctypes.c_double
@@ -79,7 +80,8 @@ class HistoryPoint(ctypes.Structure):
 
 
 class KernelStat(ctypes.Structure):
-    _fields_ = [("launches", i64), ("total_ms", f64), ("bytes_per_launch", f64)]
+    _fields_ = [("launches", i64), ("total_ms", f64), ("bytes_per_launch", f64), ("steps", i64),
+                ("total_bytes", f64)]
 
 
 # name -> (restype, argtypes); exactly the symbols include/hpbj.h declares
@@ -90,6 +92,7 @@ SIGNATURES = {
     "hpbj_kernel_launches": (i64, [vp]),
     "hpbj_set_profiling": (ctypes.c_int, [vp, ctypes.c_int]),
     "hpbj_get_kernel_stats": (ctypes.c_int, [vp, ctypes.POINTER(KernelStat)]),
+    "hpbj_set_fused": (ctypes.c_int, [vp, ctypes.c_int]),
     "hpbj_graph_from_matrix": (ctypes.c_int, [i64, i64p, i64p, f64p, i64p, i64p, f64p, i64]),
     "hpbj_partition_graph": (ctypes.c_int, [i64, i64p, i64p, f64p, i64, f64, i64p, i64p, i64p]),
     "hpbj_partition_adjacency": (ctypes.c_int, [i64, i64p, i64p, f64p, i64, f64, i64p, i64p, i64p]),

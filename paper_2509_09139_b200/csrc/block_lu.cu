@@ -311,6 +311,302 @@ __global__ void __launch_bounds__(256) k_block_lu_warp(LuParams p, int dw, int l
     }
 }
 
+// ---------------------------------------------------------------------------
+// Blocked right-looking LU for mid-size blocks (kWarpLuMax < d <= kBlkMax),
+// one CTA per block, the block in a per-CTA global scratch tile (L2 resident,
+// 16-byte rows). Per 32-column panel:
+//   (1) the panel of the not-yet-pivotal rows is factored with each thread
+//       holding its (<= 2) rows' 32 panel entries in registers: per column a
+//       CTA argmax, the pivot row broadcast through shared memory, and the
+//       rank-1 update restricted to the panel, all register-resident;
+//   (2) the 32 pivot rows' entries right of the panel (U12) by forward
+//       substitution with the panel's unit-lower part, thread per column;
+//   (3) the remaining rows' trailing entries take the rank-32 update, each
+//       element a chain of 32 FMAs in column order (warp per 4 rows, lane per
+//       column, the U12 column in registers, multipliers as float4 broadcasts).
+// Every element receives exactly the fmaf(-l, u, a) sequence, in the same
+// column order, that the column-by-column kernels apply, and the pivot rule
+// is the same, so factors and pivots are bit-identical to k_block_lu.
+constexpr int kBlkThreads = 256;
+constexpr int kBlkMax = 512;  // two panel rows per thread
+
+__host__ __device__ inline int blk_ld(int d) { return (d + 3) & ~3; }
+
+size_t blk_smem_bytes(int dhi) {
+    const int d4 = blk_ld(dhi);
+    return (size_t)dhi * 32 * sizeof(float)     // multipliers of the panel, 16-byte rows
+           + (size_t)32 * d4 * sizeof(float)    // U12 / output staging
+           + (size_t)dhi * 2 * sizeof(int)      // act, prow
+           + (size_t)dhi;                       // panel pivot flags
+}
+
+template <int NT, int RPT>  // threads, panel rows per thread (d <= NT * RPT)
+__global__ void __launch_bounds__(NT, 2) k_block_lu_blk(LuParams p, int dlo, int dhi, int ldmax) {
+    constexpr int NW = NT / 32;
+    extern __shared__ __align__(16) float bsm[];
+    const int d4hi = blk_ld(dhi);
+    float* Lm = bsm;                                  // [dhi][32]
+    float* U = Lm + (size_t)dhi * 32;                 // [32][d4hi]
+    int* act = reinterpret_cast<int*>(U + (size_t)32 * d4hi);
+    int* prow = act + dhi;
+    unsigned char* pflag = reinterpret_cast<unsigned char*>(prow + dhi);
+    __shared__ __align__(16) float Pv[32];            // pivot row of the current column
+    __shared__ unsigned long long red[NW];
+    __shared__ double redd[NW];
+    __shared__ int pc[32];
+    __shared__ int sh_na;
+
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    float* A = p.scratch + (size_t)blockIdx.x * ldmax * ldmax;
+
+    for (int b = blockIdx.x; b < p.s; b += gridDim.x) {
+        const int o = p.bstart[b];
+        const int d = p.bstart[b + 1] - o;
+        if (d <= dlo || d > dhi) continue;
+        const int ld = blk_ld(d);
+        for (int e = tid; e < d * ld; e += NT) A[e] = 0.0f;
+        for (int r = tid; r < d; r += NT) act[r] = r;
+        __syncthreads();
+        // gather (FP64 -> FP32) + FP64 inf-norm, row sums in column order
+        double wmax = 0.0;
+        for (int r = tid; r < d; r += NT) {
+            const int kb = __ldg(p.a.rp + o + r), ke = __ldg(p.a.rp + o + r + 1);
+            double rs = 0.0;
+            for (int k = kb; k < ke; ++k) {
+                const int c = __ldg(p.a.ci + k) - o;
+                if (c >= 0 && c < d) {
+                    const double v = __ldg(p.a.val + k);
+                    A[r * ld + c] = __double2float_rn(v);
+                    rs = __dadd_rn(rs, fabs(v));
+                }
+            }
+            wmax = fmax(wmax, rs);
+        }
+#pragma unroll
+        for (int o2 = 16; o2 > 0; o2 >>= 1) wmax = fmax(wmax, __shfl_xor_sync(0xffffffffu, wmax, o2));
+        if (lane == 0) redd[wid] = wmax;
+        __syncthreads();
+        double norm = 0.0;
+        for (int w = 0; w < NW; ++w) norm = fmax(norm, redd[w]);
+
+        int na = d;
+        int nperturb = 0;
+        bool abort = false;
+        for (int k0 = 0; k0 < d; k0 += 32) {
+            const int kw = min(32, d - k0);
+            // (1) panel rows into registers: position a = tid + 256 i
+            float rv[RPT][32];
+            bool fl[RPT];
+            int arow[RPT];
+#pragma unroll
+            for (int i = 0; i < RPT; ++i) {
+                const int a = tid + NT * i;
+                fl[i] = a >= na;  // no row: treated as already pivotal
+                arow[i] = a < na ? act[a] : 0;
+                const float4* src = reinterpret_cast<const float4*>(A + arow[i] * ld + k0);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (!fl[i] && 4 * q < kw) v = src[q];  // columns >= d: zero
+                    rv[i][4 * q + 0] = v.x;
+                    rv[i][4 * q + 1] = v.y;
+                    rv[i][4 * q + 2] = v.z;
+                    rv[i][4 * q + 3] = v.w;
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < 32; ++c) {
+                if (c >= kw) break;
+                const int k = k0 + c;
+                // pivot: max |a_rk| over unpivoted rows, ties -> smallest row
+                unsigned long long best = 0ull;
+#pragma unroll
+                for (int i = 0; i < RPT; ++i) {
+                    if (fl[i]) continue;
+                    const float v = fabsf(rv[i][c]);
+                    const unsigned long long key = ((unsigned long long)(__float_as_uint(v) + 1u) << 32) |
+                                                   ((unsigned long long)(0xFFFFu - (unsigned)arow[i]) << 16) |
+                                                   (unsigned)(tid + NT * i);
+                    best = umax64(best, key);
+                }
+#pragma unroll
+                for (int o2 = 16; o2 > 0; o2 >>= 1) best = umax64(best, __shfl_xor_sync(0xffffffffu, best, o2));
+                if (lane == 0) red[wid] = best;
+                __syncthreads();
+                unsigned long long f = red[0];
+#pragma unroll
+                for (int w = 1; w < NW; ++w) f = umax64(f, red[w]);
+                const int apos = (int)(f & 0xFFFFu);
+                const int pr = act[apos];
+                const int own = (apos - tid) % NT == 0 && apos >= tid ? (apos - tid) / NT : -1;
+#pragma unroll
+                for (int i = 0; i < RPT; ++i)  // broadcast the pivot row's panel entries
+                    if (own == i)
+#pragma unroll
+                        for (int c2 = 0; c2 < 32; ++c2) Pv[c2] = rv[i][c2];
+                __syncthreads();
+                // regularize_pivot (lu.cpp:10-20), FP64, identical in every thread
+                const double pvd = (double)Pv[c];
+                const bool keep = norm == 0.0 ? (pvd != 0.0) : (fabs(pvd) / norm >= p.eps);
+                const double val = keep ? pvd : ((pvd < 0.0 ? -1.0 : 1.0) * p.eps * norm);
+                if (val == 0.0) {
+                    if (tid == 0) atomicMin(p.singular, ((unsigned long long)b << 32) | (unsigned)k);
+                    abort = true;
+                    break;
+                }
+                if (!keep) {
+                    ++nperturb;
+                    if (tid == 0) {
+                        const int slot = atomicAdd(p.pert_n, 1);
+                        if (slot < p.pert_cap) p.pert[slot] = PertRecord{b, k, pvd, val};
+                    }
+                }
+                const float pv = (float)val;
+                if (tid == 0) {
+                    prow[k] = pr;
+                    pc[c] = apos;
+                }
+#pragma unroll
+                for (int i = 0; i < RPT; ++i) {
+                    if (fl[i]) continue;
+                    if (own == i) {
+                        rv[i][c] = pv;
+                        fl[i] = true;
+                        continue;
+                    }
+                    const float l = rv[i][c] / pv;  // L(i,k) = x_i / pivot (lu.cpp:207)
+                    rv[i][c] = l;
+#pragma unroll
+                    for (int c2 = c + 1; c2 < 32; ++c2) rv[i][c2] = fmaf(-l, Pv[c2], rv[i][c2]);
+                }
+            }
+            if (abort) break;
+            // panel entries back to the tile (multipliers of every row, L11\U11 of
+            // the pivot rows) and the multipliers to 16-byte shared rows; pivot flags
+#pragma unroll
+            for (int i = 0; i < RPT; ++i) {
+                const int a = tid + NT * i;
+                if (a >= na) continue;
+                float4* dstg = reinterpret_cast<float4*>(A + arow[i] * ld + k0);
+                float4* dsts = reinterpret_cast<float4*>(Lm + a * 32);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const float4 v = make_float4(rv[i][4 * q], rv[i][4 * q + 1], rv[i][4 * q + 2], rv[i][4 * q + 3]);
+                    if (4 * q < kw) dstg[q] = v;  // kw % 4 != 0 only for the last panel (d's own padding)
+                    dsts[q] = v;
+                }
+            }
+            // pivot flags from the (uniform) pivot positions of this panel
+            for (int a = tid; a < na; a += NT) pflag[a] = 0;
+            __syncthreads();
+            if (tid < kw) pflag[pc[tid]] = 1;
+            // (2) U12: pivot rows' entries right of the panel, forward substitution
+            const int j0 = k0 + kw, nj = d - j0;
+            for (int jj = tid; jj < nj; jj += NT) {
+                float x[32];
+#pragma unroll
+                for (int c = 0; c < 32; ++c) x[c] = c < kw ? A[act[pc[c]] * ld + j0 + jj] : 0.0f;
+#pragma unroll
+                for (int c = 1; c < 32; ++c) {
+                    if (c >= kw) break;
+                    const float* lrow = Lm + pc[c] * 32;
+#pragma unroll
+                    for (int m = 0; m < c; ++m) x[c] = fmaf(-lrow[m], x[m], x[c]);
+                }
+#pragma unroll
+                for (int c = 0; c < 32; ++c) {
+                    if (c < kw) {
+                        U[c * d4hi + jj] = x[c];
+                        A[act[pc[c]] * ld + j0 + jj] = x[c];
+                    }
+                }
+            }
+            __syncthreads();
+            // (3) trailing rank-32 update (kw < 32 only in the last panel, which
+            // has no trailing part)
+            if (nj > 0) {
+                for (int jc = 0; jc < nj; jc += 32) {
+                    const int jj = jc + lane;
+                    const bool colok = jj < nj;
+                    float u[32];
+#pragma unroll
+                    for (int m = 0; m < 32; ++m) u[m] = colok ? U[m * d4hi + jj] : 0.0f;
+                    for (int a0 = wid; a0 < na; a0 += 4 * NW) {
+                        float v[4];
+                        bool ok[4];
+#pragma unroll
+                        for (int r = 0; r < 4; ++r) {
+                            const int a = a0 + r * NW;
+                            ok[r] = colok && a < na && !pflag[a];
+                            v[r] = ok[r] ? A[act[a] * ld + j0 + jj] : 0.0f;
+                        }
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+#pragma unroll
+                            for (int r = 0; r < 4; ++r) {
+                                const int a = min(a0 + r * NW, na - 1);
+                                const float4 l4 = reinterpret_cast<const float4*>(Lm + a * 32)[q];
+                                v[r] = fmaf(-l4.x, u[4 * q + 0], v[r]);
+                                v[r] = fmaf(-l4.y, u[4 * q + 1], v[r]);
+                                v[r] = fmaf(-l4.z, u[4 * q + 2], v[r]);
+                                v[r] = fmaf(-l4.w, u[4 * q + 3], v[r]);
+                            }
+                        }
+#pragma unroll
+                        for (int r = 0; r < 4; ++r)
+                            if (ok[r]) A[act[a0 + r * NW] * ld + j0 + jj] = v[r];
+                    }
+                }
+            }
+            __syncthreads();
+            // drop this panel's pivot rows from the active list (order is free:
+            // the pivot rule breaks ties by row index, not list position)
+            if (wid == 0) {
+                int w = 0;
+                for (int base = 0; base < na; base += 32) {
+                    const int a = base + lane;
+                    const bool keepr = a < na && !pflag[a];
+                    const int r = a < na ? act[a] : 0;
+                    const unsigned m = __ballot_sync(0xffffffffu, keepr);
+                    __syncwarp();
+                    if (keepr) act[w + __popc(m & ((1u << lane) - 1u))] = r;
+                    w += __popc(m);
+                    __syncwarp();
+                }
+                if (lane == 0) sh_na = w;
+            }
+            __syncthreads();
+            na = sh_na;
+        }
+        if (tid == 0) p.pert_count[b] = nperturb;
+        if (!abort) {
+            // F = L\U in pivot order into packed 32-row panels: stage the 32 pivot
+            // rows of a panel in shared memory (coalesced row reads), then write the
+            // panel contiguously (streaming stores: F is read once, by the SPK build)
+            const int T = (d + 31) / 32;
+            const int dp4 = (d + 3) & ~3;
+            float* F = p.fac + p.fac_off[b];
+            for (int t = 0; t < T; ++t) {
+                __syncthreads();
+                for (int e = tid; e < 32 * dp4; e += NT) {
+                    const int kk = e / dp4, c = e - kk * dp4;
+                    const int k = 32 * t + kk;
+                    U[kk * d4hi + c] = (k < d && c < d) ? A[prow[k] * ld + c] : ((k == c) ? 1.0f : 0.0f);
+                }
+                __syncthreads();
+                float* Ft = F + (size_t)t * 32 * dp4;
+                for (int e = tid; e < 32 * dp4; e += NT) {
+                    const int c = ((e >> 7) << 2) | (e & 3);
+                    const int kk = (e >> 2) & 31;
+                    __stcs(Ft + e, U[kk * d4hi + c]);
+                }
+            }
+            for (int k = tid; k < d; k += NT) p.piv[o + k] = prow[k];
+        }
+        __syncthreads();
+    }
+}
+
 int lu_smem_dim(int dmax) {
     int d = 1;
     while (d + 1 <= dmax && (size_t)(d + 1) * ((d + 1) | 1) * sizeof(float) <= kLuSmemTile) ++d;
@@ -319,11 +615,35 @@ int lu_smem_dim(int dmax) {
 
 }  // namespace
 
+// resident CTAs per SM of the blocked kernel (registers and shared memory):
+// the grid is exactly one wave, and the scratch holds one tile per CTA
+// (one instance per size range: one panel row per thread up to 256, two above)
+using BlkFn = void (*)(LuParams, int, int, int);
+BlkFn blk_fn(int dhi) { return dhi <= kBlkThreads ? k_block_lu_blk<kBlkThreads, 1> : k_block_lu_blk<kBlkThreads, 2>; }
+
+int blk_ctas_per_sm(int dhi) {
+    const size_t smem = blk_smem_bytes(dhi);
+    const BlkFn fn = blk_fn(dhi);
+    HPBJ_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int occ = 0;
+    HPBJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kBlkThreads, smem));
+    return std::max(occ, 1);
+}
+
 size_t block_lu_scratch_floats(int dmax, int num_sms, int* smem_dim, int* scratch_ld) {
     *smem_dim = lu_smem_dim(dmax);
-    *scratch_ld = dmax | 1;
-    if (dmax <= *smem_dim) return 0;
-    return (size_t)num_sms * 4 * (*scratch_ld) * (*scratch_ld);
+    *scratch_ld = blk_ld(dmax | 1);  // odd-free 16-byte rows for the blocked kernel, >= dmax | 1
+    size_t need = 0;
+    if (dmax > kWarpLuMax) {  // blocked kernels: one tile per resident CTA
+        const int d1 = std::min(dmax, kBlkThreads);
+        need = (size_t)num_sms * blk_ctas_per_sm(d1) * (*scratch_ld) * (*scratch_ld);
+        if (dmax > kBlkThreads)
+            need = std::max(need, (size_t)num_sms * blk_ctas_per_sm(std::min(dmax, kBlkMax)) * (*scratch_ld) *
+                                      (*scratch_ld));
+    }
+    if (dmax > kBlkMax && dmax > *smem_dim)
+        need = std::max(need, (size_t)num_sms * 4 * (*scratch_ld) * (*scratch_ld));
+    return need;
 }
 
 void launch_block_lu(const LuParams& p_in, int dmax, int num_sms, cudaStream_t st, int64_t* launches) {
@@ -357,6 +677,21 @@ void launch_block_lu(const LuParams& p_in, int dmax, int num_sms, cudaStream_t s
         HPBJ_CUDA(cudaGetLastError());
         return;
     }
+    // blocked kernels for dw < d <= 256 and 256 < d <= kBlkMax
+    for (int range = 0; range < 2; ++range) {
+        const int dlo = range == 0 ? dw : kBlkThreads;
+        const int dhi = std::min(dmax, range == 0 ? kBlkThreads : kBlkMax);
+        if (dhi <= dlo) continue;
+        const size_t smem = blk_smem_bytes(dhi);
+        const int grid = std::min(p.s, num_sms * blk_ctas_per_sm(dhi));  // sets the smem attribute
+        blk_fn(dhi)<<<grid, kBlkThreads, smem, st>>>(p, dlo, dhi, p.scratch_ld);
+        *launches += 1;
+    }
+    if (dmax <= kBlkMax) {
+        HPBJ_CUDA(cudaGetLastError());
+        return;
+    }
+    p.warp_dim = kBlkMax;  // the column-by-column kernels take only d > kBlkMax
     const int sd = p.smem_dim;
     const int dsm = std::min(dmax, sd);
     const size_t smem = (size_t)dsm * (dsm | 1) * sizeof(float);
@@ -364,9 +699,11 @@ void launch_block_lu(const LuParams& p_in, int dmax, int num_sms, cudaStream_t s
     int occ = 0;
     HPBJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_block_lu, kLuThreads, smem));
     occ = std::max(occ, 1);
-    const int grid0 = std::min(p.s, num_sms * occ);
-    k_block_lu<<<grid0, kLuThreads, smem, st>>>(p, 0);
-    *launches += 1;
+    if (sd > kBlkMax) {
+        const int grid0 = std::min(p.s, num_sms * occ);
+        k_block_lu<<<grid0, kLuThreads, smem, st>>>(p, 0);
+        *launches += 1;
+    }
     if (dmax > sd) {
         const int grid1 = std::min(p.s, num_sms * 4);
         k_block_lu<<<grid1, kLuThreads, 0, st>>>(p, 1);

@@ -560,6 +560,32 @@ void ensure_graph(hpbj_ctx* c) {
     if (getenv("HPBJ_DEBUG")) fprintf(stderr, "[hpbj] solve graph built (#%d)\n", c->graph_builds);
 }
 
+// Algorithmic HBM bytes: what one pass must move at
+// minimum in the stored formats — each factor/matrix byte and each vector
+// element read or written once.
+double apply_bytes(const hpbj_ctx* c) {
+    const double n = c->A.n;
+    const double idx_b = c->dmax > kIdx16MaxDim ? 4.0 : 2.0;
+    return (4.0 + idx_b) * (double)c->spk_entries          // off-panel value + packed index
+           + (4.0 * 1024 + 16.0) * c->num_panels          // inverse-tile quads read + descriptors
+           + 4.0 * n                                      // pivot rows (int32)
+           + 8.0 * n                                      // v (FP64) in
+           + 4.0 * n                                      // z (FP32) out
+           + 8.0 * (c->s + 1);                            // block / panel starts
+}
+double spmv_bytes(const hpbj_ctx* c) {
+    const double n = c->A.n, nnz = c->A.nnz;
+    return 12.0 * nnz + 4.0 * (n + 1) + 4.0 * n + 8.0 * n;  // val+col, row ptr, z in (FP32), w out
+}
+double orth_bytes(const hpbj_ctx* c, int j) {  // step j: V_0..V_j read twice (dots, update), w in, v_{j+1} out
+    const double n = c->A.n;
+    return 2.0 * 8.0 * n * (j + 1) + 8.0 * n + 8.0 * n;
+}
+double fused_step_bytes(const hpbj_ctx* c, int j) {  // w stays on chip: no SpMV write / orth read of w
+    const double n = c->A.n;
+    return apply_bytes(c) + spmv_bytes(c) - 8.0 * n + orth_bytes(c, j) - 8.0 * n + 8.0 * n /* w to HBM */;
+}
+
 void ensure_hist(hpbj_ctx* c, int64_t max_restarts) {
     const int64_t need = max_restarts * c->kb.m + 1;
     if (c->hist_cap >= need) return;
@@ -647,10 +673,7 @@ void solve(hpbj_ctx* c, const double* d_b, double* d_x, const hpbj_gmres_opts* o
         R.converged = 1;
     } else {
         const bool use_graph = !c->profiling && c->use_graph;
-        // per-kernel events need the unfused kernels
-        c->fused = (c->use_fused && !c->profiling)
-                       ? plan_fused(n, c->s, c->dmax, c->num_sms, m, c->planB.n_long > 0)
-                       : FusedPlan{};
+        c->fused = c->use_fused ? plan_fused(n, c->s, c->dmax, c->num_sms, m, c->planB.n_long > 0) : FusedPlan{};
         if (c->fused.ok && getenv("HPBJ_FUSED_PROF") && !c->d_fprof) {
             HPBJ_CUDA(cudaMalloc(&c->d_fprof, 8 * sizeof(unsigned long long)));
             HPBJ_CUDA(cudaMemset(c->d_fprof, 0, 8 * sizeof(unsigned long long)));
@@ -671,13 +694,26 @@ void solve(hpbj_ctx* c, const double* d_b, double* d_x, const hpbj_gmres_opts* o
             if (c->profiling) c->timer.reserve((size_t)3 * m);
             for (;;) {
                 enqueue_cycle_head(c, 0);
-                if (c->fused.ok) enqueue_cycle_fused(c);
-                else
+                if (c->fused.ok) {
+                    record_kernel(c, 0, true);
+                    enqueue_cycle_fused(c);
+                    record_kernel(c, 0, false);
+                } else {
                     for (int it = 0; it < m; ++it) enqueue_step(c, 0, it);
+                }
                 enqueue_cycle_tail(c, 0);
                 HPBJ_CUDA(cudaMemcpyAsync(&hs, c->d_st, sizeof(hs), cudaMemcpyDeviceToHost, st));
                 HPBJ_CUDA(cudaStreamSynchronize(st));
-                if (c->profiling) {
+                if (c->profiling && c->fused.ok) {
+                    // one launch per cycle; algorithmic bytes summed over its steps
+                    float ms = 0.f;
+                    HPBJ_CUDA(cudaEventElapsedTime(&ms, c->timer.ev[0], c->timer.ev[1]));
+                    hpbj_kernel_stat& ks = c->stats[HPBJ_K_CYCLE];
+                    ks.launches += 1;
+                    ks.total_ms += ms;
+                    ks.steps += hs.last_steps;
+                    for (int j = 0; j < hs.last_steps; ++j) ks.total_bytes += fused_step_bytes(c, j);
+                } else if (c->profiling) {
                     for (int it = 0; it < hs.last_steps; ++it)
                         for (int k = 0; k < 3; ++k) {
                             float ms = 0.f;
@@ -685,6 +721,10 @@ void solve(hpbj_ctx* c, const double* d_b, double* d_x, const hpbj_gmres_opts* o
                                                            c->timer.ev[2 * (3 * it + k) + 1]));
                             c->stats[k].launches += 1;
                             c->stats[k].total_ms += ms;
+                            c->stats[k].steps += 1;
+                            c->stats[k].total_bytes += k == 0   ? apply_bytes(c)
+                                                       : k == 1 ? spmv_bytes(c)
+                                                                : orth_bytes(c, it);
                         }
                 }
                 if (hs.converged || hs.cycles >= hs.max_restarts || hs.last_steps == 0) break;
@@ -780,25 +820,17 @@ int hpbj_get_kernel_stats(hpbj_ctx* ctx, hpbj_kernel_stat* out) {
     t_pool = &ctx->pool;
     t_slots = &ctx->slots;
     return guard(&ctx->err, [&] {
-        // algorithmic bytes per launch
-        const double n = ctx->A.n, nnz = ctx->A.nnz;
-        double bytes_apply = 0.0;
-        if (ctx->has_pc) {
-            const double idx_b = ctx->dmax > kIdx16MaxDim ? 4.0 : 2.0;
-            bytes_apply = (4.0 + idx_b) * (double)ctx->spk_entries  // off-panel value + packed index
-                          + (4.0 * 1024 + 16.0) * ctx->num_panels    // tile quads read (8 of 9 per pass) + descriptors
-                          + 4.0 * n                               // pivot rows (int32)
-                          + 8.0 * n                               // v (FP64) in
-                          + 4.0 * n                               // z (FP32) out
-                          + 8.0 * (ctx->s + 1);                   // block / panel starts
+        for (int k = 0; k < HPBJ_K_COUNT; ++k) {
+            out[k] = ctx->stats[k];
+            out[k].bytes_per_launch = out[k].launches ? out[k].total_bytes / (double)out[k].launches : 0.0;
         }
-        const double bytes_spmv = 12.0 * nnz + 4.0 * (n + 1) + 4.0 * n + 8.0 * n;
-        for (int k = 0; k < HPBJ_K_COUNT; ++k) out[k] = ctx->stats[k];
-        out[HPBJ_K_APPLY].bytes_per_launch = bytes_apply;
-        out[HPBJ_K_SPMV].bytes_per_launch = bytes_spmv;
-        // MGS bytes depend on j: mean over recorded launches is computed by the caller
-        out[HPBJ_K_MGS].bytes_per_launch = 0.0;
     });
+}
+
+int hpbj_set_fused(hpbj_ctx* ctx, int enable) {
+    if (!ctx) return HPBJ_EINVAL;
+    ctx->use_fused = enable != 0;
+    return HPBJ_OK;
 }
 
 int hpbj_set_matrix(hpbj_ctx* ctx, int64_t n, const int64_t* row_ptr, const int64_t* col, const double* val) {
