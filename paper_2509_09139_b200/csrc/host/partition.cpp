@@ -221,8 +221,10 @@ void fit(std::vector<T>& v, size_t n) {
     if (v.size() < n) v.resize(n);
 }
 
-// Graph view: neighbours of u are idx[st[u] .. st[u+1]) whose weight w[k] is
-// kept by the reference rule !(w <= 0) (graph.cpp:41); deg[u] counts them.
+// Graph view: neighbours of u are idx[st[u] .. st[u+1]) with weights w[k];
+// deg[u] = st[u+1] - st[u]. Every edge takes part in growing and refinement
+// (partition.cpp:96-97, :122-125); dropping w <= 0 pairs is graph_from_matrix's
+// job (graph.cpp:41) and happens when the view is built (partition_csr).
 template <class Idx>
 struct GraphView {
     int64_t n;
@@ -250,7 +252,6 @@ void partition_view(const GraphView<Idx>& g, int64_t s, double tol, int64_t* ass
     const Idx* nb = g.idx;
     const double* w = g.w;
     const int64_t* deg = g.deg;
-    auto kept = [&](int64_t k) { return !(w[k] <= 0.0); };
 
     // per-node state: >= 0 block id, -1 unassigned, -2 unassigned and queued
     constexpr int32_t kFree = -1, kQueued = -2;
@@ -313,7 +314,7 @@ void partition_view(const GraphView<Idx>& g, int64_t s, double tol, int64_t* ass
             --connected_left;
             for (int64_t k = st[u]; k < st[u + 1]; ++k) {
                 const int64_t v = nb[k];
-                if (state[v] == kFree && kept(k)) {
+                if (state[v] == kFree) {
                     state[v] = kQueued;
                     queue[tail++] = (int32_t)v;
                 }
@@ -359,13 +360,13 @@ void partition_view(const GraphView<Idx>& g, int64_t s, double tol, int64_t* ass
         }
         const int32_t bu = state[u];
         if (sizes[bu] <= 1) continue;
-        // Interior fast path: with every kept neighbour in bu the reference
+        // Interior fast path: with every neighbour in bu the reference
         // touches only bu, which is never a candidate -> no move, no state
         // change (identical outcome, no floating-point work).
         {
             int64_t k = st[u];
             const int64_t ke = st[u + 1];
-            while (k < ke && (!kept(k) || state[nb[k]] == bu)) ++k;
+            while (k < ke && state[nb[k]] == bu) ++k;
             if (k == ke) continue;
         }
         const int64_t du = st[u + 1] - st[u];
@@ -376,7 +377,6 @@ void partition_view(const GraphView<Idx>& g, int64_t s, double tol, int64_t* ass
         }
         int nt = 0;
         for (int64_t k = st[u]; k < st[u + 1]; ++k) {
-            if (!kept(k)) continue;
             const int32_t bv = state[nb[k]];
             if (conn[bv] == 0.0) tch[nt++] = bv;
             conn[bv] += w[k];

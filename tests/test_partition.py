@@ -157,6 +157,36 @@ def test_partition_of_explicit_graph_matches_reference(ref, n, s):
     assert np.array_equal(a.assignment, r)
 
 
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_explicit_graph_with_nonpositive_weights_matches_reference(ref, seed):
+    """A hand-built WeightedGraph may carry w <= 0 edges (graph_from_matrix never
+    emits them): partition_graph still grows over and refines with every edge
+    (partition.cpp:96-97, :122-125), including touched-twice blocks when
+    conn returns to 0.0."""
+    rng = np.random.default_rng(seed)
+    n = 60
+    pairs = {}
+    for i in range(n):
+        for j in rng.choice(n, 4, replace=False):
+            if i != j:
+                pairs[(min(i, j), max(i, j))] = float(rng.choice([-1.0, 0.0, 0.5, 1.0, 2.0]))
+    adj = [[] for _ in range(n)]
+    for (i, j), w in pairs.items():
+        adj[i].append((j, w))
+        adj[j].append((i, w))
+    st, nb, ws = [0], [], []
+    for i in range(n):
+        for j, w in sorted(adj[i]):
+            nb.append(j)
+            ws.append(w)
+        st.append(len(nb))
+    g = hp.WeightedGraph(n, np.array(st, np.int64), np.array(nb, np.int64), np.array(ws))
+    for s in (2, 5, 9):
+        a = hp.partition_graph(g, s, 0.1)
+        r = ref.partition_graph(g.start, g.neighbor, g.weight, s, 0.1)
+        assert np.array_equal(a.assignment, r)
+
+
 def test_laplacian_and_mesh_fixtures_match_reference(ref):
     for a, s in [(fx.laplacian_2d(32, 32), 16), (fx.laplacian_2d(16, 16), 8), (fx.laplacian_2d(8, 8), 4),
                  (fx.convection_diffusion_2d(10, 10, 2.0, 1.0), 4), (fx.random_dd(80, 4, 55), 4)]:
