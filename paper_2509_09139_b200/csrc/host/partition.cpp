@@ -312,12 +312,13 @@ void partition_view(const GraphView<Idx>& g, int64_t s, double tol, int64_t* ass
             ++sizes[b];
             ++grown;
             --connected_left;
-            for (int64_t k = st[u]; k < st[u + 1]; ++k) {
-                const int64_t v = nb[k];
-                if (state[v] == kFree) {
-                    state[v] = kQueued;
-                    queue[tail++] = (int32_t)v;
-                }
+            for (int64_t k = st[u]; k < st[u + 1]; ++k) {  // branch-free push of the free neighbours
+                const int32_t v = (int32_t)nb[k];
+                const int32_t sv = state[v];
+                const bool fr = sv == kFree;
+                queue[tail] = v;
+                tail += fr;
+                state[v] = fr ? kQueued : sv;
             }
         }
         for (int64_t q = head; q < tail; ++q) state[queue[q]] = kFree;  // queue.clear()
@@ -378,7 +379,8 @@ void partition_view(const GraphView<Idx>& g, int64_t s, double tol, int64_t* ass
         int nt = 0;
         for (int64_t k = st[u]; k < st[u + 1]; ++k) {
             const int32_t bv = state[nb[k]];
-            if (conn[bv] == 0.0) tch[nt++] = bv;
+            tch[nt] = bv;  // recorded while its conn is still 0.0 (partition.cpp:123-124)
+            nt += conn[bv] == 0.0;
             conn[bv] += w[k];
         }
         int32_t best = -1;
@@ -421,28 +423,46 @@ void partition_csr(int64_t n, const int64_t* rp, const int64_t* ci, const double
     fit(W.deg, n);
     double* wk = W.wk.data();
     int64_t* deg = W.deg.data();
+    // Weights of the upper-triangle entries, written to both the entry and its
+    // mirror (one binary search per pair). w = 0.5 * (|a_pq| + |a_qp|) with
+    // p < q, the reference's accumulation order (graph.cpp:24-33). The pattern
+    // is symmetric iff every upper entry finds its mirror and the upper and
+    // lower entry counts agree (the mirrors are then all the lower entries).
     int missing = 0;
-#pragma omp parallel for schedule(dynamic, 2048) reduction(| : missing)
+    int64_t nup = 0, nlo = 0;
+#pragma omp parallel for schedule(dynamic, 2048) reduction(| : missing) reduction(+ : nup, nlo)
     for (int64_t u = 0; u < n; ++u) {
-        int64_t d = 0;
         for (int64_t k = rp[u]; k < rp[u + 1]; ++k) {
             const int64_t j = ci[k];
+            if (j < u) {
+                ++nlo;
+                continue;
+            }
             if (j == u) {
                 wk[k] = -1.0;
                 continue;
             }
+            ++nup;
             const int64_t* b = ci + rp[j];
             const int64_t* e = ci + rp[j + 1];
             const int64_t* it = std::lower_bound(b, e, u);
             if (it == e || *it != u) {
                 missing = 1;
-                break;
+                continue;
             }
             const double wt = 0.5 * (std::fabs(val[k]) + std::fabs(val[it - ci]));
             wk[k] = wt;
-            if (!(wt <= 0.0)) ++d;
+            wk[it - ci] = wt;
         }
-        deg[u] = d;
+    }
+    if (nup != nlo) missing = 1;
+    if (!missing) {
+#pragma omp parallel for schedule(static, 4096)
+        for (int64_t u = 0; u < n; ++u) {
+            int64_t d = 0;
+            for (int64_t k = rp[u]; k < rp[u + 1]; ++k) d += !(wk[k] <= 0.0);
+            deg[u] = d;
+        }
     }
     if (missing) {
         const Adjacency g = graph_general(n, rp, ci, val);
