@@ -307,7 +307,12 @@ def roofline_of(kern, peak, peak_kind, config):
     tpath = os.path.join(ROOT, "profiles", f"ncu_traffic_config{config}.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(dom)
+            t = json.load(open(tpath))
+            traffic = t.get(dom)
+            if traffic is not None and dom == "arnoldi_cycle_fused":
+                # captured launch = one cycle of t[...steps] steps; scale to this run's mean steps per launch
+                per_step = traffic / t.get("arnoldi_cycle_fused_steps", 1)
+                traffic = per_step * kern[dom]["steps"] / kern[dom]["launches"]
         except Exception:
             traffic = None
     return {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
