@@ -21,7 +21,7 @@ INC = os.path.join(ROOT, "include")
 
 NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
+NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC,-fopenmp",
               "-Xptxas", "-v", "-I" + INC, "-I" + CSRC] + ARCH
 CXX_FLAGS = ["-std=c++20", "-O3", "-fPIC", "-fopenmp", "-ffp-contract=off", "-I" + INC, "-I" + CSRC]
 

@@ -38,6 +38,34 @@ __device__ __forceinline__ unsigned long long umax64(unsigned long long a, unsig
     return a > b ? a : b;
 }
 
+// regularize_pivot's keep test (lu.cpp:10-20): norm == 0 ? p != 0 :
+// RN(|p| / norm) >= eps. A product bracket decides it without the FP64
+// division whenever |p| is not within 2^-48 (relative) of eps*norm: with
+// t = RN(eps*norm) normal, |p| >= RN(t*(1+2^-48)) implies the exact quotient
+// exceeds eps*(1+2^-49), so its rounding is >= eps; |p| <= RN(t*(1-2^-48))
+// implies it is below eps*(1-2^-49), so its rounding is < eps. Otherwise (and
+// for eps = 0, NaN, or t out of the normal range) the quotient is formed.
+__device__ __forceinline__ bool pivot_keep(double pvd, double norm, double eps) {
+    if (norm == 0.0) return pvd != 0.0;
+    const double a = fabs(pvd);
+    const double t = eps * norm;
+    if (t >= DBL_MIN && t <= DBL_MAX * 0.5) {
+        if (a >= t * (1.0 + 0x1p-48)) return true;
+        if (a <= t * (1.0 - 0x1p-48)) return false;
+    }
+    return a / norm >= eps;
+}
+
+// Warp argmax of |x| with ties to the smallest row: returns the winning row
+// (value key = float bits + 1 so that "no candidate" = 0; NaN keys win, as in
+// the 64-bit (value, ~row) key max).
+__device__ __forceinline__ int warp_pivot_row(unsigned key, int row, unsigned* kmax) {
+    const unsigned mx = __reduce_max_sync(0xffffffffu, key);
+    const unsigned pr = __reduce_min_sync(0xffffffffu, key == mx ? (unsigned)row : 0xFFFFFFFFu);
+    *kmax = mx;
+    return (int)pr;
+}
+
 // mode 0: blocks with d <= smem_dim (tile in shared memory)
 // mode 1: blocks with d >  smem_dim (tile in global scratch)
 __global__ void __launch_bounds__(kLuThreads) k_block_lu(LuParams p, int mode) {
@@ -183,7 +211,7 @@ __global__ void __launch_bounds__(kLuThreads) k_block_lu(LuParams p, int mode) {
 // (d <= kWarpLuMax): warp-synchronous right-looking elimination — lane l owns
 // rows l, l+32, ... — so no CTA barrier sits on the per-column critical path.
 // Same pivot rule, regularisation and output as k_block_lu.
-constexpr int kWarpLuMax = 96;  // measured: above this the CTA kernel is faster
+constexpr int kWarpLuMax = 96;  // measured: above this the blocked kernel is faster
 
 template <int kWarpLuRowsPerLane>  // rows per lane = ceil(max block dim / 32)
 __global__ void __launch_bounds__(256) k_block_lu_warp(LuParams p, int dw, int ldw) {
@@ -224,24 +252,25 @@ __global__ void __launch_bounds__(256) k_block_lu_warp(LuParams p, int dw, int l
         bool abort = false;
         for (int k = 0; k < d; ++k) {
             // pivot: max |a_rk| over unpivoted rows, ties -> smallest row
-            unsigned long long best = 0ull;
+            unsigned bk = 0u;
+            int brow = 0x7fffffff;
 #pragma unroll
             for (int q = 0; q < kWarpLuRowsPerLane; ++q) {
                 const int r = lane + 32 * q;
                 if (r < d && !((pivoted >> q) & 1u)) {
-                    const float v = fabsf(A[r * ld + k]);
-                    const unsigned long long key = ((unsigned long long)(__float_as_uint(v) + 1u) << 32) |
-                                                   (unsigned long long)(0xFFFFu - (unsigned)r);
-                    best = umax64(best, key);
+                    const unsigned key = __float_as_uint(fabsf(A[r * ld + k])) + 1u;
+                    if (key > bk) {  // rows ascend with q: an equal key keeps the smaller row
+                        bk = key;
+                        brow = r;
+                    }
                 }
             }
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) best = umax64(best, __shfl_xor_sync(0xffffffffu, best, off));
-            const int pr = (int)(0xFFFFu - (unsigned)(best & 0xFFFFu));
+            unsigned kmx;
+            const int pr = warp_pivot_row(bk, brow, &kmx);
             const float xp = A[pr * ld + k];
             // regularize_pivot (lu.cpp:10-20), FP64, identical in every lane
             const double pvd = (double)xp;
-            const bool keep = nrm == 0.0 ? (pvd != 0.0) : (fabs(pvd) / nrm >= p.eps);
+            const bool keep = pivot_keep(pvd, nrm, p.eps);
             const double val = keep ? pvd : ((pvd < 0.0 ? -1.0 : 1.0) * p.eps * nrm);
             if (val == 0.0) {
                 if (lane == 0) atomicMin(p.singular, ((unsigned long long)b << 32) | (unsigned)k);
@@ -274,18 +303,53 @@ __global__ void __launch_bounds__(256) k_block_lu_warp(LuParams p, int dw, int l
                     A[r * ld + k] = lq[q];
                 }
             }
-            // rank-1 update, pivot-row value loaded once per column for all
-            // of the lane's rows; rows with l == 0 are left bit-unchanged
-            const int nq = (d - lane + 31) >> 5;  // rows owned by this lane
-#pragma unroll 2
-            for (int j = k + 1; j < d; ++j) {
-                const float u = urow[j];
+            // rank-1 update with lanes over columns (j = k+1+lane+32c): the live
+            // rows (unpivoted, l != 0; a uniform ballot mask) are walked four at a
+            // time — their multipliers are shared-memory broadcasts and every
+            // lane updates its own columns, so there is no divergence and the
+            // loads of four rows are in flight together. Rows with l == 0 are
+            // left bit-unchanged.
+            unsigned lmask[kWarpLuRowsPerLane];
 #pragma unroll
-                for (int q = 0; q < kWarpLuRowsPerLane; ++q)
-                    if (q < nq && lq[q] != 0.0f) {
-                        float* a = A + (lane + 32 * q) * ld + j;
-                        *a = fmaf(-lq[q], u, *a);
+            for (int q = 0; q < kWarpLuRowsPerLane; ++q) lmask[q] = __ballot_sync(0xffffffffu, lq[q] != 0.0f);
+            constexpr int C = kWarpLuRowsPerLane;  // column groups (d <= 32 C)
+            float ucol[C];
+            bool cj[C];
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                const int j = k + 1 + lane + 32 * c;
+                cj[c] = j < d;
+                ucol[c] = cj[c] ? urow[j] : 0.0f;
+            }
+            float* Aj = A + k + 1 + lane;
+#pragma unroll
+            for (int q = 0; q < kWarpLuRowsPerLane; ++q) {
+                unsigned m = lmask[q];
+                while (m) {
+                    int rr[4];
+                    int nr = 0;
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        rr[t] = m ? 32 * q + __ffs(m) - 1 : -1;
+                        if (m) {
+                            m &= m - 1;
+                            ++nr;
+                        }
                     }
+                    float l[4], a[4][C];
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        l[t] = rr[t] >= 0 ? A[rr[t] * ld + k] : 0.0f;
+#pragma unroll
+                        for (int c = 0; c < C; ++c) a[t][c] = (rr[t] >= 0 && cj[c]) ? Aj[rr[t] * ld + 32 * c] : 0.0f;
+                    }
+#pragma unroll
+                    for (int t = 0; t < 4; ++t)
+#pragma unroll
+                        for (int c = 0; c < C; ++c)
+                            if (rr[t] >= 0 && cj[c]) Aj[rr[t] * ld + 32 * c] = fmaf(-l[t], ucol[c], a[t][c]);
+                    (void)nr;
+                }
             }
             __syncwarp();
         }
@@ -351,7 +415,8 @@ __global__ void __launch_bounds__(NT, 2) k_block_lu_blk(LuParams p, int dlo, int
     int* prow = act + dhi;
     unsigned char* pflag = reinterpret_cast<unsigned char*>(prow + dhi);
     __shared__ __align__(16) float Pv[32];            // pivot row of the current column
-    __shared__ unsigned long long red[NW];
+    __shared__ unsigned red_k[NW];
+    __shared__ int red_r[NW], red_a[NW];
     __shared__ double redd[NW];
     __shared__ int pc[32];
     __shared__ int sh_na;
@@ -419,24 +484,39 @@ __global__ void __launch_bounds__(NT, 2) k_block_lu_blk(LuParams p, int dlo, int
                 if (c >= kw) break;
                 const int k = k0 + c;
                 // pivot: max |a_rk| over unpivoted rows, ties -> smallest row
-                unsigned long long best = 0ull;
+                unsigned bk = 0u;
+                int brow = 0x7fffffff, bpos = 0;
 #pragma unroll
                 for (int i = 0; i < RPT; ++i) {
                     if (fl[i]) continue;
-                    const float v = fabsf(rv[i][c]);
-                    const unsigned long long key = ((unsigned long long)(__float_as_uint(v) + 1u) << 32) |
-                                                   ((unsigned long long)(0xFFFFu - (unsigned)arow[i]) << 16) |
-                                                   (unsigned)(tid + NT * i);
-                    best = umax64(best, key);
+                    const unsigned key = __float_as_uint(fabsf(rv[i][c])) + 1u;
+                    if (key > bk || (key == bk && arow[i] < brow)) {
+                        bk = key;
+                        brow = arow[i];
+                        bpos = tid + NT * i;
+                    }
                 }
-#pragma unroll
-                for (int o2 = 16; o2 > 0; o2 >>= 1) best = umax64(best, __shfl_xor_sync(0xffffffffu, best, o2));
-                if (lane == 0) red[wid] = best;
+                {
+                    unsigned kmx;
+                    const int wr = warp_pivot_row(bk, brow, &kmx);
+                    const unsigned own_l = __ballot_sync(0xffffffffu, bk == kmx && brow == wr);
+                    const int wpos = __shfl_sync(0xffffffffu, bpos, __ffs(own_l) - 1);
+                    if (lane == 0) {
+                        red_k[wid] = kmx;
+                        red_r[wid] = wr;
+                        red_a[wid] = wpos;
+                    }
+                }
                 __syncthreads();
-                unsigned long long f = red[0];
+                unsigned fk = red_k[0];
+                int frow = red_r[0], apos = red_a[0];
 #pragma unroll
-                for (int w = 1; w < NW; ++w) f = umax64(f, red[w]);
-                const int apos = (int)(f & 0xFFFFu);
+                for (int w = 1; w < NW; ++w)
+                    if (red_k[w] > fk || (red_k[w] == fk && red_r[w] < frow)) {
+                        fk = red_k[w];
+                        frow = red_r[w];
+                        apos = red_a[w];
+                    }
                 const int pr = act[apos];
                 const int own = (apos - tid) % NT == 0 && apos >= tid ? (apos - tid) / NT : -1;
 #pragma unroll
@@ -447,7 +527,7 @@ __global__ void __launch_bounds__(NT, 2) k_block_lu_blk(LuParams p, int dlo, int
                 __syncthreads();
                 // regularize_pivot (lu.cpp:10-20), FP64, identical in every thread
                 const double pvd = (double)Pv[c];
-                const bool keep = norm == 0.0 ? (pvd != 0.0) : (fabs(pvd) / norm >= p.eps);
+                const bool keep = pivot_keep(pvd, norm, p.eps);
                 const double val = keep ? pvd : ((pvd < 0.0 ? -1.0 : 1.0) * p.eps * norm);
                 if (val == 0.0) {
                     if (tid == 0) atomicMin(p.singular, ((unsigned long long)b << 32) | (unsigned)k);

@@ -138,6 +138,9 @@ struct hpbj_ctx {
     bool has_matrix = false;
     DevCsr A;
     std::vector<int64_t> h_rp;
+    std::vector<int> h_perm32;      // bj_setup scratch (persistent: no page faults per setup)
+    std::vector<uint32_t> h_seen;   // bijection check, generation-stamped
+    uint32_t seen_gen = 0;
     SpmvPlan planA;
     double* d_tmpx = nullptr;  // n
     double* d_tmpy = nullptr;  // n
@@ -287,24 +290,37 @@ struct hpbj_ctx {
 
 namespace {
 
-// Lanes per row from the mean row length; hub rows go to the CTA kernel.
-void make_plan(SpmvPlan& p, const std::vector<int64_t>& rp, const int* perm_or_null, int n) {
-    p.n_long = 0;
-    const double avg = n > 0 ? double(rp[n]) / n : 0.0;
+// Lanes per row from the mean row length; hub rows get CTAs of their own.
+int spmv_group(int64_t nnz, int n) {
+    const double avg = n > 0 ? double(nnz) / n : 0.0;
     // measured on B200 (configs 1-3): one thread per row wins up to
     // ~7.5 nnz/row (FP32 x gathers stay in L1/L2), then 2/4/8 lanes
-    p.group = avg <= 7.5 ? 1 : avg <= 16.0 ? 2 : avg <= 32.0 ? 4 : avg <= 64.0 ? 8 : 32;
-    if (const char* e = getenv("HPBJ_SPMV_G")) p.group = atoi(e);
-    p.long_thresh = std::max(256, 16 * p.group);
-    std::vector<int> rows;
-    for (int i = 0; i < n; ++i)
-        if (rp[i + 1] - rp[i] > p.long_thresh) rows.push_back(perm_or_null ? perm_or_null[i] : i);
+    int g = avg <= 7.5 ? 1 : avg <= 16.0 ? 2 : avg <= 32.0 ? 4 : avg <= 64.0 ? 8 : 32;
+    if (const char* e = getenv("HPBJ_SPMV_G")) g = atoi(e);
+    return g;
+}
+int spmv_long_thresh(int g) { return std::max(256, 16 * g); }
+
+// rows: indices (in the matrix's own numbering) of rows longer than the
+// plan's threshold, in any order
+void set_plan(SpmvPlan& p, int group, std::vector<int>& rows) {
+    p.group = group;
+    p.long_thresh = spmv_long_thresh(group);
     std::sort(rows.begin(), rows.end());
     p.n_long = (int)rows.size();
     if (p.n_long) {
         dslot(p.long_rows, rows.size());
         HPBJ_CUDA(cudaMemcpy(p.long_rows, rows.data(), sizeof(int) * rows.size(), cudaMemcpyHostToDevice));
     }
+}
+
+void make_plan(SpmvPlan& p, const std::vector<int64_t>& rp, const int* perm_or_null, int n) {
+    const int g = spmv_group(rp[n], n);
+    const int thr = spmv_long_thresh(g);
+    std::vector<int> rows;
+    for (int i = 0; i < n; ++i)
+        if (rp[i + 1] - rp[i] > thr) rows.push_back(perm_or_null ? perm_or_null[i] : i);
+    set_plan(p, g, rows);
 }
 
 void ensure_ws(hpbj_ctx* c, int m) {
@@ -902,17 +918,52 @@ int hpbj_bj_setup(hpbj_ctx* ctx, int64_t s, const int64_t* perm, const int64_t* 
     return guard(&ctx->err, [&] {
         if (!ctx->has_matrix) fail(HPBJ_ELOGIC, "block_jacobi: no matrix");
         if (eps_pivot < 0.0) fail(HPBJ_EINVAL, "gp_lu: negative eps_pivot");
+        const bool dbg = getenv("HPBJ_DEBUG") != nullptr;
+        auto tnow = [] { return std::chrono::steady_clock::now(); };
+        auto tms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+        const auto T0 = tnow();
         const int n = ctx->A.n;
         if (s < 1 || s > n) fail(HPBJ_EINVAL, "partition: block count must satisfy 1 <= s <= n");
-        // validate the partition (bijection, contiguous nonempty blocks)
-        std::vector<int> hperm(n);
-        std::vector<char> seen(n, 0);
-        for (int i = 0; i < n; ++i) {
-            const int64_t p = perm[i];
-            if (p < 0 || p >= n || seen[p]) fail(HPBJ_EINVAL, "permute_symmetric: not a bijection");
-            seen[p] = 1;
-            hperm[i] = (int)p;
+        // validate the partition (bijection, contiguous nonempty blocks) and,
+        // in the same pass over the rows, collect the rows that need a CTA sort
+        // after the scatter and the SpMV hub rows (permuted indices)
+        std::vector<int>& hperm = ctx->h_perm32;
+        std::vector<uint32_t>& seen = ctx->h_seen;
+        if ((int)hperm.size() < n) hperm.resize(n);
+        if ((int)seen.size() < n) seen.assign(n, 0u);
+        const uint32_t gen = ++ctx->seen_gen;
+        const int spg = spmv_group(ctx->A.nnz, n), spthr = spmv_long_thresh(spg);
+        std::vector<int> lrows, hubs;
+        int maxlen = 0, bad = 0;
+#pragma omp parallel if (n > 65536)
+        {
+            std::vector<int> lr, hb;
+            int ml = 0;
+#pragma omp for schedule(static) reduction(| : bad) nowait
+            for (int i = 0; i < n; ++i) {
+                const int64_t p = perm[i];
+                if (p < 0 || p >= n) {
+                    bad = 1;
+                    continue;
+                }
+                // a repeated target shows up as a second stamp of the same generation
+                if (__atomic_exchange_n(&seen[p], gen, __ATOMIC_RELAXED) == gen) bad = 1;
+                hperm[i] = (int)p;
+                const int len = (int)(ctx->h_rp[i + 1] - ctx->h_rp[i]);
+                if (len > kShortRow) {
+                    lr.push_back((int)p);
+                    ml = std::max(ml, len);
+                    if (len > spthr) hb.push_back((int)p);
+                }
+            }
+#pragma omp critical
+            {
+                lrows.insert(lrows.end(), lr.begin(), lr.end());
+                hubs.insert(hubs.end(), hb.begin(), hb.end());
+                maxlen = std::max(maxlen, ml);
+            }
         }
+        if (bad) fail(HPBJ_EINVAL, "permute_symmetric: not a bijection");
         if (block_starts[0] != 0 || block_starts[s] != n)
             fail(HPBJ_EINVAL, "block_jacobi: partition does not cover the matrix");
         std::vector<int> bst(s + 1);
@@ -925,6 +976,7 @@ int hpbj_bj_setup(hpbj_ctx* ctx, int64_t s, const int64_t* perm, const int64_t* 
             bst[b] = (int)block_starts[b];
         }
         bst[s] = n;
+        const auto T1 = tnow();
         ctx->release_pc();
         cudaStream_t st = ctx->stream;
         ctx->s = (int)s;
@@ -973,16 +1025,7 @@ int hpbj_bj_setup(hpbj_ctx* ctx, int64_t s, const int64_t* perm, const int64_t* 
         HPBJ_CUDA(cudaMemcpyAsync(ctx->d_bstart, bst.data(), sizeof(int) * (s + 1), cudaMemcpyHostToDevice, st));
         HPBJ_CUDA(cudaMemcpyAsync(ctx->d_fac_off, ctx->h_fac_off.data(), sizeof(int64_t) * s,
                                   cudaMemcpyHostToDevice, st));
-        // rows needing a CTA sort after the scatter (permuted indices)
-        std::vector<int> lrows;
-        int maxlen = 0;
-        for (int i = 0; i < n; ++i) {
-            const int len = (int)(ctx->h_rp[i + 1] - ctx->h_rp[i]);
-            if (len > kShortRow) {
-                lrows.push_back(hperm[i]);
-                maxlen = std::max(maxlen, len);
-            }
-        }
+        const auto T2 = tnow();
         ctx->n_long_sort = (int)lrows.size();
         ctx->max_long_sort = maxlen;
         if (!lrows.empty()) {
@@ -990,7 +1033,8 @@ int hpbj_bj_setup(hpbj_ctx* ctx, int64_t s, const int64_t* perm, const int64_t* 
             HPBJ_CUDA(cudaMemcpyAsync(ctx->d_long_sort, lrows.data(), sizeof(int) * lrows.size(),
                                       cudaMemcpyHostToDevice, st));
         }
-        make_plan(ctx->planB, ctx->h_rp, hperm.data(), n);
+        set_plan(ctx->planB, spg, hubs);
+        const auto T3 = tnow();
         int* tmp = dalloc<int>((size_t)n + 8192);
         cudaEvent_t e0, e1;
         HPBJ_CUDA(cudaEventCreate(&e0));
@@ -1006,8 +1050,12 @@ int hpbj_bj_setup(hpbj_ctx* ctx, int64_t s, const int64_t* perm, const int64_t* 
         cudaEventDestroy(e1);
         dput(tmp);
         ctx->has_pc = true;
+        const auto T4 = tnow();
         factor(ctx, info);
         if (info) info->ms_permute = ms;
+        if (dbg)
+            fprintf(stderr, "[hpbj] bj_setup host: validate %.3f alloc+h2d %.3f longrows+plan %.3f permute(sync) %.3f "
+                            "factor %.3f ms\n", tms(T0, T1), tms(T1, T2), tms(T2, T3), tms(T3, T4), tms(T4, tnow()));
     });
 }
 
