@@ -120,6 +120,33 @@ struct KernelTimer {
     }
 };
 
+// Grow-only page-locked staging buffer for host<->device copies at full
+// PCIe/C2C speed; an event fences reuse while a previous async copy is in flight.
+struct PinnedBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaEvent_t ev = nullptr;
+    void* get(size_t bytes) {
+        if (ev) HPBJ_CUDA(cudaEventSynchronize(ev));
+        if (bytes > cap) {
+            if (p) cudaFreeHost(p);
+            p = nullptr;
+            cap = 0;
+            HPBJ_CUDA(cudaHostAlloc(&p, bytes, cudaHostAllocDefault));
+            cap = bytes;
+        }
+        return p;
+    }
+    void fence(cudaStream_t st) {
+        if (!ev) HPBJ_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        HPBJ_CUDA(cudaEventRecord(ev, st));
+    }
+    ~PinnedBuf() {
+        if (ev) cudaEventDestroy(ev);
+        if (p) cudaFreeHost(p);
+    }
+};
+
 constexpr double kU53 = 1.1102230246251565e-16;  // 2^-53
 constexpr double kU24 = 5.9604644775390625e-08;  // 2^-24
 
@@ -138,7 +165,10 @@ struct hpbj_ctx {
     bool has_matrix = false;
     DevCsr A;
     std::vector<int64_t> h_rp;
+    PinnedBuf stage_mat;  // set_matrix: int32 rp, int32 ci, FP64 val
+    PinnedBuf stage_vec;  // hpbj_gmres host path: b, x
     std::vector<int> h_perm32;      // bj_setup scratch (persistent: no page faults per setup)
+    std::vector<int> h_rowlen_perm; // row lengths of Q A Q^T
     std::vector<uint32_t> h_seen;   // bijection check, generation-stamped
     uint32_t seen_gen = 0;
     SpmvPlan planA;
@@ -509,7 +539,7 @@ std::vector<uintptr_t> graph_signature(const hpbj_ctx* c) {
             (uintptr_t)c->d_dtile, (uintptr_t)c->d_eval, (uintptr_t)c->d_eidx, (uintptr_t)L.grid, (uintptr_t)L.threads, (uintptr_t)L.slice,
             (uintptr_t)L.smem, (uintptr_t)L.icwy, (uintptr_t)L.w_in_smem, (uintptr_t)c->fused.ok,
             (uintptr_t)c->fused.grid, (uintptr_t)c->fused.slice, (uintptr_t)c->fused.ystride,
-            (uintptr_t)c->fused.smem, (uintptr_t)c->d_ent_off};
+            (uintptr_t)c->fused.smem, (uintptr_t)c->fused.nnz_cap, (uintptr_t)c->d_ent_off};
 }
 
 // The whole restart loop as one CUDA graph: WHILE(cycles) { cycle_init;
@@ -689,7 +719,9 @@ void solve(hpbj_ctx* c, const double* d_b, double* d_x, const hpbj_gmres_opts* o
         R.converged = 1;
     } else {
         const bool use_graph = !c->profiling && c->use_graph;
-        c->fused = c->use_fused ? plan_fused(n, c->s, c->dmax, c->num_sms, m, c->planB.n_long > 0) : FusedPlan{};
+        c->fused = c->use_fused ? plan_fused(n, c->s, c->dmax, c->num_sms, m, c->planB.n_long > 0,
+                                             c->h_rowlen_perm.data())
+                                : FusedPlan{};
         if (c->fused.ok && getenv("HPBJ_FUSED_PROF") && !c->d_fprof) {
             HPBJ_CUDA(cudaMalloc(&c->d_fprof, 8 * sizeof(unsigned long long)));
             HPBJ_CUDA(cudaMemset(c->d_fprof, 0, 8 * sizeof(unsigned long long)));
@@ -861,17 +893,33 @@ int hpbj_set_matrix(hpbj_ctx* ctx, int64_t n, const int64_t* row_ptr, const int6
         ctx->release_matrix();
         ctx->release_ws();
         const int ni = (int)n, nnz = (int)row_ptr[n];
-        std::vector<int> rp(ni + 1), ci(nnz);
-        for (int64_t i = 0; i <= n; ++i) rp[i] = (int)row_ptr[i];
-        for (int64_t k = 0; k < nnz; ++k) ci[k] = (int)col[k];
+        // int64 -> int32 indices and the FP64 values straight into pinned
+        // staging (parallel), then asynchronous copies on the context stream
+        const size_t b_rp = sizeof(int) * ((size_t)ni + 1), b_ci = sizeof(int) * (size_t)nnz;
+        const size_t o_ci = (b_rp + 15) & ~(size_t)15, o_val = (o_ci + b_ci + 15) & ~(size_t)15;
+        char* stg = static_cast<char*>(ctx->stage_mat.get(o_val + sizeof(double) * (size_t)nnz));
+        int* rp = reinterpret_cast<int*>(stg);
+        int* ci = reinterpret_cast<int*>(stg + o_ci);
+        double* vs = reinterpret_cast<double*>(stg + o_val);
+#pragma omp parallel
+        {
+#pragma omp for schedule(static) nowait
+            for (int64_t i = 0; i <= n; ++i) rp[i] = (int)row_ptr[i];
+#pragma omp for schedule(static) nowait
+            for (int64_t k = 0; k < nnz; ++k) ci[k] = (int)col[k];
+#pragma omp for schedule(static)
+            for (int64_t k = 0; k < nnz; ++k) vs[k] = val[k];
+        }
         ctx->A.n = ni;
         ctx->A.nnz = nnz;
         dslot(ctx->A.rp, ni + 1);
         dslot(ctx->A.ci, nnz);
         dslot(ctx->A.val, nnz);
-        HPBJ_CUDA(cudaMemcpy(ctx->A.rp, rp.data(), sizeof(int) * (ni + 1), cudaMemcpyHostToDevice));
-        HPBJ_CUDA(cudaMemcpy(ctx->A.ci, ci.data(), sizeof(int) * nnz, cudaMemcpyHostToDevice));
-        HPBJ_CUDA(cudaMemcpy(ctx->A.val, val, sizeof(double) * nnz, cudaMemcpyHostToDevice));
+        cudaStream_t st = ctx->stream;
+        HPBJ_CUDA(cudaMemcpyAsync(ctx->A.rp, rp, b_rp, cudaMemcpyHostToDevice, st));
+        HPBJ_CUDA(cudaMemcpyAsync(ctx->A.ci, ci, b_ci, cudaMemcpyHostToDevice, st));
+        HPBJ_CUDA(cudaMemcpyAsync(ctx->A.val, vs, sizeof(double) * (size_t)nnz, cudaMemcpyHostToDevice, st));
+        ctx->stage_mat.fence(st);  // later work on the stream is ordered after the copies
         ctx->h_rp.assign(row_ptr, row_ptr + n + 1);
         make_plan(ctx->planA, ctx->h_rp, nullptr, ni);
         dslot(ctx->d_tmpx, ni);
@@ -933,6 +981,8 @@ int hpbj_bj_setup(hpbj_ctx* ctx, int64_t s, const int64_t* perm, const int64_t* 
         if ((int)seen.size() < n) seen.assign(n, 0u);
         const uint32_t gen = ++ctx->seen_gen;
         const int spg = spmv_group(ctx->A.nnz, n), spthr = spmv_long_thresh(spg);
+        if ((int)ctx->h_rowlen_perm.size() < n) ctx->h_rowlen_perm.resize(n);
+        int* rowlen = ctx->h_rowlen_perm.data();
         std::vector<int> lrows, hubs;
         int maxlen = 0, bad = 0;
 #pragma omp parallel if (n > 65536)
@@ -950,6 +1000,7 @@ int hpbj_bj_setup(hpbj_ctx* ctx, int64_t s, const int64_t* perm, const int64_t* 
                 if (__atomic_exchange_n(&seen[p], gen, __ATOMIC_RELAXED) == gen) bad = 1;
                 hperm[i] = (int)p;
                 const int len = (int)(ctx->h_rp[i + 1] - ctx->h_rp[i]);
+                rowlen[p] = len;
                 if (len > kShortRow) {
                     lr.push_back((int)p);
                     ml = std::max(ml, len);
@@ -1155,10 +1206,16 @@ int hpbj_gmres(hpbj_ctx* ctx, const double* b, double* x, const hpbj_gmres_opts*
         const int m = opts ? (int)opts->restart_m : 50;
         if (m >= 1) ensure_ws(ctx, m);
         else fail(HPBJ_EINVAL, "gmres: invalid config");
-        HPBJ_CUDA(cudaMemcpyAsync(ctx->d_bo, b, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+        double* sb = static_cast<double*>(ctx->stage_vec.get(sizeof(double) * 2 * (size_t)n));
+        double* sx = sb + n;
+#pragma omp parallel for schedule(static) if (n > 65536)
+        for (int i = 0; i < n; ++i) sb[i] = b[i];
+        HPBJ_CUDA(cudaMemcpyAsync(ctx->d_bo, sb, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
         solve(ctx, ctx->d_bo, ctx->d_xo, opts, rep, hist, hist_cap, cycle_res, cyc_cap);
-        HPBJ_CUDA(cudaMemcpyAsync(x, ctx->d_xo, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+        HPBJ_CUDA(cudaMemcpyAsync(sx, ctx->d_xo, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
         HPBJ_CUDA(cudaStreamSynchronize(ctx->stream));
+#pragma omp parallel for schedule(static) if (n > 65536)
+        for (int i = 0; i < n; ++i) x[i] = sx[i];
     });
 }
 

@@ -18,11 +18,13 @@
 //            cycle-exit flags).
 //   barrier  (z complete; exit flags visible)
 //   phase 2  w = A z for the CTA's rows into shared memory (FP64, G lanes per
-//            row as in spmv.cu, hub rows split over the CTA)
+//            row as in spmv.cu; the CTA's matrix rows are loaded into shared
+//            memory once per cycle)
 //   phase 3  compact-WY multi-dot c = V^T w, l = V^T v_j, ||w||^2 (see
 //            arnoldi.cu k_icwy), one warp per basis vector
 //   barrier  (partials)
-//   phase 4  h = (I + L)^-1 c by two Jacobi sweeps; w -= V h in MGS order;
+//   phase 4  h = (I + L)^-1 c by two Jacobi sweeps (every CTA keeps its own
+//            copy of the Gram table in shared memory); w -= V h in MGS order;
 //            w slice to HBM; ||w||^2
 //   barrier  (partials, w)
 //   phase 5  h_{j+1,j} = ||w||, breakdown test, v_{j+1} = w / h for the own slice
@@ -75,6 +77,7 @@ struct FusedArgs {
     int npad;
     int slice;
     int ystride;
+    int nnz_cap;               // matrix slice capacity (entries) in shared memory
     unsigned long long* prof;  // optional: CTA 0 phase timers [4], ns
 };
 
@@ -190,14 +193,31 @@ __global__ void __launch_bounds__(kThreads, 1) k_arnoldi_cycle(FusedArgs a) {
         }
     };
 
-    // per-warp apply buffers after the w slice
+    // dynamic shared memory: [w slice][v_j slice][Gram (m+1)^2][matrix slice:
+    // val, ci, local rp][per-warp apply buffers]
+    double* gram = dsm + 2 * a.slice;                         // row i: <v_i, v_k>, k < i
+    double* mval = gram + (size_t)ldl * ldl;
+    int* mci = reinterpret_cast<int*>(mval + a.nnz_cap);
+    int* mrp = mci + a.nnz_cap;                               // slice + 1 local row starts
     float* ybuf;
     SpkPanel* dsh;
     {
-        unsigned char* base = reinterpret_cast<unsigned char*>(dsm + 2 * a.slice);
+        unsigned char* base = reinterpret_cast<unsigned char*>(mrp + ((a.slice + 2) & ~1) + 2);
+        base = reinterpret_cast<unsigned char*>(((uintptr_t)base + 15) & ~(uintptr_t)15);
         const size_t per = sizeof(float) * a.ystride + sizeof(SpkPanel) * (a.ystride / 32);
         ybuf = reinterpret_cast<float*>(base + per * wid);
         dsh = reinterpret_cast<SpkPanel*>(base + per * wid + sizeof(float) * a.ystride);
+    }
+    // the CTA's rows of the (permuted) matrix stay in shared memory for the cycle
+    const int nrows = max(0, min(len, a.n - r0));
+    {
+        const int kb = nrows > 0 ? __ldg(a.a.rp + r0) : 0;
+        for (int r = tid; r <= nrows; r += kThreads) mrp[r] = __ldg(a.a.rp + r0 + r) - kb;
+        const int ke = nrows > 0 ? __ldg(a.a.rp + r0 + nrows) : 0;
+        for (int q = tid; q < ke - kb; q += kThreads) {
+            mval[q] = __ldg(a.a.val + kb + q);
+            mci[q] = __ldg(a.a.ci + kb + q);
+        }
     }
     if (blockIdx.x == 0)
         for (int i = tid; i <= m; i += kThreads) gs.g[i] = (i == 0) ? st->beta : 0.0;
@@ -232,54 +252,32 @@ __global__ void __launch_bounds__(kThreads, 1) k_arnoldi_cycle(FusedArgs a) {
         pending = false;
         lap(0);
 
-        // ---- phase 2: w = A z on the own rows (spmv.cu k_spmv / k_spmv_long)
-        for (int k = 0; k < a.n_long; ++k) {  // hub rows: whole CTA
-            const int row = __ldg(a.long_rows + k);
-            if (row < r0 || row >= r0 + len) continue;
-            const int b = __ldg(a.a.rp + row), e = __ldg(a.a.rp + row + 1);
-            double s = 0.0;
-            if (tid < 512)
-                for (int q = b + tid; q < e; q += 512) s = fma(__ldg(a.a.val + q), (double)__ldcg(a.z32 + __ldg(a.a.ci + q)), s);
-            s = warp_sum(s);
-            __syncthreads();
-            if (lane == 0 && wid < 16) wred[wid] = s;
-            __syncthreads();
-            if (wid == 0) {
-                double t = lane < 16 ? wred[lane] : 0.0;
-                t = warp_sum(t);
-                if (lane == 0) wsh[row - r0] = t;
-            }
-        }
+        // ---- phase 2: w = A z on the own rows (as spmv.cu k_spmv: G lanes per
+        // row, four strides of loads in flight), matrix slice from shared memory
         {
             const int Gl = a.group;
             const int gl = tid & (Gl - 1);
             const unsigned gmask = (Gl == 32) ? 0xffffffffu : (((1u << Gl) - 1u) << (lane & ~(Gl - 1)));
             for (int r = tid / Gl; r < len; r += kThreads / Gl) {
-                const int row = r0 + r;
                 double sum = 0.0;
-                bool skip = false;
-                if (row < a.n) {
-                    const int b = __ldg(a.a.rp + row), e = __ldg(a.a.rp + row + 1);
-                    if (e - b > a.long_thresh) {
-                        skip = true;
-                    } else {
-                        for (int q0 = b + gl; q0 < e; q0 += 4 * Gl) {  // as spmv.cu: loads of four strides in flight
-                            int c[4];
-                            double v[4];
+                if (r < nrows) {
+                    const int b = mrp[r], e = mrp[r + 1];
+                    for (int q0 = b + gl; q0 < e; q0 += 4 * Gl) {
+                        int c[4];
+                        double v[4];
 #pragma unroll
-                            for (int u = 0; u < 4; ++u) {
-                                const int q = q0 + u * Gl;
-                                c[u] = q < e ? __ldg(a.a.ci + q) : 0;
-                                v[u] = q < e ? __ldg(a.a.val + q) : 0.0;
-                            }
-#pragma unroll
-                            for (int u = 0; u < 4; ++u)
-                                if (q0 + u * Gl < e) sum = fma(v[u], (double)__ldcg(a.z32 + c[u]), sum);
+                        for (int u = 0; u < 4; ++u) {
+                            const int q = q0 + u * Gl;
+                            c[u] = q < e ? mci[q] : 0;
+                            v[u] = q < e ? mval[q] : 0.0;
                         }
-                        for (int o = Gl / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(gmask, sum, o, Gl);
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            if (q0 + u * Gl < e) sum = fma(v[u], (double)__ldcg(a.z32 + c[u]), sum);
                     }
+                    for (int o = Gl / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(gmask, sum, o, Gl);
                 }
-                if (gl == 0 && !skip) wsh[r] = sum;
+                if (gl == 0) wsh[r] = sum;
             }
         }
         __syncthreads();
@@ -349,9 +347,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_arnoldi_cycle(FusedArgs a) {
         pre_norm = sqrt(tot[2 * (j + 1)]);
         auto sweep = [&](const double* src, double* dst) {
             for (int i = wid; i <= j; i += kWarps) {
-                const double* Lrow = (i == j) ? tot + (j + 1) : a.gram + (size_t)i * ldl;
+                const double* Lrow = (i == j) ? tot + (j + 1) : gram + (size_t)i * ldl;
                 double sacc = 0.0;
-                for (int k = lane; k < i; k += 32) sacc = fma(i == j ? Lrow[k] : __ldcg(Lrow + k), src[k], sacc);
+                for (int k = lane; k < i; k += 32) sacc = fma(Lrow[k], src[k], sacc);
                 sacc = warp_sum(sacc);
                 if (lane == 0) dst[i] = tot[i] - sacc;
             }
@@ -359,10 +357,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_arnoldi_cycle(FusedArgs a) {
         };
         sweep(tot, h1);
         sweep(h1, hsh);
-        if (blockIdx.x == 0) {
+        for (int k = tid; k < j; k += kThreads) gram[(size_t)j * ldl + k] = tot[(j + 1) + k];  // every CTA's copy
+        if (blockIdx.x == 0)
             for (int i = tid; i <= j; i += kThreads) a.kb.H[(size_t)j * (m + 1) + i] = hsh[i];
-            for (int k = tid; k < j; k += kThreads) a.gram[(size_t)j * ldl + k] = tot[(j + 1) + k];
-        }
         double ss2 = 0.0;
         {
             double2* wg = reinterpret_cast<double2*>(a.kb.w + r0);
@@ -428,25 +425,34 @@ size_t apply_warp_bytes(int ystride) { return sizeof(float) * ystride + sizeof(S
 
 }  // namespace
 
-FusedPlan plan_fused(int n, int s, int dmax, int num_sms, int m, bool has_long) {
+FusedPlan plan_fused(int n, int s, int dmax, int num_sms, int m, bool has_long, const int* rowlen) {
     FusedPlan F;
     if (m > kMaxRestart || n <= 0 || dmax > kIdx16MaxDim) return F;
+    if (has_long) return F;  // hub rows: the per-kernel path gives them whole CTAs
     const int npad = (n + 1) & ~1;
     const int ystride = ((dmax + 31) / 32) * 32;
-    if (has_long) return F;  // hub rows: the per-kernel path splits them over whole CTAs
     // every SM: the apply phase is latency bound, more warps in flight win
-    int grid = std::max(1, std::min(num_sms, npad / 64));
+    const int grid = std::max(1, std::min(num_sms, npad / 64));
     int slice = (npad + grid - 1) / grid;
     slice = (slice + 1) & ~1;
-    const size_t smem = (size_t)2 * slice * sizeof(double) + (size_t)kWarps * apply_warp_bytes(ystride);
-    const size_t static_smem = sizeof(double) * (2 * (2 * kMaxRestart + 4) +
-                                                 2 * (kMaxRestart + 1) + kWarps) +
+    int nnz_cap = 0;  // largest matrix slice
+    for (int c = 0; c < grid; ++c) {
+        int64_t t = 0;
+        for (int r = c * slice; r < std::min(n, (c + 1) * slice); ++r) t += rowlen[r];
+        nnz_cap = (int)std::max<int64_t>(nnz_cap, t);
+    }
+    nnz_cap = (nnz_cap + 1) & ~1;
+    const size_t smem = (size_t)2 * slice * sizeof(double) + (size_t)(m + 1) * (m + 1) * sizeof(double) +
+                        (size_t)nnz_cap * (sizeof(double) + sizeof(int)) + (size_t)(((slice + 2) & ~1) + 2) * sizeof(int) +
+                        16 + (size_t)kWarps * apply_warp_bytes(ystride);
+    const size_t static_smem = sizeof(double) * (2 * (2 * kMaxRestart + 4) + 2 * (kMaxRestart + 1) + kWarps) +
                                sizeof(GivensSmem) + 1024;
     if (smem + static_smem > kSmemMax) return F;
     F.ok = true;
     F.grid = grid;
     F.slice = slice;
     F.ystride = ystride;
+    F.nnz_cap = nnz_cap;
     F.smem = smem;
     return F;
 }
@@ -455,7 +461,7 @@ void launch_arnoldi_cycle(const FusedPlan& F, const SpkView& pc, const DevCsr& a
                           const KrylovBufs& kb, double* gram, SolveState* sst, GridBarrier* gb, float* z32,
                           unsigned long long* prof, cudaStream_t st, int64_t* launches) {
     FusedArgs args{pc, a, plan.group, plan.long_thresh, plan.n_long, plan.long_rows, kb, gram, sst, gb, z32,
-                   a.n, (a.n + 1) & ~1, F.slice, F.ystride, prof};
+                   a.n, (a.n + 1) & ~1, F.slice, F.ystride, F.nnz_cap, prof};
     HPBJ_CUDA(cudaFuncSetAttribute((const void*)k_arnoldi_cycle, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)F.smem));
     cudaLaunchConfig_t cfg = {};

@@ -202,9 +202,12 @@ struct FusedPlan {
     int grid = 0;
     int slice = 0;
     int ystride = 0;
+    int nnz_cap = 0;
     size_t smem = 0;
 };
-FusedPlan plan_fused(int n, int s, int dmax, int num_sms, int m, bool has_long);
+// rowlen: row lengths of the permuted matrix (the CTA slices' matrix rows are
+// cached in shared memory)
+FusedPlan plan_fused(int n, int s, int dmax, int num_sms, int m, bool has_long, const int* rowlen);
 void launch_arnoldi_cycle(const FusedPlan& F, const SpkView& pc, const DevCsr& a, const SpmvPlan& plan,
                           const KrylovBufs& kb, double* gram, SolveState* sst, GridBarrier* gb, float* z32,
                           unsigned long long* prof, cudaStream_t st, int64_t* launches);
