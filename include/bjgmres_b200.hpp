@@ -33,7 +33,13 @@ private:
 };
 
 namespace detail {
-inline void check(int rc, const char* msg, index_t column = -1) {
+// The message is fetched only after the call has returned (rc is an argument,
+// so it is evaluated before check runs): ctx == nullptr selects the calling
+// thread's last context-free error.
+inline void check(int rc, const hpbj_ctx* ctx, index_t column = -1) {
+    if (rc == HPBJ_OK) return;
+    const std::string m = hpbj_last_error(ctx);
+    const char* msg = m.c_str();
     switch (rc) {
         case HPBJ_OK: return;
         case HPBJ_EINVAL: throw std::invalid_argument(msg);
@@ -86,7 +92,7 @@ inline Partition partition_graph(const SparseMatrix& a, index_t s, double imbala
     p.block_starts.resize(s + 1);
     detail::check(hpbj_partition_graph(a.rows(), a.row_starts().data(), a.col_indices().data(), a.values().data(), s,
                                        imbalance_tol, p.assignment.data(), p.perm.data(), p.block_starts.data()),
-                  hpbj_last_error(nullptr));
+                  nullptr);
     return p;
 }
 
@@ -97,7 +103,7 @@ inline Partition partition_from_assignment(std::vector<index_t> assignment, inde
     p.block_starts.resize(s + 1);
     detail::check(hpbj_partition_from_assignment(static_cast<index_t>(assignment.size()), assignment.data(), s,
                                                  p.perm.data(), p.block_starts.data()),
-                  hpbj_last_error(nullptr));
+                  nullptr);
     p.assignment = std::move(assignment);
     return p;
 }
@@ -121,14 +127,14 @@ public:
             throw std::invalid_argument("block_jacobi: partition does not cover the matrix");
         Preconditioner p;
         hpbj_ctx* raw = nullptr;
-        detail::check(hpbj_create(&raw, device), hpbj_last_error(nullptr));
+        detail::check(hpbj_create(&raw, device), nullptr);
         p.ctx_ = std::shared_ptr<hpbj_ctx>(raw, hpbj_destroy);
         detail::check(hpbj_set_matrix(raw, a.rows(), a.row_starts().data(), a.col_indices().data(), a.values().data()),
-                      hpbj_last_error(raw));
+                      raw);
         hpbj_setup_info info{};
         const int rc = hpbj_bj_setup(raw, partition.num_blocks, partition.perm.data(), partition.block_starts.data(),
                                      opts.eps_pivot, &info);
-        detail::check(rc, hpbj_last_error(raw), info.singular_column);
+        detail::check(rc, raw, info.singular_column);
         p.n_ = a.rows();
         p.matrix_ = &a;
         p.partition_ = std::make_shared<const Partition>(std::move(partition));
@@ -142,12 +148,12 @@ public:
         if (static_cast<index_t>(v.size()) != n_)
             throw std::invalid_argument("preconditioner apply: dimension mismatch");
         std::vector<double> z(n_);
-        detail::check(hpbj_bj_apply(ctx_.get(), v.data(), z.data()), hpbj_last_error(ctx_.get()));
+        detail::check(hpbj_bj_apply(ctx_.get(), v.data(), z.data()), ctx_.get());
         return z;
     }
     std::vector<PreconditionerStats> stats() const {
         std::vector<index_t> d(partition_->num_blocks), pc(partition_->num_blocks);
-        detail::check(hpbj_get_block_stats(ctx_.get(), d.data(), pc.data()), hpbj_last_error(ctx_.get()));
+        detail::check(hpbj_get_block_stats(ctx_.get(), d.data(), pc.data()), ctx_.get());
         std::vector<PreconditionerStats> out(d.size());
         for (size_t b = 0; b < d.size(); ++b) out[b] = {d[b], pc[b]};
         return out;
@@ -215,7 +221,7 @@ inline SolveResult hybrid_restart_gmres(const SparseMatrix& a, const Preconditio
     hpbj_report rep{};
     detail::check(hpbj_gmres(p.context(), b.data(), out.x.data(), &o, &rep, hist.data(),
                              static_cast<int64_t>(hist.size()), cyc.data(), static_cast<int64_t>(cyc.size())),
-                  hpbj_last_error(p.context()));
+                  p.context());
     SolveReport& r = out.report;
     r.converged = rep.converged != 0;
     r.total_iterations = rep.total_iterations;

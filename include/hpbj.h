@@ -40,6 +40,7 @@ extern "C" {
 #define HPBJ_ENOMEM 5
 #define HPBJ_ERANGE 6
 #define HPBJ_ENODEV 7
+#define HPBJ_EIO 8       /* file / parse errors (std::runtime_error)        */
 
 typedef struct hpbj_ctx hpbj_ctx;
 
@@ -186,6 +187,23 @@ int hpbj_gmres_device(hpbj_ctx* ctx, const double* d_b, double* d_x,
                       const hpbj_gmres_opts* opts, hpbj_report* rep,
                       hpbj_history_point* hist, int64_t hist_cap, double* cycle_res,
                       int64_t cyc_cap);
+
+/* ---- Matrix Market and binary CSR cache (host) ----------- */
+/* read_matrix_market_file (matrix_market.cpp:36-106): coordinate real/integer,
+ * general/symmetric, 1-based, duplicates summed as SparseMatrix::from_triplets.
+ * The arrays are malloc'ed by the library; release them with hpbj_free.
+ * Parse errors return HPBJ_EIO with "matrix market: line N: ..." in
+ * hpbj_last_error(NULL). */
+int hpbj_mm_read(const char* path, int64_t* nrows, int64_t* ncols, int64_t** row_ptr, int64_t** col,
+                 double** val);
+/* write_matrix_market_file (matrix_market.cpp:108-121): real general, %.17g. */
+int hpbj_mm_write(const char* path, int64_t nrows, int64_t ncols, const int64_t* row_ptr, const int64_t* col,
+                  const double* val);
+/* Binary CSR cache ("HPBJCSR1", n, nnz, int64 row_ptr, int64 col, FP64 val). */
+int hpbj_csr_cache_write(const char* path, int64_t n, const int64_t* row_ptr, const int64_t* col,
+                         const double* val);
+int hpbj_csr_cache_read(const char* path, int64_t* n, int64_t** row_ptr, int64_t** col, double** val);
+void hpbj_free(void* p);
 
 #ifdef __cplusplus
 }

@@ -101,6 +101,21 @@ class Ref:
             np.ascontiguousarray(v, np.float64),
         )
 
+    def mm_read(self, path):
+        """The reference's read_matrix_market_file: (nrows, ncols, rp, ci, val)."""
+        nr, nc, nz = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        self._chk(self.L.bjref_mm_read(os.fsencode(path), ctypes.byref(nr), ctypes.byref(nc), ctypes.byref(nz),
+                                       None, None, None))
+        rp, ci, v = np.zeros(nr.value + 1, np.int64), np.zeros(nz.value, np.int64), np.zeros(nz.value)
+        self._chk(self.L.bjref_mm_read(os.fsencode(path), ctypes.byref(nr), ctypes.byref(nc), ctypes.byref(nz),
+                                       _p(rp, _i64p), _p(ci, _i64p), _p(v, _f64p)))
+        return nr.value, nc.value, rp, ci, v
+
+    def mm_write(self, path, rp, ci, v):
+        rp, ci, v = self._csr(rp, ci, v)
+        self._chk(self.L.bjref_mm_write(os.fsencode(path), ctypes.c_int64(len(rp) - 1), _p(rp, _i64p),
+                                        _p(ci, _i64p), _p(v, _f64p)))
+
     def spmv(self, rp, ci, v, x, fp32=False):
         rp, ci, v = self._csr(rp, ci, v)
         n = len(rp) - 1

@@ -21,6 +21,7 @@
 #include "bjgmres/gmres.hpp"
 #include "bjgmres/graph.hpp"
 #include "bjgmres/lu.hpp"
+#include "bjgmres/matrix_market.hpp"
 #include "bjgmres/partition.hpp"
 #include "bjgmres/preconditioner.hpp"
 #include "bjgmres/sparse_matrix.hpp"
@@ -88,6 +89,30 @@ struct bjref_report {
 };
 
 const char* bjref_last_error(void) { return g_err.c_str(); }
+
+// read_matrix_market_file; rp == nullptr: only report the sizes (nrows,
+// ncols, nnz), else fill rp[nrows+1], ci[nnz], v[nnz].
+int bjref_mm_read(const char* path, int64_t* nrows, int64_t* ncols, int64_t* nnz, int64_t* rp, int64_t* ci,
+                  double* v) {
+    return guarded([&] {
+        const SparseMatrix a = read_matrix_market_file(path);
+        *nrows = a.rows();
+        *ncols = a.cols();
+        *nnz = a.nnz();
+        if (!rp) return;
+        const auto st = a.row_starts();
+        const auto cl = a.col_indices();
+        const auto vl = a.values();
+        std::copy(st.begin(), st.end(), rp);
+        std::copy(cl.begin(), cl.end(), ci);
+        std::copy(vl.begin(), vl.end(), v);
+    });
+}
+
+// write_matrix_market_file
+int bjref_mm_write(const char* path, int64_t n, const int64_t* rp, const int64_t* ci, const double* v) {
+    return guarded([&] { write_matrix_market_file(path, make_matrix(n, rp, ci, v)); });
+}
 
 int bjref_spmv(int64_t n, const int64_t* rp, const int64_t* ci, const double* v,
                const double* x, double* y, int fp32) {

@@ -29,6 +29,7 @@ the host (bit-identical to the reference). There is no CPU fallback.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass, field
 from typing import List, Optional
 
@@ -40,6 +41,8 @@ __all__ = [
     "SparseMatrix", "WeightedGraph", "Partition", "BlockJacobiOptions", "Preconditioner", "GmresConfig",
     "SolveReport", "SolveResult", "HistoryPoint", "SingularBlockError", "LogicError", "graph_from_matrix",
     "partition_graph", "partition_from_assignment", "hybrid_restart_gmres", "Context", "library",
+    "read_matrix_market", "write_matrix_market", "read_csr_cache", "write_csr_cache", "export_partition",
+    "import_partition", "measure_block_nnz", "cut_weight",
 ]
 
 ROUNDOFF_SINGLE = 2.0 ** -24  # types.hpp:12
@@ -224,6 +227,113 @@ def partition_from_assignment(assignment, s: int) -> Partition:
     if rc:
         _raise(rc, lib.hpbj_last_error(None).decode())
     return Partition(s, asg.copy(), perm, bst)
+
+
+# ---------------------------------------------------------------------------
+# Matrix Market / CSR cache / partition files
+def _take_arrays(lib, n_rows, prp, pci, pval):
+    nnz = int(prp[n_rows]) if n_rows >= 0 else 0
+    rp = np.ctypeslib.as_array(prp, (n_rows + 1,)).copy()
+    ci = np.ctypeslib.as_array(pci, (max(nnz, 1),))[:nnz].copy()
+    val = np.ctypeslib.as_array(pval, (max(nnz, 1),))[:nnz].copy()
+    for p_ in (prp, pci, pval):
+        lib.hpbj_free(ctypes.cast(p_, ctypes.c_void_p))
+    return rp, ci, val
+
+
+def read_matrix_market(path: str) -> SparseMatrix:
+    """read_matrix_market_file (matrix_market.cpp:36-106) for square matrices."""
+    lib = library()
+    nr, nc = ctypes.c_int64(), ctypes.c_int64()
+    prp, pci = ctypes.POINTER(ctypes.c_int64)(), ctypes.POINTER(ctypes.c_int64)()
+    pval = ctypes.POINTER(ctypes.c_double)()
+    rc = lib.hpbj_mm_read(os.fsencode(path), ctypes.byref(nr), ctypes.byref(nc), ctypes.byref(prp),
+                          ctypes.byref(pci), ctypes.byref(pval))
+    if rc:
+        _raise(rc, lib.hpbj_last_error(None).decode())
+    rp, ci, val = _take_arrays(lib, nr.value, prp, pci, pval)
+    if nr.value != nc.value:
+        raise ValueError(f"matrix must be square, got {nr.value}x{nc.value}")
+    return SparseMatrix(nr.value, rp, ci, val)
+
+
+def write_matrix_market(path: str, a: SparseMatrix) -> None:
+    """write_matrix_market_file (matrix_market.cpp:108-121): real general, %.17g."""
+    lib = library()
+    rc = lib.hpbj_mm_write(os.fsencode(path), a.n, a.n, _p(a.row_starts, _abi.i64p), _p(a.col_indices, _abi.i64p),
+                           _p(a.values, _abi.f64p))
+    if rc:
+        _raise(rc, lib.hpbj_last_error(None).decode())
+
+
+def write_csr_cache(path: str, a: SparseMatrix) -> None:
+    """Binary CSR cache ("HPBJCSR1"): the configs / SuiteSparse inputs load without parsing."""
+    lib = library()
+    rc = lib.hpbj_csr_cache_write(os.fsencode(path), a.n, _p(a.row_starts, _abi.i64p), _p(a.col_indices, _abi.i64p),
+                                  _p(a.values, _abi.f64p))
+    if rc:
+        _raise(rc, lib.hpbj_last_error(None).decode())
+
+
+def read_csr_cache(path: str) -> SparseMatrix:
+    lib = library()
+    n = ctypes.c_int64()
+    prp, pci = ctypes.POINTER(ctypes.c_int64)(), ctypes.POINTER(ctypes.c_int64)()
+    pval = ctypes.POINTER(ctypes.c_double)()
+    rc = lib.hpbj_csr_cache_read(os.fsencode(path), ctypes.byref(n), ctypes.byref(prp), ctypes.byref(pci),
+                                 ctypes.byref(pval))
+    if rc:
+        _raise(rc, lib.hpbj_last_error(None).decode())
+    rp, ci, val = _take_arrays(lib, n.value, prp, pci, pval)
+    return SparseMatrix(n.value, rp, ci, val)
+
+
+def export_partition(path: str, p: Partition) -> None:
+    """export_partition (partition.cpp:174-176): one block index per line."""
+    with open(path, "w") as f:
+        f.write("".join(f"{int(b)}\n" for b in p.assignment))
+
+
+def import_partition(path: str, n: int, s: int) -> Partition:
+    """import_partition (partition.cpp:145-172): blank lines skipped, errors name the line."""
+    asg = []
+    with open(path) as f:
+        for line_no, line in enumerate(f, 1):
+            tok = line.split()
+            if not tok:
+                continue
+            try:
+                b = int(tok[0])
+            except ValueError:
+                raise RuntimeError(f"partition file: line {line_no}: malformed") from None
+            if b < 0 or b >= s:
+                raise IndexError(f"partition file: line {line_no}: block index {b} out of range")
+            asg.append(b)
+    if len(asg) != n:
+        raise RuntimeError(f"partition file: expected {n} lines, got {len(asg)}")
+    return partition_from_assignment(np.asarray(asg, np.int64), s)
+
+
+def measure_block_nnz(p: Partition, a: SparseMatrix):
+    """measure_block_nnz (partition.cpp:178-195): nnz of each diagonal block and max/mean."""
+    rows = np.repeat(np.arange(a.n), np.diff(a.row_starts))
+    asg = np.asarray(p.assignment)
+    inblk = asg[rows] == asg[a.col_indices]
+    bn = np.bincount(asg[rows][inblk], minlength=p.num_blocks).astype(np.int64)
+    mean = bn.sum() / p.num_blocks
+    return bn, (bn.max() / mean if mean > 0 else 0.0)
+
+
+def cut_weight(g: "WeightedGraph", p: Partition) -> float:
+    """cut_weight (partition.cpp:197-204): sum of w over u < v edges across blocks (u ascending)."""
+    asg = np.asarray(p.assignment)
+    cut = 0.0
+    for u in range(g.num_nodes):
+        for k in range(int(g.start[u]), int(g.start[u + 1])):
+            v = int(g.neighbor[k])
+            if u < v and asg[u] != asg[v]:
+                cut += float(g.weight[k])
+    return cut
 
 
 # ---------------------------------------------------------------------------

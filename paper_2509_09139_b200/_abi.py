@@ -19,6 +19,7 @@ HPBJ_ECUDA = 4
 HPBJ_ENOMEM = 5
 HPBJ_ERANGE = 6
 HPBJ_ENODEV = 7
+HPBJ_EIO = 8
 
 HPBJ_K_APPLY = 0
 HPBJ_K_SPMV = 1
@@ -93,6 +94,17 @@ SIGNATURES = {
     "hpbj_set_profiling": (ctypes.c_int, [vp, ctypes.c_int]),
     "hpbj_get_kernel_stats": (ctypes.c_int, [vp, ctypes.POINTER(KernelStat)]),
     "hpbj_set_fused": (ctypes.c_int, [vp, ctypes.c_int]),
+    "hpbj_mm_read": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(i64), ctypes.POINTER(i64),
+                                    ctypes.POINTER(ctypes.POINTER(i64)), ctypes.POINTER(ctypes.POINTER(i64)),
+                                    ctypes.POINTER(ctypes.POINTER(f64))]),
+    "hpbj_mm_write": (ctypes.c_int, [ctypes.c_char_p, i64, i64, ctypes.POINTER(i64), ctypes.POINTER(i64),
+                                     ctypes.POINTER(f64)]),
+    "hpbj_csr_cache_write": (ctypes.c_int, [ctypes.c_char_p, i64, ctypes.POINTER(i64), ctypes.POINTER(i64),
+                                            ctypes.POINTER(f64)]),
+    "hpbj_csr_cache_read": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(i64),
+                                           ctypes.POINTER(ctypes.POINTER(i64)), ctypes.POINTER(ctypes.POINTER(i64)),
+                                           ctypes.POINTER(ctypes.POINTER(f64))]),
+    "hpbj_free": (None, [vp]),
     "hpbj_graph_from_matrix": (ctypes.c_int, [i64, i64p, i64p, f64p, i64p, i64p, f64p, i64]),
     "hpbj_partition_graph": (ctypes.c_int, [i64, i64p, i64p, f64p, i64, f64, i64p, i64p, i64p]),
     "hpbj_partition_adjacency": (ctypes.c_int, [i64, i64p, i64p, f64p, i64, f64, i64p, i64p, i64p]),

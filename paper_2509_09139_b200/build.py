@@ -26,11 +26,13 @@ NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xc
 CXX_FLAGS = ["-std=c++20", "-O3", "-fPIC", "-fopenmp", "-ffp-contract=off", "-I" + INC, "-I" + CSRC]
 
 CU_SOURCES = ["permute.cu", "block_lu.cu", "spk.cu", "spmv.cu", "arnoldi.cu", "fused.cu", "capi.cu"]
-CPP_SOURCES = ["host/partition.cpp"]
+CPP_SOURCES = ["host/partition.cpp", "host/mmio.cpp"]
 HEADERS = ["device.cuh", "kernels.cuh", "hpbj_common.hpp", "spk_dev.cuh", "sync_dev.cuh"]
 
 LIBHPBJ = os.path.join(LIB, "libhpbj.so")
 LIBGEN = os.path.join(LIB, "libhpbj_gen.so")
+CLI = os.path.join(LIB, "hpbj_cli")
+CLI_SRC = os.path.join(ROOT, "tools", "hpbj_cli.cpp")
 
 
 def _newer(target, deps):
@@ -78,6 +80,10 @@ def build(verbose: bool = False) -> str:
     gsrc = os.path.join(CSRC, "gen", "workloads.cpp")
     if _newer(LIBGEN, [gsrc]):
         _run(["g++", "-std=c++20", "-O2", "-ffp-contract=off", "-fPIC", "-shared", "-o", LIBGEN, gsrc])
+    # the reference-compatible harness (tools/hpbj_cli.cpp) over libhpbj.so
+    if _newer(CLI, [CLI_SRC, LIBHPBJ, os.path.join(INC, "bjgmres_b200.hpp"), os.path.join(INC, "hpbj.h")]):
+        _run(["g++", "-std=c++20", "-O2", "-I" + INC, "-o", CLI, CLI_SRC, "-L" + LIB, "-lhpbj",
+              "-Wl,-rpath,$ORIGIN"], os.path.join(OBJ, "cli.log"))
     if verbose:
         for cmd, log in jobs:
             print(open(log).read())
