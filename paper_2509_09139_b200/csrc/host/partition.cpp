@@ -39,6 +39,8 @@
 #include <utility>
 #include <vector>
 
+#include <omp.h>
+
 #include "../hpbj_common.hpp"
 
 namespace hpbj {
@@ -179,22 +181,43 @@ Adjacency graph_from_csr(int64_t n, const int64_t* rp, const int64_t* ci, const 
     return g;
 }
 
+// Stable gather perm[i] = next[assignment[i]]++ (partition.cpp:14-41), in
+// parallel: each thread counts its contiguous chunk per block, the per-block
+// offsets of the chunks follow from a prefix over (block, thread), and every
+// thread scatters its chunk in order — the same perm as the serial loop.
 void partition_from_assignment(int64_t n, const int64_t* assignment, int64_t s, int64_t* perm,
                                int64_t* block_starts) {
     if (s < 1 || s > n) fail(HPBJ_EINVAL, "partition: block count must satisfy 1 <= s <= n");
-    std::vector<int64_t> counts(s, 0);
-    for (int64_t i = 0; i < n; ++i) {
-        const int64_t b = assignment[i];
-        if (b < 0 || b >= s) fail(HPBJ_ERANGE, "partition: block index out of range");
-        ++counts[b];
+    const int T = n >= (1 << 16) ? std::max(1, std::min(omp_get_max_threads(), 64)) : 1;
+    const int64_t chunk = (n + T - 1) / T;
+    std::vector<int64_t> cnt((size_t)T * s, 0);  // [thread][block]
+    int bad = 0;
+#pragma omp parallel for schedule(static, 1) reduction(| : bad)
+    for (int t = 0; t < T; ++t) {  // every chunk exactly once, whatever the team size
+        int64_t* c = cnt.data() + (size_t)t * s;
+        for (int64_t i = t * chunk; i < std::min(n, (t + 1) * chunk); ++i) {
+            const int64_t b = assignment[i];
+            if (b < 0 || b >= s) bad = 1;
+            else ++c[b];
+        }
     }
-    for (int64_t b = 0; b < s; ++b)
-        if (counts[b] == 0)
-            fail(HPBJ_EINVAL, "partition: block " + std::to_string(b) + " is empty");
+    if (bad) fail(HPBJ_ERANGE, "partition: block index out of range");
     block_starts[0] = 0;
-    for (int64_t b = 0; b < s; ++b) block_starts[b + 1] = block_starts[b] + counts[b];
-    std::vector<int64_t> next(block_starts, block_starts + s);
-    for (int64_t i = 0; i < n; ++i) perm[i] = next[assignment[i]]++;  // stable gather
+    for (int64_t b = 0; b < s; ++b) {
+        int64_t off = block_starts[b];
+        for (int t = 0; t < T; ++t) {
+            const int64_t k = cnt[(size_t)t * s + b];
+            cnt[(size_t)t * s + b] = off;
+            off += k;
+        }
+        if (off == block_starts[b]) fail(HPBJ_EINVAL, "partition: block " + std::to_string(b) + " is empty");
+        block_starts[b + 1] = off;
+    }
+#pragma omp parallel for schedule(static, 1)
+    for (int t = 0; t < T; ++t) {
+        int64_t* next = cnt.data() + (size_t)t * s;
+        for (int64_t i = t * chunk; i < std::min(n, (t + 1) * chunk); ++i) perm[i] = next[assignment[i]]++;
+    }
 }
 
 namespace {
@@ -206,11 +229,13 @@ struct PartWork {
     std::vector<int64_t> deg;
     std::vector<int32_t> state;
     std::vector<int32_t> queue;
+    std::vector<uint64_t> taken;
+    std::vector<int16_t> state16;
     std::vector<int32_t> order;
     std::vector<int64_t> dstart;
     std::vector<int64_t> sizes;
     std::vector<double> conn;
-    std::vector<int64_t> adj_start;
+    std::vector<int32_t> adj_start;
     std::vector<int32_t> adj_nbr;
     std::vector<double> adj_w;
 };
@@ -225,17 +250,75 @@ void fit(std::vector<T>& v, size_t n) {
 // deg[u] = st[u+1] - st[u]. Every edge takes part in growing and refinement
 // (partition.cpp:96-97, :122-125); dropping w <= 0 pairs is graph_from_matrix's
 // job (graph.cpp:41) and happens when the view is built (partition_csr).
-template <class Idx>
+template <class Idx, class Off = int64_t>
 struct GraphView {
     int64_t n;
-    const int64_t* st;
+    const Off* st;
     const Idx* idx;
     const double* w;
     const int64_t* deg;
 };
 
-template <class Idx>
-void partition_view(const GraphView<Idx>& g, int64_t s, double tol, int64_t* assignment) {
+// One refinement sweep (partition.cpp:117-141) over block ids of type S;
+// writes the final assignment.
+template <class Idx, class Off, class S>
+void refine_sweep(const GraphView<Idx, Off>& g, S* state, int64_t* sizes, int64_t cap, double* conn,
+                  int64_t* assignment) {
+    const int64_t n = g.n;
+    const Off* st = g.st;
+    const Idx* nb = g.idx;
+    const double* w = g.w;
+    int32_t touched[4096];
+    std::vector<int32_t> touched_big;
+    constexpr int64_t kRefAhead = 8;
+    for (int64_t u = 0; u < n; ++u) {
+        if (u + kRefAhead < n) {
+            const int64_t f = u + kRefAhead;
+            for (Off k = st[f]; k < st[f + 1] && k < st[f] + 16; ++k) __builtin_prefetch(&state[nb[k]], 0, 1);
+        }
+        const int32_t bu = state[u];
+        if (sizes[bu] <= 1) continue;
+        // Interior fast path: with every neighbour in bu the reference
+        // touches only bu, which is never a candidate -> no move, no state
+        // change (identical outcome, no floating-point work).
+        {
+            Off k = st[u];
+            const Off ke = st[u + 1];
+            while (k < ke && state[nb[k]] == bu) ++k;
+            if (k == ke) continue;
+        }
+        const int64_t du = st[u + 1] - st[u];
+        int32_t* tch = touched;
+        if (du > 4096) {
+            touched_big.resize(du);
+            tch = touched_big.data();
+        }
+        int nt = 0;
+        for (Off k = st[u]; k < st[u + 1]; ++k) {
+            const int32_t bv = state[nb[k]];
+            tch[nt] = bv;  // recorded while its conn is still 0.0 (partition.cpp:123-124)
+            nt += conn[bv] == 0.0;
+            conn[bv] += w[k];
+        }
+        int32_t best = -1;
+        for (int t = 0; t < nt; ++t) {
+            const int32_t bv = tch[t];
+            if (bv == bu || sizes[bv] + 1 > cap) continue;
+            if (best < 0 || conn[bv] > conn[best] || (conn[bv] == conn[best] && bv < best)) best = bv;
+        }
+        if (best >= 0 && conn[best] > conn[bu]) {
+            state[u] = (S)best;
+            --sizes[bu];
+            ++sizes[best];
+        }
+        for (int t = 0; t < nt; ++t) conn[tch[t]] = 0.0;
+    }
+#pragma omp parallel for schedule(static) if (n > 65536)
+    for (int64_t v = 0; v < n; ++v) assignment[v] = state[v];
+}
+
+template <class Idx, class Off>
+void partition_view(const GraphView<Idx, Off>& g, int64_t s, double tol, int64_t* assignment) {
     const int64_t n = g.n;
     if (s < 1) fail(HPBJ_EINVAL, "partition_graph: s must be >= 1");
     if (s > n) fail(HPBJ_EINVAL, "partition_graph: s exceeds node count");
@@ -247,8 +330,9 @@ void partition_view(const GraphView<Idx>& g, int64_t s, double tol, int64_t* ass
         static_cast<int64_t>(std::ceil(static_cast<double>(n) / s * (1.0 + tol))),
         (n + s - 1) / s);
 
+    const auto t_pv0 = std::chrono::steady_clock::now();
     PartWork& W = t_work;
-    const int64_t* st = g.st;
+    const Off* st = g.st;
     const Idx* nb = g.idx;
     const double* w = g.w;
     const int64_t* deg = g.deg;
@@ -257,33 +341,62 @@ void partition_view(const GraphView<Idx>& g, int64_t s, double tol, int64_t* ass
     constexpr int32_t kFree = -1, kQueued = -2;
     fit(W.state, n);
     int32_t* state = W.state.data();
-    std::fill(state, state + n, kFree);
+#pragma omp parallel for schedule(static) if (n > 65536)
+    for (int64_t v = 0; v < n; ++v) state[v] = kFree;
     fit(W.sizes, s);
     int64_t* sizes = W.sizes.data();
     std::fill(sizes, sizes + s, int64_t(0));
 
-    // Seed order: degree desc, index asc (counting sort on degree).
+    // Seed order: degree desc, index asc — a stable counting sort on
+    // maxdeg - deg, parallel over contiguous chunks (per-chunk histograms, a
+    // prefix over (key, chunk), in-order scatter per chunk).
     int64_t maxdeg = 0, connected = 0;
+#pragma omp parallel for schedule(static) reduction(max : maxdeg) reduction(+ : connected) if (n > 65536)
     for (int64_t v = 0; v < n; ++v) {
-        maxdeg = std::max(maxdeg, deg[v]);
-        if (deg[v] > 0) ++connected;
+        maxdeg = std::max(maxdeg, (int64_t)deg[v]);
+        connected += deg[v] > 0;
     }
-    fit(W.dstart, maxdeg + 2);
-    int64_t* dstart = W.dstart.data();
-    std::fill(dstart, dstart + maxdeg + 2, int64_t(0));
-    for (int64_t v = 0; v < n; ++v)
-        if (deg[v] > 0) ++dstart[maxdeg - deg[v] + 1];
-    for (int64_t d = 0; d <= maxdeg; ++d) dstart[d + 1] += dstart[d];
     fit(W.order, connected + 1);
     int32_t* order = W.order.data();
-    for (int64_t v = 0; v < n; ++v)
-        if (deg[v] > 0) order[dstart[maxdeg - deg[v]]++] = (int32_t)v;
+    {
+        const int T = n > 65536 ? std::max(1, std::min(omp_get_max_threads(), 32)) : 1;
+        const int64_t K = maxdeg + 1, chunk = (n + T - 1) / T;
+        fit(W.dstart, (size_t)T * K);
+        int64_t* cnt = W.dstart.data();  // [chunk][key]
+        std::fill(cnt, cnt + (size_t)T * K, int64_t(0));
+#pragma omp parallel for schedule(static, 1)
+        for (int t = 0; t < T; ++t)
+            for (int64_t v = t * chunk; v < std::min(n, (t + 1) * chunk); ++v)
+                if (deg[v] > 0) ++cnt[(size_t)t * K + (maxdeg - deg[v])];
+        int64_t off = 0;
+        for (int64_t k = 0; k < K; ++k)
+            for (int t = 0; t < T; ++t) {
+                const int64_t c = cnt[(size_t)t * K + k];
+                cnt[(size_t)t * K + k] = off;
+                off += c;
+            }
+#pragma omp parallel for schedule(static, 1)
+        for (int t = 0; t < T; ++t) {
+            int64_t* nx = cnt + (size_t)t * K;
+            for (int64_t v = t * chunk; v < std::min(n, (t + 1) * chunk); ++v)
+                if (deg[v] > 0) order[nx[maxdeg - deg[v]]++] = (int32_t)v;
+        }
+    }
     int64_t cursor = 0;
 
     const auto t_seed = std::chrono::steady_clock::now();
-    // Region growing (partition.cpp:74-103).
+    if (getenv("HPBJ_DEBUG"))
+        fprintf(stderr, "[hpbj]   seed order %.2f ms\n",
+                std::chrono::duration<double, std::milli>(t_seed - t_pv0).count());
+    // Region growing (partition.cpp:74-103). The free/taken test of the
+    // growing loop reads a bitmap (n bits: L1/L2-resident) instead of the
+    // 4-byte state array; state receives the block id once per node.
     fit(W.queue, n + 1);
     int32_t* queue = W.queue.data();
+    fit(W.taken, (n + 63) / 64);
+    uint64_t* taken = W.taken.data();  // bit v: assigned or queued
+#pragma omp parallel for schedule(static) if (n > 65536)
+    for (int64_t w = 0; w < (n + 63) / 64; ++w) taken[w] = 0ull;
     int64_t connected_left = connected;
     constexpr int kAhead = 6;
     for (int64_t b = 0; b < s && connected_left > 0; ++b) {
@@ -294,38 +407,37 @@ void partition_view(const GraphView<Idx>& g, int64_t s, double tol, int64_t* ass
         int64_t grown = 0;
         const int32_t bb = (int32_t)b;
         while (grown < target) {
-            if (head == tail) {
-                while (cursor < connected && state[order[cursor]] >= 0) ++cursor;
+            if (head == tail) {  // queue empty: every taken node is assigned
+                while (cursor < connected && ((taken[order[cursor] >> 6] >> (order[cursor] & 63)) & 1ull)) ++cursor;
                 if (cursor == connected) break;
-                queue[tail++] = order[cursor];
-                state[order[cursor]] = kQueued;
+                const int32_t sd = order[cursor];
+                queue[tail++] = sd;
+                taken[sd >> 6] |= 1ull << (sd & 63);
             }
-            if (head + kAhead < tail) {  // prefetch the neighbourhood of a node popped soon
+            if (head + kAhead < tail) {  // prefetch the adjacency of a node popped soon
                 const int32_t f = queue[head + kAhead];
-                const Idx* p = nb + st[f];
-                const int64_t dd = st[f + 1] - st[f];
-                for (int64_t q = 0; q < dd && q < 16; ++q) __builtin_prefetch(&state[p[q]], 1, 1);
-                if (head + 2 * kAhead < tail) __builtin_prefetch(nb + st[queue[head + 2 * kAhead]], 0, 1);
+                __builtin_prefetch(nb + st[f], 0, 1);
             }
             const int32_t u = queue[head++];
             state[u] = bb;
-            ++sizes[b];
             ++grown;
             --connected_left;
-            for (int64_t k = st[u]; k < st[u + 1]; ++k) {  // branch-free push of the free neighbours
+            for (Off k = st[u]; k < st[u + 1]; ++k) {  // branch-free push of the free neighbours
                 const int32_t v = (int32_t)nb[k];
-                const int32_t sv = state[v];
-                const bool fr = sv == kFree;
+                uint64_t& word = taken[v >> 6];
+                const uint64_t bit = 1ull << (v & 63);
                 queue[tail] = v;
-                tail += fr;
-                state[v] = fr ? kQueued : sv;
+                tail += (word & bit) == 0;
+                word |= bit;
             }
         }
-        for (int64_t q = head; q < tail; ++q) state[queue[q]] = kFree;  // queue.clear()
+        sizes[b] = grown;
+        for (int64_t q = head; q < tail; ++q) taken[queue[q] >> 6] &= ~(1ull << (queue[q] & 63));  // queue.clear()
     }
 
     // Remaining nodes -> first block of minimal size (partition.cpp:105-112).
-    {
+    // (none when every node has a neighbour and growing placed them all)
+    if (connected < n || connected_left > 0) {
         using Key = std::pair<int64_t, int64_t>;  // (size, block)
         std::priority_queue<Key, std::vector<Key>, std::greater<Key>> heap;
         bool built = false;
@@ -347,56 +459,21 @@ void partition_view(const GraphView<Idx>& g, int64_t s, double tol, int64_t* ass
     if (getenv("HPBJ_DEBUG"))
         fprintf(stderr, "[hpbj]   bfs+leftovers %.1f ms\n",
                 std::chrono::duration<double, std::milli>(t_grow - t_seed).count());
-    // One boundary-refinement sweep (partition.cpp:117-141), verbatim order.
+    // One boundary-refinement sweep (partition.cpp:117-141), verbatim order,
+    // on 16-bit block ids when they fit (half the cache footprint of the
+    // random neighbour lookups).
     fit(W.conn, s);
     double* conn = W.conn.data();
     std::fill(conn, conn + s, 0.0);
-    int32_t touched[4096];
-    std::vector<int32_t> touched_big;
-    constexpr int64_t kRefAhead = 8;
-    for (int64_t u = 0; u < n; ++u) {
-        if (u + kRefAhead < n) {
-            const int64_t f = u + kRefAhead;
-            for (int64_t k = st[f]; k < st[f + 1] && k < st[f] + 16; ++k) __builtin_prefetch(&state[nb[k]], 0, 1);
-        }
-        const int32_t bu = state[u];
-        if (sizes[bu] <= 1) continue;
-        // Interior fast path: with every neighbour in bu the reference
-        // touches only bu, which is never a candidate -> no move, no state
-        // change (identical outcome, no floating-point work).
-        {
-            int64_t k = st[u];
-            const int64_t ke = st[u + 1];
-            while (k < ke && state[nb[k]] == bu) ++k;
-            if (k == ke) continue;
-        }
-        const int64_t du = st[u + 1] - st[u];
-        int32_t* tch = touched;
-        if (du > 4096) {
-            touched_big.resize(du);
-            tch = touched_big.data();
-        }
-        int nt = 0;
-        for (int64_t k = st[u]; k < st[u + 1]; ++k) {
-            const int32_t bv = state[nb[k]];
-            tch[nt] = bv;  // recorded while its conn is still 0.0 (partition.cpp:123-124)
-            nt += conn[bv] == 0.0;
-            conn[bv] += w[k];
-        }
-        int32_t best = -1;
-        for (int t = 0; t < nt; ++t) {
-            const int32_t bv = tch[t];
-            if (bv == bu || sizes[bv] + 1 > cap) continue;
-            if (best < 0 || conn[bv] > conn[best] || (conn[bv] == conn[best] && bv < best)) best = bv;
-        }
-        if (best >= 0 && conn[best] > conn[bu]) {
-            state[u] = best;
-            --sizes[bu];
-            ++sizes[best];
-        }
-        for (int t = 0; t < nt; ++t) conn[tch[t]] = 0.0;
+    if (s <= 32767) {
+        fit(W.state16, n);
+        int16_t* st16 = W.state16.data();
+#pragma omp parallel for schedule(static) if (n > 65536)
+        for (int64_t v = 0; v < n; ++v) st16[v] = (int16_t)state[v];
+        refine_sweep(g, st16, sizes, cap, conn, assignment);
+    } else {
+        refine_sweep(g, state, sizes, cap, conn, assignment);
     }
-    for (int64_t v = 0; v < n; ++v) assignment[v] = state[v];
     if (getenv("HPBJ_DEBUG"))
         fprintf(stderr, "[hpbj]   refine %.1f ms\n",
                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_grow).count());
@@ -417,6 +494,11 @@ void partition_adjacency(const Adjacency& g, int64_t s, double tol, int64_t* ass
 void partition_csr(int64_t n, const int64_t* rp, const int64_t* ci, const double* val, int64_t s, double tol,
                    int64_t* assignment) {
     const int64_t nnz = rp[n];
+    if (nnz >= INT32_MAX) {  // beyond 4-byte offsets: the general (int64) path
+        const Adjacency g = graph_general(n, rp, ci, val);
+        partition_adjacency(g, s, tol, assignment);
+        return;
+    }
     const auto t_w0 = std::chrono::steady_clock::now();
     PartWork& W = t_work;
     fit(W.wk, nnz);
@@ -473,10 +555,11 @@ void partition_csr(int64_t n, const int64_t* rp, const int64_t* ci, const double
         fprintf(stderr, "[hpbj]   weights %.1f ms\n",
                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_w0).count());
     const auto t_a0 = std::chrono::steady_clock::now();
-    // compact int32 adjacency (kept entries only): 4 B/neighbour for the
-    // sequential BFS instead of 16 B (int64 column + weight) per CSR entry
+    // compact int32 adjacency (kept entries only): 4 B/neighbour and 4-byte
+    // offsets for the sequential BFS instead of 16 B (int64 column + weight)
+    // per CSR entry
     fit(W.adj_start, n + 1);
-    int64_t* ast = W.adj_start.data();
+    int32_t* ast = W.adj_start.data();
     ast[0] = 0;
     for (int64_t u = 0; u < n; ++u) ast[u + 1] = ast[u] + deg[u];
     fit(W.adj_nbr, ast[n] + 1);
@@ -496,7 +579,7 @@ void partition_csr(int64_t n, const int64_t* rp, const int64_t* ci, const double
     if (getenv("HPBJ_DEBUG"))
         fprintf(stderr, "[hpbj]   adjacency %.1f ms\n",
                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_a0).count());
-    GraphView<int32_t> view{n, ast, anb, aw, deg};
+    GraphView<int32_t, int32_t> view{n, ast, anb, aw, deg};
     partition_view(view, s, tol, assignment);
 }
 
