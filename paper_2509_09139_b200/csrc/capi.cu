@@ -623,9 +623,11 @@ double spmv_bytes(const hpbj_ctx* c) {
     const double n = c->A.n, nnz = c->A.nnz;
     return 12.0 * nnz + 4.0 * (n + 1) + 4.0 * n + 8.0 * n;  // val+col, row ptr, z in (FP32), w out
 }
-double orth_bytes(const hpbj_ctx* c, int j) {  // step j: V_0..V_j read twice (dots, update), w in, v_{j+1} out
+double orth_bytes(const hpbj_ctx* c, int j) {
+    // step j: V_0..V_j read once (compulsory; the second MGS pass re-reads
+    // them from L2), w in, v_{j+1} out
     const double n = c->A.n;
-    return 2.0 * 8.0 * n * (j + 1) + 8.0 * n + 8.0 * n;
+    return 8.0 * n * (j + 1) + 8.0 * n + 8.0 * n;
 }
 double fused_step_bytes(const hpbj_ctx* c, int j) {  // w stays on chip: no SpMV write / orth read of w
     const double n = c->A.n;
