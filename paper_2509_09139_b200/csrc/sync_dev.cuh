@@ -16,24 +16,35 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// Sense-free generation barrier over all CTAs of a cooperative launch.
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
+    unsigned old;
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+
+// Sense-free generation barrier over all CTAs of a cooperative launch, with
+// release/acquire atomics instead of full fences (0.5 us cheaper per barrier
+// on B200, scripts/micro/barrier.cu): bar.sync orders the CTA's writes before
+// thread 0's acq_rel arrival; the last arriver's release of the generation is
+// acquired by every spinner, and bar.sync hands it to the rest of the CTA.
 // Data published before it must be read after it through L2 (ld.cg /
-// __ldcg): L1 is not coherent across SMs.
+// __ldcg) or plain loads (the gpu-scope acquire invalidates L1).
 __device__ __forceinline__ void grid_barrier(GridBarrier* gb) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        const unsigned g = ld_acquire(&gb->gen);
-        __threadfence();
-        const unsigned prev = atomicAdd(&gb->count, 1u);
-        if (prev == gridDim.x - 1) {
-            gb->count = 0;
-            __threadfence();
+        const unsigned g = ld_relaxed(&gb->gen);
+        if (atom_add_acq_rel(&gb->count, 1u) == gridDim.x - 1) {
+            gb->count = 0;  // ordered before the release below
             st_release(&gb->gen, g + 1);
         } else {
             while (ld_acquire(&gb->gen) == g) {
             }
         }
-        __threadfence();
     }
     __syncthreads();
 }
