@@ -159,33 +159,47 @@ __global__ void k_panel_owner(const int* __restrict__ pstart, int s, int* __rest
         for (int P = pstart[b]; P < pstart[b + 1]; ++P) panel_block[P] = b;
 }
 
-template <class Acc, class IdxT, class Src, class Dst>
+// STAGE: tile quads staged through shared memory by cp.async so their
+// latency overlaps the fold — a win for shallow blocks (few, short folds),
+// a loss for deep ones (long folds already hide it; fewer resident warps).
+constexpr int kStageMaxDim = 160;
+
+template <class Acc, class IdxT, bool STAGE, class Src, class Dst>
 __global__ void __launch_bounds__(kWarpsPerCta * 32) k_apply_spk(SpkView p, Src src, Dst dst,
                                                                  const SolveState* sst, int ystride) {
     if (sst && sst->done) return;
     extern __shared__ __align__(16) unsigned char spk_smem[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int tmax = ystride / 32;
-    // per warp: y/x buffer (Acc[ystride]), panel descriptors
-    unsigned char* wbase = spk_smem + (size_t)wid * (sizeof(Acc) * ystride + sizeof(SpkPanel) * tmax);
-    Acc* ybuf = reinterpret_cast<Acc*>(wbase);
-    SpkPanel* dsh = reinterpret_cast<SpkPanel*>(wbase + sizeof(Acc) * ystride);
+    constexpr int TB = STAGE ? 4096 : 0;
+    // per warp: [tile staging (8 x 32 float4)], y/x buffer (Acc[ystride]), panel descriptors
+    unsigned char* wbase = spk_smem + (size_t)wid * (TB + sizeof(Acc) * ystride + sizeof(SpkPanel) * tmax);
+    float4* tbuf = reinterpret_cast<float4*>(wbase);
+    Acc* ybuf = reinterpret_cast<Acc*>(wbase + TB);
+    SpkPanel* dsh = reinterpret_cast<SpkPanel*>(wbase + TB + sizeof(Acc) * ystride);
     const int nw = gridDim.x * kWarpsPerCta;
     const int b_first = blockIdx.x * kWarpsPerCta + wid;
     if (b_first < p.s) prefetch_block_head<IdxT>(p, b_first, lane);
     for (int b = b_first; b < p.s; b += nw)
-        spk_solve_block<Acc, IdxT>(p, b, b + nw < p.s ? b + nw : -1, src, dst, ybuf, dsh, lane);
+        spk_solve_block<Acc, IdxT, STAGE>(p, b, b + nw < p.s ? b + nw : -1, src, dst, ybuf, dsh, lane, tbuf);
 }
 
 template <class Acc, class Src, class Dst>
 void launch(const SpkView& v, Src src, Dst dst, const SolveState* sst, cudaStream_t st, int64_t* launches) {
     const int ystride = ((v.dmax + 31) / 32) * 32;
-    const size_t smem = (sizeof(Acc) * ystride + sizeof(SpkPanel) * (ystride / 32)) * kWarpsPerCta;
+    const bool stage = v.dmax <= kStageMaxDim;
+    const size_t smem =
+        ((stage ? 4096 : 0) + sizeof(Acc) * ystride + sizeof(SpkPanel) * (ystride / 32)) * kWarpsPerCta;
     const int grid = (v.s + kWarpsPerCta - 1) / kWarpsPerCta;
-    if (v.idx32)
-        k_apply_spk<Acc, uint32_t, Src, Dst><<<grid, kWarpsPerCta * 32, smem, st>>>(v, src, dst, sst, ystride);
-    else
-        k_apply_spk<Acc, uint16_t, Src, Dst><<<grid, kWarpsPerCta * 32, smem, st>>>(v, src, dst, sst, ystride);
+#define HPBJ_APPLY(IDX, STG) k_apply_spk<Acc, IDX, STG, Src, Dst><<<grid, kWarpsPerCta * 32, smem, st>>>(v, src, dst, sst, ystride)
+    if (v.idx32) {
+        if (stage) HPBJ_APPLY(uint32_t, true);
+        else HPBJ_APPLY(uint32_t, false);
+    } else {
+        if (stage) HPBJ_APPLY(uint16_t, true);
+        else HPBJ_APPLY(uint16_t, false);
+    }
+#undef HPBJ_APPLY
     *launches += 1;
     HPBJ_CUDA(cudaGetLastError());
 }

@@ -126,6 +126,14 @@ __device__ __forceinline__ void prefetch_l2(const void* p, size_t bytes) {
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((unsigned)(e - a)) : "memory");
 }
 
+// 16-byte asynchronous global -> shared copy (LDGSTS), L2 only.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 // The tile quads a pass reads ([quad][lane] float4, see kernels.cuh): the
 // forward pass quad q for lanes l >= 4q, the backward pass quad q < 8 for
 // lanes l < 4q and all of quad 8. Lanes 8..16 issue one quad each.
@@ -165,9 +173,12 @@ __device__ __forceinline__ void prefetch_block_head(const SpkView& p, int b, int
 // the unit-lower factor, backward with the upper one, write through dst.
 // ybuf (Acc[32 T]) and dsh (SpkPanel[T]) are the calling warp's shared
 // memory; next_b (or -1) is the block whose head is prefetched at the end.
-template <class Acc, class IdxT, class Src, class Dst>
+// tbuf (optional, 8 x 32 float4 of the warp's shared memory): the step's
+// tile quads are copied there asynchronously at the start of the step, so
+// their latency overlaps the off-panel fold.
+template <class Acc, class IdxT, bool STAGE = false, class Src, class Dst>
 __device__ __forceinline__ void spk_solve_block(const SpkView& p, int b, int next_b, Src src, Dst dst, Acc* ybuf,
-                                                SpkPanel* dsh, int lane) {
+                                                SpkPanel* dsh, int lane, float4* tbuf = nullptr) {
     const IdxT* eidx = reinterpret_cast<const IdxT*>(p.eidx);
     const int o = p.bstart[b];
     const int d = p.bstart[b + 1] - o;
@@ -205,15 +216,22 @@ __device__ __forceinline__ void spk_solve_block(const SpkView& p, int b, int nex
             prefetch_entries<IdxT>(p, ds.uoff, ds.nu, lane, 0, 1);
             prefetch_tile(p, P0 + t, false, lane);
         }
+        const float4* tile_f = reinterpret_cast<const float4*>(p.dtile + (size_t)(P0 + t) * kTileFloats);
+        if (STAGE) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (q <= qd) cp_async16(tbuf + q * 32 + lane, tile_f + q * 32 + lane);
+            cp_async_commit();
+        }
         fold_entries<Acc, IdxT>(p.eval, eidx, ds.off, ds.nl, ybuf, ybuf + 32 * t, lane);
         // y_t = Linv_tt r_t: quads 0..qd of row `lane` (zeros from the diagonal on)
         {
-            const float4* tile = reinterpret_cast<const float4*>(p.dtile + (size_t)(P0 + t) * kTileFloats);
             float4 f4[8];
+            if (STAGE) cp_async_wait_all();  // each lane reads back only the quads it copied
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
                 f4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (q <= qd) f4[q] = __ldg(tile + q * 32 + lane);
+                if (q <= qd) f4[q] = STAGE ? tbuf[q * 32 + lane] : __ldg(tile_f + q * 32 + lane);
             }
             const Acc* r = ybuf + 32 * t;
             Acc a0 = r[lane], a1 = (Acc)0, a2 = (Acc)0, a3 = (Acc)0;
@@ -239,16 +257,23 @@ __device__ __forceinline__ void spk_solve_block(const SpkView& p, int b, int nex
         } else if (next_b >= 0) {
             prefetch_block_head<IdxT>(p, next_b, lane);
         }
+        const float4* tile_b = reinterpret_cast<const float4*>(p.dtile + (size_t)(P0 + t) * kTileFloats);
+        if (STAGE) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (q >= qd) cp_async16(tbuf + q * 32 + lane, tile_b + (q == qd ? 8 : q) * 32 + lane);
+            cp_async_commit();
+        }
         fold_entries<Acc, IdxT>(p.eval, eidx, ds.uoff, ds.nu, ybuf, ybuf + 32 * t, lane);
         // x_t = Uinv_tt y'_t: quad 8 (the diagonal quad) and quads qd+1..7 of row `lane`
         const int k = 32 * t + lane;
         {
-            const float4* tile = reinterpret_cast<const float4*>(p.dtile + (size_t)(P0 + t) * kTileFloats);
             float4 f4[8];
+            if (STAGE) cp_async_wait_all();
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
                 f4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (q >= qd) f4[q] = __ldg(tile + (q == qd ? 8 : q) * 32 + lane);
+                if (q >= qd) f4[q] = STAGE ? tbuf[q * 32 + lane] : __ldg(tile_b + (q == qd ? 8 : q) * 32 + lane);
             }
             const Acc* r = ybuf + 32 * t;
             Acc a0 = (Acc)0, a1 = (Acc)0, a2 = (Acc)0, a3 = (Acc)0;
