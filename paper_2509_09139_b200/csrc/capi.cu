@@ -323,9 +323,9 @@ namespace {
 // Lanes per row from the mean row length; hub rows get CTAs of their own.
 int spmv_group(int64_t nnz, int n) {
     const double avg = n > 0 ? double(nnz) / n : 0.0;
-    // measured on B200 (configs 1-3): one thread per row wins up to
-    // ~7.5 nnz/row (FP32 x gathers stay in L1/L2), then 2/4/8 lanes
-    int g = avg <= 7.5 ? 1 : avg <= 16.0 ? 2 : avg <= 32.0 ? 4 : avg <= 64.0 ? 8 : 32;
+    // measured on B200 (configs 1-3): one thread per row (two rows
+    // interleaved) wins up to ~12 nnz/row, then 2/4/8 lanes
+    int g = avg <= 12.0 ? 1 : avg <= 20.0 ? 2 : avg <= 32.0 ? 4 : avg <= 64.0 ? 8 : 32;
     if (const char* e = getenv("HPBJ_SPMV_G")) g = atoi(e);
     return g;
 }

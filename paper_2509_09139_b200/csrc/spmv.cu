@@ -62,35 +62,38 @@ __global__ void __launch_bounds__(kSpmvThreads) k_spmv(DevCsr a, const XT* __res
         const int group = ((blockIdx.x - n_long) * kSpmvThreads + threadIdx.x) / G;
         const int ngroups = (gridDim.x - n_long) * (kSpmvThreads / G);
         const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
-        for (int row = group; row < a.n; row += ngroups) {
-            const int b = __ldg(a.rp + row), e = __ldg(a.rp + row + 1);
-            if (e - b > long_thresh) continue;  // uniform within the group
-            double sum = 0.0;
-            // four strides per round: their index/value loads, then their x
-            // gathers, are in flight together (same summation order as a plain loop)
-            for (int k0 = b + gl; k0 < e; k0 += 4 * G) {
-                int c[4];
-                double v[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int k = k0 + u * G;
-                    c[u] = k < e ? __ldg(a.ci + k) : 0;
-                    v[u] = k < e ? __ldg(a.val + k) : 0.0;
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    if (k0 + u * G < e) sum = fma(v[u], ldx(x, c[u]), sum);
+        auto finish = [&](int row, double sum) {
+            if (MODE == 0) {
+                y[row] = sum;
+            } else {
+                const double r = bvec[row] - sum;
+                y[row] = r;
+                ss = fma(r, r, ss);
             }
+        };
+        {
+            for (int row = group; row < a.n; row += ngroups) {
+                const int b = __ldg(a.rp + row), e = __ldg(a.rp + row + 1);
+                if (e - b > long_thresh) continue;  // uniform within the group
+                double sum = 0.0;
+                // four strides per round: their index/value loads, then their x
+                // gathers, are in flight together (same summation order as a plain loop)
+                for (int k0 = b + gl; k0 < e; k0 += 4 * G) {
+                    int c[4];
+                    double v[4];
 #pragma unroll
-            for (int o = G / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(gmask, sum, o, G);
-            if (gl == 0) {
-                if (MODE == 0) {
-                    y[row] = sum;
-                } else {
-                    const double r = bvec[row] - sum;
-                    y[row] = r;
-                    ss = fma(r, r, ss);
+                    for (int u = 0; u < 4; ++u) {
+                        const int k = k0 + u * G;
+                        c[u] = k < e ? __ldg(a.ci + k) : 0;
+                        v[u] = k < e ? __ldg(a.val + k) : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        if (k0 + u * G < e) sum = fma(v[u], ldx(x, c[u]), sum);
                 }
+#pragma unroll
+                for (int o = G / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(gmask, sum, o, G);
+                if (gl == 0) finish(row, sum);
             }
         }
     }
