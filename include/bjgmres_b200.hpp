@@ -112,9 +112,11 @@ struct BlockJacobiOptions {  // preconditioner.hpp:32-38 (Hybrid policy)
     double eps_pivot = 1e-10;
 };
 
-struct PreconditionerStats {  // preconditioner.hpp:14-20
+struct PreconditionerStats {  // preconditioner.hpp:14-20 (block_nnz: see measure_block_nnz)
     index_t block_dim = 0;
     index_t perturbation_count = 0;
+    double cond_estimate = 0.0;  // cond_estimate_block (computed on the device when requested)
+    double error_bound = 0.0;    // block_error_bound(cond, 2^-24, 2^-53)
 };
 
 // Preconditioner (preconditioner.hpp:50-98): cheap copyable handle to an
@@ -151,11 +153,15 @@ public:
         detail::check(hpbj_bj_apply(ctx_.get(), v.data(), z.data()), ctx_.get());
         return z;
     }
-    std::vector<PreconditionerStats> stats() const {
-        std::vector<index_t> d(partition_->num_blocks), pc(partition_->num_blocks);
+    std::vector<PreconditionerStats> stats(bool with_cond_estimates = true) const {
+        const size_t s = static_cast<size_t>(partition_->num_blocks);
+        std::vector<index_t> d(s), pc(s);
+        std::vector<double> cond(s, 0.0), eb(s, 0.0);
         detail::check(hpbj_get_block_stats(ctx_.get(), d.data(), pc.data()), ctx_.get());
-        std::vector<PreconditionerStats> out(d.size());
-        for (size_t b = 0; b < d.size(); ++b) out[b] = {d[b], pc[b]};
+        if (with_cond_estimates)
+            detail::check(hpbj_get_block_diagnostics(ctx_.get(), cond.data(), eb.data()), ctx_.get());
+        std::vector<PreconditionerStats> out(s);
+        for (size_t b = 0; b < s; ++b) out[b] = {d[b], pc[b], cond[b], eb[b]};
         return out;
     }
     hpbj_ctx* context() const { return ctx_.get(); }

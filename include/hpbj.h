@@ -170,6 +170,12 @@ int hpbj_bj_apply(hpbj_ctx* ctx, const double* v, double* z);
  * and LUFactors::pivot_rows (lu.hpp:37-50). */
 int hpbj_get_block_factors(hpbj_ctx* ctx, int64_t block, int64_t* dim, float* f,
                            int64_t* pivot_rows);
+/* PreconditionerStats::{cond_estimate, error_bound} per block
+ * (cond_estimate_block / block_error_bound, preconditioner.cpp:13-88): 1-norm
+ * condition estimate of each block (exact for dim <= 64, Hager otherwise) and
+ * (cond*2^-53 + 2^-24)*cond. Computed on the device on first request after a
+ * (re)factorisation. */
+int hpbj_get_block_diagnostics(hpbj_ctx* ctx, double* cond_estimate, double* error_bound);
 /* PreconditionerStats::{block_dim, perturbation_count} per block. */
 int hpbj_get_block_stats(hpbj_ctx* ctx, int64_t* dims, int64_t* perturbations);
 

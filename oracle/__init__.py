@@ -190,6 +190,17 @@ class Ref:
                                        _p(pert, _i64p), ctypes.byref(sc)))
         return dims, f32, f64, piv, pert
 
+    def block_stats(self, rp, ci, v, s, assignment, eps=1e-10):
+        """(cond_estimate, error_bound, block_nnz) per block, reference Hybrid setup."""
+        rp, ci, v = self._csr(rp, ci, v)
+        n = len(rp) - 1
+        asg = np.ascontiguousarray(assignment, np.int64)
+        cond, eb, bn = np.zeros(s), np.zeros(s), np.zeros(s, np.int64)
+        self._chk(self.L.bjref_block_stats(ctypes.c_int64(n), _p(rp, _i64p), _p(ci, _i64p), _p(v, _f64p),
+                                           ctypes.c_int64(s), _p(asg, _i64p), ctypes.c_double(eps),
+                                           _p(cond, _f64p), _p(eb, _f64p), _p(bn, _i64p)))
+        return cond, eb, bn
+
     def apply(self, rp, ci, v, s, assignment, vin, eps=1e-10, fp32=True):
         rp, ci, v = self._csr(rp, ci, v)
         n = len(rp) - 1

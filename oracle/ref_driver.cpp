@@ -196,6 +196,28 @@ int bjref_permute(int64_t n, const int64_t* rp, const int64_t* ci, const double*
 /// F = L_strict + U in pivot order, row-major d x d, concatenated over blocks
 /// in block order (offset of block b = sum_{c<b} d_c^2). F32 holds the
 /// values_low() cast (preconditioner.cpp:140), F64 the binary64 masters.
+// PreconditionerStats with the condition estimates (with_cond_estimates =
+// true, the reference default): cond_estimate, error_bound, block_nnz per block.
+int bjref_block_stats(int64_t n, const int64_t* rp, const int64_t* ci, const double* v, int64_t s,
+                      const int64_t* assignment, double eps, double* cond, double* ebound, int64_t* block_nnz) {
+    return guarded([&] {
+        SparseMatrix a = make_matrix(n, rp, ci, v);
+        a.materialize_low();
+        BlockJacobiOptions opts;
+        opts.eps_pivot = eps;
+        opts.policy.mode = PrecisionMode::Hybrid;
+        opts.with_cond_estimates = true;
+        const Preconditioner p = Preconditioner::block_jacobi(
+            a, partition_from_assignment(std::vector<index_t>(assignment, assignment + n), s), opts);
+        const BlockJacobiData* d = p.block_jacobi_data();
+        for (int64_t b = 0; b < s; ++b) {
+            cond[b] = d->stats[b].cond_estimate;
+            ebound[b] = d->stats[b].error_bound;
+            block_nnz[b] = d->stats[b].block_nnz;
+        }
+    });
+}
+
 int bjref_factors(int64_t n, const int64_t* rp, const int64_t* ci, const double* v,
                   int64_t s, const int64_t* assignment, double eps, float* f32,
                   double* f64, int64_t* pivot_rows, int64_t* pert_count,

@@ -405,6 +405,12 @@ class Context:
         self.check(self.lib.hpbj_get_block_stats(self.h, _p(dims, _abi.i64p), _p(pert, _abi.i64p)))
         return dims, pert
 
+    def block_diagnostics(self, s: int):
+        """(cond_estimate[s], error_bound[s]) of the factored blocks (device)."""
+        cond, eb = np.zeros(s), np.zeros(s)
+        self.check(self.lib.hpbj_get_block_diagnostics(self.h, _p(cond, _abi.f64p), _p(eb, _abi.f64p)))
+        return cond, eb
+
     def launches(self) -> int:
         return int(self.lib.hpbj_kernel_launches(self.h))
 
@@ -503,9 +509,14 @@ class Preconditioner:
     def block_factors(self, b: int):
         return self.ctx.block_factors(b)
 
-    def stats(self):
-        dims, pert = self.ctx.block_stats(self.partition.num_blocks)
-        return [dict(block_dim=int(d), perturbation_count=int(p)) for d, p in zip(dims, pert)]
+    def stats(self, with_cond_estimates: bool = True):
+        """PreconditionerStats per block (preconditioner.hpp:14-20); the condition
+        estimates / error bounds are computed on the device on first request."""
+        s = self.partition.num_blocks
+        dims, pert = self.ctx.block_stats(s)
+        cond, eb = self.ctx.block_diagnostics(s) if with_cond_estimates else (np.zeros(s), np.zeros(s))
+        return [dict(block_dim=int(d), perturbation_count=int(p), cond_estimate=float(c), error_bound=float(e))
+                for d, p, c, e in zip(dims, pert, cond, eb)]
 
 
 @dataclass

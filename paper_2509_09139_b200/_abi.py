@@ -94,6 +94,7 @@ SIGNATURES = {
     "hpbj_set_profiling": (ctypes.c_int, [vp, ctypes.c_int]),
     "hpbj_get_kernel_stats": (ctypes.c_int, [vp, ctypes.POINTER(KernelStat)]),
     "hpbj_set_fused": (ctypes.c_int, [vp, ctypes.c_int]),
+    "hpbj_get_block_diagnostics": (ctypes.c_int, [vp, ctypes.POINTER(f64), ctypes.POINTER(f64)]),
     "hpbj_mm_read": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(i64), ctypes.POINTER(i64),
                                     ctypes.POINTER(ctypes.POINTER(i64)), ctypes.POINTER(ctypes.POINTER(i64)),
                                     ctypes.POINTER(ctypes.POINTER(f64))]),

@@ -189,6 +189,9 @@ struct hpbj_ctx {
     int64_t fac_floats = 0;
     int* d_piv = nullptr;
     int* d_pert_count = nullptr;
+    double* d_cond = nullptr;  // diagnostics (on demand, invalidated by a refactor)
+    double* d_ebound = nullptr;
+    bool diag_valid = false;
     PertRecord* d_pert = nullptr;
     int* d_pert_n = nullptr;
     unsigned long long* d_singular = nullptr;
@@ -262,6 +265,8 @@ struct hpbj_ctx {
         dfree(d_fac);
         dfree(d_piv);
         dfree(d_pert_count);
+        dfree(d_cond);
+        dfree(d_ebound);
         dfree(d_pert);
         dfree(d_pert_n);
         dfree(d_singular);
@@ -429,6 +434,7 @@ void build_spk(hpbj_ctx* c) {
 
 void factor(hpbj_ctx* c, hpbj_setup_info* info) {
     cudaStream_t st = c->stream;
+    c->diag_valid = false;
     const unsigned long long none = ~0ull;
     HPBJ_CUDA(cudaMemcpyAsync(c->d_singular, &none, sizeof(none), cudaMemcpyHostToDevice, st));
     HPBJ_CUDA(cudaMemsetAsync(c->d_pert_n, 0, sizeof(int), st));
@@ -1168,6 +1174,30 @@ int hpbj_get_block_factors(hpbj_ctx* ctx, int64_t block, int64_t* dim, float* f,
                         packed[(size_t)(k / 32) * 32 * dp4 + (c2 / 4) * 128 + (k % 32) * 4 + (c2 % 4)];
         if (pivot_rows)
             for (int k = 0; k < d; ++k) pivot_rows[k] = piv[k];
+    });
+}
+
+int hpbj_get_block_diagnostics(hpbj_ctx* ctx, double* cond_estimate, double* error_bound) {
+    if (!ctx) return HPBJ_EINVAL;
+    t_pool = &ctx->pool;
+    t_slots = &ctx->slots;
+    return guard(&ctx->err, [&] {
+        if (!ctx->has_pc) fail(HPBJ_ELOGIC, "diagnostics: block-Jacobi preconditioner not set up");
+        if (!ctx->diag_valid) {
+            dslot(ctx->d_cond, ctx->s);
+            dslot(ctx->d_ebound, ctx->s);
+            DiagParams p{ctx->s, ctx->dmax, ctx->d_bstart, ctx->d_fac_off, ctx->d_fac, ctx->d_piv, ctx->B,
+                         ctx->d_cond, ctx->d_ebound};
+            launch_block_cond(p, ctx->num_sms, ctx->stream, &ctx->launches);
+            ctx->diag_valid = true;
+        }
+        if (cond_estimate)
+            HPBJ_CUDA(cudaMemcpyAsync(cond_estimate, ctx->d_cond, sizeof(double) * ctx->s, cudaMemcpyDeviceToHost,
+                                      ctx->stream));
+        if (error_bound)
+            HPBJ_CUDA(cudaMemcpyAsync(error_bound, ctx->d_ebound, sizeof(double) * ctx->s, cudaMemcpyDeviceToHost,
+                                      ctx->stream));
+        HPBJ_CUDA(cudaStreamSynchronize(ctx->stream));
     });
 }
 

@@ -193,6 +193,20 @@ void launch_cycle_end(const KrylovBufs& kb, SolveState* sst, cudaGraphConditiona
                       int64_t* launches);
 void launch_solve_y(const KrylovBufs& kb, SolveState* sst, cudaStream_t st, int64_t* launches);
 
+// ---- diag.cu --------------------------------------------------------------
+struct DiagParams {
+    int s;
+    int dmax;
+    const int* bstart;
+    const int64_t* fac_off;
+    const float* fac;       // dense LU panels
+    const int* piv;
+    DevCsr a;               // permuted matrix
+    double* cond;           // s: cond_1 estimate
+    double* ebound;         // s: (cond*2^-53 + 2^-24)*cond
+};
+void launch_block_cond(const DiagParams& p, int num_sms, cudaStream_t st, int64_t* launches);
+
 // ---- fused.cu -------------------------------------------------------------
 // A whole Arnoldi cycle (apply, SpMV, compact-WY MGS, Givens per step) as one
 // persistent cooperative kernel; ok = false when the shared-memory tables do

@@ -210,3 +210,25 @@ def test_dimension_mismatch_raises():
     p = hp.Preconditioner.block_jacobi(fx.diag_csr([2.0, 4.0, 1.0]), hp.partition_from_assignment([0, 1, 2], 3))
     with pytest.raises(ValueError):
         p.apply([1.0, 2.0])
+
+
+# ---------------------------------------------------------------------------
+# Preconditioner diagnostics: cond_estimate_block /
+# block_error_bound on the device vs the reference's FP64 estimates.
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape", ["small", "large"])
+def test_block_condition_estimates_match_reference(ref, shape):
+    if shape == "small":  # dims <= 64: exact inverse 1-norm
+        a, s = fx.random_dd(300, 5, 13), 6
+    else:  # dims > 64: Hager estimator
+        a, s = fx.laplacian_2d(24, 24), 4
+    part = hp.partition_graph(a, s, 0.1)
+    p = hp.Preconditioner.block_jacobi(a, part)
+    st = p.stats()
+    cond = np.array([x["cond_estimate"] for x in st])
+    eb = np.array([x["error_bound"] for x in st])
+    rc, reb, _ = ref.block_stats(a.row_starts, a.col_indices, a.values, s, part.assignment)
+    # FP64 arithmetic on the FP32 factors vs the reference's FP64 factors
+    assert np.allclose(cond, rc, rtol=1e-4), (cond, rc)
+    assert np.allclose(eb, reb, rtol=2e-4)
+    assert np.all(cond >= 1.0)

@@ -16,8 +16,7 @@
 // Differences from the reference harness: the device path
 // implements the north star's precision mix only, so --precision defaults to
 // "hybrid" and "double" is rejected; --precond accepts block-jacobi only;
-// --neumann-order must be 0 and --ritz is rejected; cond_estimate and
-// error_bound are reported as null (diagnostics are not computed on device).
+// --neumann-order must be 0 and --ritz is rejected.
 // Exit codes: 0 converged, 2 not converged (solve), 1 error.
 #include <algorithm>
 #include <chrono>
@@ -228,6 +227,7 @@ struct RunResult {
     SolveReport report;
     std::vector<double> x;
     std::vector<index_t> block_dim, block_nnz, block_pert;
+    std::vector<double> block_cond, block_ebound;
 };
 
 std::string matrix_name_of(const std::string& path) {
@@ -354,10 +354,15 @@ RunResult run_spec(const RunSpec& spec) {  // bjgmres_cli.cpp:112-168
     opts.eps_pivot = spec.eps_pivot;
     const std::vector<index_t> bnnz = block_nnz_of(part, a);
     Preconditioner p = Preconditioner::block_jacobi(a, std::move(part), opts);
+    // with_cond_estimates defaults to true in the reference (preconditioner.hpp:37):
+    // the estimates are part of its setup time
+    const auto stats = p.stats(true);
     out.setup_ms = ms_since(t_setup);
-    for (const auto& st : p.stats()) {
+    for (const auto& st : stats) {
         out.block_dim.push_back(st.block_dim);
         out.block_pert.push_back(st.perturbation_count);
+        out.block_cond.push_back(st.cond_estimate);
+        out.block_ebound.push_back(st.error_bound);
     }
     out.block_nnz = bnnz;
     const std::vector<double> b = make_rhs(spec, a);
@@ -395,7 +400,8 @@ std::string report_json(const RunSpec& spec, const RunResult& r) {  // bjgmres_c
     for (size_t b = 0; b < r.block_dim.size(); ++b) {
         o += (b ? ",\n    " : "\n    ");
         o += "{\"dim\": " + jint(r.block_dim[b]) + ", \"nnz\": " + jint(r.block_nnz[b]) + ", \"perturbations\": " +
-             jint(r.block_pert[b]) + ", \"cond_estimate\": null, \"error_bound\": null}";
+             jint(r.block_pert[b]) + ", \"cond_estimate\": " + jnum(r.block_cond[b]) + ", \"error_bound\": " +
+             jnum(r.block_ebound[b]) + "}";
     }
     o += "\n  ]}\n}\n";
     return o;
