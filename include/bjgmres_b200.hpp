@@ -110,6 +110,7 @@ inline Partition partition_from_assignment(std::vector<index_t> assignment, inde
 
 struct BlockJacobiOptions {  // preconditioner.hpp:32-38 (Hybrid policy)
     double eps_pivot = 1e-10;
+    int neumann_order = 0;  // 0 = direct block solves (preconditioner.hpp:34)
 };
 
 struct PreconditionerStats {  // preconditioner.hpp:14-20 (block_nnz: see measure_block_nnz)
@@ -131,6 +132,7 @@ public:
         hpbj_ctx* raw = nullptr;
         detail::check(hpbj_create(&raw, device), nullptr);
         p.ctx_ = std::shared_ptr<hpbj_ctx>(raw, hpbj_destroy);
+        detail::check(hpbj_bj_set_neumann_order(raw, opts.neumann_order), raw);
         detail::check(hpbj_set_matrix(raw, a.rows(), a.row_starts().data(), a.col_indices().data(), a.values().data()),
                       raw);
         hpbj_setup_info info{};
@@ -138,6 +140,7 @@ public:
                                      opts.eps_pivot, &info);
         detail::check(rc, raw, info.singular_column);
         p.n_ = a.rows();
+        p.neumann_ = opts.neumann_order;
         p.matrix_ = &a;
         p.partition_ = std::make_shared<const Partition>(std::move(partition));
         return p;
@@ -151,6 +154,16 @@ public:
             throw std::invalid_argument("preconditioner apply: dimension mismatch");
         std::vector<double> z(n_);
         detail::check(hpbj_bj_apply(ctx_.get(), v.data(), z.data()), ctx_.get());
+        return z;
+    }
+    int neumann_order() const { return neumann_; }
+    // apply_neumann<float> (preconditioner.hpp:79-83) on the matrix the
+    // preconditioner was built from: z = sum_{i<=k} (I - Phi^-1 A)^i Phi^-1 v
+    std::vector<double> apply_neumann(std::span<const double> v, int k) const {
+        if (static_cast<index_t>(v.size()) != n_)
+            throw std::invalid_argument("preconditioner apply: dimension mismatch");
+        std::vector<double> z(n_);
+        detail::check(hpbj_bj_apply_neumann(ctx_.get(), v.data(), z.data(), k), ctx_.get());
         return z;
     }
     std::vector<PreconditionerStats> stats(bool with_cond_estimates = true) const {
@@ -172,6 +185,7 @@ private:
     std::shared_ptr<const Partition> partition_;
     const SparseMatrix* matrix_ = nullptr;
     index_t n_ = 0;
+    int neumann_ = 0;
 };
 
 struct GmresConfig {  // gmres.hpp:89-97

@@ -166,6 +166,16 @@ int hpbj_bj_refactor(hpbj_ctx* ctx, hpbj_setup_info* info);
 /* Preconditioner::apply<float> (preconditioner.hpp:69-70, preconditioner.cpp:159-188),
  * original ordering; v is rounded to FP32 on load, z returned widened. */
 int hpbj_bj_apply(hpbj_ctx* ctx, const double* v, double* z);
+/* BlockJacobiOptions::neumann_order (preconditioner.hpp:34, preconditioner.cpp:110):
+ * order k > 0 makes hpbj_gmres apply the truncated Neumann series in place of
+ * the block solves (preconditioned<T>, gmres.cpp:91-95), FP32 in the Arnoldi
+ * step and FP64 in the x-update. k <= 0 (default 0) = direct block solves. */
+int hpbj_bj_set_neumann_order(hpbj_ctx* ctx, int order);
+/* Preconditioner::apply_neumann<float> (preconditioner.hpp:79-83,
+ * preconditioner.cpp:200-220): z = sum_{i=0..k} (I - Phi^-1 A)^i Phi^-1 v,
+ * original ordering. HPBJ_ELOGIC without factors, HPBJ_EINVAL for k < 0 or
+ * k > the order set with hpbj_bj_set_neumann_order. */
+int hpbj_bj_apply_neumann(hpbj_ctx* ctx, const double* v, double* z, int k);
 /* Per-block factors F = L_strict + U in pivot order, row-major dim x dim,
  * and LUFactors::pivot_rows (lu.hpp:37-50). */
 int hpbj_get_block_factors(hpbj_ctx* ctx, int64_t block, int64_t* dim, float* f,

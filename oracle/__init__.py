@@ -212,8 +212,29 @@ class Ref:
                                      ctypes.c_int(1 if fp32 else 0), _p(vin, _f64p), _p(z, _f64p)))
         return z
 
+    def apply_neumann(self, rp, ci, v, s, assignment, vin, order, k, eps=1e-10, fp32=True):
+        rp, ci, v = self._csr(rp, ci, v)
+        n = len(rp) - 1
+        asg = np.ascontiguousarray(assignment, np.int64)
+        vin = np.ascontiguousarray(vin, np.float64)
+        z = np.zeros(n)
+        self._chk(self.L.bjref_apply_neumann(ctypes.c_int64(n), _p(rp, _i64p), _p(ci, _i64p), _p(v, _f64p),
+                                             ctypes.c_int64(s), _p(asg, _i64p), ctypes.c_double(eps),
+                                             ctypes.c_int(order), ctypes.c_int(k), ctypes.c_int(1 if fp32 else 0),
+                                             _p(vin, _f64p), _p(z, _f64p)))
+        return z
+
     def solve(self, rp, ci, v, s, b, m, tol, max_restarts, hybrid=True, assignment=None,
-              absolute_tol=False, eps=1e-10, cond_estimates=False):
+              absolute_tol=False, eps=1e-10, cond_estimates=False, neumann_order=0):
+        self.L.bjref_set_neumann_order(ctypes.c_int(neumann_order))
+        try:
+            return self._solve(rp, ci, v, s, b, m, tol, max_restarts, hybrid, assignment, absolute_tol, eps,
+                               cond_estimates)
+        finally:
+            self.L.bjref_set_neumann_order(ctypes.c_int(0))
+
+    def _solve(self, rp, ci, v, s, b, m, tol, max_restarts, hybrid, assignment, absolute_tol, eps,
+               cond_estimates):
         rp, ci, v = self._csr(rp, ci, v)
         n = len(rp) - 1
         b = np.ascontiguousarray(b, np.float64)

@@ -287,6 +287,38 @@ int bjref_apply(int64_t n, const int64_t* rp, const int64_t* ci, const double* v
     });
 }
 
+/// Preconditioner::apply_neumann<T> (preconditioner.cpp:200-220), original
+/// ordering; built with BlockJacobiOptions::neumann_order = order; mode 0 =
+/// binary64, 1 = binary32 (Hybrid factors and a binary32 SpMV).
+int bjref_apply_neumann(int64_t n, const int64_t* rp, const int64_t* ci, const double* v,
+                        int64_t s, const int64_t* assignment, double eps, int order, int k, int mode,
+                        const double* vin, double* zout) {
+    return guarded([&] {
+        SparseMatrix a = make_matrix(n, rp, ci, v);
+        a.materialize_low();
+        BlockJacobiOptions opts;
+        opts.eps_pivot = eps;
+        opts.neumann_order = order;
+        opts.policy.mode = PrecisionMode::Hybrid;
+        opts.with_cond_estimates = false;
+        const Preconditioner p = Preconditioner::block_jacobi(
+            a, partition_from_assignment(std::vector<index_t>(assignment, assignment + n), s),
+            opts);
+        if (mode == 1) {
+            const std::vector<float> vf(vin, vin + n);
+            const std::vector<float> zf = p.apply_neumann<float>(a, vf, k);
+            for (int64_t i = 0; i < n; ++i) zout[i] = zf[i];
+        } else {
+            const std::vector<double> z = p.apply_neumann<double>(a, std::span<const double>(vin, n), k);
+            std::memcpy(zout, z.data(), sizeof(double) * n);
+        }
+    });
+}
+
+static int g_neumann_order = 0;  // BlockJacobiOptions::neumann_order for bjref_solve
+
+void bjref_set_neumann_order(int order) { g_neumann_order = order; }
+
 /// Full reference path exactly as run_spec (bjgmres_cli.cpp:112-168):
 /// materialize_low, graph_from_matrix, partition_graph(s, 0.1) (or the given
 /// assignment), block_jacobi, hybrid_restart_gmres. hist is (cycle, iter,
@@ -317,6 +349,7 @@ int bjref_solve(int64_t n, const int64_t* rp, const int64_t* ci, const double* v
         opts.eps_pivot = eps;
         opts.policy.mode = hybrid ? PrecisionMode::Hybrid : PrecisionMode::DoubleOnly;
         opts.with_cond_estimates = cond_estimates != 0;
+        opts.neumann_order = g_neumann_order;
         auto t0 = std::chrono::steady_clock::now();
         const Preconditioner p = Preconditioner::block_jacobi(a, std::move(part), opts);
         rep->ms_block_jacobi = ms_since(t0);

@@ -391,6 +391,15 @@ class Context:
         self.check(self.lib.hpbj_bj_apply(self.h, _p(v, _abi.f64p), _p(z, _abi.f64p)))
         return z
 
+    def set_neumann_order(self, order: int):
+        self.check(self.lib.hpbj_bj_set_neumann_order(self.h, int(order)))
+
+    def apply_neumann(self, v, k: int):
+        v = _f64(v)
+        z = np.zeros_like(v)
+        self.check(self.lib.hpbj_bj_apply_neumann(self.h, _p(v, _abi.f64p), _p(z, _abi.f64p), int(k)))
+        return z
+
     def block_factors(self, b: int):
         d = ctypes.c_int64()
         self.check(self.lib.hpbj_get_block_factors(self.h, b, ctypes.byref(d), None, None))
@@ -467,11 +476,7 @@ class BlockJacobiOptions:
     """preconditioner.hpp:32-38 (Hybrid policy only: FP32 factors)."""
 
     eps_pivot: float = 1e-10
-    neumann_order: int = 0
-
-    def __post_init__(self):
-        if self.neumann_order != 0:
-            raise ValueError("neumann_order > 0 is not on the HPBJ hot path (DESIGN.md: out of scope)")
+    neumann_order: int = 0  # 0 = direct block solves; k > 0: truncated Neumann series in the solve
 
 
 class Preconditioner:
@@ -492,6 +497,7 @@ class Preconditioner:
         if partition.num_nodes() != a.n:
             raise ValueError("block_jacobi: partition does not cover the matrix")
         ctx = ctx or Context(device)
+        ctx.set_neumann_order(opts.neumann_order)
         ctx.set_matrix(a)
         info = ctx.bj_setup(partition, opts.eps_pivot)
         return Preconditioner(ctx, a, partition, opts, info)
@@ -505,6 +511,17 @@ class Preconditioner:
         if len(v) != self.dim():
             raise ValueError("preconditioner apply: dimension mismatch")
         return self.ctx.apply(v)
+
+    def neumann_order(self) -> int:
+        return self.opts.neumann_order
+
+    def apply_neumann(self, v, k: int) -> np.ndarray:
+        """apply_neumann<float> (preconditioner.cpp:200-220): z = sum_{i=0..k}
+        (I - Phi^-1 A)^i Phi^-1 v on the matrix the preconditioner was built from."""
+        v = _f64(v)
+        if len(v) != self.dim():
+            raise ValueError("preconditioner apply: dimension mismatch")
+        return self.ctx.apply_neumann(v, k)
 
     def block_factors(self, b: int):
         return self.ctx.block_factors(b)

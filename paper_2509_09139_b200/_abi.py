@@ -116,6 +116,8 @@ SIGNATURES = {
     "hpbj_bj_setup": (ctypes.c_int, [vp, i64, i64p, i64p, f64, ctypes.POINTER(SetupInfo)]),
     "hpbj_bj_refactor": (ctypes.c_int, [vp, ctypes.POINTER(SetupInfo)]),
     "hpbj_bj_apply": (ctypes.c_int, [vp, f64p, f64p]),
+    "hpbj_bj_set_neumann_order": (ctypes.c_int, [vp, ctypes.c_int]),
+    "hpbj_bj_apply_neumann": (ctypes.c_int, [vp, f64p, f64p, ctypes.c_int]),
     "hpbj_get_block_factors": (ctypes.c_int, [vp, i64, i64p, f32p, i64p]),
     "hpbj_get_block_stats": (ctypes.c_int, [vp, i64p, i64p]),
     "hpbj_gmres_default_opts": (None, [ctypes.POINTER(GmresOpts)]),

@@ -27,12 +27,14 @@ namespace {
 struct Pool {
     std::multimap<size_t, void*> free_;
     std::unordered_map<void*, size_t> size_;
+    bool poison = false;  // HPBJ_POISON=1: every block handed out is filled with 0xff (debug)
     void* get(size_t bytes) {
         bytes = std::max<size_t>(256, (bytes + 255) & ~size_t(255));
         auto it = free_.lower_bound(bytes);
         if (it != free_.end() && it->first <= 2 * bytes + (1 << 20)) {
             void* p = it->second;
             free_.erase(it);
+            if (poison) HPBJ_CUDA(cudaMemset(p, 0xff, bytes));
             return p;
         }
         void* p = nullptr;
@@ -48,6 +50,7 @@ struct Pool {
             HPBJ_CUDA(cudaMalloc(&p, bytes));
         }
         size_[p] = bytes;
+        if (poison) HPBJ_CUDA(cudaMemset(p, 0xff, bytes));
         return p;
     }
     void put(void* p) {
@@ -220,6 +223,10 @@ struct hpbj_ctx {
     KrylovBufs kb;
     SolveState* d_st = nullptr;
     float* d_z32 = nullptr;
+    int neumann = 0;                 // BlockJacobiOptions::neumann_order (preconditioner.hpp:34)
+    float* d_nterm32 = nullptr;      // Neumann series term (Arnoldi step, FP32)
+    double* d_nterm64 = nullptr;     // Neumann series term / sum (x-update, FP64)
+    double* d_nacc64 = nullptr;
     double* d_xp = nullptr;  // x (permuted)
     double* d_bp = nullptr;  // b (permuted)
     double* d_r = nullptr;
@@ -307,6 +314,9 @@ struct hpbj_ctx {
         dfree(kb.partials);
         dfree(d_st);
         dfree(d_z32);
+        dfree(d_nterm32);
+        dfree(d_nterm64);
+        dfree(d_nacc64);
         dfree(d_xp);
         dfree(d_bp);
         dfree(d_r);
@@ -385,6 +395,9 @@ void ensure_ws(hpbj_ctx* c, int m) {
     HPBJ_CUDA(cudaMemset(c->d_st, 0, sizeof(SolveState)));
     dslot(c->d_z32, ldv);
     HPBJ_CUDA(cudaMemset(c->d_z32, 0, sizeof(float) * ldv));
+    dslot(c->d_nterm32, ldv);
+    dslot(c->d_nterm64, ldv);
+    dslot(c->d_nacc64, ldv);
     dslot(c->d_xp, ldv);
     dslot(c->d_bp, ldv);
     dslot(c->d_r, ldv);
@@ -507,7 +520,19 @@ void enqueue_cycle_head(hpbj_ctx* c, cudaGraphConditionalHandle hin) {
 void enqueue_step(hpbj_ctx* c, cudaGraphConditionalHandle hin, int it) {
     KrylovBufs& kb = c->kb;
     record_kernel(c, 3 * it + 0, true);
-    launch_apply_step(spk_view(c), kb.V, kb.ldv, c->d_st, c->d_z32, c->stream, &c->launches);
+    if (c->neumann > 0) {
+        // z = sum_{i<=k} (I - M^-1 A)^i M^-1 v_j in FP32 (preconditioned<float>, gmres.cpp:91-95);
+        // A term on the FP64 SpMV of the FP32 term, the step's w as scratch
+        launch_apply_neumann_f32(spk_view(c), nullptr, kb.V, kb.ldv, c->d_nterm32, c->d_z32, nullptr, 1, c->d_st,
+                                 c->stream, &c->launches);
+        for (int i = 1; i <= c->neumann; ++i) {
+            launch_spmv_f32x(c->B, c->planB, c->d_nterm32, kb.w, c->d_st, c->stream, &c->launches);
+            launch_apply_neumann_f32(spk_view(c), kb.w, nullptr, 0, c->d_nterm32, c->d_z32, nullptr, 0, c->d_st,
+                                     c->stream, &c->launches);
+        }
+    } else {
+        launch_apply_step(spk_view(c), kb.V, kb.ldv, c->d_st, c->d_z32, c->stream, &c->launches);
+    }
     record_kernel(c, 3 * it + 0, false);
     record_kernel(c, 3 * it + 1, true);
     launch_spmv_f32x(c->B, c->planB, c->d_z32, kb.w, c->d_st, c->stream, &c->launches);
@@ -524,7 +549,17 @@ void enqueue_cycle_fused(hpbj_ctx* c) {
 void enqueue_cycle_tail(hpbj_ctx* c, cudaGraphConditionalHandle hout) {
     KrylovBufs& kb = c->kb;
     launch_solve_y(kb, c->d_st, c->stream, &c->launches);
-    launch_apply_update(spk_view(c), kb.V, kb.ldv, kb.y, c->d_st, c->d_xp, c->stream, &c->launches);
+    if (c->neumann > 0) {  // preconditioned<double> (gmres.cpp:158): FP64 series, x += sum
+        launch_apply_neumann_f64(spk_view(c), nullptr, kb.V, kb.ldv, kb.y, c->d_nterm64, c->d_nacc64, nullptr, 1,
+                                 c->d_st, c->stream, &c->launches);
+        for (int i = 1; i <= c->neumann; ++i) {
+            launch_spmv_f64x(c->B, c->planB, c->d_nterm64, kb.w, c->stream, &c->launches);
+            launch_apply_neumann_f64(spk_view(c), kb.w, nullptr, 0, nullptr, c->d_nterm64, c->d_nacc64,
+                                     i == c->neumann ? c->d_xp : nullptr, 0, c->d_st, c->stream, &c->launches);
+        }
+    } else {
+        launch_apply_update(spk_view(c), kb.V, kb.ldv, kb.y, c->d_st, c->d_xp, c->stream, &c->launches);
+    }
     launch_residual(c->B, c->planB, c->d_xp, c->d_bp, c->d_r, c->d_st, c->d_red, c->stream, &c->launches);
     launch_cycle_end(kb, c->d_st, hout, c->stream, &c->launches);
 }
@@ -545,7 +580,8 @@ std::vector<uintptr_t> graph_signature(const hpbj_ctx* c) {
             (uintptr_t)c->d_dtile, (uintptr_t)c->d_eval, (uintptr_t)c->d_eidx, (uintptr_t)L.grid, (uintptr_t)L.threads, (uintptr_t)L.slice,
             (uintptr_t)L.smem, (uintptr_t)L.icwy, (uintptr_t)L.w_in_smem, (uintptr_t)c->fused.ok,
             (uintptr_t)c->fused.grid, (uintptr_t)c->fused.slice, (uintptr_t)c->fused.ystride,
-            (uintptr_t)c->fused.smem, (uintptr_t)c->fused.nnz_cap, (uintptr_t)c->d_ent_off};
+            (uintptr_t)c->fused.smem, (uintptr_t)c->fused.nnz_cap, (uintptr_t)c->d_ent_off,
+            (uintptr_t)c->neumann, (uintptr_t)c->d_nterm32, (uintptr_t)c->d_nterm64, (uintptr_t)c->d_nacc64};
 }
 
 // The whole restart loop as one CUDA graph: WHILE(cycles) { cycle_init;
@@ -727,7 +763,7 @@ void solve(hpbj_ctx* c, const double* d_b, double* d_x, const hpbj_gmres_opts* o
         R.converged = 1;
     } else {
         const bool use_graph = !c->profiling && c->use_graph;
-        c->fused = c->use_fused ? plan_fused(n, c->s, c->dmax, c->num_sms, m, c->planB.n_long > 0,
+        c->fused = c->use_fused && c->neumann == 0 ? plan_fused(n, c->s, c->dmax, c->num_sms, m, c->planB.n_long > 0,
                                              c->h_rowlen_perm.data())
                                 : FusedPlan{};
         if (c->fused.ok && getenv("HPBJ_FUSED_PROF") && !c->d_fprof) {
@@ -854,6 +890,8 @@ int hpbj_create(hpbj_ctx** out, int device) {
         c->use_graph = !(ng && ng[0] == '1');
         const char* nf = getenv("HPBJ_FUSED");
         c->use_fused = !(nf && nf[0] == '0');
+        const char* pz = getenv("HPBJ_POISON");
+        c->pool.poison = pz && pz[0] == '1';
         *out = c;
     });
 }
@@ -1144,6 +1182,41 @@ int hpbj_bj_apply(hpbj_ctx* ctx, const double* v, double* z) {
         HPBJ_CUDA(cudaMemcpyAsync(ctx->d_tmpx, v, sizeof(double) * n, cudaMemcpyHostToDevice, st));
         launch_permute_vec(n, ctx->d_perm, ctx->d_tmpx, ctx->d_tmpy, false, st, &ctx->launches);
         launch_apply_vec(spk_view(ctx), ctx->d_tmpy, ctx->d_tmpx, st, &ctx->launches);
+        launch_permute_vec(n, ctx->d_perm, ctx->d_tmpx, ctx->d_tmpy, true, st, &ctx->launches);
+        HPBJ_CUDA(cudaMemcpyAsync(z, ctx->d_tmpy, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+        HPBJ_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+int hpbj_bj_set_neumann_order(hpbj_ctx* ctx, int order) {
+    if (!ctx) return HPBJ_EINVAL;
+    return guard(&ctx->err, [&] {
+        ctx->neumann = order;  // <= 0: direct block solves (gmres.cpp:93 tests > 0)
+    });
+}
+
+int hpbj_bj_apply_neumann(hpbj_ctx* ctx, const double* v, double* z, int k) {
+    if (!ctx) return HPBJ_EINVAL;
+    t_pool = &ctx->pool;
+    t_slots = &ctx->slots;
+    return guard(&ctx->err, [&] {
+        if (!ctx->has_pc) fail(HPBJ_ELOGIC, "apply_neumann: block factors not available");
+        if (k < 0 || k > ctx->neumann)
+            fail(HPBJ_EINVAL, "apply_neumann: order exceeds the one the preconditioner was built with");
+        const int n = ctx->A.n;
+        cudaStream_t st = ctx->stream;
+        dslot(ctx->d_nterm32, n);
+        dslot(ctx->d_z32, n);
+        HPBJ_CUDA(cudaMemcpyAsync(ctx->d_tmpx, v, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+        launch_permute_vec(n, ctx->d_perm, ctx->d_tmpx, ctx->d_tmpy, false, st, &ctx->launches);
+        // apply_neumann<float>: term = acc = M^-1 v; k times: term -= M^-1 A term, acc += term
+        launch_apply_neumann_f32(spk_view(ctx), ctx->d_tmpy, nullptr, 0, ctx->d_nterm32, ctx->d_z32,
+                                 k == 0 ? ctx->d_tmpx : nullptr, 1, nullptr, st, &ctx->launches);
+        for (int i = 1; i <= k; ++i) {
+            launch_spmv_f32x(ctx->B, ctx->planB, ctx->d_nterm32, ctx->d_tmpy, nullptr, st, &ctx->launches);
+            launch_apply_neumann_f32(spk_view(ctx), ctx->d_tmpy, nullptr, 0, ctx->d_nterm32, ctx->d_z32,
+                                     i == k ? ctx->d_tmpx : nullptr, 0, nullptr, st, &ctx->launches);
+        }
         launch_permute_vec(n, ctx->d_perm, ctx->d_tmpx, ctx->d_tmpy, true, st, &ctx->launches);
         HPBJ_CUDA(cudaMemcpyAsync(z, ctx->d_tmpy, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
         HPBJ_CUDA(cudaStreamSynchronize(st));

@@ -14,12 +14,20 @@
 
 namespace hpbj {
 
+inline const char* src_base(const char* f) {
+    const char* b = f;
+    for (const char* p = f; *p; ++p)
+        if (*p == '/') b = p + 1;
+    return b;
+}
+
 #define HPBJ_CUDA(call)                                                                   \
     do {                                                                                  \
         cudaError_t e_ = (call);                                                          \
         if (e_ != cudaSuccess)                                                            \
             ::hpbj::fail(e_ == cudaErrorMemoryAllocation ? HPBJ_ENOMEM : HPBJ_ECUDA,      \
-                         std::string(#call) + ": " + cudaGetErrorString(e_));             \
+                         std::string(#call) + " [" + ::hpbj::src_base(__FILE__) + ":" +   \
+                             std::to_string(__LINE__) + "]: " + cudaGetErrorString(e_));  \
     } while (0)
 
 constexpr int kWarp = 32;

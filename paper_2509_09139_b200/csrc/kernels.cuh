@@ -129,6 +129,16 @@ void launch_apply_vec(const SpkView& v, const double* vin, double* z64, cudaStre
 void launch_apply_update(const SpkView& v, const double* V, int ldv, const double* y, const SolveState* sst,
                          double* x, cudaStream_t st, int64_t* launches);
 
+// Neumann-series applies (apply_neumann, preconditioner.cpp:200-220). init = 1:
+// term = acc = M^-1 src; init = 0: term -= M^-1 src, acc += term. src is V[:, st->j]
+// (V != null; f32) / sum_i y_i V[i] (V != null; f64) or vin. out/xadd optional.
+void launch_apply_neumann_f32(const SpkView& v, const double* vin, const double* V, int ldv, float* term,
+                              float* acc, double* out, int init, const SolveState* sst, cudaStream_t st,
+                              int64_t* launches);
+void launch_apply_neumann_f64(const SpkView& v, const double* vin, const double* V, int ldv, const double* y,
+                              double* term, double* acc, double* xadd, int init, const SolveState* sst,
+                              cudaStream_t st, int64_t* launches);
+
 // ---- spmv.cu --------------------------------------------------------------
 struct SpmvPlan {
     int group = 8;            // lanes per row

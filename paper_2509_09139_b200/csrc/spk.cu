@@ -84,6 +84,14 @@ __global__ void k_spk_build(SpkBuild p) {
         }
         const int base = p.ent_off[P];
         if (lane == 0) p.desc[P] = SpkPanel{base, tl, tu, base + pl};
+        // the folds read whole quads: the padding up to each part's end is (0, col 0, row 0)
+        if (lane < pl - tl) {
+            p.eval[base + tl + lane] = 0.0f;
+            reinterpret_cast<IdxT*>(p.eidx)[base + tl + lane] = (IdxT)0;
+        } else if (lane >= 4 && lane - 4 < pu - tu) {
+            p.eval[base + pl + tu + lane - 4] = 0.0f;
+            reinterpret_cast<IdxT*>(p.eidx)[base + pl + tu + lane - 4] = (IdxT)0;
+        }
         // Inverse of the 32x32 diagonal triangle, in FP64 from the FP32
         // factors: Linv (unit lower) and Uinv (upper incl. diagonal), written
         // as 9 float4 quads per row (see kernels.cuh SpkView::dtile).
@@ -222,6 +230,58 @@ void launch_spk_pack(const SpkBuild& p, cudaStream_t st, int64_t* launches) {
     fn<<<grid, 128, smem, st>>>(p);
     *launches += 1;
     HPBJ_CUDA(cudaGetLastError());
+}
+
+namespace {
+
+// Truncated Neumann series z = sum_{i=0..k} (I - Phi^-1 A)^i Phi^-1 v
+// (apply_neumann, preconditioner.cpp:200-220): the first apply seeds term and
+// acc, each later apply (of A term) folds "term -= corr; acc += term" into its
+// store, in T like the reference's vectors; xadd (optional) receives x += acc.
+template <class T>
+struct DstNeumann {
+    T* term;
+    T* acc;
+    double* xadd;
+    double* out;
+    int init;
+    template <class V>
+    __device__ void operator()(int row, V v) const {
+        T a;
+        if (init) {
+            term[row] = (T)v;
+            a = (T)v;
+        } else {
+            const T t = term[row] - (T)v;
+            term[row] = t;
+            a = acc[row] + t;
+        }
+        acc[row] = a;
+        if (xadd) xadd[row] = xadd[row] + (double)a;
+        if (out) out[row] = (double)a;
+    }
+};
+struct SrcVec64 {
+    const double* v;
+    __device__ double operator()(int row) const { return __ldg(v + row); }
+};
+
+}  // namespace
+
+void launch_apply_neumann_f32(const SpkView& v, const double* vin, const double* V, int ldv, float* term,
+                              float* acc, double* out, int init, const SolveState* sst, cudaStream_t st,
+                              int64_t* launches) {
+    const DstNeumann<float> dst{term, acc, nullptr, out, init};
+    if (V) launch<float>(v, SrcDown{V, ldv, sst}, dst, sst, st, launches);
+    else launch<float>(v, SrcVec{vin}, dst, sst, st, launches);
+}
+
+void launch_apply_neumann_f64(const SpkView& v, const double* vin, const double* V, int ldv, const double* y,
+                              double* term, double* acc, double* xadd, int init, const SolveState* sst,
+                              cudaStream_t st, int64_t* launches) {
+    const DstNeumann<double> dst{term, acc, xadd, nullptr, init};
+    if (V) launch<double>(v, SrcBasis{V, ldv, y, sst}, dst, nullptr, st, launches);
+    else launch<double>(v, SrcVec64{vin}, dst, nullptr, st, launches);
 }
 
 void launch_apply_step(const SpkView& v, const double* V, int ldv, const SolveState* sst, float* z32,

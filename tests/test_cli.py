@@ -124,3 +124,18 @@ def test_bench_table_and_csv(mtx, tmp_path):
     assert rows[0] == ["matrix_name", "n", "nnz", "nnz_per_row", "precond_setup_ms", "solve_ms", "iterations",
                        "converged", "final_residual"]
     assert len(rows) == 3 and all(row[0] == "rdd300" and row[7] == "true" for row in rows[1:])
+
+
+@pytest.mark.gpu
+def test_solve_with_neumann_order(ref, mtx, tmp_path):
+    path, a = mtx
+    rep = str(tmp_path / "r.json")
+    r = run("solve", "--matrix", path, "--blocks", "6", "--restart", "20", "--tol", "1e-10", "--rhs", "ones",
+            "--neumann-order", "2", "--report", rep)
+    assert r.returncode == 0, r.stderr
+    doc = json.load(open(rep))
+    assert doc["config"]["neumann_order"] == 2 and doc["result"]["converged"]
+    part = hp.partition_graph(a, 6, 0.1)
+    out = ref.solve(a.row_starts, a.col_indices, a.values, 6, np.ones(a.n), 20, 1e-10, 40, hybrid=True,
+                    assignment=part.assignment, neumann_order=2)
+    assert doc["result"]["iterations"] == out.total_iterations

@@ -208,3 +208,29 @@ def test_invalid_config_raises():
         hp.hybrid_restart_gmres(a, p, [1.0, 1.0], hp.GmresConfig(restart_m=0))
     with pytest.raises(ValueError):
         hp.hybrid_restart_gmres(a, p, [1.0], hp.GmresConfig())
+
+
+@pytest.mark.gpu
+def test_solve_independent_of_stale_device_memory(monkeypatch):
+    """Every device block is poisoned (0xff) on allocation: nothing the setup
+    or the solve reads may depend on memory it did not write (regression: the
+    SPK pack once left the quad padding of its entry parts unwritten)."""
+    a = fx.random_dd(300, 5, 21)
+    part = hp.partition_graph(a, 6, 0.1)
+    b = fx.ones(a.n)
+    cfg = hp.GmresConfig(restart_m=30, tol=1e-10, max_restarts=40)
+
+    def run(fused, order=0):
+        p = hp.Preconditioner.block_jacobi(a, part, hp.BlockJacobiOptions(neumann_order=order))
+        p.ctx.set_fused(fused)
+        return hp.hybrid_restart_gmres(a, p, b, cfg), p.apply(b), p.stats()
+
+    cases = [(True, 0), (False, 0), (False, 2)]
+    clean = [run(f, o) for f, o in cases]
+    monkeypatch.setenv("HPBJ_POISON", "1")
+    for (f, o), (c_out, c_z, c_st) in zip(cases, clean):
+        out, z, st = run(f, o)
+        assert out.report.total_iterations == c_out.report.total_iterations
+        assert np.array_equal(out.x, c_out.x)
+        assert np.array_equal(z, c_z)
+        assert st == c_st

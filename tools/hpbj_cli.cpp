@@ -7,7 +7,7 @@
 //
 //   hpbj_cli solve --matrix A.mtx [--rhs ones|axones|random:SEED|file:PATH]
 //            [--precond block-jacobi] [--blocks S] [--restart M] [--tol T]
-//            [--max-restarts R] [--precision hybrid] [--eps-pivot E]
+//            [--max-restarts R] [--precision hybrid] [--eps-pivot E] [--neumann-order K]
 //            [--partition-file P] [--absolute-tol] [--report R.json]
 //            [--history H.csv]
 //   hpbj_cli bench --specs specs.json [--repetitions K] [--out table.csv]
@@ -16,7 +16,7 @@
 // Differences from the reference harness: the device path
 // implements the north star's precision mix only, so --precision defaults to
 // "hybrid" and "double" is rejected; --precond accepts block-jacobi only;
-// --neumann-order must be 0 and --ritz is rejected.
+// --ritz is rejected.
 // Exit codes: 0 converged, 2 not converged (solve), 1 error.
 #include <algorithm>
 #include <chrono>
@@ -352,6 +352,7 @@ RunResult run_spec(const RunSpec& spec) {  // bjgmres_cli.cpp:112-168
     else part = partition_graph(a, spec.blocks, 0.1);
     BlockJacobiOptions opts;
     opts.eps_pivot = spec.eps_pivot;
+    opts.neumann_order = spec.neumann_order;
     const std::vector<index_t> bnnz = block_nnz_of(part, a);
     Preconditioner p = Preconditioner::block_jacobi(a, std::move(part), opts);
     // with_cond_estimates defaults to true in the reference (preconditioner.hpp:37):
@@ -445,7 +446,6 @@ std::string check_spec(const RunSpec& s, bool blocks_set, bool part_set, bool ne
     if (s.precision != "double" && s.precision != "hybrid") return "unknown precision: " + s.precision;
     if (s.precision == "double")
         return "precision 'double' is not implemented on the GPU path (the hybrid FP32/FP64 mix is)";
-    if (s.neumann_order != 0) return "--neumann-order is not implemented on the GPU path";
     if (s.ritz) return "--ritz is not implemented on the GPU path";
     if (s.blocks < 1 || s.restart_m < 1 || s.max_restarts < 1 || s.tol <= 0.0) return "numeric flags out of range";
     return "";
