@@ -5,10 +5,12 @@
 // bjgmres/{sparse_matrix,graph,partition,preconditioner,gmres}.hpp and
 // linking libhpbj.so: names, argument meaning and exception types match.
 //
-// Differences a caller can observe: the preconditioner is
-// always the Hybrid (FP32) block-Jacobi one and lives on a GPU; the matrix
-// passed to hybrid_restart_gmres must be the one the preconditioner was built
-// from (it is device-resident).
+// Differences a caller can observe: the block-Jacobi
+// preconditioner is the Hybrid (FP32) one and lives on a GPU, so
+// GmresConfig::policy defaults to Hybrid here (DoubleOnly serves the FP64
+// ILU(0) and identity preconditioners); the matrix passed to
+// hybrid_restart_gmres must be the one the preconditioner was built from (it
+// is device-resident).
 #pragma once
 
 #include <memory>
@@ -124,6 +126,30 @@ struct PreconditionerStats {  // preconditioner.hpp:14-20 (block_nnz: see measur
 // immutable device-resident factorisation.
 class Preconditioner {
 public:
+    enum class Kind { Identity, Ilu0, BlockJacobi };  // preconditioner.hpp:55
+
+    static Preconditioner identity(index_t n) {  // bound to the matrix by the solve
+        Preconditioner p;
+        p.kind_ = Kind::Identity;
+        p.n_ = n;
+        return p;
+    }
+    // Preconditioner::from_ilu0 (preconditioner.cpp:94-98): FP64 ILU(0) factors on the device
+    static Preconditioner from_ilu0(const SparseMatrix& a, int device = 0) {
+        Preconditioner p;
+        hpbj_ctx* raw = nullptr;
+        detail::check(hpbj_create(&raw, device), nullptr);
+        p.ctx_ = std::shared_ptr<hpbj_ctx>(raw, hpbj_destroy);
+        detail::check(hpbj_set_matrix(raw, a.rows(), a.row_starts().data(), a.col_indices().data(), a.values().data()),
+                      raw);
+        detail::check(hpbj_ilu0_setup(raw, nullptr), raw);
+        p.kind_ = Kind::Ilu0;
+        p.n_ = a.rows();
+        p.matrix_ = &a;
+        return p;
+    }
+    Kind kind() const { return kind_; }
+
     static Preconditioner block_jacobi(const SparseMatrix& a, Partition partition,
                                        const BlockJacobiOptions& opts = {}, int device = 0) {
         if (partition.num_nodes() != a.rows())
@@ -148,12 +174,14 @@ public:
     index_t dim() const { return n_; }
     const Partition& partition() const { return *partition_; }
 
-    // apply<float> (preconditioner.hpp:69-70): z with M z = v
+    // apply (preconditioner.hpp:69-70): z with M z = v — apply<float> for
+    // block Jacobi, apply<double> for ILU(0) and the identity
     std::vector<double> apply(std::span<const double> v) const {
         if (static_cast<index_t>(v.size()) != n_)
             throw std::invalid_argument("preconditioner apply: dimension mismatch");
+        if (kind_ == Kind::Identity) return std::vector<double>(v.begin(), v.end());
         std::vector<double> z(n_);
-        detail::check(hpbj_bj_apply(ctx_.get(), v.data(), z.data()), ctx_.get());
+        detail::check(hpbj_precond_apply(ctx_.get(), v.data(), z.data()), ctx_.get());
         return z;
     }
     int neumann_order() const { return neumann_; }
@@ -167,6 +195,7 @@ public:
         return z;
     }
     std::vector<PreconditionerStats> stats(bool with_cond_estimates = true) const {
+        if (kind_ != Kind::BlockJacobi) throw std::logic_error("stats: block-Jacobi preconditioner not set up");
         const size_t s = static_cast<size_t>(partition_->num_blocks);
         std::vector<index_t> d(s), pc(s);
         std::vector<double> cond(s, 0.0), eb(s, 0.0);
@@ -186,6 +215,14 @@ private:
     const SparseMatrix* matrix_ = nullptr;
     index_t n_ = 0;
     int neumann_ = 0;
+    Kind kind_ = Kind::BlockJacobi;
+};
+
+enum class PrecisionMode { DoubleOnly, Hybrid };  // types.hpp:15-26
+struct PrecisionPolicy {
+    PrecisionMode mode = PrecisionMode::Hybrid;  // the reference defaults to DoubleOnly (see the header note)
+    bool hybrid() const { return mode == PrecisionMode::Hybrid; }
+    double working_roundoff() const { return hybrid() ? 0x1p-24 : 0x1p-53; }
 };
 
 struct GmresConfig {  // gmres.hpp:89-97
@@ -193,6 +230,7 @@ struct GmresConfig {  // gmres.hpp:89-97
     double tol = 1e-8;
     index_t max_restarts = 40;
     bool absolute_tol = false;
+    PrecisionPolicy policy{};
     double breakdown_tol_factor = 1e2;
 };
 
@@ -226,7 +264,23 @@ inline SolveResult hybrid_restart_gmres(const SparseMatrix& a, const Preconditio
     if (static_cast<index_t>(b.size()) != a.rows()) throw std::invalid_argument("gmres: rhs dimension mismatch");
     if (config.restart_m < 1 || config.tol <= 0.0 || config.max_restarts < 1)
         throw std::invalid_argument("gmres: invalid config");
-    if (p.matrix() != &a) throw std::invalid_argument("gmres: preconditioner was built from another matrix");
+    hpbj_ctx* ctx = p.context();
+    std::shared_ptr<hpbj_ctx> bound;
+    if (p.kind() == Preconditioner::Kind::Identity) {  // identity: a context for this matrix
+        hpbj_ctx* raw = nullptr;
+        detail::check(hpbj_create(&raw, 0), nullptr);
+        bound = std::shared_ptr<hpbj_ctx>(raw, hpbj_destroy);
+        detail::check(hpbj_set_matrix(raw, a.rows(), a.row_starts().data(), a.col_indices().data(), a.values().data()),
+                      raw);
+        detail::check(hpbj_identity_setup(raw), raw);
+        ctx = raw;
+    } else if (p.matrix() != &a) {
+        throw std::invalid_argument("gmres: preconditioner was built from another matrix");
+    }
+    if (p.kind() == Preconditioner::Kind::Ilu0 && config.policy.hybrid())  // lu_solve<float> on FP64-only factors
+        throw std::logic_error("values_low requested before materialize_low()");
+    if (p.kind() == Preconditioner::Kind::BlockJacobi && !config.policy.hybrid())
+        throw std::invalid_argument("gmres: DoubleOnly block Jacobi is not implemented on the GPU path");
     hpbj_gmres_opts o;
     hpbj_gmres_default_opts(&o);
     o.restart_m = config.restart_m;
@@ -234,14 +288,15 @@ inline SolveResult hybrid_restart_gmres(const SparseMatrix& a, const Preconditio
     o.max_restarts = config.max_restarts;
     o.absolute_tol = config.absolute_tol ? 1 : 0;
     o.breakdown_tol_factor = config.breakdown_tol_factor;
+    o.floor_roundoff = config.policy.working_roundoff();
     SolveResult out;
     out.x.resize(a.rows());
     std::vector<hpbj_history_point> hist(config.restart_m * config.max_restarts + 2);
     std::vector<double> cyc(config.max_restarts + 1);
     hpbj_report rep{};
-    detail::check(hpbj_gmres(p.context(), b.data(), out.x.data(), &o, &rep, hist.data(),
-                             static_cast<int64_t>(hist.size()), cyc.data(), static_cast<int64_t>(cyc.size())),
-                  p.context());
+    detail::check(hpbj_gmres(ctx, b.data(), out.x.data(), &o, &rep, hist.data(), static_cast<int64_t>(hist.size()),
+                             cyc.data(), static_cast<int64_t>(cyc.size())),
+                  ctx);
     SolveReport& r = out.report;
     r.converged = rep.converged != 0;
     r.total_iterations = rep.total_iterations;

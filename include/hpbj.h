@@ -41,6 +41,7 @@ extern "C" {
 #define HPBJ_ERANGE 6
 #define HPBJ_ENODEV 7
 #define HPBJ_EIO 8       /* file / parse errors (std::runtime_error)        */
+#define HPBJ_ERUNTIME 9  /* numerical failure (std::runtime_error), e.g. an ILU(0) zero pivot */
 
 typedef struct hpbj_ctx hpbj_ctx;
 
@@ -171,6 +172,25 @@ int hpbj_bj_apply(hpbj_ctx* ctx, const double* v, double* z);
  * the block solves (preconditioned<T>, gmres.cpp:91-95), FP32 in the Arnoldi
  * step and FP64 in the x-update. k <= 0 (default 0) = direct block solves. */
 int hpbj_bj_set_neumann_order(hpbj_ctx* ctx, int order);
+
+/* ---- other preconditioners behind the same solve ----
+ * Each setup makes its preconditioner the one hpbj_gmres uses; block Jacobi
+ * (hpbj_bj_setup / hpbj_bj_refactor) switches back. */
+/* Preconditioner::from_ilu0 (preconditioner.cpp:94-98) with ilu0
+ * (lu.cpp:227-312): FP64 factors in A's pattern, original ordering; the solve
+ * applies them in FP64 (lu_solve<double>) — use floor_roundoff = 2^-53
+ * (DoubleOnly), the only policy under which the reference can apply ILU(0).
+ * HPBJ_EINVAL "ilu0: structurally zero diagonal in row i", HPBJ_ERUNTIME
+ * "ilu0: zero diagonal pivot in row k" (info->singular_column = the row). */
+int hpbj_ilu0_setup(hpbj_ctx* ctx, hpbj_setup_info* info);
+/* Preconditioner::identity (preconditioner.cpp:90-92). */
+int hpbj_identity_setup(hpbj_ctx* ctx);
+/* Preconditioner::apply of the active preconditioner, original ordering:
+ * apply<double> for ILU(0) / identity, apply<float> for block Jacobi. */
+int hpbj_precond_apply(hpbj_ctx* ctx, const double* v, double* z);
+/* The factored values in A's pattern: per row L (unit diagonal implied),
+ * U's diagonal, U — the reference's LUFactors lower/upper concatenated. */
+int hpbj_get_ilu0_values(hpbj_ctx* ctx, double* lu);
 /* Preconditioner::apply_neumann<float> (preconditioner.hpp:79-83,
  * preconditioner.cpp:200-220): z = sum_{i=0..k} (I - Phi^-1 A)^i Phi^-1 v,
  * original ordering. HPBJ_ELOGIC without factors, HPBJ_EINVAL for k < 0 or

@@ -254,6 +254,29 @@ class Ref:
                                      ctypes.c_int64(max_restarts + 1)))
         return self._out(x, rep, hist, cyc)
 
+    def ilu0_values(self, rp, ci, v):
+        rp, ci, v = self._csr(rp, ci, v)
+        out = np.zeros(len(v))
+        self._chk(self.L.bjref_ilu0_values(ctypes.c_int64(len(rp) - 1), _p(rp, _i64p), _p(ci, _i64p), _p(v, _f64p),
+                                           _p(out, _f64p)))
+        return out
+
+    def ilu0_apply(self, rp, ci, v, vin):
+        rp, ci, v = self._csr(rp, ci, v)
+        vin = np.ascontiguousarray(vin, np.float64)
+        z = np.zeros(len(rp) - 1)
+        self._chk(self.L.bjref_ilu0_apply(ctypes.c_int64(len(rp) - 1), _p(rp, _i64p), _p(ci, _i64p), _p(v, _f64p),
+                                          _p(vin, _f64p), _p(z, _f64p)))
+        return z
+
+    def solve_ilu0(self, rp, ci, v, b, m, tol, max_restarts, hybrid=False):
+        """run_spec with --precond ilu0 (bjgmres_cli.cpp:128-131)."""
+        self.L.bjref_set_alt_precond(ctypes.c_int(1))
+        try:
+            return self.solve_identity(rp, ci, v, b, m, tol, max_restarts, hybrid)
+        finally:
+            self.L.bjref_set_alt_precond(ctypes.c_int(0))
+
     def solve_identity(self, rp, ci, v, b, m, tol, max_restarts, hybrid=False):
         rp, ci, v = self._csr(rp, ci, v)
         n = len(rp) - 1

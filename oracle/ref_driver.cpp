@@ -386,8 +386,42 @@ int bjref_solve(int64_t n, const int64_t* rp, const int64_t* ci, const double* v
     });
 }
 
+/// ilu0 (lu.cpp:227-312): the factored values in A's pattern — per row the
+/// LUFactors lower row then the upper row (diagonal first), which is A's own
+/// column order.
+int bjref_ilu0_values(int64_t n, const int64_t* rp, const int64_t* ci, const double* v, double* out) {
+    return guarded([&] {
+        const SparseMatrix a = make_matrix(n, rp, ci, v);
+        const LUFactors f = ilu0(a);
+        const auto ls = f.lower.row_starts();
+        const auto us = f.upper.row_starts();
+        const auto lv = f.lower.values();
+        const auto uv = f.upper.values();
+        int64_t q = 0;
+        for (int64_t i = 0; i < n; ++i) {
+            for (index_t k = ls[i]; k < ls[i + 1]; ++k) out[q++] = lv[k];
+            for (index_t k = us[i]; k < us[i + 1]; ++k) out[q++] = uv[k];
+        }
+    });
+}
+
+/// Preconditioner::from_ilu0(a).apply<double> (preconditioner.cpp:168-170).
+int bjref_ilu0_apply(int64_t n, const int64_t* rp, const int64_t* ci, const double* v, const double* vin,
+                     double* zout) {
+    return guarded([&] {
+        const SparseMatrix a = make_matrix(n, rp, ci, v);
+        const Preconditioner p = Preconditioner::from_ilu0(a);
+        p.apply<double>(std::span<const double>(vin, n), std::span<double>(zout, n));
+    });
+}
+
+static int g_alt_precond = 0;  // bjref_solve_identity: 0 = identity, 1 = ILU(0) (run_spec, cli:128-131)
+
+void bjref_set_alt_precond(int kind) { g_alt_precond = kind; }
+
 /// Identity-preconditioned solve (Preconditioner::identity) for the
-/// reference's unpreconditioned Krylov known-answer tests.
+/// reference's unpreconditioned Krylov known-answer tests; with
+/// bjref_set_alt_precond(1) the ILU(0) preconditioner instead.
 int bjref_solve_identity(int64_t n, const int64_t* rp, const int64_t* ci, const double* v,
                          const double* b, int64_t m, double tol, int64_t max_restarts,
                          int hybrid, double* x, bjref_report* rep, double* hist,
@@ -401,8 +435,9 @@ int bjref_solve_identity(int64_t n, const int64_t* rp, const int64_t* ci, const 
         cfg.tol = tol;
         cfg.max_restarts = max_restarts;
         cfg.policy.mode = hybrid ? PrecisionMode::Hybrid : PrecisionMode::DoubleOnly;
-        const SolveResult sr =
-            hybrid_restart_gmres(a, Preconditioner::identity(n), std::span<const double>(b, n), cfg);
+        const Preconditioner p =
+            g_alt_precond == 1 ? Preconditioner::from_ilu0(a) : Preconditioner::identity(n);
+        const SolveResult sr = hybrid_restart_gmres(a, p, std::span<const double>(b, n), cfg);
         std::memcpy(x, sr.x.data(), sizeof(double) * n);
         const SolveReport& r = sr.report;
         rep->converged = r.converged;

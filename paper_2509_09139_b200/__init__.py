@@ -391,6 +391,25 @@ class Context:
         self.check(self.lib.hpbj_bj_apply(self.h, _p(v, _abi.f64p), _p(z, _abi.f64p)))
         return z
 
+    def ilu0_setup(self) -> _abi.SetupInfo:
+        info = _abi.SetupInfo()
+        self.check(self.lib.hpbj_ilu0_setup(self.h, ctypes.byref(info)), info)
+        return info
+
+    def identity_setup(self):
+        self.check(self.lib.hpbj_identity_setup(self.h))
+
+    def precond_apply(self, v):
+        v = _f64(v)
+        z = np.zeros_like(v)
+        self.check(self.lib.hpbj_precond_apply(self.h, _p(v, _abi.f64p), _p(z, _abi.f64p)))
+        return z
+
+    def ilu0_values(self, nnz: int):
+        out = np.zeros(nnz)
+        self.check(self.lib.hpbj_get_ilu0_values(self.h, _p(out, _abi.f64p)))
+        return out
+
     def set_neumann_order(self, order: int):
         self.check(self.lib.hpbj_bj_set_neumann_order(self.h, int(order)))
 
@@ -480,15 +499,42 @@ class BlockJacobiOptions:
 
 
 class Preconditioner:
-    """Block-Jacobi preconditioner resident on one B200 (preconditioner.hpp:50-98)."""
+    """Preconditioner resident on one B200 (preconditioner.hpp:50-98): block
+    Jacobi (FP32 factors), ILU(0) (FP64 factors) or the identity."""
 
-    def __init__(self, ctx: Context, a: SparseMatrix, part: Partition, opts: BlockJacobiOptions,
-                 info: _abi.SetupInfo):
+    BLOCK_JACOBI, ILU0, IDENTITY = "block_jacobi", "ilu0", "identity"
+
+    def __init__(self, ctx: Optional[Context], a: Optional[SparseMatrix], part: Optional[Partition],
+                 opts: Optional[BlockJacobiOptions], info: Optional[_abi.SetupInfo], kind: str = "block_jacobi",
+                 n: Optional[int] = None):
         self.ctx = ctx
         self.matrix = a
         self.partition = part
-        self.opts = opts
+        self.opts = opts or BlockJacobiOptions()
         self.info = info
+        self.kind = kind
+        self._n = a.n if a is not None else n
+
+    @staticmethod
+    def identity(n: int) -> "Preconditioner":
+        """Preconditioner::identity (preconditioner.cpp:90-92); bound to the
+        matrix by the solve."""
+        return Preconditioner(None, None, None, None, None, kind=Preconditioner.IDENTITY, n=int(n))
+
+    @staticmethod
+    def from_ilu0(a: SparseMatrix, device: int = 0, ctx: Optional[Context] = None) -> "Preconditioner":
+        """Preconditioner::from_ilu0 (preconditioner.cpp:94-98): ILU(0) on the
+        device, FP64 factors in A's pattern."""
+        ctx = ctx or Context(device)
+        ctx.set_matrix(a)
+        info = ctx.ilu0_setup()
+        return Preconditioner(ctx, a, None, None, info, kind=Preconditioner.ILU0)
+
+    def ilu0_values(self) -> np.ndarray:
+        """The factored values in A's pattern (L strictly lower, then U)."""
+        if self.kind != Preconditioner.ILU0:
+            raise LogicError("ilu0: factors not set up")
+        return self.ctx.ilu0_values(self.matrix.nnz())
 
     @staticmethod
     def block_jacobi(a: SparseMatrix, partition: Partition, opts: Optional[BlockJacobiOptions] = None,
@@ -503,13 +549,18 @@ class Preconditioner:
         return Preconditioner(ctx, a, partition, opts, info)
 
     def dim(self) -> int:
-        return self.matrix.n
+        return self._n
 
     def apply(self, v) -> np.ndarray:
-        """apply<float>: z with M z = v (FP32 factors, FP32 arithmetic)."""
+        """z with M z = v: apply<float> for block Jacobi (FP32 factors, FP32
+        arithmetic), apply<double> for ILU(0) and the identity."""
         v = _f64(v)
         if len(v) != self.dim():
             raise ValueError("preconditioner apply: dimension mismatch")
+        if self.kind == Preconditioner.IDENTITY:
+            return v.copy()
+        if self.kind == Preconditioner.ILU0:
+            return self.ctx.precond_apply(v)
         return self.ctx.apply(v)
 
     def neumann_order(self) -> int:
@@ -518,6 +569,8 @@ class Preconditioner:
     def apply_neumann(self, v, k: int) -> np.ndarray:
         """apply_neumann<float> (preconditioner.cpp:200-220): z = sum_{i=0..k}
         (I - Phi^-1 A)^i Phi^-1 v on the matrix the preconditioner was built from."""
+        if self.kind != Preconditioner.BLOCK_JACOBI:
+            raise LogicError("apply_neumann: block factors not available")
         v = _f64(v)
         if len(v) != self.dim():
             raise ValueError("preconditioner apply: dimension mismatch")
@@ -538,15 +591,19 @@ class Preconditioner:
 
 @dataclass
 class GmresConfig:
-    """gmres.hpp:89-97. Hybrid (FP32 preconditioner) is the only policy: the
-    attainable-floor break uses u = 2^-24 (gmres.cpp:130-145)."""
+    """gmres.hpp:89-97. precision is PrecisionPolicy::mode (types.hpp:15-26):
+    "hybrid" (FP32 preconditioner; the default here, the block-Jacobi device
+    path) or "double" (FP64 preconditioner: ILU(0), identity). The
+    attainable-floor break uses its working roundoff, 2^-24 or 2^-53
+    (gmres.cpp:130-145), unless floor_roundoff overrides it."""
 
     restart_m: int = 50
     tol: float = 1e-8
     max_restarts: int = 40
     absolute_tol: bool = False
     breakdown_tol_factor: float = 1e2
-    floor_roundoff: float = ROUNDOFF_SINGLE
+    floor_roundoff: Optional[float] = None
+    precision: str = "hybrid"
 
     def to_opts(self) -> _abi.GmresOpts:
         o = _abi.GmresOpts()
@@ -555,7 +612,10 @@ class GmresConfig:
         o.max_restarts = int(self.max_restarts)
         o.absolute_tol = 1 if self.absolute_tol else 0
         o.breakdown_tol_factor = float(self.breakdown_tol_factor)
-        o.floor_roundoff = float(self.floor_roundoff)
+        if self.floor_roundoff is not None:
+            o.floor_roundoff = float(self.floor_roundoff)
+        else:
+            o.floor_roundoff = ROUNDOFF_DOUBLE if self.precision == "double" else ROUNDOFF_SINGLE
         return o
 
 
@@ -594,7 +654,23 @@ def hybrid_restart_gmres(a: SparseMatrix, p: Preconditioner, b, config: GmresCon
         raise ValueError("gmres: rhs dimension mismatch")
     if config.restart_m < 1 or config.tol <= 0.0 or config.max_restarts < 1:
         raise ValueError("gmres: invalid config")
-    if p.matrix is not a:
+    if config.precision not in ("hybrid", "double"):
+        raise ValueError("gmres: unknown precision: " + str(config.precision))
+    if p.kind == Preconditioner.IDENTITY:
+        if p.dim() != a.n:
+            raise ValueError("gmres: preconditioner dimension mismatch")
+        if p.ctx is None or p.matrix is not a:  # bind the identity to this matrix
+            p.ctx = Context(0)
+            p.ctx.set_matrix(a)
+            p.ctx.identity_setup()
+            p.matrix = a
+    elif p.matrix is not a:
         raise ValueError("gmres: the preconditioner must be built from this matrix (device-resident)")
+    if p.kind == Preconditioner.ILU0 and config.precision == "hybrid":
+        # the reference applies ILU(0) through lu_solve<float> on factors that
+        # never get binary32 copies (lu.hpp:94-99): Hybrid + ILU(0) throws there
+        raise LogicError("values_low requested before materialize_low()")
+    if p.kind == Preconditioner.BLOCK_JACOBI and config.precision == "double":
+        raise ValueError("gmres: DoubleOnly block Jacobi is not implemented on the GPU path (FP32 factors)")
     x, rep = p.ctx.gmres(b, config)
     return SolveResult(x, rep)

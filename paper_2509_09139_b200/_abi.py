@@ -20,6 +20,7 @@ HPBJ_ENOMEM = 5
 HPBJ_ERANGE = 6
 HPBJ_ENODEV = 7
 HPBJ_EIO = 8
+HPBJ_ERUNTIME = 9
 
 HPBJ_K_APPLY = 0
 HPBJ_K_SPMV = 1
@@ -117,6 +118,10 @@ SIGNATURES = {
     "hpbj_bj_refactor": (ctypes.c_int, [vp, ctypes.POINTER(SetupInfo)]),
     "hpbj_bj_apply": (ctypes.c_int, [vp, f64p, f64p]),
     "hpbj_bj_set_neumann_order": (ctypes.c_int, [vp, ctypes.c_int]),
+    "hpbj_ilu0_setup": (ctypes.c_int, [vp, ctypes.c_void_p]),
+    "hpbj_identity_setup": (ctypes.c_int, [vp]),
+    "hpbj_precond_apply": (ctypes.c_int, [vp, f64p, f64p]),
+    "hpbj_get_ilu0_values": (ctypes.c_int, [vp, f64p]),
     "hpbj_bj_apply_neumann": (ctypes.c_int, [vp, f64p, f64p, ctypes.c_int]),
     "hpbj_get_block_factors": (ctypes.c_int, [vp, i64, i64p, f32p, i64p]),
     "hpbj_get_block_stats": (ctypes.c_int, [vp, i64p, i64p]),

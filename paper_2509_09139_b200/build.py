@@ -25,7 +25,7 @@ NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xc
               "-Xptxas", "-v", "-I" + INC, "-I" + CSRC] + ARCH
 CXX_FLAGS = ["-std=c++20", "-O3", "-fPIC", "-fopenmp", "-ffp-contract=off", "-I" + INC, "-I" + CSRC]
 
-CU_SOURCES = ["permute.cu", "block_lu.cu", "spk.cu", "spmv.cu", "arnoldi.cu", "fused.cu", "diag.cu", "capi.cu"]
+CU_SOURCES = ["permute.cu", "block_lu.cu", "spk.cu", "spmv.cu", "arnoldi.cu", "fused.cu", "diag.cu", "ilu.cu", "capi.cu"]
 CPP_SOURCES = ["host/partition.cpp", "host/mmio.cpp"]
 HEADERS = ["device.cuh", "kernels.cuh", "hpbj_common.hpp", "spk_dev.cuh", "sync_dev.cuh"]
 

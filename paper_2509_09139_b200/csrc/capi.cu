@@ -155,6 +155,8 @@ constexpr double kU24 = 5.9604644775390625e-08;  // 2^-24
 
 }  // namespace
 
+constexpr int kPcNone = 0, kPcBJ = 1, kPcIlu = 2, kPcIdentity = 3;
+
 struct hpbj_ctx {
     Pool pool;  // destroyed last
     Slots slots;
@@ -179,7 +181,20 @@ struct hpbj_ctx {
     double* d_tmpy = nullptr;  // n
 
     // block-Jacobi preconditioner (permuted frame)
-    bool has_pc = false;
+    bool has_pc = false;     // block-Jacobi factors present
+    int active = 0;          // preconditioner the solve uses: kPcNone / kPcBJ / kPcIlu / kPcIdentity
+    bool has_ilu = false;
+    IluParams ilu;           // ILU(0) factors in A's pattern (ilu.cu)
+    double* d_ilu_lu = nullptr;
+    int* d_ilu_dpos = nullptr;
+    int* d_ilu_flags = nullptr;
+    double2* d_ilu_ytag = nullptr;
+    double2* d_ilu_ztag = nullptr;
+    int* d_ilu_tick32 = nullptr;
+    unsigned long long* d_ilu_tick64 = nullptr;
+    unsigned long long* d_ilu_err = nullptr;
+    double* d_ilu_z = nullptr;  // preconditioned vector (FP64 preconditioners)
+    double* d_ilu_u = nullptr;  // basis combination of the x-update
     int s = 0;
     double eps = 1e-10;
     int dmin = 0, dmax = 0;
@@ -290,6 +305,18 @@ struct hpbj_ctx {
         dfree(d_eval);
         dfree(d_eidx);
         has_pc = false;
+        dfree(d_ilu_lu);
+        dfree(d_ilu_dpos);
+        dfree(d_ilu_flags);
+        dfree(d_ilu_ytag);
+        dfree(d_ilu_ztag);
+        dfree(d_ilu_tick32);
+        dfree(d_ilu_tick64);
+        dfree(d_ilu_err);
+        dfree(d_ilu_z);
+        dfree(d_ilu_u);
+        has_ilu = false;
+        active = kPcNone;
     }
     void release_matrix() {
         release_pc();
@@ -501,9 +528,30 @@ void factor(hpbj_ctx* c, hpbj_setup_info* info) {
             info->singular_column = col;
         }
         c->has_pc = false;
+        if (c->active == kPcBJ) c->active = kPcNone;
         fail(HPBJ_ESINGULAR, "gp_lu: singular block, zero pivot in column " + std::to_string(col) +
                                  " (block " + std::to_string(blk) + ")");
     }
+}
+
+// The solve's frame: Q A Q^T for block Jacobi (contiguous blocks), A itself
+// for the order-dependent ILU(0) and for the identity.
+const DevCsr& sys(const hpbj_ctx* c) { return c->active == kPcBJ ? c->B : c->A; }
+const SpmvPlan& sys_plan(const hpbj_ctx* c) { return c->active == kPcBJ ? c->planB : c->planA; }
+void to_frame(hpbj_ctx* c, const double* x, double* xf) {
+    if (c->active == kPcBJ) launch_permute_vec(c->A.n, c->d_perm, x, xf, false, c->stream, &c->launches);
+    else HPBJ_CUDA(cudaMemcpyAsync(xf, x, sizeof(double) * c->A.n, cudaMemcpyDeviceToDevice, c->stream));
+}
+void from_frame(hpbj_ctx* c, const double* xf, double* x) {
+    if (c->active == kPcBJ) launch_permute_vec(c->A.n, c->d_perm, xf, x, true, c->stream, &c->launches);
+    else HPBJ_CUDA(cudaMemcpyAsync(x, xf, sizeof(double) * c->A.n, cudaMemcpyDeviceToDevice, c->stream));
+}
+// kernels per Arnoldi step / per cycle of the unfused graph (launch accounting)
+int64_t step_launches(const hpbj_ctx* c) {
+    return 2 + (c->active == kPcBJ ? 1 + 2 * std::max(0, c->neumann) : c->active == kPcIlu ? 1 : 1);
+}
+int64_t cycle_launches(const hpbj_ctx* c) {
+    return 4 + (c->active == kPcBJ ? 1 + 2 * std::max(0, c->neumann) : c->active == kPcIlu ? 2 : 1);
 }
 
 void record_kernel(hpbj_ctx* c, size_t slot, bool begin) {
@@ -519,6 +567,21 @@ void enqueue_cycle_head(hpbj_ctx* c, cudaGraphConditionalHandle hin) {
 }
 void enqueue_step(hpbj_ctx* c, cudaGraphConditionalHandle hin, int it) {
     KrylovBufs& kb = c->kb;
+    if (c->active != kPcBJ) {  // FP64 preconditioners: z64 = M^-1 V[:, j], w = A z64
+        record_kernel(c, 3 * it + 0, true);
+        if (c->active == kPcIlu)
+            launch_ilu0_apply(c->ilu, nullptr, kb.V, kb.ldv, c->d_st, c->d_ilu_z, nullptr, c->stream, &c->launches);
+        else
+            launch_copy_column(kb, c->d_st, c->A.n, c->d_ilu_z, c->stream, &c->launches);
+        record_kernel(c, 3 * it + 0, false);
+        record_kernel(c, 3 * it + 1, true);
+        launch_spmv_f64x(c->A, c->planA, c->d_ilu_z, kb.w, c->stream, &c->launches, c->d_st);
+        record_kernel(c, 3 * it + 1, false);
+        record_kernel(c, 3 * it + 2, true);
+        launch_mgs(c->mgs, kb, c->d_gram, c->d_gb, c->d_st, c->A.n, hin, c->stream, &c->launches);
+        record_kernel(c, 3 * it + 2, false);
+        return;
+    }
     record_kernel(c, 3 * it + 0, true);
     if (c->neumann > 0) {
         // z = sum_{i<=k} (I - M^-1 A)^i M^-1 v_j in FP32 (preconditioned<float>, gmres.cpp:91-95);
@@ -549,7 +612,12 @@ void enqueue_cycle_fused(hpbj_ctx* c) {
 void enqueue_cycle_tail(hpbj_ctx* c, cudaGraphConditionalHandle hout) {
     KrylovBufs& kb = c->kb;
     launch_solve_y(kb, c->d_st, c->stream, &c->launches);
-    if (c->neumann > 0) {  // preconditioned<double> (gmres.cpp:158): FP64 series, x += sum
+    if (c->active == kPcIlu) {  // x += M^-1 (V y), FP64 (gmres.cpp:150-159)
+        launch_basis_combine(kb, c->d_st, c->A.n, c->d_ilu_u, nullptr, c->stream, &c->launches);
+        launch_ilu0_apply(c->ilu, c->d_ilu_u, nullptr, 0, c->d_st, nullptr, c->d_xp, c->stream, &c->launches);
+    } else if (c->active == kPcIdentity) {
+        launch_basis_combine(kb, c->d_st, c->A.n, nullptr, c->d_xp, c->stream, &c->launches);
+    } else if (c->neumann > 0) {  // preconditioned<double> (gmres.cpp:158): FP64 series, x += sum
         launch_apply_neumann_f64(spk_view(c), nullptr, kb.V, kb.ldv, kb.y, c->d_nterm64, c->d_nacc64, nullptr, 1,
                                  c->d_st, c->stream, &c->launches);
         for (int i = 1; i <= c->neumann; ++i) {
@@ -560,20 +628,21 @@ void enqueue_cycle_tail(hpbj_ctx* c, cudaGraphConditionalHandle hout) {
     } else {
         launch_apply_update(spk_view(c), kb.V, kb.ldv, kb.y, c->d_st, c->d_xp, c->stream, &c->launches);
     }
-    launch_residual(c->B, c->planB, c->d_xp, c->d_bp, c->d_r, c->d_st, c->d_red, c->stream, &c->launches);
+    launch_residual(sys(c), sys_plan(c), c->d_xp, c->d_bp, c->d_r, c->d_st, c->d_red, c->stream, &c->launches);
     launch_cycle_end(kb, c->d_st, hout, c->stream, &c->launches);
 }
 
 std::vector<uintptr_t> graph_signature(const hpbj_ctx* c) {
     const KrylovBufs& k = c->kb;
-    const SpmvPlan& p = c->planB;
+    const SpmvPlan& p = sys_plan(c);
+    const DevCsr& M = sys(c);
     const MgsLaunch& L = c->mgs;
     return {(uintptr_t)k.V, (uintptr_t)k.w, (uintptr_t)k.H, (uintptr_t)k.R, (uintptr_t)k.cs, (uintptr_t)k.sn,
             (uintptr_t)k.g, (uintptr_t)k.y, (uintptr_t)k.est, (uintptr_t)k.partials, (uintptr_t)k.hist,
             (uintptr_t)k.hist_cycle, (uintptr_t)k.cycres, (uintptr_t)k.m, (uintptr_t)k.ldv,
             (uintptr_t)c->d_st, (uintptr_t)c->d_z32, (uintptr_t)c->d_xp, (uintptr_t)c->d_bp, (uintptr_t)c->d_r,
-            (uintptr_t)c->d_red, (uintptr_t)c->d_gram, (uintptr_t)c->d_gb, (uintptr_t)c->B.rp, (uintptr_t)c->B.ci,
-            (uintptr_t)c->B.val, (uintptr_t)c->B.n, (uintptr_t)c->B.nnz, (uintptr_t)p.group,
+            (uintptr_t)c->d_red, (uintptr_t)c->d_gram, (uintptr_t)c->d_gb, (uintptr_t)M.rp, (uintptr_t)M.ci,
+            (uintptr_t)M.val, (uintptr_t)M.n, (uintptr_t)M.nnz, (uintptr_t)p.group,
             (uintptr_t)p.long_thresh, (uintptr_t)p.n_long, (uintptr_t)p.long_rows,
             (uintptr_t)c->s, (uintptr_t)c->d_bstart, (uintptr_t)c->d_fac_off, (uintptr_t)c->d_fac,
             (uintptr_t)c->d_piv, (uintptr_t)c->dmax, (uintptr_t)c->d_pstart, (uintptr_t)c->d_desc,
@@ -581,7 +650,12 @@ std::vector<uintptr_t> graph_signature(const hpbj_ctx* c) {
             (uintptr_t)L.smem, (uintptr_t)L.icwy, (uintptr_t)L.w_in_smem, (uintptr_t)c->fused.ok,
             (uintptr_t)c->fused.grid, (uintptr_t)c->fused.slice, (uintptr_t)c->fused.ystride,
             (uintptr_t)c->fused.smem, (uintptr_t)c->fused.nnz_cap, (uintptr_t)c->d_ent_off,
-            (uintptr_t)c->neumann, (uintptr_t)c->d_nterm32, (uintptr_t)c->d_nterm64, (uintptr_t)c->d_nacc64};
+            (uintptr_t)c->neumann, (uintptr_t)c->d_nterm32, (uintptr_t)c->d_nterm64, (uintptr_t)c->d_nacc64,
+            (uintptr_t)c->active, (uintptr_t)c->d_ilu_lu, (uintptr_t)c->d_ilu_dpos, (uintptr_t)c->d_ilu_flags,
+            (uintptr_t)c->d_ilu_ytag, (uintptr_t)c->d_ilu_ztag,
+            (uintptr_t)c->d_ilu_tick64, (uintptr_t)c->d_ilu_z, (uintptr_t)c->d_ilu_u,
+            (uintptr_t)c->ilu.apply_grid, (uintptr_t)c->ilu.seq, (uintptr_t)c->A.rp, (uintptr_t)c->A.ci, (uintptr_t)c->A.val,
+            (uintptr_t)c->planA.group, (uintptr_t)c->planA.n_long, (uintptr_t)c->planA.long_rows};
 }
 
 // The whole restart loop as one CUDA graph: WHILE(cycles) { cycle_init;
@@ -695,7 +769,8 @@ void solve(hpbj_ctx* c, const double* d_b, double* d_x, const hpbj_gmres_opts* o
     hpbj_gmres_default_opts(&opt);
     if (o) opt = *o;
     if (!c->has_matrix) fail(HPBJ_ELOGIC, "gmres: no matrix");
-    if (!c->has_pc) fail(HPBJ_ELOGIC, "gmres: block-Jacobi preconditioner not set up");
+    if (c->active == kPcNone || (c->active == kPcBJ && !c->has_pc) || (c->active == kPcIlu && !c->has_ilu))
+        fail(HPBJ_ELOGIC, "gmres: no preconditioner set up");
     if (opt.restart_m < 1 || opt.tol <= 0.0 || opt.max_restarts < 1)
         fail(HPBJ_EINVAL, "gmres: invalid config");
     if (opt.restart_m > 1024) fail(HPBJ_EINVAL, "gmres: restart_m > 1024 unsupported");
@@ -705,7 +780,7 @@ void solve(hpbj_ctx* c, const double* d_b, double* d_x, const hpbj_gmres_opts* o
     const double floor_u = opt.floor_roundoff > 0.0 ? opt.floor_roundoff : kU24;
     ensure_ws(c, m);
     {  // residual partials: one per SpMV CTA incl. one per hub row
-        const size_t need = 1184 + 64 + (size_t)c->planB.n_long;
+        const size_t need = 1184 + 64 + (size_t)sys_plan(c).n_long;
         if (need > c->red_cap) {
             dfree(c->d_red);
             dslot(c->d_red, need);
@@ -723,7 +798,7 @@ void solve(hpbj_ctx* c, const double* d_b, double* d_x, const hpbj_gmres_opts* o
     };
 
     // permuted b; ||b||
-    launch_permute_vec(n, c->d_perm, d_b, c->d_bp, false, st, &c->launches);
+    to_frame(c, d_b, c->d_bp);
     launch_norm(c->d_bp, n, c->d_st, c->d_red, st, &c->launches);
     SolveState hs{};
     HPBJ_CUDA(cudaMemcpyAsync(&hs, c->d_st, sizeof(hs), cudaMemcpyDeviceToHost, st));
@@ -753,7 +828,7 @@ void solve(hpbj_ctx* c, const double* d_b, double* d_x, const hpbj_gmres_opts* o
     HPBJ_CUDA(cudaMemcpyAsync(c->d_st, &hs, sizeof(hs), cudaMemcpyHostToDevice, st));
 
     // r = b - A*0, ||r|| (gmres.cpp:223-230)
-    launch_residual(c->B, c->planB, c->d_xp, c->d_bp, c->d_r, c->d_st, c->d_red, st, &c->launches);
+    launch_residual(sys(c), sys_plan(c), c->d_xp, c->d_bp, c->d_r, c->d_st, c->d_red, st, &c->launches);
     HPBJ_CUDA(cudaMemcpyAsync(&hs, c->d_st, sizeof(hs), cudaMemcpyDeviceToHost, st));
     HPBJ_CUDA(cudaStreamSynchronize(st));
     double rnorm = hs.rnorm;
@@ -763,7 +838,7 @@ void solve(hpbj_ctx* c, const double* d_b, double* d_x, const hpbj_gmres_opts* o
         R.converged = 1;
     } else {
         const bool use_graph = !c->profiling && c->use_graph;
-        c->fused = c->use_fused && c->neumann == 0 ? plan_fused(n, c->s, c->dmax, c->num_sms, m, c->planB.n_long > 0,
+        c->fused = c->use_fused && c->active == kPcBJ && c->neumann <= 0 ? plan_fused(n, c->s, c->dmax, c->num_sms, m, c->planB.n_long > 0,
                                              c->h_rowlen_perm.data())
                                 : FusedPlan{};
         if (c->fused.ok && getenv("HPBJ_FUSED_PROF") && !c->d_fprof) {
@@ -826,8 +901,8 @@ void solve(hpbj_ctx* c, const double* d_b, double* d_x, const hpbj_gmres_opts* o
         HPBJ_CUDA(cudaStreamSynchronize(st));
         if (use_graph && c->fused.ok)  // per cycle: init, arnoldi_cycle, solve_y, update, residual, end
             c->launches += (int64_t)hs.cycles * 6;
-        else if (use_graph)  // per step: apply, spmv, orth; per cycle: init, solve_y, update, residual, end
-            c->launches += (int64_t)hs.total_iterations * 3 + (int64_t)hs.cycles * 5;
+        else if (use_graph)  // per step: apply(s), spmv(s), orth; per cycle: init, solve_y, update, residual, end
+            c->launches += (int64_t)hs.total_iterations * step_launches(c) + (int64_t)hs.cycles * cycle_launches(c);
         std::vector<double> hv(hs.hist_len), cr(hs.cycles);
         std::vector<int> hc(hs.hist_len);
         if (hs.hist_len) {
@@ -857,7 +932,7 @@ void solve(hpbj_ctx* c, const double* d_b, double* d_x, const hpbj_gmres_opts* o
         R.restarts = hs.cycles > 0 ? hs.cycles - 1 : 0;
         R.final_residual = hs.rnorm / bnorm;
     }
-    launch_permute_vec(n, c->d_perm, c->d_xp, d_x, true, st, &c->launches);
+    from_frame(c, c->d_xp, d_x);
     HPBJ_CUDA(cudaStreamSynchronize(st));
     R.history_len = hlen;
     R.cycles = clen;
@@ -1147,6 +1222,7 @@ int hpbj_bj_setup(hpbj_ctx* ctx, int64_t s, const int64_t* perm, const int64_t* 
         cudaEventDestroy(e1);
         dput(tmp);
         ctx->has_pc = true;
+        ctx->active = kPcBJ;
         const auto T4 = tnow();
         factor(ctx, info);
         if (info) info->ms_permute = ms;
@@ -1167,6 +1243,7 @@ int hpbj_bj_refactor(hpbj_ctx* ctx, hpbj_setup_info* info) {
     return guard(&ctx->err, [&] {
         if (!ctx->d_fac) fail(HPBJ_ELOGIC, "refactor: no block-Jacobi partition set up");
         ctx->has_pc = true;
+        ctx->active = kPcBJ;
         factor(ctx, info);
     });
 }
@@ -1185,6 +1262,111 @@ int hpbj_bj_apply(hpbj_ctx* ctx, const double* v, double* z) {
         launch_permute_vec(n, ctx->d_perm, ctx->d_tmpx, ctx->d_tmpy, true, st, &ctx->launches);
         HPBJ_CUDA(cudaMemcpyAsync(z, ctx->d_tmpy, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
         HPBJ_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+int hpbj_ilu0_setup(hpbj_ctx* ctx, hpbj_setup_info* info) {
+    if (!ctx) return HPBJ_EINVAL;
+    if (info) {
+        std::memset(info, 0, sizeof(*info));
+        info->singular_block = info->singular_column = -1;
+    }
+    t_pool = &ctx->pool;
+    t_slots = &ctx->slots;
+    return guard(&ctx->err, [&] {
+        if (!ctx->has_matrix) fail(HPBJ_ELOGIC, "ilu0: no matrix");
+        const int n = ctx->A.n;
+        const int64_t nnz = ctx->A.nnz;
+        cudaStream_t st = ctx->stream;
+        if (ctx->active == kPcIlu) ctx->active = kPcNone;
+        ctx->has_ilu = false;
+        dslot(ctx->d_ilu_lu, nnz);
+        dslot(ctx->d_ilu_dpos, n);
+        dslot(ctx->d_ilu_flags, n);
+        dslot(ctx->d_ilu_ytag, n);
+        dslot(ctx->d_ilu_ztag, n);
+        dslot(ctx->d_ilu_tick32, 4);
+        dslot(ctx->d_ilu_tick64, 1);
+        dslot(ctx->d_ilu_err, 1);
+        const size_t ldv = ((size_t)n + 31) / 32 * 32;
+        dslot(ctx->d_ilu_z, ldv);
+        dslot(ctx->d_ilu_u, ldv);
+        const auto t0 = std::chrono::steady_clock::now();
+        const int bad = launch_ilu0_diag(n, ctx->A.rp, ctx->A.ci, ctx->d_ilu_dpos, ctx->d_ilu_tick32, st,
+                                         &ctx->launches);
+        if (bad >= 0) {
+            if (info) info->singular_column = bad;
+            fail(HPBJ_EINVAL, "ilu0: structurally zero diagonal in row " + std::to_string(bad));
+        }
+        IluParams& p = ctx->ilu;
+        p.n = n;
+        p.rp = ctx->A.rp;
+        p.ci = ctx->A.ci;
+        p.dpos = ctx->d_ilu_dpos;
+        p.lu = ctx->d_ilu_lu;
+        p.nch = ilu0_chunks(n);
+        p.flags = ctx->d_ilu_flags;
+        p.ytag = ctx->d_ilu_ytag;
+        p.ztag = ctx->d_ilu_ztag;
+        p.ticket32 = ctx->d_ilu_tick32;
+        p.ticket64 = ctx->d_ilu_tick64;
+        p.apply_grid = ilu0_apply_grid(n, ctx->num_sms);
+        const unsigned long long none = ~0ull;
+        HPBJ_CUDA(cudaMemcpyAsync(ctx->d_ilu_err, &none, sizeof(none), cudaMemcpyHostToDevice, st));
+        HPBJ_CUDA(cudaMemcpyAsync(ctx->d_ilu_lu, ctx->A.val, sizeof(double) * nnz, cudaMemcpyDeviceToDevice, st));
+        launch_ilu0_factor(p, ctx->d_ilu_err, ctx->num_sms, st, &ctx->launches);
+        unsigned long long err = none;
+        HPBJ_CUDA(cudaMemcpyAsync(&err, ctx->d_ilu_err, sizeof(err), cudaMemcpyDeviceToHost, st));
+        HPBJ_CUDA(cudaStreamSynchronize(st));
+        int zero_row = err != none ? (int)(err & 0xffffffffu) : launch_ilu0_zero_diag(p, ctx->d_ilu_tick32, st,
+                                                                                      &ctx->launches);
+        if (info) info->ms_factor = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        if (zero_row >= 0) {
+            if (info) info->singular_column = zero_row;
+            fail(HPBJ_ERUNTIME, "ilu0: zero diagonal pivot in row " + std::to_string(zero_row));
+        }
+        ilu0_choose_apply(p, ctx->d_tmpx, ctx->d_tmpy, st, &ctx->launches);
+        ctx->has_ilu = true;
+        ctx->active = kPcIlu;
+    });
+}
+
+int hpbj_identity_setup(hpbj_ctx* ctx) {
+    if (!ctx) return HPBJ_EINVAL;
+    t_pool = &ctx->pool;
+    t_slots = &ctx->slots;
+    return guard(&ctx->err, [&] {
+        if (!ctx->has_matrix) fail(HPBJ_ELOGIC, "identity: no matrix");
+        dslot(ctx->d_ilu_z, ((size_t)ctx->A.n + 31) / 32 * 32);
+        ctx->active = kPcIdentity;
+    });
+}
+
+int hpbj_precond_apply(hpbj_ctx* ctx, const double* v, double* z) {
+    if (!ctx) return HPBJ_EINVAL;
+    if (ctx->active == kPcBJ) return hpbj_bj_apply(ctx, v, z);
+    t_pool = &ctx->pool;
+    t_slots = &ctx->slots;
+    return guard(&ctx->err, [&] {
+        if (ctx->active == kPcNone) fail(HPBJ_ELOGIC, "apply: no preconditioner set up");
+        const int n = ctx->A.n;
+        cudaStream_t st = ctx->stream;
+        if (ctx->active == kPcIdentity) {
+            std::memcpy(z, v, sizeof(double) * n);
+            return;
+        }
+        HPBJ_CUDA(cudaMemcpyAsync(ctx->d_tmpx, v, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+        launch_ilu0_apply(ctx->ilu, ctx->d_tmpx, nullptr, 0, nullptr, ctx->d_tmpy, nullptr, st, &ctx->launches);
+        HPBJ_CUDA(cudaMemcpyAsync(z, ctx->d_tmpy, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+        HPBJ_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+int hpbj_get_ilu0_values(hpbj_ctx* ctx, double* lu) {
+    if (!ctx) return HPBJ_EINVAL;
+    return guard(&ctx->err, [&] {
+        if (!ctx->has_ilu) fail(HPBJ_ELOGIC, "ilu0: factors not set up");
+        HPBJ_CUDA(cudaMemcpy(lu, ctx->d_ilu_lu, sizeof(double) * ctx->A.nnz, cudaMemcpyDeviceToHost));
     });
 }
 

@@ -139,6 +139,50 @@ void launch_apply_neumann_f64(const SpkView& v, const double* vin, const double*
                               double* term, double* acc, double* xadd, int init, const SolveState* sst,
                               cudaStream_t st, int64_t* launches);
 
+// ---- ilu.cu ---------------------------------------------------------------
+struct KrylovBufs;
+// ILU(0) factors in place in A's pattern (original ordering), sync-free
+// ticketed passes; flags: factored rows, ytag/ztag: epoch-tagged apply
+// results, ticket64 monotone across applies, apply_grid fixed per
+// factorisation.
+struct IluParams {
+    int n = 0;
+    const int* rp = nullptr;
+    const int* ci = nullptr;
+    const int* dpos = nullptr;
+    double* lu = nullptr;
+    int nch = 0;               // 32-row chunks of the applies
+    int* flags = nullptr;      // n: factored-row flags (factorisation)
+    double2* ytag = nullptr;   // n: forward results (value, epoch)
+    double2* ztag = nullptr;   // n: backward results (value, epoch)
+    int* ticket32 = nullptr;
+    unsigned long long* ticket64 = nullptr;
+    int apply_grid = 1;
+    int seq = 0;               // apply with the one-warp sweep (deep dependency graphs)
+};
+// first row without a structural diagonal, or -1
+int launch_ilu0_diag(int n, const int* rp, const int* ci, int* dpos, int* scratch, cudaStream_t st,
+                     int64_t* launches);
+// err: min (i << 32 | k) over zero pivots met (~0 when none)
+void launch_ilu0_factor(const IluParams& p, unsigned long long* err, int num_sms, cudaStream_t st,
+                        int64_t* launches);
+// first row with a zero factored diagonal, or -1
+int launch_ilu0_zero_diag(const IluParams& p, int* scratch, cudaStream_t st, int64_t* launches);
+int ilu0_apply_grid(int n, int num_sms);
+// times the ticketed and the one-warp apply once each and sets p.seq (clobbers vin/z scratch)
+void ilu0_choose_apply(IluParams& p, double* vin, double* z, cudaStream_t st, int64_t* launches);
+int ilu0_chunks(int n);
+// z = U^-1 L^-1 src; src = V[:, st->j] (V != null, skipped when st->done) or vin;
+// z (optional) plain copy of the result, xadd (optional): x += z
+void launch_ilu0_apply(const IluParams& p, const double* vin, const double* V, int ldv, const SolveState* sst,
+                       double* z, double* xadd, cudaStream_t st, int64_t* launches);
+// u = sum_{i < st->j} y_i V_i, or x += that sum when xadd != null
+void launch_basis_combine(const KrylovBufs& kb, const SolveState* sst, int n, double* u, double* xadd,
+                          cudaStream_t st, int64_t* launches);
+// z = V[:, st->j] (skipped when st->done)
+void launch_copy_column(const KrylovBufs& kb, const SolveState* sst, int n, double* z, cudaStream_t st,
+                        int64_t* launches);
+
 // ---- spmv.cu --------------------------------------------------------------
 struct SpmvPlan {
     int group = 8;            // lanes per row
@@ -151,7 +195,7 @@ struct SpmvPlan {
 void launch_spmv_f32x(const DevCsr& a, const SpmvPlan& plan, const float* x, double* y,
                       const SolveState* sst, cudaStream_t st, int64_t* launches);
 void launch_spmv_f64x(const DevCsr& a, const SpmvPlan& plan, const double* x, double* y,
-                      cudaStream_t st, int64_t* launches);
+                      cudaStream_t st, int64_t* launches, const SolveState* sst = nullptr);
 // r = b - A x and st->rnorm = ||r||_2 (deterministic grid reduction).
 void launch_residual(const DevCsr& a, const SpmvPlan& plan, const double* x, const double* b, double* r,
                      SolveState* sst, double* partials, cudaStream_t st, int64_t* launches);

@@ -186,8 +186,8 @@ void launch_spmv_f32x(const DevCsr& a, const SpmvPlan& plan, const float* x, dou
 }
 
 void launch_spmv_f64x(const DevCsr& a, const SpmvPlan& plan, const double* x, double* y, cudaStream_t st,
-                      int64_t* launches) {
-    run<double, 0>(a, plan, x, y, nullptr, nullptr, nullptr, st, launches);
+                      int64_t* launches, const SolveState* sst) {
+    run<double, 0>(a, plan, x, y, nullptr, const_cast<SolveState*>(sst), nullptr, st, launches);
 }
 
 void launch_residual(const DevCsr& a, const SpmvPlan& plan, const double* x, const double* b, double* r,

@@ -139,3 +139,33 @@ def test_solve_with_neumann_order(ref, mtx, tmp_path):
     out = ref.solve(a.row_starts, a.col_indices, a.values, 6, np.ones(a.n), 20, 1e-10, 40, hybrid=True,
                     assignment=part.assignment, neumann_order=2)
     assert doc["result"]["iterations"] == out.total_iterations
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("precond", ["ilu0", "none"])
+def test_solve_with_other_preconditioners(ref, mtx, tmp_path, precond):
+    """--precond ilu0 / none default to precision double like the reference
+    and reproduce its iteration counts; hybrid ILU(0) fails like the reference."""
+    path, a = mtx
+    rep = str(tmp_path / "r.json")
+    r = run("solve", "--matrix", path, "--precond", precond, "--restart", "20", "--tol", "1e-10", "--rhs", "ones",
+            "--report", rep)
+    assert r.returncode == 0, r.stderr
+    doc = json.load(open(rep))
+    assert doc["config"]["precond"] == precond and doc["config"]["precision"] == "double"
+    assert doc["preconditioner"]["blocks"] == [] and doc["result"]["converged"]
+    b = np.ones(a.n)
+    if precond == "ilu0":
+        out = ref.solve_ilu0(a.row_starts, a.col_indices, a.values, b, 20, 1e-10, 40, hybrid=False)
+    else:
+        out = ref.solve_identity(a.row_starts, a.col_indices, a.values, b, 20, 1e-10, 40, hybrid=False)
+    assert abs(doc["result"]["iterations"] - out.total_iterations) <= 1
+    if precond == "ilu0":
+        r = run("solve", "--matrix", path, "--precond", "ilu0", "--precision", "hybrid")
+        assert r.returncode == 1 and "values_low requested before materialize_low" in r.stderr
+
+
+def test_unknown_preconditioner_is_reported(mtx):
+    path, _ = mtx
+    r = run("solve", "--matrix", path, "--precond", "amg")
+    assert r.returncode == 1 and "unknown preconditioner: amg" in r.stderr

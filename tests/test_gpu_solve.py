@@ -225,11 +225,16 @@ def test_solve_independent_of_stale_device_memory(monkeypatch):
         p.ctx.set_fused(fused)
         return hp.hybrid_restart_gmres(a, p, b, cfg), p.apply(b), p.stats()
 
+    def run_ilu():
+        p = hp.Preconditioner.from_ilu0(a)
+        out = hp.hybrid_restart_gmres(a, p, b, hp.GmresConfig(restart_m=30, tol=1e-10, precision="double"))
+        return out, p.apply(b), p.ilu0_values().tolist()
+
     cases = [(True, 0), (False, 0), (False, 2)]
-    clean = [run(f, o) for f, o in cases]
+    clean = [run(f, o) for f, o in cases] + [run_ilu()]
     monkeypatch.setenv("HPBJ_POISON", "1")
-    for (f, o), (c_out, c_z, c_st) in zip(cases, clean):
-        out, z, st = run(f, o)
+    poisoned = [run(f, o) for f, o in cases] + [run_ilu()]
+    for (c_out, c_z, c_st), (out, z, st) in zip(clean, poisoned):
         assert out.report.total_iterations == c_out.report.total_iterations
         assert np.array_equal(out.x, c_out.x)
         assert np.array_equal(z, c_z)

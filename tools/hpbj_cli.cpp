@@ -6,7 +6,7 @@
 // include/bjgmres_b200.hpp).
 //
 //   hpbj_cli solve --matrix A.mtx [--rhs ones|axones|random:SEED|file:PATH]
-//            [--precond block-jacobi] [--blocks S] [--restart M] [--tol T]
+//            [--precond block-jacobi|ilu0|none] [--blocks S] [--restart M] [--tol T]
 //            [--max-restarts R] [--precision hybrid] [--eps-pivot E] [--neumann-order K]
 //            [--partition-file P] [--absolute-tol] [--report R.json]
 //            [--history H.csv]
@@ -14,9 +14,10 @@
 //   hpbj_cli partition --matrix A.mtx --blocks S --out P.txt
 //
 // Differences from the reference harness: the device path
-// implements the north star's precision mix only, so --precision defaults to
-// "hybrid" and "double" is rejected; --precond accepts block-jacobi only;
-// --ritz is rejected.
+// runs block Jacobi in the north star's precision mix only, so --precision
+// defaults to "hybrid" for it and "double" is rejected there (ILU(0) and none
+// default to "double", like the reference, and run in FP64); --ritz is
+// rejected.
 // Exit codes: 0 converged, 2 not converged (solve), 1 error.
 #include <algorithm>
 #include <chrono>
@@ -210,7 +211,7 @@ struct RunSpec {  // bjgmres_cli.cpp:29-45, with this build's precision default
     index_t restart_m = 50;
     double tol = 1e-8;
     index_t max_restarts = 40;
-    std::string precision = "hybrid";
+    std::string precision;  // "" = this build's default: hybrid for block-jacobi, double otherwise
     double eps_pivot = 1e-10;
     int neumann_order = 0;
     std::string partition_file;
@@ -347,6 +348,25 @@ RunResult run_spec(const RunSpec& spec) {  // bjgmres_cli.cpp:112-168
     out.n = a.rows();
     out.nnz = a.nnz();
     const auto t_setup = std::chrono::steady_clock::now();
+    GmresConfig cfg;
+    cfg.restart_m = spec.restart_m;
+    cfg.tol = spec.tol;
+    cfg.max_restarts = spec.max_restarts;
+    cfg.absolute_tol = spec.absolute_tol;
+    cfg.policy.mode = spec.precision == "hybrid" ? PrecisionMode::Hybrid : PrecisionMode::DoubleOnly;
+    if (spec.precond != "block-jacobi") {  // bjgmres_cli.cpp:128-131, 152-154
+        Preconditioner p = Preconditioner::identity(a.rows());
+        if (spec.precond == "ilu0") p = Preconditioner::from_ilu0(a);
+        else if (spec.precond != "none") throw std::runtime_error("unknown preconditioner: " + spec.precond);
+        out.setup_ms = ms_since(t_setup);
+        const std::vector<double> b = make_rhs(spec, a);
+        const auto t_solve = std::chrono::steady_clock::now();
+        SolveResult sr = hybrid_restart_gmres(a, p, b, cfg);
+        out.solve_ms = ms_since(t_solve);
+        out.report = std::move(sr.report);
+        out.x = std::move(sr.x);
+        return out;
+    }
     Partition part;
     if (!spec.partition_file.empty()) part = import_partition_file(spec.partition_file, a.rows(), spec.blocks);
     else part = partition_graph(a, spec.blocks, 0.1);
@@ -367,11 +387,6 @@ RunResult run_spec(const RunSpec& spec) {  // bjgmres_cli.cpp:112-168
     }
     out.block_nnz = bnnz;
     const std::vector<double> b = make_rhs(spec, a);
-    GmresConfig cfg;
-    cfg.restart_m = spec.restart_m;
-    cfg.tol = spec.tol;
-    cfg.max_restarts = spec.max_restarts;
-    cfg.absolute_tol = spec.absolute_tol;
     const auto t_solve = std::chrono::steady_clock::now();
     SolveResult sr = hybrid_restart_gmres(a, p, b, cfg);
     out.solve_ms = ms_since(t_solve);
@@ -435,17 +450,17 @@ double median(std::vector<double> v) {
 
 // the option checks the reference applies (bjgmres_cli.cpp:414-433), plus
 // this build's restrictions
-std::string check_spec(const RunSpec& s, bool blocks_set, bool part_set, bool neu_set, bool eps_set) {
+std::string check_spec(RunSpec& s, bool blocks_set, bool part_set, bool neu_set, bool eps_set) {
     if (s.precond != "block-jacobi") {
         if (blocks_set) return "--blocks requires --precond block-jacobi";
         if (part_set) return "--partition-file requires --precond block-jacobi";
         if (neu_set) return "--neumann-order requires --precond block-jacobi";
         if (eps_set) return "--eps-pivot requires --precond block-jacobi";
-        return "unknown preconditioner for the GPU path: " + s.precond + " (block-jacobi only)";
     }
+    if (s.precision.empty()) s.precision = s.precond == "block-jacobi" ? "hybrid" : "double";
     if (s.precision != "double" && s.precision != "hybrid") return "unknown precision: " + s.precision;
-    if (s.precision == "double")
-        return "precision 'double' is not implemented on the GPU path (the hybrid FP32/FP64 mix is)";
+    if (s.precond == "block-jacobi" && s.precision == "double")
+        return "precision 'double' with block-jacobi is not implemented on the GPU path (FP32 block factors)";
     if (s.ritz) return "--ritz is not implemented on the GPU path";
     if (s.blocks < 1 || s.restart_m < 1 || s.max_restarts < 1 || s.tol <= 0.0) return "numeric flags out of range";
     return "";
@@ -506,7 +521,7 @@ int cmd_bench(const std::string& specs_path, int repetitions, const std::string&
     std::vector<Row> rows;
     for (const Json& j : specs.arr) {
         try {
-            const RunSpec spec = spec_from_json(j);
+            RunSpec spec = spec_from_json(j);
             const std::string bad = check_spec(spec, false, false, false, false);
             if (!bad.empty()) throw std::runtime_error(bad);
             std::vector<double> st, sv;
