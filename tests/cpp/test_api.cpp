@@ -105,6 +105,54 @@ int main() {
         }
         EXPECT(thrown);
     }
+    {  // test_preconditioners.cpp:238-249 ApplyNeumann FirstOrderSeriesExample
+        const SparseMatrix a(2, 2, {0, 2, 4}, {0, 1, 0, 1}, {2.0, 1.0, 1.0, 2.0});
+        BlockJacobiOptions opts;
+        opts.neumann_order = 1;
+        const Preconditioner p = Preconditioner::block_jacobi(a, partition_from_assignment({0, 1}, 2), opts);
+        const std::vector<double> z = p.apply_neumann(std::vector<double>{1.0, 0.0}, 1);
+        EXPECT(z[0] == 0.5 && z[1] == -0.25);
+        bool thrown = false;
+        try {
+            p.apply_neumann(std::vector<double>{1.0, 0.0}, 2);
+        } catch (const std::invalid_argument&) {
+            thrown = true;
+        }
+        EXPECT(thrown);
+    }
+    {  // block diagnostics: cond >= 1 and the bound formula (preconditioner.cpp:13-15)
+        const SparseMatrix a = laplacian_2d(8, 8);
+        const Preconditioner p = Preconditioner::block_jacobi(a, partition_graph(a, 4, 0.1));
+        for (const auto& st : p.stats()) {
+            EXPECT(st.cond_estimate >= 1.0);
+            EXPECT(std::abs(st.error_bound - (st.cond_estimate * 0x1p-53 + 0x1p-24) * st.cond_estimate) <=
+                   1e-12 * st.error_bound);
+        }
+    }
+    {  // ILU(0) and identity behind the same solve (DoubleOnly), Hybrid ILU(0) throws like the reference
+        const SparseMatrix a = laplacian_2d(16, 16);
+        const std::vector<double> b = matvec(a, std::vector<double>(a.rows(), 1.0));
+        GmresConfig cfg;
+        cfg.restart_m = 30;
+        cfg.tol = 1e-10;
+        cfg.policy.mode = PrecisionMode::DoubleOnly;
+        const Preconditioner ilu = Preconditioner::from_ilu0(a);
+        const SolveResult r = hybrid_restart_gmres(a, ilu, b, cfg);
+        EXPECT(r.report.converged && r.report.final_residual <= 1e-10);
+        const SolveResult r0 = hybrid_restart_gmres(a, Preconditioner::identity(a.rows()), b, cfg);
+        EXPECT(r0.report.converged && r0.report.total_iterations > r.report.total_iterations);
+        GmresConfig hyb = cfg;
+        hyb.policy.mode = PrecisionMode::Hybrid;
+        bool thrown = false;
+        try {
+            hybrid_restart_gmres(a, ilu, b, hyb);
+        } catch (const std::logic_error&) {
+            thrown = true;
+        }
+        EXPECT(thrown);
+        const std::vector<double> z = ilu.apply(b);
+        EXPECT(z.size() == b.size());
+    }
     std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
     return failures ? 1 : 0;
 }
