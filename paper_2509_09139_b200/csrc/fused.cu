@@ -222,7 +222,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_arnoldi_cycle(FusedArgs a) {
     if (blockIdx.x == 0)
         for (int i = tid; i <= m; i += kThreads) gs.g[i] = (i == 0) ? st->beta : 0.0;
 
-    const int gw = blockIdx.x * kWarps + wid;  // 0: the Givens warp
+    // warp slots run across the CTAs first (slot = wid * G + cta), so the
+    // apply's blocks — and their factor traffic — spread over every SM
+    // instead of filling the first CTAs' warps (per-SM bandwidth bound)
+    const int gw = wid * G + blockIdx.x;  // 0: the Givens warp (CTA 0, warp 0)
     const int naw = G * kWarps - 1;
     const double bdf = st->breakdown_factor;
     const double* asrc = V;  // v_0 (k_cycle_init)
