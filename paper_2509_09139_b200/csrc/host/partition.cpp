@@ -35,6 +35,7 @@
 #include <cmath>
 #include <cstring>
 #include <queue>
+#include <type_traits>
 #include <string>
 #include <utility>
 #include <vector>
@@ -259,62 +260,70 @@ struct GraphView {
     const int64_t* deg;
 };
 
-// One refinement sweep (partition.cpp:117-141) over block ids of type S;
-// writes the final assignment.
+// The reference's decision for node u (partition.cpp:117-141) against a given
+// state: -2 skipped (source block of size <= 1), -1 stays, else the target
+// block. conn (all zero on entry and on exit) and tch are the caller's.
 template <class Idx, class Off, class S>
-void refine_sweep(const GraphView<Idx, Off>& g, S* state, int64_t* sizes, int64_t cap, double* conn,
-                  int64_t* assignment) {
-    const int64_t n = g.n;
+inline int32_t refine_decide(const GraphView<Idx, Off>& g, const S* state, const int64_t* sizes, int64_t cap,
+                             double* conn, int32_t* tch, int64_t u) {
     const Off* st = g.st;
     const Idx* nb = g.idx;
     const double* w = g.w;
-    int32_t touched[4096];
-    std::vector<int32_t> touched_big;
+    const int32_t bu = state[u];
+    if (sizes[bu] <= 1) return -2;
+    // Interior fast path: with every neighbour in bu the reference touches
+    // only bu, which is never a candidate -> no move (no floating-point work).
+    {
+        Off k = st[u];
+        const Off ke = st[u + 1];
+        while (k < ke && state[nb[k]] == bu) ++k;
+        if (k == ke) return -1;
+    }
+    int nt = 0;
+    for (Off k = st[u]; k < st[u + 1]; ++k) {
+        const int32_t bv = state[nb[k]];
+        tch[nt] = bv;  // recorded while its conn is still 0.0 (partition.cpp:123-124)
+        nt += conn[bv] == 0.0;
+        conn[bv] += w[k];
+    }
+    int32_t best = -1;
+    for (int t = 0; t < nt; ++t) {
+        const int32_t bv = tch[t];
+        if (bv == bu || sizes[bv] + 1 > cap) continue;
+        if (best < 0 || conn[bv] > conn[best] || (conn[bv] == conn[best] && bv < best)) best = bv;
+    }
+    const int32_t dec = (best >= 0 && conn[best] > conn[bu]) ? best : -1;
+    for (int t = 0; t < nt; ++t) conn[tch[t]] = 0.0;
+    return dec;
+}
+
+// One refinement sweep (partition.cpp:117-141) in the reference's u order
+// over block ids of type S (moves applied immediately, as there). Returns
+// the number of moves.
+template <class Idx, class Off, class S>
+int64_t refine_sweep(const GraphView<Idx, Off>& g, S* state, int64_t* sizes, int64_t cap, double* conn) {
+    const int64_t n = g.n;
+    const Off* st = g.st;
+    const Idx* nb = g.idx;
+    int64_t maxdeg = 0;
+    for (int64_t u = 0; u < n; ++u) maxdeg = std::max<int64_t>(maxdeg, (int64_t)(st[u + 1] - st[u]));
+    std::vector<int32_t> tch(maxdeg + 1);
+    int64_t moves = 0;
     constexpr int64_t kRefAhead = 8;
     for (int64_t u = 0; u < n; ++u) {
         if (u + kRefAhead < n) {
             const int64_t f = u + kRefAhead;
             for (Off k = st[f]; k < st[f + 1] && k < st[f] + 16; ++k) __builtin_prefetch(&state[nb[k]], 0, 1);
         }
+        const int32_t d = refine_decide(g, state, sizes, cap, conn, tch.data(), u);
+        if (d < 0) continue;
         const int32_t bu = state[u];
-        if (sizes[bu] <= 1) continue;
-        // Interior fast path: with every neighbour in bu the reference
-        // touches only bu, which is never a candidate -> no move, no state
-        // change (identical outcome, no floating-point work).
-        {
-            Off k = st[u];
-            const Off ke = st[u + 1];
-            while (k < ke && state[nb[k]] == bu) ++k;
-            if (k == ke) continue;
-        }
-        const int64_t du = st[u + 1] - st[u];
-        int32_t* tch = touched;
-        if (du > 4096) {
-            touched_big.resize(du);
-            tch = touched_big.data();
-        }
-        int nt = 0;
-        for (Off k = st[u]; k < st[u + 1]; ++k) {
-            const int32_t bv = state[nb[k]];
-            tch[nt] = bv;  // recorded while its conn is still 0.0 (partition.cpp:123-124)
-            nt += conn[bv] == 0.0;
-            conn[bv] += w[k];
-        }
-        int32_t best = -1;
-        for (int t = 0; t < nt; ++t) {
-            const int32_t bv = tch[t];
-            if (bv == bu || sizes[bv] + 1 > cap) continue;
-            if (best < 0 || conn[bv] > conn[best] || (conn[bv] == conn[best] && bv < best)) best = bv;
-        }
-        if (best >= 0 && conn[best] > conn[bu]) {
-            state[u] = (S)best;
-            --sizes[bu];
-            ++sizes[best];
-        }
-        for (int t = 0; t < nt; ++t) conn[tch[t]] = 0.0;
+        state[u] = (S)d;
+        --sizes[bu];
+        ++sizes[d];
+        ++moves;
     }
-#pragma omp parallel for schedule(static) if (n > 65536)
-    for (int64_t v = 0; v < n; ++v) assignment[v] = state[v];
+    return moves;
 }
 
 template <class Idx, class Off>
@@ -334,15 +343,8 @@ void partition_view(const GraphView<Idx, Off>& g, int64_t s, double tol, int64_t
     PartWork& W = t_work;
     const Off* st = g.st;
     const Idx* nb = g.idx;
-    const double* w = g.w;
     const int64_t* deg = g.deg;
 
-    // per-node state: >= 0 block id, -1 unassigned, -2 unassigned and queued
-    constexpr int32_t kFree = -1, kQueued = -2;
-    fit(W.state, n);
-    int32_t* state = W.state.data();
-#pragma omp parallel for schedule(static) if (n > 65536)
-    for (int64_t v = 0; v < n; ++v) state[v] = kFree;
     fit(W.sizes, s);
     int64_t* sizes = W.sizes.data();
     std::fill(sizes, sizes + s, int64_t(0));
@@ -368,12 +370,18 @@ void partition_view(const GraphView<Idx, Off>& g, int64_t s, double tol, int64_t
         for (int t = 0; t < T; ++t)
             for (int64_t v = t * chunk; v < std::min(n, (t + 1) * chunk); ++v)
                 if (deg[v] > 0) ++cnt[(size_t)t * K + (maxdeg - deg[v])];
-        int64_t off = 0;
-        for (int64_t k = 0; k < K; ++k)
-            for (int t = 0; t < T; ++t) {
+        // prefix over (key, chunk) with row-sequential passes over [chunk][key]
+        // (a key-major walk strides T x K: ~100 ns per entry when the hub
+        // rows of config 2 make K ~ 10^4)
+        std::vector<int64_t> kst(K + 1, 0);
+        for (int t = 0; t < T; ++t)
+            for (int64_t k = 0; k < K; ++k) kst[k + 1] += cnt[(size_t)t * K + k];
+        for (int64_t k = 0; k < K; ++k) kst[k + 1] += kst[k];
+        for (int t = 0; t < T; ++t)
+            for (int64_t k = 0; k < K; ++k) {
                 const int64_t c = cnt[(size_t)t * K + k];
-                cnt[(size_t)t * K + k] = off;
-                off += c;
+                cnt[(size_t)t * K + k] = kst[k];
+                kst[k] += c;
             }
 #pragma omp parallel for schedule(static, 1)
         for (int t = 0; t < T; ++t) {
@@ -382,101 +390,108 @@ void partition_view(const GraphView<Idx, Off>& g, int64_t s, double tol, int64_t
                 if (deg[v] > 0) order[nx[maxdeg - deg[v]]++] = (int32_t)v;
         }
     }
-    int64_t cursor = 0;
 
+    const bool dbg = getenv("HPBJ_DEBUG") != nullptr;
     const auto t_seed = std::chrono::steady_clock::now();
-    if (getenv("HPBJ_DEBUG"))
+    if (dbg)
         fprintf(stderr, "[hpbj]   seed order %.2f ms\n",
                 std::chrono::duration<double, std::milli>(t_seed - t_pv0).count());
-    // Region growing (partition.cpp:74-103). The free/taken test of the
-    // growing loop reads a bitmap (n bits: L1/L2-resident) instead of the
-    // 4-byte state array; state receives the block id once per node.
+
+    fit(W.conn, s);
+    double* conn = W.conn.data();
+    std::fill(conn, conn + s, 0.0);
     fit(W.queue, n + 1);
     int32_t* queue = W.queue.data();
     fit(W.taken, (n + 63) / 64);
     uint64_t* taken = W.taken.data();  // bit v: assigned or queued
 #pragma omp parallel for schedule(static) if (n > 65536)
     for (int64_t w = 0; w < (n + 63) / 64; ++w) taken[w] = 0ull;
-    int64_t connected_left = connected;
-    constexpr int kAhead = 6;
-    for (int64_t b = 0; b < s && connected_left > 0; ++b) {
-        const int64_t blocks_left = s - b;
-        int64_t target = (connected_left + blocks_left - 1) / blocks_left;
-        target = std::min(target, cap);
-        int64_t head = 0, tail = 0;
-        int64_t grown = 0;
-        const int32_t bb = (int32_t)b;
-        while (grown < target) {
-            if (head == tail) {  // queue empty: every taken node is assigned
-                while (cursor < connected && ((taken[order[cursor] >> 6] >> (order[cursor] & 63)) & 1ull)) ++cursor;
-                if (cursor == connected) break;
-                const int32_t sd = order[cursor];
-                queue[tail++] = sd;
-                taken[sd >> 6] |= 1ull << (sd & 63);
+
+    // Block ids are stored as S (16-bit when s fits: half the cache footprint
+    // of the refinement's random neighbour lookups); -1 = unassigned.
+    auto run = [&](auto* state) {
+        using S = std::remove_pointer_t<decltype(state)>;
+#pragma omp parallel for schedule(static) if (n > 65536)
+        for (int64_t v = 0; v < n; ++v) state[v] = (S)-1;
+        // Region growing (partition.cpp:74-103). The free/taken test reads a
+        // bitmap (n bits: cache-resident) instead of the state array; state
+        // receives the block id once per node.
+        int64_t cursor = 0;
+        int64_t connected_left = connected;
+        constexpr int kAhead = 6;
+        for (int64_t b = 0; b < s && connected_left > 0; ++b) {
+            const int64_t blocks_left = s - b;
+            int64_t target = (connected_left + blocks_left - 1) / blocks_left;
+            target = std::min(target, cap);
+            int64_t head = 0, tail = 0;
+            int64_t grown = 0;
+            const S bb = (S)b;
+            while (grown < target) {
+                if (head == tail) {  // queue empty: every taken node is assigned
+                    while (cursor < connected && ((taken[order[cursor] >> 6] >> (order[cursor] & 63)) & 1ull))
+                        ++cursor;
+                    if (cursor == connected) break;
+                    const int32_t sd = order[cursor];
+                    queue[tail++] = sd;
+                    taken[sd >> 6] |= 1ull << (sd & 63);
+                }
+                if (head + 2 * kAhead < tail) __builtin_prefetch(st + queue[head + 2 * kAhead], 0, 1);
+                if (head + kAhead < tail) {  // prefetch the adjacency of a node popped soon
+                    const int32_t f = queue[head + kAhead];
+                    __builtin_prefetch(nb + st[f], 0, 1);
+                }
+                const int32_t u = queue[head++];
+                state[u] = bb;
+                ++grown;
+                --connected_left;
+                for (Off k = st[u]; k < st[u + 1]; ++k) {  // branch-free push of the free neighbours
+                    const int32_t v = (int32_t)nb[k];
+                    uint64_t& word = taken[v >> 6];
+                    const uint64_t bit = 1ull << (v & 63);
+                    queue[tail] = v;
+                    tail += (word & bit) == 0;
+                    word |= bit;
+                }
             }
-            if (head + kAhead < tail) {  // prefetch the adjacency of a node popped soon
-                const int32_t f = queue[head + kAhead];
-                __builtin_prefetch(nb + st[f], 0, 1);
-            }
-            const int32_t u = queue[head++];
-            state[u] = bb;
-            ++grown;
-            --connected_left;
-            for (Off k = st[u]; k < st[u + 1]; ++k) {  // branch-free push of the free neighbours
-                const int32_t v = (int32_t)nb[k];
-                uint64_t& word = taken[v >> 6];
-                const uint64_t bit = 1ull << (v & 63);
-                queue[tail] = v;
-                tail += (word & bit) == 0;
-                word |= bit;
+            sizes[b] = grown;
+            for (int64_t q = head; q < tail; ++q) taken[queue[q] >> 6] &= ~(1ull << (queue[q] & 63));  // queue.clear()
+        }
+        const bool leftovers = connected < n || connected_left > 0;
+        const auto t_grown = std::chrono::steady_clock::now();
+        // Remaining nodes -> first block of minimal size (partition.cpp:105-112).
+        if (leftovers) {
+            using Key = std::pair<int64_t, int64_t>;  // (size, block)
+            std::priority_queue<Key, std::vector<Key>, std::greater<Key>> heap;
+            bool built = false;
+            for (int64_t v = 0; v < n; ++v) {
+                if (state[v] >= 0) continue;
+                if (!built) {
+                    for (int64_t b = 0; b < s; ++b) heap.push({sizes[b], b});
+                    built = true;
+                }
+                const Key k = heap.top();
+                heap.pop();
+                state[v] = (S)k.second;
+                ++sizes[k.second];
+                heap.push({sizes[k.second], k.second});
             }
         }
-        sizes[b] = grown;
-        for (int64_t q = head; q < tail; ++q) taken[queue[q] >> 6] &= ~(1ull << (queue[q] & 63));  // queue.clear()
-    }
-
-    // Remaining nodes -> first block of minimal size (partition.cpp:105-112).
-    // (none when every node has a neighbour and growing placed them all)
-    if (connected < n || connected_left > 0) {
-        using Key = std::pair<int64_t, int64_t>;  // (size, block)
-        std::priority_queue<Key, std::vector<Key>, std::greater<Key>> heap;
-        bool built = false;
-        for (int64_t v = 0; v < n; ++v) {
-            if (state[v] >= 0) continue;
-            if (!built) {
-                for (int64_t b = 0; b < s; ++b) heap.push({sizes[b], b});
-                built = true;
-            }
-            const Key k = heap.top();
-            heap.pop();
-            state[v] = (int32_t)k.second;
-            ++sizes[k.second];
-            heap.push({sizes[k.second], k.second});
-        }
-    }
-
-    const auto t_grow = std::chrono::steady_clock::now();
-    if (getenv("HPBJ_DEBUG"))
-        fprintf(stderr, "[hpbj]   bfs+leftovers %.1f ms\n",
-                std::chrono::duration<double, std::milli>(t_grow - t_seed).count());
-    // One boundary-refinement sweep (partition.cpp:117-141), verbatim order,
-    // on 16-bit block ids when they fit (half the cache footprint of the
-    // random neighbour lookups).
-    fit(W.conn, s);
-    double* conn = W.conn.data();
-    std::fill(conn, conn + s, 0.0);
+        const int64_t moves = refine_sweep(g, state, sizes, cap, conn);
+        if (dbg)
+            fprintf(stderr, "[hpbj]   grow %.1f ms, refine %.1f ms (%lld moves)\n",
+                    std::chrono::duration<double, std::milli>(t_grown - t_seed).count(),
+                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_grown).count(),
+                    (long long)moves);
+#pragma omp parallel for schedule(static) if (n > 65536)
+        for (int64_t v = 0; v < n; ++v) assignment[v] = state[v];
+    };
     if (s <= 32767) {
         fit(W.state16, n);
-        int16_t* st16 = W.state16.data();
-#pragma omp parallel for schedule(static) if (n > 65536)
-        for (int64_t v = 0; v < n; ++v) st16[v] = (int16_t)state[v];
-        refine_sweep(g, st16, sizes, cap, conn, assignment);
+        run(W.state16.data());
     } else {
-        refine_sweep(g, state, sizes, cap, conn, assignment);
+        fit(W.state, n);
+        run(W.state.data());
     }
-    if (getenv("HPBJ_DEBUG"))
-        fprintf(stderr, "[hpbj]   refine %.1f ms\n",
-                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_grow).count());
 }
 
 }  // namespace

@@ -1,11 +1,19 @@
-"""Dev helper: host partition timing per config (HPBJ_DEBUG=1 prints the phases)."""
-import os, sys, time
+"""Dev helper (host only): time graph + partition per config, R repeats.
+HPBJ_DEBUG=1 prints the phases; HPBJ_PART_PIPE=0 disables the pipelined refinement."""
+import os
+import sys
+import time
+
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2509_09139_b200 as hp
 from paper_2509_09139_b200.workloads import generate
-for c in [int(x) for x in sys.argv[1:]]:
+
+for c in [int(a) for a in sys.argv[1:]] or [1]:
     s = generate(c)
     a = hp.SparseMatrix(s.n, s.row_ptr, s.col, s.val)
-    for r in range(int(os.environ.get("REPS", "3"))):
-        t0 = time.perf_counter(); p = hp.partition_graph(a, s.num_blocks, 0.1); t1 = time.perf_counter()
-        print(c, r, f"{(t1-t0)*1e3:.1f} ms", flush=True)
+    ts = []
+    for r in range(int(os.environ.get("R", "5"))):
+        t0 = time.perf_counter()
+        hp.partition_graph(a, s.num_blocks, 0.1)
+        ts.append((time.perf_counter() - t0) * 1e3)
+    print(f"config {c}: partition ms {' '.join(f'{t:.2f}' for t in ts)}", flush=True)
