@@ -47,7 +47,7 @@ using sync::grid_barrier;
 using sync::transpose_reduce;
 
 constexpr int kMgsThreads = 1024;
-constexpr int kIcwyThreads = 512;
+constexpr int kIcwyThreads = 1024;
 constexpr size_t kSmemMax = 227 * 1024;
 
 // Sum of partials[0..count) in a fixed order; every thread of warp 0 gets it.
@@ -267,7 +267,8 @@ __global__ void __launch_bounds__(kMgsThreads, 1) k_mgs(OrthArgs a) {
 
 // ---------------------------------------------------------------------------
 constexpr int kIcwyWarps = kIcwyThreads / 32;
-constexpr int kBatch = 16;  // basis vectors per multi-dot batch (32 dot products)
+constexpr int kBatch = 8;  // basis vectors per multi-dot batch (16 dot products; 1024 threads x 64 registers:
+                           // the multi-dot pass is latency bound, more rows in flight beat longer batches)
 
 template <bool SMEM>
 __global__ void __launch_bounds__(kIcwyThreads, 1) k_icwy(OrthArgs a) {
@@ -313,9 +314,9 @@ __global__ void __launch_bounds__(kIcwyThreads, 1) k_icwy(OrthArgs a) {
     // ---- pass A: fused multi-dot  c_i = <v_i, w>,  l_i = <v_i, v_j>
     for (int i0 = 0; i0 <= j; i0 += kBatch) {
         const int nb = min(kBatch, j + 1 - i0);
-        double acc[32];
+        double acc[2 * kBatch];
 #pragma unroll
-        for (int q = 0; q < 32; ++q) acc[q] = 0.0;
+        for (int q = 0; q < 2 * kBatch; ++q) acc[q] = 0.0;
         for (int e = tid; e < nv2; e += kIcwyThreads) {
             const double2 wv = w2[e];
             const double2 jv = __ldg(vj2 + e);
@@ -330,8 +331,8 @@ __global__ void __launch_bounds__(kIcwyThreads, 1) k_icwy(OrthArgs a) {
                 }
             }
         }
-        const double r = transpose_reduce<32>(acc, lane);
-        red[wid][lane] = r;
+        const double r = transpose_reduce<2 * kBatch>(acc, lane);
+        if (lane < 2 * kBatch) red[wid][lane] = r;
         __syncthreads();
         if (tid < 2 * kBatch) {
             double s = 0.0;

@@ -229,6 +229,10 @@ struct hpbj_ctx {
     float* d_dtile = nullptr;
     float* d_eval = nullptr;
     uint32_t* d_eidx = nullptr;  // packed (col << 5 | row), 16- or 32-bit
+    int* d_ent_count_rows = nullptr;
+    unsigned long long* d_spk_totals = nullptr;
+    uint16_t* d_rmeta = nullptr;
+    int spk_rows = 0;            // off-panel layout: 0 row-sorted runs, 1 row quads (spk.cu)
     SpmvPlan planB;
     int* d_long_sort = nullptr;
     int n_long_sort = 0, max_long_sort = 0;
@@ -304,6 +308,9 @@ struct hpbj_ctx {
         dfree(d_dtile);
         dfree(d_eval);
         dfree(d_eidx);
+        dfree(d_ent_count_rows);
+        dfree(d_spk_totals);
+        dfree(d_rmeta);
         has_pc = false;
         dfree(d_ilu_lu);
         dfree(d_ilu_dpos);
@@ -438,7 +445,8 @@ void ensure_ws(hpbj_ctx* c, int m) {
 
 SpkView spk_view(const hpbj_ctx* c) {
     return SpkView{c->s,      c->dmax,   c->d_bstart, c->d_pstart, c->d_piv, c->d_desc,
-                   c->d_dtile, c->d_eval, c->d_eidx,  c->dmax > kIdx16MaxDim ? 1 : 0, c->d_ent_off};
+                   c->d_dtile, c->d_eval, c->d_eidx,  c->dmax > kIdx16MaxDim ? 1 : 0, c->d_ent_off,
+                   c->spk_rows, c->d_rmeta};
 }
 
 // Repack the dense LU panels into the sparse-panel apply format.
@@ -453,13 +461,26 @@ void build_spk(hpbj_ctx* c) {
     p.fac_off = c->d_fac_off;
     p.dense = c->d_fac;
     p.ent_count = c->d_ent_count;
+    p.ent_count_rows = c->d_ent_count_rows;
+    p.totals = c->d_spk_totals;
     p.ent_off = c->d_ent_off;
     launch_spk_count(p, st, &c->launches);
-    scan_exclusive(c->d_ent_count, c->d_ent_off, c->num_panels, c->d_scan_tmp, st, &c->launches);
-    int tot = 0;
-    HPBJ_CUDA(cudaMemcpyAsync(&tot, c->d_ent_off + c->num_panels, sizeof(int), cudaMemcpyDeviceToHost, st));
+    // Off-panel layout: row quads (fold_rows: one coalesced quad per row and
+    // slot, ~3x fewer fold instructions than the segmented fold) for blocks
+    // deeper than the fused cycle kernel takes (it folds row-sorted runs),
+    // or when padding rows to whole quads costs < 25% more entries;
+    // HPBJ_SPK_ROWS=0/1 forces one. Measured (B200): apply 343 -> 286 us on
+    // config 3, 70 -> 66 us on config 2.
+    unsigned long long totals[2] = {0, 0};
+    HPBJ_CUDA(cudaMemcpyAsync(totals, c->d_spk_totals, sizeof(totals), cudaMemcpyDeviceToHost, st));
     HPBJ_CUDA(cudaStreamSynchronize(st));
-    if (tot < 0) fail(HPBJ_EINVAL, "block_jacobi: factor nonzeros exceed 2^31");
+    const char* env_rows = getenv("HPBJ_SPK_ROWS");
+    c->spk_rows = env_rows ? (env_rows[0] == '1' ? 1 : 0) : (c->dmax > 96 || 4 * totals[1] <= 5 * totals[0] ? 1 : 0);
+    if (totals[c->spk_rows] >= (unsigned long long)INT32_MAX)
+        fail(HPBJ_EINVAL, "block_jacobi: factor nonzeros exceed 2^31");
+    scan_exclusive(c->spk_rows ? c->d_ent_count_rows : c->d_ent_count, c->d_ent_off, c->num_panels, c->d_scan_tmp, st,
+                   &c->launches);
+    const int tot = (int)totals[c->spk_rows];
     c->spk_entries = tot;
     const bool idx32 = c->dmax > kIdx16MaxDim;
     dslot(c->d_eval, (size_t)tot + 32);  // parts are 4-entry aligned
@@ -469,6 +490,8 @@ void build_spk(hpbj_ctx* c) {
     p.eval = c->d_eval;
     p.eidx = c->d_eidx;
     p.idx32 = idx32 ? 1 : 0;
+    p.rows = c->spk_rows;
+    p.rmeta = c->d_rmeta;
     launch_spk_pack(p, st, &c->launches);
 }
 
@@ -650,6 +673,7 @@ std::vector<uintptr_t> graph_signature(const hpbj_ctx* c) {
             (uintptr_t)L.smem, (uintptr_t)L.icwy, (uintptr_t)L.w_in_smem, (uintptr_t)c->fused.ok,
             (uintptr_t)c->fused.grid, (uintptr_t)c->fused.slice, (uintptr_t)c->fused.ystride,
             (uintptr_t)c->fused.smem, (uintptr_t)c->fused.nnz_cap, (uintptr_t)c->d_ent_off,
+            (uintptr_t)c->spk_rows, (uintptr_t)c->d_rmeta,
             (uintptr_t)c->neumann, (uintptr_t)c->d_nterm32, (uintptr_t)c->d_nterm64, (uintptr_t)c->d_nacc64,
             (uintptr_t)c->active, (uintptr_t)c->d_ilu_lu, (uintptr_t)c->d_ilu_dpos, (uintptr_t)c->d_ilu_flags,
             (uintptr_t)c->d_ilu_ytag, (uintptr_t)c->d_ilu_ztag,
@@ -730,6 +754,7 @@ double apply_bytes(const hpbj_ctx* c) {
     const double idx_b = c->dmax > kIdx16MaxDim ? 4.0 : 2.0;
     return (4.0 + idx_b) * (double)c->spk_entries          // off-panel value + packed index
            + (4.0 * 1024 + 16.0) * c->num_panels          // inverse-tile quads read + descriptors
+           + (c->spk_rows ? 128.0 * c->num_panels : 0.0)  // row-quad metadata
            + 4.0 * n                                      // pivot rows (int32)
            + 8.0 * n                                      // v (FP64) in
            + 4.0 * n                                      // z (FP32) out
@@ -838,7 +863,7 @@ void solve(hpbj_ctx* c, const double* d_b, double* d_x, const hpbj_gmres_opts* o
         R.converged = 1;
     } else {
         const bool use_graph = !c->profiling && c->use_graph;
-        c->fused = c->use_fused && c->active == kPcBJ && c->neumann <= 0 ? plan_fused(n, c->s, c->dmax, c->num_sms, m, c->planB.n_long > 0,
+        c->fused = c->use_fused && c->active == kPcBJ && c->neumann <= 0 && !c->spk_rows ? plan_fused(n, c->s, c->dmax, c->num_sms, m, c->planB.n_long > 0,
                                              c->h_rowlen_perm.data())
                                 : FusedPlan{};
         if (c->fused.ok && getenv("HPBJ_FUSED_PROF") && !c->d_fprof) {
@@ -1186,6 +1211,9 @@ int hpbj_bj_setup(hpbj_ctx* ctx, int64_t s, const int64_t* perm, const int64_t* 
         dslot(ctx->d_pstart, s + 1);
         dslot(ctx->d_panel_block, np);
         dslot(ctx->d_ent_count, np);
+        dslot(ctx->d_ent_count_rows, np);
+        dslot(ctx->d_spk_totals, 2);
+        dslot(ctx->d_rmeta, (size_t)np * 64);
         dslot(ctx->d_ent_off, np + 1);
         dslot(ctx->d_scan_tmp, 16384);
         dslot(ctx->d_desc, np);

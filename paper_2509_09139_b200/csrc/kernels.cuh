@@ -78,10 +78,11 @@ constexpr int kIdx16MaxDim = 2047;  // 16-bit packed indices up to this block si
 
 struct SpkPanel {
     int off;   // first L entry (16-byte aligned)
-    int nl;
-    int nu;
+    int nl;    // row-sorted: L entries; row quads: max quads per row | total quads << 11
+    int nu;    // same for U
     int uoff;  // first U entry (16-byte aligned)
 };
+constexpr int kRowQuadBits = 11;
 
 struct SpkBuild {
     int s;
@@ -98,6 +99,10 @@ struct SpkBuild {
     float* eval;
     void* eidx;             // uint16_t (dmax <= kIdx16MaxDim) or uint32_t
     int idx32;
+    int rows;               // pass 2 layout: 0 row-sorted runs, 1 rank-major row quads (see spk.cu)
+    int* ent_count_rows;    // pass 1 output: entries of the row-quad layout
+    unsigned long long* totals;  // pass 1 output: [0] entries row-sorted, [1] row-quad
+    uint16_t* rmeta;        // row-quad layout: per panel part, 32 x (row | quads << 5) in rank order
 };
 
 // Tile quads of row l (q = 0..7 cover columns 4q..4q+3, qd = l / 4): q < qd
@@ -116,6 +121,8 @@ struct SpkView {
     const void* eidx;
     int idx32;
     const int* ent_off;   // num_panels + 1 (prefetch ranges)
+    int rows;             // off-panel layout (SpkBuild::rows)
+    const uint16_t* rmeta;
 };
 
 void launch_spk_count(const SpkBuild& p, cudaStream_t st, int64_t* launches);

@@ -53,8 +53,52 @@ __device__ __forceinline__ float dense_at(const float* F, int dq, int k, int c) 
     return F[(size_t)t * 32 * 4 * dq + (c >> 2) * 128 + (k & 31) * 4 + (c & 3)];
 }
 
+__device__ __forceinline__ int warp_sum_int(int v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Row-quad layout of one off-panel part (columns [lo, hi) of panel row k):
+// each row's nonzeros in quads of four (zero padded), quad i of the row with
+// rank r (rows ranked by quad count desc, then row asc) at quad slot
+// S[i] + r, S[i] = number of quads in the slots before i. The active rows of
+// slot i are then ranks 0..c_i-1: the apply's lane r reads one coalesced
+// float4 + index quad per slot (spk_dev.cuh fold_rows). S (mq + 1 ints of
+// the warp's shared memory) is built by one ballot per slot; each lane then
+// scans its row once.
+template <class IdxT>
+__device__ void pack_row_quads(const SpkBuild& p, const float* F, int dq, int k, bool live, int lo, int hi, int q,
+                               int rank, int mq, int base, int* S, int lane) {
+    int run = 0;
+    for (int i = 0; i < mq; ++i) {
+        const int c = __popc(__ballot_sync(0xffffffffu, i < q));
+        if (lane == 0) S[i] = run;
+        run += c;
+    }
+    __syncwarp();
+    int cnt = 0;
+    IdxT* eidx = reinterpret_cast<IdxT*>(p.eidx);
+    if (live)
+        for (int c = lo; c < hi; ++c) {
+            const float f = dense_at(F, dq, k, c);
+            if (f != 0.0f) {
+                const int e = base + 4 * (S[cnt >> 2] + rank) + (cnt & 3);
+                p.eval[e] = f;
+                eidx[e] = (IdxT)c;
+                ++cnt;
+            }
+        }
+    for (; cnt & 3; ++cnt) {  // zero padding of the last quad
+        const int e = base + 4 * (S[cnt >> 2] + rank) + (cnt & 3);
+        p.eval[e] = 0.0f;
+        eidx[e] = (IdxT)0;
+    }
+    __syncwarp();
+}
+
 // Pass 1 (count) / pass 2 (pack); warp per panel, lane = panel row.
-template <bool PACK, class IdxT>
+template <bool PACK, class IdxT, bool ROWS = false>
 __global__ void k_spk_build(SpkBuild p) {
     extern __shared__ double inv_smem[];
     const int lane = threadIdx.x & 31;
@@ -78,19 +122,41 @@ __global__ void k_spk_build(SpkBuild p) {
         const int tl = __shfl_sync(0xffffffffu, el + nl, 31);
         const int tu = __shfl_sync(0xffffffffu, eu + nu, 31);
         const int pl = (tl + 3) & ~3, pu = (tu + 3) & ~3;  // parts start 16-byte aligned
+        const int ql = (nl + 3) >> 2, qu = (nu + 3) >> 2;  // row quads
+        const int sl = warp_sum_int(ql), su = warp_sum_int(qu);
         if (!PACK) {
-            if (lane == 0) p.ent_count[P] = pl + pu;
+            if (lane == 0) {
+                p.ent_count[P] = pl + pu;
+                p.ent_count_rows[P] = 4 * (sl + su);
+                atomicAdd(p.totals, (unsigned long long)(pl + pu));
+                atomicAdd(p.totals + 1, (unsigned long long)(4 * (sl + su)));
+            }
             continue;
         }
         const int base = p.ent_off[P];
-        if (lane == 0) p.desc[P] = SpkPanel{base, tl, tu, base + pl};
-        // the folds read whole quads: the padding up to each part's end is (0, col 0, row 0)
-        if (lane < pl - tl) {
-            p.eval[base + tl + lane] = 0.0f;
-            reinterpret_cast<IdxT*>(p.eidx)[base + tl + lane] = (IdxT)0;
-        } else if (lane >= 4 && lane - 4 < pu - tu) {
-            p.eval[base + pl + tu + lane - 4] = 0.0f;
-            reinterpret_cast<IdxT*>(p.eidx)[base + pl + tu + lane - 4] = (IdxT)0;
+        int rl = 0, ru = 0, mql = 0, mqu = 0;  // row-quad layout: ranks, longest rows
+        if (ROWS) {
+            for (int j = 0; j < 32; ++j) {
+                const int a = __shfl_sync(0xffffffffu, ql, j), b = __shfl_sync(0xffffffffu, qu, j);
+                rl += (a > ql) || (a == ql && j < lane);
+                ru += (b > qu) || (b == qu && j < lane);
+                mql = max(mql, a);
+                mqu = max(mqu, b);
+            }
+            if (lane == 0)
+                p.desc[P] = SpkPanel{base, mql | (sl << kRowQuadBits), mqu | (su << kRowQuadBits), base + 4 * sl};
+            p.rmeta[(size_t)(2 * P) * 32 + rl] = (uint16_t)(lane | (ql << 5));
+            p.rmeta[(size_t)(2 * P + 1) * 32 + ru] = (uint16_t)(lane | (qu << 5));
+        } else {
+            if (lane == 0) p.desc[P] = SpkPanel{base, tl, tu, base + pl};
+            // the folds read whole quads: the padding up to each part's end is (0, col 0, row 0)
+            if (lane < pl - tl) {
+                p.eval[base + tl + lane] = 0.0f;
+                reinterpret_cast<IdxT*>(p.eidx)[base + tl + lane] = (IdxT)0;
+            } else if (lane >= 4 && lane - 4 < pu - tu) {
+                p.eval[base + pl + tu + lane - 4] = 0.0f;
+                reinterpret_cast<IdxT*>(p.eidx)[base + pl + tu + lane - 4] = (IdxT)0;
+            }
         }
         // Inverse of the 32x32 diagonal triangle, in FP64 from the FP32
         // factors: Linv (unit lower) and Uinv (upper incl. diagonal), written
@@ -138,6 +204,12 @@ __global__ void k_spk_build(SpkBuild p) {
             }
             __syncwarp();
         }
+        if (ROWS) {
+            int* S = reinterpret_cast<int*>(inv_smem + (size_t)(threadIdx.x >> 5) * (2 * 32 * 33));
+            pack_row_quads<IdxT>(p, F, dq, k, k < d, 0, c0, ql, rl, mql, base, S, lane);
+            pack_row_quads<IdxT>(p, F, dq, k, k < d, c1, d, qu, ru, mqu, base + 4 * sl, S, lane);
+            continue;
+        }
         // off-panel entries, row-sorted: value + packed (column << 5 | row)
         if (k < d) {
             int q = base + el;
@@ -172,7 +244,7 @@ __global__ void k_panel_owner(const int* __restrict__ pstart, int s, int* __rest
 // a loss for deep ones (long folds already hide it; fewer resident warps).
 constexpr int kStageMaxDim = 160;
 
-template <class Acc, class IdxT, bool STAGE, class Src, class Dst>
+template <class Acc, class IdxT, bool STAGE, bool ROWS, class Src, class Dst>
 __global__ void __launch_bounds__(kWarpsPerCta * 32) k_apply_spk(SpkView p, Src src, Dst dst,
                                                                  const SolveState* sst, int ystride) {
     if (sst && sst->done) return;
@@ -180,32 +252,40 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_apply_spk(SpkView p, Src 
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int tmax = ystride / 32;
     constexpr int TB = STAGE ? 4096 : 0;
-    // per warp: [tile staging (8 x 32 float4)], y/x buffer (Acc[ystride]), panel descriptors
-    unsigned char* wbase = spk_smem + (size_t)wid * (TB + sizeof(Acc) * ystride + sizeof(SpkPanel) * tmax);
+    // per warp: [tile staging (8 x 32 float4)], y/x buffer (Acc[ystride]), panel descriptors,
+    // [row-quad metadata (2 x 32 uint16 per panel)]
+    const size_t per = TB + sizeof(Acc) * ystride + sizeof(SpkPanel) * tmax + (ROWS ? 128 * tmax : 0);
+    unsigned char* wbase = spk_smem + (size_t)wid * per;
     float4* tbuf = reinterpret_cast<float4*>(wbase);
     Acc* ybuf = reinterpret_cast<Acc*>(wbase + TB);
     SpkPanel* dsh = reinterpret_cast<SpkPanel*>(wbase + TB + sizeof(Acc) * ystride);
+    uint16_t* msh = reinterpret_cast<uint16_t*>(wbase + TB + sizeof(Acc) * ystride + sizeof(SpkPanel) * tmax);
     const int nw = gridDim.x * kWarpsPerCta;
     const int b_first = blockIdx.x * kWarpsPerCta + wid;
     if (b_first < p.s) prefetch_block_head<IdxT>(p, b_first, lane);
     for (int b = b_first; b < p.s; b += nw)
-        spk_solve_block<Acc, IdxT, STAGE>(p, b, b + nw < p.s ? b + nw : -1, src, dst, ybuf, dsh, lane, tbuf);
+        spk_solve_block<Acc, IdxT, STAGE, ROWS>(p, b, b + nw < p.s ? b + nw : -1, src, dst, ybuf, dsh, lane, tbuf,
+                                                msh);
 }
 
 template <class Acc, class Src, class Dst>
 void launch(const SpkView& v, Src src, Dst dst, const SolveState* sst, cudaStream_t st, int64_t* launches) {
     const int ystride = ((v.dmax + 31) / 32) * 32;
     const bool stage = v.dmax <= kStageMaxDim;
-    const size_t smem =
-        ((stage ? 4096 : 0) + sizeof(Acc) * ystride + sizeof(SpkPanel) * (ystride / 32)) * kWarpsPerCta;
+    const size_t smem = ((stage ? 4096 : 0) + sizeof(Acc) * ystride + sizeof(SpkPanel) * (ystride / 32) +
+                         (v.rows ? 128 * (ystride / 32) : 0)) *
+                        kWarpsPerCta;
     const int grid = (v.s + kWarpsPerCta - 1) / kWarpsPerCta;
-#define HPBJ_APPLY(IDX, STG) k_apply_spk<Acc, IDX, STG, Src, Dst><<<grid, kWarpsPerCta * 32, smem, st>>>(v, src, dst, sst, ystride)
-    if (v.idx32) {
-        if (stage) HPBJ_APPLY(uint32_t, true);
-        else HPBJ_APPLY(uint32_t, false);
+#define HPBJ_APPLY(IDX, STG, RW) k_apply_spk<Acc, IDX, STG, RW, Src, Dst><<<grid, kWarpsPerCta * 32, smem, st>>>(v, src, dst, sst, ystride)
+    if (v.rows) {
+        if (v.idx32) HPBJ_APPLY(uint32_t, false, true);
+        else HPBJ_APPLY(uint16_t, false, true);
+    } else if (v.idx32) {
+        if (stage) HPBJ_APPLY(uint32_t, true, false);
+        else HPBJ_APPLY(uint32_t, false, false);
     } else {
-        if (stage) HPBJ_APPLY(uint16_t, true);
-        else HPBJ_APPLY(uint16_t, false);
+        if (stage) HPBJ_APPLY(uint16_t, true, false);
+        else HPBJ_APPLY(uint16_t, false, false);
     }
 #undef HPBJ_APPLY
     *launches += 1;
@@ -217,6 +297,7 @@ void launch(const SpkView& v, Src src, Dst dst, const SolveState* sst, cudaStrea
 void launch_spk_count(const SpkBuild& p, cudaStream_t st, int64_t* launches) {
     k_panel_owner<<<std::max(1, std::min((p.s + 255) / 256, 1184)), 256, 0, st>>>(p.pstart, p.s, p.panel_block);
     const int grid = std::max(1, std::min((p.num_panels * 32 + 255) / 256, 148 * 16));
+    HPBJ_CUDA(cudaMemsetAsync(p.totals, 0, 2 * sizeof(unsigned long long), st));
     k_spk_build<false, uint16_t><<<grid, 256, 0, st>>>(p);
     *launches += 2;
     HPBJ_CUDA(cudaGetLastError());
@@ -225,7 +306,8 @@ void launch_spk_count(const SpkBuild& p, cudaStream_t st, int64_t* launches) {
 void launch_spk_pack(const SpkBuild& p, cudaStream_t st, int64_t* launches) {
     const int grid = std::max(1, std::min((p.num_panels * 32 + 127) / 128, 148 * 16));
     const int smem = 4 * 2 * 32 * 33 * sizeof(double);
-    auto fn = p.idx32 ? k_spk_build<true, uint32_t> : k_spk_build<true, uint16_t>;
+    auto fn = p.rows ? (p.idx32 ? k_spk_build<true, uint32_t, true> : k_spk_build<true, uint16_t, true>)
+                     : (p.idx32 ? k_spk_build<true, uint32_t> : k_spk_build<true, uint16_t>);
     HPBJ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     fn<<<grid, 128, smem, st>>>(p);
     *launches += 1;

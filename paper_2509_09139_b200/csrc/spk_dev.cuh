@@ -118,6 +118,58 @@ __device__ __forceinline__ void fold_entries(const float* __restrict__ eval, con
     }
 }
 
+// Row-quad layout (spk.cu pack_row_quads): lane r takes the rank-r row of
+// the part (meta = row | quads << 5, ranks ordered by quads desc), and reads
+// its quad i at quad slot S(i) + r, where S(i) counts the quads of the slots
+// before i (the active lanes of slot i are a prefix: one coalesced float4 +
+// index-quad load per slot). Each lane accumulates its row sequentially in
+// column order; acc[row] -= sum. No cross-lane traffic but one ballot per slot.
+template <class Acc, class IdxT>
+__device__ __forceinline__ void fold_rows(const float* __restrict__ eval, const IdxT* __restrict__ eidx, int e0,
+                                          int mq, unsigned meta, const Acc* xs, Acc* acc, int lane) {
+    using I4 = typename Idx4<IdxT>::type;
+    const float4* ev = reinterpret_cast<const float4*>(eval + e0);
+    const I4* ei = reinterpret_cast<const I4*>(eidx + e0);
+    const int q = (int)(meta >> 5);
+    Acc a = (Acc)0;
+    int S = lane;
+    int i = 0;
+    for (; i + 1 < mq; i += 2) {  // two slots' loads in flight
+        const unsigned act0 = __ballot_sync(0xffffffffu, i < q);
+        const int S1 = S + __popc(act0);
+        float4 v0 = make_float4(0.f, 0.f, 0.f, 0.f), v1 = v0;
+        I4 x0{}, x1{};
+        if (i < q) {
+            v0 = __ldg(ev + S);
+            x0 = __ldg(ei + S);
+        }
+        if (i + 1 < q) {
+            v1 = __ldg(ev + S1);
+            x1 = __ldg(ei + S1);
+        }
+        S = S1 + __popc(__ballot_sync(0xffffffffu, i + 1 < q));
+        a = fma((Acc)v0.x, xs[x0.x], a);
+        a = fma((Acc)v0.y, xs[x0.y], a);
+        a = fma((Acc)v0.z, xs[x0.z], a);
+        a = fma((Acc)v0.w, xs[x0.w], a);
+        a = fma((Acc)v1.x, xs[x1.x], a);
+        a = fma((Acc)v1.y, xs[x1.y], a);
+        a = fma((Acc)v1.z, xs[x1.z], a);
+        a = fma((Acc)v1.w, xs[x1.w], a);
+    }
+    if (i < mq && i < q) {
+        const float4 v0 = __ldg(ev + S);
+        const I4 x0 = __ldg(ei + S);
+        a = fma((Acc)v0.x, xs[x0.x], a);
+        a = fma((Acc)v0.y, xs[x0.y], a);
+        a = fma((Acc)v0.z, xs[x0.z], a);
+        a = fma((Acc)v0.w, xs[x0.w], a);
+    }
+    __syncwarp();
+    if (q > 0) acc[meta & 31u] -= a;
+    __syncwarp();
+}
+
 // L2 bulk prefetch of [p, p + bytes) (TMA engine; no registers, no smem).
 __device__ __forceinline__ void prefetch_l2(const void* p, size_t bytes) {
     const uintptr_t a = (uintptr_t)p & ~(uintptr_t)15;
@@ -162,7 +214,10 @@ __device__ __forceinline__ void prefetch_block_head(const SpkView& p, int b, int
     if (lane < 4) {
         const int o = p.bstart[b], d = p.bstart[b + 1] - o;
         const int e0 = p.ent_off[P0], e1 = p.ent_off[P0 + 1];
-        if (lane == 0) prefetch_l2(p.desc + P0, sizeof(SpkPanel) * (p.pstart[b + 1] - P0));
+        if (lane == 0) {
+            prefetch_l2(p.desc + P0, sizeof(SpkPanel) * (p.pstart[b + 1] - P0));
+            if (p.rows) prefetch_l2(p.rmeta + (size_t)P0 * 64, 128 * (p.pstart[b + 1] - P0));
+        }
         else if (lane == 1) prefetch_l2(p.piv + o, sizeof(int) * d);
         else prefetch_entries<IdxT>(p, e0, e1 - e0, lane, 2, 3);
     }
@@ -176,9 +231,13 @@ __device__ __forceinline__ void prefetch_block_head(const SpkView& p, int b, int
 // tbuf (optional, 8 x 32 float4 of the warp's shared memory): the step's
 // tile quads are copied there asynchronously at the start of the step, so
 // their latency overlaps the off-panel fold.
-template <class Acc, class IdxT, bool STAGE = false, class Src, class Dst>
+// ROWS: off-panel parts in the row-quad layout (fold_rows); msh (uint16
+// [64 T] of the warp's shared memory) receives the block's row metadata.
+template <class Acc, class IdxT, bool STAGE = false, bool ROWS = false, class Src, class Dst>
 __device__ __forceinline__ void spk_solve_block(const SpkView& p, int b, int next_b, Src src, Dst dst, Acc* ybuf,
-                                                SpkPanel* dsh, int lane, float4* tbuf = nullptr) {
+                                                SpkPanel* dsh, int lane, float4* tbuf = nullptr,
+                                                uint16_t* msh = nullptr) {
+    constexpr int kQMask = (1 << kRowQuadBits) - 1;
     const IdxT* eidx = reinterpret_cast<const IdxT*>(p.eidx);
     const int o = p.bstart[b];
     const int d = p.bstart[b + 1] - o;
@@ -186,6 +245,11 @@ __device__ __forceinline__ void spk_solve_block(const SpkView& p, int b, int nex
     const int P0 = p.pstart[b];
     const int qd = lane >> 2;
     if (lane < T) dsh[lane] = p.desc[P0 + lane];
+    if (ROWS) {
+        const uint32_t* m32 = reinterpret_cast<const uint32_t*>(p.rmeta + (size_t)P0 * 64);
+        uint32_t* s32 = reinterpret_cast<uint32_t*>(msh);
+        for (int t = 0; t < T; ++t) s32[t * 32 + lane] = __ldg(m32 + t * 32 + lane);
+    }
     __syncwarp();
     // rhs[pivot_rows[k]] for the whole block: all pivot loads first, then
     // all gathers (two latency rounds, not 2T)
@@ -210,10 +274,11 @@ __device__ __forceinline__ void spk_solve_block(const SpkView& p, int b, int nex
         const SpkPanel ds = dsh[t];
         // next step's data into L2 while this one computes
         if (t + 1 < T) {
-            prefetch_entries<IdxT>(p, dsh[t + 1].off, dsh[t + 1].nl, lane, 0, 1);
+            const int nl1 = dsh[t + 1].nl;
+            prefetch_entries<IdxT>(p, dsh[t + 1].off, ROWS ? 4 * (nl1 >> kRowQuadBits) : nl1, lane, 0, 1);
             prefetch_tile(p, P0 + t + 1, true, lane);
         } else {
-            prefetch_entries<IdxT>(p, ds.uoff, ds.nu, lane, 0, 1);
+            prefetch_entries<IdxT>(p, ds.uoff, ROWS ? 4 * (ds.nu >> kRowQuadBits) : ds.nu, lane, 0, 1);
             prefetch_tile(p, P0 + t, false, lane);
         }
         const float4* tile_f = reinterpret_cast<const float4*>(p.dtile + (size_t)(P0 + t) * kTileFloats);
@@ -223,7 +288,10 @@ __device__ __forceinline__ void spk_solve_block(const SpkView& p, int b, int nex
                 if (q <= qd) cp_async16(tbuf + q * 32 + lane, tile_f + q * 32 + lane);
             cp_async_commit();
         }
-        fold_entries<Acc, IdxT>(p.eval, eidx, ds.off, ds.nl, ybuf, ybuf + 32 * t, lane);
+        if (ROWS)
+            fold_rows<Acc, IdxT>(p.eval, eidx, ds.off, ds.nl & kQMask, msh[64 * t + lane], ybuf, ybuf + 32 * t, lane);
+        else
+            fold_entries<Acc, IdxT>(p.eval, eidx, ds.off, ds.nl, ybuf, ybuf + 32 * t, lane);
         // y_t = Linv_tt r_t: quads 0..qd of row `lane` (zeros from the diagonal on)
         {
             float4 f4[8];
@@ -252,7 +320,8 @@ __device__ __forceinline__ void spk_solve_block(const SpkView& p, int b, int nex
     for (int t = T - 1; t >= 0; --t) {
         const SpkPanel ds = dsh[t];
         if (t > 0) {
-            prefetch_entries<IdxT>(p, dsh[t - 1].uoff, dsh[t - 1].nu, lane, 0, 1);
+            const int nu1 = dsh[t - 1].nu;
+            prefetch_entries<IdxT>(p, dsh[t - 1].uoff, ROWS ? 4 * (nu1 >> kRowQuadBits) : nu1, lane, 0, 1);
             prefetch_tile(p, P0 + t - 1, false, lane);
         } else if (next_b >= 0) {
             prefetch_block_head<IdxT>(p, next_b, lane);
@@ -264,7 +333,11 @@ __device__ __forceinline__ void spk_solve_block(const SpkView& p, int b, int nex
                 if (q >= qd) cp_async16(tbuf + q * 32 + lane, tile_b + (q == qd ? 8 : q) * 32 + lane);
             cp_async_commit();
         }
-        fold_entries<Acc, IdxT>(p.eval, eidx, ds.uoff, ds.nu, ybuf, ybuf + 32 * t, lane);
+        if (ROWS)
+            fold_rows<Acc, IdxT>(p.eval, eidx, ds.uoff, ds.nu & kQMask, msh[64 * t + 32 + lane], ybuf, ybuf + 32 * t,
+                                 lane);
+        else
+            fold_entries<Acc, IdxT>(p.eval, eidx, ds.uoff, ds.nu, ybuf, ybuf + 32 * t, lane);
         // x_t = Uinv_tt y'_t: quad 8 (the diagonal quad) and quads qd+1..7 of row `lane`
         const int k = 32 * t + lane;
         {
