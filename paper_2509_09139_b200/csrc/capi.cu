@@ -446,7 +446,8 @@ void ensure_ws(hpbj_ctx* c, int m) {
 SpkView spk_view(const hpbj_ctx* c) {
     return SpkView{c->s,      c->dmax,   c->d_bstart, c->d_pstart, c->d_piv, c->d_desc,
                    c->d_dtile, c->d_eval, c->d_eidx,  c->dmax > kIdx16MaxDim ? 1 : 0, c->d_ent_off,
-                   c->spk_rows, c->d_rmeta};
+                   c->spk_rows, c->d_rmeta, c->spk_entries, c->num_panels, (int)c->A.n,
+                   getenv("HPBJ_APPLY_PF") ? (getenv("HPBJ_APPLY_PF")[0] == '1' ? 1 : 0) : 1};
 }
 
 // Repack the dense LU panels into the sparse-panel apply format.
@@ -863,8 +864,8 @@ void solve(hpbj_ctx* c, const double* d_b, double* d_x, const hpbj_gmres_opts* o
         R.converged = 1;
     } else {
         const bool use_graph = !c->profiling && c->use_graph;
-        c->fused = c->use_fused && c->active == kPcBJ && c->neumann <= 0 && !c->spk_rows ? plan_fused(n, c->s, c->dmax, c->num_sms, m, c->planB.n_long > 0,
-                                             c->h_rowlen_perm.data())
+        c->fused = c->use_fused && c->active == kPcBJ && c->neumann <= 0 ? plan_fused(n, c->s, c->dmax, c->num_sms, m, c->planB.n_long > 0,
+                                             c->h_rowlen_perm.data(), c->spk_rows != 0)
                                 : FusedPlan{};
         if (c->fused.ok && getenv("HPBJ_FUSED_PROF") && !c->d_fprof) {
             HPBJ_CUDA(cudaMalloc(&c->d_fprof, 8 * sizeof(unsigned long long)));

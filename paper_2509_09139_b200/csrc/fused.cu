@@ -35,6 +35,7 @@
 // Gram-Schmidt partial-sum grouping differs (warp per basis vector).
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "device.cuh"
 #include "kernels.cuh"
@@ -50,6 +51,10 @@ using sync::grid_barrier;
 constexpr int kThreads = 1024;
 constexpr int kWarps = kThreads / 32;
 constexpr size_t kSmemMax = 227 * 1024;
+
+__host__ __device__ inline size_t apply_warp_bytes(int ystride, bool rows) {
+    return sizeof(float) * ystride + sizeof(SpkPanel) * (ystride / 32) + (rows ? 128 * (ystride / 32) : 0);
+}
 
 struct SrcScaled {  // (float)(v[row] * scale): v_j = w * (1/h) (gmres.hpp:72-73)
     const double* v;
@@ -79,6 +84,7 @@ struct FusedArgs {
     int ystride;
     int nnz_cap;               // matrix slice capacity (entries) in shared memory
     unsigned long long* prof;  // optional: CTA 0 phase timers [4], ns
+    int l2_arena;              // prefetch the factor arena into L2 before each apply phase
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -154,6 +160,7 @@ __device__ void givens_step(const FusedArgs& a, GivensSmem& gs, const double* h,
     for (int i = lane; i <= j + 1; i += 32) Rj[i] = gs.R[i];
 }
 
+template <bool ROWS>
 __global__ void __launch_bounds__(kThreads, 1) k_arnoldi_cycle(FusedArgs a) {
     SolveState* st = a.st;
     if (*(volatile int*)&st->done) return;  // converged at restart (k_cycle_init)
@@ -201,12 +208,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_arnoldi_cycle(FusedArgs a) {
     int* mrp = mci + a.nnz_cap;                               // slice + 1 local row starts
     float* ybuf;
     SpkPanel* dsh;
+    uint16_t* msh;
     {
         unsigned char* base = reinterpret_cast<unsigned char*>(mrp + ((a.slice + 2) & ~1) + 2);
         base = reinterpret_cast<unsigned char*>(((uintptr_t)base + 15) & ~(uintptr_t)15);
-        const size_t per = sizeof(float) * a.ystride + sizeof(SpkPanel) * (a.ystride / 32);
+        const size_t per = apply_warp_bytes(a.ystride, ROWS);
         ybuf = reinterpret_cast<float*>(base + per * wid);
         dsh = reinterpret_cast<SpkPanel*>(base + per * wid + sizeof(float) * a.ystride);
+        msh = reinterpret_cast<uint16_t*>(base + per * wid + sizeof(float) * a.ystride +
+                                          sizeof(SpkPanel) * (a.ystride / 32));
     }
     // the CTA's rows of the (permuted) matrix stay in shared memory for the cycle
     const int nrows = max(0, min(len, a.n - r0));
@@ -247,8 +257,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_arnoldi_cycle(FusedArgs a) {
             const int aw = gw - 1;
             if (aw < a.pc.s) spk::prefetch_block_head<uint16_t>(a.pc, aw, lane);
             for (int b = aw; b < a.pc.s; b += naw)
-                spk::spk_solve_block<float, uint16_t>(a.pc, b, b + naw < a.pc.s ? b + naw : -1, SrcScaled{asrc, ascale},
-                                            DstZ{a.z32}, ybuf, dsh, lane);
+                spk::spk_solve_block<float, uint16_t, false, ROWS>(a.pc, b, b + naw < a.pc.s ? b + naw : -1,
+                                                                  SrcScaled{asrc, ascale}, DstZ{a.z32}, ybuf, dsh,
+                                                                  lane, nullptr, msh);
         }
         grid_barrier(a.gb);
         if (pending && *(volatile int*)&st->done) break;  // converged at step j-1
@@ -382,6 +393,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_arnoldi_cycle(FusedArgs a) {
         }
         ss2 = warp_sum(ss2);
         if (lane == 0) wred[wid] = ss2;
+        // the next step's apply reads the whole factor arena: pull it into L2
+        // now (each CTA its share), overlapping the last barriers of this step
+        if (a.l2_arena && wid == kWarps - 1) spk::prefetch_arena_l2(a.pc, blockIdx.x, G, lane);
         __syncthreads();
         if (tid == 0) {
             double s = 0.0;
@@ -424,11 +438,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_arnoldi_cycle(FusedArgs a) {
         for (int k = 0; k < 4; ++k) a.prof[k] += tsh[k];
 }
 
-size_t apply_warp_bytes(int ystride) { return sizeof(float) * ystride + sizeof(SpkPanel) * (ystride / 32); }
 
 }  // namespace
 
-FusedPlan plan_fused(int n, int s, int dmax, int num_sms, int m, bool has_long, const int* rowlen) {
+FusedPlan plan_fused(int n, int s, int dmax, int num_sms, int m, bool has_long, const int* rowlen, bool rows) {
     FusedPlan F;
     if (m > kMaxRestart || n <= 0 || dmax > kIdx16MaxDim) return F;
     if (has_long) return F;  // hub rows: the per-kernel path gives them whole CTAs
@@ -447,7 +460,7 @@ FusedPlan plan_fused(int n, int s, int dmax, int num_sms, int m, bool has_long, 
     nnz_cap = (nnz_cap + 1) & ~1;
     const size_t smem = (size_t)2 * slice * sizeof(double) + (size_t)(m + 1) * (m + 1) * sizeof(double) +
                         (size_t)nnz_cap * (sizeof(double) + sizeof(int)) + (size_t)(((slice + 2) & ~1) + 2) * sizeof(int) +
-                        16 + (size_t)kWarps * apply_warp_bytes(ystride);
+                        16 + (size_t)kWarps * apply_warp_bytes(ystride, rows);
     const size_t static_smem = sizeof(double) * (2 * (2 * kMaxRestart + 4) + 2 * (kMaxRestart + 1) + kWarps) +
                                sizeof(GivensSmem) + 1024;
     if (smem + static_smem > kSmemMax) return F;
@@ -457,6 +470,7 @@ FusedPlan plan_fused(int n, int s, int dmax, int num_sms, int m, bool has_long, 
     F.ystride = ystride;
     F.nnz_cap = nnz_cap;
     F.smem = smem;
+    F.rows = rows;
     return F;
 }
 
@@ -464,9 +478,20 @@ void launch_arnoldi_cycle(const FusedPlan& F, const SpkView& pc, const DevCsr& a
                           const KrylovBufs& kb, double* gram, SolveState* sst, GridBarrier* gb, float* z32,
                           unsigned long long* prof, cudaStream_t st, int64_t* launches) {
     FusedArgs args{pc, a, plan.group, plan.long_thresh, plan.n_long, plan.long_rows, kb, gram, sst, gb, z32,
-                   a.n, (a.n + 1) & ~1, F.slice, F.ystride, F.nnz_cap, prof};
-    HPBJ_CUDA(cudaFuncSetAttribute((const void*)k_arnoldi_cycle, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)F.smem));
+                   a.n, (a.n + 1) & ~1, F.slice, F.ystride, F.nnz_cap, prof, 0};
+    // The cycle kernel's apply runs from L2 (factors, basis and matrix of
+    // the fused configs fit): its chain is latency bound, and the per-step
+    // bulk L2 prefetches (a win for the HBM-streaming standalone apply)
+    // queue behind each other in the SM's TMA unit: off (config 1: apply
+    // phase 20.2 -> 16.6 us/step). Likewise no arena prefetch.
+    {
+        const char* e = getenv("HPBJ_L2_ARENA");
+        args.l2_arena = e ? (e[0] == '1') : 0;
+        const char* f = getenv("HPBJ_FUSED_PF");
+        args.pc.pf = f ? (f[0] == '1') : 0;
+    }
+    void (*fn)(FusedArgs) = F.rows ? k_arnoldi_cycle<true> : k_arnoldi_cycle<false>;
+    HPBJ_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)F.smem));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(F.grid);
     cfg.blockDim = dim3(kThreads);
@@ -477,7 +502,7 @@ void launch_arnoldi_cycle(const FusedPlan& F, const SpkView& pc, const DevCsr& a
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    HPBJ_CUDA(cudaLaunchKernelEx(&cfg, k_arnoldi_cycle, args));
+    HPBJ_CUDA(cudaLaunchKernelEx(&cfg, fn, args));
     *launches += 1;
 }
 

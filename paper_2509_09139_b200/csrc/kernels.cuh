@@ -123,6 +123,10 @@ struct SpkView {
     const int* ent_off;   // num_panels + 1 (prefetch ranges)
     int rows;             // off-panel layout (SpkBuild::rows)
     const uint16_t* rmeta;
+    int64_t n_entries;    // stored off-panel entries (arena sizes for L2 prefetch)
+    int num_panels;
+    int n;
+    int pf;               // L2 bulk prefetch of the next step's entries / tiles
 };
 
 void launch_spk_count(const SpkBuild& p, cudaStream_t st, int64_t* launches);
@@ -279,10 +283,11 @@ struct FusedPlan {
     int ystride = 0;
     int nnz_cap = 0;
     size_t smem = 0;
+    bool rows = false;  // SPK row-quad layout
 };
 // rowlen: row lengths of the permuted matrix (the CTA slices' matrix rows are
 // cached in shared memory)
-FusedPlan plan_fused(int n, int s, int dmax, int num_sms, int m, bool has_long, const int* rowlen);
+FusedPlan plan_fused(int n, int s, int dmax, int num_sms, int m, bool has_long, const int* rowlen, bool rows);
 void launch_arnoldi_cycle(const FusedPlan& F, const SpkView& pc, const DevCsr& a, const SpmvPlan& plan,
                           const KrylovBufs& kb, double* gram, SolveState* sst, GridBarrier* gb, float* z32,
                           unsigned long long* prof, cudaStream_t st, int64_t* launches);

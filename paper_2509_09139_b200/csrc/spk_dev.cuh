@@ -190,6 +190,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // forward pass quad q for lanes l >= 4q, the backward pass quad q < 8 for
 // lanes l < 4q and all of quad 8. Lanes 8..16 issue one quad each.
 __device__ __forceinline__ void prefetch_tile(const SpkView& p, int P, bool fwd, int lane) {
+    if (!p.pf) return;
     if (lane >= 8 && lane <= 16) {
         const int q = lane - 8;
         int l0 = 0, l1 = 32;
@@ -200,8 +201,26 @@ __device__ __forceinline__ void prefetch_tile(const SpkView& p, int P, bool fwd,
     }
 }
 
+// Part `part` of `nparts` of the whole factor arena (entries, tiles,
+// descriptors, pivots) into L2 — one warp, 32 KB per bulk request.
+__device__ __forceinline__ void prefetch_arena_l2(const SpkView& p, int part, int nparts, int lane) {
+    auto one = [&](const void* base, size_t bytes) {
+        const size_t chunk = (((bytes + nparts - 1) / nparts) + 15) & ~(size_t)15;
+        const size_t b0 = chunk * part, b1 = min(bytes, b0 + chunk);
+        for (size_t off = b0 + (size_t)lane * 32768; off < b1; off += (size_t)32 * 32768)
+            prefetch_l2(static_cast<const char*>(base) + off, min((size_t)32768, b1 - off));
+    };
+    one(p.eval, sizeof(float) * (size_t)p.n_entries);
+    one(p.eidx, (p.idx32 ? 4 : 2) * (size_t)p.n_entries);
+    one(p.dtile, sizeof(float) * kTileFloats * (size_t)p.num_panels);
+    one(p.desc, sizeof(SpkPanel) * (size_t)p.num_panels);
+    one(p.piv, sizeof(int) * (size_t)p.n);
+    if (p.rows) one(p.rmeta, 128 * (size_t)p.num_panels);
+}
+
 template <class IdxT>
 __device__ __forceinline__ void prefetch_entries(const SpkView& p, int e0, int cnt, int lane, int lv, int li) {
+    if (!p.pf) return;
     if (lane == lv) prefetch_l2(p.eval + e0, sizeof(float) * cnt);
     else if (lane == li) prefetch_l2(reinterpret_cast<const IdxT*>(p.eidx) + e0, sizeof(IdxT) * cnt);
 }
@@ -210,6 +229,7 @@ __device__ __forceinline__ void prefetch_entries(const SpkView& p, int e0, int c
 // Called by the whole warp (one prefetch per lane).
 template <class IdxT>
 __device__ __forceinline__ void prefetch_block_head(const SpkView& p, int b, int lane) {
+    if (!p.pf) return;
     const int P0 = p.pstart[b];
     if (lane < 4) {
         const int o = p.bstart[b], d = p.bstart[b + 1] - o;
