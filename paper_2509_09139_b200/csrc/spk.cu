@@ -160,10 +160,15 @@ __global__ void k_spk_build(SpkBuild p) {
         }
         // Inverse of the 32x32 diagonal triangle, in FP64 from the FP32
         // factors: Linv (unit lower) and Uinv (upper incl. diagonal), written
-        // as 9 float4 quads per row (see kernels.cuh SpkView::dtile).
+        // as 9 float4 quads per row (see kernels.cuh SpkView::dtile). The
+        // block's last panel stores the product Uinv Linv instead (8 quads):
+        // its forward and backward in-panel solves are back to back (no U
+        // entries right of it), so the apply does them as one mat-vec.
+        const bool last = 32 * (t + 1) >= d;
         {
-            double* Tt = inv_smem + (size_t)(threadIdx.x >> 5) * (2 * 32 * 33);
+            double* Tt = inv_smem + (size_t)(threadIdx.x >> 5) * (3 * 32 * 33);
             double* X = Tt + 32 * 33;
+            double* Y = X + 32 * 33;  // Linv (FP64) of the last panel
             for (int c = 0; c < 32; ++c) {
                 const int cc = c0 + c;
                 double v;
@@ -182,6 +187,8 @@ __global__ void k_spk_build(SpkBuild p) {
             __syncwarp();
             float linv[32];
             for (int j = 0; j < 32; ++j) linv[j] = (float)X[lane * 33 + j];  // row `lane` of Linv
+            if (last)
+                for (int i = 0; i < 32; ++i) Y[i * 33 + c] = X[i * 33 + c];
             __syncwarp();
             for (int i = 31; i >= 0; --i) {  // U x = e_c, upper with diagonal
                 double sum = (i == c) ? 1.0 : 0.0;
@@ -191,21 +198,37 @@ __global__ void k_spk_build(SpkBuild p) {
             __syncwarp();
             float4* tile = reinterpret_cast<float4*>(p.dtile + (size_t)P * kTileFloats);
             const int qd = lane >> 2;  // the quad holding the diagonal
-            for (int q = 0; q < 9; ++q) {
-                float4 v4;
-                float* w4 = &v4.x;
-                for (int u = 0; u < 4; ++u) {
-                    const int j = 4 * (q < 8 ? q : qd) + u;
-                    const float lo = (j < lane) ? linv[j] : 0.0f;            // strictly lower Linv
-                    const float up = (j >= lane) ? (float)X[lane * 33 + j] : 0.0f;  // upper Uinv
-                    w4[u] = (q == 8) ? up : (q < qd ? lo : (q > qd ? up : lo));
+            if (last) {  // row `lane` of Uinv Linv: sum over k >= max(lane, col) (both triangular)
+                for (int q = 0; q < 9; ++q) {
+                    float4 v4 = make_float4(0.f, 0.f, 0.f, 0.f);
+                    float* w4 = &v4.x;
+                    if (q < 8)
+                        for (int u = 0; u < 4; ++u) {
+                            const int cc = 4 * q + u;
+                            double acc = 0.0;
+                            for (int kk = max(lane, cc); kk < 32; ++kk) acc += X[lane * 33 + kk] * Y[kk * 33 + cc];
+                            w4[u] = (float)acc;
+                        }
+                    tile[q * 32 + lane] = v4;
                 }
-                tile[q * 32 + lane] = v4;
+                __syncwarp();
+            } else {
+                for (int q = 0; q < 9; ++q) {
+                    float4 v4;
+                    float* w4 = &v4.x;
+                    for (int u = 0; u < 4; ++u) {
+                        const int j = 4 * (q < 8 ? q : qd) + u;
+                        const float lo = (j < lane) ? linv[j] : 0.0f;                   // strictly lower Linv
+                        const float up = (j >= lane) ? (float)X[lane * 33 + j] : 0.0f;  // upper Uinv
+                        w4[u] = (q == 8) ? up : (q < qd ? lo : (q > qd ? up : lo));
+                    }
+                    tile[q * 32 + lane] = v4;
+                }
             }
             __syncwarp();
         }
         if (ROWS) {
-            int* S = reinterpret_cast<int*>(inv_smem + (size_t)(threadIdx.x >> 5) * (2 * 32 * 33));
+            int* S = reinterpret_cast<int*>(inv_smem + (size_t)(threadIdx.x >> 5) * (3 * 32 * 33));
             pack_row_quads<IdxT>(p, F, dq, k, k < d, 0, c0, ql, rl, mql, base, S, lane);
             pack_row_quads<IdxT>(p, F, dq, k, k < d, c1, d, qu, ru, mqu, base + 4 * sl, S, lane);
             continue;
@@ -245,7 +268,7 @@ __global__ void k_panel_owner(const int* __restrict__ pstart, int s, int* __rest
 constexpr int kStageMaxDim = 160;
 
 template <class Acc, class IdxT, bool STAGE, bool ROWS, class Src, class Dst>
-__global__ void __launch_bounds__(kWarpsPerCta * 32) k_apply_spk(SpkView p, Src src, Dst dst,
+__global__ void __launch_bounds__(kWarpsPerCta * 32, ROWS ? 7 : 8) k_apply_spk(SpkView p, Src src, Dst dst,
                                                                  const SolveState* sst, int ystride) {
     if (sst && sst->done) return;
     extern __shared__ __align__(16) unsigned char spk_smem[];
@@ -305,7 +328,7 @@ void launch_spk_count(const SpkBuild& p, cudaStream_t st, int64_t* launches) {
 
 void launch_spk_pack(const SpkBuild& p, cudaStream_t st, int64_t* launches) {
     const int grid = std::max(1, std::min((p.num_panels * 32 + 127) / 128, 148 * 16));
-    const int smem = 4 * 2 * 32 * 33 * sizeof(double);
+    const int smem = 4 * 3 * 32 * 33 * sizeof(double);
     auto fn = p.rows ? (p.idx32 ? k_spk_build<true, uint32_t, true> : k_spk_build<true, uint16_t, true>)
                      : (p.idx32 ? k_spk_build<true, uint32_t> : k_spk_build<true, uint16_t>);
     HPBJ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));

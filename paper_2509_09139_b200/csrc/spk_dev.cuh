@@ -4,6 +4,7 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 
 #include "device.cuh"
 #include "kernels.cuh"
@@ -49,6 +50,20 @@ struct DstAddX {  // x = x0 + z (gmres.cpp:158-159)
     double* x;
     __device__ void operator()(int row, double v) const { x[row] = x[row] + v; }
 };
+
+// Four consecutive Acc of a 16-byte aligned shared-memory row as one load.
+template <class Acc>
+struct Vec4 {
+    Acc x, y, z, w;
+};
+__device__ __forceinline__ Vec4<float> ld_vec4(const float* p) {
+    const float4 v = *reinterpret_cast<const float4*>(p);
+    return {v.x, v.y, v.z, v.w};
+}
+__device__ __forceinline__ Vec4<double> ld_vec4(const double* p) {
+    const double2 a = reinterpret_cast<const double2*>(p)[0], b = reinterpret_cast<const double2*>(p)[1];
+    return {a.x, a.y, b.x, b.y};
+}
 
 template <class IdxT>
 struct Idx4;
@@ -189,12 +204,14 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // The tile quads a pass reads ([quad][lane] float4, see kernels.cuh): the
 // forward pass quad q for lanes l >= 4q, the backward pass quad q < 8 for
 // lanes l < 4q and all of quad 8. Lanes 8..16 issue one quad each.
-__device__ __forceinline__ void prefetch_tile(const SpkView& p, int P, bool fwd, int lane) {
+// full: the block's last panel (Uinv Linv, quads 0..7 of every lane).
+__device__ __forceinline__ void prefetch_tile(const SpkView& p, int P, bool fwd, int lane, bool full = false) {
     if (!p.pf) return;
     if (lane >= 8 && lane <= 16) {
         const int q = lane - 8;
         int l0 = 0, l1 = 32;
-        if (q == 8) l1 = fwd ? 0 : 32;
+        if (q == 8) l1 = (fwd || full) ? 0 : 32;
+        else if (full) l0 = 0;
         else if (fwd) l0 = 4 * q;
         else l1 = 4 * q;
         if (l1 > l0) prefetch_l2(p.dtile + (size_t)P * kTileFloats + q * 128 + l0 * 4, (size_t)16 * (l1 - l0));
@@ -241,7 +258,7 @@ __device__ __forceinline__ void prefetch_block_head(const SpkView& p, int b, int
         else if (lane == 1) prefetch_l2(p.piv + o, sizeof(int) * d);
         else prefetch_entries<IdxT>(p, e0, e1 - e0, lane, 2, 3);
     }
-    prefetch_tile(p, P0, true, lane);
+    prefetch_tile(p, P0, true, lane, p.pstart[b + 1] - P0 == 1);
 }
 
 // One block's substitution M_b^-1: gather rhs[piv] from src, forward with
@@ -289,55 +306,64 @@ __device__ __forceinline__ void spk_solve_block(const SpkView& p, int b, int nex
         }
     }
     __syncwarp();
-    // ---- forward: y_k = rhs_k - sum_{c<k} L_kc y_c
-    for (int t = 0; t < T; ++t) {
+    // ---- forward: y_k = rhs_k - sum_{c<k} L_kc y_c. The last panel's tile
+    // is Uinv Linv (8 full quads, spk.cu): its forward and backward solves
+    // are one mat-vec, peeled out of the loop (no extra live registers).
+    auto fwd_step = [&](int t, auto last_c) {
+        constexpr bool lastp = decltype(last_c)::value;
         const SpkPanel ds = dsh[t];
         // next step's data into L2 while this one computes
-        if (t + 1 < T) {
+        if (!lastp) {
             const int nl1 = dsh[t + 1].nl;
             prefetch_entries<IdxT>(p, dsh[t + 1].off, ROWS ? 4 * (nl1 >> kRowQuadBits) : nl1, lane, 0, 1);
-            prefetch_tile(p, P0 + t + 1, true, lane);
-        } else {
-            prefetch_entries<IdxT>(p, ds.uoff, ROWS ? 4 * (ds.nu >> kRowQuadBits) : ds.nu, lane, 0, 1);
-            prefetch_tile(p, P0 + t, false, lane);
+            prefetch_tile(p, P0 + t + 1, true, lane, t + 2 == T);
+        } else if (T >= 2) {  // the backward pass starts at panel T-2
+            const int nu1 = dsh[T - 2].nu;
+            prefetch_entries<IdxT>(p, dsh[T - 2].uoff, ROWS ? 4 * (nu1 >> kRowQuadBits) : nu1, lane, 0, 1);
+            prefetch_tile(p, P0 + T - 2, false, lane);
+        } else if (next_b >= 0) {
+            prefetch_block_head<IdxT>(p, next_b, lane);
         }
         const float4* tile_f = reinterpret_cast<const float4*>(p.dtile + (size_t)(P0 + t) * kTileFloats);
         if (STAGE) {
 #pragma unroll
             for (int q = 0; q < 8; ++q)
-                if (q <= qd) cp_async16(tbuf + q * 32 + lane, tile_f + q * 32 + lane);
+                if (q <= qd || lastp) cp_async16(tbuf + q * 32 + lane, tile_f + q * 32 + lane);
             cp_async_commit();
         }
         if (ROWS)
             fold_rows<Acc, IdxT>(p.eval, eidx, ds.off, ds.nl & kQMask, msh[64 * t + lane], ybuf, ybuf + 32 * t, lane);
         else
             fold_entries<Acc, IdxT>(p.eval, eidx, ds.off, ds.nl, ybuf, ybuf + 32 * t, lane);
-        // y_t = Linv_tt r_t: quads 0..qd of row `lane` (zeros from the diagonal on)
-        {
-            float4 f4[8];
-            if (STAGE) cp_async_wait_all();  // each lane reads back only the quads it copied
+        // y_t = Linv_tt r_t: quads 0..qd of row `lane` (zeros from the diagonal
+        // on, unit diagonal implied); last panel: x_t = (Uinv Linv)_tt r_t
+        float4 f4[8];
+        if (STAGE) cp_async_wait_all();  // each lane reads back only the quads it copied
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                f4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (q <= qd) f4[q] = STAGE ? tbuf[q * 32 + lane] : __ldg(tile_f + q * 32 + lane);
-            }
-            const Acc* r = ybuf + 32 * t;
-            Acc a0 = r[lane], a1 = (Acc)0, a2 = (Acc)0, a3 = (Acc)0;
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                a0 = fma((Acc)f4[q].x, r[4 * q + 0], a0);
-                a1 = fma((Acc)f4[q].y, r[4 * q + 1], a1);
-                a2 = fma((Acc)f4[q].z, r[4 * q + 2], a2);
-                a3 = fma((Acc)f4[q].w, r[4 * q + 3], a3);
-            }
-            const Acc yv = (a0 + a1) + (a2 + a3);
-            __syncwarp();
-            ybuf[32 * t + lane] = yv;
-            __syncwarp();
+        for (int q = 0; q < 8; ++q) {
+            f4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (q <= qd || lastp) f4[q] = STAGE ? tbuf[q * 32 + lane] : __ldg(tile_f + q * 32 + lane);
         }
-    }
+        const Acc* r = ybuf + 32 * t;
+        Acc a0 = lastp ? (Acc)0 : r[lane], a1 = (Acc)0, a2 = (Acc)0, a3 = (Acc)0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const Vec4<Acc> rq = ld_vec4(r + 4 * q);  // broadcast: one LDS.128 for four columns
+            a0 = fma((Acc)f4[q].x, rq.x, a0);
+            a1 = fma((Acc)f4[q].y, rq.y, a1);
+            a2 = fma((Acc)f4[q].z, rq.z, a2);
+            a3 = fma((Acc)f4[q].w, rq.w, a3);
+        }
+        const Acc yv = (a0 + a1) + (a2 + a3);
+        __syncwarp();
+        ybuf[32 * t + lane] = yv;
+        __syncwarp();
+        if (lastp && 32 * t + lane < d) dst(o + 32 * t + lane, yv);
+    };
+    for (int t = 0; t + 1 < T; ++t) fwd_step(t, std::false_type{});
+    fwd_step(T - 1, std::true_type{});
     // ---- backward: x_k = (y_k - sum_{c>k} U_kc x_c) / U_kk
-    for (int t = T - 1; t >= 0; --t) {
+    for (int t = T - 2; t >= 0; --t) {
         const SpkPanel ds = dsh[t];
         if (t > 0) {
             const int nu1 = dsh[t - 1].nu;
@@ -372,10 +398,11 @@ __device__ __forceinline__ void spk_solve_block(const SpkView& p, int b, int nex
             Acc a0 = (Acc)0, a1 = (Acc)0, a2 = (Acc)0, a3 = (Acc)0;
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-                a0 = fma((Acc)f4[q].x, r[4 * q + 0], a0);
-                a1 = fma((Acc)f4[q].y, r[4 * q + 1], a1);
-                a2 = fma((Acc)f4[q].z, r[4 * q + 2], a2);
-                a3 = fma((Acc)f4[q].w, r[4 * q + 3], a3);
+                const Vec4<Acc> rq = ld_vec4(r + 4 * q);
+                a0 = fma((Acc)f4[q].x, rq.x, a0);
+                a1 = fma((Acc)f4[q].y, rq.y, a1);
+                a2 = fma((Acc)f4[q].z, rq.z, a2);
+                a3 = fma((Acc)f4[q].w, rq.w, a3);
             }
             const Acc xv = (a0 + a1) + (a2 + a3);
             __syncwarp();
