@@ -166,9 +166,8 @@ __global__ void k_spk_build(SpkBuild p) {
         // entries right of it), so the apply does them as one mat-vec.
         const bool last = 32 * (t + 1) >= d;
         {
-            double* Tt = inv_smem + (size_t)(threadIdx.x >> 5) * (3 * 32 * 33);
+            double* Tt = inv_smem + (size_t)(threadIdx.x >> 5) * (2 * 32 * 33);
             double* X = Tt + 32 * 33;
-            double* Y = X + 32 * 33;  // Linv (FP64) of the last panel
             for (int c = 0; c < 32; ++c) {
                 const int cc = c0 + c;
                 double v;
@@ -187,31 +186,24 @@ __global__ void k_spk_build(SpkBuild p) {
             __syncwarp();
             float linv[32];
             for (int j = 0; j < 32; ++j) linv[j] = (float)X[lane * 33 + j];  // row `lane` of Linv
-            if (last)
-                for (int i = 0; i < 32; ++i) Y[i * 33 + c] = X[i * 33 + c];
             __syncwarp();
-            for (int i = 31; i >= 0; --i) {  // U x = e_c, upper with diagonal
-                double sum = (i == c) ? 1.0 : 0.0;
+            // U x = e_c (Uinv, upper with diagonal); last panel: U x = Linv e_c
+            // in place (X = Uinv Linv = (L U)^-1 of the diagonal tile)
+            for (int i = 31; i >= 0; --i) {
+                double sum = last ? X[i * 33 + c] : ((i == c) ? 1.0 : 0.0);
                 for (int j = i + 1; j < 32; ++j) sum -= Tt[i * 33 + j] * X[j * 33 + c];
-                X[i * 33 + c] = (i > c) ? 0.0 : sum / Tt[i * 33 + i];
+                X[i * 33 + c] = (!last && i > c) ? 0.0 : sum / Tt[i * 33 + i];
             }
             __syncwarp();
             float4* tile = reinterpret_cast<float4*>(p.dtile + (size_t)P * kTileFloats);
             const int qd = lane >> 2;  // the quad holding the diagonal
-            if (last) {  // row `lane` of Uinv Linv: sum over k >= max(lane, col) (both triangular)
+            if (last) {  // row `lane` of Uinv Linv
                 for (int q = 0; q < 9; ++q) {
                     float4 v4 = make_float4(0.f, 0.f, 0.f, 0.f);
-                    float* w4 = &v4.x;
-                    if (q < 8)
-                        for (int u = 0; u < 4; ++u) {
-                            const int cc = 4 * q + u;
-                            double acc = 0.0;
-                            for (int kk = max(lane, cc); kk < 32; ++kk) acc += X[lane * 33 + kk] * Y[kk * 33 + cc];
-                            w4[u] = (float)acc;
-                        }
+                    if (q < 8) v4 = make_float4((float)X[lane * 33 + 4 * q], (float)X[lane * 33 + 4 * q + 1],
+                                                (float)X[lane * 33 + 4 * q + 2], (float)X[lane * 33 + 4 * q + 3]);
                     tile[q * 32 + lane] = v4;
                 }
-                __syncwarp();
             } else {
                 for (int q = 0; q < 9; ++q) {
                     float4 v4;
@@ -228,7 +220,7 @@ __global__ void k_spk_build(SpkBuild p) {
             __syncwarp();
         }
         if (ROWS) {
-            int* S = reinterpret_cast<int*>(inv_smem + (size_t)(threadIdx.x >> 5) * (3 * 32 * 33));
+            int* S = reinterpret_cast<int*>(inv_smem + (size_t)(threadIdx.x >> 5) * (2 * 32 * 33));
             pack_row_quads<IdxT>(p, F, dq, k, k < d, 0, c0, ql, rl, mql, base, S, lane);
             pack_row_quads<IdxT>(p, F, dq, k, k < d, c1, d, qu, ru, mqu, base + 4 * sl, S, lane);
             continue;
@@ -328,7 +320,7 @@ void launch_spk_count(const SpkBuild& p, cudaStream_t st, int64_t* launches) {
 
 void launch_spk_pack(const SpkBuild& p, cudaStream_t st, int64_t* launches) {
     const int grid = std::max(1, std::min((p.num_panels * 32 + 127) / 128, 148 * 16));
-    const int smem = 4 * 3 * 32 * 33 * sizeof(double);
+    const int smem = 4 * 2 * 32 * 33 * sizeof(double);
     auto fn = p.rows ? (p.idx32 ? k_spk_build<true, uint32_t, true> : k_spk_build<true, uint16_t, true>)
                      : (p.idx32 ? k_spk_build<true, uint32_t> : k_spk_build<true, uint16_t>);
     HPBJ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
