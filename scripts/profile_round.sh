@@ -28,3 +28,8 @@ cap 3 k_mgs c3_mgs 0 8
 cap 3 k_block_lu_blk c3_lu 0 0
 cap 3 k_spk_build c3_spk_build 0 1
 ls -la gpurun_out | grep $RND
+# summarise on the box (the full captures exceed gpurun's copy-back limit);
+# keep only the hot kernels' reports for source-level reading here
+OUT=gpurun_out/profiles python scripts/summarize_round.py $RND > gpurun_out/${RND}_summary.log 2>&1
+for f in gpurun_out/${RND}_prof_*.ncu-rep; do case $f in *c1_arnoldi_cycle*|*c3_apply*|*c2_apply*) ;; *) rm -f $f ;; esac; done
+du -sh gpurun_out

@@ -4,8 +4,8 @@ traffic per launch used by bench.py's roofline, and SASS listings."""
 import collections, csv, io, json, os, re, subprocess, sys
 
 RND = sys.argv[1] if len(sys.argv) > 1 else "r01"
-SRC = "gpurun_out"
-OUT = "profiles"
+SRC = os.environ.get("SRC", "gpurun_out")
+OUT = os.environ.get("OUT", "profiles")
 os.makedirs(OUT, exist_ok=True)
 SC = {"ns": 1e-3, "us": 1.0, "ms": 1e3, "s": 1e6, "nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}
 
@@ -90,7 +90,8 @@ if os.path.exists(so):
     sass = subprocess.run(["cuobjdump", "-sass", so], capture_output=True, text=True).stdout
     funcs = re.split(r"\n\s*Function : ", sass)
     index = []
-    hot = ("k_apply_spk<float, unsigned short, SrcDown", "k_arnoldi_cycle", "k_spmv<1, float", "k_spmv<2, float",
+    hot = ("k_apply_spk<float, unsigned short, false, false, SrcDown", "k_apply_spk<float, unsigned short, false, true, SrcDown",
+           "k_apply_spk<float, unsigned short, true, false, SrcDown", "k_arnoldi_cycle<false", "k_spmv<1, float", "k_spmv<2, float",
            "k_icwy<true", "k_mgs<true", "k_block_lu_blk", "k_block_lu_warp<3", "k_spk_build<true, unsigned short")
     for fn in funcs[1:]:
         name = fn.split("\n", 1)[0].strip()
