@@ -357,17 +357,20 @@ __global__ void __launch_bounds__(256) k_block_lu_warp(LuParams p, int dw, int l
         if (!abort) {
             const int T = (d + 31) / 32;
             const int dp4 = (d + 3) & ~3;
-            const int total = T * 32 * dp4;
             float* F = p.fac + p.fac_off[b];
-            for (int e = lane; e < total; e += 32) {
-                const int t = e / (32 * dp4);
-                const int rem = e - t * 32 * dp4;
-                const int c = ((rem >> 7) << 2) | (rem & 3);
-                const int k = 32 * t + ((rem >> 2) & 31);
-                float v;
-                if (k < d && c < d) v = A[prow[k] * ld + c];
-                else v = (k == c) ? 1.0f : 0.0f;
-                F[e] = v;
+            // panel t, element rem = (c >> 2) * 128 + (k & 31) * 4 + (c & 3):
+            // lane-contiguous stores, the row index fixed per lane and panel
+            for (int t = 0; t < T; ++t) {
+                float* Ft = F + (size_t)t * 32 * dp4;
+                const int k = 32 * t + (lane >> 2);  // rows of rem = lane + 32 i: (lane >> 2) + 8 (i & 3)
+                for (int rem = lane; rem < 32 * dp4; rem += 32) {
+                    const int c = ((rem >> 7) << 2) | (rem & 3);
+                    const int kk = k + (((rem >> 5) & 3) << 3);
+                    float v;
+                    if (kk < d && c < d) v = A[prow[kk] * ld + c];
+                    else v = (kk == c) ? 1.0f : 0.0f;
+                    Ft[rem] = v;
+                }
             }
             for (int k = lane; k < d; k += 32) p.piv[o + k] = prow[k];
         }

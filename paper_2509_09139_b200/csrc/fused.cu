@@ -52,8 +52,10 @@ constexpr int kThreads = 1024;
 constexpr int kWarps = kThreads / 32;
 constexpr size_t kSmemMax = 227 * 1024;
 
+// per warp: y/x buffer, descriptors, [row metadata], block cache (header + pivots)
 __host__ __device__ inline size_t apply_warp_bytes(int ystride, bool rows) {
-    return sizeof(float) * ystride + sizeof(SpkPanel) * (ystride / 32) + (rows ? 128 * (ystride / 32) : 0);
+    return sizeof(float) * ystride + sizeof(SpkPanel) * (ystride / 32) + (rows ? 128 * (ystride / 32) : 0) + 16 +
+           sizeof(int) * ystride;
 }
 
 struct SrcScaled {  // (float)(v[row] * scale): v_j = w * (1/h) (gmres.hpp:72-73)
@@ -209,6 +211,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_arnoldi_cycle(FusedArgs a) {
     float* ybuf;
     SpkPanel* dsh;
     uint16_t* msh;
+    spk::BlockCache* bcache;
     {
         unsigned char* base = reinterpret_cast<unsigned char*>(mrp + ((a.slice + 2) & ~1) + 2);
         base = reinterpret_cast<unsigned char*>(((uintptr_t)base + 15) & ~(uintptr_t)15);
@@ -217,6 +220,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_arnoldi_cycle(FusedArgs a) {
         dsh = reinterpret_cast<SpkPanel*>(base + per * wid + sizeof(float) * a.ystride);
         msh = reinterpret_cast<uint16_t*>(base + per * wid + sizeof(float) * a.ystride +
                                           sizeof(SpkPanel) * (a.ystride / 32));
+        bcache = reinterpret_cast<spk::BlockCache*>(base + per * wid + sizeof(float) * a.ystride +
+                                                    sizeof(SpkPanel) * (a.ystride / 32) +
+                                                    (ROWS ? 128 * (a.ystride / 32) : 0));
     }
     // the CTA's rows of the (permuted) matrix stay in shared memory for the cycle
     const int nrows = max(0, min(len, a.n - r0));
@@ -236,7 +242,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_arnoldi_cycle(FusedArgs a) {
     // apply's blocks — and their factor traffic — spread over every SM
     // instead of filling the first CTAs' warps (per-SM bandwidth bound)
     const int gw = wid * G + blockIdx.x;  // 0: the Givens warp (CTA 0, warp 0)
-    const int naw = G * kWarps - 1;
+    const int naw = G * kWarps - 1;       // >= number of blocks (plan_fused): one block per apply warp
+    if (gw != 0 && gw - 1 < a.pc.s) spk::spk_cache_block<ROWS>(a.pc, gw - 1, dsh, msh, bcache, lane);
     const double bdf = st->breakdown_factor;
     const double* asrc = V;  // v_0 (k_cycle_init)
     double ascale = 1.0;
@@ -255,11 +262,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_arnoldi_cycle(FusedArgs a) {
             if (pending) givens_step(a, gs, hsh, j - 1, hnext, pre_norm, false, lane);
         } else {
             const int aw = gw - 1;
-            if (aw < a.pc.s) spk::prefetch_block_head<uint16_t>(a.pc, aw, lane);
-            for (int b = aw; b < a.pc.s; b += naw)
-                spk::spk_solve_block<float, uint16_t, false, ROWS>(a.pc, b, b + naw < a.pc.s ? b + naw : -1,
-                                                                  SrcScaled{asrc, ascale}, DstZ{a.z32}, ybuf, dsh,
-                                                                  lane, nullptr, msh);
+            if (aw < a.pc.s)
+                spk::spk_solve_block<float, uint16_t, false, ROWS, true>(a.pc, aw, -1, SrcScaled{asrc, ascale},
+                                                                        DstZ{a.z32}, ybuf, dsh, lane, nullptr, msh,
+                                                                        bcache);
         }
         grid_barrier(a.gb);
         if (pending && *(volatile int*)&st->done) break;  // converged at step j-1
@@ -449,6 +455,7 @@ FusedPlan plan_fused(int n, int s, int dmax, int num_sms, int m, bool has_long, 
     const int ystride = ((dmax + 31) / 32) * 32;
     // every SM: the apply phase is latency bound, more warps in flight win
     const int grid = std::max(1, std::min(num_sms, npad / 64));
+    if (s > grid * kWarps - 1) return F;  // one block per apply warp (the block cache)
     int slice = (npad + grid - 1) / grid;
     slice = (slice + 1) & ~1;
     int nnz_cap = 0;  // largest matrix slice

@@ -99,7 +99,7 @@ __device__ void pack_row_quads(const SpkBuild& p, const float* F, int dq, int k,
 
 // Pass 1 (count) / pass 2 (pack); warp per panel, lane = panel row.
 template <bool PACK, class IdxT, bool ROWS = false>
-__global__ void k_spk_build(SpkBuild p) {
+__global__ void __launch_bounds__(PACK ? 128 : 256, PACK ? 3 : 1) k_spk_build(SpkBuild p) {
     extern __shared__ double inv_smem[];
     const int lane = threadIdx.x & 31;
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -166,61 +166,84 @@ __global__ void k_spk_build(SpkBuild p) {
         // entries right of it), so the apply does them as one mat-vec.
         const bool last = 32 * (t + 1) >= d;
         {
-            double* Tt = inv_smem + (size_t)(threadIdx.x >> 5) * (2 * 32 * 33);
-            double* X = Tt + 32 * 33;
+            // tile (FP32 factor values, exact in FP64) and a transpose buffer
+            // in shared memory; the column of the inverse a lane computes
+            // stays in registers (fully unrolled substitutions)
+            float* Tt = reinterpret_cast<float*>(inv_smem) + (size_t)(threadIdx.x >> 5) * (2 * 32 * 33);
+            float* W = Tt + 32 * 33;
             for (int c = 0; c < 32; ++c) {
                 const int cc = c0 + c;
-                double v;
-                if (k < d && cc < c1) v = (double)dense_at(F, dq, k, cc);
-                else v = (c == lane) ? 1.0 : 0.0;  // padded rows/columns: identity
+                float v;
+                if (k < d && cc < c1) v = dense_at(F, dq, k, cc);
+                else v = (c == lane) ? 1.0f : 0.0f;  // padded rows/columns: identity
                 Tt[lane * 33 + c] = v;
             }
             __syncwarp();
             // lane = column c of the inverses
             const int c = lane;
+            double x[32];
+#pragma unroll
             for (int i = 0; i < 32; ++i) {  // L x = e_c, unit lower
                 double sum = (i == c) ? 1.0 : 0.0;
-                for (int j = 0; j < i; ++j) sum -= Tt[i * 33 + j] * X[j * 33 + c];
-                X[i * 33 + c] = (i < c) ? 0.0 : sum;
+#pragma unroll
+                for (int j = 0; j < i; ++j) sum -= (double)Tt[i * 33 + j] * x[j];
+                x[i] = (i < c) ? 0.0 : sum;
             }
-            __syncwarp();
-            float linv[32];
-            for (int j = 0; j < 32; ++j) linv[j] = (float)X[lane * 33 + j];  // row `lane` of Linv
-            __syncwarp();
-            // U x = e_c (Uinv, upper with diagonal); last panel: U x = Linv e_c
-            // in place (X = Uinv Linv = (L U)^-1 of the diagonal tile)
-            for (int i = 31; i >= 0; --i) {
-                double sum = last ? X[i * 33 + c] : ((i == c) ? 1.0 : 0.0);
-                for (int j = i + 1; j < 32; ++j) sum -= Tt[i * 33 + j] * X[j * 33 + c];
-                X[i * 33 + c] = (!last && i > c) ? 0.0 : sum / Tt[i * 33 + i];
-            }
-            __syncwarp();
             float4* tile = reinterpret_cast<float4*>(p.dtile + (size_t)P * kTileFloats);
             const int qd = lane >> 2;  // the quad holding the diagonal
+            if (!last) {  // quads 0..qd of row `lane`: strictly lower Linv (through the transpose buffer)
+#pragma unroll
+                for (int i = 0; i < 32; ++i) W[i * 33 + c] = (float)x[i];
+                __syncwarp();
+                for (int q = 0; q <= qd; ++q) {
+                    float4 v4;
+                    float* w4 = &v4.x;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int j = 4 * q + u;
+                        w4[u] = (j < lane) ? W[lane * 33 + j] : 0.0f;
+                    }
+                    tile[q * 32 + lane] = v4;
+                }
+                __syncwarp();
+            }
+            // U x = e_c (Uinv, upper with diagonal); last panel: U x = Linv e_c
+            // in place (x = Uinv Linv = (L U)^-1 of the diagonal tile)
+#pragma unroll
+            for (int i = 31; i >= 0; --i) {
+                double sum = last ? x[i] : ((i == c) ? 1.0 : 0.0);
+#pragma unroll
+                for (int j = i + 1; j < 32; ++j) sum -= (double)Tt[i * 33 + j] * x[j];
+                x[i] = (!last && i > c) ? 0.0 : sum / (double)Tt[i * 33 + i];
+            }
+#pragma unroll
+            for (int i = 0; i < 32; ++i) W[i * 33 + c] = (float)x[i];  // row `lane`: W[lane * 33 + j]
+            __syncwarp();
             if (last) {  // row `lane` of Uinv Linv
                 for (int q = 0; q < 9; ++q) {
                     float4 v4 = make_float4(0.f, 0.f, 0.f, 0.f);
-                    if (q < 8) v4 = make_float4((float)X[lane * 33 + 4 * q], (float)X[lane * 33 + 4 * q + 1],
-                                                (float)X[lane * 33 + 4 * q + 2], (float)X[lane * 33 + 4 * q + 3]);
+                    if (q < 8) v4 = make_float4(W[lane * 33 + 4 * q], W[lane * 33 + 4 * q + 1], W[lane * 33 + 4 * q + 2],
+                                                W[lane * 33 + 4 * q + 3]);
                     tile[q * 32 + lane] = v4;
                 }
-            } else {
-                for (int q = 0; q < 9; ++q) {
+            } else {  // quads qd+1..7 and quad 8 (the diagonal quad's part) of row `lane`: upper Uinv
+                for (int q = qd + 1; q < 10; ++q) {
+                    const int qq = q == 9 ? qd : q;
+                    if (q == 8) continue;
                     float4 v4;
                     float* w4 = &v4.x;
+#pragma unroll
                     for (int u = 0; u < 4; ++u) {
-                        const int j = 4 * (q < 8 ? q : qd) + u;
-                        const float lo = (j < lane) ? linv[j] : 0.0f;                   // strictly lower Linv
-                        const float up = (j >= lane) ? (float)X[lane * 33 + j] : 0.0f;  // upper Uinv
-                        w4[u] = (q == 8) ? up : (q < qd ? lo : (q > qd ? up : lo));
+                        const int j = 4 * qq + u;
+                        w4[u] = (j >= lane) ? W[lane * 33 + j] : 0.0f;
                     }
-                    tile[q * 32 + lane] = v4;
+                    tile[(q == 9 ? 8 : q) * 32 + lane] = v4;
                 }
             }
             __syncwarp();
         }
         if (ROWS) {
-            int* S = reinterpret_cast<int*>(inv_smem + (size_t)(threadIdx.x >> 5) * (2 * 32 * 33));
+            int* S = reinterpret_cast<int*>(inv_smem) + (size_t)(threadIdx.x >> 5) * (2 * 32 * 33);
             pack_row_quads<IdxT>(p, F, dq, k, k < d, 0, c0, ql, rl, mql, base, S, lane);
             pack_row_quads<IdxT>(p, F, dq, k, k < d, c1, d, qu, ru, mqu, base + 4 * sl, S, lane);
             continue;
@@ -320,7 +343,7 @@ void launch_spk_count(const SpkBuild& p, cudaStream_t st, int64_t* launches) {
 
 void launch_spk_pack(const SpkBuild& p, cudaStream_t st, int64_t* launches) {
     const int grid = std::max(1, std::min((p.num_panels * 32 + 127) / 128, 148 * 16));
-    const int smem = 4 * 2 * 32 * 33 * sizeof(double);
+    const int smem = 4 * 2 * 32 * 33 * sizeof(float);
     auto fn = p.rows ? (p.idx32 ? k_spk_build<true, uint32_t, true> : k_spk_build<true, uint16_t, true>)
                      : (p.idx32 ? k_spk_build<true, uint32_t> : k_spk_build<true, uint16_t>);
     HPBJ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));

@@ -270,24 +270,58 @@ __device__ __forceinline__ void prefetch_block_head(const SpkView& p, int b, int
 // their latency overlaps the off-panel fold.
 // ROWS: off-panel parts in the row-quad layout (fold_rows); msh (uint16
 // [64 T] of the warp's shared memory) receives the block's row metadata.
-template <class Acc, class IdxT, bool STAGE = false, bool ROWS = false, class Src, class Dst>
-__device__ __forceinline__ void spk_solve_block(const SpkView& p, int b, int next_b, Src src, Dst dst, Acc* ybuf,
-                                                SpkPanel* dsh, int lane, float4* tbuf = nullptr,
-                                                uint16_t* msh = nullptr) {
-    constexpr int kQMask = (1 << kRowQuadBits) - 1;
-    const IdxT* eidx = reinterpret_cast<const IdxT*>(p.eidx);
-    const int o = p.bstart[b];
-    const int d = p.bstart[b + 1] - o;
+// CACHED: a warp that applies the same block every step (fused cycle
+// kernel) keeps the block's header, descriptors, row metadata and pivots in
+// its shared memory (spk_cache_block): two dependent global loads less.
+struct BlockCache {
+    int4 hdr;  // o, d, T, P0
+    int piv[1];  // d entries (the warp's buffer is sized for dmax)
+};
+
+template <bool ROWS>
+__device__ __forceinline__ void spk_cache_block(const SpkView& p, int b, SpkPanel* dsh, uint16_t* msh, BlockCache* bc,
+                                                int lane) {
+    const int o = p.bstart[b], d = p.bstart[b + 1] - o, P0 = p.pstart[b];
     const int T = (d + 31) >> 5;
-    const int P0 = p.pstart[b];
-    const int qd = lane >> 2;
     if (lane < T) dsh[lane] = p.desc[P0 + lane];
     if (ROWS) {
         const uint32_t* m32 = reinterpret_cast<const uint32_t*>(p.rmeta + (size_t)P0 * 64);
         uint32_t* s32 = reinterpret_cast<uint32_t*>(msh);
         for (int t = 0; t < T; ++t) s32[t * 32 + lane] = __ldg(m32 + t * 32 + lane);
     }
+    for (int k = lane; k < d; k += 32) bc->piv[k] = __ldg(p.piv + o + k);
+    if (lane == 0) bc->hdr = make_int4(o, d, T, P0);
     __syncwarp();
+}
+
+template <class Acc, class IdxT, bool STAGE = false, bool ROWS = false, bool CACHED = false, class Src, class Dst>
+__device__ __forceinline__ void spk_solve_block(const SpkView& p, int b, int next_b, Src src, Dst dst, Acc* ybuf,
+                                                SpkPanel* dsh, int lane, float4* tbuf = nullptr,
+                                                uint16_t* msh = nullptr, const BlockCache* bc = nullptr) {
+    constexpr int kQMask = (1 << kRowQuadBits) - 1;
+    const IdxT* eidx = reinterpret_cast<const IdxT*>(p.eidx);
+    int o, d, P0;
+    if (CACHED) {  // header, descriptors, metadata and pivots already on chip
+        const int4 h = bc->hdr;
+        o = h.x;
+        d = h.y;
+        P0 = h.w;
+    } else {
+        o = p.bstart[b];
+        d = p.bstart[b + 1] - o;
+        P0 = p.pstart[b];
+    }
+    const int T = (d + 31) >> 5;
+    const int qd = lane >> 2;
+    if (!CACHED) {
+        if (lane < T) dsh[lane] = p.desc[P0 + lane];
+        if (ROWS) {
+            const uint32_t* m32 = reinterpret_cast<const uint32_t*>(p.rmeta + (size_t)P0 * 64);
+            uint32_t* s32 = reinterpret_cast<uint32_t*>(msh);
+            for (int t = 0; t < T; ++t) s32[t * 32 + lane] = __ldg(m32 + t * 32 + lane);
+        }
+        __syncwarp();
+    }
     // rhs[pivot_rows[k]] for the whole block: all pivot loads first, then
     // all gathers (two latency rounds, not 2T)
     {
@@ -295,14 +329,14 @@ __device__ __forceinline__ void spk_solve_block(const SpkView& p, int b, int nex
 #pragma unroll
         for (int t = 0; t < kMaxPanels; ++t) {
             const int k = 32 * t + lane;
-            pv[t] = (t < T && k < d) ? __ldg(p.piv + o + k) : -1;
+            pv[t] = (t < T && k < d) ? (CACHED ? bc->piv[k] : __ldg(p.piv + o + k)) : -1;
         }
 #pragma unroll
         for (int t = 0; t < kMaxPanels; ++t)
             if (t < T) ybuf[32 * t + lane] = pv[t] >= 0 ? (Acc)src(o + pv[t]) : (Acc)0;
         for (int t = kMaxPanels; t < T; ++t) {
             const int k = 32 * t + lane;
-            ybuf[k] = (k < d) ? (Acc)src(o + __ldg(p.piv + o + k)) : (Acc)0;
+            ybuf[k] = (k < d) ? (Acc)src(o + (CACHED ? bc->piv[k] : __ldg(p.piv + o + k))) : (Acc)0;
         }
     }
     __syncwarp();
