@@ -22,6 +22,7 @@
 // kernels.cuh panel_floats) for the coalesced apply kernel; pivot_rows.
 
 #include <cfloat>
+#include <cstdlib>
 
 #include "device.cuh"
 #include "kernels.cuh"
@@ -375,6 +376,181 @@ __global__ void __launch_bounds__(256) k_block_lu_warp(LuParams p, int dw, int l
             for (int k = lane; k < d; k += 32) p.piv[o + k] = prow[k];
         }
         __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Two warps per block (d <= kWarpLuMax): the same elimination as
+// k_block_lu_warp with the rows split between the warps (warp w owns rows
+// lane + 32 (2q + w)), so each warp walks half of the live rows per column;
+// the per-warp pivot candidates meet in shared memory behind one 64-thread
+// barrier per column (double-buffered slots). Twice the resident warps per
+// block's shared-memory tile and half the per-column chain: same pivots,
+// same FMA sequence per element, bit-identical factors.
+template <int C>  // column groups: d <= 32 C
+__global__ void __launch_bounds__(64) k_block_lu_pair(LuParams p, int dw, int ldw) {
+    extern __shared__ float wsm[];
+    __shared__ unsigned sk[2][2];
+    __shared__ int sr[2][2];
+    __shared__ float sv[2][2];  // the candidates' values (read before the owner overwrites the pivot)
+    __shared__ double snrm[2];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, tid = threadIdx.x;
+    float* A = wsm;
+    int* prow = reinterpret_cast<int*>(A + dw * ldw);
+    constexpr int R = 2;  // rows per lane and warp: lane + 32 (2q + w), q < 2 (d <= 128)
+    for (int b = blockIdx.x; b < p.s; b += gridDim.x) {
+        const int o = p.bstart[b];
+        const int d = p.bstart[b + 1] - o;
+        if (d > dw) continue;
+        const int ld = d | 1;
+        for (int e = tid; e < d * ld; e += 64) A[e] = 0.0f;
+        __syncthreads();
+        // gather + FP64 inf-norm (row sums sequential in column order)
+        double nrm = 0.0;
+        for (int r = tid; r < d; r += 64) {
+            const int kb = __ldg(p.a.rp + o + r), ke = __ldg(p.a.rp + o + r + 1);
+            double rs = 0.0;
+            for (int k = kb; k < ke; ++k) {
+                const int c = __ldg(p.a.ci + k) - o;
+                if (c >= 0 && c < d) {
+                    const double v = __ldg(p.a.val + k);
+                    A[r * ld + c] = __double2float_rn(v);
+                    rs = __dadd_rn(rs, fabs(v));
+                }
+            }
+            nrm = fmax(nrm, rs);
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) nrm = fmax(nrm, __shfl_xor_sync(0xffffffffu, nrm, off));
+        if (lane == 0) snrm[w] = nrm;
+        __syncthreads();
+        nrm = fmax(snrm[0], snrm[1]);
+        unsigned pivoted = 0u;  // bit q: row lane + 32 (2q + w) already pivotal
+        int nperturb = 0;
+        bool abort = false;
+        for (int k = 0; k < d; ++k) {
+            const int par = k & 1;
+            unsigned bk = 0u;
+            int brow = 0x7fffffff;
+#pragma unroll
+            for (int q = 0; q < R; ++q) {
+                const int r = lane + 32 * (2 * q + w);
+                if (r < d && !((pivoted >> q) & 1u)) {
+                    const unsigned key = __float_as_uint(fabsf(A[r * ld + k])) + 1u;
+                    if (key > bk) {  // rows ascend with q: an equal key keeps the smaller row
+                        bk = key;
+                        brow = r;
+                    }
+                }
+            }
+            unsigned kmx;
+            const int prw = warp_pivot_row(bk, brow, &kmx);
+            const float xw = (kmx != 0u) ? A[prw * ld + k] : 0.0f;
+            if (lane == 0) {
+                sk[par][w] = kmx;
+                sr[par][w] = prw;
+                sv[par][w] = xw;
+            }
+            __syncthreads();
+            const unsigned k0 = sk[par][0], k1 = sk[par][1];
+            const int r0 = sr[par][0], r1 = sr[par][1];
+            const bool first = k0 > k1 || (k0 == k1 && r0 < r1);  // max key, ties -> smaller row
+            const int pr = first ? r0 : r1;
+            const float xp = first ? sv[par][0] : sv[par][1];
+            const double pvd = (double)xp;
+            const bool keep = pivot_keep(pvd, nrm, p.eps);
+            const double val = keep ? pvd : ((pvd < 0.0 ? -1.0 : 1.0) * p.eps * nrm);
+            if (val == 0.0) {
+                if (tid == 0) atomicMin(p.singular, ((unsigned long long)b << 32) | (unsigned)k);
+                abort = true;
+                break;
+            }
+            if (!keep) {
+                ++nperturb;
+                if (tid == 0) {
+                    const int slot = atomicAdd(p.pert_n, 1);
+                    if (slot < p.pert_cap) p.pert[slot] = PertRecord{b, k, pvd, val};
+                }
+            }
+            const float pv = (float)val;
+            const bool own = ((pr >> 5) & 1) == w;  // warp owning the pivot row
+            __syncwarp();
+            if (own && lane == (pr & 31)) {
+                A[pr * ld + k] = pv;
+                pivoted |= 1u << (pr >> 6);
+                prow[k] = pr;
+            }
+            __syncwarp();
+            const float* urow = A + pr * ld;
+            float lq[R];
+#pragma unroll
+            for (int q = 0; q < R; ++q) {
+                const int r = lane + 32 * (2 * q + w);
+                lq[q] = 0.0f;
+                if (r < d && !((pivoted >> q) & 1u)) {
+                    lq[q] = A[r * ld + k] / pv;  // L(i,k) = x_i / pivot (lu.cpp:207)
+                    A[r * ld + k] = lq[q];
+                }
+            }
+            unsigned lmask[R];
+#pragma unroll
+            for (int q = 0; q < R; ++q) lmask[q] = __ballot_sync(0xffffffffu, lq[q] != 0.0f);
+            float ucol[C];
+            bool cj[C];
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                const int j = k + 1 + lane + 32 * c;
+                cj[c] = j < d;
+                ucol[c] = cj[c] ? urow[j] : 0.0f;
+            }
+            float* Aj = A + k + 1 + lane;
+#pragma unroll
+            for (int q = 0; q < R; ++q) {
+                unsigned m = lmask[q];
+                const int rbase = 32 * (2 * q + w);
+                while (m) {
+                    int rr[4];
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        rr[t] = m ? rbase + __ffs(m) - 1 : -1;
+                        if (m) m &= m - 1;
+                    }
+                    float l[4], a[4][C];
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        l[t] = rr[t] >= 0 ? A[rr[t] * ld + k] : 0.0f;
+#pragma unroll
+                        for (int c = 0; c < C; ++c) a[t][c] = (rr[t] >= 0 && cj[c]) ? Aj[rr[t] * ld + 32 * c] : 0.0f;
+                    }
+#pragma unroll
+                    for (int t = 0; t < 4; ++t)
+#pragma unroll
+                        for (int c = 0; c < C; ++c)
+                            if (rr[t] >= 0 && cj[c]) Aj[rr[t] * ld + 32 * c] = fmaf(-l[t], ucol[c], a[t][c]);
+                }
+            }
+        }
+        __syncthreads();
+        if (tid == 0) p.pert_count[b] = nperturb;
+        if (!abort) {
+            const int T = (d + 31) / 32;
+            const int dp4 = (d + 3) & ~3;
+            float* F = p.fac + p.fac_off[b];
+            for (int t = w; t < T; t += 2) {  // panel t: rem = (c >> 2) * 128 + (k & 31) * 4 + (c & 3)
+                float* Ft = F + (size_t)t * 32 * dp4;
+                const int k = 32 * t + (lane >> 2);
+                for (int rem = lane; rem < 32 * dp4; rem += 32) {
+                    const int c = ((rem >> 7) << 2) | (rem & 3);
+                    const int kk = k + (((rem >> 5) & 3) << 3);
+                    float v;
+                    if (kk < d && c < d) v = A[prow[kk] * ld + c];
+                    else v = (kk == c) ? 1.0f : 0.0f;
+                    Ft[rem] = v;
+                }
+            }
+            for (int k = tid; k < d; k += 64) p.piv[o + k] = prow[k];
+        }
+        __syncthreads();
     }
 }
 
@@ -737,23 +913,37 @@ void launch_block_lu(const LuParams& p_in, int dmax, int num_sms, cudaStream_t s
     p.warp_dim = dw;
     {
         const int ldw = dw | 1;
-        const size_t per_warp = ((size_t)dw * ldw + dw) * sizeof(float);
-        // few warps per CTA so several CTAs share an SM's shared memory
-        const int wpc = (int)std::max<size_t>(1, std::min<size_t>(2, (200 * 1024) / per_warp));
-        const size_t smem = per_warp * wpc;
-        void (*fn)(LuParams, int, int) = nullptr;
-        switch ((dw + 31) / 32) {
-            case 1: fn = k_block_lu_warp<1>; break;
-            case 2: fn = k_block_lu_warp<2>; break;
-            case 3: fn = k_block_lu_warp<3>; break;
-            default: fn = k_block_lu_warp<3>; break;
+        const size_t per_block = ((size_t)dw * ldw + dw) * sizeof(float);
+        const char* e = getenv("HPBJ_LU_WARP");
+        if (e && e[0] == '1') {  // one warp per block (k_block_lu_warp)
+            const int wpc = (int)std::max<size_t>(1, std::min<size_t>(2, (200 * 1024) / per_block));
+            const size_t smem = per_block * wpc;
+            void (*fn)(LuParams, int, int) = nullptr;
+            switch ((dw + 31) / 32) {
+                case 1: fn = k_block_lu_warp<1>; break;
+                case 2: fn = k_block_lu_warp<2>; break;
+                default: fn = k_block_lu_warp<3>; break;
+            }
+            HPBJ_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            int occ = 0;
+            HPBJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 32 * wpc, smem));
+            occ = std::max(occ, 1);
+            const int grid = std::max(1, std::min((p.s + wpc - 1) / wpc, num_sms * occ));
+            fn<<<grid, 32 * wpc, smem, st>>>(p, dw, ldw);
+        } else {  // two warps per block (k_block_lu_pair)
+            void (*fn)(LuParams, int, int) = nullptr;
+            switch ((dw + 31) / 32) {
+                case 1: fn = k_block_lu_pair<1>; break;
+                case 2: fn = k_block_lu_pair<2>; break;
+                default: fn = k_block_lu_pair<3>; break;
+            }
+            HPBJ_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)per_block));
+            int occ = 0;
+            HPBJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 64, per_block));
+            occ = std::max(occ, 1);
+            const int grid = std::max(1, std::min(p.s, num_sms * occ));
+            fn<<<grid, 64, per_block, st>>>(p, dw, ldw);
         }
-        HPBJ_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        int occ = 0;
-        HPBJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 32 * wpc, smem));
-        occ = std::max(occ, 1);
-        const int grid = std::max(1, std::min((p.s + wpc - 1) / wpc, num_sms * occ));
-        fn<<<grid, 32 * wpc, smem, st>>>(p, dw, ldw);
         *launches += 1;
     }
     if (dmax <= dw) {

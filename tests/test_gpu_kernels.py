@@ -93,6 +93,25 @@ def test_block_factors_match_reference(ref, config):
     assert worst <= 1e-5, worst
 
 
+@pytest.mark.parametrize("config", [0, 1])
+def test_lu_pair_and_warp_kernels_bit_identical(config, monkeypatch):
+    """k_block_lu_pair (two warps per block, default) and k_block_lu_warp
+    (HPBJ_LU_WARP=1) make the same pivots and the same FMA sequence per
+    element: factors and pivot rows bit-identical."""
+    s = generate(config)
+    a = _sys_matrix(s)
+    part = hp.partition_graph(a, s.num_blocks, 0.1)
+    out = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("HPBJ_LU_WARP", flag)
+        p = hp.Preconditioner.block_jacobi(a, part)
+        blocks = range(0, s.num_blocks, max(1, s.num_blocks // 40))
+        out.append([p.block_factors(b) for b in blocks])
+    for (f0, p0), (f1, p1) in zip(*out):
+        assert np.array_equal(p0, p1)
+        assert np.array_equal(f0.view(np.uint32), f1.view(np.uint32))
+
+
 def test_block_factors_config2_sample(ref):
     s = generate(2)
     part = hp.partition_graph(_sys_matrix(s), s.num_blocks, 0.1)
@@ -197,6 +216,25 @@ def test_apply_matches_reference(ref, config):
     zd = ref.apply(s.row_ptr, s.col, s.val, s.num_blocks, asg, v, fp32=False)
     assert np.linalg.norm(z - zr) <= 2e-6 * np.linalg.norm(zr)
     assert np.linalg.norm(z - zd) <= 1e-5 * np.linalg.norm(zd)
+
+
+@pytest.mark.parametrize("layout", ["0", "1"])
+@pytest.mark.parametrize("config", [0, 2])
+def test_apply_both_offpanel_layouts(ref, config, layout, monkeypatch):
+    """Row-sorted runs (HPBJ_SPK_ROWS=0) and row quads (=1) are two storage
+    layouts of the same factors: both match the reference FP32 apply, also
+    across the merged last panel ((L U)^-1 tile) and blocks of 1-5 panels."""
+    monkeypatch.setenv("HPBJ_SPK_ROWS", layout)
+    s = generate(config)
+    a = _sys_matrix(s)
+    part = hp.partition_graph(a, s.num_blocks, 0.1)  # bit-identical to the reference's (test_partition.py)
+    asg = part.assignment
+    p = hp.Preconditioner.block_jacobi(a, part)
+    v = np.random.default_rng(11).uniform(-1, 1, s.n)
+    z = p.apply(v)
+    zr = ref.apply(s.row_ptr, s.col, s.val, s.num_blocks, asg, v, fp32=True)
+    assert np.linalg.norm(z - zr) <= 2e-6 * np.linalg.norm(zr)
+    assert np.array_equal(z, p.apply(v))
 
 
 def test_apply_deterministic():
