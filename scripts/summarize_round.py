@@ -77,6 +77,8 @@ for cfg, t in traffic.items():
     path = f"{OUT}/ncu_traffic_config{c}.json"
     old = json.load(open(path)) if os.path.exists(path) else {}
     old.update(t)
+    if "arnoldi_cycle_fused" in t:  # the capture is the first launch: one full cycle of m steps (config 1: m = 50)
+        old.setdefault("arnoldi_cycle_fused_steps", 50)
     old["_note"] = (f"dram__bytes_read.sum + dram__bytes_write.sum per launch, ncu --set full ({RND}); "
                     "arnoldi_cycle_fused: one launch = one restart cycle (the first, m steps)")
     json.dump(old, open(path, "w"), indent=1)
