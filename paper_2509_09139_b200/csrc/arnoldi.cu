@@ -392,7 +392,9 @@ __global__ void __launch_bounds__(kIcwyThreads, 1) k_icwy(OrthArgs a) {
 
     // ---- pass B: w -= sum_i h_i v_i in MGS order; ||w||^2
     double ss2 = 0.0;
-    for (int e = tid; e < nv2; e += kIcwyThreads) {
+    // rows in reverse: pass A streamed the rows ascending, so the highest rows
+    // of its last batch of vectors are the ones still in L2
+    for (int e = nv2 - 1 - tid; e >= 0; e -= kIcwyThreads) {
         double2 wv = w2[e];
         for (int i = 0; i <= j; ++i) {
             const double2 vv = __ldg(reinterpret_cast<const double2*>(V + (size_t)i * ldv + r0) + e);

@@ -233,6 +233,7 @@ struct hpbj_ctx {
     unsigned long long* d_spk_totals = nullptr;
     uint16_t* d_rmeta = nullptr;
     int spk_rows = 0;            // off-panel layout: 0 row-sorted runs, 1 row quads (spk.cu)
+    double spk_tile_bytes = 0;   // inverse-tile bytes one apply reads (all panels)
     SpmvPlan planB;
     int* d_long_sort = nullptr;
     int n_long_sort = 0, max_long_sort = 0;
@@ -493,6 +494,15 @@ void build_spk(hpbj_ctx* c) {
     p.idx32 = idx32 ? 1 : 0;
     p.rows = c->spk_rows;
     p.rmeta = c->d_rmeta;
+    // tile bytes an apply reads: a full panel 2 x 144 quads (lane l: quads
+    // 0..l/4 forward, l/4..7 backward), a block's last panel of r rows its
+    // (L U)^-1 rows: r x ceil(r / 4) quads
+    c->spk_tile_bytes = 0;
+    for (int64_t b = 0; b < c->s; ++b) {
+        const int d = c->h_bstart[b + 1] - c->h_bstart[b];
+        const int T = (d + 31) / 32, r = d - 32 * (T - 1);
+        c->spk_tile_bytes += 16.0 * (288.0 * (T - 1) + (double)r * ((r + 3) / 4));
+    }
     launch_spk_pack(p, st, &c->launches);
 }
 
@@ -754,7 +764,7 @@ double apply_bytes(const hpbj_ctx* c) {
     const double n = c->A.n;
     const double idx_b = c->dmax > kIdx16MaxDim ? 4.0 : 2.0;
     return (4.0 + idx_b) * (double)c->spk_entries          // off-panel value + packed index
-           + (4.0 * 1024 + 16.0) * c->num_panels          // inverse-tile quads read + descriptors
+           + c->spk_tile_bytes + 16.0 * c->num_panels     // inverse-tile quads read + descriptors
            + (c->spk_rows ? 128.0 * c->num_panels : 0.0)  // row-quad metadata
            + 4.0 * n                                      // pivot rows (int32)
            + 8.0 * n                                      // v (FP64) in

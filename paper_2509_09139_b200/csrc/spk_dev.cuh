@@ -204,14 +204,16 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // The tile quads a pass reads ([quad][lane] float4, see kernels.cuh): the
 // forward pass quad q for lanes l >= 4q, the backward pass quad q < 8 for
 // lanes l < 4q and all of quad 8. Lanes 8..16 issue one quad each.
-// full: the block's last panel (Uinv Linv, quads 0..7 of every lane).
-__device__ __forceinline__ void prefetch_tile(const SpkView& p, int P, bool fwd, int lane, bool full = false) {
+// full: the block's last panel ((L U)^-1, quads 0..ceil(rows/4)-1 of its
+// first `rows` lanes — the rest is the identity padding, never read).
+__device__ __forceinline__ void prefetch_tile(const SpkView& p, int P, bool fwd, int lane, bool full = false,
+                                              int rows = 32) {
     if (!p.pf) return;
     if (lane >= 8 && lane <= 16) {
         const int q = lane - 8;
         int l0 = 0, l1 = 32;
         if (q == 8) l1 = (fwd || full) ? 0 : 32;
-        else if (full) l0 = 0;
+        else if (full) l1 = 4 * q < rows ? rows : 0;
         else if (fwd) l0 = 4 * q;
         else l1 = 4 * q;
         if (l1 > l0) prefetch_l2(p.dtile + (size_t)P * kTileFloats + q * 128 + l0 * 4, (size_t)16 * (l1 - l0));
@@ -258,7 +260,7 @@ __device__ __forceinline__ void prefetch_block_head(const SpkView& p, int b, int
         else if (lane == 1) prefetch_l2(p.piv + o, sizeof(int) * d);
         else prefetch_entries<IdxT>(p, e0, e1 - e0, lane, 2, 3);
     }
-    prefetch_tile(p, P0, true, lane, p.pstart[b + 1] - P0 == 1);
+    prefetch_tile(p, P0, true, lane, p.pstart[b + 1] - P0 == 1, p.bstart[b + 1] - p.bstart[b]);
 }
 
 // One block's substitution M_b^-1: gather rhs[piv] from src, forward with
@@ -350,7 +352,7 @@ __device__ __forceinline__ void spk_solve_block(const SpkView& p, int b, int nex
         if (!lastp) {
             const int nl1 = dsh[t + 1].nl;
             prefetch_entries<IdxT>(p, dsh[t + 1].off, ROWS ? 4 * (nl1 >> kRowQuadBits) : nl1, lane, 0, 1);
-            prefetch_tile(p, P0 + t + 1, true, lane, t + 2 == T);
+            prefetch_tile(p, P0 + t + 1, true, lane, t + 2 == T, d - 32 * (t + 1));
         } else if (T >= 2) {  // the backward pass starts at panel T-2
             const int nu1 = dsh[T - 2].nu;
             prefetch_entries<IdxT>(p, dsh[T - 2].uoff, ROWS ? 4 * (nu1 >> kRowQuadBits) : nu1, lane, 0, 1);
@@ -362,7 +364,8 @@ __device__ __forceinline__ void spk_solve_block(const SpkView& p, int b, int nex
         if (STAGE) {
 #pragma unroll
             for (int q = 0; q < 8; ++q)
-                if (q <= qd || lastp) cp_async16(tbuf + q * 32 + lane, tile_f + q * 32 + lane);
+                if (lastp ? (32 * t + lane < d && 4 * q < d - 32 * t) : q <= qd)
+                    cp_async16(tbuf + q * 32 + lane, tile_f + q * 32 + lane);
             cp_async_commit();
         }
         if (ROWS)
@@ -376,7 +379,8 @@ __device__ __forceinline__ void spk_solve_block(const SpkView& p, int b, int nex
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
             f4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (q <= qd || lastp) f4[q] = STAGE ? tbuf[q * 32 + lane] : __ldg(tile_f + q * 32 + lane);
+            const bool need = lastp ? (32 * t + lane < d && 4 * q < d - 32 * t) : q <= qd;
+            if (need) f4[q] = STAGE ? tbuf[q * 32 + lane] : __ldg(tile_f + q * 32 + lane);
         }
         const Acc* r = ybuf + 32 * t;
         Acc a0 = lastp ? (Acc)0 : r[lane], a1 = (Acc)0, a2 = (Acc)0, a3 = (Acc)0;
