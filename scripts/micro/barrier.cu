@@ -14,6 +14,7 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
 struct Bar {
     unsigned count, gen, pad[30];
     unsigned group[32 * 32];
+    unsigned flags[1024];
 };
 
 __device__ __forceinline__ unsigned atom_add_acqrel(unsigned* p, unsigned v) {
@@ -27,8 +28,28 @@ __device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
     return v;
 }
 
+// MODE 5: per-CTA arrival flags (no same-address atomics): CTA c stores the
+// epoch to flags[c], warp 0 of CTA 0 polls all flags, then releases gen.
 template <int MODE>
-__device__ __forceinline__ void barrier(Bar* b) {
+__device__ __forceinline__ void barrier(Bar* b, unsigned epoch = 0) {
+    if (MODE == 5) {
+        __syncthreads();
+        if (blockIdx.x == 0) {
+            if (threadIdx.x < 32) {
+                for (int c = 1 + threadIdx.x; c < (int)gridDim.x; c += 32)
+                    while (ld_acquire(&b->flags[c]) != epoch) {
+                    }
+                __syncwarp();
+                if (threadIdx.x == 0) st_release(&b->gen, epoch);
+            }
+        } else if (threadIdx.x == 0) {
+            st_release(&b->flags[blockIdx.x], epoch);
+            while (ld_acquire(&b->gen) != epoch) {
+            }
+        }
+        __syncthreads();
+        return;
+    }
     if (MODE == 4) {  // CUTLASS-style: release/acquire atomics, no full fences
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -78,7 +99,8 @@ __device__ __forceinline__ void barrier(Bar* b) {
 template <int MODE>
 __global__ void __launch_bounds__(1024, 1) k(Bar* b, int iters, unsigned long long* out) {
     const unsigned long long t0 = clock64();
-    for (int i = 0; i < iters; ++i) barrier<MODE>(b);
+    const unsigned base = ld_relaxed(&b->gen);
+    for (int i = 0; i < iters; ++i) barrier<MODE>(b, base + 1 + i);
     if (threadIdx.x == 0 && blockIdx.x == 0) out[0] = clock64() - t0;
 }
 
@@ -119,6 +141,7 @@ int main() {
         run<3>(b, out, grid);
         run<2>(b, out, grid);
         run<4>(b, out, grid);
+        run<5>(b, out, grid);
     }
     return 0;
 }
