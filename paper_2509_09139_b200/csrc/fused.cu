@@ -62,6 +62,7 @@ struct SrcScaled {  // (float)(v[row] * scale): v_j = w * (1/h) (gmres.hpp:72-73
     const double* v;
     double scale;
     __device__ float operator()(int row) const { return __double2float_rn(__ldcg(v + row) * scale); }
+    __device__ void prefetch(int, int) const {}
 };
 struct DstZ {
     float* z;

@@ -15,15 +15,24 @@ namespace spk {
 constexpr int kMaxPanels = 9;  // pivots of up to 288 rows gathered with full ILP
 
 // ----------------------------------------------------------------------------
+// L2 bulk prefetch of the 8-byte rows [o, o + d) of v (a block's source rows:
+// pivoting permutes only within the block).
+__device__ __forceinline__ void prefetch_rows_l2(const double* v, int o, int d) {
+    const uintptr_t a = (uintptr_t)(v + o) & ~(uintptr_t)15;
+    const uintptr_t e = ((uintptr_t)(v + o + d) + 15) & ~(uintptr_t)15;
+    if (e > a) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((unsigned)(e - a)) : "memory");
+}
 struct SrcDown {  // (float) V[:, st->j][row]  (Arnoldi step)
     const double* V;
     int ldv;
     const SolveState* sst;
     __device__ float operator()(int row) const { return __double2float_rn(__ldg(V + (size_t)sst->j * ldv + row)); }
+    __device__ void prefetch(int o, int d) const { prefetch_rows_l2(V + (size_t)sst->j * ldv, o, d); }
 };
 struct SrcVec {  // (float) v[row]
     const double* v;
     __device__ float operator()(int row) const { return __double2float_rn(__ldg(v + row)); }
+    __device__ void prefetch(int o, int d) const { prefetch_rows_l2(v, o, d); }
 };
 struct SrcBasis {  // sum_i y_i V[i][row], i ascending (gmres.cpp:152-157), FP64
     const double* V;
@@ -36,6 +45,7 @@ struct SrcBasis {  // sum_i y_i V[i][row], i ascending (gmres.cpp:152-157), FP64
         for (int i = 0; i < steps; ++i) u = fma(y[i], __ldg(V + (size_t)i * ldv + row), u);
         return u;
     }
+    __device__ void prefetch(int, int) const {}
 };
 struct DstF32 {
     float* z;
@@ -359,6 +369,7 @@ __device__ __forceinline__ void spk_solve_block(const SpkView& p, int b, int nex
             prefetch_tile(p, P0 + T - 2, false, lane);
         } else if (next_b >= 0) {
             prefetch_block_head<IdxT>(p, next_b, lane);
+            if (p.pf && lane == 5) src.prefetch(p.bstart[next_b], p.bstart[next_b + 1] - p.bstart[next_b]);
         }
         const float4* tile_f = reinterpret_cast<const float4*>(p.dtile + (size_t)(P0 + t) * kTileFloats);
         if (STAGE) {
@@ -409,6 +420,7 @@ __device__ __forceinline__ void spk_solve_block(const SpkView& p, int b, int nex
             prefetch_tile(p, P0 + t - 1, false, lane);
         } else if (next_b >= 0) {
             prefetch_block_head<IdxT>(p, next_b, lane);
+            if (p.pf && lane == 5) src.prefetch(p.bstart[next_b], p.bstart[next_b + 1] - p.bstart[next_b]);
         }
         const float4* tile_b = reinterpret_cast<const float4*>(p.dtile + (size_t)(P0 + t) * kTileFloats);
         if (STAGE) {
