@@ -65,11 +65,12 @@ struct OrthArgs {
     int slice;           // rows per CTA (even)
     int npad;            // n rounded up to even (vectors zero padded)
     cudaGraphConditionalHandle cond;  // Arnoldi WHILE node (0: not in a graph)
+    int scr;             // doubles of Givens scratch at the front of the dynamic smem (>= 3m+2, even)
 };
 
 // Shared finish of a step: normalise, Hessenberg column, Givens, exit flags.
-__device__ void finish_step(const OrthArgs& a, double2* w2, int r0, int nv2, int j, double pre_norm,
-                            double hnext, int nthreads) {
+__device__ void finish_step(const OrthArgs& a, double2* w2, double* scratch, int r0, int nv2, int j,
+                            double pre_norm, double hnext, int nthreads) {
     SolveState* st = a.st;
     const int m = a.kb.m;
     const int ldv = a.kb.ldv;
@@ -85,9 +86,9 @@ __device__ void finish_step(const OrthArgs& a, double2* w2, int r0, int nv2, int
         }
     }
     if (blockIdx.x != 0) return;
-    // CTA 0: the w slice is spent, reuse it as scratch for the rotation data
-    // (coalesced staging by warp 0, then one thread rotates out of smem).
-    __syncthreads();
+    // CTA 0: coalesced staging of the rotation data by warp 0 into its own
+    // scratch (3j+2 <= 3m+2 doubles, sized by plan_mgs independently of the
+    // w slice), then one thread rotates out of shared memory.
     if (threadIdx.x >= 32) return;
     const int lane = threadIdx.x;
     double* Hj = a.kb.H + (size_t)j * (m + 1);
@@ -95,7 +96,7 @@ __device__ void finish_step(const OrthArgs& a, double2* w2, int r0, int nv2, int
     double* cs = a.kb.cs;
     double* sn = a.kb.sn;
     double* g = a.kb.g;
-    double* sR = reinterpret_cast<double*>(w2);  // j + 2
+    double* sR = scratch;                        // j + 2
     double* scs = sR + (j + 2);                  // j
     double* ssn = scs + j;                       // j
     for (int i = lane; i <= j; i += 32) sR[i] = __ldcg(Hj + i);
@@ -157,7 +158,8 @@ template <bool SMEM>
 __global__ void __launch_bounds__(kMgsThreads, 1) k_mgs(OrthArgs a) {
     SolveState* st = a.st;
     if (st->done) return;  // uniform: nothing writes done before the final barrier
-    extern __shared__ __align__(16) double wsh[];
+    extern __shared__ __align__(16) double dsm_mgs[];
+    double* wsh = dsm_mgs + a.scr;
     __shared__ double red[2][kMgsThreads / 32];
     __shared__ double bc[2];
 
@@ -262,7 +264,7 @@ __global__ void __launch_bounds__(kMgsThreads, 1) k_mgs(OrthArgs a) {
         }
     }
     reduce2(ss, 0.0, (j + 1) & 1);
-    finish_step(a, w2, r0, nv2, j, pre_norm, sqrt(bc[0]), kMgsThreads);
+    finish_step(a, w2, dsm_mgs, r0, nv2, j, pre_norm, sqrt(bc[0]), kMgsThreads);
 }
 
 // ---------------------------------------------------------------------------
@@ -294,7 +296,7 @@ __global__ void __launch_bounds__(kIcwyThreads, 1) k_icwy(OrthArgs a) {
     const int nval = 2 * (j + 1) + 1;  // c_0..c_j, l_0..l_j, ||w||^2
     double* P = a.kb.partials;         // [value][G]
 
-    double2* w2 = SMEM ? reinterpret_cast<double2*>(dsm) : reinterpret_cast<double2*>(a.kb.w + r0);
+    double2* w2 = SMEM ? reinterpret_cast<double2*>(dsm + a.scr) : reinterpret_cast<double2*>(a.kb.w + r0);
     const double2* vj2 = reinterpret_cast<const double2*>(a.kb.V + (size_t)j * ldv + r0);
     const double2* win = reinterpret_cast<const double2*>(a.kb.w + r0);
     const double* V = a.kb.V;
@@ -421,7 +423,7 @@ __global__ void __launch_bounds__(kIcwyThreads, 1) k_icwy(OrthArgs a) {
         if (lane == 0) wred[0] = t0;
     }
     __syncthreads();
-    finish_step(a, w2, r0, nv2, j, pre_norm, sqrt(wred[0]), kIcwyThreads);
+    finish_step(a, w2, dsm, r0, nv2, j, pre_norm, sqrt(wred[0]), kIcwyThreads);
 }
 
 // v_0 = r0 / beta (element-wise division, gmres.cpp:120-122); cycle state.
@@ -527,17 +529,18 @@ MgsLaunch plan_mgs(int n, int num_sms, int m) {
     slice = (slice + 1) & ~1;
     L.grid = grid;
     L.slice = slice;
-    L.smem = (size_t)slice * sizeof(double);
+    L.scr = (3 * m + 2 + 1) & ~1;  // Givens scratch of finish_step (CTA 0)
+    const size_t scr_bytes = (size_t)L.scr * sizeof(double);
     const size_t static_smem = icwy ? (size_t)(kIcwyWarps * 2 * kBatch + 3 * (kMaxRestart * 2 + 4)) * 8 + 1024
                                     : 2048;
-    L.w_in_smem = L.smem + static_smem <= kSmemMax;
-    if (!L.w_in_smem) L.smem = 0;
+    L.w_in_smem = scr_bytes + (size_t)slice * sizeof(double) + static_smem <= kSmemMax;
+    L.smem = scr_bytes + (L.w_in_smem ? (size_t)slice * sizeof(double) : 0);
     return L;
 }
 
 void launch_mgs(const MgsLaunch& L, const KrylovBufs& kb, double* gram, GridBarrier* gb, SolveState* sst,
                 int n, cudaGraphConditionalHandle cond, cudaStream_t st, int64_t* launches) {
-    OrthArgs a{kb, gram, sst, gb, n, L.slice, (n + 1) & ~1, cond};
+    OrthArgs a{kb, gram, sst, gb, n, L.slice, (n + 1) & ~1, cond, L.scr};
     void (*fn)(OrthArgs);
     if (L.icwy) fn = L.w_in_smem ? k_icwy<true> : k_icwy<false>;
     else fn = L.w_in_smem ? k_mgs<true> : k_mgs<false>;

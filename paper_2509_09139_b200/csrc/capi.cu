@@ -233,6 +233,8 @@ struct hpbj_ctx {
     unsigned long long* d_spk_totals = nullptr;
     uint16_t* d_rmeta = nullptr;
     int spk_rows = 0;            // off-panel layout: 0 row-sorted runs, 1 row quads (spk.cu)
+    int spk_rows_env = -1;       // HPBJ_SPK_ROWS=0|1 (read once at context creation)
+    int apply_pf = 1;            // HPBJ_APPLY_PF=0: no L2 bulk prefetch in the standalone apply
     double spk_tile_bytes = 0;   // inverse-tile bytes one apply reads (all panels)
     SpmvPlan planB;
     int* d_long_sort = nullptr;
@@ -447,8 +449,7 @@ void ensure_ws(hpbj_ctx* c, int m) {
 SpkView spk_view(const hpbj_ctx* c) {
     return SpkView{c->s,      c->dmax,   c->d_bstart, c->d_pstart, c->d_piv, c->d_desc,
                    c->d_dtile, c->d_eval, c->d_eidx,  c->dmax > kIdx16MaxDim ? 1 : 0, c->d_ent_off,
-                   c->spk_rows, c->d_rmeta, c->spk_entries, c->num_panels, (int)c->A.n,
-                   getenv("HPBJ_APPLY_PF") ? (getenv("HPBJ_APPLY_PF")[0] == '1' ? 1 : 0) : 1};
+                   c->spk_rows, c->d_rmeta, c->spk_entries, c->num_panels, (int)c->A.n, c->apply_pf};
 }
 
 // Repack the dense LU panels into the sparse-panel apply format.
@@ -476,8 +477,10 @@ void build_spk(hpbj_ctx* c) {
     unsigned long long totals[2] = {0, 0};
     HPBJ_CUDA(cudaMemcpyAsync(totals, c->d_spk_totals, sizeof(totals), cudaMemcpyDeviceToHost, st));
     HPBJ_CUDA(cudaStreamSynchronize(st));
-    const char* env_rows = getenv("HPBJ_SPK_ROWS");
-    c->spk_rows = env_rows ? (env_rows[0] == '1' ? 1 : 0) : (c->dmax > 96 || 4 * totals[1] <= 5 * totals[0] ? 1 : 0);
+    // Blocks of <= 96 rows run in the fused cycle kernel, which folds
+    // row-sorted runs (row quads pad its short rows by ~46%: apply phase
+    // +11% on config 1); deeper blocks take row quads.
+    c->spk_rows = c->spk_rows_env >= 0 ? c->spk_rows_env : (c->dmax > 96 ? 1 : 0);
     if (totals[c->spk_rows] >= (unsigned long long)INT32_MAX)
         fail(HPBJ_EINVAL, "block_jacobi: factor nonzeros exceed 2^31");
     scan_exclusive(c->spk_rows ? c->d_ent_count_rows : c->d_ent_count, c->d_ent_off, c->num_panels, c->d_scan_tmp, st,
@@ -798,19 +801,25 @@ void ensure_hist(hpbj_ctx* c, int64_t max_restarts) {
     c->hist_cap = need;
 }
 
-void solve(hpbj_ctx* c, const double* d_b, double* d_x, const hpbj_gmres_opts* o, hpbj_report* rep,
-           hpbj_history_point* hist, int64_t hist_cap, double* cycle_res, int64_t cyc_cap) {
-    const auto t0 = std::chrono::steady_clock::now();
+// Config validation (gmres.cpp:203-207), before any workspace is sized.
+hpbj_gmres_opts checked_opts(const hpbj_gmres_opts* o) {
     hpbj_gmres_opts opt;
     hpbj_gmres_default_opts(&opt);
     if (o) opt = *o;
-    if (!c->has_matrix) fail(HPBJ_ELOGIC, "gmres: no matrix");
-    if (c->active == kPcNone || (c->active == kPcBJ && !c->has_pc) || (c->active == kPcIlu && !c->has_ilu))
-        fail(HPBJ_ELOGIC, "gmres: no preconditioner set up");
-    if (opt.restart_m < 1 || opt.tol <= 0.0 || opt.max_restarts < 1)
+    if (opt.restart_m < 1 || !(opt.tol > 0.0) || opt.max_restarts < 1)
         fail(HPBJ_EINVAL, "gmres: invalid config");
     if (opt.restart_m > 1024) fail(HPBJ_EINVAL, "gmres: restart_m > 1024 unsupported");
     if (opt.max_restarts > (int64_t)1 << 24) fail(HPBJ_EINVAL, "gmres: max_restarts too large");
+    return opt;
+}
+
+void solve(hpbj_ctx* c, const double* d_b, double* d_x, const hpbj_gmres_opts* o, hpbj_report* rep,
+           hpbj_history_point* hist, int64_t hist_cap, double* cycle_res, int64_t cyc_cap) {
+    const auto t0 = std::chrono::steady_clock::now();
+    if (!c->has_matrix) fail(HPBJ_ELOGIC, "gmres: no matrix");
+    if (c->active == kPcNone || (c->active == kPcBJ && !c->has_pc) || (c->active == kPcIlu && !c->has_ilu))
+        fail(HPBJ_ELOGIC, "gmres: no preconditioner set up");
+    const hpbj_gmres_opts opt = checked_opts(o);
     const int n = c->A.n;
     const int m = (int)opt.restart_m;
     const double floor_u = opt.floor_roundoff > 0.0 ? opt.floor_roundoff : kU24;
@@ -1003,6 +1012,8 @@ int hpbj_create(hpbj_ctx** out, int device) {
         c->use_fused = !(nf && nf[0] == '0');
         const char* pz = getenv("HPBJ_POISON");
         c->pool.poison = pz && pz[0] == '1';
+        if (const char* e = getenv("HPBJ_SPK_ROWS")) c->spk_rows_env = e[0] == '1' ? 1 : 0;
+        if (const char* e = getenv("HPBJ_APPLY_PF")) c->apply_pf = e[0] == '1' ? 1 : 0;
         *out = c;
     });
 }
@@ -1093,6 +1104,13 @@ int hpbj_update_values(hpbj_ctx* ctx, const double* val) {
         if (!ctx->has_matrix) fail(HPBJ_ELOGIC, "update_values: no matrix");
         HPBJ_CUDA(cudaMemcpyAsync(ctx->A.val, val, sizeof(double) * ctx->A.nnz, cudaMemcpyHostToDevice,
                                   ctx->stream));
+        // The block-Jacobi solve runs in the permuted frame: its SpMV and true
+        // residual read B = Q A Q^T, so B's values follow A now. The factors
+        // stay those of the matrix they were built from (a lagged
+        // preconditioner, as a reference Preconditioner is immutable) until
+        // hpbj_bj_refactor.
+        if (ctx->d_src && ctx->B.val)
+            launch_gather_values(ctx->d_src, ctx->A.val, ctx->B.val, ctx->B.nnz, ctx->stream, &ctx->launches);
         HPBJ_CUDA(cudaStreamSynchronize(ctx->stream));
     });
 }
@@ -1529,9 +1547,7 @@ int hpbj_gmres(hpbj_ctx* ctx, const double* b, double* x, const hpbj_gmres_opts*
     return guard(&ctx->err, [&] {
         if (!ctx->has_matrix) fail(HPBJ_ELOGIC, "gmres: no matrix");
         const int n = ctx->A.n;
-        const int m = opts ? (int)opts->restart_m : 50;
-        if (m >= 1) ensure_ws(ctx, m);
-        else fail(HPBJ_EINVAL, "gmres: invalid config");
+        ensure_ws(ctx, (int)checked_opts(opts).restart_m);
         double* sb = static_cast<double*>(ctx->stage_vec.get(sizeof(double) * 2 * (size_t)n));
         double* sx = sb + n;
 #pragma omp parallel for schedule(static) if (n > 65536)

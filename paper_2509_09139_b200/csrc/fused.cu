@@ -87,7 +87,6 @@ struct FusedArgs {
     int ystride;
     int nnz_cap;               // matrix slice capacity (entries) in shared memory
     unsigned long long* prof;  // optional: CTA 0 phase timers [4], ns
-    int l2_arena;              // prefetch the factor arena into L2 before each apply phase
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -163,8 +162,10 @@ __device__ void givens_step(const FusedArgs& a, GivensSmem& gs, const double* h,
     for (int i = lane; i <= j + 1; i += 32) Rj[i] = gs.R[i];
 }
 
-template <bool ROWS>
+// The apply folds row-sorted off-panel runs (SpkView::rows == 0): the row-quad
+// layout pads the fused configs' short rows by ~46%.
 __global__ void __launch_bounds__(kThreads, 1) k_arnoldi_cycle(FusedArgs a) {
+    constexpr bool ROWS = false;
     SolveState* st = a.st;
     if (*(volatile int*)&st->done) return;  // converged at restart (k_cycle_init)
     extern __shared__ __align__(16) double dsm[];
@@ -400,9 +401,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_arnoldi_cycle(FusedArgs a) {
         }
         ss2 = warp_sum(ss2);
         if (lane == 0) wred[wid] = ss2;
-        // the next step's apply reads the whole factor arena: pull it into L2
-        // now (each CTA its share), overlapping the last barriers of this step
-        if (a.l2_arena && wid == kWarps - 1) spk::prefetch_arena_l2(a.pc, blockIdx.x, G, lane);
         __syncthreads();
         if (tid == 0) {
             double s = 0.0;
@@ -450,7 +448,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_arnoldi_cycle(FusedArgs a) {
 
 FusedPlan plan_fused(int n, int s, int dmax, int num_sms, int m, bool has_long, const int* rowlen, bool rows) {
     FusedPlan F;
-    if (m > kMaxRestart || n <= 0 || dmax > kIdx16MaxDim) return F;
+    if (m > kMaxRestart || n <= 0 || dmax > kIdx16MaxDim || rows) return F;
     if (has_long) return F;  // hub rows: the per-kernel path gives them whole CTAs
     const int npad = (n + 1) & ~1;
     const int ystride = ((dmax + 31) / 32) * 32;
@@ -486,19 +484,14 @@ void launch_arnoldi_cycle(const FusedPlan& F, const SpkView& pc, const DevCsr& a
                           const KrylovBufs& kb, double* gram, SolveState* sst, GridBarrier* gb, float* z32,
                           unsigned long long* prof, cudaStream_t st, int64_t* launches) {
     FusedArgs args{pc, a, plan.group, plan.long_thresh, plan.n_long, plan.long_rows, kb, gram, sst, gb, z32,
-                   a.n, (a.n + 1) & ~1, F.slice, F.ystride, F.nnz_cap, prof, 0};
+                   a.n, (a.n + 1) & ~1, F.slice, F.ystride, F.nnz_cap, prof};
     // The cycle kernel's apply runs from L2 (factors, basis and matrix of
     // the fused configs fit): its chain is latency bound, and the per-step
     // bulk L2 prefetches (a win for the HBM-streaming standalone apply)
     // queue behind each other in the SM's TMA unit: off (config 1: apply
-    // phase 20.2 -> 16.6 us/step). Likewise no arena prefetch.
-    {
-        const char* e = getenv("HPBJ_L2_ARENA");
-        args.l2_arena = e ? (e[0] == '1') : 0;
-        const char* f = getenv("HPBJ_FUSED_PF");
-        args.pc.pf = f ? (f[0] == '1') : 0;
-    }
-    void (*fn)(FusedArgs) = F.rows ? k_arnoldi_cycle<true> : k_arnoldi_cycle<false>;
+    // phase 20.2 -> 16.6 us/step).
+    args.pc.pf = 0;
+    void (*fn)(FusedArgs) = k_arnoldi_cycle;
     HPBJ_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)F.smem));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(F.grid);

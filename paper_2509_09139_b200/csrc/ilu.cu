@@ -73,28 +73,39 @@ __global__ void k_ilu_zero_diag(int n, const int* __restrict__ dpos, const doubl
         if (lu[dpos[i]] == 0.0) atomicMin(first_zero, i);
 }
 
-// 16-byte value + epoch tag, one STG.128 / LDG.128 (single transaction): a
-// consumer that sees the tag sees the value — no fence, no separate flag.
+// Value + epoch tag in one 16-byte slot {value, tag}. The producer stores the
+// value, then publishes the tag with st.release; a consumer ld.acquire's the
+// tag and only then reads the value. (A single v2 access is not single-copy
+// atomic in the PTX memory model, so the tag alone may not vouch for the
+// value without this release/acquire pair.) The epoch comes from a monotone
+// ticket, so no reset is needed between applies.
 __device__ __forceinline__ void st_tagged(double2* p, double v, double tag) {
-    asm volatile("st.relaxed.gpu.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v), "d"(tag) : "memory");
+    double* q = reinterpret_cast<double*>(p);
+    asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(q), "d"(v) : "memory");
+    asm volatile("st.release.gpu.global.f64 [%0], %1;" ::"l"(q + 1), "d"(tag) : "memory");
 }
-__device__ __forceinline__ double2 ld_tagged(const double2* p) {
-    double2 r;
-    asm volatile("ld.relaxed.gpu.global.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p) : "memory");
-    return r;
+__device__ __forceinline__ double ld_tag_acquire(const double2* p) {
+    double t;
+    asm volatile("ld.acquire.gpu.global.f64 %0, [%1];" : "=d"(t) : "l"(reinterpret_cast<const double*>(p) + 1)
+                 : "memory");
+    return t;
+}
+__device__ __forceinline__ double ld_value_relaxed(const double2* p) {
+    double v;
+    asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(reinterpret_cast<const double*>(p))
+                 : "memory");
+    return v;
 }
 // Spinning lanes back off exponentially (32 ns .. kIluMaxSleep): thousands of
 // waiters polling the same few L2 lines at full rate would queue the very
 // stores they wait for behind their loads.
 __device__ __forceinline__ double wait_tagged(const double2* p, double tag) {
-    double2 r = ld_tagged(p);
     unsigned ns = 32;
-    while (r.y != tag) {
+    while (ld_tag_acquire(p) != tag) {
         __nanosleep(ns);
         ns = min(2 * ns, (unsigned)kIluMaxSleep);
-        r = ld_tagged(p);
     }
-    return r.x;
+    return ld_value_relaxed(p);
 }
 __device__ __forceinline__ void wait_flag(const int* f) {
     unsigned ns = 32;

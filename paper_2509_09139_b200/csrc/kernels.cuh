@@ -237,7 +237,8 @@ struct MgsLaunch {
     int grid = 0;
     int threads = 1024;
     int slice = 0;
-    size_t smem = 0;
+    size_t smem = 0;    // dynamic: Givens scratch (scr doubles) + the w slice when w_in_smem
+    int scr = 0;
     bool w_in_smem = true;
     bool icwy = false;  // compact-WY (2 barriers/step) instead of textbook MGS (j+2)
 };

@@ -230,23 +230,6 @@ __device__ __forceinline__ void prefetch_tile(const SpkView& p, int P, bool fwd,
     }
 }
 
-// Part `part` of `nparts` of the whole factor arena (entries, tiles,
-// descriptors, pivots) into L2 — one warp, 32 KB per bulk request.
-__device__ __forceinline__ void prefetch_arena_l2(const SpkView& p, int part, int nparts, int lane) {
-    auto one = [&](const void* base, size_t bytes) {
-        const size_t chunk = (((bytes + nparts - 1) / nparts) + 15) & ~(size_t)15;
-        const size_t b0 = chunk * part, b1 = min(bytes, b0 + chunk);
-        for (size_t off = b0 + (size_t)lane * 32768; off < b1; off += (size_t)32 * 32768)
-            prefetch_l2(static_cast<const char*>(base) + off, min((size_t)32768, b1 - off));
-    };
-    one(p.eval, sizeof(float) * (size_t)p.n_entries);
-    one(p.eidx, (p.idx32 ? 4 : 2) * (size_t)p.n_entries);
-    one(p.dtile, sizeof(float) * kTileFloats * (size_t)p.num_panels);
-    one(p.desc, sizeof(SpkPanel) * (size_t)p.num_panels);
-    one(p.piv, sizeof(int) * (size_t)p.n);
-    if (p.rows) one(p.rmeta, 128 * (size_t)p.num_panels);
-}
-
 template <class IdxT>
 __device__ __forceinline__ void prefetch_entries(const SpkView& p, int e0, int cnt, int lane, int lv, int li) {
     if (!p.pf) return;

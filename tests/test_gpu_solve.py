@@ -239,3 +239,69 @@ def test_solve_independent_of_stale_device_memory(monkeypatch):
         assert np.array_equal(out.x, c_out.x)
         assert np.array_equal(z, c_z)
         assert st == c_st
+
+
+# ------------------------------------------------ round-2 regressions
+@pytest.mark.parametrize("kind", ["identity", "ilu0", "bj1x1"])
+def test_small_system_long_cycle_givens_scratch(ref, kind):
+    """n < 3m on a one-CTA orthogonalisation grid: the Givens
+    scratch of an unfused step holds 3j+2 doubles, more than the 64-row slice
+    once j > 21. Shifted 8x8 Laplacian: 29-33 steps in the first cycle; the
+    iteration count must match the reference's and x its solution."""
+    n, m = 64, 50
+    d = fx.to_dense(fx.laplacian_2d(8, 8)) - np.eye(n)
+    rows, cols = np.nonzero(d)
+    a = hp.SparseMatrix.from_triplets(rows, cols, d[rows, cols], n)
+    b = np.random.default_rng(1).uniform(-1, 1, n)
+    rs, ci, v = a.row_starts, a.col_indices, a.values
+    if kind == "identity":
+        p = hp.Preconditioner.identity(n)
+        cfg = hp.GmresConfig(restart_m=m, tol=1e-13, max_restarts=3, precision="double")
+        out = ref.solve_identity(rs, ci, v, b, m, 1e-13, 3)
+    elif kind == "ilu0":
+        p = hp.Preconditioner.from_ilu0(a)
+        cfg = hp.GmresConfig(restart_m=m, tol=1e-13, max_restarts=3, precision="double")
+        out = ref.solve_ilu0(rs, ci, v, b, m, 1e-13, 3)
+    else:
+        p = hp.Preconditioner.block_jacobi(a, hp.partition_from_assignment(np.arange(n), n))
+        p.ctx.set_fused(False)
+        cfg = hp.GmresConfig(restart_m=m, tol=1e-13, max_restarts=3)
+        out = ref.solve(rs, ci, v, n, b, m, 1e-13, 3, hybrid=True, assignment=np.arange(n))
+    r = hp.hybrid_restart_gmres(a, p, b, cfg)
+    assert r.report.total_iterations >= 25  # the first cycle ran past j = n/3
+    assert r.report.converged and out.converged
+    assert abs(r.report.total_iterations - out.total_iterations) <= max(1, 0.05 * out.total_iterations)
+    assert np.linalg.norm(r.x - out.x) / np.linalg.norm(out.x) <= 1e-6
+    assert np.linalg.norm(b - d @ r.x) / np.linalg.norm(b) <= 1e-13 * 1.0001
+
+
+def test_update_values_then_gmres_solves_new_matrix():
+    """hpbj_update_values followed by a solve WITHOUT refactor: a lagged
+    preconditioner on the new matrix (the SpMV and the true residual must use
+    the new values in the permuted frame)."""
+    s0 = generate(4, 0)
+    s1 = generate(4, 1)
+    a0 = hp.SparseMatrix(s0.n, s0.row_ptr, s0.col, s0.val)
+    part = hp.partition_graph(a0, s0.num_blocks, 0.1)
+    p = hp.Preconditioner.block_jacobi(a0, part)
+    p.ctx.update_values(s1.val)
+    a0.values = s1.val
+    cfg = hp.GmresConfig(restart_m=s1.restart_m, tol=s1.tol, max_restarts=s1.max_restarts)
+    r = hp.hybrid_restart_gmres(a0, p, s1.b, cfg)
+    rows = np.repeat(np.arange(s1.n), np.diff(s1.row_ptr))
+    ax = np.zeros(s1.n)
+    np.add.at(ax, rows, s1.val * r.x[s1.col])
+    true = np.linalg.norm(s1.b - ax) / np.linalg.norm(s1.b)
+    assert r.report.converged and true <= s1.tol * 1.0001
+    assert abs(true - r.report.final_residual) <= 1e-3 * true
+    assert np.linalg.norm(r.x - s1.x_true) / np.linalg.norm(s1.x_true) <= 1e-6
+
+
+def test_invalid_restart_m_rejected_before_allocation():
+    a = fx.diag_csr([2.0, 3.0])
+    p = hp.Preconditioner.block_jacobi(a, hp.partition_from_assignment([0, 1], 2))
+    for m in (0, 1025, 10 ** 9):
+        with pytest.raises(ValueError):
+            hp.hybrid_restart_gmres(a, p, [1.0, 1.0], hp.GmresConfig(restart_m=m))
+    r = hp.hybrid_restart_gmres(a, p, [1.0, 1.0], hp.GmresConfig(restart_m=5, tol=1e-12))
+    assert r.report.converged

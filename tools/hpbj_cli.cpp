@@ -325,18 +325,6 @@ Partition import_partition_file(const std::string& path, index_t n, index_t s) {
     return partition_from_assignment(std::move(asg), s);
 }
 
-std::vector<index_t> block_nnz_of(const Partition& p, const SparseMatrix& a) {  // partition.cpp:178-195
-    std::vector<index_t> bn(p.num_blocks, 0);
-    const auto rs = a.row_starts();
-    const auto ci = a.col_indices();
-    for (index_t i = 0; i < a.rows(); ++i) {
-        const index_t b = p.assignment[i];
-        for (index_t k = rs[i]; k < rs[i + 1]; ++k)
-            if (p.assignment[ci[k]] == b) ++bn[b];
-    }
-    return bn;
-}
-
 double ms_since(std::chrono::steady_clock::time_point t0) {
     return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
 }
@@ -348,6 +336,7 @@ RunResult run_spec(const RunSpec& spec) {  // bjgmres_cli.cpp:112-168
     out.n = a.rows();
     out.nnz = a.nnz();
     const auto t_setup = std::chrono::steady_clock::now();
+    if (spec.precision == "hybrid") a.materialize_low();  // bjgmres_cli.cpp:126
     GmresConfig cfg;
     cfg.restart_m = spec.restart_m;
     cfg.tol = spec.tol;
@@ -373,19 +362,19 @@ RunResult run_spec(const RunSpec& spec) {  // bjgmres_cli.cpp:112-168
     BlockJacobiOptions opts;
     opts.eps_pivot = spec.eps_pivot;
     opts.neumann_order = spec.neumann_order;
-    const std::vector<index_t> bnnz = block_nnz_of(part, a);
+    opts.policy.mode = cfg.policy.mode;
     Preconditioner p = Preconditioner::block_jacobi(a, std::move(part), opts);
     // with_cond_estimates defaults to true in the reference (preconditioner.hpp:37):
     // the estimates are part of its setup time
-    const auto stats = p.stats(true);
+    const auto& stats = p.block_jacobi_data()->stats;
     out.setup_ms = ms_since(t_setup);
     for (const auto& st : stats) {
+        out.block_nnz.push_back(st.block_nnz);
         out.block_dim.push_back(st.block_dim);
         out.block_pert.push_back(st.perturbation_count);
         out.block_cond.push_back(st.cond_estimate);
         out.block_ebound.push_back(st.error_bound);
     }
-    out.block_nnz = bnnz;
     const std::vector<double> b = make_rhs(spec, a);
     const auto t_solve = std::chrono::steady_clock::now();
     SolveResult sr = hybrid_restart_gmres(a, p, b, cfg);
@@ -568,30 +557,14 @@ int cmd_bench(const std::string& specs_path, int repetitions, const std::string&
 
 int cmd_partition(const std::string& matrix_path, index_t s, const std::string& out_path) {  // :349-363
     const SparseMatrix a = read_matrix(matrix_path);
-    const index_t n = a.rows();
-    // graph_from_matrix for the cut weight (graph.cpp:17-51)
-    std::vector<int64_t> st(n + 1), nb(2 * a.nnz() + 1);
-    std::vector<double> w(2 * a.nnz() + 1);
-    if (hpbj_graph_from_matrix(n, a.row_starts().data(), a.col_indices().data(), a.values().data(), st.data(),
-                               nb.data(), w.data(), (int64_t)nb.size()) != HPBJ_OK)
-        throw std::runtime_error(hpbj_last_error(nullptr));
-    Partition p = partition_graph(a, s, 0.1);
-    const std::vector<index_t> bn = block_nnz_of(p, a);
-    index_t total = 0, mx = 0;
-    for (index_t c : bn) {
-        total += c;
-        mx = std::max(mx, c);
-    }
-    const double mean = (double)total / (double)s;
-    const double imbalance = mean > 0.0 ? (double)mx / mean : 0.0;
-    double cut = 0.0;  // cut_weight (partition.cpp:197-204)
-    for (index_t u = 0; u < n; ++u)
-        for (int64_t k = st[u]; k < st[u + 1]; ++k)
-            if (u < nb[k] && p.assignment[u] != p.assignment[nb[k]]) cut += w[k];
+    const WeightedGraph g = graph_from_matrix(a);
+    Partition p = partition_graph(g, s, 0.1);
+    measure_block_nnz(p, a);
+    const double cut = cut_weight(g, p);
     std::ofstream out(out_path);
     if (!out) throw std::runtime_error("cannot open output file: " + out_path);
-    for (index_t b : p.assignment) out << b << "\n";
-    std::printf("blocks=%lld cut_weight=%.6g nnz_imbalance=%.4f\n", (long long)s, cut, imbalance);
+    export_partition(out, p);
+    std::printf("blocks=%lld cut_weight=%.6g nnz_imbalance=%.4f\n", (long long)s, cut, p.imbalance);
     return 0;
 }
 
