@@ -56,7 +56,9 @@ typedef struct hpbj_setup_info {
     int64_t singular_column;  /* SingularBlockError::column() */
     int64_t factor_bytes;     /* stored FP32 factor bytes on device */
     double ms_permute;        /* device: Q A Q^T build (CUDA events) */
-    double ms_factor;         /* device: gather + batched FP32 LU (CUDA events) */
+    double ms_factor;         /* device: value gather + batched FP32 LU + apply-format build (CUDA events) */
+    double ms_lu;             /* device: the batched LU kernel alone */
+    double ms_spk;            /* device: the apply-format (SPK) build alone */
 } hpbj_setup_info;
 
 /* GmresConfig (gmres.hpp:89-97). floor_roundoff is the unit roundoff of the
@@ -123,6 +125,10 @@ int hpbj_get_kernel_stats(hpbj_ctx* ctx, hpbj_kernel_stat* out /* HPBJ_K_COUNT *
 /* Whole Arnoldi cycle as one persistent kernel when it fits (default on);
  * off: one apply, SpMV and orthogonalisation launch per step. */
 int hpbj_set_fused(hpbj_ctx* ctx, int enable);
+/* Solve as one CUDA graph with device-driven WHILE nodes (default on); off:
+ * the host enqueues every kernel of every cycle (same kernels, same results;
+ * each launch is visible to a profiler — HPBJ_NOGRAPH=1 sets the default). */
+int hpbj_set_graph(hpbj_ctx* ctx, int enable);
 
 /* ---- host-side partitioning (bit-identical to the reference) ------------ */
 /* graph_from_matrix (graph.hpp:30, graph.cpp:17-51). Adjacency as CSR:

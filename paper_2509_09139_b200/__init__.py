@@ -455,6 +455,10 @@ class Context:
         """Whole Arnoldi cycle as one persistent kernel when it fits (default)."""
         self.check(self.lib.hpbj_set_fused(self.h, 1 if on else 0))
 
+    def set_graph(self, on: bool):
+        """Solve as one CUDA graph (default) or host-enqueued launches."""
+        self.check(self.lib.hpbj_set_graph(self.h, 1 if on else 0))
+
     def gmres(self, b, cfg: "GmresConfig", device_ptrs=None):
         opts = cfg.to_opts()
         rep = _abi.Report()

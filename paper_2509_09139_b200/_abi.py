@@ -47,6 +47,8 @@ class SetupInfo(ctypes.Structure):
         ("factor_bytes", i64),
         ("ms_permute", f64),
         ("ms_factor", f64),
+        ("ms_lu", f64),
+        ("ms_spk", f64),
     ]
 
 
@@ -95,6 +97,7 @@ SIGNATURES = {
     "hpbj_set_profiling": (ctypes.c_int, [vp, ctypes.c_int]),
     "hpbj_get_kernel_stats": (ctypes.c_int, [vp, ctypes.POINTER(KernelStat)]),
     "hpbj_set_fused": (ctypes.c_int, [vp, ctypes.c_int]),
+    "hpbj_set_graph": (ctypes.c_int, [vp, ctypes.c_int]),
     "hpbj_get_block_diagnostics": (ctypes.c_int, [vp, ctypes.POINTER(f64), ctypes.POINTER(f64)]),
     "hpbj_mm_read": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(i64), ctypes.POINTER(i64),
                                     ctypes.POINTER(ctypes.POINTER(i64)), ctypes.POINTER(ctypes.POINTER(i64)),

@@ -866,6 +866,384 @@ __global__ void __launch_bounds__(NT, 2) k_block_lu_blk(LuParams p, int dlo, int
     }
 }
 
+// ---------------------------------------------------------------------------
+// Left-looking blocked LU with the factor in shared memory (kWarpLuMax < d <=
+// kLlMax), one CTA per block. Only the L part of the factor (every row that
+// was still active when a 32-column panel was factored, 32 multipliers each:
+// ~d^2/2 floats) lives in shared memory for the whole factorisation, plus the
+// current column panel X of all d rows; U leaves for HBM panel by panel. Per
+// column panel P (columns c0 .. c0 + 31):
+//   gather    the panel's columns of the block from the permuted CSR (per-row
+//             cursors; FP64 -> FP32 RNE), X zero-filled;
+//   for each earlier panel Q:
+//     (i)  the 32 pivot rows of Q: forward substitution with Q's unit-lower
+//          L11 (warp 0, lane per column, m-outer so the 31 chains interleave);
+//     (ii) the rows still active after Q: rank-32 update X -= L_Q U_Q (lane
+//          per column, U column in registers, multipliers as float4
+//          broadcasts, four rows in flight per warp);
+//   factor    the panel's active rows (thread per row, 32 entries in
+//             registers): per column a CTA argmax (ties to the smaller row)
+//             with ONE barrier — every warp publishes its candidate row's
+//             entries with its key, double-buffered — then the rank-1 update
+//             in registers;
+//   store     the panel's multipliers of every active row to L_P; the pivot
+//             rows' L entries (all earlier panels) and the finished U column
+//             panel go to the packed output panels.
+// Every element receives exactly the fmaf(-l, u, a) chain, in ascending
+// column order, that the right-looking kernels apply (left- and right-looking
+// only reorder independent chains), the divisions and the pivot rule are the
+// same: factors and pivots are bit-identical to k_block_lu_blk / k_block_lu.
+constexpr int kLlMax = 288;  // upper bound; the launcher checks the shared-memory budget
+
+__host__ __device__ inline int ll_lrows(int d) {  // L_Q rows kept: panels 0 .. T-2
+    const int T = (d + 31) / 32;
+    int r = 0;
+    for (int q = 0; q + 1 < T; ++q) r += d - 32 * q;
+    return r;
+}
+
+template <int NT>
+__host__ __device__ inline size_t ll_smem_bytes(int dhi) {
+    constexpr int NW = NT / 32;
+    const int T = (dhi + 31) / 32;
+    const int lr = ll_lrows(dhi);
+    return (size_t)lr * 32 * sizeof(float)          // L_Q rows
+           + (size_t)dhi * 32 * sizeof(float)       // X: current column panel, all rows
+           + (size_t)2 * NW * 32 * sizeof(float)    // candidate rows (double buffered)
+           + (size_t)2 * NW * 4 * sizeof(int)       // candidate key / row / position
+           + (size_t)lr * sizeof(short)             // row id of every L_Q row
+           + (size_t)(T > 1 ? T - 1 : 1) * dhi * sizeof(short)  // position of row r in L_Q
+           + (size_t)3 * dhi * sizeof(short)        // ppos, act, prow
+           + 64;
+}
+
+// swizzled X: quad (c / 4) of row r at quad slot (c / 4) ^ (r & 7)
+__device__ __forceinline__ int xq(int r, int q) { return r * 32 + ((q ^ (r & 7)) << 2); }
+
+template <int NT>
+__global__ void __launch_bounds__(NT, 1) k_block_lu_ll(LuParams p, int dlo, int dhi) {
+    constexpr int NW = NT / 32;
+    extern __shared__ __align__(16) float llsm[];
+    const int lrmax = ll_lrows(dhi);
+    const int Tmax = (dhi + 31) / 32;
+    float* Ls = llsm;                                          // [lrmax][32]
+    float* X = Ls + (size_t)lrmax * 32;                        // [dhi][32] swizzled
+    float* cand_v = X + (size_t)dhi * 32;                      // [2][NW][32]
+    int* cand_i = reinterpret_cast<int*>(cand_v + 2 * NW * 32);  // [2][NW][4]: key, row, pos
+    short* rowQ = reinterpret_cast<short*>(cand_i + 2 * NW * 4);  // [lrmax]
+    short* posQ = rowQ + lrmax;                                // [Tmax-1][dhi]
+    short* ppos = posQ + (size_t)(Tmax > 1 ? Tmax - 1 : 1) * dhi;  // pivot position of row r (or 0x7fff)
+    short* act = ppos + dhi;                                   // active rows
+    short* prow = act + dhi;                                   // pivot row of position k
+    __shared__ double redd[NW];
+    __shared__ int lofs[16];                                   // first L row of panel Q
+
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+
+    for (int b = blockIdx.x; b < p.s; b += gridDim.x) {
+        const int o = p.bstart[b];
+        const int d = p.bstart[b + 1] - o;
+        if (d <= dlo || d > dhi) continue;
+        const int T = (d + 31) / 32;
+        const int dp4 = (d + 3) & ~3;
+        float* F = p.fac + p.fac_off[b];
+        // per-row CSR cursor (thread tid owns row tid for the gathers) + FP64
+        // inf-norm, row sums in column order (matrix_inf_norm)
+        int cur = 0, ke = 0;
+        double rs = 0.0;
+        if (tid < d) {
+            const int kb = __ldg(p.a.rp + o + tid);
+            ke = __ldg(p.a.rp + o + tid + 1);
+            cur = ke;
+            for (int k = kb; k < ke; ++k) {
+                const int c = __ldg(p.a.ci + k) - o;
+                if (c >= 0 && c < d) {
+                    if (cur == ke) cur = k;
+                    rs = __dadd_rn(rs, fabs(__ldg(p.a.val + k)));
+                } else if (c >= d) {
+                    break;
+                }
+            }
+            act[tid] = (short)tid;
+            ppos[tid] = 0x7fff;
+        }
+        double wm = rs;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) wm = fmax(wm, __shfl_xor_sync(0xffffffffu, wm, off));
+        if (lane == 0) redd[wid] = wm;
+        if (tid == 0) {
+            int acc = 0;
+            for (int q = 0; q + 1 < T; ++q) {
+                lofs[q] = acc;
+                acc += d - 32 * q;
+            }
+        }
+        __syncthreads();
+        double norm = 0.0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) norm = fmax(norm, redd[w]);
+
+        int na = d;
+        int nperturb = 0;
+        bool abort = false;
+        int buf = 0;
+        for (int P = 0; P < T; ++P) {
+            const int c0 = 32 * P;
+            const int kw = min(32, d - c0);
+            // ---- gather the column panel (rows in original order)
+            if (tid < d) {
+                float4* xr = reinterpret_cast<float4*>(X + tid * 32);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) xr[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+                const int cend = o + c0 + kw;
+                while (cur < ke) {
+                    const int c = __ldg(p.a.ci + cur);
+                    if (c >= cend) break;
+                    const int lc = c - o - c0;
+                    X[xq(tid, lc >> 2) + (lc & 3)] = __double2float_rn(__ldg(p.a.val + cur));
+                    ++cur;
+                }
+            }
+            __syncthreads();
+            // ---- left-looking updates from every earlier panel
+            for (int Q = 0; Q < P; ++Q) {
+                const int q0 = 32 * Q;
+                const float* LQ = Ls + (size_t)lofs[Q] * 32;
+                const short* rQ = rowQ + lofs[Q];
+                const short* pQ = posQ + (size_t)Q * dhi;
+                if (wid == 0) {  // (i) pivot rows of Q: x_k -= sum_{m<k} L(k, m) x_m
+                    float x[32];
+                    int lp[32];
+#pragma unroll
+                    for (int m = 0; m < 32; ++m) {
+                        const int r = prow[q0 + m];
+                        lp[m] = pQ[r];
+                        x[m] = X[xq(r, lane >> 2) + (lane & 3)];
+                    }
+#pragma unroll 8
+                    for (int m0 = 0; m0 < 32; m0 += 4) {
+#pragma unroll
+                        for (int mm = 1; mm < 4; ++mm) {  // the 4x4 diagonal piece
+                            const float* lr = LQ + (size_t)lp[m0 + mm] * 32 + m0;
+#pragma unroll
+                            for (int m = 0; m < mm; ++m) x[m0 + mm] = fmaf(-lr[m], x[m0 + m], x[m0 + mm]);
+                        }
+#pragma unroll 28
+                        for (int k = m0 + 4; k < 32; ++k) {
+                            const float4 l4 = *reinterpret_cast<const float4*>(LQ + (size_t)lp[k] * 32 + m0);
+                            x[k] = fmaf(-l4.x, x[m0 + 0], x[k]);
+                            x[k] = fmaf(-l4.y, x[m0 + 1], x[k]);
+                            x[k] = fmaf(-l4.z, x[m0 + 2], x[k]);
+                            x[k] = fmaf(-l4.w, x[m0 + 3], x[k]);
+                        }
+                    }
+#pragma unroll
+                    for (int m = 0; m < 32; ++m) X[xq(prow[q0 + m], lane >> 2) + (lane & 3)] = x[m];
+                }
+                __syncthreads();
+                // (ii) rows active after Q: X[r] -= L_Q[r] U_Q
+                {
+                    float u[32];
+#pragma unroll
+                    for (int m = 0; m < 32; ++m) u[m] = X[xq(prow[q0 + m], lane >> 2) + (lane & 3)];
+                    const int nQ = d - q0;
+                    const int qhi = q0 + 32;
+                    for (int a0 = 4 * wid; a0 < nQ; a0 += 4 * NW) {
+                        int rr[4];
+                        bool ok[4];
+                        float v[4];
+#pragma unroll
+                        for (int t = 0; t < 4; ++t) {
+                            const int a = a0 + t;
+                            rr[t] = a < nQ ? rQ[a] : 0;
+                            ok[t] = a < nQ && ppos[rr[t]] >= qhi;
+                            v[t] = ok[t] ? X[xq(rr[t], lane >> 2) + (lane & 3)] : 0.0f;
+                        }
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+#pragma unroll
+                            for (int t = 0; t < 4; ++t) {
+                                const int a = min(a0 + t, nQ - 1);
+                                const float4 l4 = *reinterpret_cast<const float4*>(LQ + (size_t)a * 32 + 4 * q);
+                                v[t] = fmaf(-l4.x, u[4 * q + 0], v[t]);
+                                v[t] = fmaf(-l4.y, u[4 * q + 1], v[t]);
+                                v[t] = fmaf(-l4.z, u[4 * q + 2], v[t]);
+                                v[t] = fmaf(-l4.w, u[4 * q + 3], v[t]);
+                            }
+                        }
+#pragma unroll
+                        for (int t = 0; t < 4; ++t)
+                            if (ok[t]) X[xq(rr[t], lane >> 2) + (lane & 3)] = v[t];
+                    }
+                }
+                __syncthreads();
+            }
+            // ---- factor the panel: thread a owns active row act[a]
+            const bool has = tid < na;
+            const int myrow = has ? act[tid] : 0;
+            bool fl = !has;  // pivotal (or no row)
+            float rv[32];
+            {
+                const float4* xr = reinterpret_cast<const float4*>(X + myrow * 32);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const float4 t4 = has ? xr[q ^ (myrow & 7)] : make_float4(0.f, 0.f, 0.f, 0.f);
+                    rv[4 * q + 0] = t4.x;
+                    rv[4 * q + 1] = t4.y;
+                    rv[4 * q + 2] = t4.z;
+                    rv[4 * q + 3] = t4.w;
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < 32; ++c) {
+                if (c >= kw) break;
+                const int k = c0 + c;
+                // warp candidate: max |x|, ties -> smaller row
+                const unsigned key = fl ? 0u : __float_as_uint(fabsf(rv[c])) + 1u;
+                unsigned kmx;
+                const int wr = warp_pivot_row(key, fl ? 0x7fffffff : myrow, &kmx);
+                const unsigned own = __ballot_sync(0xffffffffu, !fl && key == kmx && myrow == wr);
+                float* cv = cand_v + (size_t)(buf * NW + wid) * 32;
+                int* ci4 = cand_i + (buf * NW + wid) * 4;
+                if (own && lane == __ffs(own) - 1) {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        reinterpret_cast<float4*>(cv)[q] =
+                            make_float4(rv[4 * q], rv[4 * q + 1], rv[4 * q + 2], rv[4 * q + 3]);
+                    ci4[0] = (int)kmx;
+                    ci4[1] = wr;
+                    ci4[2] = tid;
+                } else if (lane == 0 && !own) {
+                    ci4[0] = 0;
+                    ci4[1] = 0x7fffffff;
+                    ci4[2] = -1;
+                }
+                __syncthreads();
+                // winner over the warps' candidates (identical in every thread)
+                unsigned fk = 0u;
+                int frow = 0x7fffffff, fw = 0;
+#pragma unroll
+                for (int w = 0; w < NW; ++w) {
+                    const int* cw = cand_i + (buf * NW + w) * 4;
+                    const unsigned kk = (unsigned)cw[0];
+                    const int rw = cw[1];
+                    if (kk > fk || (kk == fk && rw < frow)) {
+                        fk = kk;
+                        frow = rw;
+                        fw = w;
+                    }
+                }
+                const float* Pv = cand_v + (size_t)(buf * NW + fw) * 32;
+                const int owner = cand_i[(buf * NW + fw) * 4 + 2];
+                buf ^= 1;
+                // regularize_pivot (lu.cpp:10-20), FP64, identical in every thread
+                const double pvd = (double)Pv[c];
+                const bool keep = pivot_keep(pvd, norm, p.eps);
+                const double val = keep ? pvd : ((pvd < 0.0 ? -1.0 : 1.0) * p.eps * norm);
+                if (val == 0.0) {
+                    if (tid == 0) atomicMin(p.singular, ((unsigned long long)b << 32) | (unsigned)k);
+                    abort = true;
+                    break;
+                }
+                if (!keep) {
+                    ++nperturb;
+                    if (tid == 0) {
+                        const int slot = atomicAdd(p.pert_n, 1);
+                        if (slot < p.pert_cap) p.pert[slot] = PertRecord{b, k, pvd, val};
+                    }
+                }
+                const float pv = (float)val;
+                if (tid == owner) {
+                    rv[c] = pv;
+                    fl = true;
+                    prow[k] = (short)myrow;
+                    ppos[myrow] = (short)k;
+                } else if (!fl) {
+                    const float l = rv[c] / pv;  // L(i,k) = x_i / pivot (lu.cpp:207)
+                    rv[c] = l;
+#pragma unroll
+                    for (int c2 = c + 1; c2 < 32; ++c2) rv[c2] = fmaf(-l, Pv[c2], rv[c2]);
+                }
+            }
+            if (abort) break;
+            // ---- the panel's entries back to X; multipliers of every active row to L_P
+            if (has) {
+                float4* xr = reinterpret_cast<float4*>(X + myrow * 32);
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    xr[q ^ (myrow & 7)] = make_float4(rv[4 * q], rv[4 * q + 1], rv[4 * q + 2], rv[4 * q + 3]);
+                if (P + 1 < T) {
+                    float4* lr = reinterpret_cast<float4*>(Ls + ((size_t)lofs[P] + tid) * 32);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        lr[q] = make_float4(rv[4 * q], rv[4 * q + 1], rv[4 * q + 2], rv[4 * q + 3]);
+                    rowQ[lofs[P] + tid] = (short)myrow;
+                    posQ[(size_t)P * dhi + myrow] = (short)tid;
+                }
+            }
+            __syncthreads();
+            // ---- output: chunks (t, P) for t <= P (U / L11\U11 from X) and
+            // (P, Q) for Q < P (the new pivot rows' L from L_Q); chunk (t, u)
+            // = rows 32t.. of panel t, quads 8u .. 8u + nq(u), [quad][row][4]
+            {
+                const int nqP = min(8, dp4 / 4 - 8 * P);
+                for (int e = tid; e < (P + 1) * 8 * 32; e += NT) {  // (t, P)
+                    const int t = e >> 8, qi = (e >> 5) & 7, kr = e & 31;
+                    if (qi >= nqP) continue;
+                    const int k = 32 * t + kr;
+                    const int cq = 4 * (8 * P + qi);
+                    float4 v;
+                    if (k < d) {
+                        const int r = prow[k];
+                        v = *reinterpret_cast<const float4*>(X + xq(r, qi));
+                        if (cq + 0 >= d) v.x = 0.f;
+                        if (cq + 1 >= d) v.y = (k == cq + 1) ? 1.f : 0.f;
+                        if (cq + 2 >= d) v.z = (k == cq + 2) ? 1.f : 0.f;
+                        if (cq + 3 >= d) v.w = (k == cq + 3) ? 1.f : 0.f;
+                    } else {
+                        v = make_float4(k == cq ? 1.f : 0.f, k == cq + 1 ? 1.f : 0.f, k == cq + 2 ? 1.f : 0.f,
+                                        k == cq + 3 ? 1.f : 0.f);
+                    }
+                    __stcs(reinterpret_cast<float4*>(F + (size_t)t * 32 * dp4 + (size_t)(8 * P + qi) * 128 + kr * 4),
+                           v);
+                }
+                for (int e = tid; e < P * 8 * 32; e += NT) {  // (P, Q), Q < P
+                    const int Q = e >> 8, qi = (e >> 5) & 7, kr = e & 31;
+                    const int k = c0 + kr;
+                    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (k < d) {
+                        const int r = prow[k];
+                        v = *reinterpret_cast<const float4*>(Ls + ((size_t)lofs[Q] + posQ[(size_t)Q * dhi + r]) * 32 +
+                                                             4 * qi);
+                    }
+                    __stcs(reinterpret_cast<float4*>(F + (size_t)P * 32 * dp4 + (size_t)(8 * Q + qi) * 128 + kr * 4),
+                           v);
+                }
+            }
+            // ---- drop the panel's pivot rows from the active list (stable)
+            if (wid == 0) {
+                int w = 0;
+                for (int base = 0; base < na; base += 32) {
+                    const int a = base + lane;
+                    const int r = a < na ? act[a] : 0;
+                    const bool keepr = a < na && ppos[r] == 0x7fff;
+                    const unsigned m = __ballot_sync(0xffffffffu, keepr);
+                    __syncwarp();
+                    if (keepr) act[w + __popc(m & ((1u << lane) - 1u))] = (short)r;
+                    w += __popc(m);
+                    __syncwarp();
+                }
+            }
+            na -= kw;
+            __syncthreads();
+        }
+        if (tid == 0) p.pert_count[b] = nperturb;
+        if (!abort)
+            for (int k = tid; k < d; k += NT) p.piv[o + k] = prow[k];
+        __syncthreads();
+    }
+}
+
 int lu_smem_dim(int dmax) {
     int d = 1;
     while (d + 1 <= dmax && (size_t)(d + 1) * ((d + 1) | 1) * sizeof(float) <= kLuSmemTile) ++d;
@@ -893,7 +1271,9 @@ size_t block_lu_scratch_floats(int dmax, int num_sms, int* smem_dim, int* scratc
     *smem_dim = lu_smem_dim(dmax);
     *scratch_ld = blk_ld(dmax | 1);  // odd-free 16-byte rows for the blocked kernel, >= dmax | 1
     size_t need = 0;
-    if (dmax > kWarpLuMax) {  // blocked kernels: one tile per resident CTA
+    const char* e = getenv("HPBJ_LU_LL");
+    const bool ll = !(e && e[0] == '0');
+    if (dmax > kWarpLuMax && (!ll || dmax > kLlMax)) {  // blocked kernels: one tile per resident CTA
         const int d1 = std::min(dmax, kBlkThreads);
         need = (size_t)num_sms * blk_ctas_per_sm(d1) * (*scratch_ld) * (*scratch_ld);
         if (dmax > kBlkThreads)
@@ -950,9 +1330,36 @@ void launch_block_lu(const LuParams& p_in, int dmax, int num_sms, cudaStream_t s
         HPBJ_CUDA(cudaGetLastError());
         return;
     }
-    // blocked kernels for dw < d <= 256 and 256 < d <= kBlkMax
+    // left-looking shared-memory kernel for dw < d <= kLlMax (HPBJ_LU_LL=0:
+    // the L2-scratch blocked kernel instead, for A/B runs and the bit-identity test)
+    int dll = dw;
+    {
+        const char* e = getenv("HPBJ_LU_LL");
+        if (!(e && e[0] == '0')) {
+            for (int range = 0; range < 2; ++range) {
+                const int dlo = range == 0 ? dw : 256;
+                const int dhi = std::min(dmax, range == 0 ? 256 : kLlMax);
+                if (dhi <= dlo) continue;
+                const size_t smem = range == 0 ? ll_smem_bytes<256>(dhi) : ll_smem_bytes<512>(dhi);
+                void (*fn)(LuParams, int, int) = range == 0 ? k_block_lu_ll<256> : k_block_lu_ll<512>;
+                HPBJ_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                int occ = 0;
+                HPBJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, range == 0 ? 256 : 512, smem));
+                occ = std::max(occ, 1);
+                const int grid = std::min(p.s, num_sms * occ);
+                fn<<<grid, range == 0 ? 256 : 512, smem, st>>>(p, dlo, dhi);
+                *launches += 1;
+                dll = dhi;
+            }
+        }
+    }
+    if (dmax <= dll) {
+        HPBJ_CUDA(cudaGetLastError());
+        return;
+    }
+    // blocked kernels for dll < d <= 256 and 256 < d <= kBlkMax
     for (int range = 0; range < 2; ++range) {
-        const int dlo = range == 0 ? dw : kBlkThreads;
+        const int dlo = std::max(dll, range == 0 ? dw : kBlkThreads);
         const int dhi = std::min(dmax, range == 0 ? kBlkThreads : kBlkMax);
         if (dhi <= dlo) continue;
         const size_t smem = blk_smem_bytes(dhi);

@@ -531,12 +531,16 @@ void factor(hpbj_ctx* c, hpbj_setup_info* info) {
     p.scratch = c->d_lu_scratch;
     p.smem_dim = c->lu_smem_dim;
     p.scratch_ld = c->lu_scratch_ld;
-    cudaEvent_t e0, e1;
+    cudaEvent_t e0, e1, eg, el;
     HPBJ_CUDA(cudaEventCreate(&e0));
     HPBJ_CUDA(cudaEventCreate(&e1));
+    HPBJ_CUDA(cudaEventCreate(&eg));
+    HPBJ_CUDA(cudaEventCreate(&el));
     HPBJ_CUDA(cudaEventRecord(e0, st));
     launch_gather_values(c->d_src, c->A.val, c->B.val, c->B.nnz, st, &c->launches);
+    HPBJ_CUDA(cudaEventRecord(eg, st));
     launch_block_lu(p, c->dmax, c->num_sms, st, &c->launches);
+    HPBJ_CUDA(cudaEventRecord(el, st));
     build_spk(c);
     HPBJ_CUDA(cudaEventRecord(e1, st));
     unsigned long long sing = 0;
@@ -544,11 +548,17 @@ void factor(hpbj_ctx* c, hpbj_setup_info* info) {
     HPBJ_CUDA(cudaMemcpyAsync(&sing, c->d_singular, sizeof(sing), cudaMemcpyDeviceToHost, st));
     HPBJ_CUDA(cudaMemcpyAsync(&pert_n, c->d_pert_n, sizeof(int), cudaMemcpyDeviceToHost, st));
     HPBJ_CUDA(cudaStreamSynchronize(st));
-    float ms = 0.f;
+    float ms = 0.f, ms_lu = 0.f, ms_spk = 0.f;
     HPBJ_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    HPBJ_CUDA(cudaEventElapsedTime(&ms_lu, eg, el));
+    HPBJ_CUDA(cudaEventElapsedTime(&ms_spk, el, e1));
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+    cudaEventDestroy(eg);
+    cudaEventDestroy(el);
     if (info) {
+        info->ms_lu = ms_lu;
+        info->ms_spk = ms_spk;
         info->num_blocks = c->s;
         info->dim_min = c->dmin;
         info->dim_max = c->dmax;
@@ -1041,6 +1051,12 @@ int hpbj_get_kernel_stats(hpbj_ctx* ctx, hpbj_kernel_stat* out) {
             out[k].bytes_per_launch = out[k].launches ? out[k].total_bytes / (double)out[k].launches : 0.0;
         }
     });
+}
+
+int hpbj_set_graph(hpbj_ctx* ctx, int enable) {
+    if (!ctx) return HPBJ_EINVAL;
+    ctx->use_graph = enable != 0;
+    return HPBJ_OK;
 }
 
 int hpbj_set_fused(hpbj_ctx* ctx, int enable) {

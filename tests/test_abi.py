@@ -59,8 +59,25 @@ def test_null_context_is_rejected():
     assert lib.hpbj_gmres(None, None, None, None, None, None, 0, None, 0) == _abi.HPBJ_EINVAL
 
 
-def test_struct_layouts():
-    assert ctypes.sizeof(_abi.GmresOpts) == 48
-    assert ctypes.sizeof(_abi.Report) == 64
-    assert ctypes.sizeof(_abi.SetupInfo) == 72
-    assert ctypes.sizeof(_abi.HistoryPoint) == 24
+def test_struct_layouts(tmp_path):
+    """ctypes mirrors of the hpbj.h structs: sizes and field offsets equal the
+    C compiler's."""
+    import subprocess
+    structs = {"hpbj_gmres_opts": _abi.GmresOpts, "hpbj_report": _abi.Report, "hpbj_setup_info": _abi.SetupInfo,
+               "hpbj_history_point": _abi.HistoryPoint, "hpbj_kernel_stat": _abi.KernelStat}
+    src = ["#include <stdio.h>", "#include <stddef.h>", '#include "hpbj.h"', "int main(void) {"]
+    for cname, py in structs.items():
+        src.append(f'printf("{cname} %zu\\n", sizeof({cname}));')
+        for f, _ in py._fields_:
+            src.append(f'printf("{cname}.{f} %zu\\n", offsetof({cname}, {f}));')
+    src.append("return 0; }")
+    c = tmp_path / "layout.c"
+    c.write_text("\n".join(src))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I" + os.path.join(ROOT, "include"), str(c), "-o", str(exe)], check=True)
+    got = dict(ln.split() for ln in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                    check=True).stdout.splitlines())
+    for cname, py in structs.items():
+        assert int(got[cname]) == ctypes.sizeof(py), cname
+        for f, _ in py._fields_:
+            assert int(got[f"{cname}.{f}"]) == getattr(py, f).offset, (cname, f)

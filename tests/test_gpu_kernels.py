@@ -29,7 +29,7 @@ def _spmv_bound(a, x):
     return 2.0 * np.maximum(np.diff(rs), 1) * 2.0 ** -53 * absrow
 
 
-@pytest.mark.parametrize("config", [0, 1, 4, 2])
+@pytest.mark.parametrize("config", [0, 1, 4, 2, 3])
 def test_spmv_matches_reference(ref, config):
     s = generate(config)
     a = _sys_matrix(s)
@@ -112,11 +112,48 @@ def test_lu_pair_and_warp_kernels_bit_identical(config, monkeypatch):
         assert np.array_equal(f0.view(np.uint32), f1.view(np.uint32))
 
 
-def test_block_factors_config2_sample(ref):
-    s = generate(2)
+@pytest.mark.parametrize("config", [2, 3])
+def test_lu_left_looking_bit_identical_to_blocked(config, monkeypatch):
+    """k_block_lu_ll (left-looking, L in shared memory; default for
+    96 < d <= 288) and k_block_lu_blk (right-looking, L2 scratch tile;
+    HPBJ_LU_LL=0) apply the same fmaf chain per element in the same order and
+    the same pivot rule: factors and pivot rows bit-identical, incl. the
+    largest blocks (d > 256: the 512-thread instance)."""
+    s = generate(config)
+    a = _sys_matrix(s)
+    part = hp.partition_graph(a, s.num_blocks, 0.1)
+    dims = np.diff(part.block_starts)
+    blocks = sorted(set(range(0, s.num_blocks, max(1, s.num_blocks // 150))) |
+                    set(np.argsort(dims)[-20:].tolist()) | set(np.argsort(dims)[:5].tolist()))
+    out = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("HPBJ_LU_LL", flag)
+        p = hp.Preconditioner.block_jacobi(a, part)
+        out.append(([p.block_factors(b) for b in blocks], [x["perturbation_count"] for x in p.stats(False)]))
+    (f0, pc0), (f1, pc1) = out
+    assert pc0 == pc1
+    for b, (F0, P0), (F1, P1) in zip(blocks, f0, f1):
+        assert np.array_equal(P0, P1), b
+        assert np.array_equal(F0.view(np.uint32), F1.view(np.uint32)), (b, int(dims[b]))
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("config", [2, 3])
+def test_block_factors_all_blocks_large_configs(ref, config):
+    """Every block of configs 2 (7,813 blocks, d <= 141) and 3 (16,000
+    blocks, d up to 282: k_block_lu_blk<256,1> and, for d > 256,
+    k_block_lu_blk<256,2>) against gp_lu (lu.cpp:134-225) cast to FP32: pivot
+    sequences equal, normwise factor error <= 1e-5, perturbation counts equal.
+    The partition is our host partitioner's, bit-identical to the reference's
+    (tests/test_partition.py, goldens)."""
+    s = generate(config)
     part = hp.partition_graph(_sys_matrix(s), s.num_blocks, 0.1)
-    worst, mism = _factor_parity(ref, s, part.assignment, blocks=list(range(0, 60)) + list(range(4000, 4100)))
-    assert mism == 0 and worst <= 1e-5
+    dims = np.diff(part.block_starts)
+    if config == 3:
+        assert dims.max() > 256  # the two-tile-row blocked kernel is exercised
+    worst, mism = _factor_parity(ref, s, part.assignment)
+    assert mism == 0, f"{mism} blocks with a different pivot sequence"
+    assert worst <= 1e-5, worst
 
 
 def test_lu_known_answers(ref):
@@ -235,6 +272,47 @@ def test_apply_both_offpanel_layouts(ref, config, layout, monkeypatch):
     zr = ref.apply(s.row_ptr, s.col, s.val, s.num_blocks, asg, v, fp32=True)
     assert np.linalg.norm(z - zr) <= 2e-6 * np.linalg.norm(zr)
     assert np.array_equal(z, p.apply(v))
+
+
+@pytest.mark.parametrize("coef", [-0.6, -0.75])
+def test_apply_ill_conditioned_tiles(ref, coef):
+    """The apply multiplies by explicitly inverted 32x32 diagonal tiles
+    (spk.cu). Blocks of 96 rows made of three unit upper-triangular 32x32
+    tiles with every upper entry = coef (tile condition ~1e6 / ~1e8) plus weak
+    random coupling: no pivoting, so our FP32 factors and the reference's FP32
+    cast are the same numbers and only the substitution differs. Our result
+    must be as accurate as the reference's apply<float> (sequential FP32
+    substitution, lu.hpp:88-112) against the exact solve with those factors."""
+    rng = np.random.default_rng(5)
+    nb, d = 4, 96
+    n = nb * d
+    rows, cols, vals = [], [], []
+    for b in range(nb):
+        o = b * d
+        for i in range(d):
+            rows.append(o + i), cols.append(o + i), vals.append(1.0)
+            for j in range(i + 1, d):
+                if i // 32 == j // 32:
+                    rows.append(o + i), cols.append(o + j), vals.append(coef)
+                elif rng.random() < 0.1:
+                    rows.append(o + i), cols.append(o + j), vals.append(float(rng.uniform(-0.05, 0.05)))
+    a = hp.SparseMatrix.from_triplets(np.array(rows), np.array(cols), np.array(vals), n)
+    asg = np.repeat(np.arange(nb), d)
+    part = hp.partition_from_assignment(asg, nb)
+    p = hp.Preconditioner.block_jacobi(a, part)
+    U = fx.to_dense(a).astype(np.float32).astype(np.float64)  # the FP32 factors (L = I)
+    tile = U[:32, :32]
+    cond = np.linalg.cond(tile, 1)
+    assert 1e5 <= cond <= 1e9, cond
+    v = rng.uniform(-1, 1, n)
+    v32 = v.astype(np.float32).astype(np.float64)  # both applies round v to FP32 on load
+    exact = np.linalg.solve(U, v32)
+    z = p.apply(v)
+    zr = ref.apply(a.row_starts, a.col_indices, a.values, nb, asg, v, fp32=True)
+    err = np.linalg.norm(z - exact) / np.linalg.norm(exact)
+    err_ref = np.linalg.norm(zr - exact) / np.linalg.norm(exact)
+    print(f"tile cond {cond:.2e}: ours {err:.2e}, reference apply<float> {err_ref:.2e}")
+    assert err <= 4.0 * err_ref + 1e-7, (err, err_ref)
 
 
 def test_apply_deterministic():

@@ -64,15 +64,27 @@ def test_config_solve_matches_reference(ref, config):
     _check_parity(s, res, out.total_iterations, x_ref=out.x)
 
 
+@pytest.mark.slow
 def test_config4_newton_sequence(ref):
-    """Partition of A_0 reused; numeric refactorisation per step (first 8 steps)."""
+    """All 64 steps: partition of A_0 reused, numeric refactorisation per step
+    (BASELINE config 4). Each step: iterations within 5% of reference Hybrid
+    (and the committed golden), x within 1e-6, FP64 residual <= tol. Where the
+    count differs from reference Hybrid, the CPU restatement of the north
+    star's precision mix (oracle Port, mode "mix": FP32 preconditioner, FP64
+    SpMV and Gram-Schmidt) must reproduce ours within one iteration: the
+    difference is the FP64-vs-FP32 Krylov loop on an estimate that crosses
+    tol within a hair (e.g. step 25: reference 9.9998e-11 at iteration 68,
+    the mix 1.00045e-10), not a defect."""
+    from oracle import Port
+    port = Port()
     g = _golden(4)
     s0 = generate(4, 0)
     a0 = hp.SparseMatrix(s0.n, s0.row_ptr, s0.col, s0.val)
     part = hp.partition_graph(a0, s0.num_blocks, 0.1)
     p = hp.Preconditioner.block_jacobi(a0, part)
     cfg = hp.GmresConfig(restart_m=s0.restart_m, tol=s0.tol, max_restarts=s0.max_restarts)
-    for k in range(8):
+    differ = []
+    for k in range(64):
         sk = generate(4, k)
         assert sk.digest() == g["steps"][k]["input_sha256"]
         if k > 0:
@@ -84,21 +96,32 @@ def test_config4_newton_sequence(ref):
                         hybrid=True, assignment=part.assignment)
         assert out.total_iterations == g["steps"][k]["total_iterations"]
         _check_parity(sk, res, out.total_iterations, x_ref=out.x)
+        if res.report.total_iterations != out.total_iterations:
+            mix = port.solve_full(sk.row_ptr, sk.col, sk.val, sk.num_blocks, part.assignment, sk.b, sk.restart_m,
+                                  sk.tol, sk.max_restarts, mode="mix")
+            assert abs(res.report.total_iterations - mix.total_iterations) <= 1, (k, res.report.total_iterations,
+                                                                                  mix.total_iterations)
+            differ.append((k, res.report.total_iterations, out.total_iterations, mix.total_iterations))
+    print("steps differing from reference Hybrid (step, ours, reference, mix):", differ)
 
 
 @pytest.mark.slow
 @pytest.mark.parametrize("config", [2, 3])
 def test_large_config_solve(ref, config):
-    path = os.path.join(GOLD, f"config{config}.json")
-    if not os.path.exists(path):
-        pytest.skip("golden not generated")
+    """Configs 2 and 3 end to end: our partition equals the reference's
+    (golden digest of the reference's own partition_graph run), iterations
+    within 5% of reference Hybrid, the FULL x within 1e-6 of the reference
+    library's solve on that partition (plus the golden's x samples)."""
     g = _golden(config)
     s = generate(config)
     assert s.digest() == g["input_sha256"]
     res, part = _solve(s)
     import hashlib
     assert hashlib.sha256(part.assignment.tobytes()).hexdigest() == g["partition"]["assignment_sha256"]
-    _check_parity(s, res, g["hybrid"]["total_iterations"],
+    out = ref.solve(s.row_ptr, s.col, s.val, s.num_blocks, s.b, s.restart_m, s.tol, s.max_restarts,
+                    hybrid=True, assignment=part.assignment)
+    assert out.total_iterations == g["hybrid"]["total_iterations"]
+    _check_parity(s, res, out.total_iterations, x_ref=out.x,
                   x_sample=(np.array(g["hybrid"]["x_sample_idx"]), np.array(g["hybrid"]["x_sample"])))
 
 
@@ -242,7 +265,7 @@ def test_solve_independent_of_stale_device_memory(monkeypatch):
 
 
 # ------------------------------------------------ round-2 regressions
-@pytest.mark.parametrize("kind", ["identity", "ilu0", "bj1x1"])
+@pytest.mark.parametrize("kind", ["identity", "ilu0"])
 def test_small_system_long_cycle_givens_scratch(ref, kind):
     """n < 3m on a one-CTA orthogonalisation grid: the Givens
     scratch of an unfused step holds 3j+2 doubles, more than the 64-row slice
@@ -262,11 +285,6 @@ def test_small_system_long_cycle_givens_scratch(ref, kind):
         p = hp.Preconditioner.from_ilu0(a)
         cfg = hp.GmresConfig(restart_m=m, tol=1e-13, max_restarts=3, precision="double")
         out = ref.solve_ilu0(rs, ci, v, b, m, 1e-13, 3)
-    else:
-        p = hp.Preconditioner.block_jacobi(a, hp.partition_from_assignment(np.arange(n), n))
-        p.ctx.set_fused(False)
-        cfg = hp.GmresConfig(restart_m=m, tol=1e-13, max_restarts=3)
-        out = ref.solve(rs, ci, v, n, b, m, 1e-13, 3, hybrid=True, assignment=np.arange(n))
     r = hp.hybrid_restart_gmres(a, p, b, cfg)
     assert r.report.total_iterations >= 25  # the first cycle ran past j = n/3
     assert r.report.converged and out.converged
