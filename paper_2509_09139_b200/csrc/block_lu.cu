@@ -871,29 +871,31 @@ __global__ void __launch_bounds__(NT, 2) k_block_lu_blk(LuParams p, int dlo, int
 // kLlMax), one CTA per block. Only the L part of the factor (every row that
 // was still active when a 32-column panel was factored, 32 multipliers each:
 // ~d^2/2 floats) lives in shared memory for the whole factorisation, plus the
-// current column panel X of all d rows; U leaves for HBM panel by panel. Per
-// column panel P (columns c0 .. c0 + 31):
-//   gather    the panel's columns of the block from the permuted CSR (per-row
-//             cursors; FP64 -> FP32 RNE), X zero-filled;
-//   for each earlier panel Q:
-//     (i)  the 32 pivot rows of Q: forward substitution with Q's unit-lower
-//          L11 (warp 0, lane per column, m-outer so the 31 chains interleave);
-//     (ii) the rows still active after Q: rank-32 update X -= L_Q U_Q (lane
-//          per column, U column in registers, multipliers as float4
-//          broadcasts, four rows in flight per warp);
-//   factor    the panel's active rows (thread per row, 32 entries in
-//             registers): per column a CTA argmax (ties to the smaller row)
-//             with ONE barrier — every warp publishes its candidate row's
-//             entries with its key, double-buffered — then the rank-1 update
-//             in registers;
-//   store     the panel's multipliers of every active row to L_P; the pivot
-//             rows' L entries (all earlier panels) and the finished U column
-//             panel go to the packed output panels.
+// current column panel X of all d rows; U leaves for HBM panel by panel. L_Q
+// (panel Q) stores Q's 32 pivot rows first, in pivot order, then the rows
+// still active after Q. Per column panel P (columns c0 .. c0 + 31):
+//   gather  the panel's columns from the permuted CSR (per-row cursors, FP64
+//           -> FP32 RNE into a zero-filled X);
+//   for each earlier panel Q, pipelined so that the one-warp triangular solve
+//   of Q overlaps the bulk rank-32 update of Q - 1:
+//     A_Q  every warp: (ii)_{Q-1} = X[r] -= L_{Q-1}[r] U_{Q-1} on Q's 32 pivot rows;
+//     B_Q  warp 0: (i)_Q, Q's pivot rows x_k -= sum_{m<k} L11(k, m) x_m (lane
+//          per column; L11 rows at fixed offsets of L_Q, float4 broadcasts);
+//          the other warps: (ii)_{Q-1} on the remaining rows active after Q;
+//   then every warp: (ii)_{P-1} on the rows still active;
+//   factor  the panel's active rows (thread per row, 32 entries in registers;
+//           only the warps holding rows, named barrier): per column each warp
+//           publishes its candidate (max |x|, ties to the smaller row) with
+//           the candidate's row and its regularised pivot (the owner does the
+//           FP64 test), ONE barrier, a warp-wide argmax over the candidates,
+//           the rank-1 update in registers;
+//   store   L_P; the new pivot rows' L entries and the finished U column panel
+//           to the packed output panels.
 // Every element receives exactly the fmaf(-l, u, a) chain, in ascending
 // column order, that the right-looking kernels apply (left- and right-looking
 // only reorder independent chains), the divisions and the pivot rule are the
 // same: factors and pivots are bit-identical to k_block_lu_blk / k_block_lu.
-constexpr int kLlMax = 288;  // upper bound; the launcher checks the shared-memory budget
+constexpr int kLlMax = 288;  // the launcher checks the shared-memory budget
 
 __host__ __device__ inline int ll_lrows(int d) {  // L_Q rows kept: panels 0 .. T-2
     const int T = (d + 31) / 32;
@@ -910,7 +912,7 @@ __host__ __device__ inline size_t ll_smem_bytes(int dhi) {
     return (size_t)lr * 32 * sizeof(float)          // L_Q rows
            + (size_t)dhi * 32 * sizeof(float)       // X: current column panel, all rows
            + (size_t)2 * NW * 32 * sizeof(float)    // candidate rows (double buffered)
-           + (size_t)2 * NW * 4 * sizeof(int)       // candidate key / row / position
+           + (size_t)2 * NW * 4 * sizeof(int)       // candidate key / row / owner / pivot
            + (size_t)lr * sizeof(short)             // row id of every L_Q row
            + (size_t)(T > 1 ? T - 1 : 1) * dhi * sizeof(short)  // position of row r in L_Q
            + (size_t)3 * dhi * sizeof(short)        // ppos, act, prow
@@ -919,6 +921,66 @@ __host__ __device__ inline size_t ll_smem_bytes(int dhi) {
 
 // swizzled X: quad (c / 4) of row r at quad slot (c / 4) ^ (r & 7)
 __device__ __forceinline__ int xq(int r, int q) { return r * 32 + ((q ^ (r & 7)) << 2); }
+
+__device__ __forceinline__ void bar_named(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// X[r][lane] -= sum_m L[pos][m] u[m], u = this lane's column of the 32 pivot
+// rows prv[0..31] (U of the panel behind L), for the rows given by (pos, row)
+// pairs; four rows in flight per warp. `rows(i)` yields {pos, row} or pos < 0.
+template <class Rows>
+__device__ __forceinline__ void ll_rank32(float* X, const float* L, const short* prv, int lane, int i0, int i1,
+                                          int step, Rows rows) {
+    if (i0 >= i1) return;
+    float u[32];
+#pragma unroll
+    for (int m = 0; m < 32; ++m) u[m] = X[xq(prv[m], lane >> 2) + (lane & 3)];
+    for (int i = i0; i < i1; i += 4 * step) {
+        int pos[4], rr[4];
+        float v[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int2 pr = (i + t * step < i1) ? rows(i + t * step) : make_int2(-1, 0);
+            pos[t] = pr.x;
+            rr[t] = pr.y;
+            v[t] = pos[t] >= 0 ? X[xq(rr[t], lane >> 2) + (lane & 3)] : 0.0f;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const float4 l4 = *reinterpret_cast<const float4*>(L + (size_t)max(pos[t], 0) * 32 + 4 * q);
+                v[t] = fmaf(-l4.x, u[4 * q + 0], v[t]);
+                v[t] = fmaf(-l4.y, u[4 * q + 1], v[t]);
+                v[t] = fmaf(-l4.z, u[4 * q + 2], v[t]);
+                v[t] = fmaf(-l4.w, u[4 * q + 3], v[t]);
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+            if (pos[t] >= 0) X[xq(rr[t], lane >> 2) + (lane & 3)] = v[t];
+    }
+}
+
+// x_k -= sum_{m<k} L11(k, m) x_m, m ascending per k (the fmaf chain of the
+// right-looking U12 solve), four m per step: L11 row k at LQ + 32 k.
+template <int M0>
+__device__ __forceinline__ void ll_trsv(float (&x)[32], const float* LQ) {
+#pragma unroll
+    for (int mm = 1; mm < 4; ++mm)
+#pragma unroll
+        for (int m = 0; m < mm; ++m) x[M0 + mm] = fmaf(-LQ[(M0 + mm) * 32 + M0 + m], x[M0 + m], x[M0 + mm]);
+#pragma unroll
+    for (int k = M0 + 4; k < 32; ++k) {
+        const float4 l4 = *reinterpret_cast<const float4*>(LQ + k * 32 + M0);
+        x[k] = fmaf(-l4.x, x[M0 + 0], x[k]);
+        x[k] = fmaf(-l4.y, x[M0 + 1], x[k]);
+        x[k] = fmaf(-l4.z, x[M0 + 2], x[k]);
+        x[k] = fmaf(-l4.w, x[M0 + 3], x[k]);
+    }
+    if constexpr (M0 + 4 < 32) ll_trsv<M0 + 4>(x, LQ);
+}
 
 template <int NT>
 __global__ void __launch_bounds__(NT, 1) k_block_lu_ll(LuParams p, int dlo, int dhi) {
@@ -929,14 +991,15 @@ __global__ void __launch_bounds__(NT, 1) k_block_lu_ll(LuParams p, int dlo, int 
     float* Ls = llsm;                                          // [lrmax][32]
     float* X = Ls + (size_t)lrmax * 32;                        // [dhi][32] swizzled
     float* cand_v = X + (size_t)dhi * 32;                      // [2][NW][32]
-    int* cand_i = reinterpret_cast<int*>(cand_v + 2 * NW * 32);  // [2][NW][4]: key, row, pos
+    int* cand_i = reinterpret_cast<int*>(cand_v + 2 * NW * 32);  // [2][NW][4]: key, row, owner, pivot bits
     short* rowQ = reinterpret_cast<short*>(cand_i + 2 * NW * 4);  // [lrmax]
     short* posQ = rowQ + lrmax;                                // [Tmax-1][dhi]
     short* ppos = posQ + (size_t)(Tmax > 1 ? Tmax - 1 : 1) * dhi;  // pivot position of row r (or 0x7fff)
-    short* act = ppos + dhi;                                   // active rows
+    short* act = ppos + dhi;                                   // active rows (stable order)
     short* prow = act + dhi;                                   // pivot row of position k
     __shared__ double redd[NW];
     __shared__ int lofs[16];                                   // first L row of panel Q
+    __shared__ int nact_sh;
 
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
 
@@ -1005,222 +1068,144 @@ __global__ void __launch_bounds__(NT, 1) k_block_lu_ll(LuParams p, int dlo, int 
                 }
             }
             __syncthreads();
-            // ---- left-looking updates from every earlier panel
-            for (int Q = 0; Q < P; ++Q) {
+            // ---- left-looking updates from the earlier panels
+            for (int Q = 0; Q <= P; ++Q) {
                 const int q0 = 32 * Q;
-                const float* LQ = Ls + (size_t)lofs[Q] * 32;
-                const short* rQ = rowQ + lofs[Q];
-                const short* pQ = posQ + (size_t)Q * dhi;
-                if (wid == 0) {  // (i) pivot rows of Q: x_k -= sum_{m<k} L(k, m) x_m
-                    float x[32];
-                    int lp[32];
-#pragma unroll
-                    for (int m = 0; m < 32; ++m) {
-                        const int r = prow[q0 + m];
-                        lp[m] = pQ[r];
-                        x[m] = X[xq(r, lane >> 2) + (lane & 3)];
+                const short* prv = prow + (Q > 0 ? q0 - 32 : 0);  // U_{Q-1}: pivot rows of Q - 1
+                const float* Lp = Q > 0 ? Ls + (size_t)lofs[Q - 1] * 32 : Ls;
+                const short* posp = posQ + (size_t)(Q > 0 ? Q - 1 : 0) * dhi;
+                if (Q == P) {  // (ii)_{P-1} on the rows still active (positions >= 32 of L_{P-1})
+                    if (Q > 0) {
+                        const short* rP = rowQ + lofs[Q - 1];
+                        ll_rank32(X, Lp, prv, lane, 32 + wid, d - (q0 - 32), NW,
+                                  [&](int a) { return make_int2(a, (int)rP[a]); });
+                        __syncthreads();
                     }
-#pragma unroll 8
-                    for (int m0 = 0; m0 < 32; m0 += 4) {
-#pragma unroll
-                        for (int mm = 1; mm < 4; ++mm) {  // the 4x4 diagonal piece
-                            const float* lr = LQ + (size_t)lp[m0 + mm] * 32 + m0;
-#pragma unroll
-                            for (int m = 0; m < mm; ++m) x[m0 + mm] = fmaf(-lr[m], x[m0 + m], x[m0 + mm]);
-                        }
-#pragma unroll 28
-                        for (int k = m0 + 4; k < 32; ++k) {
-                            const float4 l4 = *reinterpret_cast<const float4*>(LQ + (size_t)lp[k] * 32 + m0);
-                            x[k] = fmaf(-l4.x, x[m0 + 0], x[k]);
-                            x[k] = fmaf(-l4.y, x[m0 + 1], x[k]);
-                            x[k] = fmaf(-l4.z, x[m0 + 2], x[k]);
-                            x[k] = fmaf(-l4.w, x[m0 + 3], x[k]);
-                        }
-                    }
-#pragma unroll
-                    for (int m = 0; m < 32; ++m) X[xq(prow[q0 + m], lane >> 2) + (lane & 3)] = x[m];
-                }
-                __syncthreads();
-                // (ii) rows active after Q: X[r] -= L_Q[r] U_Q
-                {
-                    float u[32];
-#pragma unroll
-                    for (int m = 0; m < 32; ++m) u[m] = X[xq(prow[q0 + m], lane >> 2) + (lane & 3)];
-                    const int nQ = d - q0;
-                    const int qhi = q0 + 32;
-                    for (int a0 = 4 * wid; a0 < nQ; a0 += 4 * NW) {
-                        int rr[4];
-                        bool ok[4];
-                        float v[4];
-#pragma unroll
-                        for (int t = 0; t < 4; ++t) {
-                            const int a = a0 + t;
-                            rr[t] = a < nQ ? rQ[a] : 0;
-                            ok[t] = a < nQ && ppos[rr[t]] >= qhi;
-                            v[t] = ok[t] ? X[xq(rr[t], lane >> 2) + (lane & 3)] : 0.0f;
-                        }
-#pragma unroll
-                        for (int q = 0; q < 8; ++q) {
-#pragma unroll
-                            for (int t = 0; t < 4; ++t) {
-                                const int a = min(a0 + t, nQ - 1);
-                                const float4 l4 = *reinterpret_cast<const float4*>(LQ + (size_t)a * 32 + 4 * q);
-                                v[t] = fmaf(-l4.x, u[4 * q + 0], v[t]);
-                                v[t] = fmaf(-l4.y, u[4 * q + 1], v[t]);
-                                v[t] = fmaf(-l4.z, u[4 * q + 2], v[t]);
-                                v[t] = fmaf(-l4.w, u[4 * q + 3], v[t]);
-                            }
-                        }
-#pragma unroll
-                        for (int t = 0; t < 4; ++t)
-                            if (ok[t]) X[xq(rr[t], lane >> 2) + (lane & 3)] = v[t];
-                    }
-                }
-                __syncthreads();
-            }
-            // ---- factor the panel: thread a owns active row act[a]
-            const bool has = tid < na;
-            const int myrow = has ? act[tid] : 0;
-            bool fl = !has;  // pivotal (or no row)
-            float rv[32];
-            {
-                const float4* xr = reinterpret_cast<const float4*>(X + myrow * 32);
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    const float4 t4 = has ? xr[q ^ (myrow & 7)] : make_float4(0.f, 0.f, 0.f, 0.f);
-                    rv[4 * q + 0] = t4.x;
-                    rv[4 * q + 1] = t4.y;
-                    rv[4 * q + 2] = t4.z;
-                    rv[4 * q + 3] = t4.w;
-                }
-            }
-#pragma unroll
-            for (int c = 0; c < 32; ++c) {
-                if (c >= kw) break;
-                const int k = c0 + c;
-                // warp candidate: max |x|, ties -> smaller row
-                const unsigned key = fl ? 0u : __float_as_uint(fabsf(rv[c])) + 1u;
-                unsigned kmx;
-                const int wr = warp_pivot_row(key, fl ? 0x7fffffff : myrow, &kmx);
-                const unsigned own = __ballot_sync(0xffffffffu, !fl && key == kmx && myrow == wr);
-                float* cv = cand_v + (size_t)(buf * NW + wid) * 32;
-                int* ci4 = cand_i + (buf * NW + wid) * 4;
-                if (own && lane == __ffs(own) - 1) {
-#pragma unroll
-                    for (int q = 0; q < 8; ++q)
-                        reinterpret_cast<float4*>(cv)[q] =
-                            make_float4(rv[4 * q], rv[4 * q + 1], rv[4 * q + 2], rv[4 * q + 3]);
-                    ci4[0] = (int)kmx;
-                    ci4[1] = wr;
-                    ci4[2] = tid;
-                } else if (lane == 0 && !own) {
-                    ci4[0] = 0;
-                    ci4[1] = 0x7fffffff;
-                    ci4[2] = -1;
-                }
-                __syncthreads();
-                // winner over the warps' candidates (identical in every thread)
-                unsigned fk = 0u;
-                int frow = 0x7fffffff, fw = 0;
-#pragma unroll
-                for (int w = 0; w < NW; ++w) {
-                    const int* cw = cand_i + (buf * NW + w) * 4;
-                    const unsigned kk = (unsigned)cw[0];
-                    const int rw = cw[1];
-                    if (kk > fk || (kk == fk && rw < frow)) {
-                        fk = kk;
-                        frow = rw;
-                        fw = w;
-                    }
-                }
-                const float* Pv = cand_v + (size_t)(buf * NW + fw) * 32;
-                const int owner = cand_i[(buf * NW + fw) * 4 + 2];
-                buf ^= 1;
-                // regularize_pivot (lu.cpp:10-20), FP64, identical in every thread
-                const double pvd = (double)Pv[c];
-                const bool keep = pivot_keep(pvd, norm, p.eps);
-                const double val = keep ? pvd : ((pvd < 0.0 ? -1.0 : 1.0) * p.eps * norm);
-                if (val == 0.0) {
-                    if (tid == 0) atomicMin(p.singular, ((unsigned long long)b << 32) | (unsigned)k);
-                    abort = true;
                     break;
                 }
-                if (!keep) {
-                    ++nperturb;
-                    if (tid == 0) {
-                        const int slot = atomicAdd(p.pert_n, 1);
-                        if (slot < p.pert_cap) p.pert[slot] = PertRecord{b, k, pvd, val};
+                if (Q > 0) {  // A_Q: (ii)_{Q-1} on Q's pivot rows
+                    ll_rank32(X, Lp, prv, lane, wid, 32, NW, [&](int i) {
+                        const int r = prow[q0 + i];
+                        return make_int2((int)posp[r], r);
+                    });
+                    __syncthreads();
+                }
+                if (wid == 0) {  // B_Q, warp 0: (i)_Q, L11 of Q = the first 32 rows of L_Q
+                    const float* LQ = Ls + (size_t)lofs[Q] * 32;
+                    float x[32];
+#pragma unroll
+                    for (int m = 0; m < 32; ++m) x[m] = X[xq(prow[q0 + m], lane >> 2) + (lane & 3)];
+                    ll_trsv<0>(x, LQ);
+#pragma unroll
+                    for (int m = 0; m < 32; ++m) X[xq(prow[q0 + m], lane >> 2) + (lane & 3)] = x[m];
+                } else if (Q > 0) {  // B_Q, other warps: (ii)_{Q-1} on the rows active after Q
+                    const short* rP = rowQ + lofs[Q - 1];
+                    const int qhi = q0 + 32;
+                    ll_rank32(X, Lp, prv, lane, 32 + (wid - 1), d - (q0 - 32), NW - 1, [&](int a) {
+                        const int r = rP[a];
+                        return make_int2(ppos[r] >= qhi ? a : -1, r);  // Q's pivot rows: done in A_Q
+                    });
+                }
+                __syncthreads();
+            }
+            // ---- factor the panel: thread a owns active row act[a]; only
+            // the warps holding rows take part (named barrier 1)
+            const int nwa = (na + 31) >> 5;
+            if (wid < nwa) {
+                const bool has = tid < na;
+                const int myrow = has ? act[tid] : 0;
+                bool fl = !has;  // pivotal (or no row)
+                float rv[32];
+                {
+                    const float4* xr = reinterpret_cast<const float4*>(X + myrow * 32);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const float4 t4 = has ? xr[q ^ (myrow & 7)] : make_float4(0.f, 0.f, 0.f, 0.f);
+                        rv[4 * q + 0] = t4.x;
+                        rv[4 * q + 1] = t4.y;
+                        rv[4 * q + 2] = t4.z;
+                        rv[4 * q + 3] = t4.w;
                     }
                 }
-                const float pv = (float)val;
-                if (tid == owner) {
-                    rv[c] = pv;
-                    fl = true;
-                    prow[k] = (short)myrow;
-                    ppos[myrow] = (short)k;
-                } else if (!fl) {
-                    const float l = rv[c] / pv;  // L(i,k) = x_i / pivot (lu.cpp:207)
-                    rv[c] = l;
 #pragma unroll
-                    for (int c2 = c + 1; c2 < 32; ++c2) rv[c2] = fmaf(-l, Pv[c2], rv[c2]);
+                for (int c = 0; c < 32; ++c) {
+                    if (c >= kw) break;
+                    const int k = c0 + c;
+                    // warp candidate: max |x|, ties -> smaller row
+                    const unsigned key = fl ? 0u : __float_as_uint(fabsf(rv[c])) + 1u;
+                    unsigned kmx;
+                    const int wr = warp_pivot_row(key, fl ? 0x7fffffff : myrow, &kmx);
+                    const unsigned own = __ballot_sync(0xffffffffu, !fl && key == kmx && myrow == wr);
+                    float* cv = cand_v + (size_t)(buf * NW + wid) * 32;
+                    int* ci4 = cand_i + (buf * NW + wid) * 4;
+                    if (own && lane == __ffs(own) - 1) {
+#pragma unroll
+                        for (int q = 0; q < 8; ++q)
+                            reinterpret_cast<float4*>(cv)[q] =
+                                make_float4(rv[4 * q], rv[4 * q + 1], rv[4 * q + 2], rv[4 * q + 3]);
+                        // regularize_pivot (lu.cpp:10-20) in FP64 by the candidate's owner
+                        const double pvd = (double)rv[c];
+                        const bool keep = pivot_keep(pvd, norm, p.eps);
+                        const double val = keep ? pvd : ((pvd < 0.0 ? -1.0 : 1.0) * p.eps * norm);
+                        const float pvf = (float)val;
+                        reinterpret_cast<int4*>(ci4)[0] =
+                            make_int4((int)kmx, wr, tid, (int)(__float_as_uint(pvf) ^ 0u));
+                        if (!keep) ci4[1] = wr | (int)0x40000000;  // perturbed flag in the row word
+                        if (val == 0.0) ci4[1] = wr | (int)0x20000000;  // singular
+                    } else if (lane == 0 && !own) {
+                        reinterpret_cast<int4*>(ci4)[0] = make_int4(0, 0x7fffffff, -1, 0);
+                    }
+                    bar_named(1, nwa * 32);
+                    // winner over the active warps' candidates (warp-wide, identical in every warp)
+                    int4 cw = lane < nwa ? reinterpret_cast<const int4*>(cand_i + buf * NW * 4)[lane]
+                                         : make_int4(0, 0x7fffffff, -1, 0);
+                    const int crow = cw.y & 0x1fffffff;
+                    unsigned kk;
+                    const int frow = warp_pivot_row((unsigned)cw.x, lane < nwa && cw.x != 0 ? crow : 0x7fffffff, &kk);
+                    const int fw = __ffs(__ballot_sync(0xffffffffu, lane < nwa && (unsigned)cw.x == kk && crow == frow)) - 1;
+                    int4 win;
+                    win.x = __shfl_sync(0xffffffffu, cw.x, fw);
+                    win.y = __shfl_sync(0xffffffffu, cw.y, fw);
+                    win.z = __shfl_sync(0xffffffffu, cw.z, fw);
+                    win.w = __shfl_sync(0xffffffffu, cw.w, fw);
+                    const float* Pv = cand_v + (size_t)(buf * NW + fw) * 32;
+                    buf ^= 1;
+                    const float pv = __uint_as_float((unsigned)win.w);
+                    if (win.y & 0x20000000) {
+                        if (tid == 0) atomicMin(p.singular, ((unsigned long long)b << 32) | (unsigned)k);
+                        abort = true;
+                        break;
+                    }
+                    if (win.y & 0x40000000) {
+                        ++nperturb;
+                        if (tid == 0) {
+                            const int slot = atomicAdd(p.pert_n, 1);
+                            if (slot < p.pert_cap) p.pert[slot] = PertRecord{b, k, (double)Pv[c], (double)pv};
+                        }
+                    }
+                    if (tid == win.z) {
+                        rv[c] = pv;
+                        fl = true;
+                        prow[k] = (short)myrow;
+                        ppos[myrow] = (short)k;
+                    } else if (!fl) {
+                        const float l = rv[c] / pv;  // L(i,k) = x_i / pivot (lu.cpp:207)
+                        rv[c] = l;
+#pragma unroll
+                        for (int c2 = c + 1; c2 < 32; ++c2) rv[c2] = fmaf(-l, Pv[c2], rv[c2]);
+                    }
                 }
-            }
-            if (abort) break;
-            // ---- the panel's entries back to X; multipliers of every active row to L_P
-            if (has) {
-                float4* xr = reinterpret_cast<float4*>(X + myrow * 32);
-#pragma unroll
-                for (int q = 0; q < 8; ++q)
-                    xr[q ^ (myrow & 7)] = make_float4(rv[4 * q], rv[4 * q + 1], rv[4 * q + 2], rv[4 * q + 3]);
-                if (P + 1 < T) {
-                    float4* lr = reinterpret_cast<float4*>(Ls + ((size_t)lofs[P] + tid) * 32);
+                if (!abort && has) {
+                    float4* xr = reinterpret_cast<float4*>(X + myrow * 32);
 #pragma unroll
                     for (int q = 0; q < 8; ++q)
-                        lr[q] = make_float4(rv[4 * q], rv[4 * q + 1], rv[4 * q + 2], rv[4 * q + 3]);
-                    rowQ[lofs[P] + tid] = (short)myrow;
-                    posQ[(size_t)P * dhi + myrow] = (short)tid;
+                        xr[q ^ (myrow & 7)] = make_float4(rv[4 * q], rv[4 * q + 1], rv[4 * q + 2], rv[4 * q + 3]);
                 }
             }
-            __syncthreads();
-            // ---- output: chunks (t, P) for t <= P (U / L11\U11 from X) and
-            // (P, Q) for Q < P (the new pivot rows' L from L_Q); chunk (t, u)
-            // = rows 32t.. of panel t, quads 8u .. 8u + nq(u), [quad][row][4]
-            {
-                const int nqP = min(8, dp4 / 4 - 8 * P);
-                for (int e = tid; e < (P + 1) * 8 * 32; e += NT) {  // (t, P)
-                    const int t = e >> 8, qi = (e >> 5) & 7, kr = e & 31;
-                    if (qi >= nqP) continue;
-                    const int k = 32 * t + kr;
-                    const int cq = 4 * (8 * P + qi);
-                    float4 v;
-                    if (k < d) {
-                        const int r = prow[k];
-                        v = *reinterpret_cast<const float4*>(X + xq(r, qi));
-                        if (cq + 0 >= d) v.x = 0.f;
-                        if (cq + 1 >= d) v.y = (k == cq + 1) ? 1.f : 0.f;
-                        if (cq + 2 >= d) v.z = (k == cq + 2) ? 1.f : 0.f;
-                        if (cq + 3 >= d) v.w = (k == cq + 3) ? 1.f : 0.f;
-                    } else {
-                        v = make_float4(k == cq ? 1.f : 0.f, k == cq + 1 ? 1.f : 0.f, k == cq + 2 ? 1.f : 0.f,
-                                        k == cq + 3 ? 1.f : 0.f);
-                    }
-                    __stcs(reinterpret_cast<float4*>(F + (size_t)t * 32 * dp4 + (size_t)(8 * P + qi) * 128 + kr * 4),
-                           v);
-                }
-                for (int e = tid; e < P * 8 * 32; e += NT) {  // (P, Q), Q < P
-                    const int Q = e >> 8, qi = (e >> 5) & 7, kr = e & 31;
-                    const int k = c0 + kr;
-                    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-                    if (k < d) {
-                        const int r = prow[k];
-                        v = *reinterpret_cast<const float4*>(Ls + ((size_t)lofs[Q] + posQ[(size_t)Q * dhi + r]) * 32 +
-                                                             4 * qi);
-                    }
-                    __stcs(reinterpret_cast<float4*>(F + (size_t)P * 32 * dp4 + (size_t)(8 * Q + qi) * 128 + kr * 4),
-                           v);
-                }
-            }
-            // ---- drop the panel's pivot rows from the active list (stable)
+            abort = __syncthreads_or(abort);
+            if (abort) break;
+            // ---- compact the active list (stable) and store L_P: the 32 pivot
+            // rows first, in pivot order, then the rows still active
             if (wid == 0) {
                 int w = 0;
                 for (int base = 0; base < na; base += 32) {
@@ -1233,8 +1218,58 @@ __global__ void __launch_bounds__(NT, 1) k_block_lu_ll(LuParams p, int dlo, int 
                     w += __popc(m);
                     __syncwarp();
                 }
+                if (lane == 0) nact_sh = w;
             }
-            na -= kw;
+            __syncthreads();
+            const int nnew = nact_sh;
+            if (P + 1 < T) {
+                const int lo = lofs[P];
+                for (int i = tid; i < 32 + nnew; i += NT) {
+                    const int r = i < 32 ? prow[c0 + i] : act[i - 32];
+                    const float4* xr = reinterpret_cast<const float4*>(X + r * 32);
+                    float4* lr = reinterpret_cast<float4*>(Ls + ((size_t)lo + i) * 32);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) lr[q] = xr[q ^ (r & 7)];
+                    rowQ[lo + i] = (short)r;
+                    posQ[(size_t)P * dhi + r] = (short)i;
+                }
+            }
+            // ---- output: chunks (t, P) for t <= P (U / L11\U11 from X) and
+            // (P, Q) for Q < P (the new pivot rows' L from L_Q); chunk (t, u)
+            // = rows 32t.. of panel t, quads 8u .. 8u + nq(u), [quad][row][4]
+            {
+                const int nqP = min(8, dp4 / 4 - 8 * P);
+                for (int e = tid; e < (P + 1) * 8 * 32; e += NT) {  // (t, P)
+                    const int t = e >> 8, qi = (e >> 5) & 7, kr = e & 31;
+                    if (qi >= nqP) continue;
+                    const int k = 32 * t + kr;
+                    const int cq = 4 * (8 * P + qi);
+                    float4 v;
+                    if (k < d) {
+                        v = *reinterpret_cast<const float4*>(X + xq(prow[k], qi));
+                        if (cq + 0 >= d) v.x = 0.f;
+                        if (cq + 1 >= d) v.y = 0.f;
+                        if (cq + 2 >= d) v.z = 0.f;
+                        if (cq + 3 >= d) v.w = 0.f;
+                    } else {
+                        v = make_float4(k == cq ? 1.f : 0.f, k == cq + 1 ? 1.f : 0.f, k == cq + 2 ? 1.f : 0.f,
+                                        k == cq + 3 ? 1.f : 0.f);
+                    }
+                    __stcs(reinterpret_cast<float4*>(F + (size_t)t * 32 * dp4 + (size_t)(8 * P + qi) * 128 + kr * 4),
+                           v);
+                }
+                for (int e = tid; e < P * 8 * 32; e += NT) {  // (P, Q), Q < P
+                    const int Q = e >> 8, qi = (e >> 5) & 7, kr = e & 31;
+                    const int k = c0 + kr;
+                    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (k < d)
+                        v = *reinterpret_cast<const float4*>(
+                            Ls + ((size_t)lofs[Q] + posQ[(size_t)Q * dhi + prow[k]]) * 32 + 4 * qi);
+                    __stcs(reinterpret_cast<float4*>(F + (size_t)P * 32 * dp4 + (size_t)(8 * Q + qi) * 128 + kr * 4),
+                           v);
+                }
+            }
+            na = nnew;
             __syncthreads();
         }
         if (tid == 0) p.pert_count[b] = nperturb;
