@@ -39,6 +39,16 @@ __device__ __forceinline__ unsigned long long umax64(unsigned long long a, unsig
     return a > b ? a : b;
 }
 
+// x / pv, IEEE round-to-nearest (the multiplier of lu.cpp:207). A zero
+// numerator over a finite nonzero pivot is the signed zero: returned without
+// the division, whose range check (FCHK) sends zero numerators — most
+// entries of a sparse block — down the slow software path.
+__device__ __forceinline__ float div_mult(float x, float pv) {
+    if (x == 0.0f && pv != 0.0f && isfinite(pv))
+        return __int_as_float((__float_as_int(x) ^ __float_as_int(pv)) & (int)0x80000000);
+    return x / pv;
+}
+
 // regularize_pivot's keep test (lu.cpp:10-20): norm == 0 ? p != 0 :
 // RN(|p| / norm) >= eps. A product bracket decides it without the FP64
 // division whenever |p| is not within 2^-48 (relative) of eps*norm: with
@@ -176,7 +186,7 @@ __global__ void __launch_bounds__(kLuThreads) k_block_lu(LuParams p, int mode) {
             for (int a = wid; a < na; a += NW) {
                 const int r = act[a];
                 float* arow = A + r * ld;
-                const float l = arow[k] / pv;
+                const float l = div_mult(arow[k], pv);
                 for (int j = k + 1 + lane; j < d; j += 32) arow[j] = fmaf(-l, urow[j], arow[j]);
                 __syncwarp();
                 if (lane == 0) arow[k] = l;
@@ -300,7 +310,7 @@ __global__ void __launch_bounds__(256) k_block_lu_warp(LuParams p, int dw, int l
                 const int r = lane + 32 * q;
                 lq[q] = 0.0f;
                 if (r < d && !((pivoted >> q) & 1u)) {
-                    lq[q] = A[r * ld + k] / pv;  // L(i,k) = x_i / pivot (lu.cpp:207)
+                    lq[q] = div_mult(A[r * ld + k], pv);  // L(i,k) = x_i / pivot (lu.cpp:207)
                     A[r * ld + k] = lq[q];
                 }
             }
@@ -488,7 +498,7 @@ __global__ void __launch_bounds__(64) k_block_lu_pair(LuParams p, int dw, int ld
                 const int r = lane + 32 * (2 * q + w);
                 lq[q] = 0.0f;
                 if (r < d && !((pivoted >> q) & 1u)) {
-                    lq[q] = A[r * ld + k] / pv;  // L(i,k) = x_i / pivot (lu.cpp:207)
+                    lq[q] = div_mult(A[r * ld + k], pv);  // L(i,k) = x_i / pivot (lu.cpp:207)
                     A[r * ld + k] = lq[q];
                 }
             }
@@ -733,7 +743,7 @@ __global__ void __launch_bounds__(NT, 2) k_block_lu_blk(LuParams p, int dlo, int
                         fl[i] = true;
                         continue;
                     }
-                    const float l = rv[i][c] / pv;  // L(i,k) = x_i / pivot (lu.cpp:207)
+                    const float l = div_mult(rv[i][c], pv);  // L(i,k) = x_i / pivot (lu.cpp:207)
                     rv[i][c] = l;
 #pragma unroll
                     for (int c2 = c + 1; c2 < 32; ++c2) rv[i][c2] = fmaf(-l, Pv[c2], rv[i][c2]);
@@ -1143,15 +1153,7 @@ __global__ void __launch_bounds__(NT, 1) k_block_lu_ll(LuParams p, int dlo, int 
                         for (int q = 0; q < 8; ++q)
                             reinterpret_cast<float4*>(cv)[q] =
                                 make_float4(rv[4 * q], rv[4 * q + 1], rv[4 * q + 2], rv[4 * q + 3]);
-                        // regularize_pivot (lu.cpp:10-20) in FP64 by the candidate's owner
-                        const double pvd = (double)rv[c];
-                        const bool keep = pivot_keep(pvd, norm, p.eps);
-                        const double val = keep ? pvd : ((pvd < 0.0 ? -1.0 : 1.0) * p.eps * norm);
-                        const float pvf = (float)val;
-                        reinterpret_cast<int4*>(ci4)[0] =
-                            make_int4((int)kmx, wr, tid, (int)(__float_as_uint(pvf) ^ 0u));
-                        if (!keep) ci4[1] = wr | (int)0x40000000;  // perturbed flag in the row word
-                        if (val == 0.0) ci4[1] = wr | (int)0x20000000;  // singular
+                        reinterpret_cast<int4*>(ci4)[0] = make_int4((int)kmx, wr, tid, 0);
                     } else if (lane == 0 && !own) {
                         reinterpret_cast<int4*>(ci4)[0] = make_int4(0, 0x7fffffff, -1, 0);
                     }
@@ -1159,37 +1161,36 @@ __global__ void __launch_bounds__(NT, 1) k_block_lu_ll(LuParams p, int dlo, int 
                     // winner over the active warps' candidates (warp-wide, identical in every warp)
                     int4 cw = lane < nwa ? reinterpret_cast<const int4*>(cand_i + buf * NW * 4)[lane]
                                          : make_int4(0, 0x7fffffff, -1, 0);
-                    const int crow = cw.y & 0x1fffffff;
                     unsigned kk;
-                    const int frow = warp_pivot_row((unsigned)cw.x, lane < nwa && cw.x != 0 ? crow : 0x7fffffff, &kk);
-                    const int fw = __ffs(__ballot_sync(0xffffffffu, lane < nwa && (unsigned)cw.x == kk && crow == frow)) - 1;
-                    int4 win;
-                    win.x = __shfl_sync(0xffffffffu, cw.x, fw);
-                    win.y = __shfl_sync(0xffffffffu, cw.y, fw);
-                    win.z = __shfl_sync(0xffffffffu, cw.z, fw);
-                    win.w = __shfl_sync(0xffffffffu, cw.w, fw);
+                    const int frow = warp_pivot_row((unsigned)cw.x, lane < nwa && cw.x != 0 ? cw.y : 0x7fffffff, &kk);
+                    const int fw = __ffs(__ballot_sync(0xffffffffu, lane < nwa && (unsigned)cw.x == kk && cw.y == frow)) - 1;
+                    const int owner = __shfl_sync(0xffffffffu, cw.z, fw);
                     const float* Pv = cand_v + (size_t)(buf * NW + fw) * 32;
                     buf ^= 1;
-                    const float pv = __uint_as_float((unsigned)win.w);
-                    if (win.y & 0x20000000) {
+                    // regularize_pivot (lu.cpp:10-20), FP64, identical in every thread
+                    const double pvd = (double)Pv[c];
+                    const bool keep = pivot_keep(pvd, norm, p.eps);
+                    const double val = keep ? pvd : ((pvd < 0.0 ? -1.0 : 1.0) * p.eps * norm);
+                    if (val == 0.0) {
                         if (tid == 0) atomicMin(p.singular, ((unsigned long long)b << 32) | (unsigned)k);
                         abort = true;
                         break;
                     }
-                    if (win.y & 0x40000000) {
+                    if (!keep) {
                         ++nperturb;
                         if (tid == 0) {
                             const int slot = atomicAdd(p.pert_n, 1);
-                            if (slot < p.pert_cap) p.pert[slot] = PertRecord{b, k, (double)Pv[c], (double)pv};
+                            if (slot < p.pert_cap) p.pert[slot] = PertRecord{b, k, pvd, val};
                         }
                     }
-                    if (tid == win.z) {
+                    const float pv = (float)val;
+                    if (tid == owner) {
                         rv[c] = pv;
                         fl = true;
                         prow[k] = (short)myrow;
                         ppos[myrow] = (short)k;
                     } else if (!fl) {
-                        const float l = rv[c] / pv;  // L(i,k) = x_i / pivot (lu.cpp:207)
+                        const float l = div_mult(rv[c], pv);  // L(i,k) = x_i / pivot (lu.cpp:207)
                         rv[c] = l;
 #pragma unroll
                         for (int c2 = c + 1; c2 < 32; ++c2) rv[c2] = fmaf(-l, Pv[c2], rv[c2]);
