@@ -67,6 +67,35 @@ __device__ __forceinline__ bool pivot_keep(double pvd, double norm, double eps) 
     return a / norm >= eps;
 }
 
+// pivot_keep's brackets as FP32 thresholds, once per block: for a float
+// |p|, |p| >= RN(t (1 + 2^-48)) iff |p| >= its float ceiling, |p| <=
+// RN(t (1 - 2^-48)) iff |p| <= its float floor; ok = 0 when the brackets do
+// not apply (norm == 0, t outside the normal range) and the FP64 test runs.
+struct KeepBrackets {
+    float hi, lo;
+    int ok;
+};
+__device__ __forceinline__ KeepBrackets keep_brackets(double norm, double eps) {
+    KeepBrackets k{0.f, 0.f, 0};
+    const double t = eps * norm;
+    if (norm != 0.0 && t >= DBL_MIN && t <= DBL_MAX * 0.5) {
+        k.hi = __double2float_ru(t * (1.0 + 0x1p-48));
+        k.lo = __double2float_rd(t * (1.0 - 0x1p-48));
+        k.ok = 1;
+    }
+    return k;
+}
+// pivot_keep(p, norm, eps) for a float pivot: the FP32 bracket decides it
+// except within 2^-48 of the threshold
+__device__ __forceinline__ bool pivot_keep_f(float p, const KeepBrackets& kb, double norm, double eps) {
+    const float a = fabsf(p);
+    if (kb.ok) {
+        if (a >= kb.hi) return true;
+        if (a <= kb.lo) return false;
+    }
+    return pivot_keep((double)p, norm, eps);
+}
+
 // Warp argmax of |x| with ties to the smallest row: returns the winning row
 // (value key = float bits + 1 so that "no candidate" = 0; NaN keys win, as in
 // the 64-bit (value, ~row) key max).
@@ -1055,6 +1084,7 @@ __global__ void __launch_bounds__(NT, 1) k_block_lu_ll(LuParams p, int dlo, int 
         double norm = 0.0;
 #pragma unroll
         for (int w = 0; w < NW; ++w) norm = fmax(norm, redd[w]);
+        const KeepBrackets kbr = keep_brackets(norm, p.eps);
 
         int na = d;
         int nperturb = 0;
@@ -1167,23 +1197,29 @@ __global__ void __launch_bounds__(NT, 1) k_block_lu_ll(LuParams p, int dlo, int 
                     const int owner = __shfl_sync(0xffffffffu, cw.z, fw);
                     const float* Pv = cand_v + (size_t)(buf * NW + fw) * 32;
                     buf ^= 1;
-                    // regularize_pivot (lu.cpp:10-20), FP64, identical in every thread
-                    const double pvd = (double)Pv[c];
-                    const bool keep = pivot_keep(pvd, norm, p.eps);
-                    const double val = keep ? pvd : ((pvd < 0.0 ? -1.0 : 1.0) * p.eps * norm);
-                    if (val == 0.0) {
-                        if (tid == 0) atomicMin(p.singular, ((unsigned long long)b << 32) | (unsigned)k);
-                        abort = true;
-                        break;
-                    }
-                    if (!keep) {
+                    // regularize_pivot (lu.cpp:10-20), identical in every thread;
+                    // FP32 brackets, FP64 only near the threshold or to regularise
+                    const float praw = Pv[c];
+                    float pv = praw;
+                    if (!pivot_keep_f(praw, kbr, norm, p.eps)) {
+                        const double pvd = (double)praw;
+                        const double val = (pvd < 0.0 ? -1.0 : 1.0) * p.eps * norm;
+                        if (val == 0.0) {
+                            if (tid == 0) atomicMin(p.singular, ((unsigned long long)b << 32) | (unsigned)k);
+                            abort = true;
+                            break;
+                        }
                         ++nperturb;
                         if (tid == 0) {
                             const int slot = atomicAdd(p.pert_n, 1);
                             if (slot < p.pert_cap) p.pert[slot] = PertRecord{b, k, pvd, val};
                         }
+                        pv = (float)val;
+                    } else if (praw == 0.0f) {  // kept zero pivot (eps = 0, or norm = 0 impossible here)
+                        if (tid == 0) atomicMin(p.singular, ((unsigned long long)b << 32) | (unsigned)k);
+                        abort = true;
+                        break;
                     }
-                    const float pv = (float)val;
                     if (tid == owner) {
                         rv[c] = pv;
                         fl = true;
