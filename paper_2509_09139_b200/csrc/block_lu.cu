@@ -906,35 +906,40 @@ __global__ void __launch_bounds__(NT, 2) k_block_lu_blk(LuParams p, int dlo, int
 }
 
 // ---------------------------------------------------------------------------
-// Left-looking blocked LU with the factor in shared memory (kWarpLuMax < d <=
-// kLlMax), one CTA per block. Only the L part of the factor (every row that
-// was still active when a 32-column panel was factored, 32 multipliers each:
-// ~d^2/2 floats) lives in shared memory for the whole factorisation, plus the
-// current column panel X of all d rows; U leaves for HBM panel by panel. L_Q
-// (panel Q) stores Q's 32 pivot rows first, in pivot order, then the rows
-// still active after Q. Per column panel P (columns c0 .. c0 + 31):
+// Left-looking blocked LU for kWarpLuMax < d <= kLlMax, two CTAs of 256
+// threads per SM so that one block's latency-bound column chain overlaps the
+// other block's bulk updates. Per block, shared memory holds only the current
+// column panel X of all d rows (swizzled FP32) and staging buffers; the L part
+// of the factor — per 32-column panel Q the 32 pivot rows of Q in pivot order
+// (L11\U11 rows), then the rows still active after Q (their 32 multipliers),
+// L_Q — goes to a per-CTA scratch in global memory (L2-resident) and comes
+// back by bulk copies (cp.async.bulk + mbarrier): L11 of the next panels
+// double-buffered, the bulk of L_{Q-1} single-buffered. U leaves for HBM
+// panel by panel. Per column panel P (columns c0 .. c0 + 31):
 //   gather  the panel's columns from the permuted CSR (per-row cursors, FP64
 //           -> FP32 RNE into a zero-filled X);
 //   for each earlier panel Q, pipelined so that the one-warp triangular solve
 //   of Q overlaps the bulk rank-32 update of Q - 1:
 //     A_Q  every warp: (ii)_{Q-1} = X[r] -= L_{Q-1}[r] U_{Q-1} on Q's 32 pivot rows;
 //     B_Q  warp 0: (i)_Q, Q's pivot rows x_k -= sum_{m<k} L11(k, m) x_m (lane
-//          per column; L11 rows at fixed offsets of L_Q, float4 broadcasts);
-//          the other warps: (ii)_{Q-1} on the remaining rows active after Q;
+//          per column, float4 broadcasts); the other warps: (ii)_{Q-1} on the
+//          remaining rows active after Q;
 //   then every warp: (ii)_{P-1} on the rows still active;
-//   factor  the panel's active rows (thread per row, 32 entries in registers;
-//           only the warps holding rows, named barrier): per column each warp
-//           publishes its candidate (max |x|, ties to the smaller row) with
-//           the candidate's row and its regularised pivot (the owner does the
-//           FP64 test), ONE barrier, a warp-wide argmax over the candidates,
-//           the rank-1 update in registers;
-//   store   L_P; the new pivot rows' L entries and the finished U column panel
-//           to the packed output panels.
+//   factor  the panel's active rows (thread per row, RPT rows per thread, 32
+//           entries each in registers; only the warps holding rows, named
+//           barrier): per column each warp publishes its candidate (max |x|,
+//           ties to the smaller row) with the candidate's row, ONE barrier, a
+//           warp-wide argmax over the candidates, the regularisation test in
+//           FP32 brackets, the rank-1 update in registers;
+//   store   L_P to the scratch; the new pivot rows' L entries and the
+//           finished U column panel to the packed output panels.
 // Every element receives exactly the fmaf(-l, u, a) chain, in ascending
 // column order, that the right-looking kernels apply (left- and right-looking
 // only reorder independent chains), the divisions and the pivot rule are the
 // same: factors and pivots are bit-identical to k_block_lu_blk / k_block_lu.
-constexpr int kLlMax = 288;  // the launcher checks the shared-memory budget
+constexpr int kLlMax = 288;
+constexpr int kLlThreads = 256;
+constexpr int kLlCtasPerSm = 2;
 
 __host__ __device__ inline int ll_lrows(int d) {  // L_Q rows kept: panels 0 .. T-2
     const int T = (d + 31) / 32;
@@ -943,18 +948,18 @@ __host__ __device__ inline int ll_lrows(int d) {  // L_Q rows kept: panels 0 .. 
     return r;
 }
 
-template <int NT>
 __host__ __device__ inline size_t ll_smem_bytes(int dhi) {
-    constexpr int NW = NT / 32;
+    constexpr int NW = kLlThreads / 32;
     const int T = (dhi + 31) / 32;
     const int lr = ll_lrows(dhi);
-    return (size_t)lr * 32 * sizeof(float)          // L_Q rows
-           + (size_t)dhi * 32 * sizeof(float)       // X: current column panel, all rows
-           + (size_t)2 * NW * 32 * sizeof(float)    // candidate rows (double buffered)
-           + (size_t)2 * NW * 4 * sizeof(int)       // candidate key / row / owner / pivot
-           + (size_t)lr * sizeof(short)             // row id of every L_Q row
+    return (size_t)dhi * 32 * sizeof(float)                 // X: current column panel, all rows
+           + (size_t)(dhi > 32 ? dhi - 32 : 1) * 32 * sizeof(float)  // Lb: rows 32.. of L_{Q-1}
+           + (size_t)2 * 32 * 32 * sizeof(float)            // L11 of two panels
+           + (size_t)2 * NW * 32 * sizeof(float)            // candidate rows (double buffered)
+           + (size_t)2 * NW * 4 * sizeof(int)               // candidate key / row / owner
+           + (size_t)lr * sizeof(short)                     // row id of every L_Q row
            + (size_t)(T > 1 ? T - 1 : 1) * dhi * sizeof(short)  // position of row r in L_Q
-           + (size_t)3 * dhi * sizeof(short)        // ppos, act, prow
+           + (size_t)3 * dhi * sizeof(short)                // ppos, act, prow
            + 64;
 }
 
@@ -963,6 +968,34 @@ __device__ __forceinline__ int xq(int r, int q) { return r * 32 + ((q ^ (r & 7))
 
 __device__ __forceinline__ void bar_named(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* mb) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mb)) : "memory");
+}
+// one elected thread: expect `bytes` on mb and copy them global -> shared
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, unsigned long long* mb) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mb)), "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(mb))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* mb, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(mb)),
+        "r"(parity)
+        : "memory");
 }
 
 // X[r][lane] -= sum_m L[pos][m] u[m], u = this lane's column of the 32 pivot
@@ -1021,26 +1054,38 @@ __device__ __forceinline__ void ll_trsv(float (&x)[32], const float* LQ) {
     if constexpr (M0 + 4 < 32) ll_trsv<M0 + 4>(x, LQ);
 }
 
-template <int NT>
-__global__ void __launch_bounds__(NT, 1) k_block_lu_ll(LuParams p, int dlo, int dhi) {
+template <int RPT>  // active rows per thread: d <= 256 RPT
+__global__ void __launch_bounds__(kLlThreads, kLlCtasPerSm) k_block_lu_ll(LuParams p, int dlo, int dhi) {
+    constexpr int NT = kLlThreads;
     constexpr int NW = NT / 32;
-    extern __shared__ __align__(16) float llsm[];
+    extern __shared__ __align__(128) float llsm[];
     const int lrmax = ll_lrows(dhi);
     const int Tmax = (dhi + 31) / 32;
-    float* Ls = llsm;                                          // [lrmax][32]
-    float* X = Ls + (size_t)lrmax * 32;                        // [dhi][32] swizzled
-    float* cand_v = X + (size_t)dhi * 32;                      // [2][NW][32]
-    int* cand_i = reinterpret_cast<int*>(cand_v + 2 * NW * 32);  // [2][NW][4]: key, row, owner, pivot bits
+    float* X = llsm;                                           // [dhi][32] swizzled
+    float* Lb = X + (size_t)dhi * 32;                          // [dhi-32][32]
+    float* L11 = Lb + (size_t)(dhi > 32 ? dhi - 32 : 1) * 32;  // [2][32][32]
+    float* cand_v = L11 + 2 * 32 * 32;                         // [2][NW][32]
+    int* cand_i = reinterpret_cast<int*>(cand_v + 2 * NW * 32);  // [2][NW][4]: key, row, owner
     short* rowQ = reinterpret_cast<short*>(cand_i + 2 * NW * 4);  // [lrmax]
     short* posQ = rowQ + lrmax;                                // [Tmax-1][dhi]
     short* ppos = posQ + (size_t)(Tmax > 1 ? Tmax - 1 : 1) * dhi;  // pivot position of row r (or 0x7fff)
     short* act = ppos + dhi;                                   // active rows (stable order)
     short* prow = act + dhi;                                   // pivot row of position k
+    __shared__ __align__(8) unsigned long long mbar[3];        // Lb, L11[0], L11[1]
     __shared__ double redd[NW];
     __shared__ int lofs[16];                                   // first L row of panel Q
     __shared__ int nact_sh;
+    float* Lg = p.scratch + (size_t)blockIdx.x * lrmax * 32;   // this CTA's L_Q rows
 
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (tid == 0) {
+        mbar_init(&mbar[0]);
+        mbar_init(&mbar[1]);
+        mbar_init(&mbar[2]);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    unsigned nb_issue = 0, n11_issue[2] = {0u, 0u};  // completed-phase counters (uniform)
 
     for (int b = blockIdx.x; b < p.s; b += gridDim.x) {
         const int o = p.bstart[b];
@@ -1049,25 +1094,32 @@ __global__ void __launch_bounds__(NT, 1) k_block_lu_ll(LuParams p, int dlo, int 
         const int T = (d + 31) / 32;
         const int dp4 = (d + 3) & ~3;
         float* F = p.fac + p.fac_off[b];
-        // per-row CSR cursor (thread tid owns row tid for the gathers) + FP64
-        // inf-norm, row sums in column order (matrix_inf_norm)
-        int cur = 0, ke = 0;
+        // per-row CSR cursors (thread tid owns rows tid + NT i for the
+        // gathers) + FP64 inf-norm, row sums in column order (matrix_inf_norm)
+        int cur[RPT], ke[RPT];
         double rs = 0.0;
-        if (tid < d) {
-            const int kb = __ldg(p.a.rp + o + tid);
-            ke = __ldg(p.a.rp + o + tid + 1);
-            cur = ke;
-            for (int k = kb; k < ke; ++k) {
-                const int c = __ldg(p.a.ci + k) - o;
-                if (c >= 0 && c < d) {
-                    if (cur == ke) cur = k;
-                    rs = __dadd_rn(rs, fabs(__ldg(p.a.val + k)));
-                } else if (c >= d) {
-                    break;
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+            const int r = tid + NT * i;
+            cur[i] = ke[i] = 0;
+            if (r < d) {
+                const int kb = __ldg(p.a.rp + o + r);
+                ke[i] = __ldg(p.a.rp + o + r + 1);
+                cur[i] = ke[i];
+                double rsum = 0.0;
+                for (int k = kb; k < ke[i]; ++k) {
+                    const int c = __ldg(p.a.ci + k) - o;
+                    if (c >= 0 && c < d) {
+                        if (cur[i] == ke[i]) cur[i] = k;
+                        rsum = __dadd_rn(rsum, fabs(__ldg(p.a.val + k)));
+                    } else if (c >= d) {
+                        break;
+                    }
                 }
+                rs = fmax(rs, rsum);
+                act[r] = (short)r;
+                ppos[r] = 0x7fff;
             }
-            act[tid] = (short)tid;
-            ppos[tid] = 0x7fff;
         }
         double wm = rs;
 #pragma unroll
@@ -1094,44 +1146,55 @@ __global__ void __launch_bounds__(NT, 1) k_block_lu_ll(LuParams p, int dlo, int 
             const int c0 = 32 * P;
             const int kw = min(32, d - c0);
             // ---- gather the column panel (rows in original order)
-            if (tid < d) {
-                float4* xr = reinterpret_cast<float4*>(X + tid * 32);
 #pragma unroll
-                for (int q = 0; q < 8; ++q) xr[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-                const int cend = o + c0 + kw;
-                while (cur < ke) {
-                    const int c = __ldg(p.a.ci + cur);
-                    if (c >= cend) break;
-                    const int lc = c - o - c0;
-                    X[xq(tid, lc >> 2) + (lc & 3)] = __double2float_rn(__ldg(p.a.val + cur));
-                    ++cur;
+            for (int i = 0; i < RPT; ++i) {
+                const int r = tid + NT * i;
+                if (r < d) {
+                    float4* xr = reinterpret_cast<float4*>(X + r * 32);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) xr[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    const int cend = o + c0 + kw;
+                    while (cur[i] < ke[i]) {
+                        const int c = __ldg(p.a.ci + cur[i]);
+                        if (c >= cend) break;
+                        const int lc = c - o - c0;
+                        X[xq(r, lc >> 2) + (lc & 3)] = __double2float_rn(__ldg(p.a.val + cur[i]));
+                        ++cur[i];
+                    }
                 }
             }
+            // the first two L11 blocks of this panel's left-looking updates
+            if (tid == 0)
+                for (int q = 0; q < min(P, 2); ++q)
+                    bulk_load(L11 + q * 1024, Lg + (size_t)lofs[q] * 32, 4096u, &mbar[1 + q]);
             __syncthreads();
             // ---- left-looking updates from the earlier panels
             for (int Q = 0; Q <= P; ++Q) {
                 const int q0 = 32 * Q;
                 const short* prv = prow + (Q > 0 ? q0 - 32 : 0);  // U_{Q-1}: pivot rows of Q - 1
-                const float* Lp = Q > 0 ? Ls + (size_t)lofs[Q - 1] * 32 : Ls;
-                const short* posp = posQ + (size_t)(Q > 0 ? Q - 1 : 0) * dhi;
-                if (Q == P) {  // (ii)_{P-1} on the rows still active (positions >= 32 of L_{P-1})
+                const int nprev = Q > 0 ? d - (q0 - 32) : 0;       // rows of L_{Q-1}
+                if (Q > 0) mbar_wait(&mbar[0], (nb_issue - 1) & 1u);  // Lb = rows 32.. of L_{Q-1}
+                if (Q == P) {  // (ii)_{P-1} on the rows still active
                     if (Q > 0) {
                         const short* rP = rowQ + lofs[Q - 1];
-                        ll_rank32(X, Lp, prv, lane, 32 + wid, d - (q0 - 32), NW,
+                        ll_rank32(X, Lb - 32 * 32, prv, lane, 32 + wid, nprev, NW,
                                   [&](int a) { return make_int2(a, (int)rP[a]); });
                         __syncthreads();
                     }
                     break;
                 }
                 if (Q > 0) {  // A_Q: (ii)_{Q-1} on Q's pivot rows
-                    ll_rank32(X, Lp, prv, lane, wid, 32, NW, [&](int i) {
+                    const short* posp = posQ + (size_t)(Q - 1) * dhi;
+                    ll_rank32(X, Lb - 32 * 32, prv, lane, wid, 32, NW, [&](int i) {
                         const int r = prow[q0 + i];
                         return make_int2((int)posp[r], r);
                     });
                     __syncthreads();
                 }
-                if (wid == 0) {  // B_Q, warp 0: (i)_Q, L11 of Q = the first 32 rows of L_Q
-                    const float* LQ = Ls + (size_t)lofs[Q] * 32;
+                if (wid == 0) {  // B_Q, warp 0: (i)_Q with L11 of Q
+                    const int sb = Q & 1;
+                    mbar_wait(&mbar[1 + sb], n11_issue[sb] & 1u);
+                    const float* LQ = L11 + sb * 1024;
                     float x[32];
 #pragma unroll
                     for (int m = 0; m < 32; ++m) x[m] = X[xq(prow[q0 + m], lane >> 2) + (lane & 3)];
@@ -1141,60 +1204,88 @@ __global__ void __launch_bounds__(NT, 1) k_block_lu_ll(LuParams p, int dlo, int 
                 } else if (Q > 0) {  // B_Q, other warps: (ii)_{Q-1} on the rows active after Q
                     const short* rP = rowQ + lofs[Q - 1];
                     const int qhi = q0 + 32;
-                    ll_rank32(X, Lp, prv, lane, 32 + (wid - 1), d - (q0 - 32), NW - 1, [&](int a) {
+                    ll_rank32(X, Lb - 32 * 32, prv, lane, 32 + (wid - 1), nprev, NW - 1, [&](int a) {
                         const int r = rP[a];
                         return make_int2(ppos[r] >= qhi ? a : -1, r);  // Q's pivot rows: done in A_Q
                     });
                 }
+                n11_issue[Q & 1] += 1;  // L11 buffer Q & 1 consumed (phase counted in every thread)
                 __syncthreads();
+                // Lb and L11 buffer (Q & 1) are free: fetch L_Q's rows 32.. and L11 of Q + 2
+                if (tid == 0) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    const int nq = d - q0;
+                    bulk_load(Lb, Lg + ((size_t)lofs[Q] + 32) * 32, (unsigned)(nq - 32) * 128u, &mbar[0]);
+                    if (Q + 2 < P) bulk_load(L11 + (Q & 1) * 1024, Lg + (size_t)lofs[Q + 2] * 32, 4096u, &mbar[1 + (Q & 1)]);
+                }
+                nb_issue += 1;
             }
-            // ---- factor the panel: thread a owns active row act[a]; only
-            // the warps holding rows take part (named barrier 1)
-            const int nwa = (na + 31) >> 5;
+            // ---- factor the panel: thread a owns active rows act[a + NT i];
+            // only the warps holding rows take part (named barrier 1)
+            const int nwa = (min(na, NT) + 31) >> 5;
             if (wid < nwa) {
-                const bool has = tid < na;
-                const int myrow = has ? act[tid] : 0;
-                bool fl = !has;  // pivotal (or no row)
-                float rv[32];
-                {
-                    const float4* xr = reinterpret_cast<const float4*>(X + myrow * 32);
+                bool has[RPT], fl[RPT];
+                int myrow[RPT];
+                float rv[RPT][32];
+#pragma unroll
+                for (int i = 0; i < RPT; ++i) {
+                    const int a = tid + NT * i;
+                    has[i] = a < na;
+                    myrow[i] = has[i] ? act[a] : 0;
+                    fl[i] = !has[i];
+                    const float4* xr = reinterpret_cast<const float4*>(X + myrow[i] * 32);
 #pragma unroll
                     for (int q = 0; q < 8; ++q) {
-                        const float4 t4 = has ? xr[q ^ (myrow & 7)] : make_float4(0.f, 0.f, 0.f, 0.f);
-                        rv[4 * q + 0] = t4.x;
-                        rv[4 * q + 1] = t4.y;
-                        rv[4 * q + 2] = t4.z;
-                        rv[4 * q + 3] = t4.w;
+                        const float4 t4 = has[i] ? xr[q ^ (myrow[i] & 7)] : make_float4(0.f, 0.f, 0.f, 0.f);
+                        rv[i][4 * q + 0] = t4.x;
+                        rv[i][4 * q + 1] = t4.y;
+                        rv[i][4 * q + 2] = t4.z;
+                        rv[i][4 * q + 3] = t4.w;
                     }
                 }
 #pragma unroll
                 for (int c = 0; c < 32; ++c) {
                     if (c >= kw) break;
                     const int k = c0 + c;
-                    // warp candidate: max |x|, ties -> smaller row
-                    const unsigned key = fl ? 0u : __float_as_uint(fabsf(rv[c])) + 1u;
+                    // thread candidate, then warp candidate: max |x|, ties -> smaller row
+                    unsigned key = 0u;
+                    int brow = 0x7fffffff, bi = 0;
+#pragma unroll
+                    for (int i = 0; i < RPT; ++i) {
+                        const unsigned ki = fl[i] ? 0u : __float_as_uint(fabsf(rv[i][c])) + 1u;
+                        if (ki > key || (ki == key && ki != 0u && myrow[i] < brow)) {
+                            key = ki;
+                            brow = myrow[i];
+                            bi = i;
+                        }
+                    }
                     unsigned kmx;
-                    const int wr = warp_pivot_row(key, fl ? 0x7fffffff : myrow, &kmx);
-                    const unsigned own = __ballot_sync(0xffffffffu, !fl && key == kmx && myrow == wr);
+                    const int wr = warp_pivot_row(key, key ? brow : 0x7fffffff, &kmx);
+                    const unsigned own = __ballot_sync(0xffffffffu, key != 0u && key == kmx && brow == wr);
                     float* cv = cand_v + (size_t)(buf * NW + wid) * 32;
                     int* ci4 = cand_i + (buf * NW + wid) * 4;
                     if (own && lane == __ffs(own) - 1) {
 #pragma unroll
-                        for (int q = 0; q < 8; ++q)
-                            reinterpret_cast<float4*>(cv)[q] =
-                                make_float4(rv[4 * q], rv[4 * q + 1], rv[4 * q + 2], rv[4 * q + 3]);
-                        reinterpret_cast<int4*>(ci4)[0] = make_int4((int)kmx, wr, tid, 0);
+                        for (int i = 0; i < RPT; ++i)
+                            if (i == bi)
+#pragma unroll
+                                for (int q = 0; q < 8; ++q)
+                                    reinterpret_cast<float4*>(cv)[q] = make_float4(rv[i][4 * q], rv[i][4 * q + 1],
+                                                                                   rv[i][4 * q + 2], rv[i][4 * q + 3]);
+                        reinterpret_cast<int4*>(ci4)[0] = make_int4((int)kmx, wr, tid + NT * bi, 0);
                     } else if (lane == 0 && !own) {
                         reinterpret_cast<int4*>(ci4)[0] = make_int4(0, 0x7fffffff, -1, 0);
                     }
                     bar_named(1, nwa * 32);
                     // winner over the active warps' candidates (warp-wide, identical in every warp)
-                    int4 cw = lane < nwa ? reinterpret_cast<const int4*>(cand_i + buf * NW * 4)[lane]
-                                         : make_int4(0, 0x7fffffff, -1, 0);
+                    const int4 cw = lane < nwa ? reinterpret_cast<const int4*>(cand_i + buf * NW * 4)[lane]
+                                               : make_int4(0, 0x7fffffff, -1, 0);
                     unsigned kk;
-                    const int frow = warp_pivot_row((unsigned)cw.x, lane < nwa && cw.x != 0 ? cw.y : 0x7fffffff, &kk);
-                    const int fw = __ffs(__ballot_sync(0xffffffffu, lane < nwa && (unsigned)cw.x == kk && cw.y == frow)) - 1;
-                    const int owner = __shfl_sync(0xffffffffu, cw.z, fw);
+                    const int frow =
+                        warp_pivot_row((unsigned)cw.x, lane < nwa && cw.x != 0 ? cw.y : 0x7fffffff, &kk);
+                    const int fw =
+                        __ffs(__ballot_sync(0xffffffffu, lane < nwa && (unsigned)cw.x == kk && cw.y == frow)) - 1;
+                    const int owner = __shfl_sync(0xffffffffu, cw.z, fw);  // tid + NT * row slot
                     const float* Pv = cand_v + (size_t)(buf * NW + fw) * 32;
                     buf ^= 1;
                     // regularize_pivot (lu.cpp:10-20), identical in every thread;
@@ -1215,34 +1306,41 @@ __global__ void __launch_bounds__(NT, 1) k_block_lu_ll(LuParams p, int dlo, int 
                             if (slot < p.pert_cap) p.pert[slot] = PertRecord{b, k, pvd, val};
                         }
                         pv = (float)val;
-                    } else if (praw == 0.0f) {  // kept zero pivot (eps = 0, or norm = 0 impossible here)
+                    } else if (praw == 0.0f) {  // kept zero pivot (eps = 0)
                         if (tid == 0) atomicMin(p.singular, ((unsigned long long)b << 32) | (unsigned)k);
                         abort = true;
                         break;
                     }
-                    if (tid == owner) {
-                        rv[c] = pv;
-                        fl = true;
-                        prow[k] = (short)myrow;
-                        ppos[myrow] = (short)k;
-                    } else if (!fl) {
-                        const float l = div_mult(rv[c], pv);  // L(i,k) = x_i / pivot (lu.cpp:207)
-                        rv[c] = l;
 #pragma unroll
-                        for (int c2 = c + 1; c2 < 32; ++c2) rv[c2] = fmaf(-l, Pv[c2], rv[c2]);
+                    for (int i = 0; i < RPT; ++i) {
+                        if (owner == tid + NT * i) {
+                            rv[i][c] = pv;
+                            fl[i] = true;
+                            prow[k] = (short)myrow[i];
+                            ppos[myrow[i]] = (short)k;
+                        } else if (!fl[i]) {
+                            const float l = div_mult(rv[i][c], pv);  // L(i,k) = x_i / pivot (lu.cpp:207)
+                            rv[i][c] = l;
+#pragma unroll
+                            for (int c2 = c + 1; c2 < 32; ++c2) rv[i][c2] = fmaf(-l, Pv[c2], rv[i][c2]);
+                        }
                     }
                 }
-                if (!abort && has) {
-                    float4* xr = reinterpret_cast<float4*>(X + myrow * 32);
+                if (!abort)
 #pragma unroll
-                    for (int q = 0; q < 8; ++q)
-                        xr[q ^ (myrow & 7)] = make_float4(rv[4 * q], rv[4 * q + 1], rv[4 * q + 2], rv[4 * q + 3]);
-                }
+                    for (int i = 0; i < RPT; ++i)
+                        if (has[i]) {
+                            float4* xr = reinterpret_cast<float4*>(X + myrow[i] * 32);
+#pragma unroll
+                            for (int q = 0; q < 8; ++q)
+                                xr[q ^ (myrow[i] & 7)] =
+                                    make_float4(rv[i][4 * q], rv[i][4 * q + 1], rv[i][4 * q + 2], rv[i][4 * q + 3]);
+                        }
             }
             abort = __syncthreads_or(abort);
             if (abort) break;
-            // ---- compact the active list (stable) and store L_P: the 32 pivot
-            // rows first, in pivot order, then the rows still active
+            // ---- compact the active list (stable); L_P to the scratch: the 32
+            // pivot rows first, in pivot order, then the rows still active
             if (wid == 0) {
                 int w = 0;
                 for (int base = 0; base < na; base += 32) {
@@ -1264,12 +1362,14 @@ __global__ void __launch_bounds__(NT, 1) k_block_lu_ll(LuParams p, int dlo, int 
                 for (int i = tid; i < 32 + nnew; i += NT) {
                     const int r = i < 32 ? prow[c0 + i] : act[i - 32];
                     const float4* xr = reinterpret_cast<const float4*>(X + r * 32);
-                    float4* lr = reinterpret_cast<float4*>(Ls + ((size_t)lo + i) * 32);
+                    float4* lr = reinterpret_cast<float4*>(Lg + ((size_t)lo + i) * 32);
 #pragma unroll
                     for (int q = 0; q < 8; ++q) lr[q] = xr[q ^ (r & 7)];
                     rowQ[lo + i] = (short)r;
                     posQ[(size_t)P * dhi + r] = (short)i;
                 }
+                // the scratch rows are read back by the async proxy (bulk copies)
+                asm volatile("fence.proxy.async.global;" ::: "memory");
             }
             // ---- output: chunks (t, P) for t <= P (U / L11\U11 from X) and
             // (P, Q) for Q < P (the new pivot rows' L from L_Q); chunk (t, u)
@@ -1300,8 +1400,8 @@ __global__ void __launch_bounds__(NT, 1) k_block_lu_ll(LuParams p, int dlo, int 
                     const int k = c0 + kr;
                     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
                     if (k < d)
-                        v = *reinterpret_cast<const float4*>(
-                            Ls + ((size_t)lofs[Q] + posQ[(size_t)Q * dhi + prow[k]]) * 32 + 4 * qi);
+                        v = __ldcg(reinterpret_cast<const float4*>(
+                            Lg + ((size_t)lofs[Q] + posQ[(size_t)Q * dhi + prow[k]]) * 32 + 4 * qi));
                     __stcs(reinterpret_cast<float4*>(F + (size_t)P * 32 * dp4 + (size_t)(8 * Q + qi) * 128 + kr * 4),
                            v);
                 }
@@ -1345,9 +1445,11 @@ size_t block_lu_scratch_floats(int dmax, int num_sms, int* smem_dim, int* scratc
     size_t need = 0;
     const char* e = getenv("HPBJ_LU_LL");
     const bool ll = !(e && e[0] == '0');
+    if (ll && dmax > kWarpLuMax)  // left-looking kernel: L_Q rows of one block per CTA
+        need = (size_t)num_sms * kLlCtasPerSm * ll_lrows(std::min(dmax, kLlMax)) * 32;
     if (dmax > kWarpLuMax && (!ll || dmax > kLlMax)) {  // blocked kernels: one tile per resident CTA
         const int d1 = std::min(dmax, kBlkThreads);
-        need = (size_t)num_sms * blk_ctas_per_sm(d1) * (*scratch_ld) * (*scratch_ld);
+        need = std::max(need, (size_t)num_sms * blk_ctas_per_sm(d1) * (*scratch_ld) * (*scratch_ld));
         if (dmax > kBlkThreads)
             need = std::max(need, (size_t)num_sms * blk_ctas_per_sm(std::min(dmax, kBlkMax)) * (*scratch_ld) *
                                       (*scratch_ld));
@@ -1402,27 +1504,20 @@ void launch_block_lu(const LuParams& p_in, int dmax, int num_sms, cudaStream_t s
         HPBJ_CUDA(cudaGetLastError());
         return;
     }
-    // left-looking shared-memory kernel for dw < d <= kLlMax (HPBJ_LU_LL=0:
-    // the L2-scratch blocked kernel instead, for A/B runs and the bit-identity test)
+    // left-looking kernel for dw < d <= kLlMax (HPBJ_LU_LL=0: the L2-scratch
+    // blocked kernel instead, for A/B runs and the bit-identity test)
     int dll = dw;
     {
         const char* e = getenv("HPBJ_LU_LL");
         if (!(e && e[0] == '0')) {
-            for (int range = 0; range < 2; ++range) {
-                const int dlo = range == 0 ? dw : 256;
-                const int dhi = std::min(dmax, range == 0 ? 256 : kLlMax);
-                if (dhi <= dlo) continue;
-                const size_t smem = range == 0 ? ll_smem_bytes<256>(dhi) : ll_smem_bytes<512>(dhi);
-                void (*fn)(LuParams, int, int) = range == 0 ? k_block_lu_ll<256> : k_block_lu_ll<512>;
-                HPBJ_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-                int occ = 0;
-                HPBJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, range == 0 ? 256 : 512, smem));
-                occ = std::max(occ, 1);
-                const int grid = std::min(p.s, num_sms * occ);
-                fn<<<grid, range == 0 ? 256 : 512, smem, st>>>(p, dlo, dhi);
-                *launches += 1;
-                dll = dhi;
-            }
+            const int dhi = std::min(dmax, kLlMax);
+            const size_t smem = ll_smem_bytes(dhi);
+            void (*fn)(LuParams, int, int) = dhi <= kLlThreads ? k_block_lu_ll<1> : k_block_lu_ll<2>;
+            HPBJ_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            const int grid = std::min(p.s, num_sms * kLlCtasPerSm);
+            fn<<<grid, kLlThreads, smem, st>>>(p, dw, dhi);
+            *launches += 1;
+            dll = dhi;
         }
     }
     if (dmax <= dll) {
