@@ -1221,38 +1221,41 @@ __global__ void __launch_bounds__(kLlThreads, kLlCtasPerSm) k_block_lu_ll(LuPara
                 nb_issue += 1;
             }
             // ---- factor the panel: thread a owns active rows act[a + NT i];
-            // only the warps holding rows take part (named barrier 1)
+            // only the warps holding rows take part (named barrier 1). A
+            // rolled column loop over a shifting register window (rv[j] =
+            // column c + j) keeps the code small: the rank-1 update writes
+            // rv[j - 1] = fmaf(-l, Pv[j], rv[j]); each column's final entry
+            // goes to X as it is produced (a pivot row stores its U row)
             const int nwa = (min(na, NT) + 31) >> 5;
             if (wid < nwa) {
-                bool has[RPT], fl[RPT];
+                bool fl[RPT];
                 int myrow[RPT];
                 float rv[RPT][32];
 #pragma unroll
                 for (int i = 0; i < RPT; ++i) {
                     const int a = tid + NT * i;
-                    has[i] = a < na;
-                    myrow[i] = has[i] ? act[a] : 0;
-                    fl[i] = !has[i];
+                    const bool has = a < na;
+                    myrow[i] = has ? act[a] : 0;
+                    fl[i] = !has;
                     const float4* xr = reinterpret_cast<const float4*>(X + myrow[i] * 32);
 #pragma unroll
                     for (int q = 0; q < 8; ++q) {
-                        const float4 t4 = has[i] ? xr[q ^ (myrow[i] & 7)] : make_float4(0.f, 0.f, 0.f, 0.f);
+                        const float4 t4 = has ? xr[q ^ (myrow[i] & 7)] : make_float4(0.f, 0.f, 0.f, 0.f);
                         rv[i][4 * q + 0] = t4.x;
                         rv[i][4 * q + 1] = t4.y;
                         rv[i][4 * q + 2] = t4.z;
                         rv[i][4 * q + 3] = t4.w;
                     }
                 }
-#pragma unroll
-                for (int c = 0; c < 32; ++c) {
-                    if (c >= kw) break;
+#pragma unroll 1
+                for (int c = 0; c < kw; ++c) {
                     const int k = c0 + c;
                     // thread candidate, then warp candidate: max |x|, ties -> smaller row
                     unsigned key = 0u;
                     int brow = 0x7fffffff, bi = 0;
 #pragma unroll
                     for (int i = 0; i < RPT; ++i) {
-                        const unsigned ki = fl[i] ? 0u : __float_as_uint(fabsf(rv[i][c])) + 1u;
+                        const unsigned ki = fl[i] ? 0u : __float_as_uint(fabsf(rv[i][0])) + 1u;
                         if (ki > key || (ki == key && ki != 0u && myrow[i] < brow)) {
                             key = ki;
                             brow = myrow[i];
@@ -1286,11 +1289,11 @@ __global__ void __launch_bounds__(kLlThreads, kLlCtasPerSm) k_block_lu_ll(LuPara
                     const int fw =
                         __ffs(__ballot_sync(0xffffffffu, lane < nwa && (unsigned)cw.x == kk && cw.y == frow)) - 1;
                     const int owner = __shfl_sync(0xffffffffu, cw.z, fw);  // tid + NT * row slot
-                    const float* Pv = cand_v + (size_t)(buf * NW + fw) * 32;
+                    const float4* Pv4 = reinterpret_cast<const float4*>(cand_v + (size_t)(buf * NW + fw) * 32);
                     buf ^= 1;
                     // regularize_pivot (lu.cpp:10-20), identical in every thread;
                     // FP32 brackets, FP64 only near the threshold or to regularise
-                    const float praw = Pv[c];
+                    const float praw = Pv4[0].x;
                     float pv = praw;
                     if (!pivot_keep_f(praw, kbr, norm, p.eps)) {
                         const double pvd = (double)praw;
@@ -1311,31 +1314,35 @@ __global__ void __launch_bounds__(kLlThreads, kLlCtasPerSm) k_block_lu_ll(LuPara
                         abort = true;
                         break;
                     }
+                    float pw[32];  // the pivot row's window
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const float4 t4 = Pv4[q];
+                        pw[4 * q + 0] = t4.x;
+                        pw[4 * q + 1] = t4.y;
+                        pw[4 * q + 2] = t4.z;
+                        pw[4 * q + 3] = t4.w;
+                    }
 #pragma unroll
                     for (int i = 0; i < RPT; ++i) {
-                        if (owner == tid + NT * i) {
-                            rv[i][c] = pv;
+                        if (owner == tid + NT * i) {  // the pivot row: its U row (columns c..31) is final
+                            rv[i][0] = pv;
                             fl[i] = true;
                             prow[k] = (short)myrow[i];
                             ppos[myrow[i]] = (short)k;
-                        } else if (!fl[i]) {
-                            const float l = div_mult(rv[i][c], pv);  // L(i,k) = x_i / pivot (lu.cpp:207)
-                            rv[i][c] = l;
 #pragma unroll
-                            for (int c2 = c + 1; c2 < 32; ++c2) rv[i][c2] = fmaf(-l, Pv[c2], rv[i][c2]);
+                            for (int j = 0; j < 32; ++j) {
+                                const int cc = c + j;
+                                if (cc < 32) X[xq(myrow[i], cc >> 2) + (cc & 3)] = rv[i][j];
+                            }
+                        } else if (!fl[i]) {
+                            const float l = div_mult(rv[i][0], pv);  // L(i,k) = x_i / pivot (lu.cpp:207)
+                            X[xq(myrow[i], c >> 2) + (c & 3)] = l;
+#pragma unroll
+                            for (int j = 1; j < 32; ++j) rv[i][j - 1] = fmaf(-l, pw[j], rv[i][j]);
                         }
                     }
                 }
-                if (!abort)
-#pragma unroll
-                    for (int i = 0; i < RPT; ++i)
-                        if (has[i]) {
-                            float4* xr = reinterpret_cast<float4*>(X + myrow[i] * 32);
-#pragma unroll
-                            for (int q = 0; q < 8; ++q)
-                                xr[q ^ (myrow[i] & 7)] =
-                                    make_float4(rv[i][4 * q], rv[i][4 * q + 1], rv[i][4 * q + 2], rv[i][4 * q + 3]);
-                        }
             }
             abort = __syncthreads_or(abort);
             if (abort) break;
