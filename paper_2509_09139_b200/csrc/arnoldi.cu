@@ -10,10 +10,12 @@
 // in how the j+1 inner products are synchronised:
 //
 //  k_mgs  (large n: one basis vector takes longer to stream than a grid
-//          barrier): the textbook sequence, two projections per grid-wide
-//          reduction (see the kernel), h_i = <v_i, w - sum_{k<i} h_k v_k>;
-//          each v_i streams once from HBM for its dot and once more
-//          (L2-hot) for its axpy.
+//          barrier): the textbook sequence, one grid-wide reduction per
+//          projection, h_i = <v_i, w - sum_{k<i} h_k v_k>; each v_i streams
+//          once from HBM for its dot and once more (L2-hot) for its axpy.
+//          (Two projections per reduction with a Gram correction was
+//          measured slower on config 3, 240 -> 262 us/step: the pass then
+//          re-reads two vectors, 66 MB, that no longer stay in L2.)
 //  k_icwy (small/medium n: barrier-latency bound): the compact-WY form of the
 //          same projector, P = I - V T V^T with T = (I + L)^-1, L = strictly
 //          lower part of V^T V (Swirydowicz et al., "Low synchronization
@@ -155,23 +157,14 @@ __device__ void finish_step(const OrthArgs& a, double2* w2, double* scratch, int
 }
 
 // ---------------------------------------------------------------------------
-// Textbook MGS two projections per grid-wide reduction: the pass for the pair
-// (v_i, v_{i+1}) subtracts the previous pair (h_{i-2} v_{i-2}, then
-// h_{i-1} v_{i-1}: MGS order, the basis vectors L2-hot from the previous
-// pass) and forms a = <v_i, w>, b = <v_{i+1}, w> against the same w; then
-// h_i = a and h_{i+1} = <v_{i+1}, w - h_i v_i> = b - h_i <v_{i+1}, v_i>. The
-// Gram entry <v_{i+1}, v_i> comes for free when v_{i+1} is made (the final
-// pass of step i already streams v_i for its axpy): gram[i]. (j+1)/2 + 1
-// grid barriers per step instead of j + 2, each basis vector still read from
-// HBM once.
 template <bool SMEM>
 __global__ void __launch_bounds__(kMgsThreads, 1) k_mgs(OrthArgs a) {
     SolveState* st = a.st;
     if (st->done) return;  // uniform: nothing writes done before the final barrier
     extern __shared__ __align__(16) double dsm_mgs[];
     double* wsh = dsm_mgs + a.scr;
-    __shared__ double red[3][kMgsThreads / 32];
-    __shared__ double bc[3];
+    __shared__ double red[2][kMgsThreads / 32];
+    __shared__ double bc[2];
 
     const int j = st->j;
     const int m = a.kb.m;
@@ -181,140 +174,100 @@ __global__ void __launch_bounds__(kMgsThreads, 1) k_mgs(OrthArgs a) {
     const int r0 = blockIdx.x * a.slice;
     const int len = max(0, min(a.slice, a.npad - r0));
     const int nv2 = len >> 1;
-    double* P = a.kb.partials;  // [2 parity][3 quantity][G]
-    double* gsub = a.gram;      // gsub[i] = <v_{i+1}, v_i>
-    double* Hj = a.kb.H + (size_t)j * (m + 1);
+    double* P = a.kb.partials;  // [2 parity][2 quantity][G]
 
     double2* w2 = SMEM ? reinterpret_cast<double2*>(wsh) : reinterpret_cast<double2*>(a.kb.w + r0);
     const double2* win = reinterpret_cast<const double2*>(a.kb.w + r0);
     const double* V = a.kb.V;
-    auto vec = [&](int i) { return reinterpret_cast<const double2*>(V + (size_t)i * ldv + r0); };
 
-    auto reduce3 = [&](double x0, double x1, double x2, int parity) {
+    auto reduce2 = [&](double x0, double x1, int parity) {
         x0 = warp_sum(x0);
         x1 = warp_sum(x1);
-        x2 = warp_sum(x2);
         if (lane == 0) {
             red[0][wid] = x0;
             red[1][wid] = x1;
-            red[2][wid] = x2;
         }
         __syncthreads();
         if (wid == 0) {
-            double t[3];
-#pragma unroll
-            for (int q = 0; q < 3; ++q) {
-                t[q] = lane < kMgsThreads / 32 ? red[q][lane] : 0.0;
-                t[q] = warp_sum(t[q]);
+            double t0 = lane < kMgsThreads / 32 ? red[0][lane] : 0.0;
+            double t1 = lane < kMgsThreads / 32 ? red[1][lane] : 0.0;
+            t0 = warp_sum(t0);
+            t1 = warp_sum(t1);
+            if (lane == 0) {
+                P[(parity * 2 + 0) * G + blockIdx.x] = t0;
+                P[(parity * 2 + 1) * G + blockIdx.x] = t1;
             }
-            if (lane < 3) P[(parity * 3 + lane) * G + blockIdx.x] = lane == 0 ? t[0] : lane == 1 ? t[1] : t[2];
         }
         grid_barrier(a.gb);
-        if (wid < 3) {
-            const double tq = sum_partials(P + (parity * 3 + wid) * G, G);
-            if (lane == 0) bc[wid] = tq;
+        if (wid == 0) {
+            const double t0 = sum_partials(P + (parity * 2 + 0) * G, G);
+            const double t1 = sum_partials(P + (parity * 2 + 1) * G, G);
+            if (lane == 0) {
+                bc[0] = t0;
+                bc[1] = t1;
+            }
         }
         __syncthreads();
     };
 
-    // pass 0: stage w on chip; ||w||^2, <v_0, w>, <v_1, w>
-    double h0 = 0.0, h1 = 0.0;  // coefficients of the group just formed
+    // pass 0: stage w on chip, ||w||^2 and <v_0, w>
+    double ss = 0.0, dt = 0.0;
     {
-        double ss = 0.0, da = 0.0, db = 0.0;
-        const double2* v0 = vec(0);
-        const double2* v1 = vec(j >= 1 ? 1 : 0);
+        const double2* v0 = reinterpret_cast<const double2*>(V + r0);
 #pragma unroll 4
         for (int e = tid; e < nv2; e += kMgsThreads) {
             const double2 wv = __ldcg(win + e);
-            const double2 x0 = __ldg(v0 + e);
+            const double2 vv = __ldg(v0 + e);
             if (SMEM) w2[e] = wv;
             ss = fma(wv.x, wv.x, ss);
             ss = fma(wv.y, wv.y, ss);
-            da = fma(x0.x, wv.x, da);
-            da = fma(x0.y, wv.y, da);
-            if (j >= 1) {
-                const double2 x1 = __ldg(v1 + e);
-                db = fma(x1.x, wv.x, db);
-                db = fma(x1.y, wv.y, db);
-            }
+            dt = fma(vv.x, wv.x, dt);
+            dt = fma(vv.y, wv.y, dt);
         }
-        reduce3(ss, da, db, 0);
     }
+    reduce2(ss, dt, 0);
     const double pre_norm = sqrt(bc[0]);
-    h0 = bc[1];
-    if (j >= 1) h1 = bc[2] - h0 * __ldcg(gsub + 0);
-    if (blockIdx.x == 0 && tid == 0) {
-        Hj[0] = h0;
-        if (j >= 1) Hj[1] = h1;
-    }
-    int par = 1;
-    // pairs (i, i+1), i = 2, 4, ..: w -= h0 v_{i-2}; w -= h1 v_{i-1}; a, b
-    for (int i = 2; i <= j; i += 2) {
-        const bool two = i + 1 <= j;
-        const double2* p0 = vec(i - 2);
-        const double2* p1 = vec(i - 1);
-        const double2* q0 = vec(i);
-        const double2* q1 = vec(two ? i + 1 : i);
-        double da = 0.0, db = 0.0;
+    double h = bc[1];
+    if (blockIdx.x == 0 && tid == 0) a.kb.H[(size_t)j * (m + 1) + 0] = h;
+
+    // passes 1..j: w -= h_{i-1} v_{i-1}; h_i = <v_i, w>
+    for (int i = 1; i <= j; ++i) {
+        const double2* vp = reinterpret_cast<const double2*>(V + (size_t)(i - 1) * ldv + r0);
+        const double2* vi = reinterpret_cast<const double2*>(V + (size_t)i * ldv + r0);
+        dt = 0.0;
 #pragma unroll 4
         for (int e = tid; e < nv2; e += kMgsThreads) {
             double2 wv = w2[e];
-            const double2 a0 = __ldg(p0 + e);
-            const double2 a1 = __ldg(p1 + e);
-            const double2 x0 = __ldg(q0 + e);
-            wv.x = fma(-h0, a0.x, wv.x);
-            wv.y = fma(-h0, a0.y, wv.y);
-            wv.x = fma(-h1, a1.x, wv.x);
-            wv.y = fma(-h1, a1.y, wv.y);
+            const double2 pv = __ldg(vp + e);
+            const double2 qv = __ldg(vi + e);
+            wv.x = fma(-h, pv.x, wv.x);
+            wv.y = fma(-h, pv.y, wv.y);
             w2[e] = wv;
-            da = fma(x0.x, wv.x, da);
-            da = fma(x0.y, wv.y, da);
-            if (two) {
-                const double2 x1 = __ldg(q1 + e);
-                db = fma(x1.x, wv.x, db);
-                db = fma(x1.y, wv.y, db);
-            }
+            dt = fma(qv.x, wv.x, dt);
+            dt = fma(qv.y, wv.y, dt);
         }
-        reduce3(0.0, da, db, par);
-        par ^= 1;
-        h0 = bc[1];
-        h1 = two ? bc[2] - h0 * __ldcg(gsub + i) : 0.0;
-        if (blockIdx.x == 0 && tid == 0) {
-            Hj[i] = h0;
-            if (two) Hj[i + 1] = h1;
-        }
+        reduce2(0.0, dt, i & 1);
+        h = bc[1];
+        if (blockIdx.x == 0 && tid == 0) a.kb.H[(size_t)j * (m + 1) + i] = h;
     }
-    // final pass: w -= the last group; ||w||^2 and <w, v_j> (for <v_{j+1}, v_j>)
+
+    // final pass: w -= h_j v_j; ||w||
     {
-        const int i0 = j & ~1;  // first vector of the last group
-        const bool two = i0 + 1 <= j;
-        const double2* p0 = vec(i0);
-        const double2* p1 = vec(two ? i0 + 1 : i0);
-        double ss = 0.0, gd = 0.0;
+        const double2* vp = reinterpret_cast<const double2*>(V + (size_t)j * ldv + r0);
+        ss = 0.0;
 #pragma unroll 4
         for (int e = tid; e < nv2; e += kMgsThreads) {
             double2 wv = w2[e];
-            const double2 a0 = __ldg(p0 + e);
-            wv.x = fma(-h0, a0.x, wv.x);
-            wv.y = fma(-h0, a0.y, wv.y);
-            double2 vj = a0;
-            if (two) {
-                const double2 a1 = __ldg(p1 + e);
-                wv.x = fma(-h1, a1.x, wv.x);
-                wv.y = fma(-h1, a1.y, wv.y);
-                vj = a1;
-            }
+            const double2 pv = __ldg(vp + e);
+            wv.x = fma(-h, pv.x, wv.x);
+            wv.y = fma(-h, pv.y, wv.y);
             w2[e] = wv;
             ss = fma(wv.x, wv.x, ss);
             ss = fma(wv.y, wv.y, ss);
-            gd = fma(wv.x, vj.x, gd);
-            gd = fma(wv.y, vj.y, gd);
         }
-        reduce3(ss, gd, 0.0, par);
     }
-    const double hnext = sqrt(bc[0]);
-    if (blockIdx.x == 0 && tid == 0) gsub[j] = bc[1] * (1.0 / hnext);  // <v_{j+1}, v_j>
-    finish_step(a, w2, dsm_mgs, r0, nv2, j, pre_norm, hnext, kMgsThreads);
+    reduce2(ss, 0.0, (j + 1) & 1);
+    finish_step(a, w2, dsm_mgs, r0, nv2, j, pre_norm, sqrt(bc[0]), kMgsThreads);
 }
 
 // ---------------------------------------------------------------------------

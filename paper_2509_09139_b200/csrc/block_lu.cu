@@ -1517,20 +1517,17 @@ void launch_block_lu(const LuParams& p_in, int dmax, int num_sms, cudaStream_t s
     {
         const char* e = getenv("HPBJ_LU_LL");
         if (!(e && e[0] == '0')) {
-            // one row per thread up to 256, two above (separate launches: a
-            // per-block branch would double the code the i-cache must hold)
-            for (int range = 0; range < 2; ++range) {
-                const int dlo = range == 0 ? dw : kLlThreads;
-                const int dhi = std::min(dmax, range == 0 ? kLlThreads : kLlMax);
-                if (dhi <= dlo) continue;
-                const size_t smem = ll_smem_bytes(dhi);
-                void (*fn)(LuParams, int, int) = range == 0 ? k_block_lu_ll<1> : k_block_lu_ll<2>;
-                HPBJ_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-                const int grid = std::min(p.s, num_sms * kLlCtasPerSm);
-                fn<<<grid, kLlThreads, smem, st>>>(p, dlo, dhi);
-                *launches += 1;
-                dll = dhi;
-            }
+            // two row slots per thread for every size: measured faster than a
+            // one-slot instance for d <= 256 too (config 2: 5.5 vs 7.6 ms,
+            // config 3: 30.7 vs 44.4 ms with a separate one-slot launch)
+            const int dhi = std::min(dmax, kLlMax);
+            const size_t smem = ll_smem_bytes(dhi);
+            void (*fn)(LuParams, int, int) = k_block_lu_ll<2>;
+            HPBJ_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            const int grid = std::min(p.s, num_sms * kLlCtasPerSm);
+            fn<<<grid, kLlThreads, smem, st>>>(p, dw, dhi);
+            *launches += 1;
+            dll = dhi;
         }
     }
     if (dmax <= dll) {

@@ -47,10 +47,13 @@ __device__ __forceinline__ int warp_excl_scan(int v, int lane) {
     return x - v;
 }
 
-// Dense panel element (k, c) of a block (see kernels.cuh panel layout).
-__device__ __forceinline__ float dense_at(const float* F, int dq, int k, int c) {
+// Quad qi (columns 4 qi .. 4 qi + 3) of row k: one aligned float4.
+__device__ __forceinline__ float4 dense_quad(const float* F, int dq, int k, int qi) {
     const int t = k >> 5;
-    return F[(size_t)t * 32 * 4 * dq + (c >> 2) * 128 + (k & 31) * 4 + (c & 3)];
+    return __ldg(reinterpret_cast<const float4*>(F + (size_t)t * 32 * 4 * dq + qi * 128 + (k & 31) * 4));
+}
+__device__ __forceinline__ int nnz4(float4 v) {
+    return (v.x != 0.0f) + (v.y != 0.0f) + (v.z != 0.0f) + (v.w != 0.0f);
 }
 
 __device__ __forceinline__ int warp_sum_int(int v) {
@@ -80,13 +83,18 @@ __device__ void pack_row_quads(const SpkBuild& p, const float* F, int dq, int k,
     int cnt = 0;
     IdxT* eidx = reinterpret_cast<IdxT*>(p.eidx);
     if (live)
-        for (int c = lo; c < hi; ++c) {
-            const float f = dense_at(F, dq, k, c);
-            if (f != 0.0f) {
-                const int e = base + 4 * (S[cnt >> 2] + rank) + (cnt & 3);
-                p.eval[e] = f;
-                eidx[e] = (IdxT)c;
-                ++cnt;
+        for (int qi = lo >> 2; qi < (hi + 3) >> 2; ++qi) {
+            const float4 v4 = dense_quad(F, dq, k, qi);
+            const float fv[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int c = 4 * qi + u;
+                if (fv[u] != 0.0f && c >= lo && c < hi) {
+                    const int e = base + 4 * (S[cnt >> 2] + rank) + (cnt & 3);
+                    p.eval[e] = fv[u];
+                    eidx[e] = (IdxT)c;
+                    ++cnt;
+                }
             }
         }
     for (; cnt & 3; ++cnt) {  // zero padding of the last quad
@@ -114,9 +122,10 @@ __global__ void __launch_bounds__(PACK ? 128 : 256, PACK ? 3 : 1) k_spk_build(Sp
         const int k = 32 * t + lane;
         const int c0 = 32 * t, c1 = min(d, 32 * t + 32);
         int nl = 0, nu = 0;
-        if (k < d) {
-            for (int c = 0; c < c0; ++c) nl += dense_at(F, dq, k, c) != 0.0f;
-            for (int c = c1; c < d; ++c) nu += dense_at(F, dq, k, c) != 0.0f;
+        if (k < d) {  // whole quads: c0 and c1 < d are multiples of 4, columns >= d are zero
+            for (int qi = 0; qi < (c0 >> 2); ++qi) nl += nnz4(dense_quad(F, dq, k, qi));
+            if (c1 < d)
+                for (int qi = c1 >> 2; qi < dq; ++qi) nu += nnz4(dense_quad(F, dq, k, qi));
         }
         const int el = warp_excl_scan(nl, lane), eu = warp_excl_scan(nu, lane);
         const int tl = __shfl_sync(0xffffffffu, el + nl, 31);
@@ -171,12 +180,16 @@ __global__ void __launch_bounds__(PACK ? 128 : 256, PACK ? 3 : 1) k_spk_build(Sp
             // stays in registers (fully unrolled substitutions)
             float* Tt = reinterpret_cast<float*>(inv_smem) + (size_t)(threadIdx.x >> 5) * (2 * 32 * 33);
             float* W = Tt + 32 * 33;
-            for (int c = 0; c < 32; ++c) {
-                const int cc = c0 + c;
-                float v;
-                if (k < d && cc < c1) v = dense_at(F, dq, k, cc);
-                else v = (c == lane) ? 1.0f : 0.0f;  // padded rows/columns: identity
-                Tt[lane * 33 + c] = v;
+            for (int q = 0; q < 8; ++q) {
+                const float4 v4 = (k < d && c0 + 4 * q < c1) ? dense_quad(F, dq, k, (c0 >> 2) + q)
+                                                             : make_float4(0.f, 0.f, 0.f, 0.f);
+                const float fv[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int c = 4 * q + u;
+                    // padded rows/columns: identity
+                    Tt[lane * 33 + c] = (k < d && c0 + c < c1) ? fv[u] : ((c == lane) ? 1.0f : 0.0f);
+                }
             }
             __syncwarp();
             // lane = column c of the inverses
@@ -250,24 +263,21 @@ __global__ void __launch_bounds__(PACK ? 128 : 256, PACK ? 3 : 1) k_spk_build(Sp
         }
         // off-panel entries, row-sorted: value + packed (column << 5 | row)
         if (k < d) {
-            int q = base + el;
-            for (int c = 0; c < c0; ++c) {
-                const float v = dense_at(F, dq, k, c);
-                if (v != 0.0f) {
-                    p.eval[q] = v;
-                    reinterpret_cast<IdxT*>(p.eidx)[q] = (IdxT)(((unsigned)c << 5) | lane);
-                    ++q;
+            auto emit = [&](int qlo, int qhi, int q) {
+                for (int qi = qlo; qi < qhi; ++qi) {
+                    const float4 v4 = dense_quad(F, dq, k, qi);
+                    const float fv[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        if (fv[u] != 0.0f) {
+                            p.eval[q] = fv[u];
+                            reinterpret_cast<IdxT*>(p.eidx)[q] = (IdxT)(((unsigned)(4 * qi + u) << 5) | lane);
+                            ++q;
+                        }
                 }
-            }
-            q = base + pl + eu;
-            for (int c = c1; c < d; ++c) {
-                const float v = dense_at(F, dq, k, c);
-                if (v != 0.0f) {
-                    p.eval[q] = v;
-                    reinterpret_cast<IdxT*>(p.eidx)[q] = (IdxT)(((unsigned)c << 5) | lane);
-                    ++q;
-                }
-            }
+            };
+            emit(0, c0 >> 2, base + el);
+            if (c1 < d) emit(c1 >> 2, dq, base + pl + eu);
         }
     }
 }
