@@ -387,8 +387,6 @@ int spmv_long_thresh(int g) { return std::max(256, 16 * g); }
 // plan's threshold, in any order
 void set_plan(SpmvPlan& p, int group, std::vector<int>& rows) {
     p.group = group;
-    const char* e = getenv("HPBJ_SPMV_STAGED");
-    p.staged = group == 1 && !(e && e[0] == '0');
     p.long_thresh = spmv_long_thresh(group);
     std::sort(rows.begin(), rows.end());
     p.n_long = (int)rows.size();

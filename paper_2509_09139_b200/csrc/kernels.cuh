@@ -200,7 +200,6 @@ struct SpmvPlan {
     int long_thresh = 256;    // rows longer than this get a CTA of their own
     int n_long = 0;
     int* long_rows = nullptr; // indices of long rows (device), one CTA each
-    bool staged = false;      // group 1: warp-staged products (k_spmv_staged)
 };
 
 // y = A x, x FP32 (preconditioned vector) or FP64; early exit if st->done.

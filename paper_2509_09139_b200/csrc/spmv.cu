@@ -118,100 +118,6 @@ __global__ void __launch_bounds__(kSpmvThreads) k_spmv(DevCsr a, const XT* __res
     }
 }
 
-
-// Short rows (one lane per row): a warp takes 32 consecutive rows and first
-// streams their entries cooperatively — coalesced column / value loads, one
-// entry per lane, the x gathers of 32 entries in flight per instruction —
-// into products in shared memory; then lane r sums row r's products left to
-// right (the reference's order, sum = sum + a_k x_k without contraction).
-// Warps whose rows hold more than kStageCap entries (a hub row among them)
-// take the per-row loop instead.
-constexpr int kStageCap = 512;  // entries per warp (32 rows x 16)
-
-template <class XT, int MODE>
-__global__ void __launch_bounds__(kSpmvThreads) k_spmv_staged(DevCsr a, const XT* __restrict__ x,
-                                                              double* __restrict__ y, const double* __restrict__ bvec,
-                                                              const int* __restrict__ long_rows, int long_thresh,
-                                                              int n_long, SolveState* sst, double* __restrict__ partials) {
-    if (MODE == 0 && sst && sst->done) return;
-    __shared__ double sh[kSpmvThreads / 32];
-    __shared__ double prod[kSpmvThreads / 32][kStageCap];
-    double ss = 0.0;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    if ((int)blockIdx.x < n_long) {  // hub rows: one CTA each
-        const int row = long_rows[blockIdx.x];
-        const int b = __ldg(a.rp + row), e = __ldg(a.rp + row + 1);
-        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-        int k = b + threadIdx.x;
-        for (; k + 3 * kSpmvThreads < e; k += 4 * kSpmvThreads) {
-            s0 = fma(__ldg(a.val + k), ldx(x, __ldg(a.ci + k)), s0);
-            s1 = fma(__ldg(a.val + k + kSpmvThreads), ldx(x, __ldg(a.ci + k + kSpmvThreads)), s1);
-            s2 = fma(__ldg(a.val + k + 2 * kSpmvThreads), ldx(x, __ldg(a.ci + k + 2 * kSpmvThreads)), s2);
-            s3 = fma(__ldg(a.val + k + 3 * kSpmvThreads), ldx(x, __ldg(a.ci + k + 3 * kSpmvThreads)), s3);
-        }
-        for (; k < e; k += kSpmvThreads) s0 = fma(__ldg(a.val + k), ldx(x, __ldg(a.ci + k)), s0);
-        double s = block_sum<kSpmvThreads>((s0 + s1) + (s2 + s3), sh);
-        if (threadIdx.x == 0) {
-            if (MODE == 0) {
-                y[row] = s;
-            } else {
-                const double r = bvec[row] - s;
-                y[row] = r;
-                ss = r * r;
-            }
-        }
-    } else {
-        const int nwarps = (gridDim.x - n_long) * (kSpmvThreads / 32);
-        double* pr = prod[wid];
-        for (int r0 = ((blockIdx.x - n_long) * (kSpmvThreads / 32) + wid) * 32; r0 < a.n; r0 += nwarps * 32) {
-            const int row = r0 + lane;
-            const int rb = row < a.n ? __ldg(a.rp + row) : 0;
-            const int re = row < a.n ? __ldg(a.rp + row + 1) : 0;
-            const int e0 = __shfl_sync(0xffffffffu, rb, 0);
-            const int e1 = __shfl_sync(0xffffffffu, re, min(31, a.n - 1 - r0));
-            const bool mine = row < a.n && re - rb <= long_thresh;  // hub rows: their own CTAs
-            double sum = 0.0;
-            if (e1 - e0 <= kStageCap) {  // warp-uniform
-#pragma unroll 4
-                for (int e = e0 + lane; e < e1; e += 32) pr[e - e0] = __ldg(a.val + e) * ldx(x, __ldg(a.ci + e));
-                __syncwarp();
-                for (int e = rb; e < re; ++e) sum += pr[e - e0];
-                __syncwarp();
-            } else if (mine) {  // a long row among the 32: per-row loop
-                for (int e = rb; e < re; ++e) sum = fma(__ldg(a.val + e), ldx(x, __ldg(a.ci + e)), sum);
-            }
-            if (mine) {
-                if (MODE == 0) {
-                    y[row] = sum;
-                } else {
-                    const double r = bvec[row] - sum;
-                    y[row] = r;
-                    ss = fma(r, r, ss);
-                }
-            }
-        }
-    }
-    if (MODE == 1) {
-        __shared__ bool last;
-        ss = block_sum<kSpmvThreads>(ss, sh);
-        if (threadIdx.x == 0) {
-            partials[blockIdx.x] = ss;
-            __threadfence();
-            const unsigned t = atomicAdd(&sst->ticket, 1u);
-            last = (t == gridDim.x - 1);
-        }
-        __syncthreads();
-        if (last && threadIdx.x < 32) {
-            __threadfence();
-            const double tot = warp_sum_partials(partials, gridDim.x);
-            if (threadIdx.x == 0) {
-                sst->rnorm = sqrt(tot);
-                sst->ticket = 0;
-            }
-        }
-    }
-}
-
 __global__ void __launch_bounds__(kSpmvThreads) k_norm(const double* __restrict__ x, int n, SolveState* sst,
                                                        double* __restrict__ partials) {
     __shared__ double sh[kSpmvThreads / 32];
@@ -250,14 +156,6 @@ template <class XT, int MODE>
 void run(const DevCsr& a, const SpmvPlan& plan, const XT* x, double* y, const double* b, SolveState* sst,
          double* partials, cudaStream_t st, int64_t* launches) {
     const int G = plan.group;
-    if (G == 1 && plan.staged) {
-        const int grid = std::max(1, std::min((a.n + kSpmvThreads - 1) / kSpmvThreads, kMaxRedBlocks)) + plan.n_long;
-        k_spmv_staged<XT, MODE><<<grid, kSpmvThreads, 0, st>>>(a, x, y, b, plan.long_rows, plan.long_thresh,
-                                                              plan.n_long, sst, partials);
-        *launches += 1;
-        HPBJ_CUDA(cudaGetLastError());
-        return;
-    }
     const int main_grid = spmv_grid(a.n, G);
     const int grid = main_grid + plan.n_long;
 #define HPBJ_SPMV_CASE(GG)                                                                              \
