@@ -658,6 +658,10 @@ def hybrid_restart_gmres(a: SparseMatrix, p: Preconditioner, b, config: GmresCon
         raise ValueError("gmres: rhs dimension mismatch")
     if config.restart_m < 1 or config.tol <= 0.0 or config.max_restarts < 1:
         raise ValueError("gmres: invalid config")
+    if config.restart_m > 1024:  # before the history buffers are sized from it
+        raise ValueError("gmres: restart_m > 1024 unsupported")
+    if config.max_restarts > 1 << 24:
+        raise ValueError("gmres: max_restarts too large")
     if config.precision not in ("hybrid", "double"):
         raise ValueError("gmres: unknown precision: " + str(config.precision))
     if p.kind == Preconditioner.IDENTITY:

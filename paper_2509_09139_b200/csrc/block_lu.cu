@@ -965,6 +965,8 @@ __host__ __device__ inline size_t ll_smem_bytes(int dhi) {
 
 // swizzled X: quad (c / 4) of row r at quad slot (c / 4) ^ (r & 7)
 __device__ __forceinline__ int xq(int r, int q) { return r * 32 + ((q ^ (r & 7)) << 2); }
+// element (r, c) of the swizzled X: ((c / 4) ^ (r & 7)) * 4 + c % 4 = c ^ ((r & 7) << 2)
+__device__ __forceinline__ int xe(int r, int c) { return (r << 5) + (c ^ ((r & 7) << 2)); }
 
 __device__ __forceinline__ void bar_named(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
@@ -999,15 +1001,16 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* mb, unsigned parit
 }
 
 // X[r][lane] -= sum_m L[pos][m] u[m], u = this lane's column of the 32 pivot
-// rows prv[0..31] (U of the panel behind L), for the rows given by (pos, row)
+// rows of the panel behind L (ll_load_u), for the rows given by (pos, row)
 // pairs; four rows in flight per warp. `rows(i)` yields {pos, row} or pos < 0.
-template <class Rows>
-__device__ __forceinline__ void ll_rank32(float* X, const float* L, const short* prv, int lane, int i0, int i1,
-                                          int step, Rows rows) {
-    if (i0 >= i1) return;
-    float u[32];
+__device__ __forceinline__ void ll_load_u(float (&u)[32], const float* X, const short* prv, int lane) {
 #pragma unroll
-    for (int m = 0; m < 32; ++m) u[m] = X[xq(prv[m], lane >> 2) + (lane & 3)];
+    for (int m = 0; m < 32; ++m) u[m] = X[xe(prv[m], lane)];
+}
+
+template <class Rows>
+__device__ __forceinline__ void ll_rank32(float* X, const float* L, const float (&u)[32], int lane, int i0, int i1,
+                                          int step, Rows rows) {
     for (int i = i0; i < i1; i += 4 * step) {
         int pos[4], rr[4];
         float v[4];
@@ -1016,7 +1019,7 @@ __device__ __forceinline__ void ll_rank32(float* X, const float* L, const short*
             const int2 pr = (i + t * step < i1) ? rows(i + t * step) : make_int2(-1, 0);
             pos[t] = pr.x;
             rr[t] = pr.y;
-            v[t] = pos[t] >= 0 ? X[xq(rr[t], lane >> 2) + (lane & 3)] : 0.0f;
+            v[t] = pos[t] >= 0 ? X[xe(rr[t], lane)] : 0.0f;
         }
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
@@ -1031,7 +1034,7 @@ __device__ __forceinline__ void ll_rank32(float* X, const float* L, const short*
         }
 #pragma unroll
         for (int t = 0; t < 4; ++t)
-            if (pos[t] >= 0) X[xq(rr[t], lane >> 2) + (lane & 3)] = v[t];
+            if (pos[t] >= 0) X[xe(rr[t], lane)] = v[t];
     }
 }
 
@@ -1158,7 +1161,7 @@ __global__ void __launch_bounds__(kLlThreads, kLlCtasPerSm) k_block_lu_ll(LuPara
                         const int c = __ldg(p.a.ci + cur[i]);
                         if (c >= cend) break;
                         const int lc = c - o - c0;
-                        X[xq(r, lc >> 2) + (lc & 3)] = __double2float_rn(__ldg(p.a.val + cur[i]));
+                        X[xe(r, lc)] = __double2float_rn(__ldg(p.a.val + cur[i]));
                         ++cur[i];
                     }
                 }
@@ -1173,11 +1176,15 @@ __global__ void __launch_bounds__(kLlThreads, kLlCtasPerSm) k_block_lu_ll(LuPara
                 const int q0 = 32 * Q;
                 const short* prv = prow + (Q > 0 ? q0 - 32 : 0);  // U_{Q-1}: pivot rows of Q - 1
                 const int nprev = Q > 0 ? d - (q0 - 32) : 0;       // rows of L_{Q-1}
-                if (Q > 0) mbar_wait(&mbar[0], (nb_issue - 1) & 1u);  // Lb = rows 32.. of L_{Q-1}
+                float u[32];  // this lane's column of U_{Q-1} (A_Q, B_Q and the final step)
+                if (Q > 0) {
+                    ll_load_u(u, X, prv, lane);
+                    mbar_wait(&mbar[0], (nb_issue - 1) & 1u);  // Lb = rows 32.. of L_{Q-1}
+                }
                 if (Q == P) {  // (ii)_{P-1} on the rows still active
                     if (Q > 0) {
                         const short* rP = rowQ + lofs[Q - 1];
-                        ll_rank32(X, Lb - 32 * 32, prv, lane, 32 + wid, nprev, NW,
+                        ll_rank32(X, Lb - 32 * 32, u, lane, 32 + wid, nprev, NW,
                                   [&](int a) { return make_int2(a, (int)rP[a]); });
                         __syncthreads();
                     }
@@ -1185,7 +1192,7 @@ __global__ void __launch_bounds__(kLlThreads, kLlCtasPerSm) k_block_lu_ll(LuPara
                 }
                 if (Q > 0) {  // A_Q: (ii)_{Q-1} on Q's pivot rows
                     const short* posp = posQ + (size_t)(Q - 1) * dhi;
-                    ll_rank32(X, Lb - 32 * 32, prv, lane, wid, 32, NW, [&](int i) {
+                    ll_rank32(X, Lb - 32 * 32, u, lane, wid, 32, NW, [&](int i) {
                         const int r = prow[q0 + i];
                         return make_int2((int)posp[r], r);
                     });
@@ -1197,14 +1204,14 @@ __global__ void __launch_bounds__(kLlThreads, kLlCtasPerSm) k_block_lu_ll(LuPara
                     const float* LQ = L11 + sb * 1024;
                     float x[32];
 #pragma unroll
-                    for (int m = 0; m < 32; ++m) x[m] = X[xq(prow[q0 + m], lane >> 2) + (lane & 3)];
+                    for (int m = 0; m < 32; ++m) x[m] = X[xe(prow[q0 + m], lane)];
                     ll_trsv<0>(x, LQ);
 #pragma unroll
-                    for (int m = 0; m < 32; ++m) X[xq(prow[q0 + m], lane >> 2) + (lane & 3)] = x[m];
+                    for (int m = 0; m < 32; ++m) X[xe(prow[q0 + m], lane)] = x[m];
                 } else if (Q > 0) {  // B_Q, other warps: (ii)_{Q-1} on the rows active after Q
                     const short* rP = rowQ + lofs[Q - 1];
                     const int qhi = q0 + 32;
-                    ll_rank32(X, Lb - 32 * 32, prv, lane, 32 + (wid - 1), nprev, NW - 1, [&](int a) {
+                    ll_rank32(X, Lb - 32 * 32, u, lane, 32 + (wid - 1), nprev, NW - 1, [&](int a) {
                         const int r = rP[a];
                         return make_int2(ppos[r] >= qhi ? a : -1, r);  // Q's pivot rows: done in A_Q
                     });
@@ -1314,6 +1321,8 @@ __global__ void __launch_bounds__(kLlThreads, kLlCtasPerSm) k_block_lu_ll(LuPara
                         abort = true;
                         break;
                     }
+                    if (wid == 0 && c + lane < 32)  // the pivot row's U row (columns c..31) is final
+                        X[xe(frow, c + lane)] = lane == 0 ? pv : reinterpret_cast<const float*>(Pv4)[lane];
                     float pw[32];  // the pivot row's window
 #pragma unroll
                     for (int q = 0; q < 8; ++q) {
@@ -1325,19 +1334,13 @@ __global__ void __launch_bounds__(kLlThreads, kLlCtasPerSm) k_block_lu_ll(LuPara
                     }
 #pragma unroll
                     for (int i = 0; i < RPT; ++i) {
-                        if (owner == tid + NT * i) {  // the pivot row: its U row (columns c..31) is final
-                            rv[i][0] = pv;
+                        if (owner == tid + NT * i) {  // the pivot row (its U row goes to X below)
                             fl[i] = true;
                             prow[k] = (short)myrow[i];
                             ppos[myrow[i]] = (short)k;
-#pragma unroll
-                            for (int j = 0; j < 32; ++j) {
-                                const int cc = c + j;
-                                if (cc < 32) X[xq(myrow[i], cc >> 2) + (cc & 3)] = rv[i][j];
-                            }
                         } else if (!fl[i]) {
                             const float l = div_mult(rv[i][0], pv);  // L(i,k) = x_i / pivot (lu.cpp:207)
-                            X[xq(myrow[i], c >> 2) + (c & 3)] = l;
+                            X[xe(myrow[i], c)] = l;
 #pragma unroll
                             for (int j = 1; j < 32; ++j) rv[i][j - 1] = fmaf(-l, pw[j], rv[i][j]);
                         }

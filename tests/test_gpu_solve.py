@@ -4,6 +4,7 @@ reference (Hybrid mode) — north-star bars:
   * iteration count within 5% of the reference's
   * ||x - x_ref|| / ||x_ref|| <= 1e-6
 plus the reference's Krylov known-answer tests (test_krylov.cpp)."""
+import ctypes
 import json
 import os
 
@@ -318,8 +319,16 @@ def test_update_values_then_gmres_solves_new_matrix():
 def test_invalid_restart_m_rejected_before_allocation():
     a = fx.diag_csr([2.0, 3.0])
     p = hp.Preconditioner.block_jacobi(a, hp.partition_from_assignment([0, 1], 2))
-    for m in (0, 1025, 10 ** 9):
+    for m in (0, 1025, 10 ** 9):  # rejected before any buffer is sized from m (Python and C ABI)
         with pytest.raises(ValueError):
             hp.hybrid_restart_gmres(a, p, [1.0, 1.0], hp.GmresConfig(restart_m=m))
+    o = hp._abi.GmresOpts()
+    hp.library().hpbj_gmres_default_opts(ctypes.byref(o))
+    o.restart_m = 10 ** 9
+    x = np.zeros(2)
+    b = np.ones(2)
+    rc = hp.library().hpbj_gmres(p.ctx.h, b.ctypes.data_as(hp._abi.f64p), x.ctypes.data_as(hp._abi.f64p),
+                                 ctypes.byref(o), None, None, 0, None, 0)
+    assert rc == hp._abi.HPBJ_EINVAL
     r = hp.hybrid_restart_gmres(a, p, [1.0, 1.0], hp.GmresConfig(restart_m=5, tol=1e-12))
     assert r.report.converged
