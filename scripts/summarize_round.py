@@ -16,7 +16,7 @@ def short(name):
     return re.sub(r"spk::", "", n)
 
 
-# 1) launch shares of the bench (config 1, NOGRAPH) -------------------------
+# 1) launch shares of the bench (BENCH_CONFIG, default 3; NOGRAPH) -------------------------
 p = f"{SRC}/{RND}_launches_bench.csv"
 if os.path.exists(p):
     rows = [r for r in csv.reader(open(p)) if len(r) > 10]
@@ -30,7 +30,7 @@ if os.path.exists(p):
     lines = ["kernel,launches,total_us,mean_us,share"]
     for k, (n, us) in sorted(tot.items(), key=lambda kv: -kv[1][1]):
         lines.append(f"\"{k}\",{n},{us:.1f},{us / n:.2f},{us / allus:.4f}")
-    open(f"{OUT}/{RND}_launch_shares_bench_config1.csv", "w").write("\n".join(lines) + "\n")
+    open(f"{OUT}/{RND}_launch_shares_bench_config{os.environ.get('BENCH_CONFIG', '3')}.csv", "w").write("\n".join(lines) + "\n")
     print("\n".join(lines[:14]))
 
 # 2) full captures -----------------------------------------------------------
@@ -46,6 +46,7 @@ want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
 BS = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
 summary, traffic = {}, collections.defaultdict(dict)
 kmap = {"apply": "bj_apply_f32", "spmv": "spmv_csr_f64", "icwy": "arnoldi_mgs_f64", "mgs": "arnoldi_mgs_f64",
+        "lu": "block_lu_f32", "spk_build": "spk_build",
         "arnoldi_cycle": "arnoldi_cycle_fused"}
 for f in sorted(os.listdir(SRC)):
     if not (f.startswith(f"{RND}_prof_") and f.endswith(".ncu-rep")):
@@ -94,7 +95,8 @@ if os.path.exists(so):
     index = []
     hot = ("k_apply_spk<float, unsigned short, false, false, SrcDown", "k_apply_spk<float, unsigned short, false, true, SrcDown",
            "k_apply_spk<float, unsigned short, true, false, SrcDown", "k_arnoldi_cycle<false", "k_spmv<1, float", "k_spmv<2, float",
-           "k_icwy<true", "k_mgs<true", "k_block_lu_blk", "k_block_lu_warp<3", "k_spk_build<true, unsigned short")
+           "k_icwy<true", "k_mgs<true", "k_block_lu_ll", "k_block_lu_pair<3", "k_spk_build<true, unsigned short",
+           "k_spk_build<false")
     for fn in funcs[1:]:
         name = fn.split("\n", 1)[0].strip()
         dn = subprocess.run(["c++filt", name], capture_output=True, text=True).stdout.strip()

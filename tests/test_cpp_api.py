@@ -24,8 +24,16 @@ EXE = os.path.join(ROOT, "paper_2509_09139_b200", "build_obj", "test_api")
 DROPIN = os.path.join(ROOT, "oracle", "_ref", "run_spec_dropin")
 
 
+def _newest_input():
+    inc = os.path.join(ROOT, "include")
+    files = [SRC, os.path.join(LIBDIR, "libhpbj.so")]
+    for d, _, fs in os.walk(inc):
+        files += [os.path.join(d, f) for f in fs]
+    return max(os.path.getmtime(f) for f in files if os.path.exists(f))
+
+
 def build_exe():
-    if not os.path.exists(EXE) or os.path.getmtime(EXE) < max(os.path.getmtime(SRC), os.path.getmtime(HDR)):
+    if not os.path.exists(EXE) or os.path.getmtime(EXE) < _newest_input():
         subprocess.run(["g++", "-std=c++20", "-O2", "-Wall", "-Werror", "-I" + os.path.join(ROOT, "include"), SRC,
                         "-L" + LIBDIR, "-lhpbj", "-Wl,-rpath," + LIBDIR, "-o", EXE], check=True)
     return EXE
