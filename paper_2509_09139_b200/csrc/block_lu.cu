@@ -1146,6 +1146,8 @@ __global__ void __launch_bounds__(kLlThreads, kLlCtasPerSm) k_block_lu_ll(LuPara
         bool abort = false;
         int buf = 0;
         for (int P = 0; P < T; ++P) {
+            unsigned long long tp0 = 0;
+            if (p.prof && tid == 0) tp0 = clock64();
             const int c0 = 32 * P;
             const int kw = min(32, d - c0);
             // ---- gather the column panel (rows in original order)
@@ -1228,6 +1230,8 @@ __global__ void __launch_bounds__(kLlThreads, kLlCtasPerSm) k_block_lu_ll(LuPara
                 nb_issue += 1;
             }
             // ---- factor the panel: thread a owns active rows act[a + NT i];
+            unsigned long long tp1 = 0;
+            if (p.prof && tid == 0) tp1 = clock64();
             // only the warps holding rows take part (named barrier 1). A
             // rolled column loop over a shifting register window (rv[j] =
             // column c + j) keeps the code small: the rank-1 update writes
@@ -1323,15 +1327,6 @@ __global__ void __launch_bounds__(kLlThreads, kLlCtasPerSm) k_block_lu_ll(LuPara
                     }
                     if (wid == 0 && c + lane < 32)  // the pivot row's U row (columns c..31) is final
                         X[xe(frow, c + lane)] = lane == 0 ? pv : reinterpret_cast<const float*>(Pv4)[lane];
-                    float pw[32];  // the pivot row's window
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        const float4 t4 = Pv4[q];
-                        pw[4 * q + 0] = t4.x;
-                        pw[4 * q + 1] = t4.y;
-                        pw[4 * q + 2] = t4.z;
-                        pw[4 * q + 3] = t4.w;
-                    }
 #pragma unroll
                     for (int i = 0; i < RPT; ++i) {
                         if (owner == tid + NT * i) {  // the pivot row (its U row goes to X below)
@@ -1341,8 +1336,22 @@ __global__ void __launch_bounds__(kLlThreads, kLlCtasPerSm) k_block_lu_ll(LuPara
                         } else if (!fl[i]) {
                             const float l = div_mult(rv[i][0], pv);  // L(i,k) = x_i / pivot (lu.cpp:207)
                             X[xe(myrow[i], c)] = l;
+                            // the pivot row's window quad by quad from the candidate
+                            // slot (not held in registers: 128 per thread)
+                            {
+                                const float4 w0 = Pv4[0];
+                                rv[i][0] = fmaf(-l, w0.y, rv[i][1]);
+                                rv[i][1] = fmaf(-l, w0.z, rv[i][2]);
+                                rv[i][2] = fmaf(-l, w0.w, rv[i][3]);
+                            }
 #pragma unroll
-                            for (int j = 1; j < 32; ++j) rv[i][j - 1] = fmaf(-l, pw[j], rv[i][j]);
+                            for (int q = 1; q < 8; ++q) {
+                                const float4 wq = Pv4[q];
+                                rv[i][4 * q - 1] = fmaf(-l, wq.x, rv[i][4 * q]);
+                                rv[i][4 * q + 0] = fmaf(-l, wq.y, rv[i][4 * q + 1]);
+                                rv[i][4 * q + 1] = fmaf(-l, wq.z, rv[i][4 * q + 2]);
+                                rv[i][4 * q + 2] = fmaf(-l, wq.w, rv[i][4 * q + 3]);
+                            }
                         }
                     }
                 }
@@ -1350,6 +1359,7 @@ __global__ void __launch_bounds__(kLlThreads, kLlCtasPerSm) k_block_lu_ll(LuPara
             abort = __syncthreads_or(abort);
             if (abort) break;
             // ---- compact the active list (stable); L_P to the scratch: the 32
+            if (p.prof && tid == 0) { const unsigned long long t2 = clock64(); atomicAdd(p.prof + 0, tp1 - tp0); atomicAdd(p.prof + 1, t2 - tp1); tp0 = t2; }
             // pivot rows first, in pivot order, then the rows still active
             if (wid == 0) {
                 int w = 0;
@@ -1418,6 +1428,7 @@ __global__ void __launch_bounds__(kLlThreads, kLlCtasPerSm) k_block_lu_ll(LuPara
             }
             na = nnew;
             __syncthreads();
+            if (p.prof && tid == 0) atomicAdd(p.prof + 2, clock64() - tp0);
         }
         if (tid == 0) p.pert_count[b] = nperturb;
         if (!abort)

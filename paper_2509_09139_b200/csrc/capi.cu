@@ -264,6 +264,7 @@ struct hpbj_ctx {
     bool use_fused = true;
     FusedPlan fused;  // per-solve: whole Arnoldi cycle in one kernel when ok
     unsigned long long* d_fprof = nullptr;  // HPBJ_FUSED_PROF=1: phase timers of the fused kernel
+    unsigned long long* d_lu_prof = nullptr;  // HPBJ_LU_PROF=1: phase timers of the left-looking LU
     cudaGraphExec_t graph_exec = nullptr;
     int graph_builds = 0;
     std::vector<uintptr_t> graph_sig;
@@ -278,6 +279,7 @@ struct hpbj_ctx {
         t_slots = &slots;
         if (graph_exec) cudaGraphExecDestroy(graph_exec);
         if (d_fprof) cudaFree(d_fprof);
+        if (d_lu_prof) cudaFree(d_lu_prof);
         release_matrix();
         release_ws();
         if (stream) cudaStreamDestroy(stream);
@@ -531,6 +533,12 @@ void factor(hpbj_ctx* c, hpbj_setup_info* info) {
     p.scratch = c->d_lu_scratch;
     p.smem_dim = c->lu_smem_dim;
     p.scratch_ld = c->lu_scratch_ld;
+    static const bool lu_prof = getenv("HPBJ_LU_PROF") != nullptr;
+    if (lu_prof) {
+        if (!c->d_lu_prof) HPBJ_CUDA(cudaMalloc(&c->d_lu_prof, 4 * sizeof(unsigned long long)));
+        HPBJ_CUDA(cudaMemsetAsync(c->d_lu_prof, 0, 4 * sizeof(unsigned long long), st));
+        p.prof = c->d_lu_prof;
+    }
     cudaEvent_t e0, e1, eg, el;
     HPBJ_CUDA(cudaEventCreate(&e0));
     HPBJ_CUDA(cudaEventCreate(&e1));
@@ -548,6 +556,14 @@ void factor(hpbj_ctx* c, hpbj_setup_info* info) {
     HPBJ_CUDA(cudaMemcpyAsync(&sing, c->d_singular, sizeof(sing), cudaMemcpyDeviceToHost, st));
     HPBJ_CUDA(cudaMemcpyAsync(&pert_n, c->d_pert_n, sizeof(int), cudaMemcpyDeviceToHost, st));
     HPBJ_CUDA(cudaStreamSynchronize(st));
+    if (lu_prof) {
+        unsigned long long t[3];
+        HPBJ_CUDA(cudaMemcpy(t, c->d_lu_prof, sizeof(t), cudaMemcpyDeviceToHost));
+        const double tot = double(t[0] + t[1] + t[2]);
+        fprintf(stderr, "[hpbj lu] CTA cycles: left-looking updates %.3g (%.0f%%), panel factorisation %.3g (%.0f%%), "
+                        "L store + output %.3g (%.0f%%)\n", double(t[0]), 100 * t[0] / tot, double(t[1]),
+                100 * t[1] / tot, double(t[2]), 100 * t[2] / tot);
+    }
     float ms = 0.f, ms_lu = 0.f, ms_spk = 0.f;
     HPBJ_CUDA(cudaEventElapsedTime(&ms, e0, e1));
     HPBJ_CUDA(cudaEventElapsedTime(&ms_lu, eg, el));

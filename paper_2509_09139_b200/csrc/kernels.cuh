@@ -50,6 +50,7 @@ struct LuParams {
     int* pert_n;
     int pert_cap;
     unsigned long long* singular;  // min over (block << 32 | column); ~0 if none
+    unsigned long long* prof = nullptr;  // optional phase timers of k_block_lu_ll (HPBJ_LU_PROF=1)
     double eps;
     float* scratch;         // global tiles for blocks too large for shared memory
     int smem_dim;           // blocks with dim <= smem_dim factor in shared memory
