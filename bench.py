@@ -75,6 +75,7 @@ WORKLOADS = {
     4: "config4: transient Newton sequence, 64 steps sharing one pattern, n=100,000, bs 64, GMRES(30), tol 1e-10",
 }
 KNAMES = ["bj_apply_f32", "spmv_csr_f64", "arnoldi_mgs_f64", "arnoldi_cycle_fused"]
+FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # B200 CUDA-core FP32 FMA peak at the 1965 MHz max clock
 
 
 # ---------------------------------------------------------------- inputs
@@ -410,8 +411,11 @@ def measure_config(c, steps, warmup, local, sampler=None, prof_steps=None):
     if fused:  # fused path: the unfused kernels timed separately (the north star's per-kernel fractions)
         ku = profile_kernels(ctx, device_step, flush, ps, fused=False)
         kern.update({k: v for k, v in kernel_table(ku, peak).items() if k != "arnoldi_cycle_fused"})
+    dims = np.diff(np.asarray(part.block_starts, dtype=np.float64))
+    lu_flops = float(np.sum(2.0 / 3.0 * dims ** 3))  # dense LU of every diagonal block
     return {
         "sys": s, "a": a, "ctx": ctx, "cfg": cfg, "flush": flush, "assignment": part.assignment,
+        "lu_flops": lu_flops,
         "value": sum(times) / steps, "times": times, "launches": launches, "rep": rep, "x": x,
         "breakdown_ms": {"partition_host": (t1 - t0) * 1e3, "bj_setup": (t2 - t1) * 1e3,
                          "permute_dev": setup_dev["ms_permute"], "factor_dev": setup_dev["ms_factor"],
@@ -454,12 +458,18 @@ def roofline_of(m, config):
         except Exception:
             traffic = None
     total = sum(per_system.values())
+    lu_ms = m["breakdown_ms"]["lu_dev"]
+    lu = {"ms": lu_ms, "flops": m["lu_flops"], "tflops": m["lu_flops"] / (lu_ms * 1e-3) / 1e12 if lu_ms else None,
+          "fp32_peak_tflops": FP32_PEAK_TFLOPS,
+          "fp32_frac": (m["lu_flops"] / (lu_ms * 1e-3) / 1e12 / FP32_PEAK_TFLOPS) if lu_ms else None,
+          "note": "batched FP32 LU on CUDA cores (no tensor-core path: bit-exact FP32 fmaf chains); "
+                  "flops = sum (2/3) d^3 over the blocks"}
     return {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "peak_source": peak_kind, "traffic": traffic,
             "bytes_per_launch": kern[dom]["bytes_per_launch"],
             "device_ms_per_system": {k: round(v, 3) for k, v in per_system.items()},
             "share_of_device_time": round(per_system[dom] / total, 3) if total else None,
-            "largest_device_kernel": dom_any}
+            "largest_device_kernel": dom_any, "block_lu_f32": lu}
 
 
 def run_gpu_arm(args):
