@@ -41,6 +41,8 @@
 #include <vector>
 
 #include <omp.h>
+#include <sys/mman.h>
+#include <new>
 
 #include "../hpbj_common.hpp"
 
@@ -223,28 +225,75 @@ void partition_from_assignment(int64_t n, const int64_t* assignment, int64_t s, 
 
 namespace {
 
+// Host buffer on transparent huge pages (2 MB-aligned anonymous mapping +
+// MADV_HUGEPAGE): the BFS and the refinement sweep access these arrays at
+// random, and with 4 KB pages most of those accesses also miss the TLB.
+template <class T>
+struct HBuf {
+    T* p = nullptr;
+    size_t n = 0, len = 0;
+    void* base = nullptr;
+    HBuf() = default;
+    HBuf(const HBuf&) = delete;
+    HBuf& operator=(const HBuf&) = delete;
+    ~HBuf() { release(); }
+    void release() {
+        if (base) munmap(base, len);
+        base = nullptr;
+        p = nullptr;
+        n = 0;
+    }
+    void fit(size_t m) {
+        if (m <= n) return;
+        release();
+        constexpr size_t kHuge = size_t(2) << 20;
+        const size_t bytes = (m * sizeof(T) + kHuge - 1) / kHuge * kHuge;
+        len = bytes + kHuge;
+        base = mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+        if (base == MAP_FAILED) {
+            base = nullptr;
+            throw std::bad_alloc();
+        }
+        const uintptr_t a = (reinterpret_cast<uintptr_t>(base) + kHuge - 1) & ~(uintptr_t)(kHuge - 1);
+        p = reinterpret_cast<T*>(a);
+        madvise(p, bytes, MADV_HUGEPAGE);
+        n = m;
+    }
+    T* data() { return p; }
+    const T* data() const { return p; }
+    size_t size() const { return n; }
+    T& operator[](size_t i) { return p[i]; }
+};
+
 // Reusable host workspace (repeated setups — e.g. the transient Newton
 // sequence — never page-fault fresh buffers).
 struct PartWork {
-    std::vector<double> wk;
-    std::vector<int64_t> deg;
-    std::vector<int32_t> state;
-    std::vector<int32_t> queue;
-    std::vector<uint64_t> taken;
-    std::vector<int16_t> state16;
-    std::vector<int32_t> order;
-    std::vector<int64_t> dstart;
-    std::vector<int64_t> sizes;
-    std::vector<double> conn;
-    std::vector<int32_t> adj_start;
-    std::vector<int32_t> adj_nbr;
-    std::vector<double> adj_w;
+    HBuf<double> wk;
+    HBuf<int64_t> deg;
+    HBuf<int32_t> state;
+    HBuf<int32_t> queue;
+    HBuf<uint64_t> taken;
+    HBuf<int16_t> state16;
+    HBuf<int32_t> order;
+    HBuf<int64_t> dstart;
+    HBuf<int64_t> sizes;
+    HBuf<double> conn;
+    HBuf<int32_t> adj_start;
+    HBuf<int32_t> adj_nbr;
+    HBuf<double> adj_w;
+    // refinement (parallel sweep)
+    HBuf<uint8_t> spec;  // S per node
+    HBuf<uint8_t> fl;
 };
 thread_local PartWork t_work;
 
 template <class T>
 void fit(std::vector<T>& v, size_t n) {
     if (v.size() < n) v.resize(n);
+}
+template <class T>
+void fit(HBuf<T>& v, size_t n) {
+    v.fit(n);
 }
 
 // Graph view: neighbours of u are idx[st[u] .. st[u+1]) with weights w[k];
@@ -324,6 +373,191 @@ int64_t refine_sweep(const GraphView<Idx, Off>& g, S* state, int64_t* sizes, int
         ++moves;
     }
     return moves;
+}
+
+// The same sweep, exact, with the scan work spread over T threads.
+//
+// The sequential sweep's decision for u reads (a) the block of every
+// neighbour v — final if v < u, initial if v > u (a node changes only at its
+// own step) — and (b) the block sizes at step u. Phase 1 (parallel): thread t
+// sweeps its contiguous range [lo, hi) as if it were alone — neighbours in
+// earlier ranges at their initial blocks, its own moves applied to a private
+// copy `spec` and private sizes — and records, for every node with a block
+// more strongly connected than its own, the candidates in the reference's
+// preference order (conn desc, block asc), each with conn > conn[bu]. For
+// such a node the reference's decision under ANY sizes is: skip if
+// sizes[bu] <= 1, else the first candidate with sizes + 1 <= cap, else stay;
+// every other node stays whatever the sizes. Phase 2 (sequential, in u order,
+// on the real state): decide every recorded node from its list with the real
+// sizes. A node's list is exact unless some lower neighbour's real final block
+// differs from the one phase 1 assumed for it (its `spec` block in the same
+// range, its initial block across ranges); whenever a node's real block
+// differs from what a higher neighbour assumed, that neighbour is marked dirty
+// and phase 2 recomputes it from the real state (refine_decide), as the
+// sequential sweep would. Phase 2 only scans the neighbours of nodes whose
+// outcome differs from an assumption, so its cost is the cross-range
+// boundary plus the few decisions the size limits change.
+template <class Idx, class Off, class S>
+int64_t refine_sweep_par(const GraphView<Idx, Off>& g, S* state, int64_t* sizes, int64_t s, int64_t cap, int T) {
+    const int64_t n = g.n;
+    const Off* st = g.st;
+    const Idx* nb = g.idx;
+    const double* w = g.w;
+    const auto t_p0 = std::chrono::steady_clock::now();
+    PartWork& W = t_work;
+    fit(W.spec, n * sizeof(S));
+    fit(W.fl, n);
+    S* spec = reinterpret_cast<S*>(W.spec.data());
+    // per node: bit 0 recorded, bit 1 has a higher neighbour in a later range, bit 2 dirty
+    uint8_t* fl = W.fl.data();
+    std::vector<std::vector<int32_t>> rec(T);
+    std::vector<int64_t> lo(T + 1);
+    for (int t = 0; t <= T; ++t) lo[t] = n * t / T;
+    std::vector<int64_t> sizes0(sizes, sizes + s);
+#pragma omp parallel num_threads(T)
+    {
+        const int t = omp_get_thread_num();
+        const int64_t a = lo[t], e = lo[t + 1];
+        std::memcpy(spec + a, state + a, sizeof(S) * (e - a));
+        std::vector<double> conn(s, 0.0);
+        std::vector<int64_t> sz(sizes0);
+        std::vector<int32_t> tch, cand;
+        std::vector<int32_t>& R = rec[t];
+        R.reserve((size_t)(e - a) / 2);
+        for (int64_t u = a; u < e; ++u) {
+            const int32_t bu = spec[u];
+            bool cross = false, inter = true;
+            for (Off k = st[u]; k < st[u + 1]; ++k) {
+                const int64_t v = nb[k];
+                cross |= v >= e;
+                const int32_t bv = (v >= a && v < e) ? (int32_t)spec[v] : (int32_t)state[v];
+                inter &= bv == bu;
+            }
+            fl[u] = cross ? 2 : 0;
+            if (inter) continue;  // only bu touched: stays under any sizes
+            tch.clear();
+            for (Off k = st[u]; k < st[u + 1]; ++k) {
+                const int64_t v = nb[k];
+                const int32_t bv = (v >= a && v < e) ? (int32_t)spec[v] : (int32_t)state[v];
+                if (conn[bv] == 0.0) tch.push_back(bv);
+                conn[bv] += w[k];
+            }
+            cand.clear();
+            bool nan = std::isnan(conn[bu]);
+            for (int32_t bv : tch) {
+                nan |= std::isnan(conn[bv]);
+                if (bv != bu && conn[bv] > conn[bu]) cand.push_back(bv);
+            }
+            if (nan) {  // NaN weights (explicit graphs): no total order; phase 2 decides it
+                for (int32_t bv : tch) conn[bv] = 0.0;
+                fl[u] |= 4;
+                continue;
+            }
+            std::sort(cand.begin(), cand.end(), [&](int32_t x, int32_t y) {
+                return conn[x] > conn[y] || (conn[x] == conn[y] && x < y);
+            });
+            for (int32_t bv : tch) conn[bv] = 0.0;
+            if (cand.empty()) continue;
+            fl[u] |= 1;
+            R.push_back((int32_t)cand.size());
+            R.insert(R.end(), cand.begin(), cand.end());
+            if (sz[bu] <= 1) continue;  // speculative decision with this range's sizes
+            for (int32_t bv : cand)
+                if (sz[bv] + 1 <= cap) {
+                    spec[u] = (S)bv;
+                    --sz[bu];
+                    ++sz[bv];
+                    break;
+                }
+        }
+    }
+    const auto t_p1 = std::chrono::steady_clock::now();
+    // phase 2
+    std::vector<double> conn(s, 0.0);
+    int64_t ndirty = 0, nrec = 0, nscan = 0;
+    int64_t maxdeg = 0;
+    for (int64_t u = 0; u < n; ++u) maxdeg = std::max<int64_t>(maxdeg, (int64_t)(st[u + 1] - st[u]));
+    std::vector<int32_t> tch(maxdeg + 1);
+    int64_t moves = 0;
+    for (int t = 0; t < T; ++t) {
+        const int32_t* r = rec[t].data();
+        const int64_t a = lo[t], e = lo[t + 1];
+        int64_t u = a;
+        while (u < e) {
+            // skip 8 quiet nodes at a time
+            if (u + 8 <= e) {
+                uint64_t wd;
+                std::memcpy(&wd, &fl[u], 8);
+                if (wd == 0) {
+                    u += 8;
+                    continue;
+                }
+            }
+            const uint8_t f = fl[u];
+            if (!f) {
+                ++u;
+                continue;
+            }
+            const int32_t bu = state[u];
+            int32_t d = -1;
+            ndirty += (f & 4) != 0;
+            nrec += (f & 1) != 0;
+            if (f & 4) {
+                d = refine_decide(g, state, sizes, cap, conn.data(), tch.data(), u);
+                if (f & 1) r += 1 + r[0];
+            } else if (f & 1) {
+                const int nc = r[0];
+                if (sizes[bu] > 1)
+                    for (int i = 1; i <= nc; ++i)
+                        if (sizes[r[i]] + 1 <= cap) {
+                            d = r[i];
+                            break;
+                        }
+                r += 1 + nc;
+            }
+            const int32_t fin = d >= 0 ? d : bu;
+            if (d >= 0) {
+                state[u] = (S)d;
+                --sizes[bu];
+                ++sizes[d];
+                ++moves;
+            }
+            const bool same_diff = fin != (int32_t)spec[u];  // what later nodes of this range assumed
+            const bool cross_diff = (f & 2) && fin != bu;    // what later ranges assumed (the initial block)
+            nscan += same_diff || cross_diff;
+            if (same_diff || cross_diff)
+                for (Off k = st[u]; k < st[u + 1]; ++k) {
+                    const int64_t v = nb[k];
+                    if (v <= u) continue;
+                    if (v < e ? same_diff : cross_diff) fl[v] |= 4;
+                }
+            ++u;
+        }
+    }
+    if (getenv("HPBJ_DEBUG"))
+        fprintf(stderr, "[hpbj]   refine: T=%d phase1 %.1f ms, phase2 %.1f ms, %lld recorded, %lld recomputed, %lld scanned\n", T,
+                std::chrono::duration<double, std::milli>(t_p1 - t_p0).count(),
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_p1).count(),
+                (long long)nrec, (long long)ndirty, (long long)nscan);
+    return moves;
+}
+
+// Share of nodes (every 61st sampled) with a higher neighbour in a later one
+// of T equal node ranges: the parallel sweep's phase 2 recomputes about that
+// share of the moved nodes' neighbours, so on graphs whose edges ignore the
+// node order (random couplings: configs 2 and 4) the one-thread sweep is
+// faster.
+template <class Idx, class Off>
+double cross_range_fraction(const GraphView<Idx, Off>& g, int T) {
+    int64_t hit = 0, cnt = 0;
+    for (int64_t u = 0; u < g.n; u += 61) {
+        const int64_t e = (u * T / g.n + 1) * g.n / T;
+        bool c = false;
+        for (Off k = g.st[u]; k < g.st[u + 1]; ++k) c |= (int64_t)g.idx[k] >= e;
+        hit += c;
+        ++cnt;
+    }
+    return cnt ? (double)hit / cnt : 0.0;
 }
 
 template <class Idx, class Off>
@@ -480,7 +714,15 @@ void partition_view(const GraphView<Idx, Off>& g, int64_t s, double tol, int64_t
                 heap.push({sizes[k.second], k.second});
             }
         }
-        const int64_t moves = refine_sweep(g, state, sizes, cap, conn, pf);
+        // HPBJ_PART_SEQ=1: the one-thread sweep (the parallel one is exact; the
+        // switch exists for the equality test)
+        // HPBJ_REFINE_T=k forces the parallel sweep with k ranges (tests)
+        const bool seq = getenv("HPBJ_PART_SEQ") != nullptr;
+        const char* force = getenv("HPBJ_REFINE_T");
+        const int T = force ? std::max(2, atoi(force)) : std::min(omp_get_max_threads(), 32);
+        const int64_t moves = (seq || (!force && (T < 2 || n <= 65536 || cross_range_fraction(g, T) > 0.25)))
+                                  ? refine_sweep(g, state, sizes, cap, conn, pf)
+                                  : refine_sweep_par(g, state, sizes, s, cap, T);
         if (dbg)
             fprintf(stderr, "[hpbj]   grow %.1f ms, refine %.1f ms (%lld moves)\n",
                     std::chrono::duration<double, std::milli>(t_grown - t_seed).count(),

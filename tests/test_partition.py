@@ -195,6 +195,50 @@ def test_laplacian_and_mesh_fixtures_match_reference(ref):
         assert np.array_equal(p.assignment, asg)
 
 
+def _mesh3d_long_range(k, extra, seed):
+    """k^3 7-point mesh plus `extra` random long-range couplings (config 3's shape, small)."""
+    rng = np.random.default_rng(seed)
+    n = k ** 3
+    idx = np.arange(n).reshape(k, k, k)
+    r = [idx.ravel()]
+    c = [idx.ravel()]
+    v = [np.full(n, 8.0)]
+    for ax in range(3):
+        a = np.take(idx, range(k - 1), axis=ax).ravel()
+        b = np.take(idx, range(1, k), axis=ax).ravel()
+        w = rng.uniform(0.5, 1.5, a.size)
+        r += [a, b]
+        c += [b, a]
+        v += [-w, -w]
+    a, b = rng.integers(0, n, extra), rng.integers(0, n, extra)
+    keep = a != b
+    w = rng.uniform(0.01, 0.2, int(keep.sum()))
+    r += [a[keep], b[keep]]
+    c += [b[keep], a[keep]]
+    v += [-w, -w]
+    r, c, v = np.concatenate(r), np.concatenate(c), np.concatenate(v)
+    key = r * n + c
+    _, first = np.unique(key, return_index=True)  # drop duplicate long-range pairs
+    return hp.SparseMatrix.from_triplets(r[first], c[first], v[first], n)
+
+
+@pytest.mark.parametrize("T", [2, 3, 7, 16])
+def test_parallel_refinement_sweep_matches_reference(ref, monkeypatch, T):
+    """The exact parallel refinement sweep (T node ranges, speculative phase +
+    in-order resolution, partition.cpp host code) against the reference on
+    graphs where block sizes hit the cap (tolerance 0 and 0.1), uniform-weight
+    ties (Laplacian), random couplings across ranges and w <= 0 edges."""
+    monkeypatch.setenv("HPBJ_REFINE_T", str(T))
+    cases = [(fx.laplacian_2d(40, 40), 25, 0.0), (fx.laplacian_2d(40, 40), 25, 0.1),
+             (fx.random_dd(400, 3, 9), 20, 0.1), (_mesh3d_long_range(14, 30, 4), 40, 0.0),
+             (_mesh3d_long_range(14, 30, 4), 11, 0.1)]
+    for a, s, tol in cases:
+        p = hp.partition_graph(a, s, tol)
+        asg, _, _, _ = ref.partition(a.row_starts, a.col_indices, a.values, s, tol)
+        assert np.array_equal(p.assignment, asg), (a.n, s, tol)
+    test_explicit_graph_with_nonpositive_weights_matches_reference(ref, 2)
+
+
 def test_unsymmetric_pattern_with_hub_matches_reference(ref):
     # one-sided couplings (structurally unsymmetric) + a dense hub row
     rng = np.random.default_rng(5)
