@@ -232,6 +232,7 @@ struct hpbj_ctx {
     int* d_ent_count_rows = nullptr;
     unsigned long long* d_spk_totals = nullptr;
     uint16_t* d_rmeta = nullptr;
+    uint16_t* d_rowcnt = nullptr;  // count pass -> pack pass: off-panel nonzeros per panel row (L, U)
     int spk_rows = 0;            // off-panel layout: 0 row-sorted runs, 1 row quads (spk.cu)
     int spk_rows_env = -1;       // HPBJ_SPK_ROWS=0|1 (read once at context creation)
     int apply_pf = 1;            // HPBJ_APPLY_PF=0: no L2 bulk prefetch in the standalone apply
@@ -316,6 +317,7 @@ struct hpbj_ctx {
         dfree(d_ent_count_rows);
         dfree(d_spk_totals);
         dfree(d_rmeta);
+        dfree(d_rowcnt);
         has_pc = false;
         dfree(d_ilu_lu);
         dfree(d_ilu_dpos);
@@ -469,6 +471,9 @@ void build_spk(hpbj_ctx* c) {
     p.ent_count_rows = c->d_ent_count_rows;
     p.totals = c->d_spk_totals;
     p.ent_off = c->d_ent_off;
+    p.rowcnt = c->d_rowcnt;
+    p.dtile = c->d_dtile;
+    p.dmax = c->dmax;
     launch_spk_count(p, st, &c->launches);
     // Off-panel layout: row quads (fold_rows: one coalesced quad per row and
     // slot, ~3x fewer fold instructions than the segmented fold) for blocks
@@ -1275,6 +1280,7 @@ int hpbj_bj_setup(hpbj_ctx* ctx, int64_t s, const int64_t* perm, const int64_t* 
         dslot(ctx->d_ent_count_rows, np);
         dslot(ctx->d_spk_totals, 2);
         dslot(ctx->d_rmeta, (size_t)np * 64);
+        dslot(ctx->d_rowcnt, (size_t)np * 64);
         dslot(ctx->d_ent_off, np + 1);
         dslot(ctx->d_scan_tmp, 16384);
         dslot(ctx->d_desc, np);

@@ -104,6 +104,8 @@ struct SpkBuild {
     int* ent_count_rows;    // pass 1 output: entries of the row-quad layout
     unsigned long long* totals;  // pass 1 output: [0] entries row-sorted, [1] row-quad
     uint16_t* rmeta;        // row-quad layout: per panel part, 32 x (row | quads << 5) in rank order
+    int dmax;
+    uint16_t* rowcnt;       // pass 1 output: [panel][2][32] off-panel nonzeros of each row (L part, U part)
 };
 
 // Tile quads of row l (q = 0..7 cover columns 4q..4q+3, qd = l / 4): q < qd

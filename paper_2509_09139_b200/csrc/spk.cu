@@ -36,6 +36,8 @@ namespace {
 using namespace spk;
 
 constexpr int kWarpsPerCta = 4;
+// pack pass, per warp: the slot starts of the longest row-quad part
+__host__ __device__ inline int pack_slot_ints(int dmax) { return ((dmax + 3) / 4 + 4) & ~3; }
 
 __device__ __forceinline__ int warp_excl_scan(int v, int lane) {
     int x = v;
@@ -82,21 +84,29 @@ __device__ void pack_row_quads(const SpkBuild& p, const float* F, int dq, int k,
     __syncwarp();
     int cnt = 0;
     IdxT* eidx = reinterpret_cast<IdxT*>(p.eidx);
-    if (live)
-        for (int qi = lo >> 2; qi < (hi + 3) >> 2; ++qi) {
-            const float4 v4 = dense_quad(F, dq, k, qi);
-            const float fv[4] = {v4.x, v4.y, v4.z, v4.w};
+    if (live) {
+        const int qe = (hi + 3) >> 2;
+        for (int q0 = lo >> 2; q0 < qe; q0 += 4) {
+            float4 v4[4];  // four quads in flight per lane
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int c = 4 * qi + u;
-                if (fv[u] != 0.0f && c >= lo && c < hi) {
-                    const int e = base + 4 * (S[cnt >> 2] + rank) + (cnt & 3);
-                    p.eval[e] = fv[u];
-                    eidx[e] = (IdxT)c;
-                    ++cnt;
+            for (int g = 0; g < 4; ++g)
+                v4[g] = q0 + g < qe ? dense_quad(F, dq, k, q0 + g) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+                const float fv[4] = {v4[g].x, v4[g].y, v4[g].z, v4[g].w};
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int c = 4 * (q0 + g) + u;
+                    if (fv[u] != 0.0f && c >= lo && c < hi) {
+                        const int e = base + 4 * (S[cnt >> 2] + rank) + (cnt & 3);
+                        p.eval[e] = fv[u];
+                        eidx[e] = (IdxT)c;
+                        ++cnt;
+                    }
                 }
             }
         }
+    }
     for (; cnt & 3; ++cnt) {  // zero padding of the last quad
         const int e = base + 4 * (S[cnt >> 2] + rank) + (cnt & 3);
         p.eval[e] = 0.0f;
@@ -105,9 +115,107 @@ __device__ void pack_row_quads(const SpkBuild& p, const float* F, int dq, int k,
     __syncwarp();
 }
 
-// Pass 1 (count) / pass 2 (pack); warp per panel, lane = panel row.
-template <bool PACK, class IdxT, bool ROWS = false>
-__global__ void __launch_bounds__(PACK ? 128 : 256, PACK ? 3 : 1) k_spk_build(SpkBuild p) {
+// Pass 3 for one panel: inverse of the 32x32 diagonal triangle.
+__device__ __forceinline__ void spk_tile(const SpkBuild& p, const float* F, int dq, int k, int d, int c0, int c1, int P,
+                                         bool last, int lane, double* inv_smem) {
+    // Inverse of the 32x32 diagonal triangle, in FP64 from the FP32
+    // factors: Linv (unit lower) and Uinv (upper incl. diagonal), written
+    // as 9 float4 quads per row (see kernels.cuh SpkView::dtile). The
+    // block's last panel stores the product Uinv Linv instead (8 quads):
+    // its forward and backward in-panel solves are back to back (no U
+    // entries right of it), so the apply does them as one mat-vec.
+    {
+        // tile (FP32 factor values, exact in FP64) and a transpose buffer
+        // in shared memory; the column of the inverse a lane computes
+        // stays in registers (fully unrolled substitutions)
+        float* Tt = reinterpret_cast<float*>(inv_smem) + (size_t)(threadIdx.x >> 5) * (2 * 32 * 33);
+        float* W = Tt + 32 * 33;
+        for (int q = 0; q < 8; ++q) {
+            const float4 v4 = (k < d && c0 + 4 * q < c1) ? dense_quad(F, dq, k, (c0 >> 2) + q)
+                                                         : make_float4(0.f, 0.f, 0.f, 0.f);
+            const float fv[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int c = 4 * q + u;
+                // padded rows/columns: identity
+                Tt[lane * 33 + c] = (k < d && c0 + c < c1) ? fv[u] : ((c == lane) ? 1.0f : 0.0f);
+            }
+        }
+        __syncwarp();
+        // lane = column c of the inverses
+        const int c = lane;
+        double x[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {  // L x = e_c, unit lower
+            double sum = (i == c) ? 1.0 : 0.0;
+#pragma unroll
+            for (int j = 0; j < i; ++j) sum -= (double)Tt[i * 33 + j] * x[j];
+            x[i] = (i < c) ? 0.0 : sum;
+        }
+        float4* tile = reinterpret_cast<float4*>(p.dtile + (size_t)P * kTileFloats);
+        const int qd = lane >> 2;  // the quad holding the diagonal
+        if (!last) {  // quads 0..qd of row `lane`: strictly lower Linv (through the transpose buffer)
+#pragma unroll
+            for (int i = 0; i < 32; ++i) W[i * 33 + c] = (float)x[i];
+            __syncwarp();
+            for (int q = 0; q <= qd; ++q) {
+                float4 v4;
+                float* w4 = &v4.x;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int j = 4 * q + u;
+                    w4[u] = (j < lane) ? W[lane * 33 + j] : 0.0f;
+                }
+                tile[q * 32 + lane] = v4;
+            }
+            __syncwarp();
+        }
+        // U x = e_c (Uinv, upper with diagonal); last panel: U x = Linv e_c
+        // in place (x = Uinv Linv = (L U)^-1 of the diagonal tile)
+#pragma unroll
+        for (int i = 31; i >= 0; --i) {
+            double sum = last ? x[i] : ((i == c) ? 1.0 : 0.0);
+#pragma unroll
+            for (int j = i + 1; j < 32; ++j) sum -= (double)Tt[i * 33 + j] * x[j];
+            x[i] = (!last && i > c) ? 0.0 : sum / (double)Tt[i * 33 + i];
+        }
+#pragma unroll
+        for (int i = 0; i < 32; ++i) W[i * 33 + c] = (float)x[i];  // row `lane`: W[lane * 33 + j]
+        __syncwarp();
+        if (last) {  // row `lane` of Uinv Linv
+            for (int q = 0; q < 9; ++q) {
+                float4 v4 = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (q < 8) v4 = make_float4(W[lane * 33 + 4 * q], W[lane * 33 + 4 * q + 1], W[lane * 33 + 4 * q + 2],
+                                            W[lane * 33 + 4 * q + 3]);
+                tile[q * 32 + lane] = v4;
+            }
+        } else {  // quads qd+1..7 and quad 8 (the diagonal quad's part) of row `lane`: upper Uinv
+            for (int q = qd + 1; q < 10; ++q) {
+                const int qq = q == 9 ? qd : q;
+                if (q == 8) continue;
+                float4 v4;
+                float* w4 = &v4.x;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int j = 4 * qq + u;
+                    w4[u] = (j >= lane) ? W[lane * 33 + j] : 0.0f;
+                }
+                tile[(q == 9 ? 8 : q) * 32 + lane] = v4;
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// Pass 1 (count), pass 2 (pack the off-panel entries), pass 3 (invert the
+// diagonal tiles); warp per panel, lane = panel row. The pack pass streams the
+// dense panels (HBM bound: few registers, many warps, four quads in flight per
+// lane); the tile pass holds an FP64 column of the inverse in registers (168)
+// but reads only the 32x32 tiles.
+enum { kSpkCount = 0, kSpkPack = 1, kSpkTile = 2 };
+template <int MODE, class IdxT, bool ROWS = false>
+__global__ void __launch_bounds__(MODE == kSpkTile ? 128 : 256, MODE == kSpkTile ? 3 : 4) k_spk_build(SpkBuild p) {
+    constexpr bool PACK = MODE != kSpkCount;
     extern __shared__ double inv_smem[];
     const int lane = threadIdx.x & 31;
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -121,11 +229,22 @@ __global__ void __launch_bounds__(PACK ? 128 : 256, PACK ? 3 : 1) k_spk_build(Sp
         const float* F = p.dense + p.fac_off[b];
         const int k = 32 * t + lane;
         const int c0 = 32 * t, c1 = min(d, 32 * t + 32);
+        if (MODE == kSpkTile) {
+            spk_tile(p, F, dq, k, d, c0, c1, P, 32 * (t + 1) >= d, lane, inv_smem);
+            continue;
+        }
         int nl = 0, nu = 0;
-        if (k < d) {  // whole quads: c0 and c1 < d are multiples of 4, columns >= d are zero
-            for (int qi = 0; qi < (c0 >> 2); ++qi) nl += nnz4(dense_quad(F, dq, k, qi));
-            if (c1 < d)
-                for (int qi = c1 >> 2; qi < dq; ++qi) nu += nnz4(dense_quad(F, dq, k, qi));
+        if (!PACK) {
+            if (k < d) {  // whole quads: c0 and c1 < d are multiples of 4, columns >= d are zero
+                for (int qi = 0; qi < (c0 >> 2); ++qi) nl += nnz4(dense_quad(F, dq, k, qi));
+                if (c1 < d)
+                    for (int qi = c1 >> 2; qi < dq; ++qi) nu += nnz4(dense_quad(F, dq, k, qi));
+            }
+            p.rowcnt[(size_t)P * 64 + lane] = (uint16_t)nl;
+            p.rowcnt[(size_t)P * 64 + 32 + lane] = (uint16_t)nu;
+        } else {
+            nl = p.rowcnt[(size_t)P * 64 + lane];
+            nu = p.rowcnt[(size_t)P * 64 + 32 + lane];
         }
         const int el = warp_excl_scan(nl, lane), eu = warp_excl_scan(nu, lane);
         const int tl = __shfl_sync(0xffffffffu, el + nl, 31);
@@ -167,96 +286,8 @@ __global__ void __launch_bounds__(PACK ? 128 : 256, PACK ? 3 : 1) k_spk_build(Sp
                 reinterpret_cast<IdxT*>(p.eidx)[base + pl + tu + lane - 4] = (IdxT)0;
             }
         }
-        // Inverse of the 32x32 diagonal triangle, in FP64 from the FP32
-        // factors: Linv (unit lower) and Uinv (upper incl. diagonal), written
-        // as 9 float4 quads per row (see kernels.cuh SpkView::dtile). The
-        // block's last panel stores the product Uinv Linv instead (8 quads):
-        // its forward and backward in-panel solves are back to back (no U
-        // entries right of it), so the apply does them as one mat-vec.
-        const bool last = 32 * (t + 1) >= d;
-        {
-            // tile (FP32 factor values, exact in FP64) and a transpose buffer
-            // in shared memory; the column of the inverse a lane computes
-            // stays in registers (fully unrolled substitutions)
-            float* Tt = reinterpret_cast<float*>(inv_smem) + (size_t)(threadIdx.x >> 5) * (2 * 32 * 33);
-            float* W = Tt + 32 * 33;
-            for (int q = 0; q < 8; ++q) {
-                const float4 v4 = (k < d && c0 + 4 * q < c1) ? dense_quad(F, dq, k, (c0 >> 2) + q)
-                                                             : make_float4(0.f, 0.f, 0.f, 0.f);
-                const float fv[4] = {v4.x, v4.y, v4.z, v4.w};
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int c = 4 * q + u;
-                    // padded rows/columns: identity
-                    Tt[lane * 33 + c] = (k < d && c0 + c < c1) ? fv[u] : ((c == lane) ? 1.0f : 0.0f);
-                }
-            }
-            __syncwarp();
-            // lane = column c of the inverses
-            const int c = lane;
-            double x[32];
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {  // L x = e_c, unit lower
-                double sum = (i == c) ? 1.0 : 0.0;
-#pragma unroll
-                for (int j = 0; j < i; ++j) sum -= (double)Tt[i * 33 + j] * x[j];
-                x[i] = (i < c) ? 0.0 : sum;
-            }
-            float4* tile = reinterpret_cast<float4*>(p.dtile + (size_t)P * kTileFloats);
-            const int qd = lane >> 2;  // the quad holding the diagonal
-            if (!last) {  // quads 0..qd of row `lane`: strictly lower Linv (through the transpose buffer)
-#pragma unroll
-                for (int i = 0; i < 32; ++i) W[i * 33 + c] = (float)x[i];
-                __syncwarp();
-                for (int q = 0; q <= qd; ++q) {
-                    float4 v4;
-                    float* w4 = &v4.x;
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const int j = 4 * q + u;
-                        w4[u] = (j < lane) ? W[lane * 33 + j] : 0.0f;
-                    }
-                    tile[q * 32 + lane] = v4;
-                }
-                __syncwarp();
-            }
-            // U x = e_c (Uinv, upper with diagonal); last panel: U x = Linv e_c
-            // in place (x = Uinv Linv = (L U)^-1 of the diagonal tile)
-#pragma unroll
-            for (int i = 31; i >= 0; --i) {
-                double sum = last ? x[i] : ((i == c) ? 1.0 : 0.0);
-#pragma unroll
-                for (int j = i + 1; j < 32; ++j) sum -= (double)Tt[i * 33 + j] * x[j];
-                x[i] = (!last && i > c) ? 0.0 : sum / (double)Tt[i * 33 + i];
-            }
-#pragma unroll
-            for (int i = 0; i < 32; ++i) W[i * 33 + c] = (float)x[i];  // row `lane`: W[lane * 33 + j]
-            __syncwarp();
-            if (last) {  // row `lane` of Uinv Linv
-                for (int q = 0; q < 9; ++q) {
-                    float4 v4 = make_float4(0.f, 0.f, 0.f, 0.f);
-                    if (q < 8) v4 = make_float4(W[lane * 33 + 4 * q], W[lane * 33 + 4 * q + 1], W[lane * 33 + 4 * q + 2],
-                                                W[lane * 33 + 4 * q + 3]);
-                    tile[q * 32 + lane] = v4;
-                }
-            } else {  // quads qd+1..7 and quad 8 (the diagonal quad's part) of row `lane`: upper Uinv
-                for (int q = qd + 1; q < 10; ++q) {
-                    const int qq = q == 9 ? qd : q;
-                    if (q == 8) continue;
-                    float4 v4;
-                    float* w4 = &v4.x;
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const int j = 4 * qq + u;
-                        w4[u] = (j >= lane) ? W[lane * 33 + j] : 0.0f;
-                    }
-                    tile[(q == 9 ? 8 : q) * 32 + lane] = v4;
-                }
-            }
-            __syncwarp();
-        }
         if (ROWS) {
-            int* S = reinterpret_cast<int*>(inv_smem) + (size_t)(threadIdx.x >> 5) * (2 * 32 * 33);
+            int* S = reinterpret_cast<int*>(inv_smem) + (size_t)(threadIdx.x >> 5) * pack_slot_ints(p.dmax);
             pack_row_quads<IdxT>(p, F, dq, k, k < d, 0, c0, ql, rl, mql, base, S, lane);
             pack_row_quads<IdxT>(p, F, dq, k, k < d, c1, d, qu, ru, mqu, base + 4 * sl, S, lane);
             continue;
@@ -349,18 +380,23 @@ void launch_spk_count(const SpkBuild& p, cudaStream_t st, int64_t* launches) {
     k_panel_owner<<<std::max(1, std::min((p.s + 255) / 256, 1184)), 256, 0, st>>>(p.pstart, p.s, p.panel_block);
     const int grid = std::max(1, std::min((p.num_panels * 32 + 255) / 256, 148 * 16));
     HPBJ_CUDA(cudaMemsetAsync(p.totals, 0, 2 * sizeof(unsigned long long), st));
-    k_spk_build<false, uint16_t><<<grid, 256, 0, st>>>(p);
-    *launches += 2;
+    k_spk_build<kSpkCount, uint16_t><<<grid, 256, 0, st>>>(p);
+    // the tiles depend on the panel owners only
+    const int tgrid = std::max(1, std::min((p.num_panels * 32 + 127) / 128, 148 * 16));
+    const int tsmem = 4 * 2 * 32 * 33 * sizeof(float);
+    HPBJ_CUDA(cudaFuncSetAttribute(k_spk_build<kSpkTile, uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, tsmem));
+    k_spk_build<kSpkTile, uint16_t><<<tgrid, 128, tsmem, st>>>(p);
+    *launches += 3;
     HPBJ_CUDA(cudaGetLastError());
 }
 
 void launch_spk_pack(const SpkBuild& p, cudaStream_t st, int64_t* launches) {
-    const int grid = std::max(1, std::min((p.num_panels * 32 + 127) / 128, 148 * 16));
-    const int smem = 4 * 2 * 32 * 33 * sizeof(float);
-    auto fn = p.rows ? (p.idx32 ? k_spk_build<true, uint32_t, true> : k_spk_build<true, uint16_t, true>)
-                     : (p.idx32 ? k_spk_build<true, uint32_t> : k_spk_build<true, uint16_t>);
-    HPBJ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    fn<<<grid, 128, smem, st>>>(p);
+    const int grid = std::max(1, std::min((p.num_panels * 32 + 255) / 256, 148 * 16));
+    const int smem = 8 * pack_slot_ints(p.dmax) * sizeof(int);
+    auto fn = p.rows ? (p.idx32 ? k_spk_build<kSpkPack, uint32_t, true> : k_spk_build<kSpkPack, uint16_t, true>)
+                     : (p.idx32 ? k_spk_build<kSpkPack, uint32_t> : k_spk_build<kSpkPack, uint16_t>);
+    if (smem > 48 * 1024) HPBJ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    fn<<<grid, 256, smem, st>>>(p);
     *launches += 1;
     HPBJ_CUDA(cudaGetLastError());
 }
