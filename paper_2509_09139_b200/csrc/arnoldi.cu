@@ -50,6 +50,7 @@ using sync::grid_barrier;
 using sync::transpose_reduce;
 
 constexpr int kMgsThreads = 1024;
+constexpr int kMgsPre = 4;  // double2 per thread of the next vector in flight across a grid barrier
 constexpr int kIcwyThreads = 1024;
 constexpr size_t kSmemMax = 227 * 1024;
 
@@ -210,6 +211,18 @@ __global__ void __launch_bounds__(kMgsThreads, 1) k_mgs(OrthArgs a) {
         __syncthreads();
     };
 
+    // The first kMgsPre loads of every pass's HBM vector are issued before
+    // the previous pass's grid barrier, so they land while the CTA waits.
+    double2 pre[kMgsPre];
+    auto preload = [&](int i) {
+        const double2* vi = reinterpret_cast<const double2*>(V + (size_t)i * ldv + r0);
+#pragma unroll
+        for (int g = 0; g < kMgsPre; ++g) {
+            const int e = tid + g * kMgsThreads;
+            pre[g] = e < nv2 ? __ldg(vi + e) : make_double2(0.0, 0.0);
+        }
+    };
+
     // pass 0: stage w on chip, ||w||^2 and <v_0, w>
     double ss = 0.0, dt = 0.0;
     {
@@ -225,6 +238,7 @@ __global__ void __launch_bounds__(kMgsThreads, 1) k_mgs(OrthArgs a) {
             dt = fma(vv.y, wv.y, dt);
         }
     }
+    if (j >= 1) preload(1);
     reduce2(ss, dt, 0);
     const double pre_norm = sqrt(bc[0]);
     double h = bc[1];
@@ -235,8 +249,22 @@ __global__ void __launch_bounds__(kMgsThreads, 1) k_mgs(OrthArgs a) {
         const double2* vp = reinterpret_cast<const double2*>(V + (size_t)(i - 1) * ldv + r0);
         const double2* vi = reinterpret_cast<const double2*>(V + (size_t)i * ldv + r0);
         dt = 0.0;
+#pragma unroll
+        for (int g = 0; g < kMgsPre; ++g) {
+            const int e = tid + g * kMgsThreads;
+            if (e < nv2) {
+                double2 wv = w2[e];
+                const double2 pv = __ldg(vp + e);
+                const double2 qv = pre[g];
+                wv.x = fma(-h, pv.x, wv.x);
+                wv.y = fma(-h, pv.y, wv.y);
+                w2[e] = wv;
+                dt = fma(qv.x, wv.x, dt);
+                dt = fma(qv.y, wv.y, dt);
+            }
+        }
 #pragma unroll 4
-        for (int e = tid; e < nv2; e += kMgsThreads) {
+        for (int e = tid + kMgsPre * kMgsThreads; e < nv2; e += kMgsThreads) {
             double2 wv = w2[e];
             const double2 pv = __ldg(vp + e);
             const double2 qv = __ldg(vi + e);
@@ -246,6 +274,7 @@ __global__ void __launch_bounds__(kMgsThreads, 1) k_mgs(OrthArgs a) {
             dt = fma(qv.x, wv.x, dt);
             dt = fma(qv.y, wv.y, dt);
         }
+        if (i + 1 <= j) preload(i + 1);
         reduce2(0.0, dt, i & 1);
         h = bc[1];
         if (blockIdx.x == 0 && tid == 0) a.kb.H[(size_t)j * (m + 1) + i] = h;

@@ -937,6 +937,11 @@ __global__ void __launch_bounds__(NT, 2) k_block_lu_blk(LuParams p, int dlo, int
 // column order, that the right-looking kernels apply (left- and right-looking
 // only reorder independent chains), the divisions and the pivot rule are the
 // same: factors and pivots are bit-identical to k_block_lu_blk / k_block_lu.
+template <int N>
+struct IntC {
+    static constexpr int value = N;
+};
+
 constexpr int kLlMax = 288;
 constexpr int kLlThreads = 256;
 constexpr int kLlCtasPerSm = 2;
@@ -1258,103 +1263,115 @@ __global__ void __launch_bounds__(kLlThreads, kLlCtasPerSm) k_block_lu_ll(LuPara
                         rv[i][4 * q + 3] = t4.w;
                     }
                 }
+                // The window shrinks by 8 every 8 columns (W = 32, 24, 16, 8):
+                // column c + j for j >= W is past the panel, so the rank-1
+                // update and the candidate copy only cover W columns (the
+                // same fmaf chain per element as a constant 32-wide window,
+                // 39% fewer update instructions)
+                auto run_cols = [&](auto Wc, int cb, int ce) -> bool {
+                    constexpr int W = decltype(Wc)::value;
 #pragma unroll 1
-                for (int c = 0; c < kw; ++c) {
-                    const int k = c0 + c;
-                    // thread candidate, then warp candidate: max |x|, ties -> smaller row
-                    unsigned key = 0u;
-                    int brow = 0x7fffffff, bi = 0;
+                        for (int c = cb; c < ce; ++c) {
+                        const int k = c0 + c;
+                        // thread candidate, then warp candidate: max |x|, ties -> smaller row
+                        unsigned key = 0u;
+                        int brow = 0x7fffffff, bi = 0;
 #pragma unroll
-                    for (int i = 0; i < RPT; ++i) {
-                        const unsigned ki = fl[i] ? 0u : __float_as_uint(fabsf(rv[i][0])) + 1u;
-                        if (ki > key || (ki == key && ki != 0u && myrow[i] < brow)) {
-                            key = ki;
-                            brow = myrow[i];
-                            bi = i;
+                        for (int i = 0; i < RPT; ++i) {
+                            const unsigned ki = fl[i] ? 0u : __float_as_uint(fabsf(rv[i][0])) + 1u;
+                            if (ki > key || (ki == key && ki != 0u && myrow[i] < brow)) {
+                                key = ki;
+                                brow = myrow[i];
+                                bi = i;
+                            }
                         }
-                    }
-                    unsigned kmx;
-                    const int wr = warp_pivot_row(key, key ? brow : 0x7fffffff, &kmx);
-                    const unsigned own = __ballot_sync(0xffffffffu, key != 0u && key == kmx && brow == wr);
-                    float* cv = cand_v + (size_t)(buf * NW + wid) * 32;
-                    int* ci4 = cand_i + (buf * NW + wid) * 4;
-                    if (own && lane == __ffs(own) - 1) {
+                        unsigned kmx;
+                        const int wr = warp_pivot_row(key, key ? brow : 0x7fffffff, &kmx);
+                        const unsigned own = __ballot_sync(0xffffffffu, key != 0u && key == kmx && brow == wr);
+                        float* cv = cand_v + (size_t)(buf * NW + wid) * 32;
+                        int* ci4 = cand_i + (buf * NW + wid) * 4;
+                        if (own && lane == __ffs(own) - 1) {
 #pragma unroll
-                        for (int i = 0; i < RPT; ++i)
-                            if (i == bi)
+                            for (int i = 0; i < RPT; ++i)
+                                if (i == bi)
 #pragma unroll
-                                for (int q = 0; q < 8; ++q)
-                                    reinterpret_cast<float4*>(cv)[q] = make_float4(rv[i][4 * q], rv[i][4 * q + 1],
-                                                                                   rv[i][4 * q + 2], rv[i][4 * q + 3]);
-                        reinterpret_cast<int4*>(ci4)[0] = make_int4((int)kmx, wr, tid + NT * bi, 0);
-                    } else if (lane == 0 && !own) {
-                        reinterpret_cast<int4*>(ci4)[0] = make_int4(0, 0x7fffffff, -1, 0);
-                    }
-                    bar_named(1, nwa * 32);
-                    // winner over the active warps' candidates (warp-wide, identical in every warp)
-                    const int4 cw = lane < nwa ? reinterpret_cast<const int4*>(cand_i + buf * NW * 4)[lane]
-                                               : make_int4(0, 0x7fffffff, -1, 0);
-                    unsigned kk;
-                    const int frow =
-                        warp_pivot_row((unsigned)cw.x, lane < nwa && cw.x != 0 ? cw.y : 0x7fffffff, &kk);
-                    const int fw =
-                        __ffs(__ballot_sync(0xffffffffu, lane < nwa && (unsigned)cw.x == kk && cw.y == frow)) - 1;
-                    const int owner = __shfl_sync(0xffffffffu, cw.z, fw);  // tid + NT * row slot
-                    const float4* Pv4 = reinterpret_cast<const float4*>(cand_v + (size_t)(buf * NW + fw) * 32);
-                    buf ^= 1;
-                    // regularize_pivot (lu.cpp:10-20), identical in every thread;
-                    // FP32 brackets, FP64 only near the threshold or to regularise
-                    const float praw = Pv4[0].x;
-                    float pv = praw;
-                    if (!pivot_keep_f(praw, kbr, norm, p.eps)) {
-                        const double pvd = (double)praw;
-                        const double val = (pvd < 0.0 ? -1.0 : 1.0) * p.eps * norm;
-                        if (val == 0.0) {
+                                    for (int q = 0; q < W / 4; ++q)
+                                        reinterpret_cast<float4*>(cv)[q] = make_float4(rv[i][4 * q], rv[i][4 * q + 1],
+                                                                                       rv[i][4 * q + 2], rv[i][4 * q + 3]);
+                            reinterpret_cast<int4*>(ci4)[0] = make_int4((int)kmx, wr, tid + NT * bi, 0);
+                        } else if (lane == 0 && !own) {
+                            reinterpret_cast<int4*>(ci4)[0] = make_int4(0, 0x7fffffff, -1, 0);
+                        }
+                        bar_named(1, nwa * 32);
+                        // winner over the active warps' candidates (warp-wide, identical in every warp)
+                        const int4 cw = lane < nwa ? reinterpret_cast<const int4*>(cand_i + buf * NW * 4)[lane]
+                                                   : make_int4(0, 0x7fffffff, -1, 0);
+                        unsigned kk;
+                        const int frow =
+                            warp_pivot_row((unsigned)cw.x, lane < nwa && cw.x != 0 ? cw.y : 0x7fffffff, &kk);
+                        const int fw =
+                            __ffs(__ballot_sync(0xffffffffu, lane < nwa && (unsigned)cw.x == kk && cw.y == frow)) - 1;
+                        const int owner = __shfl_sync(0xffffffffu, cw.z, fw);  // tid + NT * row slot
+                        const float4* Pv4 = reinterpret_cast<const float4*>(cand_v + (size_t)(buf * NW + fw) * 32);
+                        buf ^= 1;
+                        // regularize_pivot (lu.cpp:10-20), identical in every thread;
+                        // FP32 brackets, FP64 only near the threshold or to regularise
+                        const float praw = Pv4[0].x;
+                        float pv = praw;
+                        if (!pivot_keep_f(praw, kbr, norm, p.eps)) {
+                            const double pvd = (double)praw;
+                            const double val = (pvd < 0.0 ? -1.0 : 1.0) * p.eps * norm;
+                            if (val == 0.0) {
+                                if (tid == 0) atomicMin(p.singular, ((unsigned long long)b << 32) | (unsigned)k);
+                                return true;
+                            }
+                            ++nperturb;
+                            if (tid == 0) {
+                                const int slot = atomicAdd(p.pert_n, 1);
+                                if (slot < p.pert_cap) p.pert[slot] = PertRecord{b, k, pvd, val};
+                            }
+                            pv = (float)val;
+                        } else if (praw == 0.0f) {  // kept zero pivot (eps = 0)
                             if (tid == 0) atomicMin(p.singular, ((unsigned long long)b << 32) | (unsigned)k);
-                            abort = true;
-                            break;
+                            return true;
                         }
-                        ++nperturb;
-                        if (tid == 0) {
-                            const int slot = atomicAdd(p.pert_n, 1);
-                            if (slot < p.pert_cap) p.pert[slot] = PertRecord{b, k, pvd, val};
-                        }
-                        pv = (float)val;
-                    } else if (praw == 0.0f) {  // kept zero pivot (eps = 0)
-                        if (tid == 0) atomicMin(p.singular, ((unsigned long long)b << 32) | (unsigned)k);
-                        abort = true;
-                        break;
-                    }
-                    if (wid == 0 && c + lane < 32)  // the pivot row's U row (columns c..31) is final
-                        X[xe(frow, c + lane)] = lane == 0 ? pv : reinterpret_cast<const float*>(Pv4)[lane];
+                        if (wid == 0 && c + lane < 32)  // the pivot row's U row (columns c..31) is final
+                            X[xe(frow, c + lane)] = lane == 0 ? pv : reinterpret_cast<const float*>(Pv4)[lane];
 #pragma unroll
-                    for (int i = 0; i < RPT; ++i) {
-                        if (owner == tid + NT * i) {  // the pivot row (its U row goes to X below)
-                            fl[i] = true;
-                            prow[k] = (short)myrow[i];
-                            ppos[myrow[i]] = (short)k;
-                        } else if (!fl[i]) {
-                            const float l = div_mult(rv[i][0], pv);  // L(i,k) = x_i / pivot (lu.cpp:207)
-                            X[xe(myrow[i], c)] = l;
-                            // the pivot row's window quad by quad from the candidate
-                            // slot (not held in registers: 128 per thread)
-                            {
-                                const float4 w0 = Pv4[0];
-                                rv[i][0] = fmaf(-l, w0.y, rv[i][1]);
-                                rv[i][1] = fmaf(-l, w0.z, rv[i][2]);
-                                rv[i][2] = fmaf(-l, w0.w, rv[i][3]);
-                            }
+                        for (int i = 0; i < RPT; ++i) {
+                            if (owner == tid + NT * i) {  // the pivot row (its U row goes to X below)
+                                fl[i] = true;
+                                prow[k] = (short)myrow[i];
+                                ppos[myrow[i]] = (short)k;
+                            } else if (!fl[i]) {
+                                const float l = div_mult(rv[i][0], pv);  // L(i,k) = x_i / pivot (lu.cpp:207)
+                                X[xe(myrow[i], c)] = l;
+                                // the pivot row's window quad by quad from the candidate
+                                // slot (not held in registers: 128 per thread)
+                                {
+                                    const float4 w0 = Pv4[0];
+                                    rv[i][0] = fmaf(-l, w0.y, rv[i][1]);
+                                    rv[i][1] = fmaf(-l, w0.z, rv[i][2]);
+                                    rv[i][2] = fmaf(-l, w0.w, rv[i][3]);
+                                }
 #pragma unroll
-                            for (int q = 1; q < 8; ++q) {
-                                const float4 wq = Pv4[q];
-                                rv[i][4 * q - 1] = fmaf(-l, wq.x, rv[i][4 * q]);
-                                rv[i][4 * q + 0] = fmaf(-l, wq.y, rv[i][4 * q + 1]);
-                                rv[i][4 * q + 1] = fmaf(-l, wq.z, rv[i][4 * q + 2]);
-                                rv[i][4 * q + 2] = fmaf(-l, wq.w, rv[i][4 * q + 3]);
+                                for (int q = 1; q < W / 4; ++q) {
+                                    const float4 wq = Pv4[q];
+                                    rv[i][4 * q - 1] = fmaf(-l, wq.x, rv[i][4 * q]);
+                                    rv[i][4 * q + 0] = fmaf(-l, wq.y, rv[i][4 * q + 1]);
+                                    rv[i][4 * q + 1] = fmaf(-l, wq.z, rv[i][4 * q + 2]);
+                                    rv[i][4 * q + 2] = fmaf(-l, wq.w, rv[i][4 * q + 3]);
+                                }
                             }
                         }
                     }
-                }
+                    return false;
+                };
+                bool ab = run_cols(IntC<32>{}, 0, min(kw, 8));
+                if (!ab && kw > 8) ab = run_cols(IntC<24>{}, 8, min(kw, 16));
+                if (!ab && kw > 16) ab = run_cols(IntC<16>{}, 16, min(kw, 24));
+                if (!ab && kw > 24) ab = run_cols(IntC<8>{}, 24, kw);
+                abort = ab;
             }
             abort = __syncthreads_or(abort);
             if (abort) break;

@@ -1091,9 +1091,11 @@ int hpbj_set_matrix(hpbj_ctx* ctx, int64_t n, const int64_t* row_ptr, const int6
     t_pool = &ctx->pool;
     t_slots = &ctx->slots;
     return guard(&ctx->err, [&] {
+        const auto t0 = std::chrono::steady_clock::now();
         check_csr(n, row_ptr, col, val);
         if (n >= (int64_t)INT32_MAX || row_ptr[n] >= (int64_t)INT32_MAX)
             fail(HPBJ_EINVAL, "hpbj: n and nnz must be < 2^31");
+        const auto t1 = std::chrono::steady_clock::now();
         HPBJ_CUDA(cudaSetDevice(ctx->device));
         ctx->release_matrix();
         ctx->release_ws();
@@ -1115,6 +1117,7 @@ int hpbj_set_matrix(hpbj_ctx* ctx, int64_t n, const int64_t* row_ptr, const int6
 #pragma omp for schedule(static)
             for (int64_t k = 0; k < nnz; ++k) vs[k] = val[k];
         }
+        const auto t2 = std::chrono::steady_clock::now();
         ctx->A.n = ni;
         ctx->A.nnz = nnz;
         dslot(ctx->A.rp, ni + 1);
@@ -1125,11 +1128,17 @@ int hpbj_set_matrix(hpbj_ctx* ctx, int64_t n, const int64_t* row_ptr, const int6
         HPBJ_CUDA(cudaMemcpyAsync(ctx->A.ci, ci, b_ci, cudaMemcpyHostToDevice, st));
         HPBJ_CUDA(cudaMemcpyAsync(ctx->A.val, vs, sizeof(double) * (size_t)nnz, cudaMemcpyHostToDevice, st));
         ctx->stage_mat.fence(st);  // later work on the stream is ordered after the copies
+        const auto t3 = std::chrono::steady_clock::now();
         ctx->h_rp.assign(row_ptr, row_ptr + n + 1);
         make_plan(ctx->planA, ctx->h_rp, nullptr, ni);
         dslot(ctx->d_tmpx, ni);
         dslot(ctx->d_tmpy, ni);
         ctx->has_matrix = true;
+        if (getenv("HPBJ_DEBUG")) {
+            auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+            fprintf(stderr, "[hpbj] set_matrix: check %.1f stage %.1f alloc+enqueue %.1f plan %.1f ms\n", ms(t0, t1),
+                    ms(t1, t2), ms(t2, t3), ms(t3, std::chrono::steady_clock::now()));
+        }
     });
 }
 
