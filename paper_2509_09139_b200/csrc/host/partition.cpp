@@ -39,6 +39,9 @@
 #include <string>
 #include <utility>
 #include <vector>
+#include <exception>
+#include <functional>
+#include <thread>
 
 #include <omp.h>
 #include <sys/mman.h>
@@ -284,6 +287,9 @@ struct PartWork {
     // refinement (parallel sweep)
     HBuf<uint8_t> spec;  // S per node
     HBuf<uint8_t> fl;
+    // region growing
+    HBuf<int32_t> aorder;
+    HBuf<uint32_t> ell;
 };
 thread_local PartWork t_work;
 
@@ -560,8 +566,170 @@ double cross_range_fraction(const GraphView<Idx, Off>& g, int T) {
     return cnt ? (double)hit / cnt : 0.0;
 }
 
+// Fixed-stride neighbour records for region growing: 8 ids per node, the
+// degree in the top 4 bits of the first (15: longer row, read elsewhere).
+template <class DegFn, class NbrFn>
+void build_ell(int64_t n, uint32_t* ell, DegFn deg, NbrFn nbr) {
+#pragma omp parallel for schedule(static, 4096)
+    for (int64_t u = 0; u < n; ++u) {
+        uint32_t* e = ell + (size_t)u * 8;
+        const int64_t d = deg(u);
+        if (d > 8) {
+            e[0] = 0xFu << 28;
+            continue;
+        }
+        for (int i = 0; i < 8; ++i) e[i] = i < d ? nbr(u, i) : 0u;
+        e[0] |= (uint32_t)d << 28;
+    }
+}
+
+struct GrowOpts {
+    int ahead = 16;     // prefetch distance (popped nodes), fixed-stride records
+    int ahead_csr = 6;  // the same with st + nb (two dependent lines per node)
+    bool defer = true;   // block ids written after growing (assignment-order list)
+    int ell = -1;        // fixed-stride neighbour records (-1: for n >= 2^21)
+    bool pf = true;
+    int loc = 3;
+};
+inline GrowOpts grow_opts() {
+    GrowOpts o;
+    if (const char* e = getenv("HPBJ_GROW_PF")) o.ahead = o.ahead_csr = atoi(e);
+    if (const char* e = getenv("HPBJ_GROW_DEFER")) o.defer = atoi(e) != 0;
+    if (const char* e = getenv("HPBJ_GROW_ELL")) o.ell = atoi(e);
+    if (const char* e = getenv("HPBJ_GROW_LOC")) o.loc = atoi(e);
+    return o;
+}
+
+// Region growing (partition.cpp:74-103). The free/taken test reads a bitmap
+// (n bits: cache-resident) instead of the state array. Returns the connected
+// nodes left unassigned.
+template <bool ELL, class Idx, class Off, class S>
+int64_t grow_blocks(const GraphView<Idx, Off>& g, const uint32_t* ell, const int32_t* order, int64_t connected,
+                    int64_t s, int64_t cap, int64_t* sizes, uint64_t* taken, int32_t* queue, S* state,
+                    const GrowOpts& go, HBuf<int32_t>& aorder_buf, const int64_t* raw_rp = nullptr,
+                    const int64_t* raw_ci = nullptr) {
+    const int64_t n = g.n;
+    const Off* st = g.st;
+    const Idx* nb = g.idx;
+    const int K = ELL ? go.ahead : go.ahead_csr;
+    const bool pf = go.pf && n > (1 << 18) && K > 0;
+    int32_t* ao = nullptr;
+    if (go.defer) {
+        fit(aorder_buf, connected + 1);
+        ao = aorder_buf.data();
+    }
+    int64_t fill = 0;
+    int64_t cursor = 0;
+    int64_t connected_left = connected;
+    auto push_csr = [&](int32_t u, int64_t& tail) {
+        for (Off k = st[u]; k < st[u + 1]; ++k) {  // branch-free push of the free neighbours
+            const int32_t v = (int32_t)nb[k];
+            uint64_t& word = taken[v >> 6];
+            const uint64_t bit = 1ull << (v & 63);
+            queue[tail] = v;
+            tail += (word & bit) == 0;
+            word |= bit;
+        }
+    };
+    int64_t b = 0;
+    for (; b < s && connected_left > 0; ++b) {
+        const int64_t blocks_left = s - b;
+        int64_t target = (connected_left + blocks_left - 1) / blocks_left;
+        target = std::min(target, cap);
+        int64_t head = 0, tail = 0;
+        int64_t grown = 0;
+        const S bb = (S)b;
+        while (grown < target) {
+            if (head == tail) {  // queue empty: every taken node is assigned
+                while (cursor < connected && ((taken[order[cursor] >> 6] >> (order[cursor] & 63)) & 1ull)) ++cursor;
+                if (cursor == connected) break;
+                const int32_t sd = order[cursor];
+                queue[tail++] = sd;
+                taken[sd >> 6] |= 1ull << (sd & 63);
+            }
+            if constexpr (ELL) {
+                if (pf && head + K < tail) {
+                    const uint32_t* a = ell + (size_t)queue[head + K] * 8;
+                    switch (go.loc) {
+                        case 0: __builtin_prefetch(a, 0, 0); break;
+                        case 1: __builtin_prefetch(a, 0, 1); break;
+                        case 2: __builtin_prefetch(a, 0, 2); break;
+                        default: __builtin_prefetch(a, 0, 3); break;
+                    }
+                }
+            } else {
+                if (pf && head + 2 * K < tail) __builtin_prefetch(st + queue[head + 2 * K], 0, 1);
+                if (pf && head + K < tail) {  // prefetch the adjacency of a node popped soon
+                    const int32_t f = queue[head + K];
+                    __builtin_prefetch(nb + st[f], 0, 1);
+                }
+            }
+            const int32_t u = queue[head++];
+            if (ao) ao[fill++] = u;
+            else state[u] = bb;
+            ++grown;
+            --connected_left;
+            if constexpr (ELL) {
+                const uint32_t* e = ell + (size_t)u * 8;
+                const uint32_t h = e[0];
+                const uint32_t d = h >> 28;
+                if (d <= 8) {
+#pragma GCC unroll 8
+                    for (uint32_t i = 0; i < 8; ++i) {
+                        if (i >= d) break;
+                        const int32_t v = (int32_t)(i == 0 ? (h & 0x0FFFFFFFu) : e[i]);
+                        uint64_t& word = taken[v >> 6];
+                        const uint64_t bit = 1ull << (v & 63);
+                        queue[tail] = v;
+                        tail += (word & bit) == 0;
+                        word |= bit;
+                    }
+                } else if (raw_rp) {  // graph = CSR minus the diagonal, built concurrently: read the CSR
+                    for (int64_t k = raw_rp[u]; k < raw_rp[u + 1]; ++k) {
+                        const int32_t v = (int32_t)raw_ci[k];
+                        if (v == u) continue;
+                        uint64_t& word = taken[v >> 6];
+                        const uint64_t bit = 1ull << (v & 63);
+                        queue[tail] = v;
+                        tail += (word & bit) == 0;
+                        word |= bit;
+                    }
+                } else {
+                    push_csr(u, tail);
+                }
+            } else {
+                push_csr(u, tail);
+            }
+        }
+        sizes[b] = grown;
+        for (int64_t q = head; q < tail; ++q) taken[queue[q] >> 6] &= ~(1ull << (queue[q] & 63));  // queue.clear()
+    }
+    if (ao) {  // block ids from the assignment-order list
+        std::vector<int64_t> off(b + 1, 0);
+        for (int64_t i = 0; i < b; ++i) off[i + 1] = off[i] + sizes[i];
+#pragma omp parallel for schedule(dynamic, 64) if (n > 65536)
+        for (int64_t i = 0; i < b; ++i)
+            for (int64_t k = off[i]; k < off[i + 1]; ++k) state[ao[k]] = (S)i;
+    }
+    return connected_left;
+}
+
+// Region growing overlapped with the graph build: the grow reads prebuilt
+// fixed-stride records of A's off-diagonal pattern (and A itself for rows
+// longer than a record) while `during_grow` computes the weights and the
+// refinement view on the other cores; it returns false when the weighted
+// graph turns out not to be A's pattern (structurally unsymmetric), and the
+// partition is then abandoned (partition_view returns false).
+struct GrowPipeline {
+    const uint32_t* ell = nullptr;
+    const int64_t* rp = nullptr;
+    const int64_t* ci = nullptr;
+    std::function<bool()> during_grow;
+};
+
 template <class Idx, class Off>
-void partition_view(const GraphView<Idx, Off>& g, int64_t s, double tol, int64_t* assignment) {
+bool partition_view(const GraphView<Idx, Off>& g, int64_t s, double tol, int64_t* assignment,
+                    const GrowPipeline* pl = nullptr) {
     const int64_t n = g.n;
     if (s < 1) fail(HPBJ_EINVAL, "partition_graph: s must be >= 1");
     if (s > n) fail(HPBJ_EINVAL, "partition_graph: s exceeds node count");
@@ -647,52 +815,51 @@ void partition_view(const GraphView<Idx, Off>& g, int64_t s, double tol, int64_t
     // outgrow the core's L2 (measured on the B200 host: -7% on config 1's
     // 2.1e5 nodes without it, +20% on config 2's 10^6 random-graph nodes).
     const bool pf = n > (1 << 18);
-    auto run = [&](auto* state) {
+    auto run = [&](auto* state) -> bool {
         using S = std::remove_pointer_t<decltype(state)>;
 #pragma omp parallel for schedule(static) if (n > 65536)
         for (int64_t v = 0; v < n; ++v) state[v] = (S)-1;
         // Region growing (partition.cpp:74-103). The free/taken test reads a
         // bitmap (n bits: cache-resident) instead of the state array; state
         // receives the block id once per node.
-        int64_t cursor = 0;
         int64_t connected_left = connected;
-        constexpr int kAhead = 6;
-        for (int64_t b = 0; b < s && connected_left > 0; ++b) {
-            const int64_t blocks_left = s - b;
-            int64_t target = (connected_left + blocks_left - 1) / blocks_left;
-            target = std::min(target, cap);
-            int64_t head = 0, tail = 0;
-            int64_t grown = 0;
-            const S bb = (S)b;
-            while (grown < target) {
-                if (head == tail) {  // queue empty: every taken node is assigned
-                    while (cursor < connected && ((taken[order[cursor] >> 6] >> (order[cursor] & 63)) & 1ull))
-                        ++cursor;
-                    if (cursor == connected) break;
-                    const int32_t sd = order[cursor];
-                    queue[tail++] = sd;
-                    taken[sd >> 6] |= 1ull << (sd & 63);
+        const GrowOpts go = grow_opts();
+        if (pl) {
+            std::exception_ptr gerr;
+            const GraphView<Idx, Off> gg = g;  // during_grow replaces the caller's view
+            std::thread thr([&] {
+                try {
+                    connected_left = grow_blocks<true>(gg, pl->ell, order, connected, s, cap, sizes, taken, queue,
+                                                       state, go, W.aorder, pl->rp, pl->ci);
+                } catch (...) {
+                    gerr = std::current_exception();
                 }
-                if (pf && head + 2 * kAhead < tail) __builtin_prefetch(st + queue[head + 2 * kAhead], 0, 1);
-                if (pf && head + kAhead < tail) {  // prefetch the adjacency of a node popped soon
-                    const int32_t f = queue[head + kAhead];
-                    __builtin_prefetch(nb + st[f], 0, 1);
-                }
-                const int32_t u = queue[head++];
-                state[u] = bb;
-                ++grown;
-                --connected_left;
-                for (Off k = st[u]; k < st[u + 1]; ++k) {  // branch-free push of the free neighbours
-                    const int32_t v = (int32_t)nb[k];
-                    uint64_t& word = taken[v >> 6];
-                    const uint64_t bit = 1ull << (v & 63);
-                    queue[tail] = v;
-                    tail += (word & bit) == 0;
-                    word |= bit;
-                }
+            });
+            bool ok = false;
+            try {
+                ok = pl->during_grow();
+            } catch (...) {
+                thr.join();
+                throw;
             }
-            sizes[b] = grown;
-            for (int64_t q = head; q < tail; ++q) taken[queue[q] >> 6] &= ~(1ull << (queue[q] & 63));  // queue.clear()
+            thr.join();
+            if (gerr) std::rethrow_exception(gerr);
+            if (!ok) return false;
+        } else if (go.ell != 0 && (go.ell > 0 || n >= (int64_t(1) << 21)) && n < (int64_t(1) << 28)) {
+            // fixed-stride neighbour records (8 ids, degree in the top bits of
+            // the first): one cache line per popped node instead of st + nb
+            const auto t_e0 = std::chrono::steady_clock::now();
+            fit(W.ell, (size_t)n * 8);
+            build_ell(n, W.ell.data(), [&](int64_t u) { return (int64_t)(st[u + 1] - st[u]); },
+                      [&](int64_t u, int i) { return (uint32_t)nb[st[u] + i]; });
+            if (dbg)
+                fprintf(stderr, "[hpbj]   ell build %.1f ms\n",
+                        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_e0).count());
+            connected_left = grow_blocks<true>(g, W.ell.data(), order, connected, s, cap, sizes, taken, queue, state,
+                                               go, W.aorder);
+        } else {
+            connected_left = grow_blocks<false>(g, nullptr, order, connected, s, cap, sizes, taken, queue, state, go,
+                                                W.aorder);
         }
         const bool leftovers = connected < n || connected_left > 0;
         const auto t_grown = std::chrono::steady_clock::now();
@@ -730,14 +897,14 @@ void partition_view(const GraphView<Idx, Off>& g, int64_t s, double tol, int64_t
                     (long long)moves);
 #pragma omp parallel for schedule(static) if (n > 65536)
         for (int64_t v = 0; v < n; ++v) assignment[v] = state[v];
+        return true;
     };
     if (s <= 32767) {
         fit(W.state16, n);
-        run(W.state16.data());
-    } else {
-        fit(W.state, n);
-        run(W.state.data());
+        return run(W.state16.data());
     }
+    fit(W.state, n);
+    return run(W.state.data());
 }
 
 }  // namespace
@@ -760,7 +927,10 @@ void partition_csr(int64_t n, const int64_t* rp, const int64_t* ci, const double
         partition_adjacency(g, s, tol, assignment);
         return;
     }
-    const auto t_w0 = std::chrono::steady_clock::now();
+    const bool dbg = getenv("HPBJ_DEBUG") != nullptr;
+    auto ms_since = [](std::chrono::steady_clock::time_point t) {
+        return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t).count();
+    };
     PartWork& W = t_work;
     fit(W.wk, nnz);
     fit(W.deg, n);
@@ -771,76 +941,146 @@ void partition_csr(int64_t n, const int64_t* rp, const int64_t* ci, const double
     // p < q, the reference's accumulation order (graph.cpp:24-33). The pattern
     // is symmetric iff every upper entry finds its mirror and the upper and
     // lower entry counts agree (the mirrors are then all the lower entries).
-    int missing = 0;
-    int64_t nup = 0, nlo = 0;
-#pragma omp parallel for schedule(dynamic, 2048) reduction(| : missing) reduction(+ : nup, nlo)
-    for (int64_t u = 0; u < n; ++u) {
-        for (int64_t k = rp[u]; k < rp[u + 1]; ++k) {
-            const int64_t j = ci[k];
-            if (j < u) {
-                ++nlo;
-                continue;
-            }
-            if (j == u) {
-                wk[k] = -1.0;
-                continue;
-            }
-            ++nup;
-            const int64_t* b = ci + rp[j];
-            const int64_t* e = ci + rp[j + 1];
-            const int64_t* it = std::lower_bound(b, e, u);
-            if (it == e || *it != u) {
-                missing = 1;
-                continue;
-            }
-            const double wt = 0.5 * (std::fabs(val[k]) + std::fabs(val[it - ci]));
-            wk[k] = wt;
-            wk[it - ci] = wt;
-        }
-    }
-    if (nup != nlo) missing = 1;
-    if (!missing) {
-#pragma omp parallel for schedule(static, 4096)
+    // Returns true when the pattern is symmetric.
+    auto weights = [&](int nthr) -> bool {
+        const auto t_w0 = std::chrono::steady_clock::now();
+        int missing = 0;
+        int64_t nup = 0, nlo = 0;
+#pragma omp parallel for num_threads(nthr) schedule(dynamic, 2048) reduction(| : missing) reduction(+ : nup, nlo)
         for (int64_t u = 0; u < n; ++u) {
+            for (int64_t k = rp[u]; k < rp[u + 1]; ++k) {
+                const int64_t j = ci[k];
+                if (j < u) {
+                    ++nlo;
+                    continue;
+                }
+                if (j == u) {
+                    wk[k] = -1.0;
+                    continue;
+                }
+                ++nup;
+                const int64_t* b = ci + rp[j];
+                const int64_t* e = ci + rp[j + 1];
+                const int64_t* it = std::lower_bound(b, e, u);
+                if (it == e || *it != u) {
+                    missing = 1;
+                    continue;
+                }
+                const double wt = 0.5 * (std::fabs(val[k]) + std::fabs(val[it - ci]));
+                wk[k] = wt;
+                wk[it - ci] = wt;
+            }
+        }
+        if (dbg) fprintf(stderr, "[hpbj]   weights %.1f ms\n", ms_since(t_w0));
+        return !missing && nup == nlo;
+    };
+    // compact int32 adjacency (kept entries only): 4 B/neighbour and 4-byte
+    // offsets for the sequential sweeps instead of 16 B (int64 column +
+    // weight) per CSR entry; deg[] already holds the kept counts
+    auto adjacency = [&](int nthr) -> GraphView<int32_t, int32_t> {
+        const auto t_a0 = std::chrono::steady_clock::now();
+        fit(W.adj_start, n + 1);
+        int32_t* ast = W.adj_start.data();
+        // offsets: chunked parallel prefix over deg
+        const int C = std::max(1, std::min(nthr, 64));
+        std::vector<int64_t> csum(C + 1, 0);
+#pragma omp parallel for num_threads(nthr) schedule(static, 1)
+        for (int c = 0; c < C; ++c) {
+            int64_t t = 0;
+            for (int64_t u = n * c / C; u < n * (c + 1) / C; ++u) t += deg[u];
+            csum[c + 1] = t;
+        }
+        for (int c = 0; c < C; ++c) csum[c + 1] += csum[c];
+#pragma omp parallel for num_threads(nthr) schedule(static, 1)
+        for (int c = 0; c < C; ++c) {
+            int64_t t = csum[c];
+            for (int64_t u = n * c / C; u < n * (c + 1) / C; ++u) {
+                ast[u] = (int32_t)t;
+                t += deg[u];
+            }
+        }
+        ast[n] = (int32_t)csum[C];
+        fit(W.adj_nbr, ast[n] + 1);
+        fit(W.adj_w, ast[n] + 1);
+        int32_t* anb = W.adj_nbr.data();
+        double* aw = W.adj_w.data();
+#pragma omp parallel for num_threads(nthr) schedule(static, 4096)
+        for (int64_t u = 0; u < n; ++u) {
+            int64_t d = ast[u];
+            for (int64_t k = rp[u]; k < rp[u + 1]; ++k)
+                if (!(wk[k] <= 0.0)) {
+                    anb[d] = (int32_t)ci[k];
+                    aw[d] = wk[k];
+                    ++d;
+                }
+        }
+        if (dbg) fprintf(stderr, "[hpbj]   adjacency %.1f ms\n", ms_since(t_a0));
+        return GraphView<int32_t, int32_t>{n, ast, anb, aw, deg};
+    };
+
+    // Large graphs: region growing needs only the pattern, so when A has no
+    // explicit off-diagonal zero (every entry is an edge iff the pattern is
+    // symmetric) it starts on A's off-diagonal pattern right away and the
+    // weights + refinement view are built on the other cores meanwhile.
+    const GrowOpts go = grow_opts();
+    const int nth = omp_get_max_threads();
+    if ((go.ell > 0 || (go.ell < 0 && n >= (int64_t(1) << 21))) && n < (int64_t(1) << 28) && nth >= 2 &&
+        !getenv("HPBJ_GROW_NOPIPE")) {
+        const auto t_q0 = std::chrono::steady_clock::now();
+        int zero = 0;
+        fit(W.ell, (size_t)n * 8);
+        uint32_t* ell = W.ell.data();
+        // one pass: off-diagonal counts, explicit zeros, the records
+#pragma omp parallel for schedule(static, 4096) reduction(| : zero)
+        for (int64_t u = 0; u < n; ++u) {
+            uint32_t e[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
             int64_t d = 0;
-            for (int64_t k = rp[u]; k < rp[u + 1]; ++k) d += !(wk[k] <= 0.0);
+            for (int64_t k = rp[u]; k < rp[u + 1]; ++k)
+                if (ci[k] != u) {
+                    if (d < 8) e[d] = (uint32_t)ci[k];
+                    ++d;
+                    zero |= val[k] == 0.0;
+                }
             deg[u] = d;
+            e[0] = d > 8 ? 0xFu << 28 : (e[0] | (uint32_t)d << 28);
+            std::memcpy(ell + (size_t)u * 8, e, sizeof e);
+        }
+        if (!zero) {
+            if (dbg) fprintf(stderr, "[hpbj]   pattern + records %.1f ms\n", ms_since(t_q0));
+            GraphView<int32_t, int32_t> view{n, nullptr, nullptr, nullptr, deg};
+            GrowPipeline pl;
+            pl.ell = ell;
+            pl.rp = rp;
+            pl.ci = ci;
+            // fewer threads than cores: the build's memory traffic slows the
+            // latency-bound grow, and it has the grow's whole duration
+            int wt = std::max(1, std::min(nth - 1, 8));
+            if (const char* e = getenv("HPBJ_GROW_WT")) wt = std::max(1, atoi(e));
+            pl.during_grow = [&, wt]() -> bool {
+                if (!weights(wt)) return false;
+                view = adjacency(wt);
+                return true;
+            };
+            if (partition_view(view, s, tol, assignment, &pl)) return;
+            // structurally unsymmetric: the graph has one-sided edges
+            const Adjacency g = graph_general(n, rp, ci, val);
+            partition_adjacency(g, s, tol, assignment);
+            return;
         }
     }
-    if (missing) {
+
+    if (!weights(nth)) {
         const Adjacency g = graph_general(n, rp, ci, val);
         partition_adjacency(g, s, tol, assignment);
         return;
     }
-    if (getenv("HPBJ_DEBUG"))
-        fprintf(stderr, "[hpbj]   weights %.1f ms\n",
-                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_w0).count());
-    const auto t_a0 = std::chrono::steady_clock::now();
-    // compact int32 adjacency (kept entries only): 4 B/neighbour and 4-byte
-    // offsets for the sequential BFS instead of 16 B (int64 column + weight)
-    // per CSR entry
-    fit(W.adj_start, n + 1);
-    int32_t* ast = W.adj_start.data();
-    ast[0] = 0;
-    for (int64_t u = 0; u < n; ++u) ast[u + 1] = ast[u] + deg[u];
-    fit(W.adj_nbr, ast[n] + 1);
-    fit(W.adj_w, ast[n] + 1);
-    int32_t* anb = W.adj_nbr.data();
-    double* aw = W.adj_w.data();
 #pragma omp parallel for schedule(static, 4096)
     for (int64_t u = 0; u < n; ++u) {
-        int64_t d = ast[u];
-        for (int64_t k = rp[u]; k < rp[u + 1]; ++k)
-            if (!(wk[k] <= 0.0)) {
-                anb[d] = (int32_t)ci[k];
-                aw[d] = wk[k];
-                ++d;
-            }
+        int64_t d = 0;
+        for (int64_t k = rp[u]; k < rp[u + 1]; ++k) d += !(wk[k] <= 0.0);
+        deg[u] = d;
     }
-    if (getenv("HPBJ_DEBUG"))
-        fprintf(stderr, "[hpbj]   adjacency %.1f ms\n",
-                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_a0).count());
-    GraphView<int32_t, int32_t> view{n, ast, anb, aw, deg};
+    const GraphView<int32_t, int32_t> view = adjacency(nth);
     partition_view(view, s, tol, assignment);
 }
 

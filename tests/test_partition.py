@@ -289,3 +289,48 @@ def test_assignment_errors():
         hp.partition_from_assignment([0, 0, 0, 0], 2)
     with pytest.raises(ValueError):
         hp.partition_from_assignment([0, 0], 3)
+
+
+def _with_zero_entries(a, seed):
+    """Explicit off-diagonal zeros: some pairs zero on both sides (no edge,
+    graph.cpp:41), some on one side only (an edge of half the other weight)."""
+    rng = np.random.default_rng(seed)
+    rows = np.repeat(np.arange(a.n), np.diff(a.row_starts))
+    cols = np.asarray(a.col_indices)
+    vals = np.array(a.values, dtype=np.float64)
+    off = np.nonzero(rows < cols)[0]
+    both = rng.choice(off, max(1, off.size // 20), replace=False)
+    one = rng.choice(np.setdiff1d(off, both), max(1, off.size // 20), replace=False)
+    pos = {(int(r), int(c)): k for k, (r, c) in enumerate(zip(rows, cols))}
+    for k in both:
+        vals[k] = 0.0
+        vals[pos[(int(cols[k]), int(rows[k]))]] = -0.0
+    vals[one] = 0.0
+    return hp.SparseMatrix(a.n, np.asarray(a.row_starts), cols, vals)
+
+
+@pytest.mark.parametrize("env", [{"HPBJ_GROW_ELL": "1"}, {"HPBJ_GROW_ELL": "1", "HPBJ_GROW_NOPIPE": "1"},
+                                 {"HPBJ_GROW_ELL": "0"}, {"HPBJ_GROW_ELL": "1", "HPBJ_GROW_PF": "0"}])
+def test_region_growing_variants_match_reference(ref, monkeypatch, env):
+    """Region growing over fixed-stride neighbour records — overlapped with the
+    weight/adjacency build on the other cores when A has no explicit
+    off-diagonal zero (pipelined), or after it — and over the CSR view,
+    against the reference: meshes, long-range couplings, rows longer than a
+    record (hubs), explicit zeros (both-sided: no edge; one-sided: an edge)
+    and a structurally unsymmetric pattern (the pipelined grow is abandoned)."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    rng = np.random.default_rng(3)
+    n = 300
+    t = [(i, i, 4.0) for i in range(n)] + [(i, (i + 1) % n, -1.0) for i in range(n)]
+    t += [(0, j, -0.01) for j in rng.choice(np.arange(1, n), 120, replace=False)]
+    r, c, v = zip(*t)
+    unsym = hp.SparseMatrix.from_triplets(r, c, v, n)
+    hub = fx.random_dd(500, 9, 4)
+    cases = [(fx.laplacian_2d(40, 40), 25, 0.1), (_mesh3d_long_range(14, 30, 4), 11, 0.1),
+             (hub, 20, 0.1), (_with_zero_entries(fx.laplacian_2d(30, 30), 1), 16, 0.1),
+             (_with_zero_entries(_mesh3d_long_range(10, 20, 2), 3), 9, 0.0), (unsym, 10, 0.1)]
+    for a, s, tol in cases:
+        p = hp.partition_graph(a, s, tol)
+        asg, _, _, _ = ref.partition(a.row_starts, a.col_indices, a.values, s, tol)
+        assert np.array_equal(p.assignment, asg), (a.n, s, tol)
