@@ -945,6 +945,7 @@ struct IntC {
 constexpr int kLlMax = 288;
 constexpr int kLlThreads = 256;
 constexpr int kLlCtasPerSm = 2;
+constexpr int kXld = 36;  // X row stride (floats), see xe()
 
 __host__ __device__ inline int ll_lrows(int d) {  // L_Q rows kept: panels 0 .. T-2
     const int T = (d + 31) / 32;
@@ -957,7 +958,7 @@ __host__ __device__ inline size_t ll_smem_bytes(int dhi) {
     constexpr int NW = kLlThreads / 32;
     const int T = (dhi + 31) / 32;
     const int lr = ll_lrows(dhi);
-    return (size_t)dhi * 32 * sizeof(float)                 // X: current column panel, all rows
+    return (size_t)dhi * kXld * sizeof(float)               // X: current column panel, all rows
            + (size_t)(dhi > 32 ? dhi - 32 : 1) * 32 * sizeof(float)  // Lb: rows 32.. of L_{Q-1}
            + (size_t)2 * 32 * 32 * sizeof(float)            // L11 of two panels
            + (size_t)2 * NW * 32 * sizeof(float)            // candidate rows (double buffered)
@@ -968,10 +969,12 @@ __host__ __device__ inline size_t ll_smem_bytes(int dhi) {
            + 64;
 }
 
-// swizzled X: quad (c / 4) of row r at quad slot (c / 4) ^ (r & 7)
-__device__ __forceinline__ int xq(int r, int q) { return r * 32 + ((q ^ (r & 7)) << 2); }
-// element (r, c) of the swizzled X: ((c / 4) ^ (r & 7)) * 4 + c % 4 = c ^ ((r & 7) << 2)
-__device__ __forceinline__ int xe(int r, int c) { return (r << 5) + (c ^ ((r & 7) << 2)); }
+// X rows padded to kXld = 36 floats: a warp reading one row lane by lane
+// (the updates) and eight threads reading their own rows quad by quad (the
+// panel factorisation: row r's quads start in bank group 9r mod 8) are both
+// conflict-free, and an element address is one multiply-add
+__device__ __forceinline__ int xq(int r, int q) { return r * kXld + (q << 2); }
+__device__ __forceinline__ int xe(int r, int c) { return r * kXld + c; }
 
 __device__ __forceinline__ void bar_named(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
@@ -1069,8 +1072,8 @@ __global__ void __launch_bounds__(kLlThreads, kLlCtasPerSm) k_block_lu_ll(LuPara
     extern __shared__ __align__(128) float llsm[];
     const int lrmax = ll_lrows(dhi);
     const int Tmax = (dhi + 31) / 32;
-    float* X = llsm;                                           // [dhi][32] swizzled
-    float* Lb = X + (size_t)dhi * 32;                          // [dhi-32][32]
+    float* X = llsm;                                           // [dhi][kXld]
+    float* Lb = X + (size_t)dhi * kXld;                        // [dhi-32][32]
     float* L11 = Lb + (size_t)(dhi > 32 ? dhi - 32 : 1) * 32;  // [2][32][32]
     float* cand_v = L11 + 2 * 32 * 32;                         // [2][NW][32]
     int* cand_i = reinterpret_cast<int*>(cand_v + 2 * NW * 32);  // [2][NW][4]: key, row, owner
@@ -1160,7 +1163,7 @@ __global__ void __launch_bounds__(kLlThreads, kLlCtasPerSm) k_block_lu_ll(LuPara
             for (int i = 0; i < RPT; ++i) {
                 const int r = tid + NT * i;
                 if (r < d) {
-                    float4* xr = reinterpret_cast<float4*>(X + r * 32);
+                    float4* xr = reinterpret_cast<float4*>(X + r * kXld);
 #pragma unroll
                     for (int q = 0; q < 8; ++q) xr[q] = make_float4(0.f, 0.f, 0.f, 0.f);
                     const int cend = o + c0 + kw;
@@ -1253,10 +1256,10 @@ __global__ void __launch_bounds__(kLlThreads, kLlCtasPerSm) k_block_lu_ll(LuPara
                     const bool has = a < na;
                     myrow[i] = has ? act[a] : 0;
                     fl[i] = !has;
-                    const float4* xr = reinterpret_cast<const float4*>(X + myrow[i] * 32);
+                    const float4* xr = reinterpret_cast<const float4*>(X + myrow[i] * kXld);
 #pragma unroll
                     for (int q = 0; q < 8; ++q) {
-                        const float4 t4 = has ? xr[q ^ (myrow[i] & 7)] : make_float4(0.f, 0.f, 0.f, 0.f);
+                        const float4 t4 = has ? xr[q] : make_float4(0.f, 0.f, 0.f, 0.f);
                         rv[i][4 * q + 0] = t4.x;
                         rv[i][4 * q + 1] = t4.y;
                         rv[i][4 * q + 2] = t4.z;
@@ -1398,10 +1401,10 @@ __global__ void __launch_bounds__(kLlThreads, kLlCtasPerSm) k_block_lu_ll(LuPara
                 const int lo = lofs[P];
                 for (int i = tid; i < 32 + nnew; i += NT) {
                     const int r = i < 32 ? prow[c0 + i] : act[i - 32];
-                    const float4* xr = reinterpret_cast<const float4*>(X + r * 32);
+                    const float4* xr = reinterpret_cast<const float4*>(X + r * kXld);
                     float4* lr = reinterpret_cast<float4*>(Lg + ((size_t)lo + i) * 32);
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) lr[q] = xr[q ^ (r & 7)];
+                    for (int q = 0; q < 8; ++q) lr[q] = xr[q];
                     rowQ[lo + i] = (short)r;
                     posQ[(size_t)P * dhi + r] = (short)i;
                 }

@@ -169,13 +169,12 @@ struct hpbj_ctx {
     // matrix (original ordering)
     bool has_matrix = false;
     DevCsr A;
-    std::vector<int64_t> h_rp;
+    std::vector<int> h_rp;          // row starts of A (int32)
     PinnedBuf stage_mat;  // set_matrix: int32 rp, int32 ci, FP64 val
     PinnedBuf stage_vec;  // hpbj_gmres host path: b, x
     std::vector<int> h_perm32;      // bj_setup scratch (persistent: no page faults per setup)
-    std::vector<int> h_rowlen_perm; // row lengths of Q A Q^T
-    std::vector<uint32_t> h_seen;   // bijection check, generation-stamped
-    uint32_t seen_gen = 0;
+    std::vector<int> h_brp;         // row starts of Q A Q^T, fetched for the fused-cycle plan
+    bool h_brp_valid = false;
     SpmvPlan planA;
     double* d_tmpx = nullptr;  // n
     double* d_tmpy = nullptr;  // n
@@ -400,13 +399,34 @@ void set_plan(SpmvPlan& p, int group, std::vector<int>& rows) {
     }
 }
 
-void make_plan(SpmvPlan& p, const std::vector<int64_t>& rp, const int* perm_or_null, int n) {
+void make_plan(SpmvPlan& p, const int* rp, int n) {
     const int g = spmv_group(rp[n], n);
     const int thr = spmv_long_thresh(g);
     std::vector<int> rows;
-    for (int i = 0; i < n; ++i)
-        if (rp[i + 1] - rp[i] > thr) rows.push_back(perm_or_null ? perm_or_null[i] : i);
+#pragma omp parallel if (n > 65536)
+    {
+        std::vector<int> mine;
+#pragma omp for schedule(static) nowait
+        for (int i = 0; i < n; ++i)
+            if (rp[i + 1] - rp[i] > thr) mine.push_back(i);
+#pragma omp critical
+        rows.insert(rows.end(), mine.begin(), mine.end());
+    }
     set_plan(p, g, rows);
+}
+
+// Row starts of Q A Q^T on the host, only when the fused cycle kernel could
+// take the system (its plan sizes the per-CTA matrix slices from them).
+const int* host_brp(hpbj_ctx* c) {
+    if (!fused_possible(c->A.n, c->s, c->num_sms) || !c->B.rp) return nullptr;
+    if (!c->h_brp_valid) {
+        c->h_brp.resize((size_t)c->B.n + 1);
+        HPBJ_CUDA(cudaMemcpyAsync(c->h_brp.data(), c->B.rp, sizeof(int) * ((size_t)c->B.n + 1),
+                                  cudaMemcpyDeviceToHost, c->stream));
+        HPBJ_CUDA(cudaStreamSynchronize(c->stream));
+        c->h_brp_valid = true;
+    }
+    return c->h_brp.data();
 }
 
 void ensure_ws(hpbj_ctx* c, int m) {
@@ -915,7 +935,7 @@ void solve(hpbj_ctx* c, const double* d_b, double* d_x, const hpbj_gmres_opts* o
     } else {
         const bool use_graph = !c->profiling && c->use_graph;
         c->fused = c->use_fused && c->active == kPcBJ && c->neumann <= 0 ? plan_fused(n, c->s, c->dmax, c->num_sms, m, c->planB.n_long > 0,
-                                             c->h_rowlen_perm.data(), c->spk_rows != 0)
+                                             host_brp(c), c->spk_rows != 0)
                                 : FusedPlan{};
         if (c->fused.ok && getenv("HPBJ_FUSED_PROF") && !c->d_fprof) {
             HPBJ_CUDA(cudaMalloc(&c->d_fprof, 8 * sizeof(unsigned long long)));
@@ -1108,10 +1128,12 @@ int hpbj_set_matrix(hpbj_ctx* ctx, int64_t n, const int64_t* row_ptr, const int6
         int* rp = reinterpret_cast<int*>(stg);
         int* ci = reinterpret_cast<int*>(stg + o_ci);
         double* vs = reinterpret_cast<double*>(stg + o_val);
+        if ((int64_t)ctx->h_rp.size() < n + 1) ctx->h_rp.resize(n + 1);
+        int* hrp = ctx->h_rp.data();
 #pragma omp parallel
         {
 #pragma omp for schedule(static) nowait
-            for (int64_t i = 0; i <= n; ++i) rp[i] = (int)row_ptr[i];
+            for (int64_t i = 0; i <= n; ++i) rp[i] = hrp[i] = (int)row_ptr[i];
 #pragma omp for schedule(static) nowait
             for (int64_t k = 0; k < nnz; ++k) ci[k] = (int)col[k];
 #pragma omp for schedule(static)
@@ -1129,8 +1151,7 @@ int hpbj_set_matrix(hpbj_ctx* ctx, int64_t n, const int64_t* row_ptr, const int6
         HPBJ_CUDA(cudaMemcpyAsync(ctx->A.val, vs, sizeof(double) * (size_t)nnz, cudaMemcpyHostToDevice, st));
         ctx->stage_mat.fence(st);  // later work on the stream is ordered after the copies
         const auto t3 = std::chrono::steady_clock::now();
-        ctx->h_rp.assign(row_ptr, row_ptr + n + 1);
-        make_plan(ctx->planA, ctx->h_rp, nullptr, ni);
+        make_plan(ctx->planA, ctx->h_rp.data(), ni);
         dslot(ctx->d_tmpx, ni);
         dslot(ctx->d_tmpy, ni);
         ctx->has_matrix = true;
@@ -1193,17 +1214,15 @@ int hpbj_bj_setup(hpbj_ctx* ctx, int64_t s, const int64_t* perm, const int64_t* 
         const auto T0 = tnow();
         const int n = ctx->A.n;
         if (s < 1 || s > n) fail(HPBJ_EINVAL, "partition: block count must satisfy 1 <= s <= n");
-        // validate the partition (bijection, contiguous nonempty blocks) and,
-        // in the same pass over the rows, collect the rows that need a CTA sort
-        // after the scatter and the SpMV hub rows (permuted indices)
+        // validate the partition (targets in range here, bijection on the
+        // device before the permutation kernels run; contiguous nonempty
+        // blocks) and, in the same pass over the rows, collect the rows that
+        // need a CTA sort after the scatter and the SpMV hub rows (permuted
+        // indices)
         std::vector<int>& hperm = ctx->h_perm32;
-        std::vector<uint32_t>& seen = ctx->h_seen;
         if ((int)hperm.size() < n) hperm.resize(n);
-        if ((int)seen.size() < n) seen.assign(n, 0u);
-        const uint32_t gen = ++ctx->seen_gen;
         const int spg = spmv_group(ctx->A.nnz, n), spthr = spmv_long_thresh(spg);
-        if ((int)ctx->h_rowlen_perm.size() < n) ctx->h_rowlen_perm.resize(n);
-        int* rowlen = ctx->h_rowlen_perm.data();
+        const int* hrp = ctx->h_rp.data();
         std::vector<int> lrows, hubs;
         int maxlen = 0, bad = 0;
 #pragma omp parallel if (n > 65536)
@@ -1217,11 +1236,8 @@ int hpbj_bj_setup(hpbj_ctx* ctx, int64_t s, const int64_t* perm, const int64_t* 
                     bad = 1;
                     continue;
                 }
-                // a repeated target shows up as a second stamp of the same generation
-                if (__atomic_exchange_n(&seen[p], gen, __ATOMIC_RELAXED) == gen) bad = 1;
                 hperm[i] = (int)p;
-                const int len = (int)(ctx->h_rp[i + 1] - ctx->h_rp[i]);
-                rowlen[p] = len;
+                const int len = hrp[i + 1] - hrp[i];
                 if (len > kShortRow) {
                     lr.push_back((int)p);
                     ml = std::max(ml, len);
@@ -1312,6 +1328,17 @@ int hpbj_bj_setup(hpbj_ctx* ctx, int64_t s, const int64_t* perm, const int64_t* 
         set_plan(ctx->planB, spg, hubs);
         const auto T3 = tnow();
         int* tmp = dalloc<int>((size_t)n + 8192);
+        {
+            launch_perm_check(n, ctx->d_perm, reinterpret_cast<unsigned*>(tmp), tmp + n, st, &ctx->launches);
+            int hbad = 0;
+            HPBJ_CUDA(cudaMemcpyAsync(&hbad, tmp + n, sizeof(int), cudaMemcpyDeviceToHost, st));
+            HPBJ_CUDA(cudaStreamSynchronize(st));
+            if (hbad) {
+                dput(tmp);
+                fail(HPBJ_EINVAL, "permute_symmetric: not a bijection");
+            }
+        }
+        ctx->h_brp_valid = false;
         cudaEvent_t e0, e1;
         HPBJ_CUDA(cudaEventCreate(&e0));
         HPBJ_CUDA(cudaEventCreate(&e1));

@@ -62,7 +62,7 @@ struct SrcScaled {  // (float)(v[row] * scale): v_j = w * (1/h) (gmres.hpp:72-73
     const double* v;
     double scale;
     __device__ float operator()(int row) const { return __double2float_rn(__ldcg(v + row) * scale); }
-    __device__ void prefetch(int, int) const {}
+    __device__ void prefetch(int, int, int) const {}
 };
 struct DstZ {
     float* z;
@@ -446,23 +446,28 @@ __global__ void __launch_bounds__(kThreads, 1) k_arnoldi_cycle(FusedArgs a) {
 
 }  // namespace
 
-FusedPlan plan_fused(int n, int s, int dmax, int num_sms, int m, bool has_long, const int* rowlen, bool rows) {
+static int fused_grid(int n, int num_sms) {
+    // every SM: the apply phase is latency bound, more warps in flight win
+    return std::max(1, std::min(num_sms, ((n + 1) & ~1) / 64));
+}
+
+bool fused_possible(int n, int s, int num_sms) {
+    return n > 0 && s <= fused_grid(n, num_sms) * kWarps - 1;  // one block per apply warp (the block cache)
+}
+
+FusedPlan plan_fused(int n, int s, int dmax, int num_sms, int m, bool has_long, const int* brp, bool rows) {
     FusedPlan F;
-    if (m > kMaxRestart || n <= 0 || dmax > kIdx16MaxDim || rows) return F;
+    if (m > kMaxRestart || n <= 0 || dmax > kIdx16MaxDim || rows || !brp) return F;
     if (has_long) return F;  // hub rows: the per-kernel path gives them whole CTAs
+    if (!fused_possible(n, s, num_sms)) return F;
     const int npad = (n + 1) & ~1;
     const int ystride = ((dmax + 31) / 32) * 32;
-    // every SM: the apply phase is latency bound, more warps in flight win
-    const int grid = std::max(1, std::min(num_sms, npad / 64));
-    if (s > grid * kWarps - 1) return F;  // one block per apply warp (the block cache)
+    const int grid = fused_grid(n, num_sms);
     int slice = (npad + grid - 1) / grid;
     slice = (slice + 1) & ~1;
     int nnz_cap = 0;  // largest matrix slice
-    for (int c = 0; c < grid; ++c) {
-        int64_t t = 0;
-        for (int r = c * slice; r < std::min(n, (c + 1) * slice); ++r) t += rowlen[r];
-        nnz_cap = (int)std::max<int64_t>(nnz_cap, t);
-    }
+    for (int c = 0; c < grid && c * slice < n; ++c)
+        nnz_cap = std::max(nnz_cap, brp[std::min(n, (c + 1) * slice)] - brp[c * slice]);
     nnz_cap = (nnz_cap + 1) & ~1;
     const size_t smem = (size_t)2 * slice * sizeof(double) + (size_t)(m + 1) * (m + 1) * sizeof(double) +
                         (size_t)nnz_cap * (sizeof(double) + sizeof(int)) + (size_t)(((slice + 2) & ~1) + 2) * sizeof(int) +

@@ -42,6 +42,11 @@
 #include <exception>
 #include <functional>
 #include <thread>
+#if defined(__x86_64__)
+#include <x86intrin.h>
+#else
+static inline unsigned long long __rdtsc() { return 0; }
+#endif
 
 #include <omp.h>
 #include <sys/mman.h>
@@ -352,6 +357,14 @@ inline int32_t refine_decide(const GraphView<Idx, Off>& g, const S* state, const
     return dec;
 }
 
+template <class Idx, class Off>
+int64_t max_degree(const GraphView<Idx, Off>& g) {
+    int64_t maxdeg = 0;
+#pragma omp parallel for schedule(static) reduction(max : maxdeg) if (g.n > 65536)
+    for (int64_t u = 0; u < g.n; ++u) maxdeg = std::max<int64_t>(maxdeg, (int64_t)(g.st[u + 1] - g.st[u]));
+    return maxdeg;
+}
+
 // One refinement sweep (partition.cpp:117-141) in the reference's u order
 // over block ids of type S (moves applied immediately, as there). Returns
 // the number of moves.
@@ -360,9 +373,7 @@ int64_t refine_sweep(const GraphView<Idx, Off>& g, S* state, int64_t* sizes, int
     const int64_t n = g.n;
     const Off* st = g.st;
     const Idx* nb = g.idx;
-    int64_t maxdeg = 0;
-    for (int64_t u = 0; u < n; ++u) maxdeg = std::max<int64_t>(maxdeg, (int64_t)(st[u + 1] - st[u]));
-    std::vector<int32_t> tch(maxdeg + 1);
+    std::vector<int32_t> tch(max_degree(g) + 1);
     int64_t moves = 0;
     constexpr int64_t kRefAhead = 8;
     for (int64_t u = 0; u < n; ++u) {
@@ -481,9 +492,9 @@ int64_t refine_sweep_par(const GraphView<Idx, Off>& g, S* state, int64_t* sizes,
     // phase 2
     std::vector<double> conn(s, 0.0);
     int64_t ndirty = 0, nrec = 0, nscan = 0;
-    int64_t maxdeg = 0;
-    for (int64_t u = 0; u < n; ++u) maxdeg = std::max<int64_t>(maxdeg, (int64_t)(st[u + 1] - st[u]));
-    std::vector<int32_t> tch(maxdeg + 1);
+    const bool dbg = getenv("HPBJ_DEBUG") != nullptr;
+    uint64_t cyc_dirty = 0, cyc_scan = 0;
+    std::vector<int32_t> tch(max_degree(g) + 1);
     int64_t moves = 0;
     for (int t = 0; t < T; ++t) {
         const int32_t* r = rec[t].data();
@@ -509,7 +520,9 @@ int64_t refine_sweep_par(const GraphView<Idx, Off>& g, S* state, int64_t* sizes,
             ndirty += (f & 4) != 0;
             nrec += (f & 1) != 0;
             if (f & 4) {
+                const uint64_t c0 = dbg ? __rdtsc() : 0;
                 d = refine_decide(g, state, sizes, cap, conn.data(), tch.data(), u);
+                if (dbg) cyc_dirty += __rdtsc() - c0;
                 if (f & 1) r += 1 + r[0];
             } else if (f & 1) {
                 const int nc = r[0];
@@ -531,20 +544,25 @@ int64_t refine_sweep_par(const GraphView<Idx, Off>& g, S* state, int64_t* sizes,
             const bool same_diff = fin != (int32_t)spec[u];  // what later nodes of this range assumed
             const bool cross_diff = (f & 2) && fin != bu;    // what later ranges assumed (the initial block)
             nscan += same_diff || cross_diff;
-            if (same_diff || cross_diff)
+            if (same_diff || cross_diff) {
+                const uint64_t c0 = dbg ? __rdtsc() : 0;
                 for (Off k = st[u]; k < st[u + 1]; ++k) {
                     const int64_t v = nb[k];
                     if (v <= u) continue;
                     if (v < e ? same_diff : cross_diff) fl[v] |= 4;
                 }
+                if (dbg) cyc_scan += __rdtsc() - c0;
+            }
             ++u;
         }
     }
     if (getenv("HPBJ_DEBUG"))
-        fprintf(stderr, "[hpbj]   refine: T=%d phase1 %.1f ms, phase2 %.1f ms, %lld recorded, %lld recomputed, %lld scanned\n", T,
-                std::chrono::duration<double, std::milli>(t_p1 - t_p0).count(),
+        fprintf(stderr,
+                "[hpbj]   refine: T=%d phase1 %.1f ms, phase2 %.1f ms, %lld recorded, %lld recomputed (%.1f Mcyc), "
+                "%lld scanned (%.1f Mcyc)\n",
+                T, std::chrono::duration<double, std::milli>(t_p1 - t_p0).count(),
                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_p1).count(),
-                (long long)nrec, (long long)ndirty, (long long)nscan);
+                (long long)nrec, (long long)ndirty, cyc_dirty * 1e-6, (long long)nscan, cyc_scan * 1e-6);
     return moves;
 }
 
@@ -568,6 +586,8 @@ double cross_range_fraction(const GraphView<Idx, Off>& g, int T) {
 
 // Fixed-stride neighbour records for region growing: 8 ids per node, the
 // degree in the top 4 bits of the first (15: longer row, read elsewhere).
+// Unused slots hold n, a node whose taken bit is always set (pushes nothing),
+// so every record is walked as 8 branch-free pushes.
 template <class DegFn, class NbrFn>
 void build_ell(int64_t n, uint32_t* ell, DegFn deg, NbrFn nbr) {
 #pragma omp parallel for schedule(static, 4096)
@@ -578,7 +598,7 @@ void build_ell(int64_t n, uint32_t* ell, DegFn deg, NbrFn nbr) {
             e[0] = 0xFu << 28;
             continue;
         }
-        for (int i = 0; i < 8; ++i) e[i] = i < d ? nbr(u, i) : 0u;
+        for (int i = 0; i < 8; ++i) e[i] = i < d ? nbr(u, i) : (uint32_t)n;
         e[0] |= (uint32_t)d << 28;
     }
 }
@@ -589,14 +609,14 @@ struct GrowOpts {
     bool defer = true;   // block ids written after growing (assignment-order list)
     int ell = -1;        // fixed-stride neighbour records (-1: for n >= 2^21)
     bool pf = true;
-    int loc = 3;
+    bool pushpf = false; // prefetch records when queued as well
 };
 inline GrowOpts grow_opts() {
     GrowOpts o;
     if (const char* e = getenv("HPBJ_GROW_PF")) o.ahead = o.ahead_csr = atoi(e);
     if (const char* e = getenv("HPBJ_GROW_DEFER")) o.defer = atoi(e) != 0;
     if (const char* e = getenv("HPBJ_GROW_ELL")) o.ell = atoi(e);
-    if (const char* e = getenv("HPBJ_GROW_LOC")) o.loc = atoi(e);
+    if (const char* e = getenv("HPBJ_GROW_PUSHPF")) o.pushpf = atoi(e) != 0;
     return o;
 }
 
@@ -648,15 +668,7 @@ int64_t grow_blocks(const GraphView<Idx, Off>& g, const uint32_t* ell, const int
                 taken[sd >> 6] |= 1ull << (sd & 63);
             }
             if constexpr (ELL) {
-                if (pf && head + K < tail) {
-                    const uint32_t* a = ell + (size_t)queue[head + K] * 8;
-                    switch (go.loc) {
-                        case 0: __builtin_prefetch(a, 0, 0); break;
-                        case 1: __builtin_prefetch(a, 0, 1); break;
-                        case 2: __builtin_prefetch(a, 0, 2); break;
-                        default: __builtin_prefetch(a, 0, 3); break;
-                    }
-                }
+                if (pf && head + K < tail) __builtin_prefetch(ell + (size_t)queue[head + K] * 8, 0, 3);
             } else {
                 if (pf && head + 2 * K < tail) __builtin_prefetch(st + queue[head + 2 * K], 0, 1);
                 if (pf && head + K < tail) {  // prefetch the adjacency of a node popped soon
@@ -669,14 +681,14 @@ int64_t grow_blocks(const GraphView<Idx, Off>& g, const uint32_t* ell, const int
             else state[u] = bb;
             ++grown;
             --connected_left;
+            const int64_t tail0 = tail;
             if constexpr (ELL) {
                 const uint32_t* e = ell + (size_t)u * 8;
                 const uint32_t h = e[0];
                 const uint32_t d = h >> 28;
-                if (d <= 8) {
+                if (d <= 8) {  // padding slots name node n (always taken)
 #pragma GCC unroll 8
                     for (uint32_t i = 0; i < 8; ++i) {
-                        if (i >= d) break;
                         const int32_t v = (int32_t)(i == 0 ? (h & 0x0FFFFFFFu) : e[i]);
                         uint64_t& word = taken[v >> 6];
                         const uint64_t bit = 1ull << (v & 63);
@@ -699,6 +711,10 @@ int64_t grow_blocks(const GraphView<Idx, Off>& g, const uint32_t* ell, const int
                 }
             } else {
                 push_csr(u, tail);
+            }
+            if constexpr (ELL) {  // records of the nodes just queued (popped a frontier later)
+                if (go.pushpf)
+                    for (int64_t q = tail0; q < tail; ++q) __builtin_prefetch(ell + (size_t)queue[q] * 8, 0, 3);
             }
         }
         sizes[b] = grown;
@@ -804,10 +820,11 @@ bool partition_view(const GraphView<Idx, Off>& g, int64_t s, double tol, int64_t
     std::fill(conn, conn + s, 0.0);
     fit(W.queue, n + 1);
     int32_t* queue = W.queue.data();
-    fit(W.taken, (n + 63) / 64);
+    fit(W.taken, (n + 64) / 64);
     uint64_t* taken = W.taken.data();  // bit v: assigned or queued
 #pragma omp parallel for schedule(static) if (n > 65536)
-    for (int64_t w = 0; w < (n + 63) / 64; ++w) taken[w] = 0ull;
+    for (int64_t w = 0; w < (n + 64) / 64; ++w) taken[w] = 0ull;
+    taken[n >> 6] |= 1ull << (n & 63);  // the records' padding node
 
     // Block ids are stored as S (16-bit when s fits: half the cache footprint
     // of the refinement's random neighbour lookups); -1 = unassigned.
@@ -1033,7 +1050,8 @@ void partition_csr(int64_t n, const int64_t* rp, const int64_t* ci, const double
         // one pass: off-diagonal counts, explicit zeros, the records
 #pragma omp parallel for schedule(static, 4096) reduction(| : zero)
         for (int64_t u = 0; u < n; ++u) {
-            uint32_t e[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+            uint32_t e[8];
+            for (int i = 0; i < 8; ++i) e[i] = (uint32_t)n;
             int64_t d = 0;
             for (int64_t k = rp[u]; k < rp[u + 1]; ++k)
                 if (ci[k] != u) {

@@ -29,6 +29,8 @@ void launch_gather_values(const int* src, const double* val, double* nval, int n
                           int64_t* launches);
 void launch_permute_vec(int n, const int* perm, const double* x, double* y, bool inverse, cudaStream_t st,
                         int64_t* launches);
+// perm (entries already range-checked) is a bijection: *bad = 0 (bits: (n + 31) / 32 words of scratch)
+void launch_perm_check(int n, const int* perm, unsigned* bits, int* bad, cudaStream_t st, int64_t* launches);
 
 // ---- block_lu.cu ----------------------------------------------------------
 struct PertRecord {
@@ -291,7 +293,9 @@ struct FusedPlan {
 };
 // rowlen: row lengths of the permuted matrix (the CTA slices' matrix rows are
 // cached in shared memory)
-FusedPlan plan_fused(int n, int s, int dmax, int num_sms, int m, bool has_long, const int* rowlen, bool rows);
+// brp: row starts of the permuted matrix (host), or null when unavailable
+FusedPlan plan_fused(int n, int s, int dmax, int num_sms, int m, bool has_long, const int* brp, bool rows);
+bool fused_possible(int n, int s, int num_sms);
 void launch_arnoldi_cycle(const FusedPlan& F, const SpkView& pc, const DevCsr& a, const SpmvPlan& plan,
                           const KrylovBufs& kb, double* gram, SolveState* sst, GridBarrier* gb, float* z32,
                           unsigned long long* prof, cudaStream_t st, int64_t* launches);

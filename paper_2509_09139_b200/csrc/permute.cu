@@ -76,6 +76,15 @@ __global__ void k_perm_rowlen(int n, const int* __restrict__ rp, const int* __re
         newlen[perm[i]] = rp[i + 1] - rp[i];
 }
 
+// Each target claimed once: a second claim of a bit is a repeated target.
+__global__ void k_perm_check(int n, const int* __restrict__ perm, unsigned* __restrict__ bits, int* __restrict__ bad) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int p = perm[i];
+        const unsigned bit = 1u << (p & 31);
+        if (atomicOr(&bits[p >> 5], bit) & bit) *bad = 1;
+    }
+}
+
 __global__ void k_set_total(int* out, int n, const int* in_last, const int* out_last) {
     out[n] = *out_last + *in_last;
 }
@@ -213,6 +222,15 @@ void launch_permute_pattern(const DevCsr& a, const int* perm, DevCsr& b, int* sr
         }
         *launches += 1;
     }
+    HPBJ_CUDA(cudaGetLastError());
+}
+
+void launch_perm_check(int n, const int* perm, unsigned* bits, int* bad, cudaStream_t st, int64_t* launches) {
+    HPBJ_CUDA(cudaMemsetAsync(bits, 0, sizeof(unsigned) * (((size_t)n + 31) / 32), st));
+    HPBJ_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st));
+    const int grid = std::max(1, std::min((n + 255) / 256, 148 * 16));
+    k_perm_check<<<grid, 256, 0, st>>>(n, perm, bits, bad);
+    *launches += 1;
     HPBJ_CUDA(cudaGetLastError());
 }
 

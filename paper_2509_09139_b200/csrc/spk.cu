@@ -343,7 +343,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, ROWS ? 7 : 8) k_apply_spk(S
     const int b_first = blockIdx.x * kWarpsPerCta + wid;
     if (b_first < p.s) {
         prefetch_block_head<IdxT>(p, b_first, lane);
-        if (p.pf && lane == 5) src.prefetch(p.bstart[b_first], p.bstart[b_first + 1] - p.bstart[b_first]);
+        if (p.pf) src.prefetch(p.bstart[b_first], p.bstart[b_first + 1] - p.bstart[b_first], lane);
     }
     for (int b = b_first; b < p.s; b += nw)
         spk_solve_block<Acc, IdxT, STAGE, ROWS>(p, b, b + nw < p.s ? b + nw : -1, src, dst, ybuf, dsh, lane, tbuf,
@@ -433,7 +433,7 @@ struct DstNeumann {
 struct SrcVec64 {
     const double* v;
     __device__ double operator()(int row) const { return __ldg(v + row); }
-    __device__ void prefetch(int o, int d) const { prefetch_rows_l2(v, o, d); }
+    __device__ void prefetch(int o, int d, int lane) const { prefetch_rows_l2(v, o, d, lane); }
 };
 
 }  // namespace

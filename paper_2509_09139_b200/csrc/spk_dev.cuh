@@ -15,24 +15,25 @@ namespace spk {
 constexpr int kMaxPanels = 9;  // pivots of up to 288 rows gathered with full ILP
 
 // ----------------------------------------------------------------------------
-// L2 bulk prefetch of the 8-byte rows [o, o + d) of v (a block's source rows:
-// pivoting permutes only within the block).
-__device__ __forceinline__ void prefetch_rows_l2(const double* v, int o, int d) {
-    const uintptr_t a = (uintptr_t)(v + o) & ~(uintptr_t)15;
-    const uintptr_t e = ((uintptr_t)(v + o + d) + 15) & ~(uintptr_t)15;
-    if (e > a) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((unsigned)(e - a)) : "memory");
+// L2 prefetch of the 8-byte rows [o, o + d) of v (a block's source rows:
+// pivoting permutes only within the block); warp-wide.
+__device__ __forceinline__ void prefetch_rows_l2(const double* v, int o, int d, int lane) {
+    const uintptr_t a = (uintptr_t)(v + o) & ~(uintptr_t)127;
+    const uintptr_t e = (uintptr_t)(v + o + d);
+    for (uintptr_t l = a + ((uintptr_t)lane << 7); l < e; l += 32 * 128)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(l));
 }
 struct SrcDown {  // (float) V[:, st->j][row]  (Arnoldi step)
     const double* V;
     int ldv;
     const SolveState* sst;
     __device__ float operator()(int row) const { return __double2float_rn(__ldg(V + (size_t)sst->j * ldv + row)); }
-    __device__ void prefetch(int o, int d) const { prefetch_rows_l2(V + (size_t)sst->j * ldv, o, d); }
+    __device__ void prefetch(int o, int d, int lane) const { prefetch_rows_l2(V + (size_t)sst->j * ldv, o, d, lane); }
 };
 struct SrcVec {  // (float) v[row]
     const double* v;
     __device__ float operator()(int row) const { return __double2float_rn(__ldg(v + row)); }
-    __device__ void prefetch(int o, int d) const { prefetch_rows_l2(v, o, d); }
+    __device__ void prefetch(int o, int d, int lane) const { prefetch_rows_l2(v, o, d, lane); }
 };
 struct SrcBasis {  // sum_i y_i V[i][row], i ascending (gmres.cpp:152-157), FP64
     const double* V;
@@ -45,7 +46,7 @@ struct SrcBasis {  // sum_i y_i V[i][row], i ascending (gmres.cpp:152-157), FP64
         for (int i = 0; i < steps; ++i) u = fma(y[i], __ldg(V + (size_t)i * ldv + row), u);
         return u;
     }
-    __device__ void prefetch(int, int) const {}
+    __device__ void prefetch(int, int, int) const {}
 };
 struct DstF32 {
     float* z;
@@ -195,12 +196,23 @@ __device__ __forceinline__ void fold_rows(const float* __restrict__ eval, const 
     __syncwarp();
 }
 
-// L2 bulk prefetch of [p, p + bytes) (TMA engine; no registers, no smem).
-__device__ __forceinline__ void prefetch_l2(const void* p, size_t bytes) {
-    const uintptr_t a = (uintptr_t)p & ~(uintptr_t)15;
-    const uintptr_t e = ((uintptr_t)p + bytes + 15) & ~(uintptr_t)15;
-    if (e > a)
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((unsigned)(e - a)) : "memory");
+// L2 prefetches of the next step's data, issued by the whole warp: one
+// 128-byte line per lane and instruction (prefetch.global.L2 — no registers,
+// no shared memory, no completion to wait for). A bulk prefetch
+// (cp.async.bulk.prefetch.L2) takes its address in a uniform register, so
+// issued by lane-dependent ranges it compiles to a serialised R2UR loop over
+// the active lanes (ncu, config 3: 17% of the apply's instructions).
+__device__ __forceinline__ void pf_line(const void* a) { asm volatile("prefetch.global.L2 [%0];" ::"l"(a)); }
+
+// [p0, p0 + b0) and [p1, p1 + b1), lines spread over the lanes
+__device__ __forceinline__ void warp_prefetch_l2(const void* p0, size_t b0, const void* p1, size_t b1, int lane) {
+    const uintptr_t a0 = (uintptr_t)p0 & ~(uintptr_t)127, a1 = (uintptr_t)p1 & ~(uintptr_t)127;
+    const int n0 = b0 ? (int)(((uintptr_t)p0 + b0 - a0 + 127) >> 7) : 0;
+    const int n1 = b1 ? (int)(((uintptr_t)p1 + b1 - a1 + 127) >> 7) : 0;
+    for (int k = lane; k < n0 + n1; k += 32) pf_line((const void*)(k < n0 ? a0 + ((uintptr_t)k << 7) : a1 + ((uintptr_t)(k - n0) << 7)));
+}
+__device__ __forceinline__ void warp_prefetch_l2(const void* p0, size_t b0, int lane) {
+    warp_prefetch_l2(p0, b0, nullptr, 0, lane);
 }
 
 // 16-byte asynchronous global -> shared copy (LDGSTS), L2 only.
@@ -213,47 +225,45 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 
 // The tile quads a pass reads ([quad][lane] float4, see kernels.cuh): the
 // forward pass quad q for lanes l >= 4q, the backward pass quad q < 8 for
-// lanes l < 4q and all of quad 8. Lanes 8..16 issue one quad each.
+// lanes l < 4q and all of quad 8. Each quad is 4 lines of 8 lanes; lane
+// k (+32) takes line k & 3 of quad k >> 2 when the pass reads any of it.
 // full: the block's last panel ((L U)^-1, quads 0..ceil(rows/4)-1 of its
 // first `rows` lanes — the rest is the identity padding, never read).
 __device__ __forceinline__ void prefetch_tile(const SpkView& p, int P, bool fwd, int lane, bool full = false,
                                               int rows = 32) {
     if (!p.pf) return;
-    if (lane >= 8 && lane <= 16) {
-        const int q = lane - 8;
+    const char* t = reinterpret_cast<const char*>(p.dtile + (size_t)P * kTileFloats);
+    for (int k = lane; k < 36; k += 32) {
+        const int q = k >> 2, li = k & 3;
         int l0 = 0, l1 = 32;
         if (q == 8) l1 = (fwd || full) ? 0 : 32;
         else if (full) l1 = 4 * q < rows ? rows : 0;
         else if (fwd) l0 = 4 * q;
         else l1 = 4 * q;
-        if (l1 > l0) prefetch_l2(p.dtile + (size_t)P * kTileFloats + q * 128 + l0 * 4, (size_t)16 * (l1 - l0));
+        if (8 * li < l1 && 8 * li + 8 > l0) pf_line(t + q * 512 + li * 128);
     }
 }
 
+// values and indices of `cnt` entries from e0 (warp-wide)
 template <class IdxT>
-__device__ __forceinline__ void prefetch_entries(const SpkView& p, int e0, int cnt, int lane, int lv, int li) {
+__device__ __forceinline__ void prefetch_entries(const SpkView& p, int e0, int cnt, int lane) {
     if (!p.pf) return;
-    if (lane == lv) prefetch_l2(p.eval + e0, sizeof(float) * cnt);
-    else if (lane == li) prefetch_l2(reinterpret_cast<const IdxT*>(p.eidx) + e0, sizeof(IdxT) * cnt);
+    warp_prefetch_l2(p.eval + e0, sizeof(float) * cnt, reinterpret_cast<const IdxT*>(p.eidx) + e0,
+                     sizeof(IdxT) * cnt, lane);
 }
 
-// Next block's head: descriptors, pivots and its first panel's forward data.
-// Called by the whole warp (one prefetch per lane).
+// Next block's head: descriptors, row metadata, pivots and its first
+// panel's forward data (warp-wide).
 template <class IdxT>
 __device__ __forceinline__ void prefetch_block_head(const SpkView& p, int b, int lane) {
     if (!p.pf) return;
-    const int P0 = p.pstart[b];
-    if (lane < 4) {
-        const int o = p.bstart[b], d = p.bstart[b + 1] - o;
-        const int e0 = p.ent_off[P0], e1 = p.ent_off[P0 + 1];
-        if (lane == 0) {
-            prefetch_l2(p.desc + P0, sizeof(SpkPanel) * (p.pstart[b + 1] - P0));
-            if (p.rows) prefetch_l2(p.rmeta + (size_t)P0 * 64, 128 * (p.pstart[b + 1] - P0));
-        }
-        else if (lane == 1) prefetch_l2(p.piv + o, sizeof(int) * d);
-        else prefetch_entries<IdxT>(p, e0, e1 - e0, lane, 2, 3);
-    }
-    prefetch_tile(p, P0, true, lane, p.pstart[b + 1] - P0 == 1, p.bstart[b + 1] - p.bstart[b]);
+    const int P0 = p.pstart[b], T = p.pstart[b + 1] - P0;
+    const int o = p.bstart[b], d = p.bstart[b + 1] - o;
+    const int e0 = p.ent_off[P0], e1 = p.ent_off[P0 + 1];
+    warp_prefetch_l2(p.desc + P0, sizeof(SpkPanel) * T, p.piv + o, sizeof(int) * d, lane);
+    if (p.rows) warp_prefetch_l2(p.rmeta + (size_t)P0 * 64, 128 * (size_t)T, lane);
+    prefetch_entries<IdxT>(p, e0, e1 - e0, lane);
+    prefetch_tile(p, P0, true, lane, T == 1, d);
 }
 
 // One block's substitution M_b^-1: gather rhs[piv] from src, forward with
@@ -344,15 +354,15 @@ __device__ __forceinline__ void spk_solve_block(const SpkView& p, int b, int nex
         // next step's data into L2 while this one computes
         if (!lastp) {
             const int nl1 = dsh[t + 1].nl;
-            prefetch_entries<IdxT>(p, dsh[t + 1].off, ROWS ? 4 * (nl1 >> kRowQuadBits) : nl1, lane, 0, 1);
+            prefetch_entries<IdxT>(p, dsh[t + 1].off, ROWS ? 4 * (nl1 >> kRowQuadBits) : nl1, lane);
             prefetch_tile(p, P0 + t + 1, true, lane, t + 2 == T, d - 32 * (t + 1));
         } else if (T >= 2) {  // the backward pass starts at panel T-2
             const int nu1 = dsh[T - 2].nu;
-            prefetch_entries<IdxT>(p, dsh[T - 2].uoff, ROWS ? 4 * (nu1 >> kRowQuadBits) : nu1, lane, 0, 1);
+            prefetch_entries<IdxT>(p, dsh[T - 2].uoff, ROWS ? 4 * (nu1 >> kRowQuadBits) : nu1, lane);
             prefetch_tile(p, P0 + T - 2, false, lane);
         } else if (next_b >= 0) {
             prefetch_block_head<IdxT>(p, next_b, lane);
-            if (p.pf && lane == 5) src.prefetch(p.bstart[next_b], p.bstart[next_b + 1] - p.bstart[next_b]);
+            if (p.pf) src.prefetch(p.bstart[next_b], p.bstart[next_b + 1] - p.bstart[next_b], lane);
         }
         const float4* tile_f = reinterpret_cast<const float4*>(p.dtile + (size_t)(P0 + t) * kTileFloats);
         if (STAGE) {
@@ -399,11 +409,11 @@ __device__ __forceinline__ void spk_solve_block(const SpkView& p, int b, int nex
         const SpkPanel ds = dsh[t];
         if (t > 0) {
             const int nu1 = dsh[t - 1].nu;
-            prefetch_entries<IdxT>(p, dsh[t - 1].uoff, ROWS ? 4 * (nu1 >> kRowQuadBits) : nu1, lane, 0, 1);
+            prefetch_entries<IdxT>(p, dsh[t - 1].uoff, ROWS ? 4 * (nu1 >> kRowQuadBits) : nu1, lane);
             prefetch_tile(p, P0 + t - 1, false, lane);
         } else if (next_b >= 0) {
             prefetch_block_head<IdxT>(p, next_b, lane);
-            if (p.pf && lane == 5) src.prefetch(p.bstart[next_b], p.bstart[next_b + 1] - p.bstart[next_b]);
+            if (p.pf) src.prefetch(p.bstart[next_b], p.bstart[next_b + 1] - p.bstart[next_b], lane);
         }
         const float4* tile_b = reinterpret_cast<const float4*>(p.dtile + (size_t)(P0 + t) * kTileFloats);
         if (STAGE) {

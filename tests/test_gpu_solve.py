@@ -364,3 +364,28 @@ def test_textbook_mgs_matches_compact_wy_and_reference(ref, monkeypatch, nx):
         assert abs(its[orth] - r.total_iterations) <= max(1, 0.05 * r.total_iterations), (its, r.total_iterations)
         assert np.linalg.norm(res.x - r.x) / np.linalg.norm(r.x) <= 1e-8, orth
     assert abs(its["mgs"] - its["icwy"]) <= 1, its
+
+
+@pytest.mark.gpu
+def test_setup_rejects_non_bijective_permutation():
+    """permute_symmetric's bijection requirement (sparse_matrix.cpp:113-120):
+    a repeated or out-of-range target is rejected before any permutation
+    kernel runs (the check is a device pass over the permutation), and the
+    context stays usable for a valid partition afterwards."""
+    a = fx.laplacian_2d(20, 20)
+    n = a.n
+    ctx = hp.Context(0)
+    ctx.set_matrix(a)
+    good = hp.partition_graph(a, 10, 0.1)
+    dup = np.array(good.perm, dtype=np.int64)
+    dup[7] = dup[123]
+    oob = np.array(good.perm, dtype=np.int64)
+    oob[5] = n
+    for perm in (dup, oob):
+        bad = hp.Partition(good.num_blocks, good.assignment, perm, good.block_starts)
+        with pytest.raises(ValueError, match="bijection"):
+            ctx.bj_setup(bad, 1e-10)
+    ctx.bj_setup(good, 1e-10)
+    x, r = ctx.gmres(np.ones(n), hp.GmresConfig(restart_m=30, tol=1e-10, max_restarts=20))
+    assert r.converged
+    assert np.linalg.norm(np.asarray(fx.to_dense(a)) @ x - 1.0) <= 1e-8 * np.sqrt(n)
