@@ -292,6 +292,7 @@ struct PartWork {
     // refinement (parallel sweep)
     HBuf<uint8_t> spec;  // S per node
     HBuf<uint8_t> fl;
+    HBuf<uint64_t> fbits;
     // region growing
     HBuf<int32_t> aorder;
     HBuf<uint32_t> ell;
@@ -496,64 +497,75 @@ int64_t refine_sweep_par(const GraphView<Idx, Off>& g, S* state, int64_t* sizes,
     uint64_t cyc_dirty = 0, cyc_scan = 0;
     std::vector<int32_t> tch(max_degree(g) + 1);
     int64_t moves = 0;
+    // flagged nodes as a bitmap: phase 2 visits only them (set bits in
+    // ascending order; a dirty mark on a higher node of the same word is
+    // picked up by re-reading the word)
+    const int64_t nw = (n + 63) / 64;
+    fit(W.fbits, nw);
+    uint64_t* fb = W.fbits.data();
+#pragma omp parallel for schedule(static) num_threads(T)
+    for (int64_t w = 0; w < nw; ++w) {
+        uint64_t bits = 0;
+        const int64_t u0 = w * 64, ue = std::min<int64_t>(n, u0 + 64);
+        for (int64_t u = u0; u < ue; ++u) bits |= (uint64_t)(fl[u] != 0) << (u - u0);
+        fb[w] = bits;
+    }
     for (int t = 0; t < T; ++t) {
         const int32_t* r = rec[t].data();
         const int64_t a = lo[t], e = lo[t + 1];
-        int64_t u = a;
-        while (u < e) {
-            // skip 8 quiet nodes at a time
-            if (u + 8 <= e) {
-                uint64_t wd;
-                std::memcpy(&wd, &fl[u], 8);
-                if (wd == 0) {
-                    u += 8;
-                    continue;
+        if (a >= e) continue;
+        for (int64_t w = a >> 6; w <= (e - 1) >> 6; ++w) {
+            uint64_t win = ~0ull;
+            if (w == (a >> 6)) win &= ~0ull << (a & 63);
+            if (w == ((e - 1) >> 6)) win &= ~0ull >> (63 - ((e - 1) & 63));
+            uint64_t bits = fb[w] & win;
+            while (bits) {
+                const int i = __builtin_ctzll(bits);
+                const int64_t u = w * 64 + i;
+                const uint8_t f = fl[u];
+                const int32_t bu = state[u];
+                int32_t d = -1;
+                ndirty += (f & 4) != 0;
+                nrec += (f & 1) != 0;
+                if (f & 4) {
+                    const uint64_t c0 = dbg ? __rdtsc() : 0;
+                    d = refine_decide(g, state, sizes, cap, conn.data(), tch.data(), u);
+                    if (dbg) cyc_dirty += __rdtsc() - c0;
+                    if (f & 1) r += 1 + r[0];
+                } else if (f & 1) {
+                    const int nc = r[0];
+                    if (sizes[bu] > 1)
+                        for (int k = 1; k <= nc; ++k)
+                            if (sizes[r[k]] + 1 <= cap) {
+                                d = r[k];
+                                break;
+                            }
+                    r += 1 + nc;
                 }
-            }
-            const uint8_t f = fl[u];
-            if (!f) {
-                ++u;
-                continue;
-            }
-            const int32_t bu = state[u];
-            int32_t d = -1;
-            ndirty += (f & 4) != 0;
-            nrec += (f & 1) != 0;
-            if (f & 4) {
-                const uint64_t c0 = dbg ? __rdtsc() : 0;
-                d = refine_decide(g, state, sizes, cap, conn.data(), tch.data(), u);
-                if (dbg) cyc_dirty += __rdtsc() - c0;
-                if (f & 1) r += 1 + r[0];
-            } else if (f & 1) {
-                const int nc = r[0];
-                if (sizes[bu] > 1)
-                    for (int i = 1; i <= nc; ++i)
-                        if (sizes[r[i]] + 1 <= cap) {
-                            d = r[i];
-                            break;
+                const int32_t fin = d >= 0 ? d : bu;
+                if (d >= 0) {
+                    state[u] = (S)d;
+                    --sizes[bu];
+                    ++sizes[d];
+                    ++moves;
+                }
+                const bool same_diff = fin != (int32_t)spec[u];  // what later nodes of this range assumed
+                const bool cross_diff = (f & 2) && fin != bu;    // what later ranges assumed (the initial block)
+                nscan += same_diff || cross_diff;
+                if (same_diff || cross_diff) {
+                    const uint64_t c0 = dbg ? __rdtsc() : 0;
+                    for (Off k = st[u]; k < st[u + 1]; ++k) {
+                        const int64_t v = nb[k];
+                        if (v <= u) continue;
+                        if (v < e ? same_diff : cross_diff) {
+                            fl[v] |= 4;
+                            fb[v >> 6] |= 1ull << (v & 63);
                         }
-                r += 1 + nc;
-            }
-            const int32_t fin = d >= 0 ? d : bu;
-            if (d >= 0) {
-                state[u] = (S)d;
-                --sizes[bu];
-                ++sizes[d];
-                ++moves;
-            }
-            const bool same_diff = fin != (int32_t)spec[u];  // what later nodes of this range assumed
-            const bool cross_diff = (f & 2) && fin != bu;    // what later ranges assumed (the initial block)
-            nscan += same_diff || cross_diff;
-            if (same_diff || cross_diff) {
-                const uint64_t c0 = dbg ? __rdtsc() : 0;
-                for (Off k = st[u]; k < st[u + 1]; ++k) {
-                    const int64_t v = nb[k];
-                    if (v <= u) continue;
-                    if (v < e ? same_diff : cross_diff) fl[v] |= 4;
+                    }
+                    if (dbg) cyc_scan += __rdtsc() - c0;
                 }
-                if (dbg) cyc_scan += __rdtsc() - c0;
+                bits = i == 63 ? 0ull : fb[w] & win & (~0ull << (i + 1));
             }
-            ++u;
         }
     }
     if (getenv("HPBJ_DEBUG"))

@@ -6,8 +6,7 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-VARIANTS = [dict(), dict(HPBJ_GROW_PUSHPF="1"), dict(HPBJ_GROW_PUSHPF="1", HPBJ_GROW_PF="0"),
-            dict(HPBJ_GROW_PUSHPF="1", HPBJ_GROW_PF="24")]
+VARIANTS = [dict(), dict(HPBJ_GROW_PUSHPF="1"), dict(), dict(HPBJ_GROW_PUSHPF="1"), dict(HPBJ_GROW_PF="24")]
 for c in [int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "3,2,1").split(",")]:
     for v in VARIANTS:
         env = dict(os.environ, HPBJ_DEBUG="1", **v)
