@@ -21,12 +21,25 @@
 //    min-heap.
 //  * refinement: restated verbatim, same accumulation order (:117-141).
 //
-// Performance: int32 node ids, a packed per-node state word (block id, or
-// -1 unassigned / -2 queued) so each neighbour test is one random access,
-// software prefetch ahead of the BFS queue and of the refinement sweep, and
-// an OpenMP graph build that skips the transpose when the pattern is
-// structurally symmetric (MNA/mesh matrices are): the mirror value a_ji is
-// found by binary search in row j.
+// Performance (config 3, n = 4.1M, on the 16-core GPU-box host: 190 ms in
+// round 1, ~137 ms now; the reference's O(n*s) partitioner takes ~600 s):
+//  * region growing is one sequential BFS per block by the reference's
+//    semantics (a block's seed is the first node left free by every earlier
+//    block; measured: with even one block speculated ahead, 37% of the
+//    predictions fail, so it stays single-threaded). It reads fixed-stride
+//    8-id neighbour records (one cache line per popped node instead of the
+//    offset + adjacency lines of a CSR), prefetched 16 pops ahead, tests
+//    and sets a taken bitmap (n bits, cache resident), and appends popped
+//    nodes to a list; block ids are written from that list in parallel;
+//  * on large matrices without explicit off-diagonal zeros the BFS starts on
+//    A's own off-diagonal pattern while 8 other cores compute the weights
+//    (and with them the symmetry check) and the refinement view; an
+//    unsymmetric pattern abandons that BFS for the general path;
+//  * the refinement sweep runs as a parallel speculative phase over node
+//    ranges plus an exact in-order resolution (refine_sweep_par);
+//  * block ids are 16-bit when s fits (half the cache footprint of the
+//    refinement's random neighbour lookups); host buffers sit on
+//    transparent huge pages.
 
 #include <algorithm>
 #include <chrono>
@@ -618,17 +631,13 @@ void build_ell(int64_t n, uint32_t* ell, DegFn deg, NbrFn nbr) {
 struct GrowOpts {
     int ahead = 16;     // prefetch distance (popped nodes), fixed-stride records
     int ahead_csr = 6;  // the same with st + nb (two dependent lines per node)
-    bool defer = true;   // block ids written after growing (assignment-order list)
     int ell = -1;        // fixed-stride neighbour records (-1: for n >= 2^21)
     bool pf = true;
-    bool pushpf = false; // prefetch records when queued as well
 };
 inline GrowOpts grow_opts() {
     GrowOpts o;
     if (const char* e = getenv("HPBJ_GROW_PF")) o.ahead = o.ahead_csr = atoi(e);
-    if (const char* e = getenv("HPBJ_GROW_DEFER")) o.defer = atoi(e) != 0;
     if (const char* e = getenv("HPBJ_GROW_ELL")) o.ell = atoi(e);
-    if (const char* e = getenv("HPBJ_GROW_PUSHPF")) o.pushpf = atoi(e) != 0;
     return o;
 }
 
@@ -645,11 +654,10 @@ int64_t grow_blocks(const GraphView<Idx, Off>& g, const uint32_t* ell, const int
     const Idx* nb = g.idx;
     const int K = ELL ? go.ahead : go.ahead_csr;
     const bool pf = go.pf && n > (1 << 18) && K > 0;
-    int32_t* ao = nullptr;
-    if (go.defer) {
-        fit(aorder_buf, connected + 1);
-        ao = aorder_buf.data();
-    }
+    // popped nodes in order (a sequential stream); block ids are written
+    // from it afterwards in parallel instead of one random store per pop
+    fit(aorder_buf, connected + 1);
+    int32_t* ao = aorder_buf.data();
     int64_t fill = 0;
     int64_t cursor = 0;
     int64_t connected_left = connected;
@@ -670,7 +678,6 @@ int64_t grow_blocks(const GraphView<Idx, Off>& g, const uint32_t* ell, const int
         target = std::min(target, cap);
         int64_t head = 0, tail = 0;
         int64_t grown = 0;
-        const S bb = (S)b;
         while (grown < target) {
             if (head == tail) {  // queue empty: every taken node is assigned
                 while (cursor < connected && ((taken[order[cursor] >> 6] >> (order[cursor] & 63)) & 1ull)) ++cursor;
@@ -689,11 +696,9 @@ int64_t grow_blocks(const GraphView<Idx, Off>& g, const uint32_t* ell, const int
                 }
             }
             const int32_t u = queue[head++];
-            if (ao) ao[fill++] = u;
-            else state[u] = bb;
+            ao[fill++] = u;
             ++grown;
             --connected_left;
-            const int64_t tail0 = tail;
             if constexpr (ELL) {
                 const uint32_t* e = ell + (size_t)u * 8;
                 const uint32_t h = e[0];
@@ -724,15 +729,11 @@ int64_t grow_blocks(const GraphView<Idx, Off>& g, const uint32_t* ell, const int
             } else {
                 push_csr(u, tail);
             }
-            if constexpr (ELL) {  // records of the nodes just queued (popped a frontier later)
-                if (go.pushpf)
-                    for (int64_t q = tail0; q < tail; ++q) __builtin_prefetch(ell + (size_t)queue[q] * 8, 0, 3);
-            }
         }
         sizes[b] = grown;
         for (int64_t q = head; q < tail; ++q) taken[queue[q] >> 6] &= ~(1ull << (queue[q] & 63));  // queue.clear()
     }
-    if (ao) {  // block ids from the assignment-order list
+    {  // block ids from the assignment-order list
         std::vector<int64_t> off(b + 1, 0);
         for (int64_t i = 0; i < b; ++i) off[i + 1] = off[i] + sizes[i];
 #pragma omp parallel for schedule(dynamic, 64) if (n > 65536)
