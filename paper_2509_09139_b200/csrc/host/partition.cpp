@@ -337,6 +337,8 @@ struct GraphView {
 // The reference's decision for node u (partition.cpp:117-141) against a given
 // state: -2 skipped (source block of size <= 1), -1 stays, else the target
 // block. conn (all zero on entry and on exit) and tch are the caller's.
+constexpr int kSmallDeg = 16;
+
 template <class Idx, class Off, class S>
 inline int32_t refine_decide(const GraphView<Idx, Off>& g, const S* state, const int64_t* sizes, int64_t cap,
                              double* conn, int32_t* tch, int64_t u) {
@@ -353,8 +355,47 @@ inline int32_t refine_decide(const GraphView<Idx, Off>& g, const S* state, const
         while (k < ke && state[nb[k]] == bu) ++k;
         if (k == ke) return -1;
     }
+    const Off k0 = st[u], k1 = st[u + 1];
+    if (k1 - k0 <= kSmallDeg) {
+        // The touched blocks in first-touch order with their sums kept in
+        // registers instead of the s-long conn table (random accesses into
+        // it were most of a node's cost). Each sum starts at 0.0 and adds the
+        // weights in neighbour order, as conn[bv] does (partition.cpp:121-125).
+        // The reference lists a block once more if its sum returns to 0.0
+        // (w <= 0 edges of explicit graphs); such a repeat compares equal to
+        // its first occurrence and never changes the choice below.
+        int32_t blk[kSmallDeg];
+        double cw[kSmallDeg];
+        int nblk = 0;
+        for (Off k = k0; k < k1; ++k) {
+            const int32_t bv = state[nb[k]];
+            int j = 0;
+            while (j < nblk && blk[j] != bv) ++j;
+            if (j == nblk) {
+                blk[j] = bv;
+                cw[j] = 0.0;
+                ++nblk;
+            }
+            cw[j] += w[k];
+        }
+        int bi = -1;
+        double cbest = 0.0, cbu = 0.0;
+        for (int t = 0; t < nblk; ++t) {
+            const int32_t bv = blk[t];
+            if (bv == bu) {
+                cbu = cw[t];
+                continue;
+            }
+            if (sizes[bv] + 1 > cap) continue;
+            if (bi < 0 || cw[t] > cbest || (cw[t] == cbest && bv < blk[bi])) {
+                bi = t;
+                cbest = cw[t];
+            }
+        }
+        return (bi >= 0 && cbest > cbu) ? blk[bi] : -1;
+    }
     int nt = 0;
-    for (Off k = st[u]; k < st[u + 1]; ++k) {
+    for (Off k = k0; k < k1; ++k) {
         const int32_t bv = state[nb[k]];
         tch[nt] = bv;  // recorded while its conn is still 0.0 (partition.cpp:123-124)
         nt += conn[bv] == 0.0;
@@ -466,6 +507,59 @@ int64_t refine_sweep_par(const GraphView<Idx, Off>& g, S* state, int64_t* sizes,
             }
             fl[u] = cross ? 2 : 0;
             if (inter) continue;  // only bu touched: stays under any sizes
+            if (st[u + 1] - st[u] <= kSmallDeg) {  // sums in registers (see refine_decide)
+                int32_t blk[kSmallDeg];
+                double cw[kSmallDeg];
+                int nblk = 0;
+                for (Off k = st[u]; k < st[u + 1]; ++k) {
+                    const int64_t v = nb[k];
+                    const int32_t bv = (v >= a && v < e) ? (int32_t)spec[v] : (int32_t)state[v];
+                    int j = 0;
+                    while (j < nblk && blk[j] != bv) ++j;
+                    if (j == nblk) {
+                        blk[j] = bv;
+                        cw[j] = 0.0;
+                        ++nblk;
+                    }
+                    cw[j] += w[k];
+                }
+                double cbu = 0.0;
+                for (int t = 0; t < nblk; ++t)
+                    if (blk[t] == bu) cbu = cw[t];
+                bool nan = std::isnan(cbu);
+                int ci[kSmallDeg];
+                int nc = 0;
+                for (int t = 0; t < nblk; ++t) {
+                    nan |= std::isnan(cw[t]);
+                    if (blk[t] != bu && cw[t] > cbu) {  // insertion by (sum desc, block asc)
+                        int q = nc++;
+                        while (q > 0 && (cw[ci[q - 1]] < cw[t] || (cw[ci[q - 1]] == cw[t] && blk[ci[q - 1]] > blk[t]))) {
+                            ci[q] = ci[q - 1];
+                            --q;
+                        }
+                        ci[q] = t;
+                    }
+                }
+                if (nan) {  // NaN weights (explicit graphs): no total order; phase 2 decides it
+                    fl[u] |= 4;
+                    continue;
+                }
+                if (nc == 0) continue;
+                fl[u] |= 1;
+                R.push_back(nc);
+                for (int q = 0; q < nc; ++q) R.push_back(blk[ci[q]]);
+                if (sz[bu] <= 1) continue;  // speculative decision with this range's sizes
+                for (int q = 0; q < nc; ++q) {
+                    const int32_t bv = blk[ci[q]];
+                    if (sz[bv] + 1 <= cap) {
+                        spec[u] = (S)bv;
+                        --sz[bu];
+                        ++sz[bv];
+                        break;
+                    }
+                }
+                continue;
+            }
             tch.clear();
             for (Off k = st[u]; k < st[u + 1]; ++k) {
                 const int64_t v = nb[k];
