@@ -131,7 +131,7 @@ struct SpkView {
     int64_t n_entries;    // stored off-panel entries (arena sizes for L2 prefetch)
     int num_panels;
     int n;
-    int pf;               // L2 bulk prefetch of the next step's entries / tiles
+    int pf;               // L2 prefetch (per-line, warp-wide) of the next step's entries / tiles
 };
 
 void launch_spk_count(const SpkBuild& p, cudaStream_t st, int64_t* launches);
@@ -246,6 +246,7 @@ struct MgsLaunch {
     int scr = 0;
     bool w_in_smem = true;
     bool icwy = false;  // compact-WY (2 barriers/step) instead of textbook MGS (j+2)
+    int var = 0;        // textbook MGS launch shape (HPBJ_MGS_VAR, measurement)
 };
 
 constexpr int kMaxRestart = 128;  // compact-WY tables; textbook MGS has no limit
