@@ -158,13 +158,13 @@ __device__ void finish_step(const OrthArgs& a, double2* w2, double* scratch, int
 }
 
 // ---------------------------------------------------------------------------
-template <bool SMEM, int NT = kMgsThreads, int PRE = kMgsPre, int UNR = 4>
-__global__ void __launch_bounds__(NT, 1) k_mgs(OrthArgs a) {
+template <bool SMEM>
+__global__ void __launch_bounds__(kMgsThreads, 1) k_mgs(OrthArgs a) {
     SolveState* st = a.st;
     if (st->done) return;  // uniform: nothing writes done before the final barrier
     extern __shared__ __align__(16) double dsm_mgs[];
     double* wsh = dsm_mgs + a.scr;
-    __shared__ double red[2][NT / 32];
+    __shared__ double red[2][kMgsThreads / 32];
     __shared__ double bc[2];
 
     const int j = st->j;
@@ -190,8 +190,8 @@ __global__ void __launch_bounds__(NT, 1) k_mgs(OrthArgs a) {
         }
         __syncthreads();
         if (wid == 0) {
-            double t0 = lane < NT / 32 ? red[0][lane] : 0.0;
-            double t1 = lane < NT / 32 ? red[1][lane] : 0.0;
+            double t0 = lane < kMgsThreads / 32 ? red[0][lane] : 0.0;
+            double t1 = lane < kMgsThreads / 32 ? red[1][lane] : 0.0;
             t0 = warp_sum(t0);
             t1 = warp_sum(t1);
             if (lane == 0) {
@@ -211,14 +211,14 @@ __global__ void __launch_bounds__(NT, 1) k_mgs(OrthArgs a) {
         __syncthreads();
     };
 
-    // The first PRE loads of every pass's HBM vector are issued before
+    // The first kMgsPre loads of every pass's HBM vector are issued before
     // the previous pass's grid barrier, so they land while the CTA waits.
-    double2 pre[PRE];
+    double2 pre[kMgsPre];
     auto preload = [&](int i) {
         const double2* vi = reinterpret_cast<const double2*>(V + (size_t)i * ldv + r0);
 #pragma unroll
-        for (int g = 0; g < PRE; ++g) {
-            const int e = tid + g * NT;
+        for (int g = 0; g < kMgsPre; ++g) {
+            const int e = tid + g * kMgsThreads;
             pre[g] = e < nv2 ? __ldg(vi + e) : make_double2(0.0, 0.0);
         }
     };
@@ -227,8 +227,8 @@ __global__ void __launch_bounds__(NT, 1) k_mgs(OrthArgs a) {
     double ss = 0.0, dt = 0.0;
     {
         const double2* v0 = reinterpret_cast<const double2*>(V + r0);
-#pragma unroll UNR
-        for (int e = tid; e < nv2; e += NT) {
+#pragma unroll 4
+        for (int e = tid; e < nv2; e += kMgsThreads) {
             const double2 wv = __ldcg(win + e);
             const double2 vv = __ldg(v0 + e);
             if (SMEM) w2[e] = wv;
@@ -250,8 +250,8 @@ __global__ void __launch_bounds__(NT, 1) k_mgs(OrthArgs a) {
         const double2* vi = reinterpret_cast<const double2*>(V + (size_t)i * ldv + r0);
         dt = 0.0;
 #pragma unroll
-        for (int g = 0; g < PRE; ++g) {
-            const int e = tid + g * NT;
+        for (int g = 0; g < kMgsPre; ++g) {
+            const int e = tid + g * kMgsThreads;
             if (e < nv2) {
                 double2 wv = w2[e];
                 const double2 pv = __ldg(vp + e);
@@ -263,8 +263,8 @@ __global__ void __launch_bounds__(NT, 1) k_mgs(OrthArgs a) {
                 dt = fma(qv.y, wv.y, dt);
             }
         }
-#pragma unroll UNR
-        for (int e = tid + PRE * NT; e < nv2; e += NT) {
+#pragma unroll 4
+        for (int e = tid + kMgsPre * kMgsThreads; e < nv2; e += kMgsThreads) {
             double2 wv = w2[e];
             const double2 pv = __ldg(vp + e);
             const double2 qv = __ldg(vi + e);
@@ -284,8 +284,8 @@ __global__ void __launch_bounds__(NT, 1) k_mgs(OrthArgs a) {
     {
         const double2* vp = reinterpret_cast<const double2*>(V + (size_t)j * ldv + r0);
         ss = 0.0;
-#pragma unroll UNR
-        for (int e = tid; e < nv2; e += NT) {
+#pragma unroll 4
+        for (int e = tid; e < nv2; e += kMgsThreads) {
             double2 wv = w2[e];
             const double2 pv = __ldg(vp + e);
             wv.x = fma(-h, pv.x, wv.x);
@@ -296,7 +296,7 @@ __global__ void __launch_bounds__(NT, 1) k_mgs(OrthArgs a) {
         }
     }
     reduce2(ss, 0.0, (j + 1) & 1);
-    finish_step(a, w2, dsm_mgs, r0, nv2, j, pre_norm, sqrt(bc[0]), NT);
+    finish_step(a, w2, dsm_mgs, r0, nv2, j, pre_norm, sqrt(bc[0]), kMgsThreads);
 }
 
 // ---------------------------------------------------------------------------
@@ -554,8 +554,7 @@ MgsLaunch plan_mgs(int n, int num_sms, int m) {
     if (env && std::string(env) == "mgs") icwy = false;
     if (env && std::string(env) == "icwy" && m <= kMaxRestart) icwy = true;
     L.icwy = icwy;
-    if (const char* e = getenv("HPBJ_MGS_VAR")) L.var = atoi(e);
-    L.threads = icwy ? kIcwyThreads : (L.var == 1 ? 512 : kMgsThreads);
+    L.threads = icwy ? kIcwyThreads : kMgsThreads;
     const int min_rows = icwy ? 1024 : 4096;
     int grid = std::max(1, std::min(num_sms, (npad + min_rows - 1) / min_rows));
     int slice = (npad + grid - 1) / grid;
@@ -576,12 +575,7 @@ void launch_mgs(const MgsLaunch& L, const KrylovBufs& kb, double* gram, GridBarr
     OrthArgs a{kb, gram, sst, gb, n, L.slice, (n + 1) & ~1, cond, L.scr};
     void (*fn)(OrthArgs);
     if (L.icwy) fn = L.w_in_smem ? k_icwy<true> : k_icwy<false>;
-    else if (!L.w_in_smem) fn = k_mgs<false>;
-    else if (L.var == 1) fn = k_mgs<true, 512, 8, 8>;
-    else if (L.var == 2) fn = k_mgs<true, 1024, 6, 4>;
-    else if (L.var == 3) fn = k_mgs<true, 1024, 4, 8>;
-    else if (L.var == 4) fn = k_mgs<true, 512, 4, 8>;
-    else fn = k_mgs<true>;
+    else fn = L.w_in_smem ? k_mgs<true> : k_mgs<false>;
     if (L.smem > 48 * 1024)
         HPBJ_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem));
     // cooperative attribute: co-residency guaranteed, capturable into graphs

@@ -246,7 +246,6 @@ struct MgsLaunch {
     int scr = 0;
     bool w_in_smem = true;
     bool icwy = false;  // compact-WY (2 barriers/step) instead of textbook MGS (j+2)
-    int var = 0;        // textbook MGS launch shape (HPBJ_MGS_VAR, measurement)
 };
 
 constexpr int kMaxRestart = 128;  // compact-WY tables; textbook MGS has no limit
