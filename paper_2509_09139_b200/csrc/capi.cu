@@ -5,6 +5,10 @@
 
 #include <algorithm>
 #include <chrono>
+#include <exception>
+#include <thread>
+
+#include <omp.h>
 #include <cmath>
 #include <cstdlib>
 #include <cstdio>
@@ -160,6 +164,10 @@ constexpr int kPcNone = 0, kPcBJ = 1, kPcIlu = 2, kPcIdentity = 3;
 struct hpbj_ctx {
     Pool pool;  // destroyed last
     Slots slots;
+    // hpbj_set_matrix_async: the staging + copy-out runs here; every later
+    // entry point joins it first (and reports its error)
+    std::thread bg;
+    std::exception_ptr bg_err;
     int device = 0;
     int num_sms = 148;
     cudaStream_t stream = nullptr;
@@ -275,6 +283,7 @@ struct hpbj_ctx {
     hpbj_kernel_stat stats[HPBJ_K_COUNT] = {};
 
     ~hpbj_ctx() {
+        if (bg.joinable()) bg.join();
         t_pool = &pool;
         t_slots = &slots;
         if (graph_exec) cudaGraphExecDestroy(graph_exec);
@@ -1039,6 +1048,21 @@ void solve(hpbj_ctx* c, const double* d_b, double* d_x, const hpbj_gmres_opts* o
 }  // namespace
 
 // ============================================================================
+// guard() for context entry points: a pending hpbj_set_matrix_async is
+// finished first and its error, if any, becomes this call's.
+template <class F>
+int cguard(hpbj_ctx* ctx, F&& f) {
+    return guard(&ctx->err, [&] {
+        if (ctx->bg.joinable()) ctx->bg.join();
+        if (ctx->bg_err) {
+            std::exception_ptr e = ctx->bg_err;
+            ctx->bg_err = nullptr;
+            std::rethrow_exception(e);
+        }
+        f();
+    });
+}
+
 extern "C" {
 
 int hpbj_create(hpbj_ctx** out, int device) {
@@ -1086,7 +1110,7 @@ int hpbj_get_kernel_stats(hpbj_ctx* ctx, hpbj_kernel_stat* out) {
     if (!ctx || !out) return HPBJ_EINVAL;
     t_pool = &ctx->pool;
     t_slots = &ctx->slots;
-    return guard(&ctx->err, [&] {
+    return cguard(ctx, [&] {
         for (int k = 0; k < HPBJ_K_COUNT; ++k) {
             out[k] = ctx->stats[k];
             out[k].bytes_per_launch = out[k].launches ? out[k].total_bytes / (double)out[k].launches : 0.0;
@@ -1106,60 +1130,89 @@ int hpbj_set_fused(hpbj_ctx* ctx, int enable) {
     return HPBJ_OK;
 }
 
+// The matrix after validation: int64 -> int32 indices and the FP64 values
+// straight into pinned staging (nthr threads), asynchronous copies on the
+// context stream, the SpMV plan.
+static void set_matrix_stage(hpbj_ctx* ctx, int64_t n, const int64_t* row_ptr, const int64_t* col, const double* val,
+                             int nthr) {
+    const auto t1 = std::chrono::steady_clock::now();
+    HPBJ_CUDA(cudaSetDevice(ctx->device));
+    ctx->release_matrix();
+    ctx->release_ws();
+    const int ni = (int)n, nnz = (int)row_ptr[n];
+    const size_t b_rp = sizeof(int) * ((size_t)ni + 1), b_ci = sizeof(int) * (size_t)nnz;
+    const size_t o_ci = (b_rp + 15) & ~(size_t)15, o_val = (o_ci + b_ci + 15) & ~(size_t)15;
+    char* stg = static_cast<char*>(ctx->stage_mat.get(o_val + sizeof(double) * (size_t)nnz));
+    int* rp = reinterpret_cast<int*>(stg);
+    int* ci = reinterpret_cast<int*>(stg + o_ci);
+    double* vs = reinterpret_cast<double*>(stg + o_val);
+    if ((int64_t)ctx->h_rp.size() < n + 1) ctx->h_rp.resize(n + 1);
+    int* hrp = ctx->h_rp.data();
+#pragma omp parallel num_threads(nthr)
+    {
+#pragma omp for schedule(static) nowait
+        for (int64_t i = 0; i <= n; ++i) rp[i] = hrp[i] = (int)row_ptr[i];
+#pragma omp for schedule(static) nowait
+        for (int64_t k = 0; k < nnz; ++k) ci[k] = (int)col[k];
+#pragma omp for schedule(static)
+        for (int64_t k = 0; k < nnz; ++k) vs[k] = val[k];
+    }
+    const auto t2 = std::chrono::steady_clock::now();
+    ctx->A.n = ni;
+    ctx->A.nnz = nnz;
+    dslot(ctx->A.rp, ni + 1);
+    dslot(ctx->A.ci, nnz);
+    dslot(ctx->A.val, nnz);
+    cudaStream_t st = ctx->stream;
+    HPBJ_CUDA(cudaMemcpyAsync(ctx->A.rp, rp, b_rp, cudaMemcpyHostToDevice, st));
+    HPBJ_CUDA(cudaMemcpyAsync(ctx->A.ci, ci, b_ci, cudaMemcpyHostToDevice, st));
+    HPBJ_CUDA(cudaMemcpyAsync(ctx->A.val, vs, sizeof(double) * (size_t)nnz, cudaMemcpyHostToDevice, st));
+    ctx->stage_mat.fence(st);  // later work on the stream is ordered after the copies
+    const auto t3 = std::chrono::steady_clock::now();
+    make_plan(ctx->planA, ctx->h_rp.data(), ni);
+    dslot(ctx->d_tmpx, ni);
+    dslot(ctx->d_tmpy, ni);
+    ctx->has_matrix = true;
+    if (getenv("HPBJ_DEBUG")) {
+        auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+        fprintf(stderr, "[hpbj] set_matrix: stage %.1f alloc+enqueue %.1f plan %.1f ms\n", ms(t1, t2), ms(t2, t3),
+                ms(t3, std::chrono::steady_clock::now()));
+    }
+}
+
+static void check_matrix_args(int64_t n, const int64_t* row_ptr, const int64_t* col, const double* val) {
+    check_csr(n, row_ptr, col, val);
+    if (n >= (int64_t)INT32_MAX || row_ptr[n] >= (int64_t)INT32_MAX) fail(HPBJ_EINVAL, "hpbj: n and nnz must be < 2^31");
+}
+
 int hpbj_set_matrix(hpbj_ctx* ctx, int64_t n, const int64_t* row_ptr, const int64_t* col, const double* val) {
     if (!ctx) return HPBJ_EINVAL;
     t_pool = &ctx->pool;
     t_slots = &ctx->slots;
-    return guard(&ctx->err, [&] {
-        const auto t0 = std::chrono::steady_clock::now();
-        check_csr(n, row_ptr, col, val);
-        if (n >= (int64_t)INT32_MAX || row_ptr[n] >= (int64_t)INT32_MAX)
-            fail(HPBJ_EINVAL, "hpbj: n and nnz must be < 2^31");
-        const auto t1 = std::chrono::steady_clock::now();
-        HPBJ_CUDA(cudaSetDevice(ctx->device));
-        ctx->release_matrix();
-        ctx->release_ws();
-        const int ni = (int)n, nnz = (int)row_ptr[n];
-        // int64 -> int32 indices and the FP64 values straight into pinned
-        // staging (parallel), then asynchronous copies on the context stream
-        const size_t b_rp = sizeof(int) * ((size_t)ni + 1), b_ci = sizeof(int) * (size_t)nnz;
-        const size_t o_ci = (b_rp + 15) & ~(size_t)15, o_val = (o_ci + b_ci + 15) & ~(size_t)15;
-        char* stg = static_cast<char*>(ctx->stage_mat.get(o_val + sizeof(double) * (size_t)nnz));
-        int* rp = reinterpret_cast<int*>(stg);
-        int* ci = reinterpret_cast<int*>(stg + o_ci);
-        double* vs = reinterpret_cast<double*>(stg + o_val);
-        if ((int64_t)ctx->h_rp.size() < n + 1) ctx->h_rp.resize(n + 1);
-        int* hrp = ctx->h_rp.data();
-#pragma omp parallel
-        {
-#pragma omp for schedule(static) nowait
-            for (int64_t i = 0; i <= n; ++i) rp[i] = hrp[i] = (int)row_ptr[i];
-#pragma omp for schedule(static) nowait
-            for (int64_t k = 0; k < nnz; ++k) ci[k] = (int)col[k];
-#pragma omp for schedule(static)
-            for (int64_t k = 0; k < nnz; ++k) vs[k] = val[k];
-        }
-        const auto t2 = std::chrono::steady_clock::now();
-        ctx->A.n = ni;
-        ctx->A.nnz = nnz;
-        dslot(ctx->A.rp, ni + 1);
-        dslot(ctx->A.ci, nnz);
-        dslot(ctx->A.val, nnz);
-        cudaStream_t st = ctx->stream;
-        HPBJ_CUDA(cudaMemcpyAsync(ctx->A.rp, rp, b_rp, cudaMemcpyHostToDevice, st));
-        HPBJ_CUDA(cudaMemcpyAsync(ctx->A.ci, ci, b_ci, cudaMemcpyHostToDevice, st));
-        HPBJ_CUDA(cudaMemcpyAsync(ctx->A.val, vs, sizeof(double) * (size_t)nnz, cudaMemcpyHostToDevice, st));
-        ctx->stage_mat.fence(st);  // later work on the stream is ordered after the copies
-        const auto t3 = std::chrono::steady_clock::now();
-        make_plan(ctx->planA, ctx->h_rp.data(), ni);
-        dslot(ctx->d_tmpx, ni);
-        dslot(ctx->d_tmpy, ni);
-        ctx->has_matrix = true;
-        if (getenv("HPBJ_DEBUG")) {
-            auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
-            fprintf(stderr, "[hpbj] set_matrix: check %.1f stage %.1f alloc+enqueue %.1f plan %.1f ms\n", ms(t0, t1),
-                    ms(t1, t2), ms(t2, t3), ms(t3, std::chrono::steady_clock::now()));
-        }
+    return cguard(ctx, [&] {
+        check_matrix_args(n, row_ptr, col, val);
+        set_matrix_stage(ctx, n, row_ptr, col, val, omp_get_max_threads());
+    });
+}
+
+int hpbj_set_matrix_async(hpbj_ctx* ctx, int64_t n, const int64_t* row_ptr, const int64_t* col, const double* val) {
+    if (!ctx) return HPBJ_EINVAL;
+    t_pool = &ctx->pool;
+    t_slots = &ctx->slots;
+    return cguard(ctx, [&] {
+        check_matrix_args(n, row_ptr, col, val);
+        ctx->has_matrix = false;
+        // a third of the cores: the caller's partitioner runs meanwhile
+        const int nthr = std::max(1, omp_get_max_threads() / 3);
+        ctx->bg = std::thread([ctx, n, row_ptr, col, val, nthr] {
+            t_pool = &ctx->pool;
+            t_slots = &ctx->slots;
+            try {
+                set_matrix_stage(ctx, n, row_ptr, col, val, nthr);
+            } catch (...) {
+                ctx->bg_err = std::current_exception();
+            }
+        });
     });
 }
 
@@ -1167,7 +1220,7 @@ int hpbj_update_values(hpbj_ctx* ctx, const double* val) {
     if (!ctx) return HPBJ_EINVAL;
     t_pool = &ctx->pool;
     t_slots = &ctx->slots;
-    return guard(&ctx->err, [&] {
+    return cguard(ctx, [&] {
         if (!ctx->has_matrix) fail(HPBJ_ELOGIC, "update_values: no matrix");
         HPBJ_CUDA(cudaMemcpyAsync(ctx->A.val, val, sizeof(double) * ctx->A.nnz, cudaMemcpyHostToDevice,
                                   ctx->stream));
@@ -1186,7 +1239,7 @@ int hpbj_spmv(hpbj_ctx* ctx, const double* x, double* y) {
     if (!ctx) return HPBJ_EINVAL;
     t_pool = &ctx->pool;
     t_slots = &ctx->slots;
-    return guard(&ctx->err, [&] {
+    return cguard(ctx, [&] {
         if (!ctx->has_matrix) fail(HPBJ_ELOGIC, "spmv: no matrix");
         const int n = ctx->A.n;
         HPBJ_CUDA(cudaMemcpyAsync(ctx->d_tmpx, x, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
@@ -1205,7 +1258,7 @@ int hpbj_bj_setup(hpbj_ctx* ctx, int64_t s, const int64_t* perm, const int64_t* 
     }
     t_pool = &ctx->pool;
     t_slots = &ctx->slots;
-    return guard(&ctx->err, [&] {
+    return cguard(ctx, [&] {
         if (!ctx->has_matrix) fail(HPBJ_ELOGIC, "block_jacobi: no matrix");
         if (eps_pivot < 0.0) fail(HPBJ_EINVAL, "gp_lu: negative eps_pivot");
         const bool dbg = getenv("HPBJ_DEBUG") != nullptr;
@@ -1371,7 +1424,7 @@ int hpbj_bj_refactor(hpbj_ctx* ctx, hpbj_setup_info* info) {
     }
     t_pool = &ctx->pool;
     t_slots = &ctx->slots;
-    return guard(&ctx->err, [&] {
+    return cguard(ctx, [&] {
         if (!ctx->d_fac) fail(HPBJ_ELOGIC, "refactor: no block-Jacobi partition set up");
         ctx->has_pc = true;
         ctx->active = kPcBJ;
@@ -1383,7 +1436,7 @@ int hpbj_bj_apply(hpbj_ctx* ctx, const double* v, double* z) {
     if (!ctx) return HPBJ_EINVAL;
     t_pool = &ctx->pool;
     t_slots = &ctx->slots;
-    return guard(&ctx->err, [&] {
+    return cguard(ctx, [&] {
         if (!ctx->has_pc) fail(HPBJ_ELOGIC, "apply: block-Jacobi preconditioner not set up");
         const int n = ctx->A.n;
         cudaStream_t st = ctx->stream;
@@ -1404,7 +1457,7 @@ int hpbj_ilu0_setup(hpbj_ctx* ctx, hpbj_setup_info* info) {
     }
     t_pool = &ctx->pool;
     t_slots = &ctx->slots;
-    return guard(&ctx->err, [&] {
+    return cguard(ctx, [&] {
         if (!ctx->has_matrix) fail(HPBJ_ELOGIC, "ilu0: no matrix");
         const int n = ctx->A.n;
         const int64_t nnz = ctx->A.nnz;
@@ -1466,7 +1519,7 @@ int hpbj_identity_setup(hpbj_ctx* ctx) {
     if (!ctx) return HPBJ_EINVAL;
     t_pool = &ctx->pool;
     t_slots = &ctx->slots;
-    return guard(&ctx->err, [&] {
+    return cguard(ctx, [&] {
         if (!ctx->has_matrix) fail(HPBJ_ELOGIC, "identity: no matrix");
         dslot(ctx->d_ilu_z, ((size_t)ctx->A.n + 31) / 32 * 32);
         ctx->active = kPcIdentity;
@@ -1478,7 +1531,7 @@ int hpbj_precond_apply(hpbj_ctx* ctx, const double* v, double* z) {
     if (ctx->active == kPcBJ) return hpbj_bj_apply(ctx, v, z);
     t_pool = &ctx->pool;
     t_slots = &ctx->slots;
-    return guard(&ctx->err, [&] {
+    return cguard(ctx, [&] {
         if (ctx->active == kPcNone) fail(HPBJ_ELOGIC, "apply: no preconditioner set up");
         const int n = ctx->A.n;
         cudaStream_t st = ctx->stream;
@@ -1495,7 +1548,7 @@ int hpbj_precond_apply(hpbj_ctx* ctx, const double* v, double* z) {
 
 int hpbj_get_ilu0_values(hpbj_ctx* ctx, double* lu) {
     if (!ctx) return HPBJ_EINVAL;
-    return guard(&ctx->err, [&] {
+    return cguard(ctx, [&] {
         if (!ctx->has_ilu) fail(HPBJ_ELOGIC, "ilu0: factors not set up");
         HPBJ_CUDA(cudaMemcpy(lu, ctx->d_ilu_lu, sizeof(double) * ctx->A.nnz, cudaMemcpyDeviceToHost));
     });
@@ -1503,7 +1556,7 @@ int hpbj_get_ilu0_values(hpbj_ctx* ctx, double* lu) {
 
 int hpbj_bj_set_neumann_order(hpbj_ctx* ctx, int order) {
     if (!ctx) return HPBJ_EINVAL;
-    return guard(&ctx->err, [&] {
+    return cguard(ctx, [&] {
         ctx->neumann = order;  // <= 0: direct block solves (gmres.cpp:93 tests > 0)
     });
 }
@@ -1512,7 +1565,7 @@ int hpbj_bj_apply_neumann(hpbj_ctx* ctx, const double* v, double* z, int k) {
     if (!ctx) return HPBJ_EINVAL;
     t_pool = &ctx->pool;
     t_slots = &ctx->slots;
-    return guard(&ctx->err, [&] {
+    return cguard(ctx, [&] {
         if (!ctx->has_pc) fail(HPBJ_ELOGIC, "apply_neumann: block factors not available");
         if (k < 0 || k > ctx->neumann)
             fail(HPBJ_EINVAL, "apply_neumann: order exceeds the one the preconditioner was built with");
@@ -1540,7 +1593,7 @@ int hpbj_get_block_factors(hpbj_ctx* ctx, int64_t block, int64_t* dim, float* f,
     if (!ctx) return HPBJ_EINVAL;
     t_pool = &ctx->pool;
     t_slots = &ctx->slots;
-    return guard(&ctx->err, [&] {
+    return cguard(ctx, [&] {
         if (!ctx->has_pc) fail(HPBJ_ELOGIC, "factors: block-Jacobi preconditioner not set up");
         if (block < 0 || block >= ctx->s) fail(HPBJ_ERANGE, "factors: block index out of range");
         const int o = ctx->h_bstart[block];
@@ -1567,7 +1620,7 @@ int hpbj_get_block_diagnostics(hpbj_ctx* ctx, double* cond_estimate, double* err
     if (!ctx) return HPBJ_EINVAL;
     t_pool = &ctx->pool;
     t_slots = &ctx->slots;
-    return guard(&ctx->err, [&] {
+    return cguard(ctx, [&] {
         if (!ctx->has_pc) fail(HPBJ_ELOGIC, "diagnostics: block-Jacobi preconditioner not set up");
         if (!ctx->diag_valid) {
             dslot(ctx->d_cond, ctx->s);
@@ -1591,7 +1644,7 @@ int hpbj_get_block_stats(hpbj_ctx* ctx, int64_t* dims, int64_t* perturbations) {
     if (!ctx) return HPBJ_EINVAL;
     t_pool = &ctx->pool;
     t_slots = &ctx->slots;
-    return guard(&ctx->err, [&] {
+    return cguard(ctx, [&] {
         if (!ctx->has_pc) fail(HPBJ_ELOGIC, "stats: block-Jacobi preconditioner not set up");
         std::vector<int> pc(ctx->s);
         HPBJ_CUDA(cudaMemcpy(pc.data(), ctx->d_pert_count, sizeof(int) * ctx->s, cudaMemcpyDeviceToHost));
@@ -1618,7 +1671,7 @@ int hpbj_gmres(hpbj_ctx* ctx, const double* b, double* x, const hpbj_gmres_opts*
     if (!ctx) return HPBJ_EINVAL;
     t_pool = &ctx->pool;
     t_slots = &ctx->slots;
-    return guard(&ctx->err, [&] {
+    return cguard(ctx, [&] {
         if (!ctx->has_matrix) fail(HPBJ_ELOGIC, "gmres: no matrix");
         const int n = ctx->A.n;
         ensure_ws(ctx, (int)checked_opts(opts).restart_m);
@@ -1641,7 +1694,7 @@ int hpbj_gmres_device(hpbj_ctx* ctx, const double* d_b, double* d_x, const hpbj_
     if (!ctx) return HPBJ_EINVAL;
     t_pool = &ctx->pool;
     t_slots = &ctx->slots;
-    return guard(&ctx->err, [&] { solve(ctx, d_b, d_x, opts, rep, hist, hist_cap, cycle_res, cyc_cap); });
+    return cguard(ctx, [&] { solve(ctx, d_b, d_x, opts, rep, hist, hist_cap, cycle_res, cyc_cap); });
 }
 
 }  // extern "C"
