@@ -962,7 +962,6 @@ __host__ __device__ inline size_t ll_smem_bytes(int dhi) {
            + (size_t)(dhi > 32 ? dhi - 32 : 1) * 32 * sizeof(float)  // Lb: rows 32.. of L_{Q-1}
            + (size_t)2 * 32 * 32 * sizeof(float)            // L11 of two panels
            + (size_t)2 * NW * 32 * sizeof(float)            // candidate rows (double buffered)
-           + (size_t)2 * NW * 4 * sizeof(int)               // candidate key / row / owner
            + (size_t)lr * sizeof(short)                     // row id of every L_Q row
            + (size_t)(T > 1 ? T - 1 : 1) * dhi * sizeof(short)  // position of row r in L_Q
            + (size_t)3 * dhi * sizeof(short)                // ppos, act, prow
@@ -1076,8 +1075,7 @@ __global__ void __launch_bounds__(kLlThreads, kLlCtasPerSm) k_block_lu_ll(LuPara
     float* Lb = X + (size_t)dhi * kXld;                        // [dhi-32][32]
     float* L11 = Lb + (size_t)(dhi > 32 ? dhi - 32 : 1) * 32;  // [2][32][32]
     float* cand_v = L11 + 2 * 32 * 32;                         // [2][NW][32]
-    int* cand_i = reinterpret_cast<int*>(cand_v + 2 * NW * 32);  // [2][NW][4]: key, row, owner
-    short* rowQ = reinterpret_cast<short*>(cand_i + 2 * NW * 4);  // [lrmax]
+    short* rowQ = reinterpret_cast<short*>(cand_v + 2 * NW * 32);  // [lrmax]
     short* posQ = rowQ + lrmax;                                // [Tmax-1][dhi]
     short* ppos = posQ + (size_t)(Tmax > 1 ? Tmax - 1 : 1) * dhi;  // pivot position of row r (or 0x7fff)
     short* act = ppos + dhi;                                   // active rows (stable order)
@@ -1086,6 +1084,7 @@ __global__ void __launch_bounds__(kLlThreads, kLlCtasPerSm) k_block_lu_ll(LuPara
     __shared__ double redd[NW];
     __shared__ int lofs[16];                                   // first L row of panel Q
     __shared__ int nact_sh;
+    __shared__ unsigned long long piv_best[3];                  // column winners (panel factorisation)
     float* Lg = p.scratch + (size_t)blockIdx.x * lrmax * 32;   // this CTA's L_Q rows
 
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -1143,6 +1142,7 @@ __global__ void __launch_bounds__(kLlThreads, kLlCtasPerSm) k_block_lu_ll(LuPara
                 acc += d - 32 * q;
             }
         }
+        if (tid < 3) piv_best[tid] = 0ull;
         __syncthreads();
         double norm = 0.0;
 #pragma unroll
@@ -1153,6 +1153,8 @@ __global__ void __launch_bounds__(kLlThreads, kLlCtasPerSm) k_block_lu_ll(LuPara
         int nperturb = 0;
         bool abort = false;
         int buf = 0;
+        int pb = 0;  // piv_best slot of the next column (warps that drop out of the
+                     // panel factorisation do not return before the next block)
         for (int P = 0; P < T; ++P) {
             unsigned long long tp0 = 0;
             if (p.prof && tid == 0) tp0 = clock64();
@@ -1292,7 +1294,9 @@ __global__ void __launch_bounds__(kLlThreads, kLlCtasPerSm) k_block_lu_ll(LuPara
                         const int wr = warp_pivot_row(key, key ? brow : 0x7fffffff, &kmx);
                         const unsigned own = __ballot_sync(0xffffffffu, key != 0u && key == kmx && brow == wr);
                         float* cv = cand_v + (size_t)(buf * NW + wid) * 32;
-                        int* ci4 = cand_i + (buf * NW + wid) * 4;
+                        // each warp's candidate meets the others in one 64-bit shared
+                        // atomic max: key, then the smaller row (0xFFFF - row), then
+                        // the owning thread slot (unique per row)
                         if (own && lane == __ffs(own) - 1) {
 #pragma unroll
                             for (int i = 0; i < RPT; ++i)
@@ -1301,20 +1305,19 @@ __global__ void __launch_bounds__(kLlThreads, kLlCtasPerSm) k_block_lu_ll(LuPara
                                     for (int q = 0; q < W / 4; ++q)
                                         reinterpret_cast<float4*>(cv)[q] = make_float4(rv[i][4 * q], rv[i][4 * q + 1],
                                                                                        rv[i][4 * q + 2], rv[i][4 * q + 3]);
-                            reinterpret_cast<int4*>(ci4)[0] = make_int4((int)kmx, wr, tid + NT * bi, 0);
-                        } else if (lane == 0 && !own) {
-                            reinterpret_cast<int4*>(ci4)[0] = make_int4(0, 0x7fffffff, -1, 0);
+                            atomicMax(&piv_best[pb], ((unsigned long long)kmx << 32) |
+                                                         ((unsigned long long)(0xFFFF - wr) << 16) |
+                                                         (unsigned long long)(tid + NT * bi));
                         }
                         bar_named(1, nwa * 32);
-                        // winner over the active warps' candidates (warp-wide, identical in every warp)
-                        const int4 cw = lane < nwa ? reinterpret_cast<const int4*>(cand_i + buf * NW * 4)[lane]
-                                                   : make_int4(0, 0x7fffffff, -1, 0);
-                        unsigned kk;
-                        const int frow =
-                            warp_pivot_row((unsigned)cw.x, lane < nwa && cw.x != 0 ? cw.y : 0x7fffffff, &kk);
-                        const int fw =
-                            __ffs(__ballot_sync(0xffffffffu, lane < nwa && (unsigned)cw.x == kk && cw.y == frow)) - 1;
-                        const int owner = __shfl_sync(0xffffffffu, cw.z, fw);  // tid + NT * row slot
+                        const unsigned long long wv = piv_best[pb];
+                        // the previous column's slot is read by now: clear it for the
+                        // column after next (three slots)
+                        if (tid == 0) piv_best[pb == 0 ? 2 : pb - 1] = 0ull;
+                        pb = pb == 2 ? 0 : pb + 1;
+                        const int frow = 0xFFFF - (int)((wv >> 16) & 0xFFFFu);
+                        const int owner = (int)(wv & 0xFFFFu);  // tid + NT * row slot
+                        const int fw = (owner % NT) >> 5;
                         const float4* Pv4 = reinterpret_cast<const float4*>(cand_v + (size_t)(buf * NW + fw) * 32);
                         buf ^= 1;
                         // regularize_pivot (lu.cpp:10-20), identical in every thread;
