@@ -36,6 +36,10 @@ namespace {
 using namespace spk;
 
 constexpr int kWarpsPerCta = 4;
+// tile pass, per warp: the tile as FP64 [32][kTdLd] (even stride: 16-byte
+// aligned pairs) + an FP32 [32][33] transpose buffer
+constexpr int kTdLd = 34;
+constexpr int kTileWarpDoubles = 32 * kTdLd + (32 * 33 + 1) / 2;
 // pack pass, per warp: the slot starts of the longest row-quad part
 __host__ __device__ inline int pack_slot_ints(int dmax) { return ((dmax + 3) / 4 + 4) & ~3; }
 
@@ -125,11 +129,13 @@ __device__ __forceinline__ void spk_tile(const SpkBuild& p, const float* F, int 
     // its forward and backward in-panel solves are back to back (no U
     // entries right of it), so the apply does them as one mat-vec.
     {
-        // tile (FP32 factor values, exact in FP64) and a transpose buffer
-        // in shared memory; the column of the inverse a lane computes
-        // stays in registers (fully unrolled substitutions)
-        float* Tt = reinterpret_cast<float*>(inv_smem) + (size_t)(threadIdx.x >> 5) * (2 * 32 * 33);
-        float* W = Tt + 32 * 33;
+        // tile (FP32 factor values, held as FP64 — exact — so the
+        // substitutions read each operand with one broadcast load, two per
+        // LDS.128, and no conversion) and an FP32 transpose buffer in shared
+        // memory; the column of the inverse a lane computes stays in
+        // registers (fully unrolled substitutions, two partial sums per row)
+        double* Td = reinterpret_cast<double*>(inv_smem) + (size_t)(threadIdx.x >> 5) * kTileWarpDoubles;
+        float* W = reinterpret_cast<float*>(Td + 32 * kTdLd);
         for (int q = 0; q < 8; ++q) {
             const float4 v4 = (k < d && c0 + 4 * q < c1) ? dense_quad(F, dq, k, (c0 >> 2) + q)
                                                          : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -138,7 +144,7 @@ __device__ __forceinline__ void spk_tile(const SpkBuild& p, const float* F, int 
             for (int u = 0; u < 4; ++u) {
                 const int c = 4 * q + u;
                 // padded rows/columns: identity
-                Tt[lane * 33 + c] = (k < d && c0 + c < c1) ? fv[u] : ((c == lane) ? 1.0f : 0.0f);
+                Td[lane * kTdLd + c] = (k < d && c0 + c < c1) ? (double)fv[u] : ((c == lane) ? 1.0 : 0.0);
             }
         }
         __syncwarp();
@@ -147,10 +153,15 @@ __device__ __forceinline__ void spk_tile(const SpkBuild& p, const float* F, int 
         double x[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) {  // L x = e_c, unit lower
-            double sum = (i == c) ? 1.0 : 0.0;
+            double s0 = (i == c) ? 1.0 : 0.0, s1 = 0.0;
 #pragma unroll
-            for (int j = 0; j < i; ++j) sum -= (double)Tt[i * 33 + j] * x[j];
-            x[i] = (i < c) ? 0.0 : sum;
+            for (int j = 0; j + 1 < i; j += 2) {
+                const double2 t = *reinterpret_cast<const double2*>(Td + i * kTdLd + j);
+                s0 -= t.x * x[j];
+                s1 -= t.y * x[j + 1];
+            }
+            if (i & 1) s0 -= Td[i * kTdLd + i - 1] * x[i - 1];
+            x[i] = (i < c) ? 0.0 : s0 + s1;
         }
         float4* tile = reinterpret_cast<float4*>(p.dtile + (size_t)P * kTileFloats);
         const int qd = lane >> 2;  // the quad holding the diagonal
@@ -174,10 +185,19 @@ __device__ __forceinline__ void spk_tile(const SpkBuild& p, const float* F, int 
         // in place (x = Uinv Linv = (L U)^-1 of the diagonal tile)
 #pragma unroll
         for (int i = 31; i >= 0; --i) {
-            double sum = last ? x[i] : ((i == c) ? 1.0 : 0.0);
+            double s0 = last ? x[i] : ((i == c) ? 1.0 : 0.0), s1 = 0.0;
+            int j = i + 1;
+            if (j & 1) {
+                if (j < 32) s0 -= Td[i * kTdLd + j] * x[j];
+                ++j;
+            }
 #pragma unroll
-            for (int j = i + 1; j < 32; ++j) sum -= (double)Tt[i * 33 + j] * x[j];
-            x[i] = (!last && i > c) ? 0.0 : sum / (double)Tt[i * 33 + i];
+            for (; j + 1 < 32; j += 2) {
+                const double2 t = *reinterpret_cast<const double2*>(Td + i * kTdLd + j);
+                s0 -= t.x * x[j];
+                s1 -= t.y * x[j + 1];
+            }
+            x[i] = (!last && i > c) ? 0.0 : (s0 + s1) / Td[i * kTdLd + i];
         }
 #pragma unroll
         for (int i = 0; i < 32; ++i) W[i * 33 + c] = (float)x[i];  // row `lane`: W[lane * 33 + j]
@@ -383,7 +403,7 @@ void launch_spk_count(const SpkBuild& p, cudaStream_t st, int64_t* launches) {
     k_spk_build<kSpkCount, uint16_t><<<grid, 256, 0, st>>>(p);
     // the tiles depend on the panel owners only
     const int tgrid = std::max(1, std::min((p.num_panels * 32 + 127) / 128, 148 * 16));
-    const int tsmem = 4 * 2 * 32 * 33 * sizeof(float);
+    const int tsmem = 4 * kTileWarpDoubles * sizeof(double);
     HPBJ_CUDA(cudaFuncSetAttribute(k_spk_build<kSpkTile, uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, tsmem));
     k_spk_build<kSpkTile, uint16_t><<<tgrid, 128, tsmem, st>>>(p);
     *launches += 3;
