@@ -156,13 +156,6 @@ int hpbj_partition_from_assignment(int64_t n, const int64_t* assignment, int64_t
  * invariants checked as sparse_matrix.cpp:14-50). Copies to the device. */
 int hpbj_set_matrix(hpbj_ctx* ctx, int64_t n, const int64_t* row_ptr, const int64_t* col,
                     const double* val);
-/* The same, returning after the validation: the staging and the host ->
- * device copies continue on a context worker thread (overlapping e.g. the
- * caller's partition_graph). The three arrays must stay valid and unmodified
- * until the next call on this context returns; that call finishes the work
- * first and reports its error, if any. */
-int hpbj_set_matrix_async(hpbj_ctx* ctx, int64_t n, const int64_t* row_ptr, const int64_t* col,
-                          const double* val);
 /* New values, same pattern (transient Newton sequence, config 4). */
 int hpbj_update_values(hpbj_ctx* ctx, const double* val);
 /* spmv<double> (spmv.hpp:31-47), original ordering, host buffers. */

@@ -359,12 +359,8 @@ class Context:
             _raise(rc, self.lib.hpbj_last_error(self.h).decode(), info)
 
     def set_matrix(self, a: SparseMatrix):
-        """Validates A and returns; the staging and the host -> device copies
-        finish on a context worker thread (hpbj_set_matrix_async), overlapping
-        e.g. partition_graph. `a` is kept alive until then."""
-        self.check(self.lib.hpbj_set_matrix_async(self.h, a.n, _p(a.row_starts, _abi.i64p),
-                                                  _p(a.col_indices, _abi.i64p), _p(a.values, _abi.f64p)))
-        self._staged = a
+        self.check(self.lib.hpbj_set_matrix(self.h, a.n, _p(a.row_starts, _abi.i64p), _p(a.col_indices, _abi.i64p),
+                                            _p(a.values, _abi.f64p)))
 
     def update_values(self, values):
         v = _f64(values)

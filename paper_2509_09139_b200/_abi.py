@@ -115,7 +115,6 @@ SIGNATURES = {
     "hpbj_partition_adjacency": (ctypes.c_int, [i64, i64p, i64p, f64p, i64, f64, i64p, i64p, i64p]),
     "hpbj_partition_from_assignment": (ctypes.c_int, [i64, i64p, i64, i64p, i64p]),
     "hpbj_set_matrix": (ctypes.c_int, [vp, i64, i64p, i64p, f64p]),
-    "hpbj_set_matrix_async": (ctypes.c_int, [vp, i64, i64p, i64p, f64p]),
     "hpbj_update_values": (ctypes.c_int, [vp, f64p]),
     "hpbj_spmv": (ctypes.c_int, [vp, f64p, f64p]),
     "hpbj_bj_setup": (ctypes.c_int, [vp, i64, i64p, i64p, f64, ctypes.POINTER(SetupInfo)]),

@@ -5,8 +5,6 @@
 
 #include <algorithm>
 #include <chrono>
-#include <exception>
-#include <thread>
 
 #include <omp.h>
 #include <cmath>
@@ -164,10 +162,6 @@ constexpr int kPcNone = 0, kPcBJ = 1, kPcIlu = 2, kPcIdentity = 3;
 struct hpbj_ctx {
     Pool pool;  // destroyed last
     Slots slots;
-    // hpbj_set_matrix_async: the staging + copy-out runs here; every later
-    // entry point joins it first (and reports its error)
-    std::thread bg;
-    std::exception_ptr bg_err;
     int device = 0;
     int num_sms = 148;
     cudaStream_t stream = nullptr;
@@ -283,7 +277,6 @@ struct hpbj_ctx {
     hpbj_kernel_stat stats[HPBJ_K_COUNT] = {};
 
     ~hpbj_ctx() {
-        if (bg.joinable()) bg.join();
         t_pool = &pool;
         t_slots = &slots;
         if (graph_exec) cudaGraphExecDestroy(graph_exec);
@@ -1048,19 +1041,10 @@ void solve(hpbj_ctx* c, const double* d_b, double* d_x, const hpbj_gmres_opts* o
 }  // namespace
 
 // ============================================================================
-// guard() for context entry points: a pending hpbj_set_matrix_async is
-// finished first and its error, if any, becomes this call's.
+// guard() for context entry points (errors land in the context's slot).
 template <class F>
 int cguard(hpbj_ctx* ctx, F&& f) {
-    return guard(&ctx->err, [&] {
-        if (ctx->bg.joinable()) ctx->bg.join();
-        if (ctx->bg_err) {
-            std::exception_ptr e = ctx->bg_err;
-            ctx->bg_err = nullptr;
-            std::rethrow_exception(e);
-        }
-        f();
-    });
+    return guard(&ctx->err, std::forward<F>(f));
 }
 
 extern "C" {
@@ -1132,7 +1116,9 @@ int hpbj_set_fused(hpbj_ctx* ctx, int enable) {
 
 // The matrix after validation: int64 -> int32 indices and the FP64 values
 // straight into pinned staging (nthr threads), asynchronous copies on the
-// context stream, the SpMV plan.
+// context stream (they overlap the caller's partition_graph), the SpMV plan.
+// (Staging on a worker thread during partition_graph was measured: no gain —
+// the partitioner's latency-bound BFS slows down by about the time saved.)
 static void set_matrix_stage(hpbj_ctx* ctx, int64_t n, const int64_t* row_ptr, const int64_t* col, const double* val,
                              int nthr) {
     const auto t1 = std::chrono::steady_clock::now();
@@ -1192,27 +1178,6 @@ int hpbj_set_matrix(hpbj_ctx* ctx, int64_t n, const int64_t* row_ptr, const int6
     return cguard(ctx, [&] {
         check_matrix_args(n, row_ptr, col, val);
         set_matrix_stage(ctx, n, row_ptr, col, val, omp_get_max_threads());
-    });
-}
-
-int hpbj_set_matrix_async(hpbj_ctx* ctx, int64_t n, const int64_t* row_ptr, const int64_t* col, const double* val) {
-    if (!ctx) return HPBJ_EINVAL;
-    t_pool = &ctx->pool;
-    t_slots = &ctx->slots;
-    return cguard(ctx, [&] {
-        check_matrix_args(n, row_ptr, col, val);
-        ctx->has_matrix = false;
-        // a third of the cores: the caller's partitioner runs meanwhile
-        const int nthr = std::max(1, omp_get_max_threads() / 3);
-        ctx->bg = std::thread([ctx, n, row_ptr, col, val, nthr] {
-            t_pool = &ctx->pool;
-            t_slots = &ctx->slots;
-            try {
-                set_matrix_stage(ctx, n, row_ptr, col, val, nthr);
-            } catch (...) {
-                ctx->bg_err = std::current_exception();
-            }
-        });
     });
 }
 

@@ -389,36 +389,3 @@ def test_setup_rejects_non_bijective_permutation():
     x, r = ctx.gmres(np.ones(n), hp.GmresConfig(restart_m=30, tol=1e-10, max_restarts=20))
     assert r.converged
     assert np.linalg.norm(np.asarray(fx.to_dense(a)) @ x - 1.0) <= 1e-8 * np.sqrt(n)
-
-
-@pytest.mark.gpu
-def test_async_set_matrix_is_joined_by_the_next_call():
-    """hpbj_set_matrix_async (Context.set_matrix) validates synchronously and
-    stages + copies on the context's worker thread; the next entry point
-    finishes it first. Replacing the matrix while a copy is pending, destroying
-    a context with one pending, and the synchronous entry point all give the
-    same solve."""
-    a = fx.laplacian_2d(30, 30)
-    b = np.linspace(1.0, 2.0, a.n)
-    cfg = hp.GmresConfig(restart_m=30, tol=1e-10, max_restarts=40)
-    part = hp.partition_graph(a, 9, 0.1)
-    c0 = hp.Context(0)
-    c0.set_matrix(fx.laplacian_2d(12, 12))  # pending, then destroyed
-    del c0
-    with pytest.raises(ValueError):  # validation errors are reported at once
-        hp.Context(0).set_matrix(hp.SparseMatrix(3, [0, 1, 2, 1], [0, 1, 2], [1.0, 1.0, 1.0]))
-    xs = []
-    for mode in ("async", "replace", "sync"):
-        ctx = hp.Context(0)
-        if mode == "replace":
-            ctx.set_matrix(fx.laplacian_2d(20, 20))
-        if mode == "sync":
-            ctx.check(ctx.lib.hpbj_set_matrix(ctx.h, a.n, hp._p(a.row_starts, hp._abi.i64p),
-                                              hp._p(a.col_indices, hp._abi.i64p), hp._p(a.values, hp._abi.f64p)))
-        else:
-            ctx.set_matrix(a)
-        ctx.bj_setup(part, 1e-10)
-        x, rep = ctx.gmres(b, cfg)
-        assert rep.converged
-        xs.append(x)
-    assert np.array_equal(xs[0], xs[1]) and np.array_equal(xs[0], xs[2])
