@@ -327,7 +327,15 @@ def test_region_growing_variants_match_reference(ref, monkeypatch, env):
     r, c, v = zip(*t)
     unsym = hp.SparseMatrix.from_triplets(r, c, v, n)
     hub = fx.random_dd(500, 9, 4)
-    cases = [(fx.laplacian_2d(40, 40), 25, 0.1), (_mesh3d_long_range(14, 30, 4), 11, 0.1),
+    # isolated nodes (diagonal-only rows) and two components
+    lap = fx.laplacian_2d(12, 12)
+    n2 = lap.n + 20
+    rr = np.repeat(np.arange(lap.n), np.diff(lap.row_starts))
+    r2 = np.concatenate([rr, np.arange(lap.n, n2)])
+    c2 = np.concatenate([np.asarray(lap.col_indices), np.arange(lap.n, n2)])
+    v2 = np.concatenate([np.asarray(lap.values), np.full(20, 3.0)])
+    iso = hp.SparseMatrix.from_triplets(r2, c2, v2, n2)
+    cases = [(fx.laplacian_2d(40, 40), 25, 0.1), (_mesh3d_long_range(14, 30, 4), 11, 0.1), (iso, 7, 0.1),
              (hub, 20, 0.1), (_with_zero_entries(fx.laplacian_2d(30, 30), 1), 16, 0.1),
              (_with_zero_entries(_mesh3d_long_range(10, 20, 2), 3), 9, 0.0), (unsym, 10, 0.1)]
     for a, s, tol in cases:
