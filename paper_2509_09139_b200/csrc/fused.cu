@@ -243,8 +243,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_arnoldi_cycle(FusedArgs a) {
     // warp slots run across the CTAs first (slot = wid * G + cta), so the
     // apply's blocks — and their factor traffic — spread over every SM
     // instead of filling the first CTAs' warps (per-SM bandwidth bound)
+    // (plan_fused guarantees G * kWarps - 1 >= the number of blocks: one block per apply warp)
     const int gw = wid * G + blockIdx.x;  // 0: the Givens warp (CTA 0, warp 0)
-    const int naw = G * kWarps - 1;       // >= number of blocks (plan_fused): one block per apply warp
     if (gw != 0 && gw - 1 < a.pc.s) spk::spk_cache_block<ROWS>(a.pc, gw - 1, dsh, msh, bcache, lane);
     const double bdf = st->breakdown_factor;
     const double* asrc = V;  // v_0 (k_cycle_init)
