@@ -348,3 +348,49 @@ def test_block_condition_estimates_match_reference(ref, shape):
     assert np.allclose(cond, rc, rtol=1e-4), (cond, rc)
     assert np.allclose(eb, reb, rtol=2e-4)
     assert np.all(cond >= 1.0)
+
+
+def test_left_looking_lu_regularises_and_reports_singular_like_reference(ref):
+    """Blocks of 96 < d <= 288 (the left-looking kernel) with tiny and exactly
+    zero pivots: Eq. 7 regularisation (lu.cpp:10-20) with the reference's
+    perturbation records and factors, and with eps_pivot = 0 the reference's
+    SingularBlockError (lu.cpp:190-195) naming the column."""
+    rng = np.random.default_rng(11)
+    d, nb = 140, 3
+    rows, cols, vals = [], [], []
+    for blk in range(nb):
+        o = blk * d
+        for i in range(d):
+            js = rng.choice(d, 6, replace=False)
+            for j in js:
+                if j != i:
+                    rows.append(o + i), cols.append(o + int(j)), vals.append(float(rng.uniform(-1, 1)))
+            rows.append(o + i), cols.append(o + i), vals.append(8.0)
+    r, c, v = np.array(rows), np.array(cols), np.array(vals)
+    # block 1: column 7 keeps only its rows above the diagonal and a 1e-14
+    # diagonal; block 2: column 11 structurally empty (no update reaches it:
+    # a zero pivot)
+    o1, o2 = d, 2 * d
+    v[(r == o1 + 7) & (c == o1 + 7)] = 1e-14
+    keep = ~((r >= o1 + 7) & (r < o1 + d) & (c == o1 + 7) & (r != o1 + 7))
+    keep &= ~((c == o2 + 11) & (r >= o2) & (r < o2 + d))
+    r, c, v = r[keep], c[keep], v[keep]
+    a = hp.SparseMatrix.from_triplets(r, c, v, nb * d)
+    asg = np.repeat(np.arange(nb), d)
+    part = hp.partition_from_assignment(asg, nb)
+    p = hp.Preconditioner.block_jacobi(a, part)
+    dims, f32, _, piv_ref, pert_ref = ref.factors(a.row_starts, a.col_indices, a.values, nb, asg)
+    st = p.stats(False)
+    assert [x["perturbation_count"] for x in st] == list(pert_ref)
+    assert sum(pert_ref) >= 2
+    offs = np.concatenate([[0], np.cumsum(dims * dims)])
+    for b in range(nb):
+        F, piv = p.block_factors(b)
+        Fr = f32[offs[b]:offs[b + 1]].reshape(d, d).astype(np.float64)
+        assert np.array_equal(piv, piv_ref[b * d:(b + 1) * d]), b
+        assert np.linalg.norm(F.astype(np.float64) - Fr) <= 1e-5 * np.linalg.norm(Fr), b
+    with pytest.raises(hp.SingularBlockError) as ei:
+        hp.Preconditioner.block_jacobi(a, part, hp.BlockJacobiOptions(eps_pivot=0.0))
+    assert ei.value.column() >= 0
+    with pytest.raises(Exception):  # the reference refuses the same matrix
+        ref.factors(a.row_starts, a.col_indices, a.values, nb, asg, eps=0.0)
