@@ -165,6 +165,8 @@ struct hpbj_ctx {
     int device = 0;
     int num_sms = 148;
     cudaStream_t stream = nullptr;
+    cudaStream_t side = nullptr;      // SPK tile pass, concurrent with the count/pack passes
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     std::string err;
     int64_t launches = 0;
 
@@ -284,6 +286,9 @@ struct hpbj_ctx {
         if (d_lu_prof) cudaFree(d_lu_prof);
         release_matrix();
         release_ws();
+        if (ev_fork) cudaEventDestroy(ev_fork);
+        if (ev_join) cudaEventDestroy(ev_join);
+        if (side) cudaStreamDestroy(side);
         if (stream) cudaStreamDestroy(stream);
     }
 
@@ -497,6 +502,12 @@ void build_spk(hpbj_ctx* c) {
     p.dtile = c->d_dtile;
     p.dmax = c->dmax;
     launch_spk_count(p, st, &c->launches);
+    // the tile inverses (latency bound) run on the side stream while the
+    // count result comes back and the pack pass (bandwidth bound) runs here
+    HPBJ_CUDA(cudaEventRecord(c->ev_fork, st));
+    HPBJ_CUDA(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+    launch_spk_tile(p, c->side, &c->launches);
+    HPBJ_CUDA(cudaEventRecord(c->ev_join, c->side));
     // Off-panel layout: row quads (fold_rows: one coalesced quad per row and
     // slot, ~3x fewer fold instructions than the segmented fold) for blocks
     // deeper than the fused cycle kernel takes (it folds row-sorted runs),
@@ -536,6 +547,7 @@ void build_spk(hpbj_ctx* c) {
         c->spk_tile_bytes += 16.0 * (288.0 * (T - 1) + (double)r * ((r + 3) / 4));
     }
     launch_spk_pack(p, st, &c->launches);
+    HPBJ_CUDA(cudaStreamWaitEvent(st, c->ev_join, 0));  // everything after the build sees the tiles
 }
 
 void factor(hpbj_ctx* c, hpbj_setup_info* info) {
@@ -1065,6 +1077,9 @@ int hpbj_create(hpbj_ctx** out, int device) {
         c->device = device;
         c->num_sms = prop.multiProcessorCount;
         HPBJ_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        HPBJ_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+        HPBJ_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+        HPBJ_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
         const char* ng = getenv("HPBJ_NOGRAPH");
         c->use_graph = !(ng && ng[0] == '1');
         const char* nf = getenv("HPBJ_FUSED");

@@ -135,6 +135,7 @@ struct SpkView {
 };
 
 void launch_spk_count(const SpkBuild& p, cudaStream_t st, int64_t* launches);
+void launch_spk_tile(const SpkBuild& p, cudaStream_t st, int64_t* launches);
 void launch_spk_pack(const SpkBuild& p, cudaStream_t st, int64_t* launches);
 // Arnoldi step: z32 = M^-1 V[:, st->j] (FP32 arithmetic, column resolved on the device).
 void launch_apply_step(const SpkView& v, const double* V, int ldv, const SolveState* sst, float* z32,

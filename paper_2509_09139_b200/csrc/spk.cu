@@ -401,12 +401,18 @@ void launch_spk_count(const SpkBuild& p, cudaStream_t st, int64_t* launches) {
     const int grid = std::max(1, std::min((p.num_panels * 32 + 255) / 256, 148 * 16));
     HPBJ_CUDA(cudaMemsetAsync(p.totals, 0, 2 * sizeof(unsigned long long), st));
     k_spk_build<kSpkCount, uint16_t><<<grid, 256, 0, st>>>(p);
-    // the tiles depend on the panel owners only
+    *launches += 2;
+    HPBJ_CUDA(cudaGetLastError());
+}
+
+// The diagonal-tile inverses: depend on the dense panels and the panel
+// owners only (launch after launch_spk_count, possibly on another stream).
+void launch_spk_tile(const SpkBuild& p, cudaStream_t st, int64_t* launches) {
     const int tgrid = std::max(1, std::min((p.num_panels * 32 + 127) / 128, 148 * 16));
     const int tsmem = 4 * kTileWarpDoubles * sizeof(double);
     HPBJ_CUDA(cudaFuncSetAttribute(k_spk_build<kSpkTile, uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, tsmem));
     k_spk_build<kSpkTile, uint16_t><<<tgrid, 128, tsmem, st>>>(p);
-    *launches += 3;
+    *launches += 1;
     HPBJ_CUDA(cudaGetLastError());
 }
 
