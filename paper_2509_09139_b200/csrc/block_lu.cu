@@ -1097,7 +1097,15 @@ __global__ void __launch_bounds__(kLlThreads, kLlCtasPerSm) k_block_lu_ll(LuPara
     __syncthreads();
     unsigned nb_issue = 0, n11_issue[2] = {0u, 0u};  // completed-phase counters (uniform)
 
-    for (int b = blockIdx.x; b < p.s; b += gridDim.x) {
+    // dynamic schedule: a CTA takes the next unclaimed block (static striding
+    // left the CTAs with the most expensive block mixes ~10% behind)
+    __shared__ int next_b;
+    for (;;) {
+        __syncthreads();
+        if (tid == 0) next_b = atomicAdd(p.next_block, 1);
+        __syncthreads();
+        const int b = next_b;
+        if (b >= p.s) break;
         const int o = p.bstart[b];
         const int d = p.bstart[b + 1] - o;
         if (d <= dlo || d > dhi) continue;
@@ -1562,6 +1570,7 @@ void launch_block_lu(const LuParams& p_in, int dmax, int num_sms, cudaStream_t s
             void (*fn)(LuParams, int, int) = k_block_lu_ll<2>;
             HPBJ_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             const int grid = std::min(p.s, num_sms * kLlCtasPerSm);
+            HPBJ_CUDA(cudaMemsetAsync(p.next_block, 0, sizeof(int), st));
             fn<<<grid, kLlThreads, smem, st>>>(p, dw, dhi);
             *launches += 1;
             dll = dhi;

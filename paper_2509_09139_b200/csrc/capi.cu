@@ -215,6 +215,7 @@ struct hpbj_ctx {
     bool diag_valid = false;
     PertRecord* d_pert = nullptr;
     int* d_pert_n = nullptr;
+    int* d_lu_next = nullptr;       // left-looking LU: next block to take (dynamic schedule)
     unsigned long long* d_singular = nullptr;
     float* d_lu_scratch = nullptr;
     int lu_smem_dim = 0, lu_scratch_ld = 0;
@@ -566,6 +567,7 @@ void factor(hpbj_ctx* c, hpbj_setup_info* info) {
     p.pert_count = c->d_pert_count;
     p.pert = c->d_pert;
     p.pert_n = c->d_pert_n;
+    p.next_block = c->d_lu_next;
     p.pert_cap = 4096;
     p.singular = c->d_singular;
     p.eps = c->eps;
@@ -1330,6 +1332,7 @@ int hpbj_bj_setup(hpbj_ctx* ctx, int64_t s, const int64_t* perm, const int64_t* 
         dslot(ctx->d_pert_count, s);
         dslot(ctx->d_pert, 4096);
         dslot(ctx->d_pert_n, 1);
+        dslot(ctx->d_lu_next, 1);
         dslot(ctx->d_singular, 1);
         const int np = ctx->num_panels;
         dslot(ctx->d_pstart, s + 1);

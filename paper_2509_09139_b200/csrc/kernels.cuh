@@ -58,6 +58,7 @@ struct LuParams {
     int smem_dim;           // blocks with dim <= smem_dim factor in shared memory
     int scratch_ld;
     int warp_dim = 0;       // blocks with dim <= warp_dim: one warp per block (set by the launcher)
+    int* next_block = nullptr;  // left-looking LU: block counter (zeroed by the launcher)
 };
 
 // Packed factor layout: block b with dim d, T = ceil(d/32)
