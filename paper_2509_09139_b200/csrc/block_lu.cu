@@ -1097,15 +1097,16 @@ __global__ void __launch_bounds__(kLlThreads, kLlCtasPerSm) k_block_lu_ll(LuPara
     __syncthreads();
     unsigned nb_issue = 0, n11_issue[2] = {0u, 0u};  // completed-phase counters (uniform)
 
-    // dynamic schedule: a CTA takes the next unclaimed block (static striding
-    // left the CTAs with the most expensive block mixes ~10% behind)
+    // dynamic schedule, largest blocks first: a CTA takes the next unclaimed
+    // block (static striding left the CTAs with the most expensive block
+    // mixes behind; the small blocks at the end even out the tail)
     __shared__ int next_b;
     for (;;) {
         __syncthreads();
         if (tid == 0) next_b = atomicAdd(p.next_block, 1);
         __syncthreads();
-        const int b = next_b;
-        if (b >= p.s) break;
+        if (next_b >= p.s) break;
+        const int b = p.block_order ? p.block_order[next_b] : next_b;
         const int o = p.bstart[b];
         const int d = p.bstart[b + 1] - o;
         if (d <= dlo || d > dhi) continue;

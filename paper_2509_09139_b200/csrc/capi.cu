@@ -216,6 +216,8 @@ struct hpbj_ctx {
     PertRecord* d_pert = nullptr;
     int* d_pert_n = nullptr;
     int* d_lu_next = nullptr;       // left-looking LU: next block to take (dynamic schedule)
+    int* d_lu_order = nullptr;      // blocks by decreasing size (largest first)
+    std::vector<int> h_lu_order;
     unsigned long long* d_singular = nullptr;
     float* d_lu_scratch = nullptr;
     int lu_smem_dim = 0, lu_scratch_ld = 0;
@@ -568,6 +570,7 @@ void factor(hpbj_ctx* c, hpbj_setup_info* info) {
     p.pert = c->d_pert;
     p.pert_n = c->d_pert_n;
     p.next_block = c->d_lu_next;
+    p.block_order = c->d_lu_order;
     p.pert_cap = 4096;
     p.singular = c->d_singular;
     p.eps = c->eps;
@@ -1347,6 +1350,20 @@ int hpbj_bj_setup(hpbj_ctx* ctx, int64_t s, const int64_t* perm, const int64_t* 
         dslot(ctx->d_desc, np);
         dslot(ctx->d_dtile, (size_t)np * kTileFloats);
         HPBJ_CUDA(cudaMemcpyAsync(ctx->d_pstart, hps.data(), sizeof(int) * (s + 1), cudaMemcpyHostToDevice, st));
+        {  // LU schedule: largest blocks first (counting sort on the size, stable)
+            std::vector<int>& ord = ctx->h_lu_order;
+            ord.resize(s);
+            std::vector<int> cnt(dmax + 2, 0);
+            for (int64_t b = 0; b < s; ++b) ++cnt[dmax - (bst[b + 1] - bst[b])];
+            for (int k = 0, acc = 0; k <= dmax; ++k) {
+                const int c0 = cnt[k];
+                cnt[k] = acc;
+                acc += c0;
+            }
+            for (int64_t b = 0; b < s; ++b) ord[cnt[dmax - (bst[b + 1] - bst[b])]++] = (int)b;
+            dslot(ctx->d_lu_order, s);
+            HPBJ_CUDA(cudaMemcpyAsync(ctx->d_lu_order, ord.data(), sizeof(int) * s, cudaMemcpyHostToDevice, st));
+        }
         const size_t scr = block_lu_scratch_floats(dmax, ctx->num_sms, &ctx->lu_smem_dim, &ctx->lu_scratch_ld);
         if (scr) dslot(ctx->d_lu_scratch, scr);
         HPBJ_CUDA(cudaMemcpyAsync(ctx->d_perm, hperm.data(), sizeof(int) * n, cudaMemcpyHostToDevice, st));

@@ -59,6 +59,7 @@ struct LuParams {
     int scratch_ld;
     int warp_dim = 0;       // blocks with dim <= warp_dim: one warp per block (set by the launcher)
     int* next_block = nullptr;  // left-looking LU: block counter (zeroed by the launcher)
+    const int* block_order = nullptr;  // its schedule (largest blocks first), or null: index order
 };
 
 // Packed factor layout: block b with dim d, T = ceil(d/32)
