@@ -70,6 +70,7 @@ struct OrthArgs {
     int npad;            // n rounded up to even (vectors zero padded)
     cudaGraphConditionalHandle cond;  // Arnoldi WHILE node (0: not in a graph)
     int scr;             // doubles of Givens scratch at the front of the dynamic smem (>= 3m+2, even)
+    unsigned long long* prof;  // HPBJ_MGS_PROF=1: per CTA [stream, CTA reduce, grid barrier, broadcast, passes] cycles
 };
 
 // Shared finish of a step: normalise, Hessenberg column, Givens, exit flags.
@@ -181,6 +182,8 @@ __global__ void __launch_bounds__(kMgsThreads, 1) k_mgs(OrthArgs a) {
     const double2* win = reinterpret_cast<const double2*>(a.kb.w + r0);
     const double* V = a.kb.V;
 
+    unsigned long long pacc[5] = {0, 0, 0, 0, 0};
+    long long tp = a.prof ? clock64() : 0;
     auto reduce2 = [&](double x0, double x1, int parity) {
         x0 = warp_sum(x0);
         x1 = warp_sum(x1);
@@ -189,6 +192,11 @@ __global__ void __launch_bounds__(kMgsThreads, 1) k_mgs(OrthArgs a) {
             red[1][wid] = x1;
         }
         __syncthreads();
+        long long t1 = 0;
+        if (a.prof) {
+            t1 = clock64();
+            pacc[0] += t1 - tp;
+        }
         if (wid == 0) {
             double t0 = lane < kMgsThreads / 32 ? red[0][lane] : 0.0;
             double t1 = lane < kMgsThreads / 32 ? red[1][lane] : 0.0;
@@ -199,16 +207,23 @@ __global__ void __launch_bounds__(kMgsThreads, 1) k_mgs(OrthArgs a) {
                 P[(parity * 2 + 1) * G + blockIdx.x] = t1;
             }
         }
+        long long t2 = 0;
+        if (a.prof) t2 = clock64();
         grid_barrier(a.gb);
-        if (wid == 0) {
-            const double t0 = sum_partials(P + (parity * 2 + 0) * G, G);
-            const double t1 = sum_partials(P + (parity * 2 + 1) * G, G);
-            if (lane == 0) {
-                bc[0] = t0;
-                bc[1] = t1;
-            }
+        long long t3 = 0;
+        if (a.prof) t3 = clock64();
+        if (wid < 2) {  // the two totals by two warps at once
+            const double t = sum_partials(P + (parity * 2 + wid) * G, G);
+            if (lane == 0) bc[wid] = t;
         }
         __syncthreads();
+        if (a.prof) {
+            tp = clock64();
+            pacc[1] += t2 - t1;
+            pacc[2] += t3 - t2;
+            pacc[3] += tp - t3;
+            pacc[4] += 1;
+        }
     };
 
     // The first kMgsPre loads of every pass's HBM vector are issued before
@@ -296,6 +311,8 @@ __global__ void __launch_bounds__(kMgsThreads, 1) k_mgs(OrthArgs a) {
         }
     }
     reduce2(ss, 0.0, (j + 1) & 1);
+    if (a.prof && tid == 0)
+        for (int k = 0; k < 5; ++k) atomicAdd(a.prof + (size_t)blockIdx.x * 5 + k, pacc[k]);
     finish_step(a, w2, dsm_mgs, r0, nv2, j, pre_norm, sqrt(bc[0]), kMgsThreads);
 }
 
@@ -392,7 +409,7 @@ __global__ void __launch_bounds__(kIcwyThreads, 1) k_icwy(OrthArgs a) {
         for (int u = 0; u < 4; ++u) {  // all loads of four values in flight together
             const int t = t0 + u * kIcwyWarps;
             if (t < nval)
-                for (int b = lane; b < G; b += 32) part[u] += __ldcg(P + (size_t)t * G + b);
+                part[u] = lane_sum_partials(P + (size_t)t * G, G);
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -572,7 +589,14 @@ MgsLaunch plan_mgs(int n, int num_sms, int m) {
 
 void launch_mgs(const MgsLaunch& L, const KrylovBufs& kb, double* gram, GridBarrier* gb, SolveState* sst,
                 int n, cudaGraphConditionalHandle cond, cudaStream_t st, int64_t* launches) {
-    OrthArgs a{kb, gram, sst, gb, n, L.slice, (n + 1) & ~1, cond, L.scr};
+    static unsigned long long* prof = nullptr;
+    static int prof_calls = 0;
+    static const bool want_prof = getenv("HPBJ_MGS_PROF") != nullptr;
+    if (want_prof && !prof) {
+        HPBJ_CUDA(cudaMallocManaged(&prof, sizeof(unsigned long long) * 5 * L.grid));
+        HPBJ_CUDA(cudaMemset(prof, 0, sizeof(unsigned long long) * 5 * L.grid));
+    }
+    OrthArgs a{kb, gram, sst, gb, n, L.slice, (n + 1) & ~1, cond, L.scr, want_prof && !L.icwy ? prof : nullptr};
     void (*fn)(OrthArgs);
     if (L.icwy) fn = L.w_in_smem ? k_icwy<true> : k_icwy<false>;
     else fn = L.w_in_smem ? k_mgs<true> : k_mgs<false>;
@@ -591,6 +615,26 @@ void launch_mgs(const MgsLaunch& L, const KrylovBufs& kb, double* gram, GridBarr
     cfg.numAttrs = 1;
     HPBJ_CUDA(cudaLaunchKernelEx(&cfg, fn, a));
     *launches += 1;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (a.prof && cudaStreamIsCapturing(st, &cap) == cudaSuccess && cap == cudaStreamCaptureStatusNone &&
+        ++prof_calls % 200 == 0) {
+        HPBJ_CUDA(cudaStreamSynchronize(st));
+        // per phase: min / mean / max over CTAs of the cycles per pass
+        double mn[4] = {1e30, 1e30, 1e30, 1e30}, mx[4] = {0, 0, 0, 0}, me[4] = {0, 0, 0, 0};
+        for (int c = 0; c < L.grid; ++c) {
+            const double np = (double)std::max(1ull, prof[(size_t)c * 5 + 4]);
+            for (int k = 0; k < 4; ++k) {
+                const double v = prof[(size_t)c * 5 + k] / np;
+                mn[k] = std::min(mn[k], v);
+                mx[k] = std::max(mx[k], v);
+                me[k] += v / L.grid;
+            }
+        }
+        fprintf(stderr, "[hpbj mgs prof] %d launches, %.0f passes/launch; cycles per pass (min/mean/max over CTAs): "
+                "stream %.0f/%.0f/%.0f  cta-reduce %.0f/%.0f/%.0f  grid-barrier %.0f/%.0f/%.0f  broadcast %.0f/%.0f/%.0f\n",
+                prof_calls, (double)prof[4] / prof_calls, mn[0], me[0], mx[0], mn[1], me[1], mx[1], mn[2], me[2], mx[2],
+                mn[3], me[3], mx[3]);
+    }
 }
 
 void launch_cycle_init(const KrylovBufs& kb, SolveState* sst, const double* r, int n,

@@ -113,11 +113,26 @@ __device__ __forceinline__ double block_sum(double v, double* sh /* NT/32 */) {
 }
 
 // Sums partials[0..count) in a fixed order (lane-strided then xor tree).
-__device__ __forceinline__ double warp_sum_partials(const double* partials, int count) {
+// Lane l's share: s = ((0 + p[l]) + p[l + 32]) + ... . The loads go out in
+// batches of eight independent L2 reads (one round trip per 256 partials
+// instead of one per 32: with the loop-carried sum the compiler waited on
+// each load before issuing the next), summed in the same order.
+__device__ __forceinline__ double lane_sum_partials(const double* partials, int count) {
     const int lane = threadIdx.x & 31;
     double s = 0.0;
-    for (int i = lane; i < count; i += 32) s += __ldcg(partials + i);
-    return warp_sum(s);
+    for (int i0 = lane; i0 < count; i0 += 8 * 32) {
+        double v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = i0 + 32 * k < count ? __ldcg(partials + i0 + 32 * k) : 0.0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            if (i0 + 32 * k < count) s += v[k];
+    }
+    return s;
+}
+
+__device__ __forceinline__ double warp_sum_partials(const double* partials, int count) {
+    return warp_sum(lane_sum_partials(partials, count));
 }
 
 }  // namespace hpbj

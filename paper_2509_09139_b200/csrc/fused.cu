@@ -356,7 +356,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_arnoldi_cycle(FusedArgs a) {
             for (int u = 0; u < 4; ++u) {
                 const int t = t0v + u * kWarps;
                 if (t < nval)
-                    for (int b = lane; b < G; b += 32) part[u] += __ldcg(P + (size_t)t * G + b);
+                    part[u] = lane_sum_partials(P + (size_t)t * G, G);
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u) {

@@ -156,7 +156,13 @@ template <class XT, int MODE>
 void run(const DevCsr& a, const SpmvPlan& plan, const XT* x, double* y, const double* b, SolveState* sst,
          double* partials, cudaStream_t st, int64_t* launches) {
     const int G = plan.group;
-    const int main_grid = spmv_grid(a.n, G);
+    // y = A x: one CTA per 256 / G rows, no grid stride — the hardware CTA
+    // scheduler backfills the SMs the hub-row CTAs and slow CTAs hold (a
+    // one-wave grid-stride launch waited on its last CTAs: config 2
+    // 42.0 -> 38.2 us, config 3 79.0 -> 76.2 us). The residual keeps the
+    // capped grid (one reduction partial per CTA).
+    const int main_grid = MODE == 0 ? std::max(1, (a.n + kSpmvThreads / G - 1) / (kSpmvThreads / G))
+                                    : spmv_grid(a.n, G);
     const int grid = main_grid + plan.n_long;
 #define HPBJ_SPMV_CASE(GG)                                                                              \
     case GG:                                                                                            \

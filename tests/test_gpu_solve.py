@@ -389,3 +389,33 @@ def test_setup_rejects_non_bijective_permutation():
     x, r = ctx.gmres(np.ones(n), hp.GmresConfig(restart_m=30, tol=1e-10, max_restarts=20))
     assert r.converged
     assert np.linalg.norm(np.asarray(fx.to_dense(a)) @ x - 1.0) <= 1e-8 * np.sqrt(n)
+
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("config,fused", [(4, True), (4, False), (2, False)])
+def test_solve_bit_reproducible_across_contexts(config, fused):
+    """Fresh contexts (new streams, pools and workspaces) on the same system
+    give bit-identical solutions and iteration counts, also after
+    update_values + refactor (config 4's Newton step): no reduction or
+    kernel depends on the schedule or on stale memory."""
+    s = generate(config)
+    a = hp.SparseMatrix(s.n, s.row_ptr, s.col, s.val)
+    part = hp.partition_graph(a, s.num_blocks, 0.1)
+    cfg = hp.GmresConfig(restart_m=s.restart_m, tol=s.tol, max_restarts=s.max_restarts)
+    st1 = generate(4, step=1) if config == 4 else None
+    out = []
+    for _ in range(3):
+        p = hp.Preconditioner.block_jacobi(a, part)
+        p.ctx.set_fused(fused)
+        res = [p.ctx.gmres(s.b, cfg)]
+        if st1 is not None:
+            p.ctx.update_values(st1.val)
+            p.ctx.bj_refactor()
+            res.append(p.ctx.gmres(st1.b, cfg))
+        out.append(res)
+    for other in out[1:]:
+        for (x0, r0), (x1, r1) in zip(out[0], other):
+            assert r0.converged and r1.converged
+            assert r0.total_iterations == r1.total_iterations
+            assert np.array_equal(x0, x1)
