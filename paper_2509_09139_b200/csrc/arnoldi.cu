@@ -9,8 +9,10 @@
 // memory for the whole step (w never round-trips to HBM). They differ only
 // in how the j+1 inner products are synchronised:
 //
-//  k_mgs  (large n: one basis vector takes longer to stream than a grid
-//          barrier): the textbook sequence, one grid-wide reduction per
+//  k_mgs_pipe (large n, the default there): textbook MGS with the grid-wide
+//          reductions taken off the critical path - see the kernel.
+//  k_mgs  (its fallback: w slice not in shared memory, HPBJ_MGS=bar): the
+//          textbook sequence, one grid-wide reduction per
 //          projection, h_i = <v_i, w - sum_{k<i} h_k v_k>; each v_i streams
 //          once from HBM for its dot and once more (L2-hot) for its axpy.
 //          (Two projections per reduction with a Gram correction was
@@ -317,6 +319,318 @@ __global__ void __launch_bounds__(kMgsThreads, 1) k_mgs(OrthArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// Pipelined textbook MGS (w slice in shared memory): no projection pass waits
+// for the grid.
+//
+// Warps 0..30 stream; warp 31 only communicates. Pass i (streaming warps)
+// merges u -= h_{i-2} v_{i-2} (v_{i-2} from L2, read two passes ago, loaded
+// evict-first; the HBM stream of v_i is loaded evict-last) with
+// d_i = <v_i, u>; at the dot u lacks only h_{i-1} v_{i-1}, so
+//   h_i = d_i - h_{i-1} <v_i, v_{i-1}>
+// is exactly <v_i, w - sum_{k<i} h_k v_k> (the missing term is linear).
+// <v_{k+1}, v_k> is a by-product of the step that created v_{k+1} (final pass:
+// <u, v_k> / ||u||), kept in gram[(k+1)(m+1) + k].
+//
+// While pass i+1 streams, the communication warp exchanges the partial sums
+// of pass i: every CTA stores its two partials into ll[slot i & 3][cta] as
+// four 64-bit words (32 payload bits << 32 | 32-bit epoch). A 64-bit word is
+// single-copy atomic, so data and flag arrive together: relaxed stores and
+// loads, no fence, no atomic. CTA 0 polls all CTAs' words (all loads of a
+// round in flight together), sums the partials in the order of sum_partials
+// (run-to-run reproducible), and stores the totals the same way into
+// tot[slot], which the other CTAs poll (one line). The warp then forms h_i
+// and leaves it in shared memory for pass i+2. A slot is reused four passes
+// later: a CTA that publishes pass p + 4 has read the totals of pass p + 3,
+// which CTA 0 stored after reading every partial of pass p + 3, which each
+// CTA stored after reading the totals of pass p. Only h_j and the final norm
+// wait for the grid.
+constexpr int kPipeStream = kMgsThreads - 32;  // streaming threads
+__device__ __forceinline__ unsigned long long l2_policy_evict_last() {
+    unsigned long long p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ unsigned long long l2_policy_evict_first() {
+    unsigned long long p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ double2 ld_hint(const double2* p, unsigned long long pol) {
+    double2 v;
+    asm volatile("ld.global.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+    return v;
+}
+
+__global__ void __launch_bounds__(kMgsThreads, 1) k_mgs_pipe(OrthArgs a) {
+    SolveState* st = a.st;
+    if (st->done) return;
+    extern __shared__ __align__(16) double dsm_mgs[];
+    double* wsh = dsm_mgs + a.scr;
+    __shared__ double red[2][2][32];  // [pass parity][quantity][warp]
+    __shared__ double hs[2];          // h_i by pass parity
+    __shared__ double misc[2];        // pre_norm^2, final ||w||^2
+
+    const int j = st->j;
+    const int m = a.kb.m;
+    const int ldv = a.kb.ldv;
+    const int G = gridDim.x;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const bool comm = wid == kMgsThreads / 32 - 1;
+    const int r0 = blockIdx.x * a.slice;
+    const int len = max(0, min(a.slice, a.npad - r0));
+    const int nv2 = len >> 1;
+    GridBarrier* gb = a.gb;
+    const unsigned long long seq = __ldcg(&gb->seq);
+    const unsigned long long ebase = (seq + 1ull) << 12;  // passes per launch <= m + 2 < 4096
+    // The epoch is 32 bits (2^20 launches): every 2^16 launches each CTA wipes
+    // its own words, so no stale word is old enough to match after the wrap.
+    if ((seq & 0xffffull) == 0 && tid < kFlagSlots * 4) {
+        gb->ll[tid >> 2][blockIdx.x][tid & 3] = 0ull;
+        if (blockIdx.x == 0) gb->tot[tid >> 2][tid & 3] = 0ull;
+    }
+
+    double2* w2 = reinterpret_cast<double2*>(wsh);
+    const double2* win = reinterpret_cast<const double2*>(a.kb.w + r0);
+    const double* V = a.kb.V;
+    const double* gsub = a.gram;  // <v_i, v_{i-1}> at gram[i (m+1) + i-1]
+    double* Hj = a.kb.H + (size_t)j * (m + 1);
+    const unsigned long long pol_last = l2_policy_evict_last(), pol_first = l2_policy_evict_first();
+
+    // streaming warps: leave the warp partials of pass p
+    auto deposit = [&](double x0, double x1, int p) {
+        x0 = warp_sum(x0);
+        x1 = warp_sum(x1);
+        if (lane == 0) {
+            red[p & 1][0][wid] = x0;
+            red[p & 1][1][wid] = x1;
+        }
+    };
+    // communication warp, after the CTA barrier that ends pass p: publish the
+    // CTA partial, gather all CTAs'; returns the two totals (all lanes)
+    double hlast = 0.0;  // communication warp: h_{p-1}
+    auto ll_store = [&](unsigned long long* q, double x0, double x1, unsigned long long ep) {
+        const unsigned long long b0 = (unsigned long long)__double_as_longlong(x0);
+        const unsigned long long b1 = (unsigned long long)__double_as_longlong(x1);
+        sync::st_relaxed_v2u64(q, (b0 << 32) | ep, (b0 & 0xffffffff00000000ull) | ep);
+        sync::st_relaxed_v2u64(q + 2, (b1 << 32) | ep, (b1 & 0xffffffff00000000ull) | ep);
+    };
+    auto ll_decode = [](unsigned long long lo, unsigned long long hi) {
+        return __longlong_as_double((long long)((lo >> 32) | (hi & 0xffffffff00000000ull)));
+    };
+    auto exchange = [&](int p, double& c0, double& c1) {
+        const int slot = p & (kFlagSlots - 1);
+        const unsigned long long want = ebase + (unsigned)p;  // low 32 bits are the epoch
+        const unsigned ep32 = (unsigned)want;
+        double t0 = lane < kPipeStream / 32 ? red[p & 1][0][lane] : 0.0;
+        double t1 = lane < kPipeStream / 32 ? red[p & 1][1][lane] : 0.0;
+        t0 = warp_sum(t0);
+        t1 = warp_sum(t1);
+        if (blockIdx.x != 0) {
+            if (lane == 0) ll_store(gb->ll[slot][blockIdx.x], t0, t1, want & 0xffffffffull);
+            // the totals come back from CTA 0 (one line, one request per poll)
+            unsigned long long w0, w1, w2, w3;
+            for (;;) {
+                sync::ld_relaxed_v2u64(gb->tot[slot], w0, w1);
+                sync::ld_relaxed_v2u64(gb->tot[slot] + 2, w2, w3);
+                if ((unsigned)w0 == ep32 && (unsigned)w1 == ep32 && (unsigned)w2 == ep32 && (unsigned)w3 == ep32) break;
+                __nanosleep(64);
+            }
+            c0 = ll_decode(w0, w1);
+            c1 = ll_decode(w2, w3);
+            return;
+        }
+        // CTA 0: lane l gathers CTAs l, l + 32, ... (all loads of a round in
+        // flight together); a word whose low half is the epoch carries this
+        // pass's data. Its own partial goes in directly.
+        constexpr int kPer = kFlagMaxCtas / 32;
+        unsigned long long wd[kPer][4];
+        for (;;) {
+            bool ok = true;
+#pragma unroll
+            for (int k = 0; k < kPer; ++k) {
+                const int c = lane + 32 * k;
+                if (c < G && c > 0) {
+                    sync::ld_relaxed_v2u64(gb->ll[slot][c], wd[k][0], wd[k][1]);
+                    sync::ld_relaxed_v2u64(gb->ll[slot][c] + 2, wd[k][2], wd[k][3]);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < kPer; ++k)
+                if (lane + 32 * k < G && lane + 32 * k > 0)
+                    ok &= (unsigned)wd[k][0] == ep32 && (unsigned)wd[k][1] == ep32 && (unsigned)wd[k][2] == ep32 &&
+                          (unsigned)wd[k][3] == ep32;
+            if (ok) break;
+        }
+        // the summation order of sum_partials: lane-strided, then the xor tree
+        double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            const int c = lane + 32 * k;
+            if (c == 0) {
+                s0 += t0;
+                s1 += t1;
+            } else if (c < G) {
+                s0 += ll_decode(wd[k][0], wd[k][1]);
+                s1 += ll_decode(wd[k][2], wd[k][3]);
+            }
+        }
+        c0 = warp_sum(s0);
+        c1 = warp_sum(s1);
+        if (lane == 0) ll_store(gb->tot[slot], c0, c1, want & 0xffffffffull);
+    };
+    // communication warp: h_p from the totals of pass p -> hs[p & 1], H
+    auto coefficient = [&](int p, double c0, double c1) {
+        double h = c1;
+        if (p == 0) {
+            if (lane == 0) misc[0] = c0;
+        } else {
+            h = fma(-hlast, __ldcg(gsub + (size_t)p * (m + 1) + (p - 1)), c1);
+        }
+        hlast = h;
+        if (lane == 0) {
+            hs[p & 1] = h;
+            if (blockIdx.x == 0) Hj[p] = h;
+        }
+    };
+
+    // pass 0: stage w on chip, ||w||^2 and <v_0, w>
+    if (!comm) {
+        double ss = 0.0, dt = 0.0;
+        const double2* v0 = reinterpret_cast<const double2*>(V + r0);
+#pragma unroll 4
+        for (int e = tid; e < nv2; e += kPipeStream) {
+            const double2 wv = __ldcg(win + e);
+            const double2 vv = ld_hint(v0 + e, pol_last);
+            w2[e] = wv;
+            ss = fma(wv.x, wv.x, ss);
+            ss = fma(wv.y, wv.y, ss);
+            dt = fma(vv.x, wv.x, dt);
+            dt = fma(vv.y, wv.y, dt);
+        }
+        deposit(ss, dt, 0);
+    }
+    __syncthreads();  // end of pass 0
+
+    // passes 1..j; the communication warp works one pass behind
+    unsigned long long pacc[3] = {0, 0, 0};  // HPBJ_MGS_PROF: stream, wait at the pass barrier, exchange
+    for (int i = 1; i <= j; ++i) {
+        const long long tq0 = a.prof ? clock64() : 0;
+        if (comm) {
+            double c0, c1;
+            exchange(i - 1, c0, c1);
+            coefficient(i - 1, c0, c1);
+            if (a.prof) pacc[2] += clock64() - tq0;
+        } else {
+            const double2* vi = reinterpret_cast<const double2*>(V + (size_t)i * ldv + r0);
+            double dt = 0.0;
+            if (i >= 2) {
+                const double h = hs[i & 1];  // h_{i-2}: written before the barrier that ended pass i-1
+                const double2* vp = reinterpret_cast<const double2*>(V + (size_t)(i - 2) * ldv + r0);
+#pragma unroll 4
+                for (int e = tid; e < nv2; e += kPipeStream) {
+                    double2 wv = w2[e];
+                    const double2 pv = ld_hint(vp + e, pol_first);
+                    const double2 qv = ld_hint(vi + e, pol_last);
+                    wv.x = fma(-h, pv.x, wv.x);
+                    wv.y = fma(-h, pv.y, wv.y);
+                    w2[e] = wv;
+                    dt = fma(qv.x, wv.x, dt);
+                    dt = fma(qv.y, wv.y, dt);
+                }
+            } else {
+#pragma unroll 8
+                for (int e = tid; e < nv2; e += kPipeStream) {
+                    const double2 wv = w2[e];
+                    const double2 qv = ld_hint(vi + e, pol_last);
+                    dt = fma(qv.x, wv.x, dt);
+                    dt = fma(qv.y, wv.y, dt);
+                }
+            }
+            deposit(0.0, dt, i);
+        }
+        const long long tq1 = a.prof ? clock64() : 0;
+        __syncthreads();  // end of pass i: red[i & 1] and hs[(i - 1) & 1] are published
+        if (a.prof) {
+            pacc[0] += tq1 - tq0;
+            pacc[1] += clock64() - tq1;
+        }
+    }
+    if (a.prof && (tid == 0 || (comm && lane == 0))) {
+        if (tid == 0) {
+            atomicAdd(a.prof + (size_t)blockIdx.x * 5 + 0, pacc[0]);
+            atomicAdd(a.prof + (size_t)blockIdx.x * 5 + 1, pacc[1]);
+            atomicAdd(a.prof + (size_t)blockIdx.x * 5 + 4, (unsigned long long)j);
+        } else {
+            atomicAdd(a.prof + (size_t)blockIdx.x * 5 + 2, pacc[2]);
+        }
+    }
+
+    // h_j: the one projection coefficient the CTA waits for
+    if (comm) {
+        double c0, c1;
+        exchange(j, c0, c1);
+        coefficient(j, c0, c1);
+    }
+    __syncthreads();
+    const double pre_norm = sqrt(misc[0]);
+
+    // final pass: w -= h_{j-1} v_{j-1} + h_j v_j; ||w||^2 and <w, v_j>
+    if (!comm) {
+        const double hj = hs[j & 1];
+        const double hj1 = j >= 1 ? hs[(j - 1) & 1] : 0.0;
+        const double2* vp = reinterpret_cast<const double2*>(V + (size_t)j * ldv + r0);
+        const double2* vq = reinterpret_cast<const double2*>(V + (size_t)max(j - 1, 0) * ldv + r0);
+        double ss = 0.0, gv = 0.0;
+        if (j >= 1) {
+#pragma unroll 4
+            for (int e = tid; e < nv2; e += kPipeStream) {
+                double2 wv = w2[e];
+                const double2 qv = ld_hint(vq + e, pol_first);
+                const double2 pv = __ldg(vp + e);
+                wv.x = fma(-hj1, qv.x, wv.x);  // MGS order: v_{j-1} first
+                wv.y = fma(-hj1, qv.y, wv.y);
+                wv.x = fma(-hj, pv.x, wv.x);
+                wv.y = fma(-hj, pv.y, wv.y);
+                w2[e] = wv;
+                ss = fma(wv.x, wv.x, ss);
+                ss = fma(wv.y, wv.y, ss);
+                gv = fma(wv.x, pv.x, gv);
+                gv = fma(wv.y, pv.y, gv);
+            }
+        } else {
+#pragma unroll 4
+            for (int e = tid; e < nv2; e += kPipeStream) {
+                double2 wv = w2[e];
+                const double2 pv = __ldg(vp + e);
+                wv.x = fma(-hj, pv.x, wv.x);
+                wv.y = fma(-hj, pv.y, wv.y);
+                w2[e] = wv;
+                ss = fma(wv.x, wv.x, ss);
+                ss = fma(wv.y, wv.y, ss);
+                gv = fma(wv.x, pv.x, gv);
+                gv = fma(wv.y, pv.y, gv);
+            }
+        }
+        deposit(ss, gv, j + 1);
+    }
+    __syncthreads();
+    if (comm) {
+        double c0, c1;
+        exchange(j + 1, c0, c1);
+        if (lane == 0) {
+            misc[1] = c0;
+            if (blockIdx.x == 0) {
+                const double hn = sqrt(c0);
+                a.gram[(size_t)(j + 1) * (m + 1) + j] = hn > 0.0 ? c1 / hn : 0.0;
+                gb->seq = ebase >> 12;  // every CTA read seq before its first publish, all of which this warp has seen
+            }
+        }
+    }
+    __syncthreads();
+    finish_step(a, w2, dsm_mgs, r0, nv2, j, pre_norm, sqrt(misc[1]), kMgsThreads);
+}
+
+// ---------------------------------------------------------------------------
 constexpr int kIcwyWarps = kIcwyThreads / 32;
 constexpr int kBatch = 8;  // basis vectors per multi-dot batch (16 dot products; 1024 threads x 64 registers:
                            // the multi-dot pass is latency bound, more rows in flight beat longer batches)
@@ -571,6 +885,8 @@ MgsLaunch plan_mgs(int n, int num_sms, int m) {
     if (env && std::string(env) == "mgs") icwy = false;
     if (env && std::string(env) == "icwy" && m <= kMaxRestart) icwy = true;
     L.icwy = icwy;
+    const char* fm = getenv("HPBJ_MGS");  // bar: the grid-barrier kernel
+    L.pipelined = !(fm && std::string(fm) == "bar");
     L.threads = icwy ? kIcwyThreads : kMgsThreads;
     const int min_rows = icwy ? 1024 : 4096;
     int grid = std::max(1, std::min(num_sms, (npad + min_rows - 1) / min_rows));
@@ -599,6 +915,7 @@ void launch_mgs(const MgsLaunch& L, const KrylovBufs& kb, double* gram, GridBarr
     OrthArgs a{kb, gram, sst, gb, n, L.slice, (n + 1) & ~1, cond, L.scr, want_prof && !L.icwy ? prof : nullptr};
     void (*fn)(OrthArgs);
     if (L.icwy) fn = L.w_in_smem ? k_icwy<true> : k_icwy<false>;
+    else if (L.w_in_smem && L.pipelined && L.grid <= kFlagMaxCtas) fn = k_mgs_pipe;
     else fn = L.w_in_smem ? k_mgs<true> : k_mgs<false>;
     if (L.smem > 48 * 1024)
         HPBJ_CUDA(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem));
@@ -631,7 +948,8 @@ void launch_mgs(const MgsLaunch& L, const KrylovBufs& kb, double* gram, GridBarr
             }
         }
         fprintf(stderr, "[hpbj mgs prof] %d launches, %.0f passes/launch; cycles per pass (min/mean/max over CTAs): "
-                "stream %.0f/%.0f/%.0f  cta-reduce %.0f/%.0f/%.0f  grid-barrier %.0f/%.0f/%.0f  broadcast %.0f/%.0f/%.0f\n",
+                "stream %.0f/%.0f/%.0f  cta-reduce %.0f/%.0f/%.0f  grid-barrier %.0f/%.0f/%.0f  broadcast %.0f/%.0f/%.0f "
+                "(k_mgs_pipe: stream, wait at the pass barrier, exchange, -)\n",
                 prof_calls, (double)prof[4] / prof_calls, mn[0], me[0], mx[0], mn[1], me[1], mx[1], mn[2], me[2], mx[2],
                 mn[3], me[3], mx[3]);
     }

@@ -36,7 +36,10 @@ struct Pool {
         if (it != free_.end() && it->first <= 2 * bytes + (1 << 20)) {
             void* p = it->second;
             free_.erase(it);
-            if (poison) HPBJ_CUDA(cudaMemset(p, 0xff, bytes));
+            if (poison) {  // legacy-stream memset: finish it before a non-blocking stream initialises the block
+                HPBJ_CUDA(cudaMemset(p, 0xff, bytes));
+                HPBJ_CUDA(cudaDeviceSynchronize());
+            }
             return p;
         }
         void* p = nullptr;
@@ -52,7 +55,10 @@ struct Pool {
             HPBJ_CUDA(cudaMalloc(&p, bytes));
         }
         size_[p] = bytes;
-        if (poison) HPBJ_CUDA(cudaMemset(p, 0xff, bytes));
+        if (poison) {
+            HPBJ_CUDA(cudaMemset(p, 0xff, bytes));
+            HPBJ_CUDA(cudaDeviceSynchronize());
+        }
         return p;
     }
     void put(void* p) {

@@ -74,9 +74,19 @@ struct SolveState {
 };
 
 // Generation barrier of one cooperative launch (zero-initialised).
+constexpr int kFlagSlots = 4;      // reductions of the pipelined MGS that may be in flight at once (+ reuse distance)
+constexpr int kFlagMaxCtas = 160;  // CTAs of its all-gather (one per SM; larger grids use the barrier kernel)
 struct GridBarrier {
     unsigned int count;
     unsigned int gen;
+    // All-gather of k_mgs_pipe (arnoldi.cu): seq counts its launches (CTA 0
+    // bumps it after the last collect); ll[slot][cta] carries that CTA's two
+    // partial sums as four 64-bit words (32 payload bits << 32 | epoch): a
+    // word is single-copy atomic, so data and flag arrive together and the
+    // exchange needs no fence.
+    unsigned long long seq;
+    alignas(32) unsigned long long ll[kFlagSlots][kFlagMaxCtas][4];
+    alignas(32) unsigned long long tot[kFlagSlots][4];  // the totals, from CTA 0, same encoding
 };
 
 // Grid-wide deterministic reduction: each CTA deposits a partial; the last

@@ -248,6 +248,7 @@ struct MgsLaunch {
     size_t smem = 0;    // dynamic: Givens scratch (scr doubles) + the w slice when w_in_smem
     int scr = 0;
     bool w_in_smem = true;
+    bool pipelined = true;  // textbook MGS: k_mgs_pipe (no pass waits for the grid) instead of k_mgs (a grid barrier per pass)
     bool icwy = false;  // compact-WY (2 barriers/step) instead of textbook MGS (j+2)
 };
 

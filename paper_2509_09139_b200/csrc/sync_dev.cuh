@@ -27,6 +27,14 @@ __device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
     return old;
 }
 
+__device__ __forceinline__ void ld_relaxed_v2u64(const unsigned long long* p, unsigned long long& x,
+                                                 unsigned long long& y) {
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(x), "=l"(y) : "l"(p) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_v2u64(unsigned long long* p, unsigned long long x, unsigned long long y) {
+    asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(x), "l"(y) : "memory");
+}
+
 // Sense-free generation barrier over all CTAs of a cooperative launch, with
 // release/acquire atomics instead of full fences (0.5 us cheaper per barrier
 // on B200, scripts/micro/barrier.cu): bar.sync orders the CTA's writes before

@@ -336,8 +336,8 @@ def test_invalid_restart_m_rejected_before_allocation():
 
 @pytest.mark.parametrize("nx", [40, 300])
 def test_textbook_mgs_matches_compact_wy_and_reference(ref, monkeypatch, nx):
-    """The per-kernel cycle with textbook MGS (`k_mgs`, chosen for n > 1.5M:
-    config 3) forced on smaller systems: one CTA with a slice shorter than the
+    """The per-kernel cycle with textbook MGS (`k_mgs_pipe` and its fallback
+    `k_mgs`, chosen for n > 1.5M: config 3) forced on smaller systems: one CTA with a slice shorter than the
     loads it issues across each grid barrier (nx = 40) and a 148-CTA grid
     (nx = 300, n = 90,000). Iteration counts within the parity bar of the
     reference Hybrid solve and within 1 of compact-WY, x within 1e-8."""
@@ -349,11 +349,21 @@ def test_textbook_mgs_matches_compact_wy_and_reference(ref, monkeypatch, nx):
     part = hp.partition_graph(a, max(2, a.n // 200), 0.1)
     cfg = hp.GmresConfig(restart_m=40, tol=1e-9, max_restarts=20)
     out = {}
-    for orth in ("mgs", "icwy"):
-        monkeypatch.setenv("HPBJ_ORTH", orth)
+    # "mgs": the pipelined kernel (k_mgs_pipe, the default for textbook MGS);
+    # "bar": its grid-barrier fallback k_mgs
+    for orth in ("mgs", "bar", "icwy"):
+        monkeypatch.setenv("HPBJ_ORTH", "mgs" if orth == "bar" else orth)
+        if orth == "bar":
+            monkeypatch.setenv("HPBJ_MGS", "bar")
+        else:
+            monkeypatch.delenv("HPBJ_MGS", raising=False)
         p = hp.Preconditioner.block_jacobi(a, part)
         p.ctx.set_fused(False)
         out[orth] = hp.hybrid_restart_gmres(a, p, b, cfg)
+        if orth == "mgs":  # same context again: the exchange epochs carry over, x bit for bit
+            again = hp.hybrid_restart_gmres(a, p, b, cfg)
+            assert again.report.total_iterations == out[orth].report.total_iterations
+            assert np.array_equal(again.x, out[orth].x)
     r = ref.solve(a.row_starts, a.col_indices, a.values, part.num_blocks, b, 40, 1e-9, 20, hybrid=True,
                   assignment=part.assignment)
     its = {k: v.report.total_iterations for k, v in out.items()}
@@ -364,6 +374,7 @@ def test_textbook_mgs_matches_compact_wy_and_reference(ref, monkeypatch, nx):
         assert abs(its[orth] - r.total_iterations) <= max(1, 0.05 * r.total_iterations), (its, r.total_iterations)
         assert np.linalg.norm(res.x - r.x) / np.linalg.norm(r.x) <= 1e-8, orth
     assert abs(its["mgs"] - its["icwy"]) <= 1, its
+    assert abs(its["mgs"] - its["bar"]) <= 1, its
 
 
 @pytest.mark.gpu
