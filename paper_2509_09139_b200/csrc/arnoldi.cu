@@ -323,8 +323,8 @@ __global__ void __launch_bounds__(kMgsThreads, 1) k_mgs(OrthArgs a) {
 // for the grid.
 //
 // Warps 0..30 stream; warp 31 only communicates. Pass i (streaming warps)
-// merges u -= h_{i-2} v_{i-2} (v_{i-2} from L2, read two passes ago, loaded
-// evict-first; the HBM stream of v_i is loaded evict-last) with
+// merges u -= h_{i-2} v_{i-2} (v_{i-2} read two passes ago: about half of it
+// still in L2; loaded evict-first, its last use) with
 // d_i = <v_i, u>; at the dot u lacks only h_{i-1} v_{i-1}, so
 //   h_i = d_i - h_{i-1} <v_i, v_{i-1}>
 // is exactly <v_i, w - sum_{k<i} h_k v_k> (the missing term is linear).
@@ -345,9 +345,9 @@ __global__ void __launch_bounds__(kMgsThreads, 1) k_mgs(OrthArgs a) {
 // CTA stored after reading the totals of pass p. Only h_j and the final norm
 // wait for the grid.
 constexpr int kPipeStream = kMgsThreads - 32;  // streaming threads
-__device__ __forceinline__ unsigned long long l2_policy_evict_last() {
+__device__ __forceinline__ unsigned long long l2_policy_evict_normal() {
     unsigned long long p;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
 __device__ __forceinline__ unsigned long long l2_policy_evict_first() {
@@ -357,7 +357,7 @@ __device__ __forceinline__ unsigned long long l2_policy_evict_first() {
 }
 __device__ __forceinline__ double2 ld_hint(const double2* p, unsigned long long pol) {
     double2 v;
-    asm volatile("ld.global.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+    asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
     return v;
 }
 
@@ -394,7 +394,11 @@ __global__ void __launch_bounds__(kMgsThreads, 1) k_mgs_pipe(OrthArgs a) {
     const double* V = a.kb.V;
     const double* gsub = a.gram;  // <v_i, v_{i-1}> at gram[i (m+1) + i-1]
     double* Hj = a.kb.H + (size_t)j * (m + 1);
-    const unsigned long long pol_last = l2_policy_evict_last(), pol_first = l2_policy_evict_first();
+    // The stream keeps the default priority; the re-read is the last use of a
+    // line (evict-first). Measured on config 3: 201 us/step; without the
+    // evict-first 255; with the stream also evict-last 201, but the lines that
+    // stay behind slow the next apply by 10 us.
+    const unsigned long long pol_last = l2_policy_evict_normal(), pol_first = l2_policy_evict_first();
 
     // streaming warps: leave the warp partials of pass p
     auto deposit = [&](double x0, double x1, int p) {
@@ -512,14 +516,11 @@ __global__ void __launch_bounds__(kMgsThreads, 1) k_mgs_pipe(OrthArgs a) {
     __syncthreads();  // end of pass 0
 
     // passes 1..j; the communication warp works one pass behind
-    unsigned long long pacc[3] = {0, 0, 0};  // HPBJ_MGS_PROF: stream, wait at the pass barrier, exchange
     for (int i = 1; i <= j; ++i) {
-        const long long tq0 = a.prof ? clock64() : 0;
         if (comm) {
             double c0, c1;
             exchange(i - 1, c0, c1);
             coefficient(i - 1, c0, c1);
-            if (a.prof) pacc[2] += clock64() - tq0;
         } else {
             const double2* vi = reinterpret_cast<const double2*>(V + (size_t)i * ldv + r0);
             double dt = 0.0;
@@ -548,21 +549,7 @@ __global__ void __launch_bounds__(kMgsThreads, 1) k_mgs_pipe(OrthArgs a) {
             }
             deposit(0.0, dt, i);
         }
-        const long long tq1 = a.prof ? clock64() : 0;
         __syncthreads();  // end of pass i: red[i & 1] and hs[(i - 1) & 1] are published
-        if (a.prof) {
-            pacc[0] += tq1 - tq0;
-            pacc[1] += clock64() - tq1;
-        }
-    }
-    if (a.prof && (tid == 0 || (comm && lane == 0))) {
-        if (tid == 0) {
-            atomicAdd(a.prof + (size_t)blockIdx.x * 5 + 0, pacc[0]);
-            atomicAdd(a.prof + (size_t)blockIdx.x * 5 + 1, pacc[1]);
-            atomicAdd(a.prof + (size_t)blockIdx.x * 5 + 4, (unsigned long long)j);
-        } else {
-            atomicAdd(a.prof + (size_t)blockIdx.x * 5 + 2, pacc[2]);
-        }
     }
 
     // h_j: the one projection coefficient the CTA waits for
@@ -948,8 +935,7 @@ void launch_mgs(const MgsLaunch& L, const KrylovBufs& kb, double* gram, GridBarr
             }
         }
         fprintf(stderr, "[hpbj mgs prof] %d launches, %.0f passes/launch; cycles per pass (min/mean/max over CTAs): "
-                "stream %.0f/%.0f/%.0f  cta-reduce %.0f/%.0f/%.0f  grid-barrier %.0f/%.0f/%.0f  broadcast %.0f/%.0f/%.0f "
-                "(k_mgs_pipe: stream, wait at the pass barrier, exchange, -)\n",
+                "stream %.0f/%.0f/%.0f  cta-reduce %.0f/%.0f/%.0f  grid-barrier %.0f/%.0f/%.0f  broadcast %.0f/%.0f/%.0f\n",
                 prof_calls, (double)prof[4] / prof_calls, mn[0], me[0], mx[0], mn[1], me[1], mx[1], mn[2], me[2], mx[2],
                 mn[3], me[3], mx[3]);
     }
